@@ -1,0 +1,274 @@
+/*
+ * gs.h — C-ABI of the B200-native differentiable Gaussian-splatting rasterizer
+ * (the hot path of Gaussian-SLAM, arXiv 2312.10070).
+ *
+ * Citation shorthand: "P:n" = PAPER.md line n (the paper's LaTeX), "S:n" =
+ * SPEC.md line n, "SURVEY §x" = /root/repo/SURVEY.md.  Readings of silent or
+ * ambiguous passages ("R1".."R26") are listed in DESIGN.md §3.
+ *
+ * Conventions shared by every entry point
+ * ----------------------------------------
+ *  - Every pointer is a DEVICE pointer to caller-owned memory unless marked
+ *    (host).  The library never allocates, frees or synchronises inside a hot
+ *    call; every call is asynchronous on `stream` (a cudaStream_t passed as
+ *    void*, NULL = legacy default stream).
+ *  - All float arrays are IEEE fp32, all "[n][4]" arrays are 16-byte aligned
+ *    float4 records (misalignment is GS_ERR_INVALID_ARG).
+ *  - Images are planar, row-major: color[3][H][W], depth[H][W], ...; pixel
+ *    (i, j) = (column, row) is sampled at the point (i, j) (R3).
+ *  - Tiles are 16x16 pixels, TX = ceil(W/16), TY = ceil(H/16), tile id =
+ *    ty*TX + tx; edge tiles are partial (R9).
+ *  - Return value: GS_OK or a negative GS_ERR_* code.  Host-side validation
+ *    failures never touch the device.  GS_ERR_CUDA carries the CUDA error
+ *    string in gs_last_error() (thread-local).  Device-side conditions
+ *    (non-finite projection, pair-capacity overflow) do not fail the call:
+ *    they increment gs_counters, which the caller reads asynchronously.
+ *  - Thread-safe across streams: there is no global mutable state.
+ */
+#ifndef GS_H
+#define GS_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define GS_ABI_VERSION 1
+
+/* Rasterizer constants (fp32 bit patterns in DESIGN.md R11). */
+#define GS_TILE 16                   /* 16x16 pixel tiles           */
+#define GS_DILATION 0.3f             /* +0.3 px^2 low-pass dilation (R7)    */
+#define GS_ALPHA_MAX 0.999f          /* alpha clamp (R11)                   */
+#define GS_ALPHA_MIN (1.0f / 255.0f) /* skip alpha < 1/255 (R11)            */
+#define GS_T_EPS 1e-4f               /* stop after T < 1e-4 (R11)           */
+#define GS_RADIUS_SIGMAS 3           /* radius = ceil(3 sqrt(lambda_max))  */
+
+/* Status codes. */
+#define GS_OK 0
+#define GS_ERR_INVALID_ARG (-1)
+#define GS_ERR_WORKSPACE (-2)
+#define GS_ERR_CUDA (-3)
+#define GS_ERR_UNSUPPORTED (-4)
+
+/* gs_render_bwd flags. */
+#define GS_GRAD_PARAMS 1u /* per-Gaussian parameter gradients (mapping) */
+#define GS_GRAD_POSE 2u   /* camera-pose partials (tracking)           */
+
+/* Pinhole camera, passed by value (R4, R5). */
+typedef struct gs_camera {
+  int32_t width, height; /* pixels, > 0                                  */
+  float fx, fy;          /* focal lengths in pixels, > 0                 */
+  float cx, cy;          /* principal point in pixels                    */
+  float z_near, z_far;   /* keep a Gaussian iff z_near <= p_z <= z_far   */
+} gs_camera;
+
+/* World->camera rigid transform T_wc: p = R mu + t, R row-major.
+ * Always passed as a DEVICE pointer so the tracking loop can update it in
+ * place (gs_pose_grad). 48 bytes. */
+typedef struct gs_view {
+  float R[9];
+  float t[3];
+} gs_view;
+
+/* Gaussian parameters (R18, R19), SoA of
+ * float4 records, all [n][4]:
+ *   mean_opa = (mu_x, mu_y, mu_z, opacity logit)   o = sigmoid(logit)
+ *   quat     = (w, x, y, z)                        normalised inside gs_project
+ *   logscale = (ln s_x, ln s_y, ln s_z, unused)    s = exp(logscale)
+ *   rgb      = (r, g, b, unused)                   raw RGB, no activation   */
+typedef struct gs_params {
+  const float *mean_opa;
+  const float *quat;
+  const float *logscale;
+  const float *rgb;
+  int32_t n; /* >= 0 */
+} gs_params;
+
+/* Per-Gaussian projection results written by gs_project (Eqs. 1-2,
+ * P:123-131), all indexed by Gaussian id:
+ *   uv            [n][2] fp64  splatted mean mu^I = (u, v) in pixels (R1, H2)
+ *   conic_o       [n][4] fp32  (A, B, C, o): (Sigma^I + 0.3 I)^-1 = [[A,B],[B,C]]
+ *   coef          [n][4] fp32  (a', b', d', log2 o) with
+ *                              sigma*log2(e) = (a' dx + b' dy)^2 + (d' dy)^2
+ *   rgbz          [n][4] fp32  (r, g, b, p_z) — colour and camera depth (R12)
+ *   depth         [n]    fp32  RN(p_z), the sort key; +inf when culled
+ *   rect          [n][4] int16 inclusive tile rect (x0, y0, x1, y1);
+ *                              (0, 0, -1, -1) when culled
+ *   tiles_touched [n]    int32 (x1-x0+1)(y1-y0+1), 0 when culled
+ * Fields of culled Gaussians other than depth/rect/tiles_touched are
+ * unspecified. */
+typedef struct gs_proj {
+  double *uv;
+  float *conic_o;
+  float *coef;
+  float *rgbz;
+  float *depth;
+  int16_t *rect;
+  int32_t *tiles_touched;
+} gs_proj;
+
+/* Device-side diagnostic counters, accumulated (never reset by the library). */
+typedef struct gs_counters {
+  int64_t n_nonfinite; /* non-finite or singular projections, culled */
+  int64_t n_culled;    /* all culled Gaussians (near/far, off-screen, non-finite)    */
+  int64_t n_overflow;  /* gs_bin_sort calls whose pair count exceeded capacity      */
+  int64_t reserved;
+} gs_counters;
+
+/* Adam step on the left-perturbation twist of T_wc (host, by value).
+ * Defaults: lr_trans 2e-3 m, lr_rot 1e-3 rad, 0.9, 0.999, 1e-8. */
+typedef struct gs_pose_step {
+  float lr_trans, lr_rot, beta1, beta2, eps;
+} gs_pose_step;
+
+/* ---------------------------------------------------------------------- */
+/* Library / device queries (host).                                        */
+
+/* ABI version (GS_ABI_VERSION). */
+int gs_version(void);
+
+/* Last error message of the calling thread; never NULL. */
+const char *gs_last_error(void);
+
+/* Returns GS_OK iff `device` is an sm_100 (B200-class) GPU; writes its SM
+ * count to *sm_count (host, nullable). GS_ERR_UNSUPPORTED otherwise. */
+int gs_check_device(int device, int *sm_count);
+
+/* Number of tiles of a camera: ceil(W/16)*ceil(H/16); 0 on invalid camera. */
+int32_t gs_num_tiles(gs_camera cam);
+
+/* Workspace bytes gs_bin_sort needs for n Gaussians on camera `cam`. */
+size_t gs_binsort_workspace_bytes(int32_t n, gs_camera cam);
+
+/* Workspace bytes gs_loss needs for camera `cam`. */
+size_t gs_loss_workspace_bytes(gs_camera cam);
+
+/* Workspace bytes gs_render_bwd needs for n Gaussians: the grad2d scratch
+ * [n][12] fp32, zeroed by the library at the start of every call. */
+size_t gs_bwd_workspace_bytes(int32_t n);
+
+/* Number of pose-partial records [count][12] gs_render_bwd writes with
+ * GS_GRAD_POSE for n Gaussians. */
+int32_t gs_pose_partials_count(int32_t n);
+
+/* ---------------------------------------------------------------------- */
+/* S1 — EWA projection (Eqs. 1-2).
+ *
+ * Per Gaussian: q^ = q/|q|, R_q(q^), s = exp(logscale), Sigma = R_q S^2 R_q^T;
+ * p = R mu + t; culled iff not z_near <= p_z <= z_far; u = fx p_x/p_z + cx,
+ * v = fy p_y/p_z + cy; Sigma^I = J R Sigma R^T J^T + 0.3 I with the unclamped
+ * perspective Jacobian J (R6); conic = (Sigma^I)^-1 (culled if det <= 0);
+ * r = ceil(3 sqrt(lambda_max)); tile rect clamped to the image (culled if
+ * empty); o = sigmoid(logit).  The decision path (p, u, v, Sigma^I,
+ * lambda_max, r, rect) is evaluated in IEEE fp64 in the operation order of
+ * DESIGN.md §3 R1 without FMA contraction, so tile and sort indices are
+ * reproducible bit-for-bit.
+ *   p      (device) parameters, n >= 0
+ *   view   (device) T_wc
+ *   cam    camera by value
+ *   out    (device) output arrays, each sized for p.n
+ *   cnt    (device) counters, nullable
+ * Errors: GS_ERR_INVALID_ARG on null arrays (n > 0), bad camera, misalignment. */
+int gs_project(gs_params p, const gs_view *view, gs_camera cam, gs_proj out,
+               gs_counters *cnt, void *stream);
+
+/* S2 — tile binning and depth ordering ("m ordered Gaussians"; S:132,
+ * S:142; R10).
+ *
+ * Emits one (tile, Gaussian) pair per tile of each visible Gaussian's rect and
+ * orders all pairs by the key (tile asc, fp32 depth asc, Gaussian id asc).
+ *   pr.depth, pr.rect, pr.tiles_touched (device) inputs from gs_project
+ *   ws/ws_bytes   (device) workspace >= gs_binsort_workspace_bytes(n, cam)
+ *   capacity      length of sorted_idx
+ *   sorted_idx    (device) [capacity] Gaussian ids, tile-major
+ *   tile_range    (device) [T][2] int32 [start, end) into sorted_idx
+ *   n_pairs       (device) [1] int64 total pair count P
+ *   cnt           (device) counters, nullable
+ * If P > capacity, n_overflow is incremented, every tile range is set empty
+ * and sorted_idx is left untouched (the caller re-sizes and repeats). */
+int gs_bin_sort(gs_proj pr, int32_t n, gs_camera cam, void *ws, size_t ws_bytes,
+                int64_t capacity, int32_t *sorted_idx, int32_t *tile_range,
+                int64_t *n_pairs, gs_counters *cnt, void *stream);
+
+/* S3 — front-to-back alpha compositing (Eqs. 3, 4, 6; P:133-141, P:161-166;
+ * S:129-138; R11-R15).
+ *
+ * Per pixel over its tile's ordered list: Delta = (u - i, v - j);
+ * alpha = min(o exp(-1/2 Delta^T conic Delta), 0.999); skip if alpha < 1/255;
+ * C += c alpha T; D += p_z alpha T; A += alpha T; T *= (1 - alpha); stop
+ * after compositing an entry that leaves T < 1e-4.  Background is zero.
+ *   color     (device) [3][H][W]    depth, alpha, T_final (device) [H][W]
+ *   n_contrib (device) [H][W] int32 (position in the tile list of the last
+ *             composited entry) + 1, 0 if none
+ *   stats     (device, nullable) [2][H][W] int32: entries scanned, entries
+ *             composited — the per-pixel counts of SURVEY §8(d). */
+int gs_render_fwd(gs_proj pr, const int32_t *sorted_idx, const int32_t *tile_range,
+                  gs_camera cam, float *color, float *depth, float *alpha,
+                  float *T_final, int32_t *n_contrib, int32_t *stats, void *stream);
+
+/* S4 — L1 colour + L1 depth loss (Eqs. 9, 10 L1 part, 12; P:178-202;
+ * S:256-264; R20, R21).
+ *
+ * L_c = sum w |C^ - C*| / (3HW);  L_d = sum_{D* > 0} w |D^ - D*| / |V|;
+ * loss = (lambda_color L_c + lambda_depth L_d, L_c, L_d).
+ * dL_dcolor = lambda_color w sign(C^ - C*) / (3HW);
+ * dL_ddepth = lambda_depth w sign(D^ - D*) / |V| on valid pixels, 0 else;
+ * sign(0) = 0; |V| = 0 gives L_d = 0 and a zero depth gradient.
+ *   weight (device, nullable) [H][W] per-pixel weight w (1 when NULL)
+ *   ws     (device) >= gs_loss_workspace_bytes(cam)
+ *   loss   (device) [3]
+ * The loss value is bit-deterministic (fixed-order two-stage reduction). */
+int gs_loss(gs_camera cam, const float *color, const float *depth,
+            const float *tgt_color, const float *tgt_depth, const float *weight,
+            float lambda_color, float lambda_depth, void *ws, size_t ws_bytes,
+            float *loss, float *dL_dcolor, float *dL_ddepth, void *stream);
+
+/* S5+S6 — backward (Eqs. 7-8; R16, R17).
+ *
+ * Per pixel, replays the composited entries back to front (same alpha
+ * decisions as gs_render_fwd, bit for bit) with suffix accumulators
+ * (Eq. 8 form), reduces per-Gaussian 2-D gradients (u, v, A, B, C, logit,
+ * r, g, b, p_z) with warp shuffles before global atomics, then chains them
+ * to the 3-D parameters.
+ *   dL_dcolor [3][H][W], dL_ddepth [H][W] (device); dL_dalpha [H][W]
+ *             (device, nullable = 0)
+ *   flags     GS_GRAD_PARAMS and/or GS_GRAD_POSE
+ *   ws        (device) >= gs_bwd_workspace_bytes(n)
+ *   g_mean_opa, g_quat, g_logscale, g_rgb (device) [n][4], ACCUMULATED (+=)
+ *             in the layout of gs_params; required iff GS_GRAD_PARAMS
+ *   pose_partials (device) [gs_pose_partials_count(n)][12] =
+ *             (dL/dR row-major 9, dL/dt 3) per block; required iff
+ *             GS_GRAD_POSE, overwritten. */
+int gs_render_bwd(gs_params p, const gs_view *view, gs_camera cam, gs_proj pr,
+                  const int32_t *sorted_idx, const int32_t *tile_range,
+                  const float *T_final, const int32_t *n_contrib,
+                  const float *dL_dcolor, const float *dL_ddepth,
+                  const float *dL_dalpha, uint32_t flags, void *ws, size_t ws_bytes,
+                  float *g_mean_opa, float *g_quat, float *g_logscale, float *g_rgb,
+                  float *pose_partials, void *stream);
+
+/* S7 — camera-pose gradient (Eq. 14; R22).
+ *
+ * Reduces the pose partials in a fixed order to dL/dR, dL/dt and converts
+ * them to the left-perturbation twist xi = (v, w) (T <- exp(xi^) T) and to
+ * the (q, t) parameterisation of T_wc (q = (w, x, y, z)).
+ *   view          (device) T_wc; updated in place iff step != NULL:
+ *                 Adam on the twist, T <- exp(-step^) T, R re-orthonormalised
+ *   pose_partials (device) [n_partials][12]
+ *   step          (host, nullable) Adam hyper-parameters
+ *   adam_state    (device) [13] = m[6], v[6], t; required iff step != NULL;
+ *                 zero it before the first iteration
+ *   dL_dview      (device, nullable) [12] = dL/dR (9), dL/dt (3)
+ *   dL_dtwist     (device, nullable) [6]  = dL/dv (3), dL/dw (3)
+ *   dL_dqt        (device, nullable) [7]  = dL/dq (4), dL/dt (3) */
+int gs_pose_grad(gs_view *view, const float *pose_partials, int32_t n_partials,
+                 const gs_pose_step *step, float *adam_state, float *dL_dview,
+                 float *dL_dtwist, float *dL_dqt, void *stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* GS_H */
