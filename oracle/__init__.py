@@ -56,8 +56,11 @@ def _ptr(a):
 
 
 def _cam(cam):
-    return np.ascontiguousarray(np.array(cam.as_tuple() if hasattr(cam, "as_tuple") else cam,
-                                         np.float64))
+    """(W, H, fx, fy, cx, cy, z_near, z_far): the camera is an fp32 gs_camera in
+    the C-ABI, so the float fields are promoted from their fp32 values."""
+    c = list(cam.as_tuple() if hasattr(cam, "as_tuple") else cam)
+    c = c[:2] + [float(np.float32(x)) for x in c[2:]]
+    return np.ascontiguousarray(np.array(c, np.float64))
 
 
 def _view(view):

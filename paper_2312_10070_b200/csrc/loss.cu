@@ -1,0 +1,147 @@
+// loss.cu — S4 gs_loss: L1 colour + L1 depth (Eqs. 9, 10 (L1 part), 12;
+// P:178-202; R20, R21).
+//
+// Three launches, all HBM-bound and deterministic:
+//   k_loss_count  per-block counts of valid target depths (D* > 0);
+//   k_loss_main   every block first sums the count partials in a fixed order
+//                 (|V|), then writes the final gradient maps and its own
+//                 fp64 partial sums of w|residual|;
+//   k_loss_final  one block reduces the partials in a fixed order -> loss[3].
+#include "gs_internal.cuh"
+
+namespace gs {
+
+constexpr int kLossThreads = 256;
+constexpr int kLossBlocks = 592;  // 4 x 148 SMs
+
+static size_t loss_ws_bytes() { return size_t(kLossBlocks) * (sizeof(double) * 2 + sizeof(uint32_t)) + 256; }
+
+__device__ __forceinline__ double block_sum_d(double v, double *sh) {
+  // fixed-shape tree: deterministic for a fixed blockDim
+  sh[threadIdx.x] = v;
+  __syncthreads();
+  for (int s = blockDim.x / 2; s > 0; s >>= 1) {
+    if (threadIdx.x < s) sh[threadIdx.x] += sh[threadIdx.x + s];
+    __syncthreads();
+  }
+  double r = sh[0];
+  __syncthreads();
+  return r;
+}
+
+__global__ void __launch_bounds__(kLossThreads) k_loss_count(const float *__restrict__ tgt_depth, int64_t HW,
+                                                             uint32_t *cnt_part) {
+  __shared__ uint32_t sh[kLossThreads / 32];
+  uint32_t c = 0;
+  for (int64_t q = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; q < HW; q += int64_t(gridDim.x) * blockDim.x)
+    c += __ldg(tgt_depth + q) > 0.f;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
+  if ((threadIdx.x & 31) == 0) sh[threadIdx.x >> 5] = c;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    uint32_t s = 0;
+    for (int w = 0; w < kLossThreads / 32; ++w) s += sh[w];
+    cnt_part[blockIdx.x] = s;
+  }
+}
+
+__global__ void __launch_bounds__(kLossThreads) k_loss_main(const float *__restrict__ color,
+                                                            const float *__restrict__ depth,
+                                                            const float *__restrict__ tc,
+                                                            const float *__restrict__ td,
+                                                            const float *__restrict__ weight, int64_t HW, float lc,
+                                                            float ld, const uint32_t *__restrict__ cnt_part,
+                                                            double *part, float *g_color, float *g_depth) {
+  __shared__ double sh[kLossThreads];
+  __shared__ float s_scale[2];
+  if (threadIdx.x < 32) {  // integer sum: order-independent
+    uint32_t nv = 0;
+    for (int b = threadIdx.x; b < gridDim.x; b += 32) nv += cnt_part[b];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) nv += __shfl_xor_sync(0xffffffffu, nv, o);
+    if (threadIdx.x == 0) {
+      s_scale[0] = float(double(lc) / (3.0 * double(HW)));
+      s_scale[1] = nv ? float(double(ld) / double(nv)) : 0.f;
+    }
+  }
+  __syncthreads();
+  const float sc = s_scale[0], sd = s_scale[1];
+  double ac = 0.0, ad = 0.0;
+  for (int64_t q = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; q < HW; q += int64_t(gridDim.x) * blockDim.x) {
+    const float w = weight ? __ldg(weight + q) : 1.f;
+#pragma unroll
+    for (int ch = 0; ch < 3; ++ch) {
+      const float r = __ldg(color + ch * HW + q) - __ldg(tc + ch * HW + q);
+      ac += double(w) * fabs(double(r));
+      const float sg = float((r > 0.f) - (r < 0.f));  // sign(0) = 0 (R21)
+      g_color[ch * HW + q] = sc * w * sg;
+    }
+    const float t = __ldg(td + q);
+    float gd = 0.f;
+    if (t > 0.f) {
+      const float r = __ldg(depth + q) - t;
+      ad += double(w) * fabs(double(r));
+      gd = sd * w * float((r > 0.f) - (r < 0.f));
+    }
+    g_depth[q] = gd;
+  }
+  ac = block_sum_d(ac, sh);
+  ad = block_sum_d(ad, sh);
+  if (threadIdx.x == 0) {
+    part[2 * blockIdx.x] = ac;
+    part[2 * blockIdx.x + 1] = ad;
+  }
+}
+
+__global__ void __launch_bounds__(kLossThreads) k_loss_final(const double *part, const uint32_t *cnt_part, int nblk,
+                                                             int64_t HW, float lc, float ld, float *loss) {
+  __shared__ double sh[kLossThreads];
+  double ac = 0.0, ad = 0.0, nv = 0.0;
+  for (int b = threadIdx.x; b < nblk; b += blockDim.x) {  // fixed order per thread
+    ac += part[2 * b];
+    ad += part[2 * b + 1];
+    nv += double(cnt_part[b]);
+  }
+  ac = block_sum_d(ac, sh);
+  ad = block_sum_d(ad, sh);
+  nv = block_sum_d(nv, sh);
+  if (threadIdx.x == 0) {
+    const double Lc = ac / (3.0 * double(HW));
+    const double Ld = nv > 0.0 ? ad / nv : 0.0;
+    loss[0] = float(double(lc) * Lc + double(ld) * Ld);
+    loss[1] = float(Lc);
+    loss[2] = float(Ld);
+  }
+}
+
+}  // namespace gs
+
+extern "C" size_t gs_loss_workspace_bytes(gs_camera cam) {
+  if (!gs::camera_ok(cam)) return 0;
+  return gs::loss_ws_bytes();
+}
+
+extern "C" int gs_loss(gs_camera cam, const float *color, const float *depth, const float *tgt_color,
+                       const float *tgt_depth, const float *weight, float lambda_color, float lambda_depth,
+                       void *ws, size_t ws_bytes, float *loss, float *dL_dcolor, float *dL_ddepth, void *stream) {
+  using namespace gs;
+  if (!camera_ok(cam) || !color || !depth || !tgt_color || !tgt_depth || !loss || !dL_dcolor || !dL_ddepth ||
+      !(lambda_color >= 0.f) || !(lambda_depth >= 0.f)) {
+    set_error("gs_loss: invalid argument");
+    return GS_ERR_INVALID_ARG;
+  }
+  if (!ws || ws_bytes < loss_ws_bytes()) {
+    set_error("gs_loss: workspace %zu < %zu bytes", ws_bytes, loss_ws_bytes());
+    return GS_ERR_WORKSPACE;
+  }
+  cudaStream_t s = as_stream(stream);
+  const int64_t HW = int64_t(cam.width) * cam.height;
+  double *part = static_cast<double *>(ws);
+  uint32_t *cnt_part = reinterpret_cast<uint32_t *>(part + 2 * kLossBlocks);
+  k_loss_count<<<kLossBlocks, kLossThreads, 0, s>>>(tgt_depth, HW, cnt_part);
+  k_loss_main<<<kLossBlocks, kLossThreads, 0, s>>>(color, depth, tgt_color, tgt_depth, weight, HW, lambda_color,
+                                                   lambda_depth, cnt_part, part, dL_dcolor, dL_ddepth);
+  k_loss_final<<<1, kLossThreads, 0, s>>>(part, cnt_part, kLossBlocks, HW, lambda_color, lambda_depth, loss);
+  return check_launch("gs_loss");
+}

@@ -1,0 +1,276 @@
+"""Thin torch-facing binding of the C-ABI (include/gs.h).
+
+Functions named like the C entry points (``gs_project`` ... ``gs_pose_grad``)
+only marshal torch CUDA tensors into pointers and call the library on the
+current torch stream: every step of the path runs in the CUDA kernels of
+``csrc/``.  PyTorch is used for device memory, streams and process groups only.
+
+``Rasterizer`` owns the buffers of one (N, camera) problem and strings the
+calls together; ``Params`` / ``Grads`` hold the four float4 SoA arrays.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass
+
+import torch
+
+from . import _lib
+from ._lib import GS_GRAD_PARAMS, GS_GRAD_POSE, GsCamera, GsError, GsParams, GsPoseStep, GsProj, check, lib
+
+__all__ = ["Params", "Grads", "Proj", "Frame", "Rasterizer", "camera", "gs_project", "gs_bin_sort",
+           "gs_render_fwd", "gs_loss", "gs_render_bwd", "gs_pose_grad", "GS_GRAD_PARAMS", "GS_GRAD_POSE",
+           "GsError", "device_check"]
+
+
+def _p(t):
+    if t is None:
+        return None
+    if not t.is_cuda:
+        raise GsError("tensor is not on a CUDA device")
+    if not t.is_contiguous():
+        raise GsError("tensor must be contiguous")
+    return C.c_void_p(t.data_ptr())
+
+
+def _stream(stream=None):
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return C.c_void_p(s.cuda_stream)
+
+
+def camera(cam) -> GsCamera:
+    """gs_camera from an inputs.Camera (or any object with the same fields)."""
+    return GsCamera(int(cam.width), int(cam.height), float(cam.fx), float(cam.fy), float(cam.cx), float(cam.cy),
+                    float(cam.z_near), float(cam.z_far))
+
+
+def device_check(device=0):
+    sm = C.c_int(0)
+    check(lib().gs_check_device(int(device), C.byref(sm)), "gs_check_device")
+    return sm.value
+
+
+@dataclass
+class Params:
+    mean_opa: torch.Tensor  # [N,4] (x, y, z, opacity logit)
+    quat: torch.Tensor      # [N,4] (w, x, y, z)
+    logscale: torch.Tensor  # [N,4]
+    rgb: torch.Tensor       # [N,4]
+
+    @property
+    def n(self):
+        return self.mean_opa.shape[0]
+
+    def c(self):
+        return GsParams(_p(self.mean_opa), _p(self.quat), _p(self.logscale), _p(self.rgb), self.n)
+
+    @staticmethod
+    def from_numpy(mean_opa, quat, logscale, rgb, device="cuda"):
+        f = lambda a: torch.as_tensor(a, dtype=torch.float32).contiguous().to(device)
+        return Params(f(mean_opa), f(quat), f(logscale), f(rgb))
+
+
+@dataclass
+class Grads:
+    """Parameter gradients in the gs_params layout, views of ONE contiguous
+    [4, N, 4] buffer so a single NCCL all-reduce covers them."""
+    buf: torch.Tensor
+
+    @staticmethod
+    def zeros(n, device="cuda"):
+        return Grads(torch.zeros(4, n, 4, dtype=torch.float32, device=device))
+
+    @property
+    def mean_opa(self):
+        return self.buf[0]
+
+    @property
+    def quat(self):
+        return self.buf[1]
+
+    @property
+    def logscale(self):
+        return self.buf[2]
+
+    @property
+    def rgb(self):
+        return self.buf[3]
+
+    def zero_(self):
+        self.buf.zero_()
+        return self
+
+
+class Proj:
+    """gs_proj buffers for n Gaussians."""
+
+    def __init__(self, n, device="cuda"):
+        m = max(n, 1)
+        self.n = n
+        self.uv = torch.empty(m, 2, dtype=torch.float64, device=device)
+        self.conic_o = torch.empty(m, 4, dtype=torch.float32, device=device)
+        self.coef = torch.empty(m, 4, dtype=torch.float32, device=device)
+        self.rgbz = torch.empty(m, 4, dtype=torch.float32, device=device)
+        self.depth = torch.empty(m, dtype=torch.float32, device=device)
+        self.rect = torch.empty(m, 4, dtype=torch.int16, device=device)
+        self.tiles_touched = torch.empty(m, dtype=torch.int32, device=device)
+
+    def c(self):
+        return GsProj(_p(self.uv), _p(self.conic_o), _p(self.coef), _p(self.rgbz), _p(self.depth),
+                      _p(self.rect), _p(self.tiles_touched))
+
+
+class Frame:
+    """Rendered frame buffers (planar)."""
+
+    def __init__(self, H, W, device="cuda"):
+        self.color = torch.empty(3, H, W, dtype=torch.float32, device=device)
+        self.depth = torch.empty(H, W, dtype=torch.float32, device=device)
+        self.alpha = torch.empty(H, W, dtype=torch.float32, device=device)
+        self.T_final = torch.empty(H, W, dtype=torch.float32, device=device)
+        self.n_contrib = torch.empty(H, W, dtype=torch.int32, device=device)
+        self.stats = torch.empty(2, H, W, dtype=torch.int32, device=device)
+
+
+# ---------------------------------------------------------------------------
+# Entry points, same names as include/gs.h
+
+
+def gs_project(params: Params, view, cam: GsCamera, proj: Proj, counters=None, stream=None):
+    check(lib().gs_project(params.c(), _p(view), cam, proj.c(), _p(counters), _stream(stream)), "gs_project")
+
+
+def gs_bin_sort(proj: Proj, n, cam: GsCamera, ws, capacity, sorted_idx, tile_range, n_pairs, counters=None,
+                stream=None):
+    check(lib().gs_bin_sort(proj.c(), int(n), cam, _p(ws), ws.numel() * ws.element_size(), int(capacity),
+                            _p(sorted_idx), _p(tile_range), _p(n_pairs), _p(counters), _stream(stream)),
+          "gs_bin_sort")
+
+
+def gs_render_fwd(proj: Proj, sorted_idx, tile_range, cam: GsCamera, frame: Frame, stats=False, stream=None):
+    check(lib().gs_render_fwd(proj.c(), _p(sorted_idx), _p(tile_range), cam, _p(frame.color), _p(frame.depth),
+                              _p(frame.alpha), _p(frame.T_final), _p(frame.n_contrib),
+                              _p(frame.stats) if stats else None, _stream(stream)), "gs_render_fwd")
+
+
+def gs_loss(cam: GsCamera, color, depth, tgt_color, tgt_depth, weight, lambda_color, lambda_depth, ws, loss,
+            dL_dcolor, dL_ddepth, stream=None):
+    check(lib().gs_loss(cam, _p(color), _p(depth), _p(tgt_color), _p(tgt_depth), _p(weight), float(lambda_color),
+                        float(lambda_depth), _p(ws), ws.numel() * ws.element_size(), _p(loss), _p(dL_dcolor),
+                        _p(dL_ddepth), _stream(stream)), "gs_loss")
+
+
+def gs_render_bwd(params: Params, view, cam: GsCamera, proj: Proj, sorted_idx, tile_range, T_final, n_contrib,
+                  dL_dcolor, dL_ddepth, dL_dalpha, flags, ws, grads: Grads = None, pose_partials=None,
+                  stream=None):
+    g = grads
+    check(lib().gs_render_bwd(params.c(), _p(view), cam, proj.c(), _p(sorted_idx), _p(tile_range), _p(T_final),
+                              _p(n_contrib), _p(dL_dcolor), _p(dL_ddepth), _p(dL_dalpha), int(flags), _p(ws),
+                              ws.numel() * ws.element_size(),
+                              _p(g.mean_opa) if g is not None else None, _p(g.quat) if g is not None else None,
+                              _p(g.logscale) if g is not None else None, _p(g.rgb) if g is not None else None,
+                              _p(pose_partials), _stream(stream)), "gs_render_bwd")
+
+
+def gs_pose_grad(view, pose_partials, n_partials, step=None, adam_state=None, dL_dview=None, dL_dtwist=None,
+                 dL_dqt=None, stream=None):
+    st = None
+    if step is not None:
+        st = C.byref(GsPoseStep(*[float(x) for x in step]))
+    check(lib().gs_pose_grad(_p(view), _p(pose_partials), int(n_partials), st, _p(adam_state), _p(dL_dview),
+                             _p(dL_dtwist), _p(dL_dqt), _stream(stream)), "gs_pose_grad")
+
+
+# ---------------------------------------------------------------------------
+
+
+class Rasterizer:
+    """All buffers of one (N Gaussians, camera) problem; no allocation in the
+    per-iteration calls, so a whole iteration can be CUDA-graph captured."""
+
+    def __init__(self, n, cam, capacity=None, device="cuda"):
+        self.n = n
+        self.cam_py = cam
+        self.cam = camera(cam)
+        self.device = device
+        L = lib()
+        self.T = L.gs_num_tiles(self.cam)
+        if self.T <= 0:
+            raise GsError("invalid camera")
+        H, W = cam.height, cam.width
+        self.proj = Proj(n, device)
+        ws = L.gs_binsort_workspace_bytes(n, self.cam)
+        if ws == 0:
+            raise GsError("gs_binsort_workspace_bytes: problem not supported")
+        self.sort_ws = torch.empty((ws + 15) // 16 * 4, dtype=torch.float32, device=device)
+        self.tile_range = torch.empty(self.T, 2, dtype=torch.int32, device=device)
+        self.n_pairs = torch.zeros(1, dtype=torch.int64, device=device)
+        self.counters = torch.zeros(4, dtype=torch.int64, device=device)
+        self.frame = Frame(H, W, device)
+        self.loss_ws = torch.empty((L.gs_loss_workspace_bytes(self.cam) + 15) // 16 * 4, dtype=torch.float32,
+                                   device=device)
+        self.loss = torch.zeros(3, dtype=torch.float32, device=device)
+        self.dL_dcolor = torch.zeros(3, H, W, dtype=torch.float32, device=device)
+        self.dL_ddepth = torch.zeros(H, W, dtype=torch.float32, device=device)
+        self.bwd_ws = torch.empty((L.gs_bwd_workspace_bytes(n) + 15) // 16 * 4, dtype=torch.float32, device=device)
+        self.n_partials = L.gs_pose_partials_count(n)
+        self.pose_partials = torch.zeros(self.n_partials, 12, dtype=torch.float32, device=device)
+        self.capacity = 0
+        self.sorted_idx = torch.empty(1, dtype=torch.int32, device=device)
+        if capacity is not None:
+            self.set_capacity(capacity)
+
+    @property
+    def grad2d(self):
+        """The [N, 12] 2-D gradient scratch of the last gs_render_bwd:
+        (u, v, A, B), (C, p_z, logit, 0), (r, g, b, 0)."""
+        return self.bwd_ws[: self.n * 12].view(self.n, 12)
+
+    def set_capacity(self, capacity):
+        capacity = int(max(capacity, 1))
+        if capacity > self.capacity:
+            self.sorted_idx = torch.empty(capacity, dtype=torch.int32, device=self.device)
+            self.capacity = capacity
+
+    def size_for(self, params: Params, view, slack=1.25):
+        """Host-synchronising helper (setup only): project + sort once and size
+        the pair capacity to slack x the pair count."""
+        self.project(params, view)
+        self.bin_sort()
+        P = int(self.n_pairs.item())
+        if P > self.capacity:
+            self.set_capacity(int(P * slack) + 1024)
+            self.bin_sort()
+        return P
+
+    # -- stages ---------------------------------------------------------------
+    def project(self, params: Params, view):
+        gs_project(params, view, self.cam, self.proj, self.counters)
+
+    def bin_sort(self):
+        gs_bin_sort(self.proj, self.n, self.cam, self.sort_ws, self.capacity, self.sorted_idx, self.tile_range,
+                    self.n_pairs, self.counters)
+
+    def render(self, stats=False):
+        gs_render_fwd(self.proj, self.sorted_idx, self.tile_range, self.cam, self.frame, stats)
+
+    def forward(self, params: Params, view, stats=False):
+        self.project(params, view)
+        self.bin_sort()
+        self.render(stats)
+        return self.frame
+
+    def compute_loss(self, tgt_color, tgt_depth, weight=None, lambda_color=1.0, lambda_depth=1.0):
+        gs_loss(self.cam, self.frame.color, self.frame.depth, tgt_color, tgt_depth, weight, lambda_color,
+                lambda_depth, self.loss_ws, self.loss, self.dL_dcolor, self.dL_ddepth)
+        return self.loss
+
+    def backward(self, params: Params, view, flags=GS_GRAD_PARAMS, grads: Grads = None, dL_dcolor=None,
+                 dL_ddepth=None, dL_dalpha=None):
+        gs_render_bwd(params, view, self.cam, self.proj, self.sorted_idx, self.tile_range, self.frame.T_final,
+                      self.frame.n_contrib, self.dL_dcolor if dL_dcolor is None else dL_dcolor,
+                      self.dL_ddepth if dL_ddepth is None else dL_ddepth, dL_dalpha, flags, self.bwd_ws, grads,
+                      self.pose_partials if flags & GS_GRAD_POSE else None)
+
+    def pose_grad(self, view, step=None, adam_state=None, dL_dview=None, dL_dtwist=None, dL_dqt=None):
+        gs_pose_grad(view, self.pose_partials, self.n_partials, step, adam_state, dL_dview, dL_dtwist, dL_dqt)

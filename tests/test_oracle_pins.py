@@ -86,9 +86,11 @@ def test_projection_on_axis(orc):
 
 
 def test_projection_near_far_cull(orc):
-    """z = z_near/2 is culled; R5 keeps z_near <= z <= z_far."""
+    """z = z_near/2 is culled; R5 keeps z_near <= z <= z_far (the camera is
+    fp32 in the C-ABI, so the boundary is fp32(0.2))."""
     cam = _cam(64, 64, 60.0)
-    p = _params([[0, 0, 0.1], [0, 0, 150.0], [0, 0, 0.2], [0, 0, 100.0], [0, 0, -1.0]],
+    zn = float(np.float32(0.2))
+    p = _params([[0, 0, 0.1], [0, 0, 150.0], [0, 0, zn], [0, 0, 100.0], [0, 0, -1.0]],
                 [[-3, -3, -3]] * 5, [0.0] * 5, [[1, 1, 1]] * 5)
     pr = orc.project(p, IDV, cam)
     assert list(pr["culled"]) == [1, 1, 0, 0, 1]
