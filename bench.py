@@ -1,0 +1,450 @@
+#!/usr/bin/env python
+"""Benchmark of the Gaussian-SLAM rasterizer hot path on B200 (BASELINE.json metric).
+
+    python bench.py [--gpus N --steps K --warmup W] [--impl ours|reference] [--config 3]
+
+One *step* = one multi-view sub-map mapping iteration of BJ.configs[3]
+(500k Gaussians, 1200x680, 8 keyframe views): per view gs_project ->
+gs_bin_sort -> gs_render_fwd -> gs_loss -> gs_render_bwd (all parameters), and
+for N > 1 one NCCL all-reduce of the gradient buffer.  Views are sharded
+round-robin across ranks (strong scaling: 8 views in total for every N).
+Metric: fwd+bwd megapixels/s = (8 x 1200 x 680 / 1e6) / step time, max over
+ranks.  Also reported: tracking iterations/s (BJ.configs[2], 100 iterations
+in one CUDA graph, N = 1 only), the roofline of the dominant kernel, the
+oracle as a CPU baseline, and the end-to-end number with host buffers.
+
+--impl reference times the fp64 CPU oracle (the only reference this tier has)
+on a bounded sample of the same workload.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "fwd+bwd megapixels/s at 1200x680 (500k Gaussians)"
+UNIT = "MP/s"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", type=int, default=3, choices=[1, 3, 4])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-tracking", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--profile", action="store_true", help="short run for ncu (no clocks/cpu/e2e/tracking)")
+    ap.add_argument("--cpu-tiles", type=int, default=192, help="tiles of the oracle sample")
+    return ap.parse_args()
+
+
+def dist_env():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
+# ---------------------------------------------------------------------------
+# clocks (nvidia-smi sampled during the timed region)
+
+class Clocks:
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.f = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
+        self.p = None
+
+    def __enter__(self):
+        try:
+            self.p = subprocess.Popen(["nvidia-smi", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                                       "-lms", "200", "-i", str(self.index)], stdout=self.f,
+                                      stderr=subprocess.DEVNULL)
+        except Exception:
+            self.p = None
+        return self
+
+    def __exit__(self, *a):
+        if self.p is not None:
+            time.sleep(0.25)
+            self.p.terminate()
+            try:
+                self.p.wait(timeout=5)
+            except Exception:
+                self.p.kill()
+
+    def summary(self):
+        self.f.flush()
+        rows = [l.split(",") for l in open(self.f.name).read().strip().splitlines() if l.strip()]
+        os.unlink(self.f.name)
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        sm = [float(r[1]) for r in rows if r[1].strip().replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in rows if r[2].strip().replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = set()
+        for r in rows:
+            for k, nm in enumerate(names):
+                if len(r) > 5 + k and "Active" in r[5 + k] and "Not" not in r[5 + k]:
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": sorted(reasons), "samples": len(rows)}
+
+
+# ---------------------------------------------------------------------------
+# workload
+
+def make_workload(cfg, device, rank, world):
+    import torch
+    from paper_2312_10070_b200 import Params, Rasterizer, inputs
+    s = {1: inputs.config1, 3: inputs.config3, 4: inputs.config4}[cfg]()
+    P = Params.from_numpy(*s.params(), device=device)
+    views = torch.as_tensor(s.views, device=device)
+    V = views.shape[0]
+    tc, td = {}, {}
+    if "target_params" in s.extra:
+        # targets = renders of the perturbed copy, rendered by this path at setup
+        Pt = Params.from_numpy(*s.extra["target_params"], device=device)
+        r = Rasterizer(s.n, s.cam, device=device)
+        for v in range(rank, V, world):
+            r.size_for(Pt, views[v])
+            r.forward(Pt, views[v])
+            tc[v] = r.frame.color.clone()
+            td[v] = r.frame.depth.clone()
+        del r
+    else:
+        for v in range(V):
+            tc[v] = torch.as_tensor(s.extra["tgt_color"][v], device=device)
+            td[v] = torch.as_tensor(s.extra["tgt_depth"][v], device=device)
+    torch.cuda.synchronize()
+    return s, P, views, tc, td
+
+
+def roofline_for(step, stats_views, peaks, sm_mhz, fwd_ms, bwd_ms):
+    """FP32-pipe roofline of the compositing kernels.
+
+    Algorithmic flops: forward 10 s + 11 c per pixel, backward
+    10 r + 64 c per pixel (r = entries replayed = n_contrib, c = composited).
+    Peak = 148 SMs x 128 FP32 lanes x 2 flop x the SM clock measured during the
+    run (no measured FP32 peak exists in MEASURED_PEAKS.json)."""
+    s = sum(x["scanned"] for x in stats_views)
+    c = sum(x["contrib"] for x in stats_views)
+    r = sum(x["replayed"] for x in stats_views)
+    nv = len(stats_views)
+    fwd_flops = (10 * s + 11 * c) / nv     # per launch (one view)
+    bwd_flops = (10 * r + 64 * c) / nv
+    mhz = sm_mhz or peaks.get("sm_max_mhz", 1965.0)
+    peak = 148 * 128 * 2 * mhz * 1e6 / 1e12
+    out = {}
+    for name, fl, ms in (("render_bwd_pixels", bwd_flops, bwd_ms), ("render_fwd", fwd_flops, fwd_ms)):
+        ach = fl / (ms * 1e-3) / 1e12 if ms else None
+        out[name] = {"bound": "alu", "achieved": ach, "peak": peak, "unit": "TFLOP/s",
+                     "frac": ach / peak if ach else None, "traffic": None, "flops_per_launch": fl,
+                     "ms_per_launch": ms}
+    return out
+
+
+def bench_ours(a):
+    import torch
+    import torch.distributed as dist
+    from paper_2312_10070_b200 import raster
+    from paper_2312_10070_b200.pipeline import MapStep, kernels_per_view
+
+    world, rank, local = dist_env()
+    if world != a.gpus:
+        if a.gpus != 1 or world != 1:
+            print(f"warning: --gpus {a.gpus} but WORLD_SIZE={world}", file=sys.stderr)
+    torch.cuda.set_device(local)
+    device = torch.device("cuda", local)
+    group = None
+    if world > 1:
+        dist.init_process_group("nccl", device_id=device)
+    sm_count = raster.device_check(local)
+    s, P, views, tc, td = make_workload(a.config, device, rank, world)
+    V = views.shape[0]
+    ms = MapStep(P, views, s.cam, tc, td, rank, world, group, device=device)
+    ms.size()
+    # per-view work counts for the roofline (untimed)
+    stats_views = []
+    for v in ms.mine:
+        ms.r.forward(P, views[v], stats=True)
+        st = ms.r.frame.stats
+        stats_views.append({"scanned": int(st[0].sum().item()), "contrib": int(st[1].sum().item()),
+                            "replayed": int(ms.r.frame.n_contrib.sum().item()),
+                            "pairs": int(ms.r.n_pairs.item())})
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=device)
+    stream = torch.cuda.current_stream()
+
+    # per-stage events around the dominant kernels inside the timed steps
+    ev_fwd, ev_bwd = [], []
+
+    def timed_view(m, k, v):
+        r = m.r
+        r.project(m.params, m.views[v])
+        r.bin_sort()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        r.render()
+        e1.record(stream)
+        ev_fwd.append((e0, e1))
+        r.compute_loss(m.tgt_color[v], m.tgt_depth[v], None, m.lc, m.ld)
+        m.losses[k].copy_(r.loss)
+        b0, b1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        # the backward's two phases are timed separately: pixels (dominant) then Gaussians
+        raster.gs_render_bwd(m.params, m.views[v], r.cam, r.proj, r.sorted_idx, r.tile_range, r.frame.T_final,
+                             r.frame.n_contrib, r.dL_dcolor, r.dL_ddepth, None,
+                             raster.GS_GRAD_PARAMS | raster.GS_BWD_PIXELS_ONLY, r.bwd_ws, m.grads, None,
+                             event_pair=(b0, b1))
+        raster.gs_render_bwd(m.params, m.views[v], r.cam, r.proj, r.sorted_idx, r.tile_range, r.frame.T_final,
+                             r.frame.n_contrib, r.dL_dcolor, r.dL_ddepth, None,
+                             raster.GS_GRAD_PARAMS | raster.GS_BWD_GAUSS_ONLY, r.bwd_ws, m.grads, None)
+        ev_bwd.append((b0, b1))
+
+    for _ in range(max(a.warmup, 3)):
+        ms.step(timed_view)
+    ev_fwd.clear()
+    ev_bwd.clear()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    step_ms = []
+    with Clocks(local) as clk:
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        for _ in range(a.steps):
+            flush.zero_()  # L2 flush between timed steps (outside the step events)
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            ms.step(timed_view)
+            e1.record(stream)
+            step_ms.append((e0, e1))
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+    clocks = clk.summary()
+    tot = sum(e0.elapsed_time(e1) for e0, e1 in step_ms)
+    fwd_ms = statistics.mean(e0.elapsed_time(e1) for e0, e1 in ev_fwd) if ev_fwd else None
+    bwd_ms = statistics.mean(e0.elapsed_time(e1) for e0, e1 in ev_bwd) if ev_bwd else None
+    t = torch.tensor([tot], dtype=torch.float64, device=device)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms_per_step = float(t.item()) / a.steps
+    W, H = s.cam.width, s.cam.height
+    mp = V * W * H / 1e6
+    value = mp / (ms_per_step * 1e-3)
+    peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))) if os.path.exists(
+        os.path.join(ROOT, "MEASURED_PEAKS.json")) else {}
+    roof = roofline_for(ms, stats_views, peaks, clocks.get("sm_mhz"), fwd_ms, bwd_ms)
+    launches = (ms.launches_per_step() + 0) * a.steps
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": a.steps, "warmup": max(a.warmup, 3),
+        "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+        "dtype": "f32", "data": "synthetic (seeded BJ.configs[%d] generator; targets = render of a perturbed copy)"
+        % a.config,
+        "config": {"workload": f"BJ.configs[{a.config}] sub-map mapping iteration", "gaussians": s.n,
+                   "width": W, "height": H, "views_per_step": V, "views_per_rank": len(ms.mine),
+                   "parallelism": f"view-sharded dp{world}, NCCL all-reduce of gradients" if world > 1 else "1 GPU",
+                   "l2": "256 MiB buffer written between timed steps (outside the step events)",
+                   "pairs_per_view": int(np.mean([x["pairs"] for x in stats_views])),
+                   "scanned_per_px": sum(x["scanned"] for x in stats_views) / (len(stats_views) * W * H),
+                   "contrib_per_px": sum(x["contrib"] for x in stats_views) / (len(stats_views) * W * H)},
+        "roofline": roof["render_bwd_pixels"],
+        "roofline_other": {"render_fwd": roof["render_fwd"]},
+        "clocks": clocks, "gpu_launches": launches, "sm_count": sm_count,
+    }
+    if rank == 0 and not a.profile and not a.no_e2e:
+        line["e2e"] = e2e_ours(a, s, ms, device)
+    if world > 1:
+        dist.barrier()
+    if rank == 0 and world == 1 and not a.profile and not a.no_tracking:
+        line["tracking"] = bench_tracking(device)
+    if rank == 0 and world == 1 and not a.profile and not a.no_cpu_baseline:
+        line["cpu_baseline"] = cpu_baseline(a, s)
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def e2e_ours(a, s, ms, device):
+    """Same metric through the public API with HOST buffers: every step copies
+    its inputs (Gaussian parameters, view poses, this rank's RGB-D targets)
+    from pinned host memory and reads the per-view losses back."""
+    import torch
+    P = ms.params
+    host = {k: getattr(P, k).cpu().pin_memory() for k in ("mean_opa", "quat", "logscale", "rgb")}
+    hviews = ms.views.cpu().pin_memory()
+    htc = {v: ms.tgt_color[v].cpu().pin_memory() for v in ms.mine}
+    htd = {v: ms.tgt_depth[v].cpu().pin_memory() for v in ms.mine}
+    hloss = torch.empty_like(ms.losses, device="cpu").pin_memory()
+    h2d = sum(t.numel() * t.element_size() for t in host.values()) + hviews.numel() * 4 + \
+        sum(htc[v].numel() * 4 + htd[v].numel() * 4 for v in ms.mine)
+    d2h = hloss.numel() * 4
+
+    def one():
+        for k, t in host.items():
+            getattr(P, k).copy_(t, non_blocking=True)
+        ms.views.copy_(hviews, non_blocking=True)
+        for v in ms.mine:
+            ms.tgt_color[v].copy_(htc[v], non_blocking=True)
+            ms.tgt_depth[v].copy_(htd[v], non_blocking=True)
+        ms.step()
+        hloss.copy_(ms.losses, non_blocking=True)
+
+    for _ in range(2):
+        one()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    n = max(3, a.steps // 2)
+    for _ in range(n):
+        one()
+    e1.record()
+    torch.cuda.synchronize()
+    ms_step = e0.elapsed_time(e1) / n
+    mp = ms.V * s.cam.width * s.cam.height / 1e6
+    return {"value": mp / (ms_step * 1e-3), "unit": UNIT, "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
+            "ms_per_step": ms_step}
+
+
+def bench_tracking(device):
+    """BJ.configs[2]: 200k Gaussians, 1200x680, 100 pose iterations in one CUDA graph."""
+    import torch
+    from paper_2312_10070_b200 import Params, Rasterizer, inputs
+    from paper_2312_10070_b200.pipeline import TrackingLoop
+    s = inputs.config2()
+    P = Params.from_numpy(*s.params(), device=device)
+    gt = torch.as_tensor(s.extra["gt_view"], device=device)
+    r = Rasterizer(s.n, s.cam, device=device)
+    r.size_for(P, gt)
+    r.forward(P, gt)
+    tc, td = r.frame.color.clone(), r.frame.depth.clone()
+    del r
+    loop = TrackingLoop(P, s.cam, tc, td, torch.as_tensor(s.extra["start_view"], device=device), iters=100)
+    loop.size()
+    loop.capture()
+    for _ in range(2):
+        loop.run()
+    torch.cuda.synchronize()
+    times = []
+    for _ in range(5):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        loop.reset()
+        e0.record()
+        loop.graph.replay()
+        e1.record()
+        torch.cuda.synchronize()
+        times.append(e0.elapsed_time(e1))
+    med = statistics.median(times)
+    v = loop.view.cpu().numpy().astype(np.float64)
+    R, t = v[:9].reshape(3, 3), v[9:]
+    rot_err = np.degrees(np.arccos(np.clip((np.trace(R) - 1) / 2, -1, 1)))
+    sv = s.extra["start_view"].astype(np.float64)
+    rot0 = np.degrees(np.arccos(np.clip((np.trace(sv[:9].reshape(3, 3)) - 1) / 2, -1, 1)))
+    return {"metric": "tracking iterations/s (BJ.configs[2], 200k Gaussians, 1200x680)",
+            "value": 100 / (med * 1e-3), "unit": "iter/s", "ms_per_iter": med / 100,
+            "graph": "100 iterations captured once (project, sort, render, loss, pose bwd, pose grad + Adam)",
+            "gpu_launches_per_iter": loop.launches_per_iter(),
+            "start_err": {"rot_deg": float(rot0), "trans_cm": float(np.linalg.norm(sv[9:]) * 100)},
+            "final_err": {"rot_deg": float(rot_err), "trans_cm": float(np.linalg.norm(t) * 100)}}
+
+
+def cpu_baseline(a, s, budget_s=30.0):
+    """The fp64 oracle as it stands, on this host's cores, on a bounded sample of
+    one view: full projection + binning, compositing + backward on a random
+    subset of tiles, the per-Gaussian chain in full; per-view time
+    extrapolated to all tiles."""
+    import oracle
+    t0 = time.perf_counter()
+    rng = np.random.default_rng(0)
+    p64 = oracle.params64(*s.params())
+    view = s.views[0].astype(np.float64)
+    cam = s.cam
+    T = cam.tiles
+    tiles = rng.choice(T, size=min(a.cpu_tiles, T), replace=False)
+    mask = np.zeros(T, np.uint8)
+    mask[tiles] = 1
+    ta = time.perf_counter()
+    pr = oracle.project(p64, view, cam)
+    idx, trg = oracle.bin_sort(pr["rect"], pr["culled"], pr["depth_key"], cam)
+    tb = time.perf_counter()
+    fr = oracle.render(pr, p64["rgb"], idx, trg, cam, tile_mask=mask)
+    tc_ = time.perf_counter()
+    gc, gd, ga = [np.zeros_like(x) for x in (fr["color"], fr["depth"], fr["alpha"])]
+    tgt_c = np.zeros_like(fr["color"])
+    tgt_d = np.ones_like(fr["depth"])
+    _, gc, gd = oracle.loss(cam, fr["color"], fr["depth"], tgt_c, tgt_d)
+    td0 = time.perf_counter()
+    oracle.backward(p64, view, cam, idx, trg, gc, gd, None, tile_mask=mask)
+    te = time.perf_counter()
+    oracle.backward(p64, view, cam, idx, trg, gc, gd, None, tile_mask=np.zeros(T, np.uint8))
+    tf = time.perf_counter()
+    t_ps = tb - ta
+    t_px = (tc_ - tb) + max((te - td0) - (tf - te), 0.0)
+    t_fixed = (tf - te) + (td0 - tc_)
+    per_view = t_ps + t_fixed + t_px * T / len(tiles)
+    mp = cam.width * cam.height / 1e6
+    return {"value": mp / per_view, "unit": UNIT, "cores": oracle.num_threads(), "kind": "oracle",
+            "sample": f"1 of {s.views.shape[0]} views: projection + binning of all {s.n} Gaussians, compositing + "
+                      f"backward on {len(tiles)} of {T} random tiles (per-pixel time extrapolated to all tiles), "
+                      f"per-Gaussian chain in full; {time.perf_counter() - t0:.1f} s of CPU work",
+            "s_per_view_extrapolated": per_view}
+
+
+def bench_reference(a):
+    """--impl reference: the fp64 oracle timed on the host cores (rank 0 only)."""
+    world, rank, _ = dist_env()
+    if rank != 0:
+        return
+    import oracle
+    from paper_2312_10070_b200 import inputs
+    s = {1: inputs.config1, 3: inputs.config3, 4: inputs.config4}[a.config]()
+    oracle.build()
+    warm = max(a.warmup, 0)
+    a.cpu_tiles = min(a.cpu_tiles, 48)
+    vals = []
+    for i in range(warm + a.steps):
+        r = cpu_baseline(a, s)
+        if i >= warm:
+            vals.append(r)
+    v = statistics.median(x["value"] for x in vals)
+    per_view = statistics.median(x["s_per_view_extrapolated"] for x in vals)
+    V = s.views.shape[0]
+    line = {"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": a.gpus, "steps": a.steps,
+            "warmup": warm, "ms_per_step": per_view * V * 1e3, "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded generator)",
+            "config": {"workload": f"BJ.configs[{a.config}] sub-map mapping iteration (oracle, sampled)",
+                       "gaussians": s.n, "width": s.cam.width, "height": s.cam.height, "views_per_step": V},
+            "cpu_baseline": {"value": v, "unit": UNIT, "cores": vals[0]["cores"], "kind": "oracle",
+                             "sample": vals[0]["sample"]},
+            "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    a = parse()
+    if a.impl == "reference":
+        bench_reference(a)
+    else:
+        bench_ours(a)
+
+
+if __name__ == "__main__":
+    main()

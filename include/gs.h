@@ -55,6 +55,8 @@ extern "C" {
 /* gs_render_bwd flags. */
 #define GS_GRAD_PARAMS 1u /* per-Gaussian parameter gradients (mapping) */
 #define GS_GRAD_POSE 2u   /* camera-pose partials (tracking)           */
+#define GS_BWD_PIXELS_ONLY 4u /* run only the per-pixel phase (S5)                 */
+#define GS_BWD_GAUSS_ONLY 8u  /* run only the per-Gaussian phase (S6)              */
 
 /* Pinhole camera, passed by value (R4, R5). */
 typedef struct gs_camera {
@@ -146,7 +148,10 @@ size_t gs_binsort_workspace_bytes(int32_t n, gs_camera cam);
 size_t gs_loss_workspace_bytes(gs_camera cam);
 
 /* Workspace bytes gs_render_bwd needs for n Gaussians: the grad2d scratch
- * [n][12] fp32, zeroed by the library at the start of every call. */
+ * [n][12] fp32 = (u, v, A, B), (C, p_z, logit, 0), (r, g, b, 0) per Gaussian.
+ * The caller zeroes it ONCE before first use; the per-Gaussian phase zeroes
+ * every record it consumes, so it is zero again when gs_render_bwd returns
+ * (no memset per call). */
 size_t gs_bwd_workspace_bytes(int32_t n);
 
 /* Number of pose-partial records [count][12] gs_render_bwd writes with
@@ -234,8 +239,11 @@ int gs_loss(gs_camera cam, const float *color, const float *depth,
  * to the 3-D parameters.
  *   dL_dcolor [3][H][W], dL_ddepth [H][W] (device); dL_dalpha [H][W]
  *             (device, nullable = 0)
- *   flags     GS_GRAD_PARAMS and/or GS_GRAD_POSE
- *   ws        (device) >= gs_bwd_workspace_bytes(n)
+ *   flags     GS_GRAD_PARAMS and/or GS_GRAD_POSE, optionally one of
+ *             GS_BWD_PIXELS_ONLY (accumulate grad2d only; it then holds the
+ *             2-D gradients) / GS_BWD_GAUSS_ONLY (chain an accumulated grad2d
+ *             and re-zero it); the two split calls equal one full call
+ *   ws        (device) >= gs_bwd_workspace_bytes(n), zero on entry
  *   g_mean_opa, g_quat, g_logscale, g_rgb (device) [n][4], ACCUMULATED (+=)
  *             in the layout of gs_params; required iff GS_GRAD_PARAMS
  *   pose_partials (device) [gs_pose_partials_count(n)][12] =

@@ -21,6 +21,8 @@ GS_ERR_CUDA = -3
 GS_ERR_UNSUPPORTED = -4
 GS_GRAD_PARAMS = 1
 GS_GRAD_POSE = 2
+GS_BWD_PIXELS_ONLY = 4
+GS_BWD_GAUSS_ONLY = 8
 
 
 class GsCamera(C.Structure):

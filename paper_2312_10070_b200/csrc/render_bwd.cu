@@ -160,7 +160,7 @@ struct GaussArgs {
   float fx, fy;
   const float4 *conic_o;
   const int32_t *tiles_touched;
-  const float *grad2d;
+  float *grad2d;
   float4 *g_mean_opa, *g_quat, *g_logscale, *g_rgb;
   float *pose_partials;
 };
@@ -181,9 +181,12 @@ __global__ void __launch_bounds__(256) k_bwd_gauss(GaussArgs a) {
     const float4 qf = __ldg(reinterpret_cast<const float4 *>(a.p.quat) + i);
     const float4 lf = __ldg(reinterpret_cast<const float4 *>(a.p.logscale) + i);
     const float4 cn = __ldg(a.conic_o + i);
-    const float4 ga = __ldg(reinterpret_cast<const float4 *>(a.grad2d) + 3 * i);
-    const float4 gb = __ldg(reinterpret_cast<const float4 *>(a.grad2d) + 3 * i + 1);
-    const float4 gc = __ldg(reinterpret_cast<const float4 *>(a.grad2d) + 3 * i + 2);
+    float4 *g2 = reinterpret_cast<float4 *>(a.grad2d) + 3 * i;
+    const float4 ga = g2[0], gb = g2[1], gc = g2[2];
+    const float4 z4 = make_float4(0.f, 0.f, 0.f, 0.f);
+    g2[0] = z4;  // leave the scratch zeroed for the next call
+    g2[1] = z4;
+    g2[2] = z4;
     const float gu = ga.x, gv = ga.y, gA = ga.z, gB = ga.w, gC = gb.x, gz = gb.y;
     const float mu[3] = {mo.x, mo.y, mo.z};
     float p[3];
@@ -362,8 +365,10 @@ extern "C" int gs_render_bwd(gs_params p, const gs_view *view, gs_camera cam, gs
                              float *g_rgb, float *pose_partials, void *stream) {
   using namespace gs;
   const bool want_params = flags & GS_GRAD_PARAMS, want_pose = flags & GS_GRAD_POSE;
+  const bool run_pixels = !(flags & GS_BWD_GAUSS_ONLY), run_gauss = !(flags & GS_BWD_PIXELS_ONLY);
   if (p.n < 0 || !view || !camera_ok(cam) || !tile_range || !T_final || !n_contrib || !dL_dcolor || !dL_ddepth ||
-      (flags & ~(GS_GRAD_PARAMS | GS_GRAD_POSE)) || !(want_params || want_pose)) {
+      (flags & ~(GS_GRAD_PARAMS | GS_GRAD_POSE | GS_BWD_PIXELS_ONLY | GS_BWD_GAUSS_ONLY)) ||
+      !(want_params || want_pose) || !(run_pixels || run_gauss)) {
     set_error("gs_render_bwd: invalid argument");
     return GS_ERR_INVALID_ARG;
   }
@@ -394,16 +399,19 @@ extern "C" int gs_render_bwd(gs_params p, const gs_view *view, gs_camera cam, gs
   }
   cudaStream_t s = as_stream(stream);
   float *grad2d = static_cast<float *>(ws);
-  if (p.n > 0) cudaMemsetAsync(grad2d, 0, size_t(p.n) * kG2 * sizeof(float), s);
+  if (p.n == 0) return GS_OK;
   BwdArgs b{reinterpret_cast<const double2 *>(pr.uv), reinterpret_cast<const float4 *>(pr.coef),
             reinterpret_cast<const float4 *>(pr.rgbz), reinterpret_cast<const float4 *>(pr.conic_o), sorted_idx,
             reinterpret_cast<const int2 *>(tile_range), T_final, n_contrib, dL_dcolor, dL_ddepth, dL_dalpha,
             cam.width, cam.height, tiles_x(cam), grad2d};
   const int T = tiles_x(cam) * tiles_y(cam);
-  if (want_params)
-    k_bwd_pixels<true><<<T, kTilePx, 0, s>>>(b);
-  else
-    k_bwd_pixels<false><<<T, kTilePx, 0, s>>>(b);
+  if (run_pixels) {
+    if (want_params)
+      k_bwd_pixels<true><<<T, kTilePx, 0, s>>>(b);
+    else
+      k_bwd_pixels<false><<<T, kTilePx, 0, s>>>(b);
+  }
+  if (!run_gauss) return check_launch("gs_render_bwd");
   GaussArgs g{p, view, cam.fx, cam.fy, reinterpret_cast<const float4 *>(pr.conic_o), pr.tiles_touched, grad2d,
               reinterpret_cast<float4 *>(g_mean_opa), reinterpret_cast<float4 *>(g_quat),
               reinterpret_cast<float4 *>(g_logscale), reinterpret_cast<float4 *>(g_rgb), pose_partials};

@@ -1,0 +1,158 @@
+"""Orchestration of the C-ABI calls for the two optimisations of Gaussian-SLAM.
+
+* ``MapStep`` — one multi-view sub-map mapping iteration (Eq. 12
+  colour L1 + depth L1 terms): for each keyframe view of this rank
+  gs_project -> gs_bin_sort -> gs_render_fwd -> gs_loss -> gs_render_bwd,
+  gradients accumulated (+=) into one contiguous buffer, then one NCCL
+  all-reduce (SUM) across ranks when world_size > 1.  The
+  1/V view mean is folded into gs_loss's lambdas, so the SUM is the mean.
+* ``TrackingLoop`` — frame-to-model tracking (Eqs. 14): K
+  iterations of render -> L1 loss -> pose-only backward -> gs_pose_grad with
+  the device-side Adam step, captured once in a CUDA graph (no host sync).
+
+No arithmetic of the method happens here: only buffer management and the
+order of calls.
+"""
+from __future__ import annotations
+
+import torch
+
+from .raster import GS_GRAD_PARAMS, GS_GRAD_POSE, Grads, Params, Rasterizer, lib
+
+
+def shard_views(n_views, rank, world):
+    """Round-robin view assignment: rank r takes views r, r + world, ..."""
+    return list(range(rank, n_views, world))
+
+
+class MapStep:
+    def __init__(self, params: Params, views, cam, tgt_color, tgt_depth, rank=0, world=1, group=None,
+                 lambda_color=1.0, lambda_depth=1.0, device="cuda"):
+        self.params = params
+        self.views = views                  # [V, 12] device tensor (all views)
+        self.V = views.shape[0]
+        self.mine = shard_views(self.V, rank, world)
+        self.tgt_color = tgt_color          # dict view -> [3,H,W] (only this rank's views needed)
+        self.tgt_depth = tgt_depth
+        self.world = world
+        self.group = group
+        self.lc = lambda_color / self.V     # R20: mean over the V views of an iteration
+        self.ld = lambda_depth / self.V
+        self.r = Rasterizer(params.n, cam, device=device)
+        self.grads = Grads.zeros(params.n, device)
+        self.losses = torch.zeros(max(len(self.mine), 1), 3, dtype=torch.float32, device=device)
+
+    def size(self, slack=1.25):
+        """Setup only (host sync): pair capacity = slack x max pairs over my views."""
+        best = 0
+        for v in self.mine:
+            self.r.project(self.params, self.views[v])
+            self.r.set_capacity(max(self.r.capacity, 1))
+            self.r.bin_sort()
+            torch.cuda.synchronize()
+            best = max(best, int(self.r.n_pairs.item()))
+        self.r.set_capacity(int(best * slack) + 1024)
+        return best
+
+    def view_fwd_bwd(self, k, v):
+        r = self.r
+        r.forward(self.params, self.views[v])
+        r.compute_loss(self.tgt_color[v], self.tgt_depth[v], None, self.lc, self.ld)
+        self.losses[k].copy_(r.loss)
+        r.backward(self.params, self.views[v], GS_GRAD_PARAMS, self.grads)
+
+    def step(self, on_view=None):
+        self.grads.zero_()
+        for k, v in enumerate(self.mine):
+            if on_view is None:
+                self.view_fwd_bwd(k, v)
+            else:
+                on_view(self, k, v)
+        if self.world > 1:
+            torch.distributed.all_reduce(self.grads.buf, op=torch.distributed.ReduceOp.SUM, group=self.group)
+        return self.grads
+
+    def launches_per_step(self):
+        """Kernels of ours launched per step."""
+        return len(self.mine) * kernels_per_view(self.r.cam)
+
+
+def sort_passes(cam):
+    import numpy as np
+    zb = int(np.float32(cam.z_near).view(np.uint32))
+    ze = int(np.float32(cam.z_far).view(np.uint32))
+    bits = max(1, (ze - zb).bit_length())
+    return (bits + 8) // 9
+
+
+def kernels_per_view(cam, loss=True, bwd=True):
+    # project 1; bin_sort: 5 per radix pass (upsweep, 3-kernel scan, downsweep)
+    # + count, 3-kernel scan, finish, scatter; render 1; loss 3; bwd 2
+    n = 1 + 5 * sort_passes(cam) + 6 + 1
+    if loss:
+        n += 3
+    if bwd:
+        n += 2
+    return n
+
+
+class TrackingLoop:
+    """K tracking iterations on one GPU, graph-captured."""
+
+    def __init__(self, params: Params, cam, tgt_color, tgt_depth, start_view, iters=100, lambda_color=1.0,
+                 lambda_depth=1.0, step=(2e-3, 1e-3, 0.9, 0.999, 1e-8), device="cuda"):
+        self.params = params
+        self.r = Rasterizer(params.n, cam, device=device)
+        self.tc, self.td = tgt_color, tgt_depth
+        self.start = start_view.clone()
+        self.view = start_view.clone()
+        self.adam = torch.zeros(13, dtype=torch.float32, device=device)
+        self.dtwist = torch.zeros(6, dtype=torch.float32, device=device)
+        self.iters = iters
+        self.lc, self.ld = lambda_color, lambda_depth
+        self.stepcfg = step
+        self.graph = None
+
+    def size(self, slack=1.5):
+        P = self.r.size_for(self.params, self.view)
+        self.r.set_capacity(int(P * slack) + 4096)
+        return P
+
+    def iteration(self):
+        r = self.r
+        r.forward(self.params, self.view)
+        r.compute_loss(self.tc, self.td, None, self.lc, self.ld)
+        r.backward(self.params, self.view, GS_GRAD_POSE)
+        r.pose_grad(self.view, self.stepcfg, self.adam, dL_dtwist=self.dtwist)
+
+    def reset(self):
+        self.view.copy_(self.start)
+        self.adam.zero_()
+
+    def capture(self):
+        self.reset()
+        s = torch.cuda.Stream()
+        s.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(s):
+            for _ in range(2):  # warm-up outside capture (lazy attributes, module load)
+                self.iteration()
+        torch.cuda.current_stream().wait_stream(s)
+        torch.cuda.synchronize()
+        self.reset()
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g):
+            for _ in range(self.iters):
+                self.iteration()
+        self.graph = g
+        return g
+
+    def run(self):
+        self.reset()
+        if self.graph is None:
+            for _ in range(self.iters):
+                self.iteration()
+        else:
+            self.graph.replay()
+
+    def launches_per_iter(self):
+        return kernels_per_view(self.r.cam) + 1

@@ -16,10 +16,10 @@ from dataclasses import dataclass
 import torch
 
 from . import _lib
-from ._lib import GS_GRAD_PARAMS, GS_GRAD_POSE, GsCamera, GsError, GsParams, GsPoseStep, GsProj, check, lib
+from ._lib import GS_BWD_GAUSS_ONLY, GS_BWD_PIXELS_ONLY, GS_GRAD_PARAMS, GS_GRAD_POSE, GsCamera, GsError, GsParams, GsPoseStep, GsProj, check, lib
 
 __all__ = ["Params", "Grads", "Proj", "Frame", "Rasterizer", "camera", "gs_project", "gs_bin_sort",
-           "gs_render_fwd", "gs_loss", "gs_render_bwd", "gs_pose_grad", "GS_GRAD_PARAMS", "GS_GRAD_POSE",
+           "gs_render_fwd", "gs_loss", "gs_render_bwd", "gs_pose_grad", "GS_GRAD_PARAMS", "GS_GRAD_POSE", "GS_BWD_PIXELS_ONLY", "GS_BWD_GAUSS_ONLY",
            "GsError", "device_check"]
 
 
@@ -162,14 +162,19 @@ def gs_loss(cam: GsCamera, color, depth, tgt_color, tgt_depth, weight, lambda_co
 
 def gs_render_bwd(params: Params, view, cam: GsCamera, proj: Proj, sorted_idx, tile_range, T_final, n_contrib,
                   dL_dcolor, dL_ddepth, dL_dalpha, flags, ws, grads: Grads = None, pose_partials=None,
-                  stream=None):
+                  stream=None, event_pair=None):
+    """event_pair: optional (start, end) torch.cuda.Event recorded around the call."""
     g = grads
+    if event_pair is not None:
+        event_pair[0].record(torch.cuda.current_stream() if stream is None else stream)
     check(lib().gs_render_bwd(params.c(), _p(view), cam, proj.c(), _p(sorted_idx), _p(tile_range), _p(T_final),
                               _p(n_contrib), _p(dL_dcolor), _p(dL_ddepth), _p(dL_dalpha), int(flags), _p(ws),
                               ws.numel() * ws.element_size(),
                               _p(g.mean_opa) if g is not None else None, _p(g.quat) if g is not None else None,
                               _p(g.logscale) if g is not None else None, _p(g.rgb) if g is not None else None,
                               _p(pose_partials), _stream(stream)), "gs_render_bwd")
+    if event_pair is not None:
+        event_pair[1].record(torch.cuda.current_stream() if stream is None else stream)
 
 
 def gs_pose_grad(view, pose_partials, n_partials, step=None, adam_state=None, dL_dview=None, dL_dtwist=None,
@@ -212,7 +217,8 @@ class Rasterizer:
         self.loss = torch.zeros(3, dtype=torch.float32, device=device)
         self.dL_dcolor = torch.zeros(3, H, W, dtype=torch.float32, device=device)
         self.dL_ddepth = torch.zeros(H, W, dtype=torch.float32, device=device)
-        self.bwd_ws = torch.empty((L.gs_bwd_workspace_bytes(n) + 15) // 16 * 4, dtype=torch.float32, device=device)
+        # zeroed once; gs_render_bwd returns it zeroed (include/gs.h)
+        self.bwd_ws = torch.zeros((L.gs_bwd_workspace_bytes(n) + 15) // 16 * 4, dtype=torch.float32, device=device)
         self.n_partials = L.gs_pose_partials_count(n)
         self.pose_partials = torch.zeros(self.n_partials, 12, dtype=torch.float32, device=device)
         self.capacity = 0
@@ -222,8 +228,9 @@ class Rasterizer:
 
     @property
     def grad2d(self):
-        """The [N, 12] 2-D gradient scratch of the last gs_render_bwd:
-        (u, v, A, B), (C, p_z, logit, 0), (r, g, b, 0)."""
+        """The [N, 12] 2-D gradient scratch, (u, v, A, B), (C, p_z, logit, 0),
+        (r, g, b, 0): holds the 2-D gradients only between a
+        GS_BWD_PIXELS_ONLY and a GS_BWD_GAUSS_ONLY call."""
         return self.bwd_ws[: self.n * 12].view(self.n, 12)
 
     def set_capacity(self, capacity):
@@ -266,11 +273,11 @@ class Rasterizer:
         return self.loss
 
     def backward(self, params: Params, view, flags=GS_GRAD_PARAMS, grads: Grads = None, dL_dcolor=None,
-                 dL_ddepth=None, dL_dalpha=None):
+                 dL_ddepth=None, dL_dalpha=None, event_pair=None):
         gs_render_bwd(params, view, self.cam, self.proj, self.sorted_idx, self.tile_range, self.frame.T_final,
                       self.frame.n_contrib, self.dL_dcolor if dL_dcolor is None else dL_dcolor,
                       self.dL_ddepth if dL_ddepth is None else dL_ddepth, dL_dalpha, flags, self.bwd_ws, grads,
-                      self.pose_partials if flags & GS_GRAD_POSE else None)
+                      self.pose_partials if flags & GS_GRAD_POSE else None, event_pair=event_pair)
 
     def pose_grad(self, view, step=None, adam_state=None, dL_dview=None, dL_dtwist=None, dL_dqt=None):
         gs_pose_grad(view, self.pose_partials, self.n_partials, step, adam_state, dL_dview, dL_dtwist, dL_dqt)

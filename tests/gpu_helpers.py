@@ -5,6 +5,7 @@ import torch
 
 import oracle
 from paper_2312_10070_b200 import GS_GRAD_PARAMS, GS_GRAD_POSE, Grads, Params, Rasterizer
+from paper_2312_10070_b200.raster import GS_BWD_GAUSS_ONLY, GS_BWD_PIXELS_ONLY
 
 # grad2d columns of the CUDA scratch in the oracle's g2 order
 # (u, v, A, B, C, logit, r, g, b, p_z)
@@ -71,9 +72,13 @@ def gpu_backward(r, P, v, gC, gD, gA=None, flags=GS_GRAD_PARAMS):
     d = dev()
     t = lambda a: None if a is None else torch.as_tensor(np.ascontiguousarray(a, np.float32), device=d)
     g = Grads.zeros(r.n, d) if flags & GS_GRAD_PARAMS else None
-    r.backward(P, v, flags, g, dL_dcolor=t(gC), dL_ddepth=t(gD), dL_dalpha=t(gA))
+    maps = dict(dL_dcolor=t(gC), dL_ddepth=t(gD), dL_dalpha=t(gA))
+    r.backward(P, v, flags | GS_BWD_PIXELS_ONLY, g, **maps)
     torch.cuda.synchronize()
-    out = dict(g2=to_np(r.grad2d)[:, G2_FROM_GPU])
+    out = dict(g2=to_np(r.grad2d)[:, G2_FROM_GPU].copy())
+    r.backward(P, v, flags | GS_BWD_GAUSS_ONLY, g, **maps)
+    torch.cuda.synchronize()
+    assert not to_np(r.grad2d).any()  # scratch returned zeroed
     if g is not None:
         out["g3"] = np.concatenate([to_np(g.mean_opa), to_np(g.quat), to_np(g.logscale), to_np(g.rgb)], 1)
     return out
