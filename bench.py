@@ -210,10 +210,11 @@ def bench_ours(a):
         raster.gs_render_bwd(m.params, m.views[v], r.cam, r.proj, r.sorted_idx, r.tile_range, r.frame.T_final,
                              r.frame.n_contrib, r.dL_dcolor, r.dL_ddepth, None,
                              raster.GS_GRAD_PARAMS | raster.GS_BWD_PIXELS_ONLY, r.bwd_ws, m.grads, None,
-                             event_pair=(b0, b1))
+                             event_pair=(b0, b1), tile_order=r.tile_order)
         raster.gs_render_bwd(m.params, m.views[v], r.cam, r.proj, r.sorted_idx, r.tile_range, r.frame.T_final,
                              r.frame.n_contrib, r.dL_dcolor, r.dL_ddepth, None,
-                             raster.GS_GRAD_PARAMS | raster.GS_BWD_GAUSS_ONLY, r.bwd_ws, m.grads, None)
+                             raster.GS_GRAD_PARAMS | raster.GS_BWD_GAUSS_ONLY, r.bwd_ws, m.grads, None,
+                             tile_order=r.tile_order)
         ev_bwd.append((b0, b1))
 
     for _ in range(max(a.warmup, 3)):

@@ -189,13 +189,17 @@ int gs_project(gs_params p, const gs_view *view, gs_camera cam, gs_proj out,
  *   capacity      length of sorted_idx
  *   sorted_idx    (device) [capacity] Gaussian ids, tile-major
  *   tile_range    (device) [T][2] int32 [start, end) into sorted_idx
+ *   tile_order    (device, nullable) [T] int32 tile ids by descending list
+ *                 length (64 buckets; order within a bucket unspecified): a
+ *                 scheduling hint for gs_render_fwd / gs_render_bwd, which
+ *                 then start the heaviest tiles first (no effect on results)
  *   n_pairs       (device) [1] int64 total pair count P
  *   cnt           (device) counters, nullable
  * If P > capacity, n_overflow is incremented, every tile range is set empty
  * and sorted_idx is left untouched (the caller re-sizes and repeats). */
 int gs_bin_sort(gs_proj pr, int32_t n, gs_camera cam, void *ws, size_t ws_bytes,
                 int64_t capacity, int32_t *sorted_idx, int32_t *tile_range,
-                int64_t *n_pairs, gs_counters *cnt, void *stream);
+                int32_t *tile_order, int64_t *n_pairs, gs_counters *cnt, void *stream);
 
 /* S3 — front-to-back alpha compositing (Eqs. 3, 4, 6; P:133-141, P:161-166;
  * S:129-138; R11-R15).
@@ -204,14 +208,16 @@ int gs_bin_sort(gs_proj pr, int32_t n, gs_camera cam, void *ws, size_t ws_bytes,
  * alpha = min(o exp(-1/2 Delta^T conic Delta), 0.999); skip if alpha < 1/255;
  * C += c alpha T; D += p_z alpha T; A += alpha T; T *= (1 - alpha); stop
  * after compositing an entry that leaves T < 1e-4.  Background is zero.
+ *   tile_order (device, nullable) from gs_bin_sort: launch order of the tiles
  *   color     (device) [3][H][W]    depth, alpha, T_final (device) [H][W]
  *   n_contrib (device) [H][W] int32 (position in the tile list of the last
  *             composited entry) + 1, 0 if none
  *   stats     (device, nullable) [2][H][W] int32: entries scanned, entries
  *             composited — the per-pixel counts of SURVEY §8(d). */
 int gs_render_fwd(gs_proj pr, const int32_t *sorted_idx, const int32_t *tile_range,
-                  gs_camera cam, float *color, float *depth, float *alpha,
-                  float *T_final, int32_t *n_contrib, int32_t *stats, void *stream);
+                  const int32_t *tile_order, gs_camera cam, float *color, float *depth,
+                  float *alpha, float *T_final, int32_t *n_contrib, int32_t *stats,
+                  void *stream);
 
 /* S4 — L1 colour + L1 depth loss (Eqs. 9, 10 L1 part, 12; P:178-202;
  * S:256-264; R20, R21).
@@ -237,6 +243,7 @@ int gs_loss(gs_camera cam, const float *color, const float *depth,
  * (Eq. 8 form), reduces per-Gaussian 2-D gradients (u, v, A, B, C, logit,
  * r, g, b, p_z) with warp shuffles before global atomics, then chains them
  * to the 3-D parameters.
+ *   tile_order (device, nullable) from gs_bin_sort: launch order of the tiles
  *   dL_dcolor [3][H][W], dL_ddepth [H][W] (device); dL_dalpha [H][W]
  *             (device, nullable = 0)
  *   flags     GS_GRAD_PARAMS and/or GS_GRAD_POSE, optionally one of
@@ -251,7 +258,7 @@ int gs_loss(gs_camera cam, const float *color, const float *depth,
  *             GS_GRAD_POSE, overwritten. */
 int gs_render_bwd(gs_params p, const gs_view *view, gs_camera cam, gs_proj pr,
                   const int32_t *sorted_idx, const int32_t *tile_range,
-                  const float *T_final, const int32_t *n_contrib,
+                  const int32_t *tile_order, const float *T_final, const int32_t *n_contrib,
                   const float *dL_dcolor, const float *dL_ddepth,
                   const float *dL_dalpha, uint32_t flags, void *ws, size_t ws_bytes,
                   float *g_mean_opa, float *g_quat, float *g_logscale, float *g_rgb,

@@ -26,7 +26,7 @@ NVCC_FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-I", INC
               "--expt-relaxed-constexpr", "-Xptxas", "-warn-spills"]
 PER_FILE = {"project.cu": ["--fmad=false"]}
 SOURCES = ["abi.cpp", "project.cu", "binsort.cu", "render_fwd.cu", "loss.cu", "render_bwd.cu", "pose.cu"]
-HEADERS = ["gs_internal.cuh"]
+HEADERS = ["gs_internal.cuh", "raster_common.cuh"]
 
 
 def nvcc():

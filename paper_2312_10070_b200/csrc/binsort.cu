@@ -290,7 +290,7 @@ __global__ void __launch_bounds__(kRThreads) k_radix_downsweep(RadixIn in, bool 
 #pragma unroll
   for (int r = 0; r < kRItems; ++r) ok[r] = radix_item(in, first, base + r * 32 + lane, limit, key[r], val[r]);
   // walk 1: per-warp digit counts
-#pragma unroll
+#pragma unroll 1
   for (int r = 0; r < kRItems; ++r) {
     const unsigned act = __ballot_sync(0xffffffffu, ok[r]);
     const uint32_t d = (key[r] >> shift) & (kRDigits - 1);
@@ -460,6 +460,42 @@ __global__ void k_bin_finish(const uint32_t *thist, int T, int nblk, const uint3
   }
 }
 
+// Tiles by descending list length, bucketed into 64 classes of
+// maxlen/64 (single CTA; order inside a bucket follows the atomics).
+__global__ void __launch_bounds__(1024) k_tile_order(const int2 *__restrict__ tile_range, int T, int32_t *order) {
+  __shared__ int s_max;
+  __shared__ unsigned s_cnt[64];
+  if (threadIdx.x == 0) s_max = 0;
+  if (threadIdx.x < 64) s_cnt[threadIdx.x] = 0;
+  __syncthreads();
+  int m = 0;
+  for (int t = threadIdx.x; t < T; t += blockDim.x) {
+    const int2 r = tile_range[t];
+    m = max(m, r.y - r.x);
+  }
+  atomicMax(&s_max, m);
+  __syncthreads();
+  const int den = s_max + 1;
+  for (int t = threadIdx.x; t < T; t += blockDim.x) {
+    const int2 r = tile_range[t];
+    atomicAdd(&s_cnt[63 - int((int64_t(r.y - r.x) * 64) / den)], 1u);
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    unsigned run = 0;
+    for (int b = 0; b < 64; ++b) {
+      const unsigned c = s_cnt[b];
+      s_cnt[b] = run;
+      run += c;
+    }
+  }
+  __syncthreads();
+  for (int t = threadIdx.x; t < T; t += blockDim.x) {
+    const int2 r = tile_range[t];
+    order[atomicAdd(&s_cnt[63 - int((int64_t(r.y - r.x) * 64) / den)], 1u)] = t;
+  }
+}
+
 __global__ void k_bin_scatter(const int32_t *__restrict__ sorted_vals, const uint32_t *__restrict__ cstart,
                               const short4 *__restrict__ rect, int T, int TX, int tbits, int nblk,
                               const uint32_t *__restrict__ thist, const uint32_t *__restrict__ overflow_flag,
@@ -497,8 +533,8 @@ extern "C" size_t gs_binsort_workspace_bytes(int32_t n, gs_camera cam) {
 }
 
 extern "C" int gs_bin_sort(gs_proj pr, int32_t n, gs_camera cam, void *ws, size_t ws_bytes, int64_t capacity,
-                           int32_t *sorted_idx, int32_t *tile_range, int64_t *n_pairs, gs_counters *cnt,
-                           void *stream) {
+                           int32_t *sorted_idx, int32_t *tile_range, int32_t *tile_order, int64_t *n_pairs,
+                           gs_counters *cnt, void *stream) {
   using namespace gs;
   if (n < 0 || !camera_ok(cam) || !tile_range || !n_pairs || capacity < 0 || (capacity > 0 && !sorted_idx)) {
     set_error("gs_bin_sort: invalid argument");
@@ -566,5 +602,6 @@ extern "C" int gs_bin_sort(gs_proj pr, int32_t n, gs_camera cam, void *ws, size_
                                                   misc + 2, cnt);
   k_bin_scatter<<<L.nblk_b, 32 * L.W, scat_smem, s>>>(svals, cstart, rect, L.T, L.TX, L.tbits, L.nblk_b, thist,
                                                       misc + 2, sorted_idx);
+  if (tile_order) k_tile_order<<<1, 1024, 0, s>>>(reinterpret_cast<const int2 *>(tile_range), L.T, tile_order);
   return check_launch("gs_bin_sort");
 }

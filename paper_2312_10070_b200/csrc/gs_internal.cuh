@@ -37,32 +37,6 @@ __device__ __forceinline__ float ex2_approx(float x) {
   return y;
 }
 
-// The single alpha evaluation used by BOTH gs_render_fwd and gs_render_bwd
-// (H5: bit-identical replay).  Eq. 4: alpha~ = o exp(-sigma),
-// sigma = 1/2 Delta^T conic Delta, evaluated as
-//   log2 alpha~ = log2 o - (a' dx + b' dy)^2 - (d' dy)^2
-// with tile-local fp32 offsets (H2) and explicit round-to-nearest intrinsics
-// so no contraction can differ between the two kernels.
-// Returns the exponent e; alpha~ = 2^e.
-__device__ __forceinline__ float alpha_exponent(float4 coef, float ul, float vl, float fpx,
-                                                float fpy, float &dx, float &dy) {
-  dx = __fsub_rn(ul, fpx);
-  dy = __fsub_rn(vl, fpy);
-  float y2 = __fmul_rn(coef.z, dy);
-  float y1 = __fmaf_rn(coef.x, dx, __fmul_rn(coef.y, dy));
-  float e = __fmaf_rn(-y2, y2, coef.w);
-  return __fmaf_rn(-y1, y1, e);
-}
-
-// alpha = min(alpha~, 0.999); returns true iff the entry composites
-// (alpha >= 1/255, R11).  alpha_t receives alpha~.
-__device__ __forceinline__ bool alpha_decide(float e, float &alpha, float &alpha_t) {
-  if (e < kExpSkip) return false;
-  alpha_t = ex2_approx(e);
-  alpha = fminf(alpha_t, kAlphaMax);
-  return alpha >= kAlphaMin;
-}
-
 __device__ __forceinline__ unsigned lanemask_lt() {
   unsigned m;
   asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));

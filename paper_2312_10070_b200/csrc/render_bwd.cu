@@ -13,17 +13,12 @@
 // S6 (k_bwd_gauss): one thread per visible Gaussian chains the 2-D gradients
 // to mean, quaternion, log-scales, opacity logit and colour ("derived as in
 // [kerbl]"), and for tracking reduces the pose partials block-wise.
-#include "gs_internal.cuh"
+#include "raster_common.cuh"
 
 namespace gs {
 
 // grad2d record [n][12]: (u, v, A, B), (C, p_z, logit, 0), (r, g, b, 0)
 constexpr int kG2 = 12;
-
-__device__ __forceinline__ void red_add_v4(float *addr, float a, float b, float c, float d) {
-  asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(addr), "f"(a), "f"(b), "f"(c), "f"(d)
-               : "memory");
-}
 
 struct BwdArgs {
   const double2 *uv;
@@ -32,6 +27,7 @@ struct BwdArgs {
   const float4 *conic_o;
   const int32_t *sorted_idx;
   const int2 *tile_range;
+  const int32_t *tile_order;
   const float *T_final;
   const int32_t *n_contrib;
   const float *dL_dcolor, *dL_ddepth, *dL_dalpha;
@@ -39,116 +35,176 @@ struct BwdArgs {
   float *grad2d;
 };
 
+// Transposed warp reduce-scatter of 10 values (u, v, A, B, C, z, logit, r, g, b):
+// 12 shuffles instead of 5 x 10.  Each stage halves the lanes' value sets;
+// on return this lane holds the warp total of value `idx`, and `writer` is
+// set on exactly one lane per value.
+__device__ __forceinline__ float warp_reduce10(const float v[10], int &idx, bool &writer) {
+  const unsigned F = 0xffffffffu;
+  const int lane = threadIdx.x & 31;
+  const bool h16 = lane & 16, h8 = lane & 8, h4 = lane & 4, h2 = lane & 2, h1 = lane & 1;
+  float a[5];
+#pragma unroll
+  for (int k = 0; k < 5; ++k) {  // A (xor 16): low half keeps 0..4, high half 5..9
+    const float snd = h16 ? v[k] : v[k + 5];
+    a[k] = (h16 ? v[k + 5] : v[k]) + __shfl_xor_sync(F, snd, 16);
+  }
+  float b[3];
+#pragma unroll
+  for (int k = 0; k < 3; ++k) {  // B (xor 8): !h8 keeps a0..a2, h8 keeps a3, a4
+    const float snd = h8 ? a[k] : (k < 2 ? a[3 + k] : 0.f);
+    const float r = __shfl_xor_sync(F, snd, 8);
+    b[k] = h8 ? (k < 2 ? a[3 + k] + r : 0.f) : a[k] + r;
+  }
+  // C (xor 4): (!h8,!h4) keeps b0,b1; (!h8,h4) keeps b2; (h8,!h4) keeps b0; (h8,h4) keeps b1
+  const float s1 = !h8 ? (!h4 ? b[2] : b[0]) : (!h4 ? b[1] : b[0]);
+  const float s2 = (!h8 && h4) ? b[1] : 0.f;
+  const float r1 = __shfl_xor_sync(F, s1, 4);
+  const float r2 = __shfl_xor_sync(F, s2, 4);
+  const bool two = !h8 && !h4;
+  const float c0 = (!h8 ? (!h4 ? b[0] : b[2]) : (!h4 ? b[0] : b[1])) + r1;
+  const float c1 = b[1] + r2;  // meaningful only when `two`
+  // D (xor 2): lanes holding two values split them; others add their pair
+  const float sd = two ? (h2 ? c0 : c1) : c0;
+  const float d0 = (two ? (h2 ? c1 : c0) : c0) + __shfl_xor_sync(F, sd, 2);
+  const float e0 = d0 + __shfl_xor_sync(F, d0, 1);  // E (xor 1)
+  const int sub = two ? (h2 ? 1 : 0) : (!h8 ? 2 : (!h4 ? 3 : 4));
+  idx = (h16 ? 5 : 0) + sub;
+  writer = !h1 && (two || !h2);
+  return e0;
+}
+
 template <bool kParams>
-__global__ void __launch_bounds__(kTilePx) k_bwd_pixels(BwdArgs a) {
-  __shared__ int s_idx[kTilePx];
-  __shared__ float2 s_uv[kTilePx];
-  __shared__ float4 s_coef[kTilePx];
-  __shared__ float4 s_rgbz[kTilePx];
-  __shared__ float4 s_conic[kTilePx];
+__global__ void __launch_bounds__(kRThreadsTile) k_bwd_pixels(BwdArgs a) {
+  __shared__ int s_idx[kBatch];
+  __shared__ float2 s_uv[kBatch];
+  __shared__ float4 s_coef[kBatch];
+  __shared__ float4 s_rgbz[kBatch];
+  __shared__ float4 s_conic[kBatch];
+  __shared__ float4 s_box[kBatch];
   __shared__ int s_lmax;
-  const int tile = blockIdx.x;
+  const int tile = a.tile_order ? __ldg(a.tile_order + blockIdx.x) : int(blockIdx.x);
   const int tx = tile % a.TX, ty = tile / a.TX;
-  const int lx = threadIdx.x & (kTile - 1), ly = threadIdx.x / kTile;
-  const int px = tx * kTile + lx, py = ty * kTile + ly;
-  const bool inside = px < a.W && py < a.H;
+  const PixGeom pg = pix_geom(tx, ty, a.H);
   const double ox = double(tx * kTile), oy = double(ty * kTile);
-  const float fpx = float(lx), fpy = float(ly);
   const int2 range = a.tile_range[tile];
-  const size_t HW = size_t(a.W) * a.H, q = size_t(py) * a.W + px;
-  float T = 1.f, G0 = 0.f, G1 = 0.f, G2 = 0.f, GD = 0.f, GA = 0.f;
-  int last = 0;
-  if (inside) {
-    T = a.T_final[q];
-    last = a.n_contrib[q];
-    G0 = a.dL_dcolor[q];
-    G1 = a.dL_dcolor[HW + q];
-    G2 = a.dL_dcolor[2 * HW + q];
-    GD = a.dL_ddepth[q];
-    GA = a.dL_dalpha ? a.dL_dalpha[q] : 0.f;
+  const size_t HW = size_t(a.W) * a.H;
+  float T[kPxPerThread], G0[kPxPerThread], G1[kPxPerThread], G2[kPxPerThread], GD[kPxPerThread],
+      GA[kPxPerThread];
+  float S0[kPxPerThread], S1[kPxPerThread], S2[kPxPerThread], SD[kPxPerThread], SA[kPxPerThread];
+  int last[kPxPerThread];
+  int tmax = 0;
+#pragma unroll
+  for (int k = 0; k < kPxPerThread; ++k) {
+    T[k] = 1.f;
+    G0[k] = G1[k] = G2[k] = GD[k] = GA[k] = 0.f;
+    S0[k] = S1[k] = S2[k] = SD[k] = SA[k] = 0.f;  // suffix accumulators (Eq. 8)
+    last[k] = 0;
+    if (pg.row_in && pg.px0 + k < a.W) {
+      const size_t q = size_t(pg.py) * a.W + pg.px0 + k;
+      T[k] = a.T_final[q];
+      last[k] = a.n_contrib[q];
+      G0[k] = a.dL_dcolor[q];
+      G1[k] = a.dL_dcolor[HW + q];
+      G2[k] = a.dL_dcolor[2 * HW + q];
+      GD[k] = a.dL_ddepth[q];
+      GA[k] = a.dL_dalpha ? a.dL_dalpha[q] : 0.f;
+      tmax = max(tmax, last[k]);
+    }
   }
   if (threadIdx.x == 0) s_lmax = 0;
   __syncthreads();
-  if (last > 0) atomicMax(&s_lmax, last);
+  // warp-level bound: entries at or beyond every lane's n_contrib are skipped
+  int wmax = tmax;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) wmax = max(wmax, __shfl_xor_sync(0xffffffffu, wmax, o));
+  if ((threadIdx.x & 31) == 0 && wmax > 0) atomicMax(&s_lmax, wmax);
   __syncthreads();
   const int lmax = s_lmax;
-  float S0 = 0.f, S1 = 0.f, S2 = 0.f, SD = 0.f, SA = 0.f;  // suffix accumulators (Eq. 8)
-  const int lane = threadIdx.x & 31;
-  for (int end = lmax; end > 0; end -= kTilePx) {
-    const int beg = max(end - kTilePx, 0);
+  for (int end = lmax; end > 0; end -= kBatch) {
+    const int beg = max(end - kBatch, 0);
     __syncthreads();
-    const int k = beg + threadIdx.x;
-    if (k < end) {
-      const int g = __ldg(a.sorted_idx + range.x + k);
-      const double2 u = __ldg(a.uv + g);
-      s_idx[threadIdx.x] = g;
-      s_uv[threadIdx.x] = make_float2(float(u.x - ox), float(u.y - oy));
-      s_coef[threadIdx.x] = __ldg(a.coef + g);
-      s_rgbz[threadIdx.x] = __ldg(a.rgbz + g);
-      s_conic[threadIdx.x] = __ldg(a.conic_o + g);
+#pragma unroll
+    for (int h = 0; h < kBatch / kRThreadsTile; ++h) {
+      const int i = h * kRThreadsTile + threadIdx.x;
+      const int k = beg + i;
+      if (k < end) {
+        const int g = __ldg(a.sorted_idx + range.x + k);
+        const double2 u = __ldg(a.uv + g);
+        const float4 cf = __ldg(a.coef + g);
+        const float ul = float(u.x - ox), vl = float(u.y - oy);
+        s_idx[i] = g;
+        s_uv[i] = make_float2(ul, vl);
+        s_coef[i] = cf;
+        s_rgbz[i] = __ldg(a.rgbz + g);
+        s_conic[i] = __ldg(a.conic_o + g);
+        s_box[i] = entry_box(cf, ul, vl);
+      }
     }
     __syncthreads();
-    for (int j = end - beg - 1; j >= 0; --j) {
-      const int pos = beg + j;
-      float gu = 0.f, gv = 0.f, gA = 0.f, gB = 0.f, gC = 0.f, gz = 0.f, gl = 0.f, gr = 0.f, gg = 0.f, gb = 0.f;
-      bool con = false;
-      if (pos < last) {
-        const float2 ul = s_uv[j];
-        float dx, dy, al, at;
-        const float e = alpha_exponent(s_coef[j], ul.x, ul.y, fpx, fpy, dx, dy);
-        con = alpha_decide(e, al, at);
-        if (con) {
-          const float4 c = s_rgbz[j];
-          const float om = __fsub_rn(1.f, al);
-          T = __fdiv_rn(T, om);  // T_j (R16)
-          const float w = al * T;
-          // dX/dalpha_j = T_j (X_j - S_X) (Eq. 8), chained with dL/dX (Eq. 7)
-          const float galpha = T * (G0 * (c.x - S0) + G1 * (c.y - S1) + G2 * (c.z - S2) + GD * (c.w - SD) +
-                                    GA * (1.f - SA));
-          gz = w * GD;  // dD/dz_j = alpha_j T_j
-          if (kParams) {
-            gr = w * G0;  // dC/dc_j = alpha_j T_j
-            gg = w * G1;
-            gb = w * G2;
-          }
-          S0 = fmaf(al, c.x - S0, S0);
-          S1 = fmaf(al, c.y - S1, S1);
-          S2 = fmaf(al, c.z - S2, S2);
-          SD = fmaf(al, c.w - SD, SD);
-          SA = fmaf(al, 1.f - SA, SA);
-          if (at < kAlphaMax) {  // a clamped alpha has no gradient (R17)
-            const float4 cn = s_conic[j];
-            if (kParams) gl = galpha * al * (1.f - cn.w);  // d alpha / d logit = alpha (1 - o)
-            const float gs = -al * galpha;                   // d alpha / d sigma = -alpha
-            gu = gs * (cn.x * dx + cn.y * dy);
-            gv = gs * (cn.y * dx + cn.z * dy);
-            gA = 0.5f * gs * dx * dx;
-            gB = gs * dx * dy;
-            gC = 0.5f * gs * dy * dy;
-          }
-        }
-      }
-      if (__ballot_sync(0xffffffffu, con) == 0) continue;
+    for (int j = min(end, wmax) - beg - 1; j >= 0; --j) {
+      const int pos = beg + j;  // entry position in the tile list
+      if (!box_hits_strip(s_box[j], pg.wy0)) continue;  // warp-uniform skip (no decision changes)
+      const float2 ul = s_uv[j];
+      const RowTerms rt = row_terms(s_coef[j], ul.x, ul.y, pg.fpy);
+      float e[kPxPerThread];
+      unsigned pass = 0;
 #pragma unroll
-      for (int o = 16; o > 0; o >>= 1) {
-        gu += __shfl_down_sync(0xffffffffu, gu, o);
-        gv += __shfl_down_sync(0xffffffffu, gv, o);
-        gA += __shfl_down_sync(0xffffffffu, gA, o);
-        gB += __shfl_down_sync(0xffffffffu, gB, o);
-        gC += __shfl_down_sync(0xffffffffu, gC, o);
-        gz += __shfl_down_sync(0xffffffffu, gz, o);
-        if (kParams) {
-          gl += __shfl_down_sync(0xffffffffu, gl, o);
-          gr += __shfl_down_sync(0xffffffffu, gr, o);
-          gg += __shfl_down_sync(0xffffffffu, gg, o);
-          gb += __shfl_down_sync(0xffffffffu, gb, o);
+      for (int k = 0; k < kPxPerThread; ++k) {
+        e[k] = pixel_exponent(rt, pg.fpx0 + float(k));
+        if (pos < last[k] && e[k] >= kExpSkip) pass |= 1u << k;
+      }
+      float acc[10];
+#pragma unroll
+      for (int m = 0; m < 10; ++m) acc[m] = 0.f;
+      bool any = false;
+      if (pass) {
+        const float4 c = s_rgbz[j];
+        const float4 cn = s_conic[j];
+#pragma unroll
+        for (int k = 0; k < kPxPerThread; ++k) {
+          if (!((pass >> k) & 1u)) continue;
+          const float at = ex2_approx(e[k]);
+          const float al = fminf(at, kAlphaMax);
+          if (al < kAlphaMin) continue;  // same decision as the forward (H5)
+          any = true;
+          T[k] = __fdividef(T[k], 1.f - al);  // T_j = T_{j+1} / (1 - alpha_j) (R16)
+          const float w = al * T[k];
+          // dX/dalpha_j = T_j (X_j - S_X) (Eq. 8), chained with dL/dX (Eq. 7)
+          const float galpha = T[k] * (G0[k] * (c.x - S0[k]) + G1[k] * (c.y - S1[k]) + G2[k] * (c.z - S2[k]) +
+                                       GD[k] * (c.w - SD[k]) + GA[k] * (1.f - SA[k]));
+          acc[5] = fmaf(w, GD[k], acc[5]);  // dD/dz_j = alpha_j T_j
+          if (kParams) {
+            acc[7] = fmaf(w, G0[k], acc[7]);  // dC/dc_j = alpha_j T_j
+            acc[8] = fmaf(w, G1[k], acc[8]);
+            acc[9] = fmaf(w, G2[k], acc[9]);
+          }
+          S0[k] = fmaf(al, c.x - S0[k], S0[k]);
+          S1[k] = fmaf(al, c.y - S1[k], S1[k]);
+          S2[k] = fmaf(al, c.z - S2[k], S2[k]);
+          SD[k] = fmaf(al, c.w - SD[k], SD[k]);
+          SA[k] = fmaf(al, 1.f - SA[k], SA[k]);
+          if (at < kAlphaMax) {  // a clamped alpha has no gradient (R17)
+            if (kParams) acc[6] = fmaf(galpha * al, 1.f - cn.w, acc[6]);  // d alpha/d logit = alpha (1 - o)
+            const float gs = -al * galpha;                               // d alpha/d sigma = -alpha
+            const float dx = ul.x - (pg.fpx0 + float(k)), dy = ul.y - pg.fpy;  // Delta = mu^I - pixel
+            const float gsx = gs * dx, gsy = gs * dy;
+            acc[0] = fmaf(cn.x, gsx, fmaf(cn.y, gsy, acc[0]));
+            acc[1] = fmaf(cn.y, gsx, fmaf(cn.z, gsy, acc[1]));
+            acc[2] = fmaf(0.5f * gsx, dx, acc[2]);
+            acc[3] = fmaf(gsx, dy, acc[3]);
+            acc[4] = fmaf(0.5f * gsy, dy, acc[4]);
+          }
         }
       }
-      if (lane == 0) {
-        float *dst = a.grad2d + size_t(s_idx[j]) * kG2;
-        red_add_v4(dst, gu, gv, gA, gB);
-        red_add_v4(dst + 4, gC, gz, gl, 0.f);
-        if (kParams) red_add_v4(dst + 8, gr, gg, gb, 0.f);
+      if (!__any_sync(0xffffffffu, any)) continue;
+      int idx;
+      bool writer;
+      const float tot = warp_reduce10(acc, idx, writer);
+      if (writer && (kParams || idx < 6)) {
+        // grad2d record: (u, v, A, B), (C, p_z, logit, 0), (r, g, b, 0)
+        const int off = idx < 7 ? idx : idx + 1;
+        atomicAdd(a.grad2d + size_t(s_idx[j]) * kG2 + off, tot);
       }
     }
   }
@@ -171,22 +227,37 @@ __global__ void __launch_bounds__(256) k_bwd_gauss(GaussArgs a) {
   float pose[12];
 #pragma unroll
   for (int k = 0; k < 12; ++k) pose[k] = 0.f;
-  if (i < a.p.n && __ldg(a.tiles_touched + i) > 0) {
+  // all loads are issued up front (one DRAM round trip per thread, not three)
+  const bool inb = i < a.p.n;
+  const int tt = inb ? __ldg(a.tiles_touched + i) : 0;
+  float4 mo = make_float4(0.f, 0.f, 0.f, 0.f), qf = mo, lf = mo, cn = mo, ga = mo, gb = mo, gc = mo;
+  float4 old_m = mo, old_q = mo, old_l = mo, old_c = mo;
+  float4 *g2 = reinterpret_cast<float4 *>(a.grad2d) + 3 * size_t(inb ? i : 0);
+  if (inb) {
+    mo = __ldg(reinterpret_cast<const float4 *>(a.p.mean_opa) + i);
+    qf = __ldg(reinterpret_cast<const float4 *>(a.p.quat) + i);
+    lf = __ldg(reinterpret_cast<const float4 *>(a.p.logscale) + i);
+    cn = __ldg(a.conic_o + i);
+    ga = g2[0];
+    gb = g2[1];
+    if (kParams) {
+      gc = g2[2];
+      old_m = a.g_mean_opa[i];
+      old_q = a.g_quat[i];
+      old_l = a.g_logscale[i];
+      old_c = a.g_rgb[i];
+    }
+  }
+  if (tt > 0) {
     float R[9], t[3];
 #pragma unroll
     for (int k = 0; k < 9; ++k) R[k] = __ldg(&a.view->R[k]);
 #pragma unroll
     for (int k = 0; k < 3; ++k) t[k] = __ldg(&a.view->t[k]);
-    const float4 mo = __ldg(reinterpret_cast<const float4 *>(a.p.mean_opa) + i);
-    const float4 qf = __ldg(reinterpret_cast<const float4 *>(a.p.quat) + i);
-    const float4 lf = __ldg(reinterpret_cast<const float4 *>(a.p.logscale) + i);
-    const float4 cn = __ldg(a.conic_o + i);
-    float4 *g2 = reinterpret_cast<float4 *>(a.grad2d) + 3 * i;
-    const float4 ga = g2[0], gb = g2[1], gc = g2[2];
     const float4 z4 = make_float4(0.f, 0.f, 0.f, 0.f);
     g2[0] = z4;  // leave the scratch zeroed for the next call
     g2[1] = z4;
-    g2[2] = z4;
+    if (kParams) g2[2] = z4;
     const float gu = ga.x, gv = ga.y, gA = ga.z, gB = ga.w, gC = gb.x, gz = gb.y;
     const float mu[3] = {mo.x, mo.y, mo.z};
     float p[3];
@@ -301,14 +372,10 @@ __global__ void __launch_bounds__(256) k_bwd_gauss(GaussArgs a) {
       const float dot = gw * qw + gx * qx + gy * qy + gzq * qz;
       // q^ = q / |q| (R18)
       const float4 gq = make_float4((gw - qw * dot) * iq, (gx - qx * dot) * iq, (gy - qy * dot) * iq, (gzq - qz * dot) * iq);
-      float4 m = a.g_mean_opa[i];
-      a.g_mean_opa[i] = make_float4(m.x + gmu[0], m.y + gmu[1], m.z + gmu[2], m.w + gb.z);
-      float4 qq = a.g_quat[i];
-      a.g_quat[i] = make_float4(qq.x + gq.x, qq.y + gq.y, qq.z + gq.z, qq.w + gq.w);
-      float4 l = a.g_logscale[i];
-      a.g_logscale[i] = make_float4(l.x + gls[0], l.y + gls[1], l.z + gls[2], l.w);
-      float4 cc = a.g_rgb[i];
-      a.g_rgb[i] = make_float4(cc.x + gc.x, cc.y + gc.y, cc.z + gc.z, cc.w);
+      a.g_mean_opa[i] = make_float4(old_m.x + gmu[0], old_m.y + gmu[1], old_m.z + gmu[2], old_m.w + gb.z);
+      a.g_quat[i] = make_float4(old_q.x + gq.x, old_q.y + gq.y, old_q.z + gq.z, old_q.w + gq.w);
+      a.g_logscale[i] = make_float4(old_l.x + gls[0], old_l.y + gls[1], old_l.z + gls[2], old_l.w);
+      a.g_rgb[i] = make_float4(old_c.x + gc.x, old_c.y + gc.y, old_c.z + gc.z, old_c.w);
     }
     if (kPose) {
       // dL/dt = dL/dp; dL/dR = dL/dp mu^T + 2 G_Sc R Sigma
@@ -359,7 +426,7 @@ extern "C" int32_t gs_pose_partials_count(int32_t n) {
 }
 
 extern "C" int gs_render_bwd(gs_params p, const gs_view *view, gs_camera cam, gs_proj pr, const int32_t *sorted_idx,
-                             const int32_t *tile_range, const float *T_final, const int32_t *n_contrib,
+                             const int32_t *tile_range, const int32_t *tile_order, const float *T_final, const int32_t *n_contrib,
                              const float *dL_dcolor, const float *dL_ddepth, const float *dL_dalpha, uint32_t flags,
                              void *ws, size_t ws_bytes, float *g_mean_opa, float *g_quat, float *g_logscale,
                              float *g_rgb, float *pose_partials, void *stream) {
@@ -402,14 +469,14 @@ extern "C" int gs_render_bwd(gs_params p, const gs_view *view, gs_camera cam, gs
   if (p.n == 0) return GS_OK;
   BwdArgs b{reinterpret_cast<const double2 *>(pr.uv), reinterpret_cast<const float4 *>(pr.coef),
             reinterpret_cast<const float4 *>(pr.rgbz), reinterpret_cast<const float4 *>(pr.conic_o), sorted_idx,
-            reinterpret_cast<const int2 *>(tile_range), T_final, n_contrib, dL_dcolor, dL_ddepth, dL_dalpha,
+            reinterpret_cast<const int2 *>(tile_range), tile_order, T_final, n_contrib, dL_dcolor, dL_ddepth, dL_dalpha,
             cam.width, cam.height, tiles_x(cam), grad2d};
   const int T = tiles_x(cam) * tiles_y(cam);
   if (run_pixels) {
     if (want_params)
-      k_bwd_pixels<true><<<T, kTilePx, 0, s>>>(b);
+      k_bwd_pixels<true><<<T, kRThreadsTile, 0, s>>>(b);
     else
-      k_bwd_pixels<false><<<T, kTilePx, 0, s>>>(b);
+      k_bwd_pixels<false><<<T, kRThreadsTile, 0, s>>>(b);
   }
   if (!run_gauss) return check_launch("gs_render_bwd");
   GaussArgs g{p, view, cam.fx, cam.fy, reinterpret_cast<const float4 *>(pr.conic_o), pr.tiles_touched, grad2d,

@@ -2,12 +2,17 @@
 // of colour (Eq. 3), depth (Eq. 6) and accumulated alpha (P:133-141,
 // P:161-166; R11-R15).
 //
-// One CTA per 16x16 tile, one pixel per thread.  The tile's depth-ordered
-// list is staged in batches of 256 records in shared memory: each thread
-// gathers one record (uv in fp64 -> tile-local fp32 offsets (H2), the H2b
-// coefficients, rgb and camera depth).  Every thread then walks the batch;
-// the CTA leaves as soon as all of its pixels have terminated (T < 1e-4).
-#include "gs_internal.cuh"
+// One CTA (4 warps) per 16x16 tile; each thread owns 2 pixels of a row
+// (raster_common.cuh).  The tile's depth-ordered list is staged in batches of
+// 128 records in shared memory (each thread gathers one: uv in fp64 ->
+// tile-local fp32 offsets (H2), the H2b coefficients, rgb and camera depth,
+// plus a conservative box of the entry's alpha >= 1/255 region).  A warp
+// skips entries whose box misses its 16x4 strip; otherwise the row terms of
+// the exponent are computed once per (thread, entry) and reused by the 2
+// pixels (2 FFMA + compare per pixel); ex2 and the blend run only for entries
+// that pass the exponent pre-test.  The CTA leaves as soon as all of its
+// pixels have terminated (T < 1e-4).
+#include "raster_common.cuh"
 
 namespace gs {
 
@@ -17,84 +22,110 @@ struct FwdArgs {
   const float4 *rgbz;
   const int32_t *sorted_idx;
   const int2 *tile_range;
+  const int32_t *tile_order;
   int W, H, TX;
   float *color, *depth, *alpha, *T_final;
   int32_t *n_contrib, *stats;
 };
 
 template <bool kStats>
-__global__ void __launch_bounds__(kTilePx) k_render_fwd(FwdArgs a) {
-  __shared__ float2 s_uv[kTilePx];
-  __shared__ float4 s_coef[kTilePx];
-  __shared__ float4 s_rgbz[kTilePx];
-  const int tile = blockIdx.x;
+__global__ void __launch_bounds__(kRThreadsTile) k_render_fwd(FwdArgs a) {
+  __shared__ float2 s_uv[kBatch];
+  __shared__ float4 s_coef[kBatch];
+  __shared__ float4 s_rgbz[kBatch];
+  __shared__ float4 s_box[kBatch];
+  const int tile = a.tile_order ? __ldg(a.tile_order + blockIdx.x) : int(blockIdx.x);
   const int tx = tile % a.TX, ty = tile / a.TX;
-  const int lx = threadIdx.x & (kTile - 1), ly = threadIdx.x / kTile;
-  const int px = tx * kTile + lx, py = ty * kTile + ly;
-  const bool inside = px < a.W && py < a.H;
+  const PixGeom pg = pix_geom(tx, ty, a.H);
   const double ox = double(tx * kTile), oy = double(ty * kTile);
-  const float fpx = float(lx), fpy = float(ly);
   const int2 range = a.tile_range[tile];
-  bool done = !inside;
-  float T = 1.f, c0 = 0.f, c1 = 0.f, c2 = 0.f, D = 0.f, A = 0.f;
-  int last = 0, nscan = 0, ncon = 0;
-  for (int start = range.x; start < range.y; start += kTilePx) {
-    if (__syncthreads_count(done) == kTilePx) break;
-    const int k = start + threadIdx.x;
-    if (k < range.y) {
-      const int g = __ldg(a.sorted_idx + k);
-      const double2 u = __ldg(a.uv + g);
-      s_uv[threadIdx.x] = make_float2(float(u.x - ox), float(u.y - oy));
-      s_coef[threadIdx.x] = __ldg(a.coef + g);
-      s_rgbz[threadIdx.x] = __ldg(a.rgbz + g);
+  float T[kPxPerThread], c0[kPxPerThread], c1[kPxPerThread], c2[kPxPerThread], D[kPxPerThread], A[kPxPerThread];
+  int last[kPxPerThread], nscan[kPxPerThread], ncon[kPxPerThread];
+  bool live[kPxPerThread];
+#pragma unroll
+  for (int k = 0; k < kPxPerThread; ++k) {
+    T[k] = 1.f;
+    c0[k] = c1[k] = c2[k] = D[k] = A[k] = 0.f;
+    last[k] = nscan[k] = ncon[k] = 0;
+    live[k] = pg.row_in && pg.px0 + k < a.W;
+  }
+  for (int start = range.x; start < range.y; start += kBatch) {
+    if (__syncthreads_count(live[0] || live[1]) == 0) break;
+    {
+      const int k = start + threadIdx.x;
+      if (k < range.y) {
+        const int g = __ldg(a.sorted_idx + k);
+        const double2 u = __ldg(a.uv + g);
+        const float4 cf = __ldg(a.coef + g);
+        const float ul = float(u.x - ox), vl = float(u.y - oy);
+        s_uv[threadIdx.x] = make_float2(ul, vl);
+        s_coef[threadIdx.x] = cf;
+        s_rgbz[threadIdx.x] = __ldg(a.rgbz + g);
+        s_box[threadIdx.x] = entry_box(cf, ul, vl);
+      }
     }
     __syncthreads();
-    const int cnt = min(kTilePx, range.y - start);
-    if (!done) {
-      for (int j = 0; j < cnt; ++j) {
-        const float2 ul = s_uv[j];
-        float dx, dy;
-        const float e = alpha_exponent(s_coef[j], ul.x, ul.y, fpx, fpy, dx, dy);
-        if (kStats) ++nscan;
-        float al, at;
-        if (!alpha_decide(e, al, at)) continue;
-        const float4 c = s_rgbz[j];
-        const float w = __fmul_rn(al, T);  // alpha_j T_j
-        c0 = __fmaf_rn(c.x, w, c0);        // Eq. 3
-        c1 = __fmaf_rn(c.y, w, c1);
-        c2 = __fmaf_rn(c.z, w, c2);
-        D = __fmaf_rn(c.w, w, D);          // Eq. 6 (camera-frame z, R12)
-        A = __fadd_rn(A, w);               // R14
-        T = __fmul_rn(T, __fsub_rn(1.f, al));
-        last = start - range.x + j + 1;
-        if (kStats) ++ncon;
-        if (T < kTEps) {                   // include, then stop (R11)
-          done = true;
-          break;
-        }
+    const int cnt = min(kBatch, range.y - start);
+    for (int j = 0; j < cnt && (live[0] || live[1]); ++j) {
+      if (kStats) {
+#pragma unroll
+        for (int k = 0; k < kPxPerThread; ++k) nscan[k] += live[k];
+      }
+      if (!box_hits_strip(s_box[j], pg.wy0)) continue;  // warp-uniform skip
+      const float2 ul = s_uv[j];
+      const RowTerms rt = row_terms(s_coef[j], ul.x, ul.y, pg.fpy);
+      float e[kPxPerThread];
+      bool pass[kPxPerThread];
+#pragma unroll
+      for (int k = 0; k < kPxPerThread; ++k) {
+        e[k] = pixel_exponent(rt, pg.fpx0 + float(k));
+        pass[k] = live[k] && e[k] >= kExpSkip;
+      }
+      if (!(pass[0] || pass[1])) continue;
+      const float4 c = s_rgbz[j];
+      const int pos = start - range.x + j + 1;
+#pragma unroll
+      for (int k = 0; k < kPxPerThread; ++k) {
+        if (!pass[k]) continue;
+        const float al = fminf(ex2_approx(e[k]), kAlphaMax);
+        if (al < kAlphaMin) continue;         // skip (R11)
+        const float w = __fmul_rn(al, T[k]);  // alpha_j T_j
+        c0[k] = __fmaf_rn(c.x, w, c0[k]);     // Eq. 3
+        c1[k] = __fmaf_rn(c.y, w, c1[k]);
+        c2[k] = __fmaf_rn(c.z, w, c2[k]);
+        D[k] = __fmaf_rn(c.w, w, D[k]);       // Eq. 6 (camera-frame z, R12)
+        A[k] = __fadd_rn(A[k], w);            // R14
+        T[k] = __fmul_rn(T[k], __fsub_rn(1.f, al));
+        last[k] = pos;
+        if (kStats) ++ncon[k];
+        live[k] = !(T[k] < kTEps);            // include, then stop (R11)
       }
     }
   }
-  if (inside) {
-    const size_t HW = size_t(a.W) * a.H, q = size_t(py) * a.W + px;
-    a.color[q] = c0;
-    a.color[HW + q] = c1;
-    a.color[2 * HW + q] = c2;
-    a.depth[q] = D;
-    a.alpha[q] = A;
-    a.T_final[q] = T;
-    a.n_contrib[q] = last;
+  if (!pg.row_in) return;
+  const size_t HW = size_t(a.W) * a.H;
+#pragma unroll
+  for (int k = 0; k < kPxPerThread; ++k) {
+    if (pg.px0 + k >= a.W) break;
+    const size_t q = size_t(pg.py) * a.W + pg.px0 + k;
+    a.color[q] = c0[k];
+    a.color[HW + q] = c1[k];
+    a.color[2 * HW + q] = c2[k];
+    a.depth[q] = D[k];
+    a.alpha[q] = A[k];
+    a.T_final[q] = T[k];
+    a.n_contrib[q] = last[k];
     if (kStats) {
-      a.stats[q] = nscan;
-      a.stats[HW + q] = ncon;
+      a.stats[q] = nscan[k];
+      a.stats[HW + q] = ncon[k];
     }
   }
 }
 
 }  // namespace gs
 
-extern "C" int gs_render_fwd(gs_proj pr, const int32_t *sorted_idx, const int32_t *tile_range, gs_camera cam,
-                             float *color, float *depth, float *alpha, float *T_final, int32_t *n_contrib,
+extern "C" int gs_render_fwd(gs_proj pr, const int32_t *sorted_idx, const int32_t *tile_range,
+                             const int32_t *tile_order, gs_camera cam, float *color, float *depth, float *alpha, float *T_final, int32_t *n_contrib,
                              int32_t *stats, void *stream) {
   using namespace gs;
   if (!camera_ok(cam) || !tile_range || !color || !depth || !alpha || !T_final || !n_contrib) {
@@ -108,11 +139,11 @@ extern "C" int gs_render_fwd(gs_proj pr, const int32_t *sorted_idx, const int32_
   }
   FwdArgs a{reinterpret_cast<const double2 *>(pr.uv), reinterpret_cast<const float4 *>(pr.coef),
             reinterpret_cast<const float4 *>(pr.rgbz), sorted_idx, reinterpret_cast<const int2 *>(tile_range),
-            cam.width, cam.height, tiles_x(cam), color, depth, alpha, T_final, n_contrib, stats};
+            tile_order, cam.width, cam.height, tiles_x(cam), color, depth, alpha, T_final, n_contrib, stats};
   const int T = tiles_x(cam) * tiles_y(cam);
   if (stats)
-    k_render_fwd<true><<<T, kTilePx, 0, as_stream(stream)>>>(a);
+    k_render_fwd<true><<<T, kRThreadsTile, 0, as_stream(stream)>>>(a);
   else
-    k_render_fwd<false><<<T, kTilePx, 0, as_stream(stream)>>>(a);
+    k_render_fwd<false><<<T, kRThreadsTile, 0, as_stream(stream)>>>(a);
   return check_launch("gs_render_fwd");
 }

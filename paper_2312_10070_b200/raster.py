@@ -141,14 +141,15 @@ def gs_project(params: Params, view, cam: GsCamera, proj: Proj, counters=None, s
 
 
 def gs_bin_sort(proj: Proj, n, cam: GsCamera, ws, capacity, sorted_idx, tile_range, n_pairs, counters=None,
-                stream=None):
+                stream=None, tile_order=None):
     check(lib().gs_bin_sort(proj.c(), int(n), cam, _p(ws), ws.numel() * ws.element_size(), int(capacity),
-                            _p(sorted_idx), _p(tile_range), _p(n_pairs), _p(counters), _stream(stream)),
-          "gs_bin_sort")
+                            _p(sorted_idx), _p(tile_range), _p(tile_order), _p(n_pairs), _p(counters),
+                            _stream(stream)), "gs_bin_sort")
 
 
-def gs_render_fwd(proj: Proj, sorted_idx, tile_range, cam: GsCamera, frame: Frame, stats=False, stream=None):
-    check(lib().gs_render_fwd(proj.c(), _p(sorted_idx), _p(tile_range), cam, _p(frame.color), _p(frame.depth),
+def gs_render_fwd(proj: Proj, sorted_idx, tile_range, cam: GsCamera, frame: Frame, stats=False, stream=None,
+                  tile_order=None):
+    check(lib().gs_render_fwd(proj.c(), _p(sorted_idx), _p(tile_range), _p(tile_order), cam, _p(frame.color), _p(frame.depth),
                               _p(frame.alpha), _p(frame.T_final), _p(frame.n_contrib),
                               _p(frame.stats) if stats else None, _stream(stream)), "gs_render_fwd")
 
@@ -162,12 +163,13 @@ def gs_loss(cam: GsCamera, color, depth, tgt_color, tgt_depth, weight, lambda_co
 
 def gs_render_bwd(params: Params, view, cam: GsCamera, proj: Proj, sorted_idx, tile_range, T_final, n_contrib,
                   dL_dcolor, dL_ddepth, dL_dalpha, flags, ws, grads: Grads = None, pose_partials=None,
-                  stream=None, event_pair=None):
+                  stream=None, event_pair=None, tile_order=None):
     """event_pair: optional (start, end) torch.cuda.Event recorded around the call."""
     g = grads
     if event_pair is not None:
         event_pair[0].record(torch.cuda.current_stream() if stream is None else stream)
-    check(lib().gs_render_bwd(params.c(), _p(view), cam, proj.c(), _p(sorted_idx), _p(tile_range), _p(T_final),
+    check(lib().gs_render_bwd(params.c(), _p(view), cam, proj.c(), _p(sorted_idx), _p(tile_range),
+                              _p(tile_order), _p(T_final),
                               _p(n_contrib), _p(dL_dcolor), _p(dL_ddepth), _p(dL_dalpha), int(flags), _p(ws),
                               ws.numel() * ws.element_size(),
                               _p(g.mean_opa) if g is not None else None, _p(g.quat) if g is not None else None,
@@ -209,6 +211,7 @@ class Rasterizer:
             raise GsError("gs_binsort_workspace_bytes: problem not supported")
         self.sort_ws = torch.empty((ws + 15) // 16 * 4, dtype=torch.float32, device=device)
         self.tile_range = torch.empty(self.T, 2, dtype=torch.int32, device=device)
+        self.tile_order = torch.empty(self.T, dtype=torch.int32, device=device)
         self.n_pairs = torch.zeros(1, dtype=torch.int64, device=device)
         self.counters = torch.zeros(4, dtype=torch.int64, device=device)
         self.frame = Frame(H, W, device)
@@ -256,10 +259,11 @@ class Rasterizer:
 
     def bin_sort(self):
         gs_bin_sort(self.proj, self.n, self.cam, self.sort_ws, self.capacity, self.sorted_idx, self.tile_range,
-                    self.n_pairs, self.counters)
+                    self.n_pairs, self.counters, tile_order=self.tile_order)
 
     def render(self, stats=False):
-        gs_render_fwd(self.proj, self.sorted_idx, self.tile_range, self.cam, self.frame, stats)
+        gs_render_fwd(self.proj, self.sorted_idx, self.tile_range, self.cam, self.frame, stats,
+                      tile_order=self.tile_order)
 
     def forward(self, params: Params, view, stats=False):
         self.project(params, view)
@@ -277,7 +281,8 @@ class Rasterizer:
         gs_render_bwd(params, view, self.cam, self.proj, self.sorted_idx, self.tile_range, self.frame.T_final,
                       self.frame.n_contrib, self.dL_dcolor if dL_dcolor is None else dL_dcolor,
                       self.dL_ddepth if dL_ddepth is None else dL_ddepth, dL_dalpha, flags, self.bwd_ws, grads,
-                      self.pose_partials if flags & GS_GRAD_POSE else None, event_pair=event_pair)
+                      self.pose_partials if flags & GS_GRAD_POSE else None, event_pair=event_pair,
+                      tile_order=self.tile_order)
 
     def pose_grad(self, view, step=None, adam_state=None, dL_dview=None, dL_dtwist=None, dL_dqt=None):
         gs_pose_grad(view, self.pose_partials, self.n_partials, step, adam_state, dL_dview, dL_dtwist, dL_dqt)
