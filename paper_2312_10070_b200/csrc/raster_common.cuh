@@ -7,32 +7,40 @@
 
 namespace gs {
 
-// One CTA per 16x16 tile, 4 warps; every thread owns 2 adjacent pixels of one
-// row: lane -> columns 2*(lane&7), +1, row 4*warp + (lane>>3).  A warp covers a
-// 16x4 strip.  The 2 pixels share dy, so the row terms of the quadratic form
-// are evaluated once per (thread, entry).
-constexpr int kRThreadsTile = 128;
-constexpr int kPxPerThread = 2;
-constexpr int kWarpRows = 4;
-constexpr int kBatch = 128;  // records staged per shared-memory batch (1 per thread)
+// One CTA per 16x16 tile; every thread owns PX adjacent pixels of one row:
+// lane -> columns PX*(lane % (16/PX)) .. +PX-1, row (2 PX) w + lane / (16/PX).
+// A warp covers a 16 x (2 PX) strip; a tile has 8/PX warps.  The PX pixels
+// share dy, so the row terms of the quadratic form are evaluated once per
+// (thread, entry).  The forward uses PX = 2 (short per-warp critical path),
+// the backward PX = 4 (half the warp reductions per pixel).
+constexpr int kBatch = 128;  // records staged per shared-memory batch
+
+template <int PX>
+struct Geo {
+  static constexpr int kThreads = kTilePx / PX;
+  static constexpr int kWarps = kThreads / 32;
+  static constexpr int kLanesPerRow = kTile / PX;
+  static constexpr int kRows = 32 / kLanesPerRow;  // rows per warp strip
+  static constexpr int kRecPerThread = kBatch / kThreads;
+};
 
 struct PixGeom {
   int px0, py;  // first pixel of the thread (absolute)
   float fpx0;   // tile-local column of the first pixel
   float fpy;    // tile-local row
-  float wy0;    // first tile-local row of the warp's strip
   bool row_in;  // py < H
 };
 
+template <int PX>
 __device__ __forceinline__ PixGeom pix_geom(int tx, int ty, int H) {
+  using G = Geo<PX>;
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   PixGeom g;
-  const int lx = (lane & 7) * kPxPerThread, ly = w * kWarpRows + (lane >> 3);
+  const int lx = (lane % G::kLanesPerRow) * PX, ly = w * G::kRows + lane / G::kLanesPerRow;
   g.px0 = tx * kTile + lx;
   g.py = ty * kTile + ly;
   g.fpx0 = float(lx);
   g.fpy = float(ly);
-  g.wy0 = float(w * kWarpRows);
   g.row_in = g.py < H;
   return g;
 }
@@ -77,9 +85,29 @@ __device__ __forceinline__ float4 entry_box(float4 coef, float ul, float vl) {
   return make_float4(ul - hx, ul + hx, vl - hy, vl + hy);
 }
 
-// Does the box meet the warp's strip [0, 15] x [wy0, wy0 + kWarpRows - 1]?
-__device__ __forceinline__ bool box_hits_strip(float4 b, float wy0) {
-  return b.y >= 0.f && b.x <= float(kTile - 1) && b.w >= wy0 && b.z <= wy0 + float(kWarpRows - 1);
+// Bit w set iff the box meets warp w's strip [0, 15] x [R w, R w + R - 1].
+template <int PX>
+__device__ __forceinline__ unsigned box_strip_mask(float4 b) {
+  using G = Geo<PX>;
+  if (!(b.y >= 0.f && b.x <= float(kTile - 1))) return 0u;
+  unsigned m = 0u;
+#pragma unroll
+  for (int w = 0; w < G::kWarps; ++w) {
+    const float y0 = float(w * G::kRows), y1 = y0 + float(G::kRows - 1);
+    if (b.w >= y0 && b.z <= y1) m |= 1u << w;
+  }
+  return m;
+}
+
+// This warp's hit bitmaps over a staged batch of kBatch entries: word h has
+// bit l set iff entry 32 h + l hits the warp's strip (4 ballots per batch).
+__device__ __forceinline__ void warp_hits(const unsigned char *s_mask, int cnt, unsigned hits[kBatch / 32]) {
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+#pragma unroll
+  for (int h = 0; h < kBatch / 32; ++h) {
+    const int j = h * 32 + lane;
+    hits[h] = __ballot_sync(0xffffffffu, j < cnt && ((s_mask[j] >> w) & 1u));
+  }
 }
 
 }  // namespace gs

@@ -74,31 +74,41 @@ __device__ __forceinline__ float warp_reduce10(const float v[10], int &idx, bool
   return e0;
 }
 
+__device__ __forceinline__ void red_add_v4(float *addr, float x, float y, float z, float w) {
+  asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(addr), "f"(x), "f"(y), "f"(z), "f"(w)
+               : "memory");
+}
+
+constexpr int kBPX = 4;  // pixels per thread in the backward
+using BG = Geo<kBPX>;
+
+// acc layout: 0 u, 1 v, 2 2*A-term, 3 B, 4 2*C-term, 5 p_z, 6 logit, 7 r, 8 g, 9 b
+// (the 1/2 of dsigma/dA and dsigma/dC is applied once, by the writing lane)
 template <bool kParams>
-__global__ void __launch_bounds__(kRThreadsTile) k_bwd_pixels(BwdArgs a) {
+__global__ void __launch_bounds__(BG::kThreads) k_bwd_pixels(BwdArgs a) {
   __shared__ int s_idx[kBatch];
   __shared__ float2 s_uv[kBatch];
   __shared__ float4 s_coef[kBatch];
   __shared__ float4 s_rgbz[kBatch];
   __shared__ float4 s_conic[kBatch];
-  __shared__ float4 s_box[kBatch];
+  __shared__ unsigned char s_mask[kBatch];
   __shared__ int s_lmax;
   const int tile = a.tile_order ? __ldg(a.tile_order + blockIdx.x) : int(blockIdx.x);
   const int tx = tile % a.TX, ty = tile / a.TX;
-  const PixGeom pg = pix_geom(tx, ty, a.H);
+  const PixGeom pg = pix_geom<kBPX>(tx, ty, a.H);
   const double ox = double(tx * kTile), oy = double(ty * kTile);
   const int2 range = a.tile_range[tile];
   const size_t HW = size_t(a.W) * a.H;
-  float T[kPxPerThread], G0[kPxPerThread], G1[kPxPerThread], G2[kPxPerThread], GD[kPxPerThread],
-      GA[kPxPerThread];
-  float S0[kPxPerThread], S1[kPxPerThread], S2[kPxPerThread], SD[kPxPerThread], SA[kPxPerThread];
-  int last[kPxPerThread];
+  // per pixel: T (reconstructed back to front), upstream G, and the single
+  // suffix scalar Q = G . S of Eq. 8's accumulators S = (S_C, S_D, S_A):
+  // dL/dalpha_j = T_j (G . X_j - Q),  Q <- Q + alpha_j (G . X_j - Q)
+  float T[kBPX], G0[kBPX], G1[kBPX], G2[kBPX], GD[kBPX], GA[kBPX], Q[kBPX];
+  int last[kBPX];
   int tmax = 0;
 #pragma unroll
-  for (int k = 0; k < kPxPerThread; ++k) {
+  for (int k = 0; k < kBPX; ++k) {
     T[k] = 1.f;
-    G0[k] = G1[k] = G2[k] = GD[k] = GA[k] = 0.f;
-    S0[k] = S1[k] = S2[k] = SD[k] = SA[k] = 0.f;  // suffix accumulators (Eq. 8)
+    G0[k] = G1[k] = G2[k] = GD[k] = GA[k] = Q[k] = 0.f;
     last[k] = 0;
     if (pg.row_in && pg.px0 + k < a.W) {
       const size_t q = size_t(pg.py) * a.W + pg.px0 + k;
@@ -125,8 +135,8 @@ __global__ void __launch_bounds__(kRThreadsTile) k_bwd_pixels(BwdArgs a) {
     const int beg = max(end - kBatch, 0);
     __syncthreads();
 #pragma unroll
-    for (int h = 0; h < kBatch / kRThreadsTile; ++h) {
-      const int i = h * kRThreadsTile + threadIdx.x;
+    for (int r = 0; r < BG::kRecPerThread; ++r) {
+      const int i = r * BG::kThreads + threadIdx.x;
       const int k = beg + i;
       if (k < end) {
         const int g = __ldg(a.sorted_idx + range.x + k);
@@ -138,73 +148,93 @@ __global__ void __launch_bounds__(kRThreadsTile) k_bwd_pixels(BwdArgs a) {
         s_coef[i] = cf;
         s_rgbz[i] = __ldg(a.rgbz + g);
         s_conic[i] = __ldg(a.conic_o + g);
-        s_box[i] = entry_box(cf, ul, vl);
+        s_mask[i] = (unsigned char)box_strip_mask<kBPX>(entry_box(cf, ul, vl));
       }
     }
     __syncthreads();
-    for (int j = min(end, wmax) - beg - 1; j >= 0; --j) {
-      const int pos = beg + j;  // entry position in the tile list
-      if (!box_hits_strip(s_box[j], pg.wy0)) continue;  // warp-uniform skip (no decision changes)
-      const float2 ul = s_uv[j];
-      const RowTerms rt = row_terms(s_coef[j], ul.x, ul.y, pg.fpy);
-      float e[kPxPerThread];
-      unsigned pass = 0;
+    unsigned hits[kBatch / 32];
+    warp_hits(s_mask, min(end, wmax) - beg, hits);
+    // back to front over this warp's hits (entries missing its strip cannot
+    // pass the exponent pre-test at any of its pixels)
 #pragma unroll
-      for (int k = 0; k < kPxPerThread; ++k) {
-        e[k] = pixel_exponent(rt, pg.fpx0 + float(k));
-        if (pos < last[k] && e[k] >= kExpSkip) pass |= 1u << k;
-      }
-      float acc[10];
+    for (int h = kBatch / 32 - 1; h >= 0; --h) {
+      unsigned bits = hits[h];
+      while (bits) {
+        const int hb = 31 - __clz(bits);
+        bits &= ~(1u << hb);
+        const int j = h * 32 + hb;
+        const int pos = beg + j;  // entry position in the tile list
+        const float2 ul = s_uv[j];
+        const RowTerms rt = row_terms(s_coef[j], ul.x, ul.y, pg.fpy);
+        float e[kBPX];
+        bool pass[kBPX];
+        bool anyp = false;
 #pragma unroll
-      for (int m = 0; m < 10; ++m) acc[m] = 0.f;
-      bool any = false;
-      if (pass) {
-        const float4 c = s_rgbz[j];
-        const float4 cn = s_conic[j];
+        for (int k = 0; k < kBPX; ++k) {
+          e[k] = pixel_exponent(rt, pg.fpx0 + float(k));
+          pass[k] = pos < last[k] && e[k] >= kExpSkip;
+          anyp |= pass[k];
+        }
+        float acc[10];
 #pragma unroll
-        for (int k = 0; k < kPxPerThread; ++k) {
-          if (!((pass >> k) & 1u)) continue;
-          const float at = ex2_approx(e[k]);
-          const float al = fminf(at, kAlphaMax);
-          if (al < kAlphaMin) continue;  // same decision as the forward (H5)
-          any = true;
-          T[k] = __fdividef(T[k], 1.f - al);  // T_j = T_{j+1} / (1 - alpha_j) (R16)
-          const float w = al * T[k];
-          // dX/dalpha_j = T_j (X_j - S_X) (Eq. 8), chained with dL/dX (Eq. 7)
-          const float galpha = T[k] * (G0[k] * (c.x - S0[k]) + G1[k] * (c.y - S1[k]) + G2[k] * (c.z - S2[k]) +
-                                       GD[k] * (c.w - SD[k]) + GA[k] * (1.f - SA[k]));
-          acc[5] = fmaf(w, GD[k], acc[5]);  // dD/dz_j = alpha_j T_j
-          if (kParams) {
-            acc[7] = fmaf(w, G0[k], acc[7]);  // dC/dc_j = alpha_j T_j
-            acc[8] = fmaf(w, G1[k], acc[8]);
-            acc[9] = fmaf(w, G2[k], acc[9]);
-          }
-          S0[k] = fmaf(al, c.x - S0[k], S0[k]);
-          S1[k] = fmaf(al, c.y - S1[k], S1[k]);
-          S2[k] = fmaf(al, c.z - S2[k], S2[k]);
-          SD[k] = fmaf(al, c.w - SD[k], SD[k]);
-          SA[k] = fmaf(al, 1.f - SA[k], SA[k]);
-          if (at < kAlphaMax) {  // a clamped alpha has no gradient (R17)
-            if (kParams) acc[6] = fmaf(galpha * al, 1.f - cn.w, acc[6]);  // d alpha/d logit = alpha (1 - o)
-            const float gs = -al * galpha;                               // d alpha/d sigma = -alpha
-            const float dx = ul.x - (pg.fpx0 + float(k)), dy = ul.y - pg.fpy;  // Delta = mu^I - pixel
-            const float gsx = gs * dx, gsy = gs * dy;
-            acc[0] = fmaf(cn.x, gsx, fmaf(cn.y, gsy, acc[0]));
-            acc[1] = fmaf(cn.y, gsx, fmaf(cn.z, gsy, acc[1]));
-            acc[2] = fmaf(0.5f * gsx, dx, acc[2]);
-            acc[3] = fmaf(gsx, dy, acc[3]);
-            acc[4] = fmaf(0.5f * gsy, dy, acc[4]);
+        for (int m = 0; m < 10; ++m) acc[m] = 0.f;
+        bool any = false;
+        if (anyp) {
+          const float4 c = s_rgbz[j];
+          const float4 cn = s_conic[j];
+          const float dy = ul.y - pg.fpy;  // Delta = mu^I - pixel
+#pragma unroll
+          for (int k = 0; k < kBPX; ++k) {
+            if (!pass[k]) continue;
+            const float at = ex2_approx(e[k]);
+            const float al = fminf(at, kAlphaMax);
+            if (al < kAlphaMin) continue;  // same decision as the forward (H5)
+            any = true;
+            T[k] = __fdividef(T[k], 1.f - al);  // T_j = T_{j+1} / (1 - alpha_j) (R16)
+            const float w = al * T[k];
+            // Eq. 8 chained with Eq. 7 through the suffix scalar Q
+            const float gx = fmaf(G0[k], c.x, fmaf(G1[k], c.y, fmaf(G2[k], c.z, fmaf(GD[k], c.w, GA[k]))));
+            const float d = gx - Q[k];
+            const float galpha = T[k] * d;
+            Q[k] = fmaf(al, d, Q[k]);
+            acc[5] = fmaf(w, GD[k], acc[5]);  // dD/dz_j = alpha_j T_j
+            if (kParams) {
+              acc[7] = fmaf(w, G0[k], acc[7]);  // dC/dc_j = alpha_j T_j
+              acc[8] = fmaf(w, G1[k], acc[8]);
+              acc[9] = fmaf(w, G2[k], acc[9]);
+            }
+            if (at < kAlphaMax) {  // a clamped alpha has no gradient (R17)
+              if (kParams) acc[6] = fmaf(galpha * al, 1.f - cn.w, acc[6]);  // d alpha/d logit = alpha (1 - o)
+              const float gs = -al * galpha;                               // d alpha/d sigma = -alpha
+              const float dx = ul.x - (pg.fpx0 + float(k));
+              const float gsx = gs * dx, gsy = gs * dy;
+              acc[0] = fmaf(cn.x, gsx, fmaf(cn.y, gsy, acc[0]));
+              acc[1] = fmaf(cn.y, gsx, fmaf(cn.z, gsy, acc[1]));
+              acc[2] = fmaf(gsx, dx, acc[2]);
+              acc[3] = fmaf(gsx, dy, acc[3]);
+              acc[4] = fmaf(gsy, dy, acc[4]);
+            }
           }
         }
-      }
-      if (!__any_sync(0xffffffffu, any)) continue;
-      int idx;
-      bool writer;
-      const float tot = warp_reduce10(acc, idx, writer);
-      if (writer && (kParams || idx < 6)) {
-        // grad2d record: (u, v, A, B), (C, p_z, logit, 0), (r, g, b, 0)
-        const int off = idx < 7 ? idx : idx + 1;
-        atomicAdd(a.grad2d + size_t(s_idx[j]) * kG2 + off, tot);
+        const unsigned ball = __ballot_sync(0xffffffffu, any);
+        if (!ball) continue;
+        float *dst = a.grad2d + size_t(s_idx[j]) * kG2;
+        if (__popc(ball) <= 2) {  // few contributing lanes: write directly, skip the reduction
+          if (any) {
+            // grad2d record: (u, v, A, B), (C, p_z, logit, 0), (r, g, b, 0)
+            red_add_v4(dst, acc[0], acc[1], 0.5f * acc[2], acc[3]);
+            red_add_v4(dst + 4, 0.5f * acc[4], acc[5], acc[6], 0.f);
+            if (kParams) red_add_v4(dst + 8, acc[7], acc[8], acc[9], 0.f);
+          }
+          continue;
+        }
+        int idx;
+        bool writer;
+        const float tot = warp_reduce10(acc, idx, writer);
+        if (writer && (kParams || idx < 6)) {
+          const int off = idx < 7 ? idx : idx + 1;
+          atomicAdd(dst + off, (idx == 2 || idx == 4) ? 0.5f * tot : tot);
+        }
       }
     }
   }
@@ -474,9 +504,9 @@ extern "C" int gs_render_bwd(gs_params p, const gs_view *view, gs_camera cam, gs
   const int T = tiles_x(cam) * tiles_y(cam);
   if (run_pixels) {
     if (want_params)
-      k_bwd_pixels<true><<<T, kRThreadsTile, 0, s>>>(b);
+      k_bwd_pixels<true><<<T, BG::kThreads, 0, s>>>(b);
     else
-      k_bwd_pixels<false><<<T, kRThreadsTile, 0, s>>>(b);
+      k_bwd_pixels<false><<<T, BG::kThreads, 0, s>>>(b);
   }
   if (!run_gauss) return check_launch("gs_render_bwd");
   GaussArgs g{p, view, cam.fx, cam.fy, reinterpret_cast<const float4 *>(pr.conic_o), pr.tiles_touched, grad2d,

@@ -28,29 +28,34 @@ struct FwdArgs {
   int32_t *n_contrib, *stats;
 };
 
+constexpr int kFPX = 2;  // pixels per thread in the forward
+using FG = Geo<kFPX>;
+
 template <bool kStats>
-__global__ void __launch_bounds__(kRThreadsTile) k_render_fwd(FwdArgs a) {
+__global__ void __launch_bounds__(FG::kThreads) k_render_fwd(FwdArgs a) {
   __shared__ float2 s_uv[kBatch];
   __shared__ float4 s_coef[kBatch];
   __shared__ float4 s_rgbz[kBatch];
-  __shared__ float4 s_box[kBatch];
+  __shared__ unsigned char s_mask[kBatch];
   const int tile = a.tile_order ? __ldg(a.tile_order + blockIdx.x) : int(blockIdx.x);
   const int tx = tile % a.TX, ty = tile / a.TX;
-  const PixGeom pg = pix_geom(tx, ty, a.H);
+  const PixGeom pg = pix_geom<kFPX>(tx, ty, a.H);
   const double ox = double(tx * kTile), oy = double(ty * kTile);
   const int2 range = a.tile_range[tile];
-  float T[kPxPerThread], c0[kPxPerThread], c1[kPxPerThread], c2[kPxPerThread], D[kPxPerThread], A[kPxPerThread];
-  int last[kPxPerThread], nscan[kPxPerThread], ncon[kPxPerThread];
-  bool live[kPxPerThread];
+  float T[kFPX], c0[kFPX], c1[kFPX], c2[kFPX], D[kFPX], A[kFPX];
+  int last[kFPX], ncon[kFPX], term[kFPX];
+  bool live[kFPX];
 #pragma unroll
-  for (int k = 0; k < kPxPerThread; ++k) {
+  for (int k = 0; k < kFPX; ++k) {
     T[k] = 1.f;
     c0[k] = c1[k] = c2[k] = D[k] = A[k] = 0.f;
-    last[k] = nscan[k] = ncon[k] = 0;
+    last[k] = ncon[k] = 0;
+    term[k] = range.y - range.x;  // entries scanned if the pixel never terminates
     live[k] = pg.row_in && pg.px0 + k < a.W;
   }
   for (int start = range.x; start < range.y; start += kBatch) {
     if (__syncthreads_count(live[0] || live[1]) == 0) break;
+    static_assert(FG::kRecPerThread == 1, "one staged record per thread");
     {
       const int k = start + threadIdx.x;
       if (k < range.y) {
@@ -61,51 +66,58 @@ __global__ void __launch_bounds__(kRThreadsTile) k_render_fwd(FwdArgs a) {
         s_uv[threadIdx.x] = make_float2(ul, vl);
         s_coef[threadIdx.x] = cf;
         s_rgbz[threadIdx.x] = __ldg(a.rgbz + g);
-        s_box[threadIdx.x] = entry_box(cf, ul, vl);
+        s_mask[threadIdx.x] = (unsigned char)box_strip_mask<kFPX>(entry_box(cf, ul, vl));
       }
     }
     __syncthreads();
-    const int cnt = min(kBatch, range.y - start);
-    for (int j = 0; j < cnt && (live[0] || live[1]); ++j) {
-      if (kStats) {
+    unsigned hits[kBatch / 32];
+    warp_hits(s_mask, min(kBatch, range.y - start), hits);
+    // walk this warp's hits in list order; entries that miss its strip cannot
+    // pass the exponent pre-test at any of its pixels (no decision changes)
 #pragma unroll
-        for (int k = 0; k < kPxPerThread; ++k) nscan[k] += live[k];
-      }
-      if (!box_hits_strip(s_box[j], pg.wy0)) continue;  // warp-uniform skip
-      const float2 ul = s_uv[j];
-      const RowTerms rt = row_terms(s_coef[j], ul.x, ul.y, pg.fpy);
-      float e[kPxPerThread];
-      bool pass[kPxPerThread];
+    for (int h = 0; h < kBatch / 32; ++h) {
+      unsigned bits = hits[h];
+      while (bits && (live[0] || live[1])) {
+        const int j = h * 32 + __ffs(bits) - 1;
+        bits &= bits - 1;
+        const float2 ul = s_uv[j];
+        const RowTerms rt = row_terms(s_coef[j], ul.x, ul.y, pg.fpy);
+        float e[kFPX];
+        bool pass[kFPX];
 #pragma unroll
-      for (int k = 0; k < kPxPerThread; ++k) {
-        e[k] = pixel_exponent(rt, pg.fpx0 + float(k));
-        pass[k] = live[k] && e[k] >= kExpSkip;
-      }
-      if (!(pass[0] || pass[1])) continue;
-      const float4 c = s_rgbz[j];
-      const int pos = start - range.x + j + 1;
+        for (int k = 0; k < kFPX; ++k) {
+          e[k] = pixel_exponent(rt, pg.fpx0 + float(k));
+          pass[k] = live[k] && e[k] >= kExpSkip;
+        }
+        if (!(pass[0] || pass[1])) continue;
+        const float4 c = s_rgbz[j];
+        const int pos = start - range.x + j + 1;
 #pragma unroll
-      for (int k = 0; k < kPxPerThread; ++k) {
-        if (!pass[k]) continue;
-        const float al = fminf(ex2_approx(e[k]), kAlphaMax);
-        if (al < kAlphaMin) continue;         // skip (R11)
-        const float w = __fmul_rn(al, T[k]);  // alpha_j T_j
-        c0[k] = __fmaf_rn(c.x, w, c0[k]);     // Eq. 3
-        c1[k] = __fmaf_rn(c.y, w, c1[k]);
-        c2[k] = __fmaf_rn(c.z, w, c2[k]);
-        D[k] = __fmaf_rn(c.w, w, D[k]);       // Eq. 6 (camera-frame z, R12)
-        A[k] = __fadd_rn(A[k], w);            // R14
-        T[k] = __fmul_rn(T[k], __fsub_rn(1.f, al));
-        last[k] = pos;
-        if (kStats) ++ncon[k];
-        live[k] = !(T[k] < kTEps);            // include, then stop (R11)
+        for (int k = 0; k < kFPX; ++k) {
+          if (!pass[k]) continue;
+          const float al = fminf(ex2_approx(e[k]), kAlphaMax);
+          if (al < kAlphaMin) continue;         // skip (R11)
+          const float w = __fmul_rn(al, T[k]);  // alpha_j T_j
+          c0[k] = __fmaf_rn(c.x, w, c0[k]);     // Eq. 3
+          c1[k] = __fmaf_rn(c.y, w, c1[k]);
+          c2[k] = __fmaf_rn(c.z, w, c2[k]);
+          D[k] = __fmaf_rn(c.w, w, D[k]);       // Eq. 6 (camera-frame z, R12)
+          A[k] = __fadd_rn(A[k], w);            // R14
+          T[k] = __fmul_rn(T[k], __fsub_rn(1.f, al));
+          last[k] = pos;
+          if (kStats) ++ncon[k];
+          if (T[k] < kTEps) {                   // include, then stop (R11)
+            live[k] = false;
+            term[k] = pos;
+          }
+        }
       }
     }
   }
   if (!pg.row_in) return;
   const size_t HW = size_t(a.W) * a.H;
 #pragma unroll
-  for (int k = 0; k < kPxPerThread; ++k) {
+  for (int k = 0; k < kFPX; ++k) {
     if (pg.px0 + k >= a.W) break;
     const size_t q = size_t(pg.py) * a.W + pg.px0 + k;
     a.color[q] = c0[k];
@@ -116,7 +128,7 @@ __global__ void __launch_bounds__(kRThreadsTile) k_render_fwd(FwdArgs a) {
     a.T_final[q] = T[k];
     a.n_contrib[q] = last[k];
     if (kStats) {
-      a.stats[q] = nscan[k];
+      a.stats[q] = term[k];  // entries scanned = termination position or list length
       a.stats[HW + q] = ncon[k];
     }
   }
@@ -142,8 +154,8 @@ extern "C" int gs_render_fwd(gs_proj pr, const int32_t *sorted_idx, const int32_
             tile_order, cam.width, cam.height, tiles_x(cam), color, depth, alpha, T_final, n_contrib, stats};
   const int T = tiles_x(cam) * tiles_y(cam);
   if (stats)
-    k_render_fwd<true><<<T, kRThreadsTile, 0, as_stream(stream)>>>(a);
+    k_render_fwd<true><<<T, FG::kThreads, 0, as_stream(stream)>>>(a);
   else
-    k_render_fwd<false><<<T, kRThreadsTile, 0, as_stream(stream)>>>(a);
+    k_render_fwd<false><<<T, FG::kThreads, 0, as_stream(stream)>>>(a);
   return check_launch("gs_render_fwd");
 }
