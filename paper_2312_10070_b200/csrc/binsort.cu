@@ -353,65 +353,47 @@ __global__ void k_chunk_starts(const uint32_t *__restrict__ poff, const uint32_t
   }
 }
 
-// Lane -> pair mapping of one 32-item group: lane l holds item k0+l with
-// `ntile` tiles and exclusive prefix `excl`; pair q of the group belongs to the
-// largest lane j with excl_j <= q (lanes with no tiles repeat the next prefix).
-__device__ __forceinline__ int pair_owner(uint32_t excl, uint32_t q) {
-  int lo = 0;
-#pragma unroll
-  for (int step = 16; step >= 1; step >>= 1) {
-    const int cand = lo + step;
-    const uint32_t e = __shfl_sync(0xffffffffu, excl, cand & 31);
-    if (cand < 32 && e <= q) lo = cand;
-  }
-  return lo;
-}
-
-// One warp walks the pairs of items [kbeg, kend) of the depth-sorted stream
-// 32 at a time, in stream order.  Equal tiles within a round are ranked by
-// lane with the ballot-sliced peer mask; wcnt is this warp's u16 tile counter
-// row.  SCATTER=false counts, SCATTER=true writes sorted_idx.
+// One warp walks items [kbeg, kend) of the depth-sorted stream in stream
+// order, ONE item per step: lane l takes the item's l-th tile (row-major in its
+// rect; items with more than 32 tiles take several steps).  The tiles of one
+// item are distinct, so no two lanes of a step touch the same counter and the
+// per-tile order is the stream order without any ranking.  Tile (row, col) of
+// lane l comes from one multiply-high by ceil(2^32 / width) (exact for
+// l, width < 2^16).  wcnt is this warp's u16 tile counter row.
+// SCATTER=false counts, SCATTER=true writes sorted_idx.
 template <bool SCATTER>
 __device__ __forceinline__ void bin_walk(const int32_t *__restrict__ sorted_vals, const short4 *__restrict__ rect,
-                                         int kbeg, int kend, int TX, int tbits, uint16_t *wcnt,
-                                         const uint32_t *base, int32_t *sorted_idx) {
+                                         int kbeg, int kend, int TX, uint16_t *wcnt, const uint32_t *base,
+                                         int32_t *sorted_idx) {
   const int lane = threadIdx.x & 31;
   for (int k0 = kbeg; k0 < kend; k0 += 32) {
+    // each lane preloads one item of the group
     const int k = k0 + lane;
-    int g = 0;
-    short4 r = make_short4(0, 0, -1, -1);
+    int g = 0, rxy = 0, wdt = 1, nt = 0;
+    uint32_t magic = 0;
     if (k < kend) {
       g = __ldg(sorted_vals + k);
-      r = __ldg(rect + g);
+      const short4 r = __ldg(rect + g);
+      wdt = r.z - r.x + 1;
+      nt = wdt * (r.w - r.y + 1);
+      rxy = (int(r.x) & 0xffff) | (int(r.y) << 16);
+      magic = wdt > 1 ? uint32_t((0x100000000ull + uint64_t(wdt) - 1) / uint64_t(wdt)) : 0u;
     }
-    const uint32_t nt = uint32_t(max(0, r.z - r.x + 1) * max(0, r.w - r.y + 1));
-    const uint32_t inc = warp_incl_scan(nt);
-    const uint32_t excl = inc - nt;
-    const uint32_t total = __shfl_sync(0xffffffffu, inc, 31);
-    const int rxy = (int(r.x) & 0xffff) | (int(r.y) << 16);
-    const int rzw = (int(r.z) & 0xffff) | (int(r.w) << 16);
-    for (uint32_t q0 = 0; q0 < total; q0 += 32) {
-      const uint32_t q = q0 + lane;
-      const int j = pair_owner(excl, q);
-      const uint32_t ej = __shfl_sync(0xffffffffu, excl, j);
-      const int jxy = __shfl_sync(0xffffffffu, rxy, j);
-      const int jzw = __shfl_sync(0xffffffffu, rzw, j);
-      const int jg = __shfl_sync(0xffffffffu, g, j);
-      const bool valid = q < total;
-      const unsigned act = __ballot_sync(0xffffffffu, valid);
-      const int x0 = int(short(jxy & 0xffff)), y0 = jxy >> 16;
-      const int x1 = int(short(jzw & 0xffff));
-      const int width = max(1, x1 - x0 + 1);
-      const int local = valid ? int(q - ej) : 0;
-      const int ty = y0 + local / width, tx = x0 + local % width;
-      const int t = valid ? ty * TX + tx : 0;
-      const unsigned peers = peer_mask_rt(act, uint32_t(t), tbits);
-      const bool leader = valid && lane == 31 - __clz(peers);
-      if (SCATTER) {
-        if (valid) sorted_idx[base[t] + wcnt[t] + __popc(peers & lanemask_lt())] = jg;
-        __syncwarp();
+    const int cnt = min(32, kend - k0);
+    for (int i = 0; i < cnt; ++i) {
+      const int ig = __shfl_sync(0xffffffffu, g, i);
+      const int ixy = __shfl_sync(0xffffffffu, rxy, i);
+      const int iw = __shfl_sync(0xffffffffu, wdt, i);
+      const int int_ = __shfl_sync(0xffffffffu, nt, i);
+      const uint32_t im = __shfl_sync(0xffffffffu, magic, i);
+      const int x0 = int(short(ixy & 0xffff)), y0 = ixy >> 16;
+      for (int l = lane; l < int_; l += 32) {
+        const int row = iw == 1 ? l : int(__umulhi(uint32_t(l), im));
+        const int t = (y0 + row) * TX + x0 + (l - row * iw);
+        const uint16_t c = wcnt[t];
+        if (SCATTER) sorted_idx[base[t] + c] = ig;
+        wcnt[t] = uint16_t(c + 1);
       }
-      if (leader) wcnt[t] = uint16_t(wcnt[t] + __popc(peers));
       __syncwarp();
     }
   }
@@ -432,7 +414,7 @@ __global__ void k_bin_count(const int32_t *__restrict__ sorted_vals, const uint3
   __syncthreads();
   int kbeg, kend;
   warp_chunk(cstart, W, kbeg, kend);
-  bin_walk<false>(sorted_vals, rect, kbeg, kend, TX, tbits, wc + size_t(w) * T, nullptr, nullptr);
+  bin_walk<false>(sorted_vals, rect, kbeg, kend, TX, wc + size_t(w) * T, nullptr, nullptr);
   __syncthreads();
   for (int t = threadIdx.x; t < T; t += blockDim.x) {
     uint32_t c = 0;
@@ -509,7 +491,7 @@ __global__ void k_bin_scatter(const int32_t *__restrict__ sorted_vals, const uin
   __syncthreads();
   int kbeg, kend;
   warp_chunk(cstart, W, kbeg, kend);
-  bin_walk<false>(sorted_vals, rect, kbeg, kend, TX, tbits, wc + size_t(w) * T, nullptr, nullptr);
+  bin_walk<false>(sorted_vals, rect, kbeg, kend, TX, wc + size_t(w) * T, nullptr, nullptr);
   __syncthreads();
   for (int t = threadIdx.x; t < T; t += blockDim.x) {
     base[t] = thist[size_t(t) * nblk + blockIdx.x];
@@ -521,7 +503,7 @@ __global__ void k_bin_scatter(const int32_t *__restrict__ sorted_vals, const uin
     }
   }
   __syncthreads();
-  bin_walk<true>(sorted_vals, rect, kbeg, kend, TX, tbits, wc + size_t(w) * T, base, sorted_idx);
+  bin_walk<true>(sorted_vals, rect, kbeg, kend, TX, wc + size_t(w) * T, base, sorted_idx);
 }
 
 }  // namespace gs

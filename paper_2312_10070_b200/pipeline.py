@@ -17,7 +17,7 @@ from __future__ import annotations
 
 import torch
 
-from .raster import GS_GRAD_PARAMS, GS_GRAD_POSE, Grads, Params, Rasterizer, lib
+from .raster import GS_BWD_GAUSS_ONLY, GS_BWD_PIXELS_ONLY, GS_GRAD_PARAMS, GS_GRAD_POSE, Grads, Params, Rasterizer, lib
 
 
 def shard_views(n_views, rank, world):
@@ -26,8 +26,17 @@ def shard_views(n_views, rank, world):
 
 
 class MapStep:
+    """One mapping iteration over this rank's views.
+
+    Views are pipelined over `lanes` CUDA streams, each with its own
+    Rasterizer buffers: the latency-bound sort / loss kernels of one view
+    overlap the compute-bound compositing kernels of another.  Only the
+    per-Gaussian phase of gs_render_bwd (a read-modify-write of the shared
+    gradient buffer) is serialised across views, by events, in view order.
+    """
+
     def __init__(self, params: Params, views, cam, tgt_color, tgt_depth, rank=0, world=1, group=None,
-                 lambda_color=1.0, lambda_depth=1.0, device="cuda"):
+                 lambda_color=1.0, lambda_depth=1.0, device="cuda", lanes=2):
         self.params = params
         self.views = views                  # [V, 12] device tensor (all views)
         self.V = views.shape[0]
@@ -38,36 +47,56 @@ class MapStep:
         self.group = group
         self.lc = lambda_color / self.V     # R20: mean over the V views of an iteration
         self.ld = lambda_depth / self.V
-        self.r = Rasterizer(params.n, cam, device=device)
+        nl = max(1, min(lanes, len(self.mine)))
+        self.lanes = [Rasterizer(params.n, cam, device=device) for _ in range(nl)]
+        self.streams = [torch.cuda.Stream(device=device) for _ in range(nl)]
+        self.r = self.lanes[0]
         self.grads = Grads.zeros(params.n, device)
         self.losses = torch.zeros(max(len(self.mine), 1), 3, dtype=torch.float32, device=device)
 
     def size(self, slack=1.25):
         """Setup only (host sync): pair capacity = slack x max pairs over my views."""
         best = 0
+        r = self.lanes[0]
         for v in self.mine:
-            self.r.project(self.params, self.views[v])
-            self.r.set_capacity(max(self.r.capacity, 1))
-            self.r.bin_sort()
+            r.project(self.params, self.views[v])
+            r.set_capacity(max(r.capacity, 1))
+            r.bin_sort()
             torch.cuda.synchronize()
-            best = max(best, int(self.r.n_pairs.item()))
-        self.r.set_capacity(int(best * slack) + 1024)
+            best = max(best, int(r.n_pairs.item()))
+        for r in self.lanes:
+            r.set_capacity(int(best * slack) + 1024)
         return best
 
-    def view_fwd_bwd(self, k, v):
-        r = self.r
+    def view_pixels(self, r, k, v):
+        """Everything of view v up to the per-pixel backward phase."""
         r.forward(self.params, self.views[v])
         r.compute_loss(self.tgt_color[v], self.tgt_depth[v], None, self.lc, self.ld)
         self.losses[k].copy_(r.loss)
-        r.backward(self.params, self.views[v], GS_GRAD_PARAMS, self.grads)
+        r.backward(self.params, self.views[v], GS_GRAD_PARAMS | GS_BWD_PIXELS_ONLY, self.grads)
 
-    def step(self, on_view=None):
+    def view_gauss(self, r, k, v):
+        r.backward(self.params, self.views[v], GS_GRAD_PARAMS | GS_BWD_GAUSS_ONLY, self.grads)
+
+    def step(self, hooks=None):
+        """hooks: optional (pixels_fn, gauss_fn) replacing view_pixels / view_gauss."""
+        pix, gau = hooks if hooks is not None else (self.view_pixels, self.view_gauss)
+        main = torch.cuda.current_stream()
         self.grads.zero_()
+        start = main.record_event()
+        for s in self.streams:
+            s.wait_event(start)
+        prev = start
         for k, v in enumerate(self.mine):
-            if on_view is None:
-                self.view_fwd_bwd(k, v)
-            else:
-                on_view(self, k, v)
+            lane = k % len(self.lanes)
+            s, r = self.streams[lane], self.lanes[lane]
+            with torch.cuda.stream(s):
+                pix(r, k, v)
+                s.wait_event(prev)
+                gau(r, k, v)
+                prev = s.record_event()
+        for s in self.streams:
+            main.wait_stream(s)
         if self.world > 1:
             torch.distributed.all_reduce(self.grads.buf, op=torch.distributed.ReduceOp.SUM, group=self.group)
         return self.grads
