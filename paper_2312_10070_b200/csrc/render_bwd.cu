@@ -279,37 +279,41 @@ __global__ void __launch_bounds__(256) k_bwd_gauss(GaussArgs a) {
     }
   }
   if (tt > 0) {
-    float R[9], t[3];
-#pragma unroll
-    for (int k = 0; k < 9; ++k) R[k] = __ldg(&a.view->R[k]);
-#pragma unroll
-    for (int k = 0; k < 3; ++k) t[k] = __ldg(&a.view->t[k]);
     const float4 z4 = make_float4(0.f, 0.f, 0.f, 0.f);
     g2[0] = z4;  // leave the scratch zeroed for the next call
     g2[1] = z4;
     if (kParams) g2[2] = z4;
-    const float gu = ga.x, gv = ga.y, gA = ga.z, gB = ga.w, gC = gb.x, gz = gb.y;
-    const float mu[3] = {mo.x, mo.y, mo.z};
-    float p[3];
+    // The chain of P:172 in fp64: it is ~600 flops per Gaussian in a kernel
+    // bound by HBM, and fp32 loses digits to cancellation (e.g. the
+    // log-scale term of small splats, the tangent projection of dL/dq).
+    double R[9], t[3];
+#pragma unroll
+    for (int k = 0; k < 9; ++k) R[k] = __ldg(&a.view->R[k]);
+#pragma unroll
+    for (int k = 0; k < 3; ++k) t[k] = __ldg(&a.view->t[k]);
+    const double gu = ga.x, gv = ga.y, gA = ga.z, gB = ga.w, gC = gb.x, gz = gb.y;
+    const double mu[3] = {mo.x, mo.y, mo.z};
+    double p[3];
 #pragma unroll
     for (int r = 0; r < 3; ++r) p[r] = R[3 * r] * mu[0] + R[3 * r + 1] * mu[1] + R[3 * r + 2] * mu[2] + t[r];
-    const float x = p[0], y = p[1], z = p[2];
+    const double x = p[0], y = p[1], z = p[2];
     // Sigma = M M^T, M = R_q S
-    const float qn = sqrtf(qf.x * qf.x + qf.y * qf.y + qf.z * qf.z + qf.w * qf.w);
-    const float iq = 1.f / qn;
-    const float qw = qf.x * iq, qx = qf.y * iq, qy = qf.z * iq, qz = qf.w * iq;
-    float Rq[9];
-    Rq[0] = 1.f - 2.f * (qy * qy + qz * qz);
-    Rq[1] = 2.f * (qx * qy - qw * qz);
-    Rq[2] = 2.f * (qx * qz + qw * qy);
-    Rq[3] = 2.f * (qx * qy + qw * qz);
-    Rq[4] = 1.f - 2.f * (qx * qx + qz * qz);
-    Rq[5] = 2.f * (qy * qz - qw * qx);
-    Rq[6] = 2.f * (qx * qz - qw * qy);
-    Rq[7] = 2.f * (qy * qz + qw * qx);
-    Rq[8] = 1.f - 2.f * (qx * qx + qy * qy);
-    const float s[3] = {expf(lf.x), expf(lf.y), expf(lf.z)};
-    float M[9], Sig[9], W[9], Sc[9];
+    const double q0 = qf.x, q1 = qf.y, q2 = qf.z, q3 = qf.w;
+    const double qn = sqrt(q0 * q0 + q1 * q1 + q2 * q2 + q3 * q3);
+    const double iq = 1.0 / qn;
+    const double qw = q0 * iq, qx = q1 * iq, qy = q2 * iq, qz = q3 * iq;
+    double Rq[9];
+    Rq[0] = 1.0 - 2.0 * (qy * qy + qz * qz);
+    Rq[1] = 2.0 * (qx * qy - qw * qz);
+    Rq[2] = 2.0 * (qx * qz + qw * qy);
+    Rq[3] = 2.0 * (qx * qy + qw * qz);
+    Rq[4] = 1.0 - 2.0 * (qx * qx + qz * qz);
+    Rq[5] = 2.0 * (qy * qz - qw * qx);
+    Rq[6] = 2.0 * (qx * qz - qw * qy);
+    Rq[7] = 2.0 * (qy * qz + qw * qx);
+    Rq[8] = 1.0 - 2.0 * (qx * qx + qy * qy);
+    const double s[3] = {exp(double(lf.x)), exp(double(lf.y)), exp(double(lf.z))};
+    double M[9], Sig[9], W[9], Sc[9];
 #pragma unroll
     for (int r = 0; r < 3; ++r)
 #pragma unroll
@@ -326,30 +330,30 @@ __global__ void __launch_bounds__(256) k_bwd_gauss(GaussArgs a) {
     for (int r = 0; r < 3; ++r)
 #pragma unroll
       for (int c = 0; c < 3; ++c) Sc[3 * r + c] = W[3 * r] * R[3 * c] + W[3 * r + 1] * R[3 * c + 1] + W[3 * r + 2] * R[3 * c + 2];
-    const float iz = 1.f / z, iz2 = iz * iz, iz3 = iz2 * iz;
-    const float J0 = a.fx * iz, J2 = -a.fx * x * iz2, J4 = a.fy * iz, J5 = -a.fy * y * iz2;
+    const double fx = a.fx, fy = a.fy;
+    const double iz = 1.0 / z, iz2 = iz * iz, iz3 = iz2 * iz;
+    const double J0 = fx * iz, J2 = -fx * x * iz2, J4 = fy * iz, J5 = -fy * y * iz2;
     // conic -> Sigma^I: G_S2 = -Conic G_M Conic, G_M = [[gA, gB/2], [gB/2, gC]]
-    const float A = cn.x, B = cn.y, C = cn.z;
-    const float hB = 0.5f * gB;
-    const float t00 = A * gA + B * hB, t01 = A * hB + B * gC, t10 = B * gA + C * hB, t11 = B * hB + C * gC;
-    const float S00 = -(t00 * A + t01 * B), S01 = -(t00 * B + t01 * C), S11 = -(t10 * B + t11 * C);
-    // Sigma^I = J Sigma_c J^T: G_Sc = J^T G_S2 J, G_J = 2 G_S2 J Sigma_c
-    // J = [[J0, 0, J2], [0, J4, J5]]
-    const float Jm[6] = {J0, 0.f, J2, 0.f, J4, J5};
-    const float GS2[4] = {S00, S01, S01, S11};
-    float GSc[9];
+    const double A = cn.x, B = cn.y, C = cn.z;
+    const double hB = 0.5 * gB;
+    const double t00 = A * gA + B * hB, t01 = A * hB + B * gC, t10 = B * gA + C * hB, t11 = B * hB + C * gC;
+    const double S00 = -(t00 * A + t01 * B), S01 = -(t00 * B + t01 * C), S11 = -(t10 * B + t11 * C);
+    // Sigma^I = J Sigma_c J^T: G_Sc = J^T G_S2 J, G_J = 2 G_S2 J Sigma_c, J = [[J0, 0, J2], [0, J4, J5]]
+    const double Jm[6] = {J0, 0.0, J2, 0.0, J4, J5};
+    const double GS2[4] = {S00, S01, S01, S11};
+    double GSc[9];
 #pragma unroll
     for (int r = 0; r < 3; ++r)
 #pragma unroll
       for (int c = 0; c < 3; ++c) {
-        float acc = 0.f;
+        double acc = 0.0;
 #pragma unroll
         for (int u = 0; u < 2; ++u)
 #pragma unroll
           for (int v = 0; v < 2; ++v) acc += Jm[3 * u + r] * GS2[2 * u + v] * Jm[3 * v + c];
         GSc[3 * r + c] = acc;
       }
-    float GJ0[6], GJ[6];
+    double GJ0[6], GJ[6];
 #pragma unroll
     for (int r = 0; r < 2; ++r)
 #pragma unroll
@@ -358,19 +362,19 @@ __global__ void __launch_bounds__(256) k_bwd_gauss(GaussArgs a) {
     for (int r = 0; r < 2; ++r)
 #pragma unroll
       for (int c = 0; c < 3; ++c)
-        GJ[3 * r + c] = 2.f * (GJ0[3 * r] * Sc[c] + GJ0[3 * r + 1] * Sc[3 + c] + GJ0[3 * r + 2] * Sc[6 + c]);
+        GJ[3 * r + c] = 2.0 * (GJ0[3 * r] * Sc[c] + GJ0[3 * r + 1] * Sc[3 + c] + GJ0[3 * r + 2] * Sc[6 + c]);
     // camera-frame mean p: through (u, v) (Eq. 1), J(p) and the depth term (Eq. 6)
-    float gp[3];
-    gp[0] = gu * a.fx * iz - GJ[2] * a.fx * iz2;
-    gp[1] = gv * a.fy * iz - GJ[5] * a.fy * iz2;
-    gp[2] = -gu * a.fx * x * iz2 - gv * a.fy * y * iz2 + gz - GJ[0] * a.fx * iz2 + GJ[2] * 2.f * a.fx * x * iz3 -
-            GJ[4] * a.fy * iz2 + GJ[5] * 2.f * a.fy * y * iz3;
+    double gp[3];
+    gp[0] = gu * fx * iz - GJ[2] * fx * iz2;
+    gp[1] = gv * fy * iz - GJ[5] * fy * iz2;
+    gp[2] = -gu * fx * x * iz2 - gv * fy * y * iz2 + gz - GJ[0] * fx * iz2 + GJ[2] * 2.0 * fx * x * iz3 -
+            GJ[4] * fy * iz2 + GJ[5] * 2.0 * fy * y * iz3;
     if (kParams) {
-      float gmu[3];
+      double gmu[3];
 #pragma unroll
       for (int c = 0; c < 3; ++c) gmu[c] = R[c] * gp[0] + R[3 + c] * gp[1] + R[6 + c] * gp[2];
       // G_Sigma = R^T G_Sc R; G_M = 2 G_Sigma M
-      float tmp[9], GSig[9], GM3[9];
+      double tmp[9], GSig[9], GM3[9];
 #pragma unroll
       for (int r = 0; r < 3; ++r)
 #pragma unroll
@@ -383,8 +387,8 @@ __global__ void __launch_bounds__(256) k_bwd_gauss(GaussArgs a) {
       for (int r = 0; r < 3; ++r)
 #pragma unroll
         for (int c = 0; c < 3; ++c)
-          GM3[3 * r + c] = 2.f * (GSig[3 * r] * M[c] + GSig[3 * r + 1] * M[3 + c] + GSig[3 * r + 2] * M[6 + c]);
-      float gls[3], GRq[9];
+          GM3[3 * r + c] = 2.0 * (GSig[3 * r] * M[c] + GSig[3 * r + 1] * M[3 + c] + GSig[3 * r + 2] * M[6 + c]);
+      double gls[3], GRq[9];
 #pragma unroll
       for (int k = 0; k < 3; ++k) {
         gls[k] = s[k] * (GM3[k] * Rq[k] + GM3[3 + k] * Rq[3 + k] + GM3[6 + k] * Rq[6 + k]);
@@ -392,24 +396,25 @@ __global__ void __launch_bounds__(256) k_bwd_gauss(GaussArgs a) {
         for (int r = 0; r < 3; ++r) GRq[3 * r + k] = GM3[3 * r + k] * s[k];
       }
       // dR(q^)/dq^ contracted with G_Rq
-      const float gw = 2.f * (-qz * GRq[1] + qy * GRq[2] + qz * GRq[3] - qx * GRq[5] - qy * GRq[6] + qx * GRq[7]);
-      const float gx = 2.f * (qy * GRq[1] + qz * GRq[2] + qy * GRq[3] - 2.f * qx * GRq[4] - qw * GRq[5] + qz * GRq[6] +
-                              qw * GRq[7] - 2.f * qx * GRq[8]);
-      const float gy = 2.f * (-2.f * qy * GRq[0] + qx * GRq[1] + qw * GRq[2] + qx * GRq[3] + qz * GRq[5] - qw * GRq[6] +
-                              qz * GRq[7] - 2.f * qy * GRq[8]);
-      const float gzq = 2.f * (-2.f * qz * GRq[0] - qw * GRq[1] + qx * GRq[2] + qw * GRq[3] - 2.f * qz * GRq[4] +
-                               qy * GRq[5] + qx * GRq[6] + qy * GRq[7]);
-      const float dot = gw * qw + gx * qx + gy * qy + gzq * qz;
+      const double gw = 2.0 * (-qz * GRq[1] + qy * GRq[2] + qz * GRq[3] - qx * GRq[5] - qy * GRq[6] + qx * GRq[7]);
+      const double gx = 2.0 * (qy * GRq[1] + qz * GRq[2] + qy * GRq[3] - 2.0 * qx * GRq[4] - qw * GRq[5] + qz * GRq[6] +
+                               qw * GRq[7] - 2.0 * qx * GRq[8]);
+      const double gy = 2.0 * (-2.0 * qy * GRq[0] + qx * GRq[1] + qw * GRq[2] + qx * GRq[3] + qz * GRq[5] - qw * GRq[6] +
+                               qz * GRq[7] - 2.0 * qy * GRq[8]);
+      const double gzq = 2.0 * (-2.0 * qz * GRq[0] - qw * GRq[1] + qx * GRq[2] + qw * GRq[3] - 2.0 * qz * GRq[4] +
+                                qy * GRq[5] + qx * GRq[6] + qy * GRq[7]);
+      const double dot = gw * qw + gx * qx + gy * qy + gzq * qz;
       // q^ = q / |q| (R18)
-      const float4 gq = make_float4((gw - qw * dot) * iq, (gx - qx * dot) * iq, (gy - qy * dot) * iq, (gzq - qz * dot) * iq);
-      a.g_mean_opa[i] = make_float4(old_m.x + gmu[0], old_m.y + gmu[1], old_m.z + gmu[2], old_m.w + gb.z);
-      a.g_quat[i] = make_float4(old_q.x + gq.x, old_q.y + gq.y, old_q.z + gq.z, old_q.w + gq.w);
-      a.g_logscale[i] = make_float4(old_l.x + gls[0], old_l.y + gls[1], old_l.z + gls[2], old_l.w);
+      a.g_mean_opa[i] = make_float4(float(old_m.x + gmu[0]), float(old_m.y + gmu[1]), float(old_m.z + gmu[2]),
+                                    old_m.w + gb.z);
+      a.g_quat[i] = make_float4(float(old_q.x + (gw - qw * dot) * iq), float(old_q.y + (gx - qx * dot) * iq),
+                                float(old_q.z + (gy - qy * dot) * iq), float(old_q.w + (gzq - qz * dot) * iq));
+      a.g_logscale[i] = make_float4(float(old_l.x + gls[0]), float(old_l.y + gls[1]), float(old_l.z + gls[2]), old_l.w);
       a.g_rgb[i] = make_float4(old_c.x + gc.x, old_c.y + gc.y, old_c.z + gc.z, old_c.w);
     }
     if (kPose) {
       // dL/dt = dL/dp; dL/dR = dL/dp mu^T + 2 G_Sc R Sigma
-      float RS[9];
+      double RS[9];
 #pragma unroll
       for (int r = 0; r < 3; ++r)
 #pragma unroll
@@ -419,9 +424,9 @@ __global__ void __launch_bounds__(256) k_bwd_gauss(GaussArgs a) {
 #pragma unroll
         for (int c = 0; c < 3; ++c)
           pose[3 * r + c] =
-              gp[r] * mu[c] + 2.f * (GSc[3 * r] * RS[c] + GSc[3 * r + 1] * RS[3 + c] + GSc[3 * r + 2] * RS[6 + c]);
+              float(gp[r] * mu[c] + 2.0 * (GSc[3 * r] * RS[c] + GSc[3 * r + 1] * RS[3 + c] + GSc[3 * r + 2] * RS[6 + c]));
 #pragma unroll
-      for (int k = 0; k < 3; ++k) pose[9 + k] = gp[k];
+      for (int k = 0; k < 3; ++k) pose[9 + k] = float(gp[k]);
     }
   }
   if (kPose) {

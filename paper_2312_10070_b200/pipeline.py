@@ -36,7 +36,7 @@ class MapStep:
     """
 
     def __init__(self, params: Params, views, cam, tgt_color, tgt_depth, rank=0, world=1, group=None,
-                 lambda_color=1.0, lambda_depth=1.0, device="cuda", lanes=2):
+                 lambda_color=1.0, lambda_depth=1.0, device="cuda", lanes=2, allreduce=None):
         self.params = params
         self.views = views                  # [V, 12] device tensor (all views)
         self.V = views.shape[0]
@@ -45,6 +45,10 @@ class MapStep:
         self.tgt_depth = tgt_depth
         self.world = world
         self.group = group
+        # SUM across ranks (S8); default: NCCL through torch.distributed when world > 1
+        self.allreduce = allreduce if allreduce is not None else (
+            (lambda buf: torch.distributed.all_reduce(buf, op=torch.distributed.ReduceOp.SUM, group=group))
+            if world > 1 else None)
         self.lc = lambda_color / self.V     # R20: mean over the V views of an iteration
         self.ld = lambda_depth / self.V
         nl = max(1, min(lanes, len(self.mine)))
@@ -97,8 +101,8 @@ class MapStep:
                 prev = s.record_event()
         for s in self.streams:
             main.wait_stream(s)
-        if self.world > 1:
-            torch.distributed.all_reduce(self.grads.buf, op=torch.distributed.ReduceOp.SUM, group=self.group)
+        if self.allreduce is not None:
+            self.allreduce(self.grads.buf)
         return self.grads
 
     def launches_per_step(self):
