@@ -19,6 +19,7 @@ namespace gs {
 
 // grad2d record [n][12]: (u, v, A, B), (C, p_z, logit, 0), (r, g, b, 0)
 constexpr int kG2 = 12;
+constexpr int kGaussThreads = 128;  // k_bwd_gauss block (one pose-partial record per block)
 
 struct BwdArgs {
   const double2 *uv;
@@ -84,7 +85,7 @@ using BG = Geo<kBPX>;
 
 // acc layout: 0 u, 1 v, 2 2*A-term, 3 B, 4 2*C-term, 5 p_z, 6 logit, 7 r, 8 g, 9 b
 // (the 1/2 of dsigma/dA and dsigma/dC is applied once, by the writing lane)
-template <bool kParams>
+template <bool kParams, bool kAlphaUp>
 __global__ void __launch_bounds__(BG::kThreads) k_bwd_pixels(BwdArgs a) {
   __shared__ int s_idx[kBatch];
   __shared__ float2 s_uv[kBatch];
@@ -118,7 +119,7 @@ __global__ void __launch_bounds__(BG::kThreads) k_bwd_pixels(BwdArgs a) {
       G1[k] = a.dL_dcolor[HW + q];
       G2[k] = a.dL_dcolor[2 * HW + q];
       GD[k] = a.dL_ddepth[q];
-      GA[k] = a.dL_dalpha ? a.dL_dalpha[q] : 0.f;
+      if (kAlphaUp) GA[k] = a.dL_dalpha[q];
       tmax = max(tmax, last[k]);
     }
   }
@@ -155,7 +156,9 @@ __global__ void __launch_bounds__(BG::kThreads) k_bwd_pixels(BwdArgs a) {
     unsigned hits[kBatch / 32];
     warp_hits(s_mask, min(end, wmax) - beg, hits);
     // back to front over this warp's hits (entries missing its strip cannot
-    // pass the exponent pre-test at any of its pixels)
+    // pass the exponent pre-test at any of its pixels).  Branch-free per
+    // pixel: a pixel that did not composite the entry uses alpha = 0, which
+    // leaves T and Q unchanged and contributes exact zeros.
 #pragma unroll
     for (int h = kBatch / 32 - 1; h >= 0; --h) {
       unsigned bits = hits[h];
@@ -175,46 +178,43 @@ __global__ void __launch_bounds__(BG::kThreads) k_bwd_pixels(BwdArgs a) {
           pass[k] = pos < last[k] && e[k] >= kExpSkip;
           anyp |= pass[k];
         }
+        if (!__any_sync(0xffffffffu, anyp)) continue;
+        const float4 c = s_rgbz[j];
+        const float4 cn = s_conic[j];
+        const float dy = ul.y - pg.fpy;  // Delta = mu^I - pixel
+        const float om = 1.f - cn.w;
         float acc[10];
 #pragma unroll
         for (int m = 0; m < 10; ++m) acc[m] = 0.f;
         bool any = false;
-        if (anyp) {
-          const float4 c = s_rgbz[j];
-          const float4 cn = s_conic[j];
-          const float dy = ul.y - pg.fpy;  // Delta = mu^I - pixel
 #pragma unroll
-          for (int k = 0; k < kBPX; ++k) {
-            if (!pass[k]) continue;
-            const float at = ex2_approx(e[k]);
-            const float al = fminf(at, kAlphaMax);
-            if (al < kAlphaMin) continue;  // same decision as the forward (H5)
-            any = true;
-            T[k] = __fdividef(T[k], 1.f - al);  // T_j = T_{j+1} / (1 - alpha_j) (R16)
-            const float w = al * T[k];
-            // Eq. 8 chained with Eq. 7 through the suffix scalar Q
-            const float gx = fmaf(G0[k], c.x, fmaf(G1[k], c.y, fmaf(G2[k], c.z, fmaf(GD[k], c.w, GA[k]))));
-            const float d = gx - Q[k];
-            const float galpha = T[k] * d;
-            Q[k] = fmaf(al, d, Q[k]);
-            acc[5] = fmaf(w, GD[k], acc[5]);  // dD/dz_j = alpha_j T_j
-            if (kParams) {
-              acc[7] = fmaf(w, G0[k], acc[7]);  // dC/dc_j = alpha_j T_j
-              acc[8] = fmaf(w, G1[k], acc[8]);
-              acc[9] = fmaf(w, G2[k], acc[9]);
-            }
-            if (at < kAlphaMax) {  // a clamped alpha has no gradient (R17)
-              if (kParams) acc[6] = fmaf(galpha * al, 1.f - cn.w, acc[6]);  // d alpha/d logit = alpha (1 - o)
-              const float gs = -al * galpha;                               // d alpha/d sigma = -alpha
-              const float dx = ul.x - (pg.fpx0 + float(k));
-              const float gsx = gs * dx, gsy = gs * dy;
-              acc[0] = fmaf(cn.x, gsx, fmaf(cn.y, gsy, acc[0]));
-              acc[1] = fmaf(cn.y, gsx, fmaf(cn.z, gsy, acc[1]));
-              acc[2] = fmaf(gsx, dx, acc[2]);
-              acc[3] = fmaf(gsx, dy, acc[3]);
-              acc[4] = fmaf(gsy, dy, acc[4]);
-            }
+        for (int k = 0; k < kBPX; ++k) {
+          const float at = ex2_approx(e[k]);
+          float al = fminf(at, kAlphaMax);
+          al = (pass[k] && al >= kAlphaMin) ? al : 0.f;  // same decision as the forward (H5)
+          any |= al > 0.f;
+          T[k] = __fdividef(T[k], 1.f - al);  // T_j = T_{j+1} / (1 - alpha_j) (R16)
+          const float w = al * T[k];
+          // Eq. 8 chained with Eq. 7 through the suffix scalar Q
+          const float gx = fmaf(G0[k], c.x, fmaf(G1[k], c.y, fmaf(G2[k], c.z, fmaf(GD[k], c.w, GA[k]))));
+          const float d = gx - Q[k];
+          const float galpha = T[k] * d;
+          Q[k] = fmaf(al, d, Q[k]);
+          acc[5] = fmaf(w, GD[k], acc[5]);  // dD/dz_j = alpha_j T_j
+          if (kParams) {
+            acc[7] = fmaf(w, G0[k], acc[7]);  // dC/dc_j = alpha_j T_j
+            acc[8] = fmaf(w, G1[k], acc[8]);
+            acc[9] = fmaf(w, G2[k], acc[9]);
           }
+          const float ga = (at < kAlphaMax ? al : 0.f) * galpha;  // clamped alpha: no gradient (R17)
+          if (kParams) acc[6] = fmaf(ga, om, acc[6]);             // d alpha/d logit = alpha (1 - o)
+          const float dx = ul.x - (pg.fpx0 + float(k));
+          const float gsx = -ga * dx, gsy = -ga * dy;             // d alpha/d sigma = -alpha
+          acc[0] = fmaf(cn.x, gsx, fmaf(cn.y, gsy, acc[0]));
+          acc[1] = fmaf(cn.y, gsx, fmaf(cn.z, gsy, acc[1]));
+          acc[2] = fmaf(gsx, dx, acc[2]);
+          acc[3] = fmaf(gsx, dy, acc[3]);
+          acc[4] = fmaf(gsy, dy, acc[4]);
         }
         const unsigned ball = __ballot_sync(0xffffffffu, any);
         if (!ball) continue;
@@ -252,7 +252,7 @@ struct GaussArgs {
 };
 
 template <bool kParams, bool kPose>
-__global__ void __launch_bounds__(256) k_bwd_gauss(GaussArgs a) {
+__global__ void __launch_bounds__(kGaussThreads, 4) k_bwd_gauss(GaussArgs a) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   float pose[12];
 #pragma unroll
@@ -431,7 +431,7 @@ __global__ void __launch_bounds__(256) k_bwd_gauss(GaussArgs a) {
   }
   if (kPose) {
     // fixed-order block reduction: warp shuffles, then warp partials summed by thread order
-    __shared__ float sh[8][12];
+    __shared__ float sh[kGaussThreads / 32][12];
 #pragma unroll
     for (int k = 0; k < 12; ++k) {
       float v = pose[k];
@@ -457,7 +457,7 @@ extern "C" size_t gs_bwd_workspace_bytes(int32_t n) {
 
 extern "C" int32_t gs_pose_partials_count(int32_t n) {
   if (n < 0) return 0;
-  return n > 0 ? (n + 255) / 256 : 1;
+  return n > 0 ? (n + gs::kGaussThreads - 1) / gs::kGaussThreads : 1;
 }
 
 extern "C" int gs_render_bwd(gs_params p, const gs_view *view, gs_camera cam, gs_proj pr, const int32_t *sorted_idx,
@@ -509,9 +509,11 @@ extern "C" int gs_render_bwd(gs_params p, const gs_view *view, gs_camera cam, gs
   const int T = tiles_x(cam) * tiles_y(cam);
   if (run_pixels) {
     if (want_params)
-      k_bwd_pixels<true><<<T, BG::kThreads, 0, s>>>(b);
+      dL_dalpha ? k_bwd_pixels<true, true><<<T, BG::kThreads, 0, s>>>(b)
+                : k_bwd_pixels<true, false><<<T, BG::kThreads, 0, s>>>(b);
     else
-      k_bwd_pixels<false><<<T, BG::kThreads, 0, s>>>(b);
+      dL_dalpha ? k_bwd_pixels<false, true><<<T, BG::kThreads, 0, s>>>(b)
+                : k_bwd_pixels<false, false><<<T, BG::kThreads, 0, s>>>(b);
   }
   if (!run_gauss) return check_launch("gs_render_bwd");
   GaussArgs g{p, view, cam.fx, cam.fy, reinterpret_cast<const float4 *>(pr.conic_o), pr.tiles_touched, grad2d,
@@ -519,10 +521,10 @@ extern "C" int gs_render_bwd(gs_params p, const gs_view *view, gs_camera cam, gs
               reinterpret_cast<float4 *>(g_logscale), reinterpret_cast<float4 *>(g_rgb), pose_partials};
   const int blocks = gs_pose_partials_count(p.n);
   if (want_params && want_pose)
-    k_bwd_gauss<true, true><<<blocks, 256, 0, s>>>(g);
+    k_bwd_gauss<true, true><<<blocks, kGaussThreads, 0, s>>>(g);
   else if (want_params)
-    k_bwd_gauss<true, false><<<blocks, 256, 0, s>>>(g);
+    k_bwd_gauss<true, false><<<blocks, kGaussThreads, 0, s>>>(g);
   else
-    k_bwd_gauss<false, true><<<blocks, 256, 0, s>>>(g);
+    k_bwd_gauss<false, true><<<blocks, kGaussThreads, 0, s>>>(g);
   return check_launch("gs_render_bwd");
 }

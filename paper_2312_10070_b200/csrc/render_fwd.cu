@@ -43,18 +43,21 @@ __global__ void __launch_bounds__(FG::kThreads) k_render_fwd(FwdArgs a) {
   const double ox = double(tx * kTile), oy = double(ty * kTile);
   const int2 range = a.tile_range[tile];
   float T[kFPX], c0[kFPX], c1[kFPX], c2[kFPX], D[kFPX], A[kFPX];
+  // thr[k]: exponent threshold of the pre-test while pixel k composites,
+  // +inf once it has terminated (or lies outside the image)
+  float thr[kFPX];
   int last[kFPX], ncon[kFPX], term[kFPX];
-  bool live[kFPX];
+  const float kInf = __int_as_float(0x7f800000);
 #pragma unroll
   for (int k = 0; k < kFPX; ++k) {
     T[k] = 1.f;
     c0[k] = c1[k] = c2[k] = D[k] = A[k] = 0.f;
     last[k] = ncon[k] = 0;
     term[k] = range.y - range.x;  // entries scanned if the pixel never terminates
-    live[k] = pg.row_in && pg.px0 + k < a.W;
+    thr[k] = (pg.row_in && pg.px0 + k < a.W) ? kExpSkip : kInf;
   }
   for (int start = range.x; start < range.y; start += kBatch) {
-    if (__syncthreads_count(live[0] || live[1]) == 0) break;
+    if (__syncthreads_count(thr[0] < kInf || thr[1] < kInf) == 0) break;
     static_assert(FG::kRecPerThread == 1, "one staged record per thread");
     {
       const int k = start + threadIdx.x;
@@ -73,11 +76,14 @@ __global__ void __launch_bounds__(FG::kThreads) k_render_fwd(FwdArgs a) {
     unsigned hits[kBatch / 32];
     warp_hits(s_mask, min(kBatch, range.y - start), hits);
     // walk this warp's hits in list order; entries that miss its strip cannot
-    // pass the exponent pre-test at any of its pixels (no decision changes)
+    // pass the exponent pre-test at any of its pixels (no decision changes).
+    // The blend is branch-free: a pixel that does not composite uses alpha = 0,
+    // which leaves C, D, A and T bit-identical.
 #pragma unroll
     for (int h = 0; h < kBatch / 32; ++h) {
       unsigned bits = hits[h];
-      while (bits && (live[0] || live[1])) {
+      if (bits && !__any_sync(0xffffffffu, thr[0] < kInf || thr[1] < kInf)) break;
+      while (bits) {
         const int j = h * 32 + __ffs(bits) - 1;
         bits &= bits - 1;
         const float2 ul = s_uv[j];
@@ -87,29 +93,28 @@ __global__ void __launch_bounds__(FG::kThreads) k_render_fwd(FwdArgs a) {
 #pragma unroll
         for (int k = 0; k < kFPX; ++k) {
           e[k] = pixel_exponent(rt, pg.fpx0 + float(k));
-          pass[k] = live[k] && e[k] >= kExpSkip;
+          pass[k] = e[k] >= thr[k];
         }
-        if (!(pass[0] || pass[1])) continue;
+        if (!__any_sync(0xffffffffu, pass[0] || pass[1])) continue;
         const float4 c = s_rgbz[j];
         const int pos = start - range.x + j + 1;
 #pragma unroll
         for (int k = 0; k < kFPX; ++k) {
-          if (!pass[k]) continue;
-          const float al = fminf(ex2_approx(e[k]), kAlphaMax);
-          if (al < kAlphaMin) continue;         // skip (R11)
-          const float w = __fmul_rn(al, T[k]);  // alpha_j T_j
-          c0[k] = __fmaf_rn(c.x, w, c0[k]);     // Eq. 3
+          float al = fminf(ex2_approx(e[k]), kAlphaMax);
+          al = (pass[k] && al >= kAlphaMin) ? al : 0.f;  // skip (R11)
+          const float w = __fmul_rn(al, T[k]);           // alpha_j T_j
+          c0[k] = __fmaf_rn(c.x, w, c0[k]);              // Eq. 3
           c1[k] = __fmaf_rn(c.y, w, c1[k]);
           c2[k] = __fmaf_rn(c.z, w, c2[k]);
-          D[k] = __fmaf_rn(c.w, w, D[k]);       // Eq. 6 (camera-frame z, R12)
-          A[k] = __fadd_rn(A[k], w);            // R14
+          D[k] = __fmaf_rn(c.w, w, D[k]);                // Eq. 6 (camera-frame z, R12)
+          A[k] = __fadd_rn(A[k], w);                     // R14
           T[k] = __fmul_rn(T[k], __fsub_rn(1.f, al));
-          last[k] = pos;
-          if (kStats) ++ncon[k];
-          if (T[k] < kTEps) {                   // include, then stop (R11)
-            live[k] = false;
-            term[k] = pos;
-          }
+          const bool comp = al > 0.f;
+          last[k] = comp ? pos : last[k];
+          if (kStats) ncon[k] += comp;
+          const bool stop = comp && T[k] < kTEps;        // include, then stop (R11)
+          term[k] = stop ? pos : term[k];
+          thr[k] = stop ? kInf : thr[k];
         }
       }
     }
