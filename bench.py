@@ -48,6 +48,7 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--profile", action="store_true", help="short run for ncu (no clocks/cpu/e2e/tracking)")
     ap.add_argument("--cpu-tiles", type=int, default=192, help="tiles of the oracle sample")
+    ap.add_argument("--lanes", type=int, default=4, help="CUDA streams the views are pipelined over")
     return ap.parse_args()
 
 
@@ -178,7 +179,7 @@ def bench_ours(a):
     sm_count = raster.device_check(local)
     s, P, views, tc, td = make_workload(a.config, device, rank, world)
     V = views.shape[0]
-    ms = MapStep(P, views, s.cam, tc, td, rank, world, group, device=device)
+    ms = MapStep(P, views, s.cam, tc, td, rank, world, group, device=device, lanes=a.lanes)
     ms.size()
     # per-view work counts for the roofline (untimed)
     stats_views = []

@@ -141,8 +141,10 @@ int gs_check_device(int device, int *sm_count);
 /* Number of tiles of a camera: ceil(W/16)*ceil(H/16); 0 on invalid camera. */
 int32_t gs_num_tiles(gs_camera cam);
 
-/* Workspace bytes gs_bin_sort needs for n Gaussians on camera `cam`. */
-size_t gs_binsort_workspace_bytes(int32_t n, gs_camera cam);
+/* Workspace bytes gs_bin_sort needs for n Gaussians, a pair capacity and
+ * camera `cam` (0 if unsupported: > 4 radix passes of depth bits, > 2^21 tiles,
+ * or n / capacity >= 2^30). */
+size_t gs_binsort_workspace_bytes(int32_t n, int64_t capacity, gs_camera cam);
 
 /* Workspace bytes gs_loss needs for camera `cam`. */
 size_t gs_loss_workspace_bytes(gs_camera cam);
@@ -185,7 +187,7 @@ int gs_project(gs_params p, const gs_view *view, gs_camera cam, gs_proj out,
  * Emits one (tile, Gaussian) pair per tile of each visible Gaussian's rect and
  * orders all pairs by the key (tile asc, fp32 depth asc, Gaussian id asc).
  *   pr.depth, pr.rect, pr.tiles_touched (device) inputs from gs_project
- *   ws/ws_bytes   (device) workspace >= gs_binsort_workspace_bytes(n, cam)
+ *   ws/ws_bytes   (device) workspace >= gs_binsort_workspace_bytes(n, capacity, cam)
  *   capacity      length of sorted_idx
  *   sorted_idx    (device) [capacity] Gaussian ids, tile-major
  *   tile_range    (device) [T][2] int32 [start, end) into sorted_idx

@@ -56,7 +56,7 @@ _PROTOS = {
     "gs_last_error": (C.c_char_p, []),
     "gs_check_device": (C.c_int, [C.c_int, C.POINTER(C.c_int)]),
     "gs_num_tiles": (_I32, [GsCamera]),
-    "gs_binsort_workspace_bytes": (_SZ, [_I32, GsCamera]),
+    "gs_binsort_workspace_bytes": (_SZ, [_I32, _I64, GsCamera]),
     "gs_loss_workspace_bytes": (_SZ, [GsCamera]),
     "gs_bwd_workspace_bytes": (_SZ, [_I32]),
     "gs_pose_partials_count": (_I32, [_I32]),

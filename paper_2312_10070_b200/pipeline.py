@@ -36,7 +36,7 @@ class MapStep:
     """
 
     def __init__(self, params: Params, views, cam, tgt_color, tgt_depth, rank=0, world=1, group=None,
-                 lambda_color=1.0, lambda_depth=1.0, device="cuda", lanes=2, allreduce=None):
+                 lambda_color=1.0, lambda_depth=1.0, device="cuda", lanes=4, allreduce=None):
         self.params = params
         self.views = views                  # [V, 12] device tensor (all views)
         self.V = views.shape[0]
@@ -111,17 +111,24 @@ class MapStep:
 
 
 def sort_passes(cam):
+    """Depth radix passes of gs_bin_sort (9-bit digits over bits(z) - bits(z_near))."""
     import numpy as np
     zb = int(np.float32(cam.z_near).view(np.uint32))
     ze = int(np.float32(cam.z_far).view(np.uint32))
-    bits = max(1, (ze - zb).bit_length())
+    bits = max(1, (ze - zb + 1).bit_length())
     return (bits + 8) // 9
 
 
+def tile_passes(cam):
+    T = ((cam.width + 15) // 16) * ((cam.height + 15) // 16)
+    return (max(1, (T - 1).bit_length()) + 6) // 7
+
+
 def kernels_per_view(cam, loss=True, bwd=True):
-    # project 1; bin_sort: 5 per radix pass (upsweep, 3-kernel scan, downsweep)
-    # + count, 3-kernel scan, finish, scatter; render 1; loss 3; bwd 2
-    n = 1 + 5 * sort_passes(cam) + 6 + 1
+    """Kernels of ours per view (the sort's memset is a copy-engine node, not a kernel):
+    project 1; bin_sort: prep, tile counts, depth passes, scan, emit, tile passes,
+    gather; render 1; loss 3; backward 2."""
+    n = 1 + (2 + sort_passes(cam) + 2 + tile_passes(cam) + 1) + 1
     if loss:
         n += 3
     if bwd:

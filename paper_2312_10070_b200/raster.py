@@ -206,10 +206,7 @@ class Rasterizer:
             raise GsError("invalid camera")
         H, W = cam.height, cam.width
         self.proj = Proj(n, device)
-        ws = L.gs_binsort_workspace_bytes(n, self.cam)
-        if ws == 0:
-            raise GsError("gs_binsort_workspace_bytes: problem not supported")
-        self.sort_ws = torch.empty((ws + 15) // 16 * 4, dtype=torch.float32, device=device)
+        self.sort_ws = torch.empty(4, dtype=torch.float32, device=device)  # sized by set_capacity
         self.tile_range = torch.empty(self.T, 2, dtype=torch.int32, device=device)
         self.tile_order = torch.empty(self.T, dtype=torch.int32, device=device)
         self.n_pairs = torch.zeros(1, dtype=torch.int64, device=device)
@@ -226,8 +223,7 @@ class Rasterizer:
         self.pose_partials = torch.zeros(self.n_partials, 12, dtype=torch.float32, device=device)
         self.capacity = 0
         self.sorted_idx = torch.empty(1, dtype=torch.int32, device=device)
-        if capacity is not None:
-            self.set_capacity(capacity)
+        self.set_capacity(1 if capacity is None else capacity)
 
     @property
     def grad2d(self):
@@ -237,8 +233,13 @@ class Rasterizer:
         return self.bwd_ws[: self.n * 12].view(self.n, 12)
 
     def set_capacity(self, capacity):
+        """Pair capacity of the binning (sorted_idx and the sort workspace)."""
         capacity = int(max(capacity, 1))
         if capacity > self.capacity:
+            ws = lib().gs_binsort_workspace_bytes(self.n, capacity, self.cam)
+            if ws == 0:
+                raise GsError("gs_binsort_workspace_bytes: problem not supported")
+            self.sort_ws = torch.empty((ws + 15) // 16 * 4, dtype=torch.float32, device=self.device)
             self.sorted_idx = torch.empty(capacity, dtype=torch.int32, device=self.device)
             self.capacity = capacity
 
