@@ -181,11 +181,12 @@ __global__ void __launch_bounds__(BG::kThreads) k_bwd_pixels(BwdArgs a) {
         if (!__any_sync(0xffffffffu, anyp)) continue;
         const float4 c = s_rgbz[j];
         const float4 cn = s_conic[j];
-        const float dy = ul.y - pg.fpy;  // Delta = mu^I - pixel
-        const float om = 1.f - cn.w;
-        float acc[10];
-#pragma unroll
-        for (int m = 0; m < 10; ++m) acc[m] = 0.f;
+        const float dy = ul.y - pg.fpy;  // Delta = mu^I - pixel; one row: dy is shared
+        const float dx0 = ul.x - pg.fpx0;
+        // per-thread sums over its pixels of ga = alpha dL/dalpha (0 if clamped) and
+        // ga dx, ga dx^2; dsigma/d(u, v, A, B, C) and dalpha/dlogit are formed once
+        // per (thread, entry) from them, the conic, dy and o (entry constants)
+        float sga = 0.f, sgx = 0.f, sgxx = 0.f, sz = 0.f, sr = 0.f, sg = 0.f, sb = 0.f;
         bool any = false;
 #pragma unroll
         for (int k = 0; k < kBPX; ++k) {
@@ -200,22 +201,32 @@ __global__ void __launch_bounds__(BG::kThreads) k_bwd_pixels(BwdArgs a) {
           const float d = gx - Q[k];
           const float galpha = T[k] * d;
           Q[k] = fmaf(al, d, Q[k]);
-          acc[5] = fmaf(w, GD[k], acc[5]);  // dD/dz_j = alpha_j T_j
+          sz = fmaf(w, GD[k], sz);  // dD/dz_j = alpha_j T_j
           if (kParams) {
-            acc[7] = fmaf(w, G0[k], acc[7]);  // dC/dc_j = alpha_j T_j
-            acc[8] = fmaf(w, G1[k], acc[8]);
-            acc[9] = fmaf(w, G2[k], acc[9]);
+            sr = fmaf(w, G0[k], sr);  // dC/dc_j = alpha_j T_j
+            sg = fmaf(w, G1[k], sg);
+            sb = fmaf(w, G2[k], sb);
           }
           const float ga = (at < kAlphaMax ? al : 0.f) * galpha;  // clamped alpha: no gradient (R17)
-          if (kParams) acc[6] = fmaf(ga, om, acc[6]);             // d alpha/d logit = alpha (1 - o)
-          const float dx = ul.x - (pg.fpx0 + float(k));
-          const float gsx = -ga * dx, gsy = -ga * dy;             // d alpha/d sigma = -alpha
-          acc[0] = fmaf(cn.x, gsx, fmaf(cn.y, gsy, acc[0]));
-          acc[1] = fmaf(cn.y, gsx, fmaf(cn.z, gsy, acc[1]));
-          acc[2] = fmaf(gsx, dx, acc[2]);
-          acc[3] = fmaf(gsx, dy, acc[3]);
-          acc[4] = fmaf(gsy, dy, acc[4]);
+          const float dx = dx0 - float(k);
+          const float t = ga * dx;
+          sga += ga;
+          sgx += t;
+          sgxx = fmaf(t, dx, sgxx);
         }
+        // dalpha/dsigma = -alpha, dsigma/du = A dx + B dy, dsigma/dv = B dx + C dy,
+        // dsigma/d(A, B, C) = (dx^2/2, dx dy, dy^2/2), dalpha/dlogit = alpha (1 - o)
+        float acc[10];
+        acc[0] = -fmaf(cn.x, sgx, cn.y * dy * sga);
+        acc[1] = -fmaf(cn.y, sgx, cn.z * dy * sga);
+        acc[2] = -sgxx;  // x2 (the writer applies 1/2)
+        acc[3] = -dy * sgx;
+        acc[4] = -dy * dy * sga;  // x2
+        acc[5] = sz;
+        acc[6] = kParams ? (1.f - cn.w) * sga : 0.f;
+        acc[7] = sr;
+        acc[8] = sg;
+        acc[9] = sb;
         const unsigned ball = __ballot_sync(0xffffffffu, any);
         if (!ball) continue;
         float *dst = a.grad2d + size_t(s_idx[j]) * kG2;
