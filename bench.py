@@ -47,7 +47,6 @@ def parse():
     ap.add_argument("--no-tracking", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--profile", action="store_true", help="short run for ncu (no clocks/cpu/e2e/tracking)")
-    ap.add_argument("--cpu-tiles", type=int, default=192, help="tiles of the oracle sample")
     ap.add_argument("--lanes", type=int, default=4, help="CUDA streams the views are pipelined over")
     return ap.parse_args()
 
@@ -75,7 +74,7 @@ class Clocks:
     def __enter__(self):
         try:
             self.p = subprocess.Popen(["nvidia-smi", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
-                                       "-lms", "200", "-i", str(self.index)], stdout=self.f,
+                                       "-lms", "100", "-i", str(self.index)], stdout=self.f,
                                       stderr=subprocess.DEVNULL)
         except Exception:
             self.p = None
@@ -153,10 +152,15 @@ def roofline_for(step, stats_views, peaks, sm_mhz, fwd_ms, bwd_ms):
     mhz = sm_mhz or peaks.get("sm_max_mhz", 1965.0)
     peak = 148 * 128 * 2 * mhz * 1e6 / 1e12
     out = {}
+    traffic = None
+    tp = os.path.join(ROOT, "profiles", "traffic.json")
+    if os.path.exists(tp):  # dram bytes of the dominant kernel from the committed ncu --set full capture
+        traffic = json.load(open(tp)).get("dram_bytes_per_launch")
     for name, fl, ms in (("render_bwd_pixels", bwd_flops, bwd_ms), ("render_fwd", fwd_flops, fwd_ms)):
         ach = fl / (ms * 1e-3) / 1e12 if ms else None
         out[name] = {"bound": "alu", "achieved": ach, "peak": peak, "unit": "TFLOP/s",
-                     "frac": ach / peak if ach else None, "traffic": None, "flops_per_launch": fl,
+                     "frac": ach / peak if ach else None,
+                     "traffic": traffic if name == "render_bwd_pixels" else None, "flops_per_launch": fl,
                      "ms_per_launch": ms}
     return out
 
@@ -250,6 +254,26 @@ def bench_ours(a):
     peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))) if os.path.exists(
         os.path.join(ROOT, "MEASURED_PEAKS.json")) else {}
     roof = roofline_for(ms, stats_views, peaks, clocks.get("sm_mhz"), fwd_ms, bwd_ms)
+    # the same kernels timed alone (one view at a time, no other stream active)
+    iso_f, iso_b = [], []
+    r0 = ms.lanes[0]
+    for v in ms.mine:
+        for _ in range(3):
+            r0.forward(P, views[v])
+            e0, e1, e2, e3 = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
+            r0.project(P, views[v])
+            r0.bin_sort()
+            e0.record()
+            r0.render()
+            e1.record()
+            r0.compute_loss(tc[v], td[v], None, ms.lc, ms.ld)
+            r0.backward(P, views[v], raster.GS_GRAD_PARAMS | raster.GS_BWD_PIXELS_ONLY, ms.grads, event_pair=(e2, e3))
+            r0.backward(P, views[v], raster.GS_GRAD_PARAMS | raster.GS_BWD_GAUSS_ONLY, ms.grads)
+            torch.cuda.synchronize()
+            iso_f.append(e0.elapsed_time(e1))
+            iso_b.append(e2.elapsed_time(e3))
+    roof_iso = roofline_for(ms, stats_views, peaks, clocks.get("sm_mhz"), statistics.median(iso_f),
+                            statistics.median(iso_b))
     launches = (ms.launches_per_step() + 0) * a.steps
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": a.steps, "warmup": max(a.warmup, 3),
@@ -264,7 +288,11 @@ def bench_ours(a):
                    "scanned_per_px": sum(x["scanned"] for x in stats_views) / (len(stats_views) * W * H),
                    "contrib_per_px": sum(x["contrib"] for x in stats_views) / (len(stats_views) * W * H)},
         "roofline": roof["render_bwd_pixels"],
-        "roofline_other": {"render_fwd": roof["render_fwd"]},
+        "roofline_other": {"render_fwd": roof["render_fwd"],
+                           "note": "in-step event times include sharing the GPU with the other pipeline lanes; "
+                                   "*_isolated = the same launch timed alone (median of 3 x views)",
+                           "render_bwd_pixels_isolated": roof_iso["render_bwd_pixels"],
+                           "render_fwd_isolated": roof_iso["render_fwd"]},
         "clocks": clocks, "gpu_launches": launches, "sm_count": sm_count,
     }
     if rank == 0 and not a.profile and not a.no_e2e:
@@ -364,46 +392,35 @@ def bench_tracking(device):
             "final_err": {"rot_deg": float(rot_err), "trans_cm": float(np.linalg.norm(t) * 100)}}
 
 
-def cpu_baseline(a, s, budget_s=30.0):
-    """The fp64 oracle as it stands, on this host's cores, on a bounded sample of
-    one view: full projection + binning, compositing + backward on a random
-    subset of tiles, the per-Gaussian chain in full; per-view time
-    extrapolated to all tiles."""
+def cpu_baseline(a, s, max_views=None):
+    """The fp64 oracle as it stands, on this host's cores: the full mapping step
+    (projection, binning, compositing, L1 loss and backward of every pixel) of
+    the first `max_views` views of the workload (all of them by default)."""
     import oracle
     t0 = time.perf_counter()
-    rng = np.random.default_rng(0)
     p64 = oracle.params64(*s.params())
-    view = s.views[0].astype(np.float64)
     cam = s.cam
-    T = cam.tiles
-    tiles = rng.choice(T, size=min(a.cpu_tiles, T), replace=False)
-    mask = np.zeros(T, np.uint8)
-    mask[tiles] = 1
-    ta = time.perf_counter()
-    pr = oracle.project(p64, view, cam)
-    idx, trg = oracle.bin_sort(pr["rect"], pr["culled"], pr["depth_key"], cam)
-    tb = time.perf_counter()
-    fr = oracle.render(pr, p64["rgb"], idx, trg, cam, tile_mask=mask)
-    tc_ = time.perf_counter()
-    gc, gd, ga = [np.zeros_like(x) for x in (fr["color"], fr["depth"], fr["alpha"])]
-    tgt_c = np.zeros_like(fr["color"])
-    tgt_d = np.ones_like(fr["depth"])
-    _, gc, gd = oracle.loss(cam, fr["color"], fr["depth"], tgt_c, tgt_d)
-    td0 = time.perf_counter()
-    oracle.backward(p64, view, cam, idx, trg, gc, gd, None, tile_mask=mask)
-    te = time.perf_counter()
-    oracle.backward(p64, view, cam, idx, trg, gc, gd, None, tile_mask=np.zeros(T, np.uint8))
-    tf = time.perf_counter()
-    t_ps = tb - ta
-    t_px = (tc_ - tb) + max((te - td0) - (tf - te), 0.0)
-    t_fixed = (tf - te) + (td0 - tc_)
-    per_view = t_ps + t_fixed + t_px * T / len(tiles)
-    mp = cam.width * cam.height / 1e6
-    return {"value": mp / per_view, "unit": UNIT, "cores": oracle.num_threads(), "kind": "oracle",
-            "sample": f"1 of {s.views.shape[0]} views: projection + binning of all {s.n} Gaussians, compositing + "
-                      f"backward on {len(tiles)} of {T} random tiles (per-pixel time extrapolated to all tiles), "
-                      f"per-Gaussian chain in full; {time.perf_counter() - t0:.1f} s of CPU work",
-            "s_per_view_extrapolated": per_view}
+    V = s.views.shape[0] if max_views is None else min(max_views, s.views.shape[0])
+    tp = oracle.params64(*s.extra["target_params"]) if "target_params" in s.extra else None
+    tsum = 0.0
+    for v in range(V):
+        view = s.views[v].astype(np.float64)
+        if tp is not None:  # targets (not timed): the oracle's own render of the perturbed copy
+            tgt = oracle.forward(tp, view, cam)
+            tc_, td_ = tgt["color"], tgt["depth"]
+        else:
+            tc_, td_ = s.extra["tgt_color"][v], s.extra["tgt_depth"][v]
+        ta = time.perf_counter()
+        fr = oracle.forward(p64, view, cam)
+        _, gc, gd = oracle.loss(cam, fr["color"], fr["depth"], tc_, td_, None, 1.0 / V, 1.0 / V)
+        oracle.backward(p64, view, cam, fr["sorted_idx"], fr["tile_range"], gc, gd)
+        tsum += time.perf_counter() - ta
+    mp = V * cam.width * cam.height / 1e6
+    return {"value": mp / tsum, "unit": UNIT, "cores": oracle.num_threads(), "kind": "oracle",
+            "sample": f"{V} of {s.views.shape[0]} views of BJ.configs[{a.config}], every pixel (projection, binning, "
+                      f"compositing, L1 loss, backward incl. gradient magnitude scales); {tsum:.1f} s timed, "
+                      f"{time.perf_counter() - t0:.1f} s with target renders",
+            "s_per_view": tsum / V}
 
 
 def bench_reference(a):
@@ -415,15 +432,14 @@ def bench_reference(a):
     from paper_2312_10070_b200 import inputs
     s = {1: inputs.config1, 3: inputs.config3, 4: inputs.config4}[a.config]()
     oracle.build()
-    warm = max(a.warmup, 0)
-    a.cpu_tiles = min(a.cpu_tiles, 48)
+    # each "step" is a bounded sample: one view of the workload (warm-up steps are not timed)
     vals = []
-    for i in range(warm + a.steps):
-        r = cpu_baseline(a, s)
-        if i >= warm:
+    for i in range(min(a.warmup, 1) + a.steps):
+        r = cpu_baseline(a, s, max_views=1)
+        if i >= min(a.warmup, 1):
             vals.append(r)
     v = statistics.median(x["value"] for x in vals)
-    per_view = statistics.median(x["s_per_view_extrapolated"] for x in vals)
+    per_view = statistics.median(x["s_per_view"] for x in vals)
     V = s.views.shape[0]
     line = {"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": a.gpus, "steps": a.steps,
             "warmup": warm, "ms_per_step": per_view * V * 1e3, "higher_is_better": True, "scaling": "strong",
