@@ -43,7 +43,6 @@ extern "C" {
 #define GS_ALPHA_MAX 0.999f          /* alpha clamp (R11)                   */
 #define GS_ALPHA_MIN (1.0f / 255.0f) /* skip alpha < 1/255 (R11)            */
 #define GS_T_EPS 1e-4f               /* stop after T < 1e-4 (R11)           */
-#define GS_RADIUS_SIGMAS 3           /* radius = ceil(3 sqrt(lambda_max))  */
 
 /* Status codes. */
 #define GS_OK 0
@@ -167,9 +166,11 @@ int32_t gs_pose_partials_count(int32_t n);
  * p = R mu + t; culled iff not z_near <= p_z <= z_far; u = fx p_x/p_z + cx,
  * v = fy p_y/p_z + cy; Sigma^I = J R Sigma R^T J^T + 0.3 I with the unclamped
  * perspective Jacobian J (R6); conic = (Sigma^I)^-1 (culled if det <= 0);
- * r = ceil(3 sqrt(lambda_max)); tile rect clamped to the image (culled if
- * empty); o = sigmoid(logit).  The decision path (p, u, v, Sigma^I,
- * lambda_max, r, rect) is evaluated in IEEE fp64 in the operation order of
+ * o = sigmoid(logit); tile rect = tiles meeting the box of the region where
+ * alpha~ = o exp(-sigma) >= 1/255 (half-widths sqrt(2 tau a), sqrt(2 tau c),
+ * tau = ln(o / (1/255)), R8'), clamped to the image (culled if empty or
+ * tau <= 0).  The decision path (p, u, v, Sigma^I, tau, rect) is evaluated in
+ * IEEE fp64 in the operation order of
  * DESIGN.md §3 R1 without FMA contraction, so tile and sort indices are
  * reproducible bit-for-bit.
  *   p      (device) parameters, n >= 0

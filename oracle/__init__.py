@@ -101,13 +101,13 @@ def project(p64, view, cam):
     n = p64["mean"].shape[0]
     R, t = _view(view)
     out = dict(uv=np.zeros((n, 2)), conic=np.zeros((n, 3)), opac=np.zeros(n), pz=np.zeros(n),
-               depth_key=np.zeros(n, np.float32), radius=np.zeros(n, np.int32),
+               depth_key=np.zeros(n, np.float32), hxy=np.zeros((n, 2)),
                rect=np.zeros((n, 4), np.int32), culled=np.zeros(n, np.int32),
                cov2d=np.zeros((n, 3)))
     lib().or_project(C.c_int(n), _ptr(p64["mean"]), _ptr(p64["quat"]), _ptr(p64["logscale"]),
                      _ptr(p64["logit"]), _ptr(R), _ptr(t), _ptr(_cam(cam)),
                      _ptr(out["uv"]), _ptr(out["conic"]), _ptr(out["opac"]), _ptr(out["pz"]),
-                     _ptr(out["depth_key"]), _ptr(out["radius"]), _ptr(out["rect"]),
+                     _ptr(out["depth_key"]), _ptr(out["hxy"]), _ptr(out["rect"]),
                      _ptr(out["culled"]), _ptr(out["cov2d"]))
     return out
 

@@ -110,8 +110,8 @@ typedef struct {
   double Sc[9];  /* R Sigma R^T */
   double a, b, c; /* Sigma^I + 0.3 I = [[a, b], [b, c]] */
   double det, A, B, C; /* conic = inverse */
-  double u, v, lmax;
-  int radius;
+  double u, v;
+  double hx, hy; /* half-widths of the alpha >= 1/255 box (R8') */
   int rect[4];
   double o;
 } ogauss;
@@ -187,16 +187,20 @@ static void project_one(const double *mu, const double *qin, const double *ls, d
   g->A = g->c / g->det;
   g->B = -g->b / g->det;
   g->C = g->a / g->det;
-  /* largest eigenvalue and 3-sigma radius (R8) */
-  double mid = 0.5 * (g->a + g->c);
-  double hd = 0.5 * (g->a - g->c);
-  double disc = hd * hd + g->b * g->b;
-  g->lmax = mid + sqrt(disc > 0.0 ? disc : 0.0);
-  g->radius = (int)ceil(3.0 * sqrt(g->lmax));
-  /* tile rect (R9) */
-  double r = (double)g->radius;
-  int x0 = (int)floor((g->u - r) / OR_TILE), x1 = (int)floor((g->u + r) / OR_TILE);
-  int y0 = (int)floor((g->v - r) / OR_TILE), y1 = (int)floor((g->v + r) / OR_TILE);
+  /* tile membership (R8'): the tiles meeting the axis-aligned box of the region
+   * where alpha~ = o exp(-sigma) >= 1/255, i.e. sigma <= tau = ln(o / alpha_min):
+   * the ellipse Delta^T (Sigma^I)^-1 Delta <= 2 tau, whose half-widths are
+   * sqrt(2 tau a) and sqrt(2 tau c).  A Gaussian whose alpha~ never reaches
+   * 1/255 (tau <= 0) touches no tile. */
+  double tau = log(g->o / OR_ALPHA_MIN);
+  if (!(tau > 0.0)) {
+    g->culled = 3;
+    return;
+  }
+  g->hx = sqrt((2.0 * tau) * g->a);
+  g->hy = sqrt((2.0 * tau) * g->c);
+  int x0 = (int)floor((g->u - g->hx) / OR_TILE), x1 = (int)floor((g->u + g->hx) / OR_TILE);
+  int y0 = (int)floor((g->v - g->hy) / OR_TILE), y1 = (int)floor((g->v + g->hy) / OR_TILE);
   if (x0 < 0) x0 = 0;
   if (y0 < 0) y0 = 0;
   if (x1 > k->TX - 1) x1 = k->TX - 1;
@@ -214,11 +218,12 @@ static void project_one(const double *mu, const double *qin, const double *ls, d
 /* Public projection.  Arrays: mean[n][3], quat[n][4], logscale[n][3],
  * logit[n], R[9], t[3], cam[8].  Outputs (nullable each): uv[n][2],
  * conic[n][3] (A, B, C), opac[n], pz[n], depth_key[n] (fp32 RN(p_z), +inf if
- * culled), radius[n], rect[n][4], culled[n], cov2d[n][3] (a, b, c). */
+ * culled), hxy[n][2] (half-widths of the alpha >= 1/255 box), rect[n][4],
+ * culled[n], cov2d[n][3] (a, b, c). */
 void or_project(int n, const double *mean, const double *quat, const double *logscale,
                 const double *logit, const double *R, const double *t, const double *cam,
                 double *uv, double *conic, double *opac, double *pz, float *depth_key,
-                int *radius, int *rect, int *culled, double *cov2d) {
+                double *hxy, int *rect, int *culled, double *cov2d) {
   ocam k = mkcam(cam);
 #pragma omp parallel for schedule(static)
   for (int i = 0; i < n; ++i) {
@@ -229,7 +234,7 @@ void or_project(int n, const double *mean, const double *quat, const double *log
     if (opac) opac[i] = g.o;
     if (pz) pz[i] = g.p[2];
     if (depth_key) depth_key[i] = g.culled ? INFINITY : (float)g.p[2];
-    if (radius) radius[i] = g.culled ? 0 : g.radius;
+    if (hxy) { hxy[2 * i] = g.culled ? 0.0 : g.hx; hxy[2 * i + 1] = g.culled ? 0.0 : g.hy; }
     if (rect) for (int j = 0; j < 4; ++j) rect[4 * i + j] = g.rect[j];
     if (culled) culled[i] = g.culled;
     if (cov2d) { cov2d[3 * i] = g.a; cov2d[3 * i + 1] = g.b; cov2d[3 * i + 2] = g.c; }

@@ -1,7 +1,7 @@
 // project.cu — S1 gs_project: EWA projection (Eqs. 1-2).
 //
 // One thread per Gaussian, coalesced float4 SoA loads.  The decision path
-// (p, u, v, Sigma^I, lambda_max, radius, rect, depth key) is evaluated in IEEE
+// (p, u, v, Sigma^I, alpha >= 1/255 box, rect, depth key) is evaluated in IEEE
 // fp64 in the operation order documented in DESIGN.md §3 R1.  This file is
 // compiled with --fmad=false so no multiply-add is contracted: with correctly
 // rounded +,-,*,/,sqrt the tile rects and sort keys are reproducible
@@ -100,20 +100,21 @@ __global__ void __launch_bounds__(256) k_project(gs_params p, const gs_view *__r
         nonfinite = true;  // singular Sigma^I
       } else {
         const double A = c / det, B = -b / det, C = a / det;
-        // lambda_max, 3-sigma radius (R8)
-        const double mid = 0.5 * (a + c), hd = 0.5 * (a - c);
-        const double disc = hd * hd + b * b;
-        const double lmax = mid + sqrt(disc > 0.0 ? disc : 0.0);
-        const double r = ceil(3.0 * sqrt(lmax));
-        int x0 = (int)floor((u - r) / kTile), x1 = (int)floor((u + r) / kTile);
-        int y0 = (int)floor((v - r) / kTile), y1 = (int)floor((v + r) / kTile);
-        x0 = max(x0, 0);
-        y0 = max(y0, 0);
-        x1 = min(x1, TX - 1);
-        y1 = min(y1, TY - 1);
+        // tile membership (R8'): tiles meeting the box of the region where
+        // o exp(-sigma) >= 1/255, sigma <= tau = ln(o / alpha_min): half-widths
+        // sqrt(2 tau a), sqrt(2 tau c); no tile when tau <= 0
+        const double o = 1.0 / (1.0 + exp(-(double)mo.w));  // sigmoid (R18)
+        const double tau = log(o / (double)GS_ALPHA_MIN);
+        int x0 = 0, x1 = -1, y0 = 0, y1 = -1;
+        if (tau > 0.0) {
+          const double hx = sqrt((2.0 * tau) * a), hy = sqrt((2.0 * tau) * c);
+          x0 = max((int)floor((u - hx) / kTile), 0);
+          x1 = min((int)floor((u + hx) / kTile), TX - 1);
+          y0 = max((int)floor((v - hy) / kTile), 0);
+          y1 = min((int)floor((v + hy) / kTile), TY - 1);
+        }
         if (x0 <= x1 && y0 <= y1) {
           culled = false;
-          const double o = 1.0 / (1.0 + exp(-(double)mo.w));  // sigmoid (R18)
           const float4 cf = __ldg(reinterpret_cast<const float4 *>(p.rgb) + i);
           reinterpret_cast<double2 *>(out.uv)[i] = make_double2(u, v);
           reinterpret_cast<float4 *>(out.conic_o)[i] = make_float4((float)A, (float)B, (float)C, (float)o);

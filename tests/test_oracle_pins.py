@@ -104,7 +104,8 @@ def _pinhole(p, cam):
 def test_projection_matches_numeric_jacobian(orc):
     """Eq. 2: Sigma^I - 0.3 I = J R Sigma R^T J^T with J the Jacobian of the
     pinhole map (central differences here, not the oracle's closed form), and
-    conic = inverse(Sigma^I), lambda_max = eigvalsh, r = ceil(3 sqrt(lambda_max))."""
+    conic = inverse(Sigma^I), and the alpha >= 1/255 box half-widths against the
+    extreme points of the ellipse sampled on its boundary (R8')."""
     rng = np.random.default_rng(2)
     cam = _cam(320, 240, 300.0)
     n = 40
@@ -133,13 +134,17 @@ def test_projection_matches_numeric_jacobian(orc):
         if pr["culled"][i] == 0:
             Ci = np.linalg.inv(np.array([[a, b], [b, c]]))
             assert np.allclose(pr["conic"][i], [Ci[0, 0], Ci[0, 1], Ci[1, 1]], rtol=1e-12)
-            lm = np.linalg.eigvalsh(np.array([[a, b], [b, c]]))[-1]
-            assert pr["radius"][i] == int(np.ceil(3 * np.sqrt(lm)))
+            # boundary of {Delta : Delta^T conic Delta = 2 tau}, tau = ln(o / alpha_min)
+            tau = np.log(pr["opac"][i] / np.float64(np.float32(1 / 255)))
+            L = np.linalg.cholesky(np.array([[a, b], [b, c]]))
+            th = np.linspace(0, 2 * np.pi, 20001)
+            pts = np.sqrt(2 * tau) * (L @ np.stack([np.cos(th), np.sin(th)]))
+            assert np.allclose(pr["hxy"][i], np.abs(pts).max(1), rtol=1e-6)
 
 
 def test_rect_brute_force(orc):
-    """R9: the rect is exactly the set of tiles whose pixel square meets the
-    axis-aligned square [u-r, u+r] x [v-r, v+r] (brute force over all tiles)."""
+    """R8'/R9: the rect is exactly the set of tiles whose pixel square meets the
+    box [u-hx, u+hx] x [v-hy, v+hy] (brute force over all tiles)."""
     s = inputs.random_scene(7, 300, 100, 70, spread=1.6, ls=(-2.0, 0.6))
     p = s.params64()
     pr = orc.project(p, s.views[0], s.cam)
@@ -148,15 +153,33 @@ def test_rect_brute_force(orc):
         if pr["culled"][i] in (1, 2):
             continue
         u, v = pr["uv"][i]
-        r = pr["radius"][i]
+        hx, hy = pr["hxy"][i]
         hit = [(tx, ty) for ty in range(TY) for tx in range(TX)
-               if 16 * tx <= u + r and u - r < 16 * (tx + 1) and 16 * ty <= v + r and v - r < 16 * (ty + 1)]
+               if 16 * tx <= u + hx and u - hx < 16 * (tx + 1) and 16 * ty <= v + hy and v - hy < 16 * (ty + 1)]
         if pr["culled"][i] == 3:
-            assert hit == []
+            assert hit == [] or hx == 0.0
             continue
         x0, y0, x1, y1 = pr["rect"][i]
         exp = [(tx, ty) for ty in range(y0, y1 + 1) for tx in range(x0, x1 + 1)]
         assert sorted(hit) == sorted(exp)
+
+
+def test_rect_covers_every_pixel_with_alpha_over_threshold(orc):
+    """Eq. 4 + R8': wherever alpha~ = o exp(-sigma) >= 1/255, the pixel's tile is
+    in the Gaussian's rect (brute force over every pixel; opaque Gaussians reach
+    ~3.33 sigma, beyond a 3-sigma square)."""
+    s = inputs.random_scene(8, 120, 96, 80, spread=1.2, ls=(-2.2, 0.6), lo=(2.0, 2.0))
+    p = s.params64()
+    pr = orc.project(p, s.views[0], s.cam)
+    ys, xs = np.mgrid[0:80, 0:96]
+    amin = np.float64(np.float32(1 / 255))
+    for i in np.nonzero(pr["culled"] == 0)[0]:
+        A, B, C = pr["conic"][i]
+        dx, dy = pr["uv"][i, 0] - xs, pr["uv"][i, 1] - ys
+        al = pr["opac"][i] * np.exp(-0.5 * (A * dx * dx + 2 * B * dx * dy + C * dy * dy))
+        tx, ty = xs[al >= amin] // 16, ys[al >= amin] // 16
+        x0, y0, x1, y1 = pr["rect"][i]
+        assert ((tx >= x0) & (tx <= x1) & (ty >= y0) & (ty <= y1)).all()
 
 
 # --------------------------------------------------------------------------
@@ -250,19 +273,28 @@ def test_render_eq4_unit_conic(orc):
 
 def test_render_stop_and_skip_rules(orc):
     """R11: alpha < 1/255 is skipped; compositing stops after the entry that
-    leaves T < 1e-4 (include, then stop)."""
+    leaves T < 1e-4 (include, then stop).  R8': a Gaussian whose alpha never
+    reaches 1/255 (o < 1/255) is in no tile list."""
     cam = _cam(32, 32, 30.0)
     ms, lss = [], []
-    for z in (1.0, 1.5, 2.0, 2.5):
-        m, ls = _iso_at_pixel(cam, 8, 8, z, 2.0)
+    for z, (i, j) in zip((1.0, 1.5, 2.0, 2.5), ((15, 8), (8, 8), (8, 8), (8, 8))):
+        m, ls = _iso_at_pixel(cam, i, j, z, 2.0)
         ms.append(m)
         lss.append(ls)
+    m, ls = _iso_at_pixel(cam, 8, 8, 0.5, 2.0)  # o = 1/300 < 1/255: culled
+    ms.append(m)
+    lss.append(ls)
     o_hi = 0.99995
     lo = np.log(o_hi / (1 - o_hi))
     faint = 1.0 / 300.0
-    p = _params(ms, lss, [np.log(faint / (1 - faint)), lo, lo, lo], [[1, 0, 0], [0, 1, 0], [0, 0, 1], [1, 1, 1]])
+    p = _params(ms, lss, [0.0, lo, lo, lo, np.log(faint / (1 - faint))],
+                [[1, 0, 0], [0, 1, 0], [0, 0, 1], [1, 1, 1], [1, 1, 1]])
     fr = orc.forward(p, IDV, cam)
-    # entry 0 (faint) is skipped, entries 1 and 2 composite (T = 1e-6 < 1e-4), entry 3 is not reached
+    assert fr["proj"]["culled"][4] == 3
+    # entry 0 (o = 0.5, 7 px away: alpha = 0.5 e^-5.7 < 1/255 but its box meets the
+    # tile) is scanned and skipped; entries 1 and 2 composite (T = 1e-6 < 1e-4);
+    # entry 3 is not reached
+    assert fr["tile_range"][0, 1] - fr["tile_range"][0, 0] == 4
     assert fr["contrib"][8, 8] == 2 and fr["n_contrib"][8, 8] == 3 and fr["scanned"][8, 8] == 3
     a = np.float64(np.float32(0.999))
     assert np.isclose(fr["T_final"][8, 8], (1 - a) ** 2, rtol=1e-12)
