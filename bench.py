@@ -206,12 +206,14 @@ def bench_ours(a):
         r.bin_sort()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record(st)
-        r.render()
+        raster.gs_render_fwd(r.proj, r.sorted_idx, r.tile_range, r.cam, r.frame, False, tile_order=r.tile_order,
+                             tile_work=r.tile_work)
         e1.record(st)
         ev_fwd.append((e0, e1))
         r.compute_loss(m.tgt_color[v], m.tgt_depth[v], None, m.lc, m.ld)
         m.losses[k].copy_(r.loss)
         b0, b1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        raster.gs_tile_order(r.tile_work, r.T, r.bwd_order)
         r.backward(m.params, m.views[v], raster.GS_GRAD_PARAMS | raster.GS_BWD_PIXELS_ONLY, m.grads,
                    event_pair=(b0, b1))
         ev_bwd.append((b0, b1))
@@ -264,8 +266,10 @@ def bench_ours(a):
             r0.project(P, views[v])
             r0.bin_sort()
             e0.record()
-            r0.render()
+            raster.gs_render_fwd(r0.proj, r0.sorted_idx, r0.tile_range, r0.cam, r0.frame, False,
+                                 tile_order=r0.tile_order, tile_work=r0.tile_work)
             e1.record()
+            raster.gs_tile_order(r0.tile_work, r0.T, r0.bwd_order)
             r0.compute_loss(tc[v], td[v], None, ms.lc, ms.ld)
             r0.backward(P, views[v], raster.GS_GRAD_PARAMS | raster.GS_BWD_PIXELS_ONLY, ms.grads, event_pair=(e2, e3))
             r0.backward(P, views[v], raster.GS_GRAD_PARAMS | raster.GS_BWD_GAUSS_ONLY, ms.grads)
@@ -295,8 +299,8 @@ def bench_ours(a):
                            "render_fwd_isolated": roof_iso["render_fwd"]},
         "clocks": clocks, "gpu_launches": launches, "sm_count": sm_count,
     }
-    if rank == 0 and not a.profile and not a.no_e2e:
-        line["e2e"] = e2e_ours(a, s, ms, device)
+    if not a.profile and not a.no_e2e:  # every rank: the step contains the all-reduce
+        line["e2e"] = e2e_ours(a, s, ms, device, world)
     if world > 1:
         dist.barrier()
     if rank == 0 and world == 1 and not a.profile and not a.no_tracking:
@@ -309,7 +313,7 @@ def bench_ours(a):
         dist.destroy_process_group()
 
 
-def e2e_ours(a, s, ms, device):
+def e2e_ours(a, s, ms, device, world=1):
     """Same metric through the public API with HOST buffers: every step copies
     its inputs (Gaussian parameters, view poses, this rank's RGB-D targets)
     from pinned host memory and reads the per-view losses back."""
@@ -345,6 +349,10 @@ def e2e_ours(a, s, ms, device):
     e1.record()
     torch.cuda.synchronize()
     ms_step = e0.elapsed_time(e1) / n
+    if world > 1:  # max over ranks
+        t = torch.tensor([ms_step], dtype=torch.float64, device=device)
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        ms_step = float(t.item())
     mp = ms.V * s.cam.width * s.cam.height / 1e6
     return {"value": mp / (ms_step * 1e-3), "unit": UNIT, "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
             "ms_per_step": ms_step}

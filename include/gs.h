@@ -216,11 +216,18 @@ int gs_bin_sort(gs_proj pr, int32_t n, gs_camera cam, void *ws, size_t ws_bytes,
  *   n_contrib (device) [H][W] int32 (position in the tile list of the last
  *             composited entry) + 1, 0 if none
  *   stats     (device, nullable) [2][H][W] int32: entries scanned, entries
- *             composited — the per-pixel counts of SURVEY §8(d). */
+ *             composited — the per-pixel counts of SURVEY §8(d)
+ *   tile_work (device, nullable) [T] int32: sum of n_contrib over the tile's
+ *             pixels (the backward's work per tile, for gs_tile_order). */
 int gs_render_fwd(gs_proj pr, const int32_t *sorted_idx, const int32_t *tile_range,
                   const int32_t *tile_order, gs_camera cam, float *color, float *depth,
                   float *alpha, float *T_final, int32_t *n_contrib, int32_t *stats,
-                  void *stream);
+                  int32_t *tile_work, void *stream);
+
+/* Scheduling utility: tile ids by descending work (64 buckets of max/64, order
+ * inside a bucket unspecified), e.g. from gs_render_fwd's tile_work for
+ * gs_render_bwd.  work (device) [T] >= 0; order (device) [T]. */
+int gs_tile_order(const int32_t *work, int32_t T, int32_t *order, void *stream);
 
 /* S4 — L1 colour + L1 depth loss (Eqs. 9, 10 L1 part, 12; P:178-202;
  * S:256-264; R20, R21).

@@ -62,7 +62,8 @@ _PROTOS = {
     "gs_pose_partials_count": (_I32, [_I32]),
     "gs_project": (C.c_int, [GsParams, _VP, GsCamera, GsProj, _VP, _VP]),
     "gs_bin_sort": (C.c_int, [GsProj, _I32, GsCamera, _VP, _SZ, _I64, _VP, _VP, _VP, _VP, _VP, _VP]),
-    "gs_render_fwd": (C.c_int, [GsProj, _VP, _VP, _VP, GsCamera, _VP, _VP, _VP, _VP, _VP, _VP, _VP]),
+    "gs_render_fwd": (C.c_int, [GsProj, _VP, _VP, _VP, GsCamera, _VP, _VP, _VP, _VP, _VP, _VP, _VP, _VP]),
+    "gs_tile_order": (C.c_int, [_VP, _I32, _VP, _VP]),
     "gs_loss": (C.c_int, [GsCamera, _VP, _VP, _VP, _VP, _VP, _F, _F, _VP, _SZ, _VP, _VP, _VP, _VP]),
     "gs_render_bwd": (C.c_int, [GsParams, _VP, GsCamera, GsProj, _VP, _VP, _VP, _VP, _VP, _VP, _VP, _VP, _U32, _VP,
                                 _SZ, _VP, _VP, _VP, _VP, _VP, _VP]),

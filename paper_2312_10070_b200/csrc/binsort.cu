@@ -518,6 +518,46 @@ __global__ void __launch_bounds__(256) k_gather_ids(const uint32_t *__restrict__
 
 }  // namespace gs
 
+namespace gs {
+// Tiles by descending work, 64 buckets of max/64 (single CTA).
+__global__ void __launch_bounds__(1024) k_order_by_work(const int32_t *__restrict__ work, int T, int32_t *order) {
+  __shared__ int s_max;
+  __shared__ unsigned s_b[64];
+  if (threadIdx.x == 0) s_max = 0;
+  if (threadIdx.x < 64) s_b[threadIdx.x] = 0;
+  __syncthreads();
+  int m = 0;
+  for (int t = threadIdx.x; t < T; t += blockDim.x) m = max(m, work[t]);
+  atomicMax(&s_max, m);
+  __syncthreads();
+  const int64_t den = int64_t(s_max) + 1;
+  for (int t = threadIdx.x; t < T; t += blockDim.x)
+    atomicAdd(&s_b[63 - int(int64_t(max(work[t], 0)) * 64 / den)], 1u);
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    unsigned run = 0;
+    for (int b = 0; b < 64; ++b) {
+      const unsigned c = s_b[b];
+      s_b[b] = run;
+      run += c;
+    }
+  }
+  __syncthreads();
+  for (int t = threadIdx.x; t < T; t += blockDim.x)
+    order[atomicAdd(&s_b[63 - int(int64_t(max(work[t], 0)) * 64 / den)], 1u)] = t;
+}
+}  // namespace gs
+
+extern "C" int gs_tile_order(const int32_t *work, int32_t T, int32_t *order, void *stream) {
+  using namespace gs;
+  if (!work || !order || T <= 0) {
+    set_error("gs_tile_order: invalid argument");
+    return GS_ERR_INVALID_ARG;
+  }
+  k_order_by_work<<<1, 1024, 0, as_stream(stream)>>>(work, T, order);
+  return check_launch("gs_tile_order");
+}
+
 extern "C" size_t gs_binsort_workspace_bytes(int32_t n, int64_t capacity, gs_camera cam) {
   gs::SortLayout L;
   if (n < 0 || capacity < 0 || !gs::camera_ok(cam) || !gs::make_layout(n, capacity, cam, L)) return 0;

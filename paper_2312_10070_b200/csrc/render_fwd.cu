@@ -25,7 +25,7 @@ struct FwdArgs {
   const int32_t *tile_order;
   int W, H, TX;
   float *color, *depth, *alpha, *T_final;
-  int32_t *n_contrib, *stats;
+  int32_t *n_contrib, *stats, *tile_work;
 };
 
 constexpr int kFPX = 2;  // pixels per thread in the forward
@@ -43,21 +43,18 @@ __global__ void __launch_bounds__(FG::kThreads) k_render_fwd(FwdArgs a) {
   const double ox = double(tx * kTile), oy = double(ty * kTile);
   const int2 range = a.tile_range[tile];
   float T[kFPX], c0[kFPX], c1[kFPX], c2[kFPX], D[kFPX], A[kFPX];
-  // thr[k]: exponent threshold of the pre-test while pixel k composites,
-  // +inf once it has terminated (or lies outside the image)
-  float thr[kFPX];
+  // a pixel composites while T >= 1e-4 (include, then stop: T < 1e-4 happens
+  // exactly at the stopping entry); pixels outside the image start with T = 0
   int last[kFPX], ncon[kFPX], term[kFPX];
-  const float kInf = __int_as_float(0x7f800000);
 #pragma unroll
   for (int k = 0; k < kFPX; ++k) {
-    T[k] = 1.f;
+    T[k] = (pg.row_in && pg.px0 + k < a.W) ? 1.f : 0.f;
     c0[k] = c1[k] = c2[k] = D[k] = A[k] = 0.f;
     last[k] = ncon[k] = 0;
     term[k] = range.y - range.x;  // entries scanned if the pixel never terminates
-    thr[k] = (pg.row_in && pg.px0 + k < a.W) ? kExpSkip : kInf;
   }
   for (int start = range.x; start < range.y; start += kBatch) {
-    if (__syncthreads_count(thr[0] < kInf || thr[1] < kInf) == 0) break;
+    if (__syncthreads_count(T[0] >= kTEps || T[1] >= kTEps) == 0) break;
     static_assert(FG::kRecPerThread == 1, "one staged record per thread");
     {
       const int k = start + threadIdx.x;
@@ -82,7 +79,7 @@ __global__ void __launch_bounds__(FG::kThreads) k_render_fwd(FwdArgs a) {
 #pragma unroll
     for (int h = 0; h < kBatch / 32; ++h) {
       unsigned bits = hits[h];
-      if (bits && !__any_sync(0xffffffffu, thr[0] < kInf || thr[1] < kInf)) break;
+      if (bits && !__any_sync(0xffffffffu, T[0] >= kTEps || T[1] >= kTEps)) break;
       while (bits) {
         const int j = h * 32 + __ffs(bits) - 1;
         bits &= bits - 1;
@@ -93,7 +90,7 @@ __global__ void __launch_bounds__(FG::kThreads) k_render_fwd(FwdArgs a) {
 #pragma unroll
         for (int k = 0; k < kFPX; ++k) {
           e[k] = pixel_exponent(rt, pg.fpx0 + float(k));
-          pass[k] = e[k] >= thr[k];
+          pass[k] = e[k] >= kExpSkip && T[k] >= kTEps;
         }
         if (!__any_sync(0xffffffffu, pass[0] || pass[1])) continue;
         const float4 c = s_rgbz[j];
@@ -109,15 +106,25 @@ __global__ void __launch_bounds__(FG::kThreads) k_render_fwd(FwdArgs a) {
           D[k] = __fmaf_rn(c.w, w, D[k]);                // Eq. 6 (camera-frame z, R12)
           A[k] = __fadd_rn(A[k], w);                     // R14
           T[k] = __fmul_rn(T[k], __fsub_rn(1.f, al));
-          const bool comp = al > 0.f;
-          last[k] = comp ? pos : last[k];
-          if (kStats) ncon[k] += comp;
-          const bool stop = comp && T[k] < kTEps;        // include, then stop (R11)
-          term[k] = stop ? pos : term[k];
-          thr[k] = stop ? kInf : thr[k];
+          last[k] = al > 0.f ? pos : last[k];
+          if (kStats) {
+            ncon[k] += al > 0.f;
+            term[k] = (al > 0.f && T[k] < kTEps) ? pos : term[k];  // include, then stop (R11)
+          }
         }
       }
     }
+  }
+  if (a.tile_work) {  // the backward's work on this tile: sum of n_contrib
+    __shared__ int s_work;
+    if (threadIdx.x == 0) s_work = 0;
+    __syncthreads();
+    int wk = last[0] + last[1];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) wk += __shfl_xor_sync(0xffffffffu, wk, o);
+    if ((threadIdx.x & 31) == 0) atomicAdd(&s_work, wk);
+    __syncthreads();
+    if (threadIdx.x == 0) a.tile_work[tile] = s_work;
   }
   if (!pg.row_in) return;
   const size_t HW = size_t(a.W) * a.H;
@@ -142,8 +149,8 @@ __global__ void __launch_bounds__(FG::kThreads) k_render_fwd(FwdArgs a) {
 }  // namespace gs
 
 extern "C" int gs_render_fwd(gs_proj pr, const int32_t *sorted_idx, const int32_t *tile_range,
-                             const int32_t *tile_order, gs_camera cam, float *color, float *depth, float *alpha, float *T_final, int32_t *n_contrib,
-                             int32_t *stats, void *stream) {
+                             const int32_t *tile_order, gs_camera cam, float *color, float *depth, float *alpha,
+                             float *T_final, int32_t *n_contrib, int32_t *stats, int32_t *tile_work, void *stream) {
   using namespace gs;
   if (!camera_ok(cam) || !tile_range || !color || !depth || !alpha || !T_final || !n_contrib) {
     set_error("gs_render_fwd: invalid argument");
@@ -156,7 +163,8 @@ extern "C" int gs_render_fwd(gs_proj pr, const int32_t *sorted_idx, const int32_
   }
   FwdArgs a{reinterpret_cast<const double2 *>(pr.uv), reinterpret_cast<const float4 *>(pr.coef),
             reinterpret_cast<const float4 *>(pr.rgbz), sorted_idx, reinterpret_cast<const int2 *>(tile_range),
-            tile_order, cam.width, cam.height, tiles_x(cam), color, depth, alpha, T_final, n_contrib, stats};
+            tile_order, cam.width, cam.height, tiles_x(cam), color, depth, alpha, T_final, n_contrib, stats,
+            tile_work};
   const int T = tiles_x(cam) * tiles_y(cam);
   if (stats)
     k_render_fwd<true><<<T, FG::kThreads, 0, as_stream(stream)>>>(a);

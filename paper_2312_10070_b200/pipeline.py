@@ -126,9 +126,9 @@ def tile_passes(cam):
 
 def kernels_per_view(cam, loss=True, bwd=True):
     """Kernels of ours per view (the sort's memset is a copy-engine node, not a kernel):
-    project 1; bin_sort: prep, tile counts, depth passes, scan, emit, tile passes,
-    gather; render 1; loss 3; backward 2."""
-    n = 1 + (2 + sort_passes(cam) + 2 + tile_passes(cam) + 1) + 1
+    project 1; bin_sort: prep, tile counts, 3 per depth pass, scan, emit, 3 per
+    tile pass, gather; render 1 + tile order 1; loss 3; backward 2."""
+    n = 1 + (2 + 3 * sort_passes(cam) + 2 + 3 * tile_passes(cam) + 1) + 2
     if loss:
         n += 3
     if bwd:

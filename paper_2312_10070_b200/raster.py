@@ -19,7 +19,7 @@ from . import _lib
 from ._lib import GS_BWD_GAUSS_ONLY, GS_BWD_PIXELS_ONLY, GS_GRAD_PARAMS, GS_GRAD_POSE, GsCamera, GsError, GsParams, GsPoseStep, GsProj, check, lib
 
 __all__ = ["Params", "Grads", "Proj", "Frame", "Rasterizer", "camera", "gs_project", "gs_bin_sort",
-           "gs_render_fwd", "gs_loss", "gs_render_bwd", "gs_pose_grad", "GS_GRAD_PARAMS", "GS_GRAD_POSE", "GS_BWD_PIXELS_ONLY", "GS_BWD_GAUSS_ONLY",
+           "gs_render_fwd", "gs_tile_order", "gs_loss", "gs_render_bwd", "gs_pose_grad", "GS_GRAD_PARAMS", "GS_GRAD_POSE", "GS_BWD_PIXELS_ONLY", "GS_BWD_GAUSS_ONLY",
            "GsError", "device_check"]
 
 
@@ -148,10 +148,15 @@ def gs_bin_sort(proj: Proj, n, cam: GsCamera, ws, capacity, sorted_idx, tile_ran
 
 
 def gs_render_fwd(proj: Proj, sorted_idx, tile_range, cam: GsCamera, frame: Frame, stats=False, stream=None,
-                  tile_order=None):
+                  tile_order=None, tile_work=None):
     check(lib().gs_render_fwd(proj.c(), _p(sorted_idx), _p(tile_range), _p(tile_order), cam, _p(frame.color), _p(frame.depth),
                               _p(frame.alpha), _p(frame.T_final), _p(frame.n_contrib),
-                              _p(frame.stats) if stats else None, _stream(stream)), "gs_render_fwd")
+                              _p(frame.stats) if stats else None, _p(tile_work), _stream(stream)),
+          "gs_render_fwd")
+
+
+def gs_tile_order(work, T, order, stream=None):
+    check(lib().gs_tile_order(_p(work), int(T), _p(order), _stream(stream)), "gs_tile_order")
 
 
 def gs_loss(cam: GsCamera, color, depth, tgt_color, tgt_depth, weight, lambda_color, lambda_depth, ws, loss,
@@ -209,6 +214,8 @@ class Rasterizer:
         self.sort_ws = torch.empty(4, dtype=torch.float32, device=device)  # sized by set_capacity
         self.tile_range = torch.empty(self.T, 2, dtype=torch.int32, device=device)
         self.tile_order = torch.empty(self.T, dtype=torch.int32, device=device)
+        self.tile_work = torch.empty(self.T, dtype=torch.int32, device=device)
+        self.bwd_order = torch.empty(self.T, dtype=torch.int32, device=device)
         self.n_pairs = torch.zeros(1, dtype=torch.int64, device=device)
         self.counters = torch.zeros(4, dtype=torch.int64, device=device)
         self.frame = Frame(H, W, device)
@@ -264,7 +271,8 @@ class Rasterizer:
 
     def render(self, stats=False):
         gs_render_fwd(self.proj, self.sorted_idx, self.tile_range, self.cam, self.frame, stats,
-                      tile_order=self.tile_order)
+                      tile_order=self.tile_order, tile_work=self.tile_work)
+        gs_tile_order(self.tile_work, self.T, self.bwd_order)  # the backward's heaviest-first order
 
     def forward(self, params: Params, view, stats=False):
         self.project(params, view)
@@ -283,7 +291,7 @@ class Rasterizer:
                       self.frame.n_contrib, self.dL_dcolor if dL_dcolor is None else dL_dcolor,
                       self.dL_ddepth if dL_ddepth is None else dL_ddepth, dL_dalpha, flags, self.bwd_ws, grads,
                       self.pose_partials if flags & GS_GRAD_POSE else None, event_pair=event_pair,
-                      tile_order=self.tile_order)
+                      tile_order=self.bwd_order)
 
     def pose_grad(self, view, step=None, adam_state=None, dL_dview=None, dL_dtwist=None, dL_dqt=None):
         gs_pose_grad(view, self.pose_partials, self.n_partials, step, adam_state, dL_dview, dL_dtwist, dL_dqt)

@@ -54,8 +54,9 @@ def test_invalid_arguments_rejected_on_host():
     p = _lib.GsParams(None, None, None, None, 10)
     assert L.gs_project(p, C.c_void_p(16), cam, pr, None, None) == _lib.GS_ERR_INVALID_ARG
     badcam = camera(inputs.Camera(64, 48, -1.0, 60.0, 32.0, 24.0))
-    assert L.gs_render_fwd(pr, None, None, None, badcam, None, None, None, None, None, None,
+    assert L.gs_render_fwd(pr, None, None, None, badcam, None, None, None, None, None, None, None,
                            None) == _lib.GS_ERR_INVALID_ARG
+    assert L.gs_tile_order(None, 10, None, None) == _lib.GS_ERR_INVALID_ARG
     assert L.gs_bin_sort(pr, 10, cam, None, 0, 100, C.c_void_p(16), C.c_void_p(16), None, C.c_void_p(16), None,
                          None) == _lib.GS_ERR_INVALID_ARG  # null projection arrays
     assert L.gs_loss(cam, None, None, None, None, None, 1.0, 1.0, None, 0, None, None, None, None) == _lib.GS_ERR_INVALID_ARG
