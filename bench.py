@@ -442,15 +442,15 @@ def bench_reference(a):
     oracle.build()
     # each "step" is a bounded sample: one view of the workload (warm-up steps are not timed)
     vals = []
-    for i in range(min(a.warmup, 1) + a.steps):
+    for i in range(a.warmup + a.steps):
         r = cpu_baseline(a, s, max_views=1)
-        if i >= min(a.warmup, 1):
+        if i >= a.warmup:
             vals.append(r)
     v = statistics.median(x["value"] for x in vals)
     per_view = statistics.median(x["s_per_view"] for x in vals)
     V = s.views.shape[0]
     line = {"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": a.gpus, "steps": a.steps,
-            "warmup": warm, "ms_per_step": per_view * V * 1e3, "higher_is_better": True, "scaling": "strong",
+            "warmup": a.warmup, "ms_per_step": per_view * V * 1e3, "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded generator)",
             "config": {"workload": f"BJ.configs[{a.config}] sub-map mapping iteration (oracle, sampled)",
                        "gaussians": s.n, "width": s.cam.width, "height": s.cam.height, "views_per_step": V},
