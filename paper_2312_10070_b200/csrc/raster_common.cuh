@@ -7,21 +7,28 @@
 
 namespace gs {
 
-// One CTA per 16x16 tile; every thread owns PX adjacent pixels of one row:
-// lane -> columns PX*(lane % (16/PX)) .. +PX-1, row (2 PX) w + lane / (16/PX).
-// A warp covers a 16 x (2 PX) strip; a tile has 8/PX warps.  The PX pixels
-// share dy, so the row terms of the quadratic form are evaluated once per
-// (thread, entry).  The forward uses PX = 2 (short per-warp critical path),
-// the backward PX = 4 (half the warp reductions per pixel).
+// One CTA per 16x16 tile; every thread owns PX adjacent pixels of one row.
+// A warp covers a WX x (32 PX / WX) block of the tile (WX = 8 or 16); warps
+// tile the 16x16 tile row-major.  The PX pixels of a thread share dy, so the
+// row terms of the quadratic form are evaluated once per (thread, entry), and
+// they are processed in pairs with the packed fp32x2 pipe (FFMA2).
+//   forward  : PX = 2, WX = 8  -> 4 warps, 8x8 blocks
+//   backward : PX = 4, WX = 16 -> 2 warps, 16x8 strips
 constexpr int kBatch = 128;  // records staged per shared-memory batch
 
-template <int PX>
+template <int PX, int WX>
 struct Geo {
+  static_assert(PX % 2 == 0, "pixels are processed in pairs");
   static constexpr int kThreads = kTilePx / PX;
   static constexpr int kWarps = kThreads / 32;
-  static constexpr int kLanesPerRow = kTile / PX;
-  static constexpr int kRows = 32 / kLanesPerRow;  // rows per warp strip
+  static constexpr int kLanesPerRow = WX / PX;
+  static constexpr int kRows = 32 / kLanesPerRow;  // rows per warp block
+  static constexpr int kAcross = kTile / WX;       // warp blocks per tile row
   static constexpr int kRecPerThread = kBatch / kThreads;
+  static_assert(kWarps * WX * kRows == kTilePx, "warp blocks must tile the tile");
+  // tile-local origin of warp w's block
+  static __host__ __device__ constexpr int bx(int w) { return (w % kAcross) * WX; }
+  static __host__ __device__ constexpr int by(int w) { return (w / kAcross) * kRows; }
 };
 
 struct PixGeom {
@@ -31,12 +38,12 @@ struct PixGeom {
   bool row_in;  // py < H
 };
 
-template <int PX>
+template <class G>
 __device__ __forceinline__ PixGeom pix_geom(int tx, int ty, int H) {
-  using G = Geo<PX>;
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   PixGeom g;
-  const int lx = (lane % G::kLanesPerRow) * PX, ly = w * G::kRows + lane / G::kLanesPerRow;
+  const int lx = G::bx(w) + (lane % G::kLanesPerRow) * (kTilePx / G::kThreads);
+  const int ly = G::by(w) + lane / G::kLanesPerRow;
   g.px0 = tx * kTile + lx;
   g.py = ty * kTile + ly;
   g.fpx0 = float(lx);
@@ -45,30 +52,48 @@ __device__ __forceinline__ PixGeom pix_geom(int tx, int ty, int H) {
   return g;
 }
 
-// Per-(thread, entry) row terms of log2 alpha~ = log2 o - y1^2 - y2^2 with
-// y1 = a' (u_l - x) + b' (v_l - y), y2 = d' (v_l - y), tile-local fp32
-// offsets (H2) and the H2b coefficients (a', b', d', log2 o):
-//   e0 = log2 o - y2^2,  c0 = a' u_l + b' (v_l - y)
-// and per pixel x:  y1 = c0 - a' x,  e = e0 - y1^2.
-// Explicit round-to-nearest intrinsics: no contraction can differ between the
-// forward and the backward kernel.
-struct RowTerms {
-  float e0, c0, na;  // na = -a'
+// log2 alpha~ = log2 o - y1^2 - y2^2 with y1 = a' (u_l - x) + b' (v_l - y),
+// y2 = d' (v_l - y): the H2b Cholesky form of sigma, in tile-local fp32
+// offsets (H2).  Staged once per entry (EntryTerms):
+//   p = (a', b', d', K = a' u_l + b' v_l),  q = (DV = d' v_l, log2 o)
+// per (thread, entry) row terms (3 FFMA):
+//   c0 = K - b' y,  y2 = DV - d' y,  e0 = log2 o - y2^2
+// and per pixel x (2 FFMA, as FFMA2 over a pixel pair):
+//   y1 = c0 - a' x,  e = e0 - y1^2.
+// Explicit round-to-nearest intrinsics and FMA-only chains: no contraction
+// can differ between the forward and the backward kernel (an FFMA2 lane is
+// the correctly rounded FMA, identical to the scalar one).
+struct EntryTerms {
+  float4 p;
+  float2 q;
 };
 
-__device__ __forceinline__ RowTerms row_terms(float4 coef, float ul, float vl, float fpy) {
-  const float dy = __fsub_rn(vl, fpy);
-  const float y2 = __fmul_rn(coef.z, dy);
+__device__ __forceinline__ EntryTerms entry_terms(float4 coef, float ul, float vl) {
+  EntryTerms t;
+  t.p = make_float4(coef.x, coef.y, coef.z, __fmaf_rn(coef.x, ul, __fmul_rn(coef.y, vl)));
+  t.q = make_float2(__fmul_rn(coef.z, vl), coef.w);
+  return t;
+}
+
+struct RowTerms {
+  float2 na, c0, e0;  // broadcast pairs: -a', c0, e0
+};
+
+__device__ __forceinline__ RowTerms row_terms(float4 p, float2 q, float fpy) {
+  const float c0 = __fmaf_rn(-p.y, fpy, p.w);
+  const float y2 = __fmaf_rn(-p.z, fpy, q.x);
+  const float e0 = __fmaf_rn(-y2, y2, q.y);
   RowTerms r;
-  r.e0 = __fmaf_rn(-y2, y2, coef.w);
-  r.c0 = __fmaf_rn(coef.x, ul, __fmul_rn(coef.y, dy));
-  r.na = -coef.x;
+  r.na = make_float2(-p.x, -p.x);
+  r.c0 = make_float2(c0, c0);
+  r.e0 = make_float2(e0, e0);
   return r;
 }
 
-__device__ __forceinline__ float pixel_exponent(const RowTerms &r, float fpx) {
-  const float y1 = __fmaf_rn(r.na, fpx, r.c0);
-  return __fmaf_rn(-y1, y1, r.e0);
+// exponent at the pixel pair x = (fx.x, fx.y)
+__device__ __forceinline__ float2 pair_exponent(const RowTerms &r, float2 fx) {
+  const float2 y1 = __ffma2_rn(r.na, fx, r.c0);
+  return __ffma2_rn(make_float2(-y1.x, -y1.y), y1, r.e0);
 }
 
 // Conservative tile-local box of the region where an entry can pass the
@@ -85,29 +110,37 @@ __device__ __forceinline__ float4 entry_box(float4 coef, float ul, float vl) {
   return make_float4(ul - hx, ul + hx, vl - hy, vl + hy);
 }
 
-// Bit w set iff the box meets warp w's strip [0, 15] x [R w, R w + R - 1].
-template <int PX>
-__device__ __forceinline__ unsigned box_strip_mask(float4 b) {
-  using G = Geo<PX>;
-  if (!(b.y >= 0.f && b.x <= float(kTile - 1))) return 0u;
+// Bit w set iff the box meets warp w's block.
+template <class G>
+__device__ __forceinline__ unsigned box_block_mask(float4 b) {
   unsigned m = 0u;
 #pragma unroll
   for (int w = 0; w < G::kWarps; ++w) {
-    const float y0 = float(w * G::kRows), y1 = y0 + float(G::kRows - 1);
-    if (b.w >= y0 && b.z <= y1) m |= 1u << w;
+    const float x0 = float(G::bx(w)), y0 = float(G::by(w));
+    if (b.y >= x0 && b.x <= x0 + float(16 / G::kAcross - 1) && b.w >= y0 && b.z <= y0 + float(G::kRows - 1))
+      m |= 1u << w;
   }
   return m;
 }
 
-// This warp's hit bitmaps over a staged batch of kBatch entries: word h has
-// bit l set iff entry 32 h + l hits the warp's strip (4 ballots per batch).
-__device__ __forceinline__ void warp_hits(const unsigned char *s_mask, int cnt, unsigned hits[kBatch / 32]) {
+// This warp's hit list over a staged batch: the indices (ascending) of the
+// entries j < cnt whose mask has bit w, written to list[0..n), followed by
+// `sentinel` at list[n].  Returns n.
+__device__ __forceinline__ int warp_hit_list(const unsigned char *s_mask, int cnt, unsigned char *list,
+                                             int sentinel) {
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  int n = 0;
 #pragma unroll
   for (int h = 0; h < kBatch / 32; ++h) {
     const int j = h * 32 + lane;
-    hits[h] = __ballot_sync(0xffffffffu, j < cnt && ((s_mask[j] >> w) & 1u));
+    const bool hit = j < cnt && ((s_mask[j] >> w) & 1u);
+    const unsigned b = __ballot_sync(0xffffffffu, hit);
+    if (hit) list[n + __popc(b & lanemask_lt())] = (unsigned char)j;
+    n += __popc(b);
   }
+  if (lane == 0) list[n] = (unsigned char)sentinel;
+  __syncwarp();
+  return n;
 }
 
 }  // namespace gs

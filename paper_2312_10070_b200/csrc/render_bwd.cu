@@ -1,14 +1,17 @@
 // render_bwd.cu — S5 + S6 gs_render_bwd (Eqs. 7-8).
 //
-// S5 (k_bwd_pixels): one CTA per tile, one pixel per thread.  Every pixel
-// replays its composited entries back to front starting from T_final and
-// n_contrib, recomputing alpha with the very same alpha_exponent /
-// alpha_decide as gs_render_fwd (H5), reconstructing T_j = T_{j+1}/(1-alpha_j)
-// and carrying the suffix accumulators of Eq. 8
-//   S_X <- alpha_j X_j + (1 - alpha_j) S_X,  dX/dalpha_j = T_j (X_j - S_X)
-// for X = colour (3), camera depth, alpha.  Per-entry 2-D gradients are summed
-// across the warp with shuffles (skipped when no lane composited the entry)
-// and added to the grad2d scratch with one vector red per float4.
+// S5 (k_bwd_pixels): one CTA (2 warps) per tile, 4 pixels of a row per
+// thread, each warp a 16x8 strip.  Every pixel replays its composited entries
+// back to front starting from T_final and n_contrib, recomputing alpha with
+// the very same entry/row terms and pair exponent as gs_render_fwd (H5),
+// reconstructing T_j = T_{j+1}/(1-alpha_j) and carrying the suffix form of
+// Eq. 8 (one scalar Q = G . S per pixel).  The per-pixel arithmetic runs on
+// fp32x2 pixel pairs (FFMA2).  Each warp walks, back to front, the compacted
+// list of staged entries that meet its strip; per (thread, entry) the 2-D
+// gradients are summed over the thread's pixels, then across the warp by a
+// transposed reduce-scatter (skipped when no lane composited the entry, and
+// replaced by direct vector reds when <= 2 lanes did) and added to the
+// grad2d scratch.
 //
 // S6 (k_bwd_gauss): one thread per visible Gaussian chains the 2-D gradients
 // to mean, quaternion, log-scales, opacity logit and colour ("derived as in
@@ -80,50 +83,162 @@ __device__ __forceinline__ void red_add_v4(float *addr, float x, float y, float 
                : "memory");
 }
 
-constexpr int kBPX = 4;  // pixels per thread in the backward
-using BG = Geo<kBPX>;
+constexpr int kBPX = 4;   // pixels per thread in the backward (two fp32x2 pairs)
+using BG = Geo<kBPX, 16>;  // 2 warps, 16x8 pixel strips
 
+__device__ __forceinline__ float rcp_approx(float x) {
+  float y;
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+
+__device__ __forceinline__ float2 bcast(float x) { return make_float2(x, x); }
+
+// per-thread backward state of its 4 pixels (two fp32x2 pairs): T
+// (reconstructed back to front), upstream G, and the single suffix scalar
+// Q = G . S of Eq. 8's accumulators S = (S_C, S_D, S_A):
+//   dL/dalpha_j = T_j (G . X_j - Q),  Q <- Q + alpha_j (G . X_j - Q)
+struct BwdPix {
+  float2 T[2], G0[2], G1[2], G2[2], GD[2], GA[2], Q[2];
+  int last[kBPX];
+};
+
+// One list entry j at the thread's pixels: alpha replay (H5), T by division
+// (R16), Eq. 8 through Q, per-thread sums, then the warp reduction into
+// grad2d.  Branch-free per pixel: alpha = 0 leaves T and Q unchanged and
+// contributes exact zeros.
 // acc layout: 0 u, 1 v, 2 2*A-term, 3 B, 4 2*C-term, 5 p_z, 6 logit, 7 r, 8 g, 9 b
 // (the 1/2 of dsigma/dA and dsigma/dC is applied once, by the writing lane)
+template <bool kParams>
+__device__ __forceinline__ void bwd_entry(BwdPix &s, const float2 e[2], const bool pass[kBPX], float4 c, float4 cn,
+                                          float2 ul, float fpy, const float2 fx[2], float *dst) {
+  const float dy = ul.y - fpy;  // Delta = mu^I - pixel; one row: dy is shared
+  // per-thread sums over its pixels (as pair sums) of ga = alpha dL/dalpha
+  // (0 if clamped) and ga dx, ga dx^2; dsigma/d(u, v, A, B, C) and
+  // dalpha/dlogit are formed once per (thread, entry) from them, the conic,
+  // dy and o (entry constants)
+  float2 sga = make_float2(0.f, 0.f), sgx = sga, sgxx = sga, sz = sga, sr = sga, sg = sga, sb = sga;
+  bool any = false;
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+    const float at0 = ex2_approx(e[h].x), at1 = ex2_approx(e[h].y);
+    const float m0 = fminf(at0, kAlphaMax), m1 = fminf(at1, kAlphaMax);
+    const bool q0 = pass[2 * h] && m0 >= kAlphaMin, q1 = pass[2 * h + 1] && m1 >= kAlphaMin;
+    const float a0 = q0 ? m0 : 0.f, a1 = q1 ? m1 : 0.f;  // same decision as the forward (H5)
+    any |= q0 || q1;
+    const float2 al = make_float2(a0, a1);
+    // T_j = T_{j+1} / (1 - alpha_j) (R16)
+    s.T[h] = __fmul2_rn(s.T[h], make_float2(rcp_approx(1.f - a0), rcp_approx(1.f - a1)));
+    const float2 wt = __fmul2_rn(al, s.T[h]);
+    // Eq. 8 chained with Eq. 7 through the suffix scalar Q
+    const float2 gx = __ffma2_rn(
+        s.G0[h], bcast(c.x), __ffma2_rn(s.G1[h], bcast(c.y), __ffma2_rn(s.G2[h], bcast(c.z), __ffma2_rn(s.GD[h], bcast(c.w), s.GA[h]))));
+    const float2 d = __fadd2_rn(gx, make_float2(-s.Q[h].x, -s.Q[h].y));
+    const float2 galpha = __fmul2_rn(s.T[h], d);
+    s.Q[h] = __ffma2_rn(al, d, s.Q[h]);
+    sz = __ffma2_rn(wt, s.GD[h], sz);  // dD/dz_j = alpha_j T_j
+    if (kParams) {
+      sr = __ffma2_rn(wt, s.G0[h], sr);  // dC/dc_j = alpha_j T_j
+      sg = __ffma2_rn(wt, s.G1[h], sg);
+      sb = __ffma2_rn(wt, s.G2[h], sb);
+    }
+    // clamped alpha: no gradient (R17)
+    const float2 ga = __fmul2_rn(make_float2(at0 < kAlphaMax ? a0 : 0.f, at1 < kAlphaMax ? a1 : 0.f), galpha);
+    const float2 dx = __fadd2_rn(bcast(ul.x), make_float2(-fx[h].x, -fx[h].y));
+    const float2 t = __fmul2_rn(ga, dx);
+    sga = __fadd2_rn(sga, ga);
+    sgx = __fadd2_rn(sgx, t);
+    sgxx = __ffma2_rn(t, dx, sgxx);
+  }
+  const unsigned ball = __ballot_sync(0xffffffffu, any);
+  if (!ball) return;
+  const float Sga = sga.x + sga.y, Sgx = sgx.x + sgx.y;
+  // dalpha/dsigma = -alpha, dsigma/du = A dx + B dy, dsigma/dv = B dx + C dy,
+  // dsigma/d(A, B, C) = (dx^2/2, dx dy, dy^2/2), dalpha/dlogit = alpha (1 - o)
+  float acc[10];
+  acc[0] = -fmaf(cn.x, Sgx, cn.y * dy * Sga);
+  acc[1] = -fmaf(cn.y, Sgx, cn.z * dy * Sga);
+  acc[2] = -(sgxx.x + sgxx.y);  // x2 (the writer applies 1/2)
+  acc[3] = -dy * Sgx;
+  acc[4] = -dy * dy * Sga;  // x2
+  acc[5] = sz.x + sz.y;
+  acc[6] = kParams ? (1.f - cn.w) * Sga : 0.f;
+  acc[7] = sr.x + sr.y;
+  acc[8] = sg.x + sg.y;
+  acc[9] = sb.x + sb.y;
+  if (__popc(ball) <= 2) {  // few contributing lanes: write directly, skip the reduction
+    if (any) {
+      // grad2d record: (u, v, A, B), (C, p_z, logit, 0), (r, g, b, 0)
+      red_add_v4(dst, acc[0], acc[1], 0.5f * acc[2], acc[3]);
+      red_add_v4(dst + 4, 0.5f * acc[4], acc[5], acc[6], 0.f);
+      if (kParams) red_add_v4(dst + 8, acc[7], acc[8], acc[9], 0.f);
+    }
+    return;
+  }
+  int idx;
+  bool writer;
+  const float tot = warp_reduce10(acc, idx, writer);
+  if (writer && (kParams || idx < 6)) {
+    const int off = idx < 7 ? idx : idx + 1;
+    atomicAdd(dst + off, (idx == 2 || idx == 4) ? 0.5f * tot : tot);
+  }
+}
+
 template <bool kParams, bool kAlphaUp>
 __global__ void __launch_bounds__(BG::kThreads) k_bwd_pixels(BwdArgs a) {
+  // slot kBatch of s_p / s_q is a sentinel entry whose exponent is -inf
   __shared__ int s_idx[kBatch];
+  __shared__ float4 s_p[kBatch + 1];
+  __shared__ float2 s_q[kBatch + 1];
   __shared__ float2 s_uv[kBatch];
-  __shared__ float4 s_coef[kBatch];
   __shared__ float4 s_rgbz[kBatch];
   __shared__ float4 s_conic[kBatch];
   __shared__ unsigned char s_mask[kBatch];
+  __shared__ unsigned char s_list[BG::kWarps][kBatch + 2];
   __shared__ int s_lmax;
   const int tile = a.tile_order ? __ldg(a.tile_order + blockIdx.x) : int(blockIdx.x);
   const int tx = tile % a.TX, ty = tile / a.TX;
-  const PixGeom pg = pix_geom<kBPX>(tx, ty, a.H);
+  const int w = threadIdx.x >> 5;
+  const PixGeom pg = pix_geom<BG>(tx, ty, a.H);
   const double ox = double(tx * kTile), oy = double(ty * kTile);
   const int2 range = a.tile_range[tile];
   const size_t HW = size_t(a.W) * a.H;
-  // per pixel: T (reconstructed back to front), upstream G, and the single
-  // suffix scalar Q = G . S of Eq. 8's accumulators S = (S_C, S_D, S_A):
-  // dL/dalpha_j = T_j (G . X_j - Q),  Q <- Q + alpha_j (G . X_j - Q)
-  float T[kBPX], G0[kBPX], G1[kBPX], G2[kBPX], GD[kBPX], GA[kBPX], Q[kBPX];
-  int last[kBPX];
+  const float2 fx[2] = {make_float2(pg.fpx0, pg.fpx0 + 1.f), make_float2(pg.fpx0 + 2.f, pg.fpx0 + 3.f)};
+  BwdPix s;
   int tmax = 0;
 #pragma unroll
-  for (int k = 0; k < kBPX; ++k) {
-    T[k] = 1.f;
-    G0[k] = G1[k] = G2[k] = GD[k] = GA[k] = Q[k] = 0.f;
-    last[k] = 0;
-    if (pg.row_in && pg.px0 + k < a.W) {
-      const size_t q = size_t(pg.py) * a.W + pg.px0 + k;
-      T[k] = a.T_final[q];
-      last[k] = a.n_contrib[q];
-      G0[k] = a.dL_dcolor[q];
-      G1[k] = a.dL_dcolor[HW + q];
-      G2[k] = a.dL_dcolor[2 * HW + q];
-      GD[k] = a.dL_ddepth[q];
-      if (kAlphaUp) GA[k] = a.dL_dalpha[q];
-      tmax = max(tmax, last[k]);
+  for (int h = 0; h < 2; ++h) {
+    float t[2] = {1.f, 1.f}, g0[2] = {0.f, 0.f}, g1[2] = {0.f, 0.f}, g2[2] = {0.f, 0.f}, gd[2] = {0.f, 0.f},
+          ga[2] = {0.f, 0.f};
+#pragma unroll
+    for (int m = 0; m < 2; ++m) {
+      const int k = 2 * h + m;
+      s.last[k] = 0;
+      if (pg.row_in && pg.px0 + k < a.W) {
+        const size_t q = size_t(pg.py) * a.W + pg.px0 + k;
+        t[m] = a.T_final[q];
+        s.last[k] = a.n_contrib[q];
+        g0[m] = a.dL_dcolor[q];
+        g1[m] = a.dL_dcolor[HW + q];
+        g2[m] = a.dL_dcolor[2 * HW + q];
+        gd[m] = a.dL_ddepth[q];
+        if (kAlphaUp) ga[m] = a.dL_dalpha[q];
+        tmax = max(tmax, s.last[k]);
+      }
     }
+    s.T[h] = make_float2(t[0], t[1]);
+    s.G0[h] = make_float2(g0[0], g0[1]);
+    s.G1[h] = make_float2(g1[0], g1[1]);
+    s.G2[h] = make_float2(g2[0], g2[1]);
+    s.GD[h] = make_float2(gd[0], gd[1]);
+    s.GA[h] = make_float2(ga[0], ga[1]);
+    s.Q[h] = make_float2(0.f, 0.f);
   }
-  if (threadIdx.x == 0) s_lmax = 0;
+  if (threadIdx.x == 0) {
+    s_lmax = 0;
+    s_p[kBatch] = make_float4(0.f, 0.f, 0.f, 0.f);
+    s_q[kBatch] = make_float2(0.f, -INFINITY);
+  }
   __syncthreads();
   // warp-level bound: entries at or beyond every lane's n_contrib are skipped
   int wmax = tmax;
@@ -132,6 +247,7 @@ __global__ void __launch_bounds__(BG::kThreads) k_bwd_pixels(BwdArgs a) {
   if ((threadIdx.x & 31) == 0 && wmax > 0) atomicMax(&s_lmax, wmax);
   __syncthreads();
   const int lmax = s_lmax;
+  unsigned char *list = s_list[w];
   for (int end = lmax; end > 0; end -= kBatch) {
     const int beg = max(end - kBatch, 0);
     __syncthreads();
@@ -144,108 +260,46 @@ __global__ void __launch_bounds__(BG::kThreads) k_bwd_pixels(BwdArgs a) {
         const double2 u = __ldg(a.uv + g);
         const float4 cf = __ldg(a.coef + g);
         const float ul = float(u.x - ox), vl = float(u.y - oy);
+        const EntryTerms et = entry_terms(cf, ul, vl);
         s_idx[i] = g;
+        s_p[i] = et.p;
+        s_q[i] = et.q;
         s_uv[i] = make_float2(ul, vl);
-        s_coef[i] = cf;
         s_rgbz[i] = __ldg(a.rgbz + g);
         s_conic[i] = __ldg(a.conic_o + g);
-        s_mask[i] = (unsigned char)box_strip_mask<kBPX>(entry_box(cf, ul, vl));
+        s_mask[i] = (unsigned char)box_block_mask<BG>(entry_box(cf, ul, vl));
       }
     }
     __syncthreads();
-    unsigned hits[kBatch / 32];
-    warp_hits(s_mask, min(end, wmax) - beg, hits);
-    // back to front over this warp's hits (entries missing its strip cannot
-    // pass the exponent pre-test at any of its pixels).  Branch-free per
-    // pixel: a pixel that did not composite the entry uses alpha = 0, which
-    // leaves T and Q unchanged and contributes exact zeros.
+    // back to front over this warp's hits, two per step (their exponents are
+    // independent; the entries are replayed in order).  Entries missing the
+    // warp's strip cannot pass the exponent pre-test at any of its pixels.
+    // Hits are list[1..nh]; list[0] is the sentinel.
+    if ((threadIdx.x & 31) == 0) list[0] = (unsigned char)kBatch;
+    const int nh = warp_hit_list(s_mask, min(end, wmax) - beg, list + 1, kBatch);
+    for (int kk = nh; kk >= 1; kk -= 2) {
+      const int ja = list[kk], jb = list[kk - 1];
+      const RowTerms ra = row_terms(s_p[ja], s_q[ja], pg.fpy);
+      const RowTerms rb = row_terms(s_p[jb], s_q[jb], pg.fpy);
+      float2 ea[2], eb[2];
 #pragma unroll
-    for (int h = kBatch / 32 - 1; h >= 0; --h) {
-      unsigned bits = hits[h];
-      while (bits) {
-        const int hb = 31 - __clz(bits);
-        bits &= ~(1u << hb);
-        const int j = h * 32 + hb;
+      for (int h = 0; h < 2; ++h) {
+        ea[h] = pair_exponent(ra, fx[h]);
+        eb[h] = pair_exponent(rb, fx[h]);
+      }
+#pragma unroll
+      for (int u = 0; u < 2; ++u) {
+        const int j = u ? jb : ja;
+        const float2 *e = u ? eb : ea;
         const int pos = beg + j;  // entry position in the tile list
-        const float2 ul = s_uv[j];
-        const RowTerms rt = row_terms(s_coef[j], ul.x, ul.y, pg.fpy);
-        float e[kBPX];
         bool pass[kBPX];
-        bool anyp = false;
 #pragma unroll
-        for (int k = 0; k < kBPX; ++k) {
-          e[k] = pixel_exponent(rt, pg.fpx0 + float(k));
-          pass[k] = pos < last[k] && e[k] >= kExpSkip;
-          anyp |= pass[k];
+        for (int h = 0; h < 2; ++h) {
+          pass[2 * h] = pos < s.last[2 * h] && e[h].x >= kExpSkip;
+          pass[2 * h + 1] = pos < s.last[2 * h + 1] && e[h].y >= kExpSkip;
         }
-        if (!__any_sync(0xffffffffu, anyp)) continue;
-        const float4 c = s_rgbz[j];
-        const float4 cn = s_conic[j];
-        const float dy = ul.y - pg.fpy;  // Delta = mu^I - pixel; one row: dy is shared
-        const float dx0 = ul.x - pg.fpx0;
-        // per-thread sums over its pixels of ga = alpha dL/dalpha (0 if clamped) and
-        // ga dx, ga dx^2; dsigma/d(u, v, A, B, C) and dalpha/dlogit are formed once
-        // per (thread, entry) from them, the conic, dy and o (entry constants)
-        float sga = 0.f, sgx = 0.f, sgxx = 0.f, sz = 0.f, sr = 0.f, sg = 0.f, sb = 0.f;
-        bool any = false;
-#pragma unroll
-        for (int k = 0; k < kBPX; ++k) {
-          const float at = ex2_approx(e[k]);
-          float al = fminf(at, kAlphaMax);
-          al = (pass[k] && al >= kAlphaMin) ? al : 0.f;  // same decision as the forward (H5)
-          any |= al > 0.f;
-          T[k] = __fdividef(T[k], 1.f - al);  // T_j = T_{j+1} / (1 - alpha_j) (R16)
-          const float w = al * T[k];
-          // Eq. 8 chained with Eq. 7 through the suffix scalar Q
-          const float gx = fmaf(G0[k], c.x, fmaf(G1[k], c.y, fmaf(G2[k], c.z, fmaf(GD[k], c.w, GA[k]))));
-          const float d = gx - Q[k];
-          const float galpha = T[k] * d;
-          Q[k] = fmaf(al, d, Q[k]);
-          sz = fmaf(w, GD[k], sz);  // dD/dz_j = alpha_j T_j
-          if (kParams) {
-            sr = fmaf(w, G0[k], sr);  // dC/dc_j = alpha_j T_j
-            sg = fmaf(w, G1[k], sg);
-            sb = fmaf(w, G2[k], sb);
-          }
-          const float ga = (at < kAlphaMax ? al : 0.f) * galpha;  // clamped alpha: no gradient (R17)
-          const float dx = dx0 - float(k);
-          const float t = ga * dx;
-          sga += ga;
-          sgx += t;
-          sgxx = fmaf(t, dx, sgxx);
-        }
-        // dalpha/dsigma = -alpha, dsigma/du = A dx + B dy, dsigma/dv = B dx + C dy,
-        // dsigma/d(A, B, C) = (dx^2/2, dx dy, dy^2/2), dalpha/dlogit = alpha (1 - o)
-        float acc[10];
-        acc[0] = -fmaf(cn.x, sgx, cn.y * dy * sga);
-        acc[1] = -fmaf(cn.y, sgx, cn.z * dy * sga);
-        acc[2] = -sgxx;  // x2 (the writer applies 1/2)
-        acc[3] = -dy * sgx;
-        acc[4] = -dy * dy * sga;  // x2
-        acc[5] = sz;
-        acc[6] = kParams ? (1.f - cn.w) * sga : 0.f;
-        acc[7] = sr;
-        acc[8] = sg;
-        acc[9] = sb;
-        const unsigned ball = __ballot_sync(0xffffffffu, any);
-        if (!ball) continue;
-        float *dst = a.grad2d + size_t(s_idx[j]) * kG2;
-        if (__popc(ball) <= 2) {  // few contributing lanes: write directly, skip the reduction
-          if (any) {
-            // grad2d record: (u, v, A, B), (C, p_z, logit, 0), (r, g, b, 0)
-            red_add_v4(dst, acc[0], acc[1], 0.5f * acc[2], acc[3]);
-            red_add_v4(dst + 4, 0.5f * acc[4], acc[5], acc[6], 0.f);
-            if (kParams) red_add_v4(dst + 8, acc[7], acc[8], acc[9], 0.f);
-          }
-          continue;
-        }
-        int idx;
-        bool writer;
-        const float tot = warp_reduce10(acc, idx, writer);
-        if (writer && (kParams || idx < 6)) {
-          const int off = idx < 7 ? idx : idx + 1;
-          atomicAdd(dst + off, (idx == 2 || idx == 4) ? 0.5f * tot : tot);
-        }
+        if (!__any_sync(0xffffffffu, pass[0] || pass[1] || pass[2] || pass[3])) continue;
+        bwd_entry<kParams>(s, e, pass, s_rgbz[j], s_conic[j], s_uv[j], pg.fpy, fx, a.grad2d + size_t(s_idx[j]) * kG2);
       }
     }
   }

@@ -2,16 +2,18 @@
 // of colour (Eq. 3), depth (Eq. 6) and accumulated alpha (P:133-141,
 // P:161-166; R11-R15).
 //
-// One CTA (4 warps) per 16x16 tile; each thread owns 2 pixels of a row
-// (raster_common.cuh).  The tile's depth-ordered list is staged in batches of
-// 128 records in shared memory (each thread gathers one: uv in fp64 ->
-// tile-local fp32 offsets (H2), the H2b coefficients, rgb and camera depth,
-// plus a conservative box of the entry's alpha >= 1/255 region).  A warp
-// skips entries whose box misses its 16x4 strip; otherwise the row terms of
-// the exponent are computed once per (thread, entry) and reused by the 2
-// pixels (2 FFMA + compare per pixel); ex2 and the blend run only for entries
-// that pass the exponent pre-test.  The CTA leaves as soon as all of its
-// pixels have terminated (T < 1e-4).
+// One CTA (4 warps) per 16x16 tile; each warp owns an 8x8 pixel block and
+// each thread 2 adjacent pixels of a row (raster_common.cuh).  The tile's
+// depth-ordered list is staged in batches of 128 records in shared memory
+// (each thread gathers one: uv in fp64 -> tile-local fp32 offsets (H2), the
+// H2b entry terms, rgb and camera depth, plus the set of warp blocks met by a
+// conservative box of the entry's alpha >= 1/255 region).  Every warp then
+// compacts the indices of the entries that meet its block into a hit list and
+// walks it: the row terms of the exponent are computed once per (thread,
+// entry) and the 2 pixels are evaluated as one fp32x2 pair (FFMA2); ex2 and
+// the branch-free blend (also FFMA2) run only for entries that pass the
+// exponent pre-test at some pixel of the warp.  The CTA leaves as soon as all
+// of its pixels have terminated (T < 1e-4).
 #include "raster_common.cuh"
 
 namespace gs {
@@ -28,33 +30,73 @@ struct FwdArgs {
   int32_t *n_contrib, *stats, *tile_work;
 };
 
-constexpr int kFPX = 2;  // pixels per thread in the forward
-using FG = Geo<kFPX>;
+constexpr int kFPX = 2;  // pixels per thread in the forward (one fp32x2 pair)
+using FG = Geo<kFPX, 8>;  // 4 warps, 8x8 pixel blocks
+
+// per-thread compositing state of its pixel pair
+struct FwdPix {
+  float2 T, c0, c1, c2, D, A;
+  bool live0, live1;
+  int last0, last1, ncon0, ncon1, term0, term1;
+};
+
+// One list entry at the pixel pair: alpha decision (R11) and the blend of
+// Eqs. 3, 6 and R14, branch-free (alpha = 0 leaves the state bit-identical).
+template <bool kStats>
+__device__ __forceinline__ void fwd_blend(FwdPix &s, float2 e, bool p0, bool p1, float4 c, int pos) {
+  float a0 = fminf(ex2_approx(e.x), kAlphaMax), a1 = fminf(ex2_approx(e.y), kAlphaMax);
+  const bool q0 = p0 && a0 >= kAlphaMin, q1 = p1 && a1 >= kAlphaMin;  // skip (R11)
+  a0 = q0 ? a0 : 0.f;
+  a1 = q1 ? a1 : 0.f;
+  s.last0 = q0 ? pos : s.last0;
+  s.last1 = q1 ? pos : s.last1;
+  const float2 wt = __fmul2_rn(make_float2(a0, a1), s.T);           // alpha_j T_j
+  s.c0 = __ffma2_rn(make_float2(c.x, c.x), wt, s.c0);               // Eq. 3
+  s.c1 = __ffma2_rn(make_float2(c.y, c.y), wt, s.c1);
+  s.c2 = __ffma2_rn(make_float2(c.z, c.z), wt, s.c2);
+  s.D = __ffma2_rn(make_float2(c.w, c.w), wt, s.D);                 // Eq. 6 (camera-frame z, R12)
+  s.A = __fadd2_rn(s.A, wt);                                        // R14
+  s.T = __ffma2_rn(make_float2(-a0, -a1), s.T, s.T);                // T_{j+1} = T_j (1 - alpha_j)
+  s.live0 = s.T.x >= kTEps;
+  s.live1 = s.T.y >= kTEps;
+  if (kStats) {
+    s.ncon0 += q0;
+    s.ncon1 += q1;
+    s.term0 = (q0 && !s.live0) ? pos : s.term0;  // include, then stop (R11)
+    s.term1 = (q1 && !s.live1) ? pos : s.term1;
+  }
+}
 
 template <bool kStats>
 __global__ void __launch_bounds__(FG::kThreads) k_render_fwd(FwdArgs a) {
-  __shared__ float2 s_uv[kBatch];
-  __shared__ float4 s_coef[kBatch];
+  // slot kBatch of s_p / s_q is a sentinel entry whose exponent is -inf
+  __shared__ float4 s_p[kBatch + 1];
+  __shared__ float2 s_q[kBatch + 1];
   __shared__ float4 s_rgbz[kBatch];
   __shared__ unsigned char s_mask[kBatch];
+  __shared__ unsigned char s_list[FG::kWarps][kBatch + 2];
   const int tile = a.tile_order ? __ldg(a.tile_order + blockIdx.x) : int(blockIdx.x);
   const int tx = tile % a.TX, ty = tile / a.TX;
-  const PixGeom pg = pix_geom<kFPX>(tx, ty, a.H);
+  const int w = threadIdx.x >> 5;
+  const PixGeom pg = pix_geom<FG>(tx, ty, a.H);
   const double ox = double(tx * kTile), oy = double(ty * kTile);
   const int2 range = a.tile_range[tile];
-  float T[kFPX], c0[kFPX], c1[kFPX], c2[kFPX], D[kFPX], A[kFPX];
+  const float2 fx = make_float2(pg.fpx0, pg.fpx0 + 1.f);
+  if (threadIdx.x == 0) {
+    s_p[kBatch] = make_float4(0.f, 0.f, 0.f, 0.f);
+    s_q[kBatch] = make_float2(0.f, -INFINITY);
+  }
   // a pixel composites while T >= 1e-4 (include, then stop: T < 1e-4 happens
   // exactly at the stopping entry); pixels outside the image start with T = 0
-  int last[kFPX], ncon[kFPX], term[kFPX];
-#pragma unroll
-  for (int k = 0; k < kFPX; ++k) {
-    T[k] = (pg.row_in && pg.px0 + k < a.W) ? 1.f : 0.f;
-    c0[k] = c1[k] = c2[k] = D[k] = A[k] = 0.f;
-    last[k] = ncon[k] = 0;
-    term[k] = range.y - range.x;  // entries scanned if the pixel never terminates
-  }
+  FwdPix s;
+  s.T = make_float2((pg.row_in && pg.px0 < a.W) ? 1.f : 0.f, (pg.row_in && pg.px0 + 1 < a.W) ? 1.f : 0.f);
+  s.c0 = s.c1 = s.c2 = s.D = s.A = make_float2(0.f, 0.f);
+  s.live0 = s.T.x >= kTEps;
+  s.live1 = s.T.y >= kTEps;
+  s.last0 = s.last1 = s.ncon0 = s.ncon1 = 0;
+  s.term0 = s.term1 = range.y - range.x;  // entries scanned if the pixel never terminates
   for (int start = range.x; start < range.y; start += kBatch) {
-    if (__syncthreads_count(T[0] >= kTEps || T[1] >= kTEps) == 0) break;
+    if (__syncthreads_count(s.live0 || s.live1) == 0) break;
     static_assert(FG::kRecPerThread == 1, "one staged record per thread");
     {
       const int k = start + threadIdx.x;
@@ -63,55 +105,33 @@ __global__ void __launch_bounds__(FG::kThreads) k_render_fwd(FwdArgs a) {
         const double2 u = __ldg(a.uv + g);
         const float4 cf = __ldg(a.coef + g);
         const float ul = float(u.x - ox), vl = float(u.y - oy);
-        s_uv[threadIdx.x] = make_float2(ul, vl);
-        s_coef[threadIdx.x] = cf;
+        const EntryTerms et = entry_terms(cf, ul, vl);
+        s_p[threadIdx.x] = et.p;
+        s_q[threadIdx.x] = et.q;
         s_rgbz[threadIdx.x] = __ldg(a.rgbz + g);
-        s_mask[threadIdx.x] = (unsigned char)box_strip_mask<kFPX>(entry_box(cf, ul, vl));
+        s_mask[threadIdx.x] = (unsigned char)box_block_mask<FG>(entry_box(cf, ul, vl));
       }
     }
     __syncthreads();
-    unsigned hits[kBatch / 32];
-    warp_hits(s_mask, min(kBatch, range.y - start), hits);
-    // walk this warp's hits in list order; entries that miss its strip cannot
-    // pass the exponent pre-test at any of its pixels (no decision changes).
-    // The blend is branch-free: a pixel that does not composite uses alpha = 0,
-    // which leaves C, D, A and T bit-identical.
-#pragma unroll
-    for (int h = 0; h < kBatch / 32; ++h) {
-      unsigned bits = hits[h];
-      if (bits && !__any_sync(0xffffffffu, T[0] >= kTEps || T[1] >= kTEps)) break;
-      while (bits) {
-        const int j = h * 32 + __ffs(bits) - 1;
-        bits &= bits - 1;
-        const float2 ul = s_uv[j];
-        const RowTerms rt = row_terms(s_coef[j], ul.x, ul.y, pg.fpy);
-        float e[kFPX];
-        bool pass[kFPX];
-#pragma unroll
-        for (int k = 0; k < kFPX; ++k) {
-          e[k] = pixel_exponent(rt, pg.fpx0 + float(k));
-          pass[k] = e[k] >= kExpSkip && T[k] >= kTEps;
-        }
-        if (!__any_sync(0xffffffffu, pass[0] || pass[1])) continue;
-        const float4 c = s_rgbz[j];
-        const int pos = start - range.x + j + 1;
-#pragma unroll
-        for (int k = 0; k < kFPX; ++k) {
-          float al = fminf(ex2_approx(e[k]), kAlphaMax);
-          al = (pass[k] && al >= kAlphaMin) ? al : 0.f;  // skip (R11)
-          const float w = __fmul_rn(al, T[k]);           // alpha_j T_j
-          c0[k] = __fmaf_rn(c.x, w, c0[k]);              // Eq. 3
-          c1[k] = __fmaf_rn(c.y, w, c1[k]);
-          c2[k] = __fmaf_rn(c.z, w, c2[k]);
-          D[k] = __fmaf_rn(c.w, w, D[k]);                // Eq. 6 (camera-frame z, R12)
-          A[k] = __fadd_rn(A[k], w);                     // R14
-          T[k] = __fmul_rn(T[k], __fsub_rn(1.f, al));
-          last[k] = al > 0.f ? pos : last[k];
-          if (kStats) {
-            ncon[k] += al > 0.f;
-            term[k] = (al > 0.f && T[k] < kTEps) ? pos : term[k];  // include, then stop (R11)
-          }
-        }
+    // walk this warp's hits in list order, two per step (their exponents are
+    // independent; the blends stay in order).  Entries that miss the warp's
+    // block cannot pass the exponent pre-test at any of its pixels (no
+    // decision changes); list[nh] is the sentinel.
+    unsigned char *list = s_list[w];
+    const int nh = warp_hit_list(s_mask, min(kBatch, range.y - start), list, kBatch);
+    const int base = start - range.x + 1;
+    for (int k = 0; k < nh; k += 2) {
+      if ((k & 31) == 0 && !__any_sync(0xffffffffu, s.live0 || s.live1)) break;
+      const int ja = list[k], jb = list[k + 1];
+      const float2 ea = pair_exponent(row_terms(s_p[ja], s_q[ja], pg.fpy), fx);
+      const float2 eb = pair_exponent(row_terms(s_p[jb], s_q[jb], pg.fpy), fx);
+      {
+        const bool p0 = s.live0 && ea.x >= kExpSkip, p1 = s.live1 && ea.y >= kExpSkip;
+        if (__any_sync(0xffffffffu, p0 || p1)) fwd_blend<kStats>(s, ea, p0, p1, s_rgbz[ja], base + ja);
+      }
+      {
+        const bool p0 = s.live0 && eb.x >= kExpSkip, p1 = s.live1 && eb.y >= kExpSkip;
+        if (__any_sync(0xffffffffu, p0 || p1)) fwd_blend<kStats>(s, eb, p0, p1, s_rgbz[jb], base + jb);
       }
     }
   }
@@ -119,7 +139,7 @@ __global__ void __launch_bounds__(FG::kThreads) k_render_fwd(FwdArgs a) {
     __shared__ int s_work;
     if (threadIdx.x == 0) s_work = 0;
     __syncthreads();
-    int wk = last[0] + last[1];
+    int wk = s.last0 + s.last1;
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) wk += __shfl_xor_sync(0xffffffffu, wk, o);
     if ((threadIdx.x & 31) == 0) atomicAdd(&s_work, wk);
@@ -128,20 +148,23 @@ __global__ void __launch_bounds__(FG::kThreads) k_render_fwd(FwdArgs a) {
   }
   if (!pg.row_in) return;
   const size_t HW = size_t(a.W) * a.H;
+  const float cc0[2] = {s.c0.x, s.c0.y}, cc1[2] = {s.c1.x, s.c1.y}, cc2[2] = {s.c2.x, s.c2.y},
+              DD[2] = {s.D.x, s.D.y}, AA[2] = {s.A.x, s.A.y}, TT[2] = {s.T.x, s.T.y};
+  const int ll[2] = {s.last0, s.last1}, nc[2] = {s.ncon0, s.ncon1}, tm[2] = {s.term0, s.term1};
 #pragma unroll
   for (int k = 0; k < kFPX; ++k) {
     if (pg.px0 + k >= a.W) break;
     const size_t q = size_t(pg.py) * a.W + pg.px0 + k;
-    a.color[q] = c0[k];
-    a.color[HW + q] = c1[k];
-    a.color[2 * HW + q] = c2[k];
-    a.depth[q] = D[k];
-    a.alpha[q] = A[k];
-    a.T_final[q] = T[k];
-    a.n_contrib[q] = last[k];
+    a.color[q] = cc0[k];
+    a.color[HW + q] = cc1[k];
+    a.color[2 * HW + q] = cc2[k];
+    a.depth[q] = DD[k];
+    a.alpha[q] = AA[k];
+    a.T_final[q] = TT[k];
+    a.n_contrib[q] = ll[k];
     if (kStats) {
-      a.stats[q] = term[k];  // entries scanned = termination position or list length
-      a.stats[HW + q] = ncon[k];
+      a.stats[q] = tm[k];  // entries scanned = termination position or list length
+      a.stats[HW + q] = nc[k];
     }
   }
 }

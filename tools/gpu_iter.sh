@@ -1,0 +1,19 @@
+#!/bin/bash
+# Quick GPU iteration (on the box): parity tests, then a short bench with the
+# kernel-level numbers.   tools/gpu_iter.sh [pytest -k expr]
+mkdir -p gpurun_out
+if [ -n "$1" ]; then K="-k $1"; else K=""; fi
+timeout 900 python -m pytest tests -m gpu -x -q $K > gpurun_out/gpu_tests.log 2>&1
+echo "tests rc=$?"; tail -4 gpurun_out/gpu_tests.log
+timeout 300 python bench.py --steps 20 --warmup 5 --no-cpu-baseline ${BENCH_ARGS} > gpurun_out/bench.json 2> gpurun_out/bench.err
+echo "bench rc=$?"; tail -3 gpurun_out/bench.err
+python - <<'PY'
+import json
+d = json.load(open("gpurun_out/bench.json"))
+print("MP/s %.1f  ms/step %.3f  e2e %s" % (d["value"], d["ms_per_step"], d.get("e2e", {}).get("value")))
+ro = d["roofline_other"]
+for k in ("render_fwd_isolated", "render_bwd_pixels_isolated"):
+    print("%-28s %.1f us  frac %.3f" % (k, ro[k]["ms_per_launch"] * 1e3, ro[k]["frac"]))
+print("roofline(in-step) frac %.3f  %.1f us" % (d["roofline"]["frac"], d["roofline"]["ms_per_launch"] * 1e3))
+if "tracking" in d: print("tracking it/s %.1f" % d["tracking"]["value"])
+PY
