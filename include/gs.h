@@ -141,8 +141,9 @@ int gs_check_device(int device, int *sm_count);
 int32_t gs_num_tiles(gs_camera cam);
 
 /* Workspace bytes gs_bin_sort needs for n Gaussians, a pair capacity and
- * camera `cam` (0 if unsupported: > 4 radix passes of depth bits, > 2^21 tiles,
- * or n / capacity >= 2^30). */
+ * camera `cam`: ~12 bytes per pair of capacity (scratch of the exact sort of
+ * long tile lists) + 12 bytes per tile.  0 if unsupported (> 2^21 tiles or
+ * capacity >= 2^31 - 1). */
 size_t gs_binsort_workspace_bytes(int32_t n, int64_t capacity, gs_camera cam);
 
 /* Workspace bytes gs_loss needs for camera `cam`. */
@@ -209,8 +210,9 @@ int gs_bin_sort(gs_proj pr, int32_t n, gs_camera cam, void *ws, size_t ws_bytes,
  *
  * Per pixel over its tile's ordered list: Delta = (u - i, v - j);
  * alpha = min(o exp(-1/2 Delta^T conic Delta), 0.999); skip if alpha < 1/255;
- * C += c alpha T; D += p_z alpha T; A += alpha T; T *= (1 - alpha); stop
- * after compositing an entry that leaves T < 1e-4.  Background is zero.
+ * C += c alpha T; D += p_z alpha T; A += alpha T; T <- T - alpha T (one
+ * fused rounding); stop after compositing an entry that leaves T < 1e-4.
+ * Background is zero.
  *   tile_order (device, nullable) from gs_bin_sort: launch order of the tiles
  *   color     (device) [3][H][W]    depth, alpha, T_final (device) [H][W]
  *   n_contrib (device) [H][W] int32 (position in the tile list of the last

@@ -2,22 +2,30 @@
 // ("m ordered Gaussians"; R10).
 //
 // Result = every (tile, Gaussian) pair ordered by the composite key
-// (tile asc, fp32 depth asc, Gaussian id asc), computed as two stable LSD
-// radix sorts that together equal one sort on that key:
-//   1. the Gaussians by depth bits (z_near-relative, 9-bit digits; invisible
-//      Gaussians get an all-ones key and land after the Nv visible ones; the
-//      input order is the Gaussian id, so equal depths stay in id order);
-//   2. the (tile, depth rank) pairs, emitted in depth-rank order, by the tile
-//      bits only (7-bit digits): stability keeps rank (= depth, id) order
-//      inside every tile.
-// Every radix pass is ONE "onesweep" kernel: blocks take tickets in launch
-// order, rank their keys per warp with ballot-sliced peer masks (MATCH.ANY is
-// ~100x slower on this part), publish per-digit block counts and find their
-// global offsets by decoupled look-back over the preceding blocks.  The global
-// digit histograms are known up front: depth digits from the prep kernel,
-// tile digits from the per-tile pair counts (a 2-D difference array of the
-// tile rects, 4 updates per Gaussian).  Everything is integer arithmetic: the
-// output is bit-deterministic.
+// (tile asc, fp32 depth asc, Gaussian id asc).  Built tile by tile, with no
+// global sort and no pass whose blocks wait on each other:
+//   1. k_bin_prep: per-tile pair counts from a 2-D difference array of the
+//      tile rects (4 shared-memory updates per visible Gaussian, merged into
+//      one global array per block);
+//   2. k_tile_counts (one CTA): 2-D prefix -> counts -> tile ranges (scan),
+//      the capacity check, per-tile write cursors and the heaviest-first
+//      launch order;
+//   3. k_emit: every visible Gaussian appends its id to the segment of each
+//      tile of its rect (block-aggregated: shared-memory counts, one global
+//      cursor reservation per (block, tile), warp-balanced pair expansion);
+//      the order inside a segment is arbitrary at this point;
+//   4. k_tile_sort: one CTA per tile sorts its segment in shared memory in
+//      one pass: a counting sort on the top 11 bits of (depth bits - tile
+//      minimum), then every entry ranked inside its bucket (~n / 2048
+//      entries) on the exact key (depth bits, id).  Segments longer than 4096
+//      entries, or with a bucket of more than 128 (a dense cluster of depths
+//      next to a far outlier), are left to k_tile_sort_big: an exact two-key
+//      stable LSD radix sort (id digits, then depth digits; 9-bit digits,
+//      warp ranks from ballot-sliced peer masks) chunk by chunk over global
+//      memory.
+// Everything is integer arithmetic on the fp32 depth bits (positive floats
+// order as their bit patterns): the output is bit-deterministic whatever the
+// order of the atomics in step 3.
 #include <algorithm>
 #include <cstring>
 
@@ -25,27 +33,25 @@
 
 namespace gs {
 
-constexpr int kOSThreads = 256;  // onesweep block: 8 warps
-constexpr int kDepthBits = 9;    // depth digit width
-constexpr int kTileBits = 7;     // tile digit width
-constexpr int kDepthItems = 8;   // keys per thread (2048 per block)
-constexpr int kPairItems = 8;    // pairs per thread (2048 per block)
-constexpr int kScanItems1 = 16;  // 1-pass scan: 4096 values per block
-constexpr uint32_t kFlagA = 1u << 30, kFlagP = 2u << 30, kValMask = (1u << 30) - 1;
-constexpr int kMaxDepthPasses = 4, kMaxTilePasses = 3;
+constexpr int kSortThreads = 256;  // k_tile_sort CTA: 8 warps
+constexpr int kSortWarps = kSortThreads / 32;
+constexpr int kSortItems = 16;                          // keys per thread
+constexpr int kChunk = kSortThreads * kSortItems;       // 4096 keys sorted in shared memory at once
+constexpr int kDigitBits = 9;
+constexpr int kDigits = 1 << kDigitBits;
+constexpr int kBucketBits = 11;
+constexpr int kBuckets = 1 << kBucketBits;  // k_tile_sort counting-sort buckets
+constexpr int kBucketThreads = 256;  // k_tile_sort CTA
+constexpr int kMaxBucket = 128;     // fuller buckets -> exact two-key sort (k_tile_sort_big)
+constexpr int kEmitThreads = 1024;
+constexpr int kEmitPer = 2;        // Gaussians per k_emit thread
+constexpr int kBigBlocks = 148;    // k_tile_sort_big grid (grid-stride over the long tiles)
 
 struct SortLayout {
   int n, T, TX, TY;
-  int dpasses, tpasses;
-  uint32_t zbase, kinvis;
-  int nblk_d, nblk_p, nblk_s;
   int64_t capacity;
-  // zeroed region (one memset per call)
-  size_t diff, st_s, tickets, misc, zero_end;
-  // per-pass digit-major count matrices [D][nblk] (written in full by the upsweeps)
-  size_t cnt_d, cnt_p, st_cd, st_cp;
-  // other
-  size_t dkeys_a, dkeys_b, dvals_a, dvals_b, pkeys_a, pkeys_b, pvals_a, pvals_b, total;
+  size_t diff, misc, zero_end;  // zeroed region (one memset per call)
+  size_t cursor, slow, key_a, key_b, val_b, total;
 };
 
 static size_t align_up(size_t x) { return (x + 255) & ~size_t(255); }
@@ -56,53 +62,22 @@ static bool make_layout(int32_t n, int64_t capacity, const gs_camera &cam, SortL
   L.TX = tiles_x(cam);
   L.TY = tiles_y(cam);
   L.T = L.TX * L.TY;
-  int tbits = 1;
-  while ((1 << tbits) < L.T) ++tbits;
-  L.tpasses = (tbits + kTileBits - 1) / kTileBits;
-  // positive floats order as their bit patterns; keys are bits(z) - bits(z_near)
-  uint32_t zb, ze;
-  float zn = cam.z_near, zf = cam.z_far;
-  memcpy(&zb, &zn, 4);
-  memcpy(&ze, &zf, 4);
-  L.zbase = zb;
-  const uint64_t span = uint64_t(ze - zb) + 2;  // visible keys <= ze - zb < the all-ones key
-  int bits = 1;
-  while ((uint64_t(1) << bits) < span) ++bits;
-  L.dpasses = (bits + kDepthBits - 1) / kDepthBits;
-  if (L.dpasses > kMaxDepthPasses || L.tpasses > kMaxTilePasses || L.T > (1 << 21)) return false;
-  L.kinvis = uint32_t((uint64_t(1) << (kDepthBits * L.dpasses)) - 1);
-  if (capacity >= int64_t(kValMask) || int64_t(n) >= int64_t(kValMask)) return false;
-  L.nblk_d = std::max(1, (n + kOSThreads * kDepthItems - 1) / (kOSThreads * kDepthItems));
-  L.nblk_p = int(std::max<int64_t>(1, (capacity + kOSThreads * kPairItems - 1) / (kOSThreads * kPairItems)));
-  L.nblk_s = std::max(1, (n + kOSThreads * kScanItems1 - 1) / (kOSThreads * kScanItems1));
+  if (L.T > (1 << 21) || capacity >= (int64_t(1) << 31) - 1) return false;
   size_t off = 0;
   auto take = [&](size_t bytes) {
     size_t o = off;
     off = align_up(off + bytes);
     return o;
   };
-  const size_t Dd = size_t(1) << kDepthBits, Dt = size_t(1) << kTileBits;
-  const size_t ncd = Dd * L.nblk_d, ncp = Dt * L.nblk_p;
-  const size_t sbd = (ncd + kOSThreads * kScanItems1 - 1) / (kOSThreads * kScanItems1);
-  const size_t sbp = (ncp + kOSThreads * kScanItems1 - 1) / (kOSThreads * kScanItems1);
   L.diff = take(4 * size_t(L.TX + 1) * (L.TY + 1));
-  L.st_s = take(4 * size_t(L.nblk_s));
-  L.st_cd = take(4 * sbd * L.dpasses);
-  L.st_cp = take(4 * sbp * L.tpasses);
-  L.tickets = take(4 * 16);
-  L.misc = take(64);  // [0] nvis, [1] P, [2] overflow
+  L.misc = take(64);  // [1] P, [2] overflow, [3] slow-list length
   L.zero_end = off;
-  L.cnt_d = take(4 * ncd);
-  L.cnt_p = take(4 * ncp);
-  const size_t nn = size_t(n > 0 ? n : 1), cc = size_t(capacity > 0 ? capacity : 1);
-  L.dkeys_a = take(4 * nn);
-  L.dkeys_b = take(4 * nn);
-  L.dvals_a = take(4 * nn);
-  L.dvals_b = take(4 * nn);
-  L.pkeys_a = take(4 * cc);
-  L.pkeys_b = take(4 * cc);
-  L.pvals_a = take(4 * cc);
-  L.pvals_b = take(4 * cc);
+  L.cursor = take(4 * size_t(L.T));
+  L.slow = take(4 * size_t(L.T));
+  const size_t cc = size_t(capacity > 0 ? capacity : 1);
+  L.key_a = take(4 * cc);  // scratch of the chunked (long-segment) sort
+  L.key_b = take(4 * cc);
+  L.val_b = take(4 * cc);
   L.total = off;
   return true;
 }
@@ -139,235 +114,57 @@ __device__ uint32_t block_excl_scan(uint32_t v, uint32_t *sh /* >= 33 */, uint32
   return r;
 }
 
-// Lanes of `act` whose key agrees with this lane's in its low kBits bits:
-// one ballot per bit.  Every lane of the warp must call it.
-template <int kBits>
-__device__ __forceinline__ unsigned peer_mask(unsigned act, uint32_t key) {
+// Lanes of `act` whose digit equals this lane's: one ballot per digit bit.
+// Every lane of the warp must call it.
+__device__ __forceinline__ unsigned peer_mask(unsigned act, uint32_t d) {
   unsigned m = act;
 #pragma unroll
-  for (int b = 0; b < kBits; ++b) {
-    const bool bit = (key >> b) & 1u;
+  for (int b = 0; b < kDigitBits; ++b) {
+    const bool bit = (d >> b) & 1u;
     const unsigned bb = __ballot_sync(0xffffffffu, bit);
     m &= bit ? bb : ~bb;
   }
   return m;
 }
 
-__device__ __forceinline__ uint32_t ld_volatile(const uint32_t *p) {
-  return *reinterpret_cast<const volatile uint32_t *>(p);
-}
-
-__device__ __forceinline__ void st_volatile(uint32_t *p, uint32_t v) { *reinterpret_cast<volatile uint32_t *>(p) = v; }
-
-// Decoupled look-back, one warp: publish this block's aggregate, then read the
-// status words of up to 32 predecessors at once; the nearest inclusive prefix
-// (flag P) ends the walk, aggregates (flag A) in front of it are added, and a
-// window containing an unpublished word (0) is re-read.  Returns the
-// exclusive prefix of `count` on every lane.
-__device__ __forceinline__ uint32_t warp_look_back(uint32_t *status, int bid, uint32_t count) {
-  const int lane = threadIdx.x & 31;
-  if (bid == 0) {
-    if (lane == 0) st_volatile(status, kFlagP | count);
-    return 0;
-  }
-  if (lane == 0) st_volatile(status + bid, kFlagA | count);
-  uint32_t excl = 0;
-  int top = bid - 1;  // newest predecessor of the current window
-  while (true) {
-    const int j = top - lane;
-    const uint32_t sv = j >= 0 ? ld_volatile(status + j) : kFlagP;  // virtual P before block 0
-    const unsigned pmask = __ballot_sync(0xffffffffu, sv & kFlagP);
-    const unsigned zmask = __ballot_sync(0xffffffffu, !(sv & (kFlagA | kFlagP)));
-    const int first_p = pmask ? __ffs(pmask) - 1 : 32;
-    const unsigned upto = first_p == 32 ? 0xffffffffu : (first_p == 31 ? 0xffffffffu : ((2u << first_p) - 1u));
-    if (zmask & upto) continue;  // someone in front of the nearest P has not published yet
-    uint32_t v = (lane <= first_p && j >= 0) ? (sv & kValMask) : 0u;
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-    excl += v;
-    if (first_p < 32) break;
-    top -= 32;
-  }
-  if (lane == 0) st_volatile(status + bid, kFlagP | (excl + count));
-  return excl;
-}
-
 // ---------------------------------------------------------------------------
-// Single-pass exclusive scan (in place) with decoupled look-back; total out.
+// Step 1: tile-rect difference array (per-block in shared memory, merged with
+// one global atomic per nonzero cell).
 
-__global__ void __launch_bounds__(kOSThreads) k_scan_1pass(uint32_t *a, int64_t L, uint32_t *status, uint32_t *ticket,
-                                                           uint32_t *total) {
-  __shared__ uint32_t sh[33];
-  __shared__ uint32_t s_bid, s_prefix;
-  if (threadIdx.x == 0) s_bid = atomicAdd(ticket, 1u);
-  __syncthreads();
-  const int bid = int(s_bid);
-  const int64_t base = int64_t(bid) * kOSThreads * kScanItems1 + int64_t(threadIdx.x) * kScanItems1;
-  uint32_t v[kScanItems1];
-  uint32_t s = 0;
-#pragma unroll
-  for (int k = 0; k < kScanItems1; ++k) {
-    v[k] = base + k < L ? a[base + k] : 0u;
-    s += v[k];
-  }
-  uint32_t tot;
-  uint32_t ex = block_excl_scan(s, sh, tot);
-  if (threadIdx.x < 32) {
-    const uint32_t pre = warp_look_back(status, bid, tot);
-    if (threadIdx.x == 0) {
-      s_prefix = pre;
-      if (bid == int(gridDim.x) - 1 && total) *total = pre + tot;
-    }
-  }
-  __syncthreads();
-  ex += s_prefix;
-#pragma unroll
-  for (int k = 0; k < kScanItems1; ++k) {
-    if (base + k < L) a[base + k] = ex;
-    ex += v[k];
-  }
-}
-
-// ---------------------------------------------------------------------------
-// Depth prep: radix keys of all Gaussians and the tile-rect difference array
-// (per-block in shared memory, merged with one global atomic per nonzero cell).
-
-struct PrepArgs {
-  const float *depth;
-  const int32_t *tiles_touched;
-  const short4 *rect;
-  int n, TX, TY;
-  uint32_t zbase, kinvis;
-  uint32_t *keys, *vals, *diff, *nvis;
-};
-
-__global__ void __launch_bounds__(kOSThreads) k_depth_prep(PrepArgs a) {
+__global__ void __launch_bounds__(256) k_bin_prep(const int32_t *__restrict__ tiles_touched,
+                                                  const short4 *__restrict__ rect, int n, int TX, int TY,
+                                                  uint32_t *diff) {
   extern __shared__ uint32_t s_diff[];
-  const int W1 = a.TX + 1, cells = W1 * (a.TY + 1);
+  const int W1 = TX + 1, cells = W1 * (TY + 1);
   for (int i = threadIdx.x; i < cells; i += blockDim.x) s_diff[i] = 0;
   __syncthreads();
-  uint32_t vis = 0;
-  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < a.n; i += gridDim.x * blockDim.x) {
-    uint32_t key = a.kinvis;
-    if (__ldg(a.tiles_touched + i) > 0) {
-      key = __float_as_uint(__ldg(a.depth + i)) - a.zbase;
-      ++vis;
-      // +1 over the rect [x0, x1] x [y0, y1]
-      const short4 r = __ldg(a.rect + i);
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    if (__ldg(tiles_touched + i) > 0) {  // +1 over the rect [x0, x1] x [y0, y1]
+      const short4 r = __ldg(rect + i);
       atomicAdd(s_diff + r.y * W1 + r.x, 1u);
       atomicAdd(s_diff + r.y * W1 + r.z + 1, 0xffffffffu);
       atomicAdd(s_diff + (r.w + 1) * W1 + r.x, 0xffffffffu);
       atomicAdd(s_diff + (r.w + 1) * W1 + r.z + 1, 1u);
     }
-    a.keys[i] = key;
-    a.vals[i] = uint32_t(i);
   }
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) vis += __shfl_xor_sync(0xffffffffu, vis, o);
-  if ((threadIdx.x & 31) == 0 && vis) atomicAdd(a.nvis, vis);
   __syncthreads();
   for (int i = threadIdx.x; i < cells; i += blockDim.x) {
     const uint32_t c = s_diff[i];
-    if (c) atomicAdd(a.diff + i, c);
+    if (c) atomicAdd(diff + i, c);
   }
 }
 
 // ---------------------------------------------------------------------------
-// One stable LSD radix pass = upsweep (per-block digit counts, digit-major) +
-// one-pass exclusive scan of the count matrix + downsweep (stable rank and
-// scatter).  Block = 8 warps x 32 lanes x ITEMS keys; warp w owns the keys
-// [base + 32 ITEMS w, +32 ITEMS), walked in ITEMS rounds of 32.
-
-struct RSArgs {
-  const uint32_t *keys_in, *vals_in;
-  uint32_t *keys_out, *vals_out;
-  const uint32_t *n_dev;  // element count (device), or nullptr -> n
-  int64_t n;
-  int shift, nblk;
-  uint32_t *counts;          // [D][nblk]
-  const int32_t *tiles_out;  // depth sort, last pass: write tiles_touched[val] as key
-  const uint32_t *skip;      // optional flag: skip the pass when *skip != 0
-};
-
-template <int RB, int ITEMS>
-__global__ void __launch_bounds__(kOSThreads) k_rs_upsweep(RSArgs a) {
-  constexpr int D = 1 << RB;
-  __shared__ uint32_t h[D];
-  for (int d = threadIdx.x; d < D; d += blockDim.x) h[d] = 0;
-  __syncthreads();
-  const bool skip = a.skip && *a.skip;
-  const int64_t n = skip ? 0 : (a.n_dev ? int64_t(*a.n_dev) : a.n);
-  const int64_t base = int64_t(blockIdx.x) * (kOSThreads * ITEMS);
-#pragma unroll
-  for (int r = 0; r < ITEMS; ++r) {
-    const int64_t i = base + r * kOSThreads + threadIdx.x;
-    if (i < n) atomicAdd(&h[(a.keys_in[i] >> a.shift) & (D - 1)], 1u);
-  }
-  __syncthreads();
-  for (int d = threadIdx.x; d < D; d += blockDim.x) a.counts[size_t(d) * a.nblk + blockIdx.x] = h[d];
-}
-
-template <int RB, int ITEMS>
-__global__ void __launch_bounds__(kOSThreads) k_rs_downsweep(RSArgs a) {
-  constexpr int D = 1 << RB, W = kOSThreads / 32;
-  __shared__ uint32_t s_wc[W][D];
-  if (a.skip && *a.skip) return;
-  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  for (int i = threadIdx.x; i < W * D; i += blockDim.x) (&s_wc[0][0])[i] = 0;
-  __syncthreads();
-  const int64_t n = a.n_dev ? int64_t(*a.n_dev) : a.n;
-  const int64_t base = int64_t(blockIdx.x) * (kOSThreads * ITEMS) + int64_t(w) * (32 * ITEMS);
-  uint32_t key[ITEMS], val[ITEMS], rank[ITEMS];
-#pragma unroll
-  for (int r = 0; r < ITEMS; ++r) {
-    const int64_t i = base + r * 32 + lane;
-    key[r] = i < n ? a.keys_in[i] : 0xffffffffu;
-    val[r] = i < n ? a.vals_in[i] : 0u;
-  }
-  // per-warp stable ranks (rounds in input order, lanes in input order)
-#pragma unroll
-  for (int r = 0; r < ITEMS; ++r) {
-    const bool ok = base + r * 32 + lane < n;
-    const unsigned act = __ballot_sync(0xffffffffu, ok);
-    const uint32_t d = (key[r] >> a.shift) & (D - 1);
-    const unsigned peers = peer_mask<RB>(act, d);
-    const uint32_t before = ok ? s_wc[w][d] : 0u;
-    rank[r] = before + __popc(peers & lanemask_lt());
-    __syncwarp();
-    if (ok && lane == 31 - __clz(peers)) s_wc[w][d] = before + __popc(peers);
-    __syncwarp();
-  }
-  __syncthreads();
-  // per digit: exclusive warp prefixes + the block's global offset
-  for (int d = threadIdx.x; d < D; d += kOSThreads) {
-    uint32_t run = a.counts[size_t(d) * a.nblk + blockIdx.x];
-#pragma unroll
-    for (int ww = 0; ww < W; ++ww) {
-      const uint32_t c = s_wc[ww][d];
-      s_wc[ww][d] = run;
-      run += c;
-    }
-  }
-  __syncthreads();
-#pragma unroll
-  for (int r = 0; r < ITEMS; ++r) {
-    if (base + r * 32 + lane >= n) continue;
-    const uint32_t d = (key[r] >> a.shift) & (D - 1);
-    const uint32_t pos = s_wc[w][d] + rank[r];
-    a.keys_out[pos] = a.tiles_out ? uint32_t(__ldg(a.tiles_out + val[r])) : key[r];
-    a.vals_out[pos] = val[r];
-  }
-}
-
-// ---------------------------------------------------------------------------
-// Per-tile pair counts (2-D prefix of the difference array, in shared
-// memory), tile ranges, P and the capacity check, heaviest-first tile order.
+// Step 2: per-tile pair counts (2-D prefix of the difference array, in shared
+// memory), tile ranges, write cursors, P and the capacity check,
+// heaviest-first tile order.
 
 struct TileArgs {
   const uint32_t *diff;  // (TY+1) x (TX+1)
   int TX, TY, T;
   int64_t capacity;
   int32_t *tile_range, *tile_order;
+  uint32_t *cursor;
   int64_t *n_pairs;
   uint32_t *misc;  // [1] P, [2] overflow
   gs_counters *cnt;
@@ -421,6 +218,7 @@ __global__ void __launch_bounds__(1024) k_tile_counts(TileArgs a) {
     if (t < a.T) {
       const uint32_t c = s_c[(t / a.TX) * W1 + t % a.TX];
       reinterpret_cast<int2 *>(a.tile_range)[t] = over ? make_int2(0, 0) : make_int2(int(ex), int(ex + c));
+      a.cursor[t] = ex;
       ex += c;
     }
   }
@@ -455,70 +253,439 @@ __global__ void __launch_bounds__(1024) k_tile_counts(TileArgs a) {
 }
 
 // ---------------------------------------------------------------------------
-// Pair emission in depth-rank order: one item per warp step, lanes = its tiles.
+// Step 3: pair emission into the tile segments (unordered inside a segment).
+// Per block of kEmitThreads * kEmitPer Gaussians: the block's per-tile counts
+// from a shared-memory 2-D difference array (4 updates per Gaussian), one
+// global cursor reservation per (block, tile), then the pairs: every warp
+// expands the rects of 32 Gaussians into one flat list of (Gaussian, tile)
+// pairs walked 32 at a time (a lane finds its Gaussian by a binary search of
+// the warp's inclusive prefix of tile counts), so lanes stay busy whatever
+// the mix of rect sizes.
 
-__global__ void __launch_bounds__(kOSThreads) k_emit_pairs(const uint32_t *__restrict__ svals,
-                                                           const uint32_t *__restrict__ poff,
-                                                           const short4 *__restrict__ rect,
-                                                           const uint32_t *__restrict__ nvis,
-                                                           const uint32_t *__restrict__ overflow, int TX,
-                                                           uint32_t *pkeys, uint32_t *pvals) {
-  if (*overflow) return;
-  const int nv = int(*nvis);
+__global__ void __launch_bounds__(kEmitThreads) k_emit(const int32_t *__restrict__ tiles_touched,
+                                                       const short4 *__restrict__ rect, int n, int TX, int TY,
+                                                       uint32_t *cursor, const uint32_t *__restrict__ misc,
+                                                       int32_t *ids) {
+  extern __shared__ uint32_t s_e[];  // [(TY+1)(TX+1)] diff -> counts -> cursors, [T] bases
+  if (misc[2]) return;               // overflow: leave sorted_idx untouched
+  const int W1 = TX + 1, cells = W1 * (TY + 1), T = TX * TY;
+  uint32_t *s_cur = s_e, *s_base = s_e + cells;
   const int lane = threadIdx.x & 31;
-  const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  const int k0 = warp * 32;
-  if (k0 >= nv) return;
-  const int k = k0 + lane;
-  int rxy = 0, wdt = 1, nt = 0;
-  uint32_t po = 0, magic = 0;
-  if (k < nv) {
-    const short4 r = __ldg(rect + __ldg(svals + k));
-    wdt = r.z - r.x + 1;
-    nt = wdt * (r.w - r.y + 1);
-    rxy = (int(r.x) & 0xffff) | (int(r.y) << 16);
-    po = __ldg(poff + k);
-    magic = wdt > 1 ? uint32_t((0x100000000ull + uint64_t(wdt) - 1) / uint64_t(wdt)) : 0u;
+  for (int c = threadIdx.x; c < cells; c += blockDim.x) s_cur[c] = 0;
+  __syncthreads();
+  short4 r[kEmitPer];
+#pragma unroll
+  for (int k = 0; k < kEmitPer; ++k) {
+    const int i = (blockIdx.x * kEmitPer + k) * kEmitThreads + threadIdx.x;
+    const bool vis = i < n && __ldg(tiles_touched + i) > 0;
+    r[k] = vis ? __ldg(rect + i) : make_short4(0, 0, -1, -1);
+    if (vis) {
+      atomicAdd(s_cur + r[k].y * W1 + r[k].x, 1u);
+      atomicAdd(s_cur + r[k].y * W1 + r[k].z + 1, 0xffffffffu);
+      atomicAdd(s_cur + (r[k].w + 1) * W1 + r[k].x, 0xffffffffu);
+      atomicAdd(s_cur + (r[k].w + 1) * W1 + r[k].z + 1, 1u);
+    }
   }
-  const int cnt = min(32, nv - k0);
-  for (int i = 0; i < cnt; ++i) {
-    const int ixy = __shfl_sync(0xffffffffu, rxy, i);
-    const int iw = __shfl_sync(0xffffffffu, wdt, i);
-    const int int_ = __shfl_sync(0xffffffffu, nt, i);
-    const uint32_t ipo = __shfl_sync(0xffffffffu, po, i);
-    const uint32_t im = __shfl_sync(0xffffffffu, magic, i);
-    const int x0 = int(short(ixy & 0xffff)), y0 = ixy >> 16;
-    for (int l = lane; l < int_; l += 32) {
-      const int row = iw == 1 ? l : int(__umulhi(uint32_t(l), im));  // exact for l, width < 2^16
-      pkeys[ipo + l] = uint32_t((y0 + row) * TX + x0 + (l - row * iw));
-      pvals[ipo + l] = uint32_t(k0 + i);
+  __syncthreads();
+  for (int y = threadIdx.x; y < TY; y += blockDim.x) {
+    uint32_t run = 0;
+    for (int x = 0; x < TX; ++x) {
+      run += s_cur[y * W1 + x];
+      s_cur[y * W1 + x] = run;
+    }
+  }
+  __syncthreads();
+  for (int x = threadIdx.x; x < TX; x += blockDim.x) {
+    uint32_t run = 0;
+    for (int y = 0; y < TY; ++y) {
+      run += s_cur[y * W1 + x];
+      s_cur[y * W1 + x] = run;
+    }
+  }
+  __syncthreads();
+  for (int t = threadIdx.x; t < T; t += blockDim.x) {
+    const int c = (t / TX) * W1 + t % TX;
+    const uint32_t cnt = s_cur[c];
+    if (cnt) s_base[t] = atomicAdd(cursor + t, cnt);
+    s_cur[c] = 0;
+  }
+  __syncthreads();
+#pragma unroll
+  for (int k = 0; k < kEmitPer; ++k) {
+    const int i = (blockIdx.x * kEmitPer + k) * kEmitThreads + threadIdx.x;
+    const int wdt = r[k].z - r[k].x + 1;
+    const int nt = wdt * (r[k].w - r[k].y + 1);  // 0 when not visible
+    const int incl = int(warp_incl_scan(uint32_t(nt)));
+    const int total = __shfl_sync(0xffffffffu, incl, 31);
+    const int xy = (int(r[k].x) & 0xffff) | (int(r[k].y) << 16);
+    for (int p0 = 0; p0 < total; p0 += 32) {
+      const int p = p0 + lane;
+      // j = number of lanes whose inclusive prefix is <= p
+      int j = 0;
+#pragma unroll
+      for (int b = 16; b > 0; b >>= 1) {
+        const int v = __shfl_sync(0xffffffffu, incl, j + b - 1);
+        j += v <= p ? b : 0;
+      }
+      j = min(j, 31);
+      const int ij = __shfl_sync(0xffffffffu, incl, j), nj = __shfl_sync(0xffffffffu, nt, j);
+      const int wj = __shfl_sync(0xffffffffu, wdt, j), xyj = __shfl_sync(0xffffffffu, xy, j);
+      if (p < total) {
+        const int local = p - (ij - nj);
+        const int row = local / wj, col = local - row * wj;
+        const int x = (xyj & 0xffff) + col, y = (xyj >> 16) + row;
+        const uint32_t pos = s_base[y * TX + x] + atomicAdd(s_cur + y * W1 + x, 1u);
+        ids[pos] = i - lane + j;
+      }
     }
   }
 }
 
-// sorted_idx[p] = Gaussian of the p-th pair (rank -> id through the depth sort).
-__global__ void __launch_bounds__(256) k_gather_ids(const uint32_t *__restrict__ prank,
-                                                    const uint32_t *__restrict__ svals,
-                                                    const uint32_t *__restrict__ misc, int32_t *sorted_idx) {
-  if (misc[2]) return;
-  const int64_t P = misc[1];
-  const int64_t p0 = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) * 4;
-  if (p0 + 3 < P) {
-    const uint4 r = __ldg(reinterpret_cast<const uint4 *>(prank + p0));
-    int4 o;
-    o.x = int32_t(__ldg(svals + r.x));
-    o.y = int32_t(__ldg(svals + r.y));
-    o.z = int32_t(__ldg(svals + r.z));
-    o.w = int32_t(__ldg(svals + r.w));
-    *reinterpret_cast<int4 *>(sorted_idx + p0) = o;
-  } else {
-    for (int64_t p = p0; p < P && p < p0 + 4; ++p) sorted_idx[p] = int32_t(__ldg(svals + __ldg(prank + p)));
+// ---------------------------------------------------------------------------
+// Step 4: per-tile sort.  Keys are held "blocked": warp w owns the positions
+// [w*32*items, (w+1)*32*items) of the current order, its k-th round the 32
+// positions w*32*items + 32k + lane.  One stable LSD pass:
+//   ranks    per warp round, ballot-sliced peer masks (stable: rounds in
+//            order, lanes in order) and per-warp digit counters s_cnt[w][d];
+//   offsets  digit-major, warp-minor: s_off[d] (digit base) + the warps
+//            before w in digit d;
+//   scatter  into the shared-memory buffers, reload blocked.
+
+struct SortSmem {
+  uint32_t key[kChunk];
+  uint32_t val[kChunk];
+  uint16_t cnt[kSortWarps][kDigits];
+  uint32_t off[kDigits];
+  uint32_t sh[33];
+  int flag;
+  uint32_t red[3][kSortWarps];
+};
+
+// Per-warp stable ranks of the digits of one chunk; leaves the per-warp digit
+// counts in s.cnt (zeroed here) and returns the ranks in rank[].
+__device__ __forceinline__ void chunk_rank(const uint32_t key[kSortItems], const uint32_t val[kSortItems], int n,
+                                           int items, bool by_val, int shift, SortSmem &s,
+                                           uint16_t rank[kSortItems]) {
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  for (int i = threadIdx.x; i < kSortWarps * kDigits / 2; i += kSortThreads)
+    reinterpret_cast<uint32_t *>(&s.cnt[0][0])[i] = 0u;
+  __syncthreads();
+  const int base = w * 32 * items;
+#pragma unroll
+  for (int k = 0; k < kSortItems; ++k) {
+    if (k >= items) break;
+    const bool ok = base + 32 * k + lane < n;
+    const unsigned act = __ballot_sync(0xffffffffu, ok);
+    const uint32_t d = ((by_val ? val[k] : key[k]) >> shift) & (kDigits - 1);
+    const unsigned peers = peer_mask(act, d);
+    const uint32_t before = ok ? s.cnt[w][d] : 0u;
+    rank[k] = uint16_t(before + __popc(peers & lanemask_lt()));
+    __syncwarp();
+    if (ok && lane == 31 - __clz(peers)) s.cnt[w][d] = uint16_t(before + __popc(peers));
+    __syncwarp();
+  }
+  __syncthreads();
+}
+
+// s.cnt[w][d] <- sum of the counts of warps < w in digit d; returns the digit
+// totals of digits 2t and 2t+1 (thread t).
+__device__ __forceinline__ uint2 warp_prefix(SortSmem &s) {
+  uint32_t tot[2];
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+    const int d = 2 * threadIdx.x + h;
+    uint32_t run = 0;
+#pragma unroll
+    for (int w = 0; w < kSortWarps; ++w) {
+      const uint32_t c = s.cnt[w][d];
+      s.cnt[w][d] = uint16_t(run);
+      run += c;
+    }
+    tot[h] = run;
+  }
+  return make_uint2(tot[0], tot[1]);
+}
+
+// One stable pass over a chunk held blocked in registers, scattered to
+// out_key/out_val at s.off[d] + (warps before) + rank.  `local`: the chunk is
+// the whole sequence, s.off = exclusive scan of its digit totals; otherwise
+// s.off holds running global digit bases and is advanced by the totals.
+template <bool kGlobalOut>
+__device__ __forceinline__ void chunk_pass(const uint32_t key[kSortItems], const uint32_t val[kSortItems], int n,
+                                           int items, bool by_val, int shift, bool local, SortSmem &s,
+                                           uint32_t *out_key, uint32_t *out_val) {
+  static_assert(kDigits == 2 * kSortThreads, "two digits per thread in the offset scan");
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  uint16_t rank[kSortItems];
+  chunk_rank(key, val, n, items, by_val, shift, s, rank);
+  const uint2 tot = warp_prefix(s);
+  if (local) {
+    uint32_t all;
+    const uint32_t ex = block_excl_scan(tot.x + tot.y, s.sh, all);
+    s.off[2 * threadIdx.x] = ex;
+    s.off[2 * threadIdx.x + 1] = ex + tot.x;
+  }
+  __syncthreads();
+  const int base = w * 32 * items;
+#pragma unroll
+  for (int k = 0; k < kSortItems; ++k) {
+    if (k >= items) break;
+    if (base + 32 * k + lane < n) {
+      const uint32_t d = ((by_val ? val[k] : key[k]) >> shift) & (kDigits - 1);
+      const uint32_t pos = s.off[d] + s.cnt[w][d] + rank[k];
+      out_key[pos] = key[k];
+      out_val[pos] = val[k];
+    }
+  }
+  __syncthreads();
+  if (!local) {
+    s.off[2 * threadIdx.x] += tot.x;
+    s.off[2 * threadIdx.x + 1] += tot.y;
+    __syncthreads();
   }
 }
 
-}  // namespace gs
+__device__ __forceinline__ void load_blocked(uint32_t key[kSortItems], uint32_t val[kSortItems], const uint32_t *k_src,
+                                             const uint32_t *v_src, int n, int items) {
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int base = w * 32 * items;
+#pragma unroll
+  for (int k = 0; k < kSortItems; ++k) {
+    if (k >= items) break;
+    const int i = base + 32 * k + lane;
+    key[k] = i < n ? k_src[i] : 0u;
+    val[k] = i < n ? v_src[i] : 0u;
+  }
+}
 
-namespace gs {
+// Bits needed for values <= x.
+__device__ __forceinline__ int nbits(uint32_t x) { return x ? 32 - __clz(x) : 0; }
+
+// Block max of three values (s.red scratch); all threads get the results.
+__device__ __forceinline__ uint3 block_max3(uint3 v, SortSmem &s) {
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    v.x = max(v.x, __shfl_xor_sync(0xffffffffu, v.x, o));
+    v.y = max(v.y, __shfl_xor_sync(0xffffffffu, v.y, o));
+    v.z = max(v.z, __shfl_xor_sync(0xffffffffu, v.z, o));
+  }
+  if (lane == 0) {
+    s.red[0][w] = v.x;
+    s.red[1][w] = v.y;
+    s.red[2][w] = v.z;
+  }
+  __syncthreads();
+  uint3 r = make_uint3(0u, 0u, 0u);
+#pragma unroll
+  for (int k = 0; k < kSortWarps; ++k) {
+    r.x = max(r.x, s.red[0][k]);
+    r.y = max(r.y, s.red[1][k]);
+    r.z = max(r.z, s.red[2][k]);
+  }
+  __syncthreads();
+  return r;
+}
+
+struct TileSortArgs {
+  const float *depth;
+  const int32_t *tile_range;
+  const int32_t *order;  // tile launch order (nullable)
+  uint32_t *misc;        // [2] overflow, [3] length of the slow-path tile list
+  int T;
+  int32_t *ids;  // sorted_idx
+  uint32_t *key_a, *key_b, *val_b;
+  int32_t *slow;  // [T] tiles left to k_tile_sort_big
+};
+
+// Tiles with <= kChunk entries, one CTA each, one pass: a counting sort on
+// the top kBucketBits bits of (depth bits - tile min) into shared memory
+// (positions within a bucket from shared-memory atomics, i.e. unordered),
+// then every entry placed at its bucket start + the number of entries of its
+// bucket with a smaller exact key (depth bits, id) (buckets hold ~n / 2048
+// entries).  A tile whose buckets
+// exceed kMaxBucket entries (a dense cluster of depths next to a far
+// outlier), or whose list exceeds kChunk, is appended to the slow list.
+struct BucketSmem {
+  uint32_t key[kChunk];
+  uint32_t val[kChunk];
+  uint32_t cnt[kBuckets];  // counts, then bucket starts
+  uint32_t sh[33];
+  uint32_t red[2][kBucketThreads / 32];
+  int flag;
+};
+
+__global__ void __launch_bounds__(kBucketThreads, 4) k_tile_sort(TileSortArgs a) {
+  __shared__ BucketSmem s;
+  if (a.misc[2]) return;
+  const int tile = a.order ? __ldg(a.order + blockIdx.x) : int(blockIdx.x);
+  const int2 r = reinterpret_cast<const int2 *>(a.tile_range)[tile];
+  const int n = r.y - r.x;
+  if (n <= 1) return;
+  if (n > kChunk) {
+    if (threadIdx.x == 0) a.slow[atomicAdd(&a.misc[3], 1u)] = tile;
+    return;
+  }
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  for (int b = threadIdx.x; b < kBuckets; b += kBucketThreads) s.cnt[b] = 0u;
+  if (threadIdx.x == 0) s.flag = 0;
+  constexpr int kIt = kChunk / kBucketThreads;
+  uint32_t key[kIt], val[kIt];
+  uint32_t kmin = 0xffffffffu, kmax = 0u;
+#pragma unroll
+  for (int k = 0; k < kIt; ++k) {
+    const int i = threadIdx.x + k * kBucketThreads;
+    if (i < n) {
+      val[k] = uint32_t(a.ids[r.x + i]);
+      key[k] = __float_as_uint(__ldg(a.depth + val[k]));
+      kmin = min(kmin, key[k]);
+      kmax = max(kmax, key[k]);
+    }
+  }
+  // block min / max of the depth bits
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    kmin = min(kmin, __shfl_xor_sync(0xffffffffu, kmin, o));
+    kmax = max(kmax, __shfl_xor_sync(0xffffffffu, kmax, o));
+  }
+  if (lane == 0) {
+    s.red[0][w] = kmin;
+    s.red[1][w] = kmax;
+  }
+  __syncthreads();
+#pragma unroll
+  for (int k = 0; k < (kBucketThreads / 32); ++k) {
+    kmin = min(kmin, s.red[0][k]);
+    kmax = max(kmax, s.red[1][k]);
+  }
+  const int shift = max(0, nbits(kmax - kmin) - kBucketBits);
+  uint16_t slot[kIt];
+#pragma unroll
+  for (int k = 0; k < kIt; ++k) {
+    const int i = threadIdx.x + k * kBucketThreads;
+    if (i < n) slot[k] = uint16_t(atomicAdd(&s.cnt[(key[k] - kmin) >> shift], 1u));
+  }
+  __syncthreads();
+  // bucket starts (exclusive scan, kBuckets / kBucketThreads buckets per thread)
+  constexpr int kPer = kBuckets / kBucketThreads;
+  uint32_t c[kPer], sum = 0, big = 0;
+#pragma unroll
+  for (int k = 0; k < kPer; ++k) {
+    c[k] = s.cnt[threadIdx.x * kPer + k];
+    sum += c[k];
+    big |= c[k] > kMaxBucket;
+  }
+  if (big) s.flag = 1;
+  uint32_t all;
+  uint32_t ex = block_excl_scan(sum, s.sh, all);
+#pragma unroll
+  for (int k = 0; k < kPer; ++k) {
+    s.cnt[threadIdx.x * kPer + k] = ex;
+    ex += c[k];
+  }
+  __syncthreads();
+  if (s.flag) {  // dense buckets: exact two-key path
+    if (threadIdx.x == 0) a.slow[atomicAdd(&a.misc[3], 1u)] = tile;
+    return;
+  }
+  // scatter into the buckets (unordered inside a bucket)
+#pragma unroll
+  for (int k = 0; k < kIt; ++k) {
+    const int i = threadIdx.x + k * kBucketThreads;
+    if (i < n) {
+      const uint32_t pos = s.cnt[(key[k] - kmin) >> shift] + slot[k];
+      s.key[pos] = key[k];
+      s.val[pos] = val[k];
+    }
+  }
+  __syncthreads();
+  // final position = bucket start + number of bucket entries with a smaller
+  // exact key (depth bits, id): O(bucket size) per entry, no serial chain
+#pragma unroll
+  for (int k = 0; k < kIt; ++k) {
+    const int i = threadIdx.x + k * kBucketThreads;
+    if (i < n) {
+      const uint32_t b = (key[k] - kmin) >> shift;
+      const uint32_t b0 = s.cnt[b];
+      const uint32_t be = b + 1 < kBuckets ? s.cnt[b + 1] : uint32_t(n);
+      uint32_t rank = 0;
+      for (uint32_t j = b0; j < be; ++j) {
+        const uint32_t kj = s.key[j], vj = s.val[j];
+        rank += (kj < key[k]) || (kj == key[k] && vj < val[k]);
+      }
+      a.ids[r.x + b0 + rank] = int32_t(val[k]);
+    }
+  }
+}
+
+// Tiles of the slow list (grid-stride): exact two-key LSD (id digits, then
+// depth digits) over global memory, chunk by chunk: each chunk of kChunk
+// entries ranked stably per warp round (ballot-sliced peer masks, per-warp
+// digit counters), digit bases carried across chunks from a per-pass
+// histogram.
+__global__ void __launch_bounds__(kSortThreads) k_tile_sort_big(TileSortArgs a) {
+  __shared__ SortSmem s;
+  if (a.misc[2]) return;
+  const int nslow = int(a.misc[3]);
+  for (int q = blockIdx.x; q < nslow; q += gridDim.x) {
+    const int tile = a.slow[q];
+    const int2 r = reinterpret_cast<const int2 *>(a.tile_range)[tile];
+    const int n = r.y - r.x;
+    uint32_t *vA = reinterpret_cast<uint32_t *>(a.ids) + r.x, *kA = a.key_a + r.x;
+    uint32_t *vB = a.val_b + r.x, *kB = a.key_b + r.x;
+    uint32_t kmin = 0xffffffffu, kmax = 0u, vmax = 0u;
+    for (int i = threadIdx.x; i < n; i += kSortThreads) {
+      const uint32_t v = vA[i];
+      const uint32_t k = __float_as_uint(__ldg(a.depth + v));
+      kA[i] = k;
+      kmin = min(kmin, k);
+      kmax = max(kmax, k);
+      vmax = max(vmax, v);
+    }
+    const uint3 m = block_max3(make_uint3(~kmin, kmax, vmax), s);
+    kmin = ~m.x;
+    for (int i = threadIdx.x; i < n; i += kSortThreads) kA[i] -= kmin;
+    __syncthreads();
+    const int kbits = nbits(m.y - kmin), vbits = nbits(m.z);
+    const int npass_v = (vbits + kDigitBits - 1) / kDigitBits, npass_k = (kbits + kDigitBits - 1) / kDigitBits;
+    for (int p = 0; p < npass_v + npass_k; ++p) {
+      const bool by_val = p < npass_v;
+      const int shift = (by_val ? p : p - npass_v) * kDigitBits;
+      // digit histogram of the whole segment -> global digit bases
+      for (int d = threadIdx.x; d < kDigits; d += kSortThreads) s.off[d] = 0;
+      __syncthreads();
+      for (int i = threadIdx.x; i < n; i += kSortThreads)
+        atomicAdd(&s.off[((by_val ? vA[i] : kA[i]) >> shift) & (kDigits - 1)], 1u);
+      __syncthreads();
+      {
+        const uint32_t c0 = s.off[2 * threadIdx.x], c1 = s.off[2 * threadIdx.x + 1];
+        uint32_t all;
+        const uint32_t ex = block_excl_scan(c0 + c1, s.sh, all);
+        s.off[2 * threadIdx.x] = ex;
+        s.off[2 * threadIdx.x + 1] = ex + c0;
+        __syncthreads();
+      }
+      for (int c0 = 0; c0 < n; c0 += kChunk) {
+        const int cn = min(kChunk, n - c0);
+        const int items = (cn + kSortThreads - 1) / kSortThreads;
+        uint32_t key[kSortItems], val[kSortItems];
+        load_blocked(key, val, kA + c0, vA + c0, cn, items);
+        chunk_pass<true>(key, val, cn, items, by_val, shift, false, s, kB, vB);
+      }
+      uint32_t *t0 = kA, *t1 = vA;
+      kA = kB;
+      vA = vB;
+      kB = t0;
+      vB = t1;
+      __syncthreads();
+    }
+    uint32_t *dst = reinterpret_cast<uint32_t *>(a.ids) + r.x;
+    if (vA != dst)
+      for (int i = threadIdx.x; i < n; i += kSortThreads) dst[i] = vA[i];
+    __syncthreads();
+  }
+}
+
 // Tiles by descending work, 64 buckets of max/64 (single CTA).
 __global__ void __launch_bounds__(1024) k_order_by_work(const int32_t *__restrict__ work, int T, int32_t *order) {
   __shared__ int s_max;
@@ -546,6 +713,7 @@ __global__ void __launch_bounds__(1024) k_order_by_work(const int32_t *__restric
   for (int t = threadIdx.x; t < T; t += blockDim.x)
     order[atomicAdd(&s_b[63 - int(int64_t(max(work[t], 0)) * 64 / den)], 1u)] = t;
 }
+
 }  // namespace gs
 
 extern "C" int gs_tile_order(const int32_t *work, int32_t T, int32_t *order, void *stream) {
@@ -563,17 +731,6 @@ extern "C" size_t gs_binsort_workspace_bytes(int32_t n, int64_t capacity, gs_cam
   if (n < 0 || capacity < 0 || !gs::camera_ok(cam) || !gs::make_layout(n, capacity, cam, L)) return 0;
   return L.total;
 }
-
-namespace gs {
-template <int RB, int ITEMS>
-static void radix_pass(const RSArgs &a, uint32_t *scan_status, uint32_t *ticket, cudaStream_t s) {
-  const int64_t L = int64_t(1 << RB) * a.nblk;
-  k_rs_upsweep<RB, ITEMS><<<a.nblk, kOSThreads, 0, s>>>(a);
-  const int nb = int((L + kOSThreads * kScanItems1 - 1) / (kOSThreads * kScanItems1));
-  k_scan_1pass<<<nb, kOSThreads, 0, s>>>(a.counts, L, scan_status, ticket, nullptr);
-  k_rs_downsweep<RB, ITEMS><<<a.nblk, kOSThreads, 0, s>>>(a);
-}
-}  // namespace gs
 
 extern "C" int gs_bin_sort(gs_proj pr, int32_t n, gs_camera cam, void *ws, size_t ws_bytes, int64_t capacity,
                            int32_t *sorted_idx, int32_t *tile_range, int32_t *tile_order, int64_t *n_pairs,
@@ -600,59 +757,35 @@ extern "C" int gs_bin_sort(gs_proj pr, int32_t n, gs_camera cam, void *ws, size_
   cudaStream_t s = as_stream(stream);
   char *w = static_cast<char *>(ws);
   auto U = [&](size_t off) { return reinterpret_cast<uint32_t *>(w + off); };
-  uint32_t *misc = U(L.misc), *tickets = U(L.tickets);
+  uint32_t *misc = U(L.misc);
   cudaMemsetAsync(w, 0, L.zero_end, s);
   const short4 *rect = reinterpret_cast<const short4 *>(pr.rect);
   const size_t diff_bytes = size_t(4) * (L.TX + 1) * (L.TY + 1);
+  const size_t emit_bytes = diff_bytes + size_t(4) * L.T;
   static thread_local size_t smem_set = 0;
-  if (diff_bytes > 48 * 1024 && diff_bytes > smem_set) {
-    cudaFuncSetAttribute(k_depth_prep, cudaFuncAttributeMaxDynamicSharedMemorySize, int(diff_bytes));
+  const size_t need = std::max(diff_bytes, emit_bytes);
+  if (need > 48 * 1024 && need > smem_set) {
+    cudaFuncSetAttribute(k_bin_prep, cudaFuncAttributeMaxDynamicSharedMemorySize, int(diff_bytes));
     cudaFuncSetAttribute(k_tile_counts, cudaFuncAttributeMaxDynamicSharedMemorySize, int(diff_bytes));
-    smem_set = diff_bytes;
+    cudaFuncSetAttribute(k_emit, cudaFuncAttributeMaxDynamicSharedMemorySize, int(emit_bytes));
+    smem_set = need;
   }
-  // ---- depth keys, tile difference array, per-tile pair counts ----
-  {
-    PrepArgs a{pr.depth, pr.tiles_touched, rect, n, L.TX, L.TY, L.zbase, L.kinvis,
-               U(L.dkeys_a), U(L.dvals_a), U(L.diff), misc + 0};
-    const int blocks = std::max(1, std::min(2 * 148, (n + kOSThreads - 1) / kOSThreads));
-    k_depth_prep<<<blocks, kOSThreads, diff_bytes, s>>>(a);
+  if (n > 0) {
+    const int blocks = std::max(1, std::min(2 * 148, (n + 255) / 256));
+    k_bin_prep<<<blocks, 256, diff_bytes, s>>>(pr.tiles_touched, rect, n, L.TX, L.TY, U(L.diff));
   }
   {
-    TileArgs a{U(L.diff), L.TX, L.TY, L.T, capacity, tile_range, tile_order, n_pairs, misc, cnt};
+    TileArgs a{U(L.diff), L.TX, L.TY, L.T, capacity, tile_range, tile_order, U(L.cursor), n_pairs, misc, cnt};
     k_tile_counts<<<1, 1024, diff_bytes, s>>>(a);
   }
-  // ---- stage 1: depth radix passes (last pass writes tiles_touched[val]) ----
-  uint32_t *dk[2] = {U(L.dkeys_a), U(L.dkeys_b)}, *dv[2] = {U(L.dvals_a), U(L.dvals_b)};
-  const size_t sbd = (size_t(1 << kDepthBits) * L.nblk_d + kOSThreads * kScanItems1 - 1) / (kOSThreads * kScanItems1);
-  const size_t sbp = (size_t(1 << kTileBits) * L.nblk_p + kOSThreads * kScanItems1 - 1) / (kOSThreads * kScanItems1);
-  int cur = 0;
-  for (int p = 0; p < L.dpasses; ++p) {
-    const bool last = p == L.dpasses - 1;
-    RSArgs a{dk[cur], dv[cur], dk[cur ^ 1], dv[cur ^ 1], nullptr, n, p * kDepthBits, L.nblk_d, U(L.cnt_d),
-             last ? pr.tiles_touched : nullptr, nullptr};
-    radix_pass<kDepthBits, kDepthItems>(a, U(L.st_cd) + p * sbd, tickets + p, s);
-    cur ^= 1;
-  }
-  uint32_t *svals = dv[cur], *poff = dk[cur];
-  // ---- pair offsets of the depth-sorted stream, pair emission ----
-  k_scan_1pass<<<L.nblk_s, kOSThreads, 0, s>>>(poff, n, U(L.st_s), tickets + 8, nullptr);
-  {
-    const int blocks = std::max(1, (n + kOSThreads - 1) / kOSThreads);
-    k_emit_pairs<<<blocks, kOSThreads, 0, s>>>(svals, poff, rect, misc + 0, misc + 2, L.TX, U(L.pkeys_a),
-                                               U(L.pvals_a));
-  }
-  // ---- stage 2: stable tile radix passes over the pairs ----
-  uint32_t *pk[2] = {U(L.pkeys_a), U(L.pkeys_b)}, *pv[2] = {U(L.pvals_a), U(L.pvals_b)};
-  int pc = 0;
-  for (int p = 0; p < L.tpasses; ++p) {
-    RSArgs a{pk[pc], pv[pc], pk[pc ^ 1], pv[pc ^ 1], misc + 1, capacity, p * kTileBits, L.nblk_p, U(L.cnt_p),
-             nullptr, misc + 2};
-    radix_pass<kTileBits, kPairItems>(a, U(L.st_cp) + p * sbp, tickets + 4 + p, s);
-    pc ^= 1;
-  }
-  if (capacity > 0) {
-    const int blocks = int((capacity + 1023) / 1024);
-    k_gather_ids<<<blocks, 256, 0, s>>>(pv[pc], svals, misc, sorted_idx);
+  if (n > 0 && capacity > 0) {
+    const int per_block = kEmitThreads * kEmitPer;
+    k_emit<<<(n + per_block - 1) / per_block, kEmitThreads, emit_bytes, s>>>(
+        pr.tiles_touched, rect, n, L.TX, L.TY, U(L.cursor), misc, sorted_idx);
+    TileSortArgs a{pr.depth, tile_range, tile_order, misc, L.T, sorted_idx, U(L.key_a), U(L.key_b), U(L.val_b),
+                   reinterpret_cast<int32_t *>(U(L.slow))};
+    k_tile_sort<<<L.T, kBucketThreads, 0, s>>>(a);
+    k_tile_sort_big<<<std::min(L.T, kBigBlocks), kSortThreads, 0, s>>>(a);
   }
   return check_launch("gs_bin_sort");
 }

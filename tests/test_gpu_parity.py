@@ -112,6 +112,41 @@ def test_sort_ties_by_index():
         assert np.all((keys[1:] > keys[:-1]) | ((keys[1:] == keys[:-1]) & (seg[1:] > seg[:-1])))
 
 
+def _conditional_sort_check(s):
+    """The oracle bins the GPU's own rects / depth keys: bit-identical lists."""
+    r, _, _ = gpu_forward(s, stats=False)
+    idx, rng = gpu_sort(r)
+    g = gpu_proj(r)
+    culled = (g["tiles_touched"] == 0).astype(np.int32)
+    oi, orng = oracle.bin_sort(g["rect"], culled, g["depth"], s.cam)
+    assert np.array_equal(rng, orng) and np.array_equal(idx, oi)
+    return rng
+
+
+def test_sort_long_tiles():
+    """Tile lists longer than one shared-memory chunk (4096 entries) take the
+    chunked two-key path of gs_bin_sort."""
+    s = inputs.random_scene(32, 9000, 40, 40, spread=0.6, ls=(-1.2, 0.2), lo=(2.0, 0.5))
+    rng = _conditional_sort_check(s)
+    assert (rng[:, 1] - rng[:, 0]).max() > 4096
+
+
+def test_sort_dense_depth_cluster():
+    """A tight cluster of depths next to one far outlier (the counting sort's
+    buckets overflow) and long runs of exactly equal depths: both take the
+    exact two-key path and must still equal the (depth, id) order."""
+    s = inputs.random_scene(33, 3000, 48, 48, spread=0.9, ls=(-2.0, 0.3), lo=(2.0, 0.5))
+    z = s.mean_opa[:, 2].astype(np.float64)
+    z = 2.0 + (z - 1.0) * 1e-5                       # ~400 ulps of depth for 2999 Gaussians
+    z[0] = 90.0                                      # far outlier covering the image
+    s.mean_opa[:, 0] *= (z / s.mean_opa[:, 2]).astype(np.float32)
+    s.mean_opa[:, 1] *= (z / s.mean_opa[:, 2]).astype(np.float32)
+    s.mean_opa[:, 2] = z.astype(np.float32)
+    s.logscale[0, :3] = 1.5
+    s.mean_opa[1500:1700, 2] = np.float32(2.0)       # a run of 200 equal depths
+    _conditional_sort_check(s)
+
+
 # ---------------------------------------------------------------------------
 # S3 compositing
 

@@ -14,7 +14,7 @@ for r in rows:
 idx = [i for i, d in enumerate(data) if "k_project" in d["Kernel Name"]][-1]
 agg = collections.OrderedDict()
 tot = 0.0
-for d in data[idx:]:
+for d in [d for d in data[idx:] if d.get("Metric Name", "gpu__time_duration.sum") == "gpu__time_duration.sum"]:
     v = float(d["Metric Value"].replace(",", "")) / 1000.0
     k = d["Kernel Name"].split("(")[0].replace("void ", "")
     agg.setdefault(k, [0.0, 0])
