@@ -316,36 +316,20 @@ def bench_ours(a):
 def e2e_ours(a, s, ms, device, world=1):
     """Same metric through the public API with HOST buffers: every step copies
     its inputs (Gaussian parameters, view poses, this rank's RGB-D targets)
-    from pinned host memory and reads the per-view losses back."""
+    from pinned host memory and reads the per-view losses back
+    (MapStep.step(host=...): the targets of later views upload while earlier
+    views compute)."""
     import torch
-    P = ms.params
-    host = {k: getattr(P, k).cpu().pin_memory() for k in ("mean_opa", "quat", "logscale", "rgb")}
-    hviews = ms.views.cpu().pin_memory()
-    htc = {v: ms.tgt_color[v].cpu().pin_memory() for v in ms.mine}
-    htd = {v: ms.tgt_depth[v].cpu().pin_memory() for v in ms.mine}
-    hloss = torch.empty_like(ms.losses, device="cpu").pin_memory()
-    h2d = sum(t.numel() * t.element_size() for t in host.values()) + hviews.numel() * 4 + \
-        sum(htc[v].numel() * 4 + htd[v].numel() * 4 for v in ms.mine)
-    d2h = hloss.numel() * 4
-
-    def one():
-        for k, t in host.items():
-            getattr(P, k).copy_(t, non_blocking=True)
-        ms.views.copy_(hviews, non_blocking=True)
-        for v in ms.mine:
-            ms.tgt_color[v].copy_(htc[v], non_blocking=True)
-            ms.tgt_depth[v].copy_(htd[v], non_blocking=True)
-        ms.step()
-        hloss.copy_(ms.losses, non_blocking=True)
-
+    from paper_2312_10070_b200.pipeline import HostInputs
+    host = HostInputs(ms.params, ms.views, ms.tgt_color, ms.tgt_depth, ms.mine, ms.losses.shape[0])
     for _ in range(2):
-        one()
+        ms.step(host=host)
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record()
     n = max(3, a.steps // 2)
     for _ in range(n):
-        one()
+        ms.step(host=host)
     e1.record()
     torch.cuda.synchronize()
     ms_step = e0.elapsed_time(e1) / n
@@ -354,8 +338,8 @@ def e2e_ours(a, s, ms, device, world=1):
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
         ms_step = float(t.item())
     mp = ms.V * s.cam.width * s.cam.height / 1e6
-    return {"value": mp / (ms_step * 1e-3), "unit": UNIT, "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
-            "ms_per_step": ms_step}
+    return {"value": mp / (ms_step * 1e-3), "unit": UNIT, "h2d_bytes_per_step": int(host.h2d_bytes()),
+            "d2h_bytes_per_step": int(host.d2h_bytes()), "ms_per_step": ms_step}
 
 
 def bench_tracking(device):

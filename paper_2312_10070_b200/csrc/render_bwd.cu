@@ -84,6 +84,7 @@ __device__ __forceinline__ void red_add_v4(float *addr, float x, float y, float 
 }
 
 constexpr int kBPX = 4;   // pixels per thread in the backward (two fp32x2 pairs)
+constexpr bool kSmemReduce = true;  // per-entry warp sums through shared memory (else shuffles)
 using BG = Geo<kBPX, 16>;  // 2 warps, 16x8 pixel strips
 
 __device__ __forceinline__ float rcp_approx(float x) {
@@ -111,7 +112,7 @@ struct BwdPix {
 // (the 1/2 of dsigma/dA and dsigma/dC is applied once, by the writing lane)
 template <bool kParams>
 __device__ __forceinline__ void bwd_entry(BwdPix &s, const float2 e[2], const bool pass[kBPX], float4 c, float4 cn,
-                                          float2 ul, float fpy, const float2 fx[2], float *dst) {
+                                          float2 ul, float fpy, const float2 fx[2], float *dst, float *red) {
   const float dy = ul.y - fpy;  // Delta = mu^I - pixel; one row: dy is shared
   // per-thread sums over its pixels (as pair sums) of ga = alpha dL/dalpha
   // (0 if clamped) and ga dx, ga dx^2; dsigma/d(u, v, A, B, C) and
@@ -175,6 +176,30 @@ __device__ __forceinline__ void bwd_entry(BwdPix &s, const float2 e[2], const bo
     }
     return;
   }
+  if (kSmemReduce) {
+    // through this warp's shared-memory slab: lane l stores its 10 values in
+    // row l (stride 11: conflict-free both ways); lane 3v + p (v < 10, p < 3)
+    // sums value v over the rows = p mod 3, the 3 partial sums meet by two
+    // shuffles, lane 3v adds the total to grad2d
+    const int lane = threadIdx.x & 31;
+    float *row = red + lane * 11;
+#pragma unroll
+    for (int v = 0; v < 10; ++v) row[v] = acc[v];
+    __syncwarp();
+    const int v = lane / 3, p = lane - 3 * v;
+    float part = 0.f;
+    if (lane < 30) {
+#pragma unroll
+      for (int t = 0; t < 11; ++t) {
+        const int i = p + 3 * t;
+        if (i < 32) part += red[i * 11 + v];
+      }
+    }
+    part += __shfl_down_sync(0xffffffffu, part, 1) + __shfl_down_sync(0xffffffffu, part, 2);
+    if (lane < 30 && p == 0 && (kParams || v < 6))
+      atomicAdd(dst + (v < 7 ? v : v + 1), (v == 2 || v == 4) ? 0.5f * part : part);
+    return;
+  }
   int idx;
   bool writer;
   const float tot = warp_reduce10(acc, idx, writer);
@@ -196,6 +221,8 @@ __global__ void __launch_bounds__(BG::kThreads) k_bwd_pixels(BwdArgs a) {
   __shared__ unsigned char s_mask[kBatch];
   __shared__ unsigned char s_list[BG::kWarps][kBatch + 2];
   __shared__ int s_lmax;
+  __shared__ float s_red[BG::kWarps][2][32 * 11];  // per-warp reduction slabs (double-buffered)
+  int rbuf = 0;
   const int tile = a.tile_order ? __ldg(a.tile_order + blockIdx.x) : int(blockIdx.x);
   const int tx = tile % a.TX, ty = tile / a.TX;
   const int w = threadIdx.x >> 5;
@@ -299,7 +326,9 @@ __global__ void __launch_bounds__(BG::kThreads) k_bwd_pixels(BwdArgs a) {
           pass[2 * h + 1] = pos < s.last[2 * h + 1] && e[h].y >= kExpSkip;
         }
         if (!__any_sync(0xffffffffu, pass[0] || pass[1] || pass[2] || pass[3])) continue;
-        bwd_entry<kParams>(s, e, pass, s_rgbz[j], s_conic[j], s_uv[j], pg.fpy, fx, a.grad2d + size_t(s_idx[j]) * kG2);
+        bwd_entry<kParams>(s, e, pass, s_rgbz[j], s_conic[j], s_uv[j], pg.fpy, fx, a.grad2d + size_t(s_idx[j]) * kG2,
+                           s_red[w][rbuf]);
+        rbuf ^= 1;
       }
     }
   }

@@ -20,6 +20,26 @@ import torch
 from .raster import GS_BWD_GAUSS_ONLY, GS_BWD_PIXELS_ONLY, GS_GRAD_PARAMS, GS_GRAD_POSE, Grads, Params, Rasterizer, lib
 
 
+class HostInputs:
+    """Pinned host buffers of one mapping step's inputs (parameters, view
+    poses, this rank's RGB-D targets) and its per-view loss output."""
+
+    def __init__(self, params: Params, views, tgt_color, tgt_depth, mine, n_losses):
+        pin = lambda t: t.detach().cpu().contiguous().pin_memory()
+        self.params = {k: pin(getattr(params, k)) for k in ("mean_opa", "quat", "logscale", "rgb")}
+        self.views = pin(views)
+        self.tgt_color = {v: pin(tgt_color[v]) for v in mine}
+        self.tgt_depth = {v: pin(tgt_depth[v]) for v in mine}
+        self.loss = torch.empty(n_losses, 3, dtype=torch.float32).pin_memory()
+
+    def h2d_bytes(self):
+        b = sum(t.numel() * t.element_size() for t in self.params.values()) + self.views.numel() * 4
+        return b + sum(t.numel() * 4 for t in self.tgt_color.values()) + sum(t.numel() * 4 for t in self.tgt_depth.values())
+
+    def d2h_bytes(self):
+        return self.loss.numel() * 4
+
+
 def shard_views(n_views, rank, world):
     """Round-robin view assignment: rank r takes views r, r + world, ..."""
     return list(range(rank, n_views, world))
@@ -57,6 +77,7 @@ class MapStep:
         self.r = self.lanes[0]
         self.grads = Grads.zeros(params.n, device)
         self.losses = torch.zeros(max(len(self.mine), 1), 3, dtype=torch.float32, device=device)
+        self.copy_stream = None
 
     def size(self, slack=1.25):
         """Setup only (host sync): pair capacity = slack x max pairs over my views."""
@@ -72,9 +93,12 @@ class MapStep:
             r.set_capacity(int(best * slack) + 1024)
         return best
 
-    def view_pixels(self, r, k, v):
-        """Everything of view v up to the per-pixel backward phase."""
+    def view_pixels(self, r, k, v, tgt_ready=None):
+        """Everything of view v up to the per-pixel backward phase
+        (tgt_ready: event after which this view's targets are on the device)."""
         r.forward(self.params, self.views[v])
+        if tgt_ready is not None:
+            torch.cuda.current_stream().wait_event(tgt_ready)
         r.compute_loss(self.tgt_color[v], self.tgt_depth[v], None, self.lc, self.ld)
         self.losses[k].copy_(r.loss)
         r.backward(self.params, self.views[v], GS_GRAD_PARAMS | GS_BWD_PIXELS_ONLY, self.grads)
@@ -82,10 +106,33 @@ class MapStep:
     def view_gauss(self, r, k, v):
         r.backward(self.params, self.views[v], GS_GRAD_PARAMS | GS_BWD_GAUSS_ONLY, self.grads)
 
-    def step(self, hooks=None):
-        """hooks: optional (pixels_fn, gauss_fn) replacing view_pixels / view_gauss."""
+    def step(self, hooks=None, host=None):
+        """hooks: optional (pixels_fn, gauss_fn) replacing view_pixels / view_gauss.
+
+        host: optional HostInputs (pinned host buffers of this step's inputs).
+        A copy stream uploads the parameters and poses, then every view's
+        RGB-D targets in view order; a lane waits for the parameters before
+        projecting and for its view's targets only before the loss, so the
+        target uploads overlap the projection, binning and compositing of the
+        views ahead.  The per-view losses are read back into host.loss."""
         pix, gau = hooks if hooks is not None else (self.view_pixels, self.view_gauss)
         main = torch.cuda.current_stream()
+        tgt_ready = {}
+        if host is not None:
+            if self.copy_stream is None:
+                self.copy_stream = torch.cuda.Stream(device=self.params.mean_opa.device)
+            cs = self.copy_stream
+            cs.wait_stream(main)  # the previous step no longer reads these buffers
+            with torch.cuda.stream(cs):
+                for k in ("mean_opa", "quat", "logscale", "rgb"):
+                    getattr(self.params, k).copy_(host.params[k], non_blocking=True)
+                self.views.copy_(host.views, non_blocking=True)
+                params_ready = cs.record_event()
+                for v in self.mine:
+                    self.tgt_color[v].copy_(host.tgt_color[v], non_blocking=True)
+                    self.tgt_depth[v].copy_(host.tgt_depth[v], non_blocking=True)
+                    tgt_ready[v] = cs.record_event()
+            main.wait_event(params_ready)
         self.grads.zero_()
         start = main.record_event()
         for s in self.streams:
@@ -95,14 +142,21 @@ class MapStep:
             lane = k % len(self.lanes)
             s, r = self.streams[lane], self.lanes[lane]
             with torch.cuda.stream(s):
-                pix(r, k, v)
+                if host is not None:
+                    pix(r, k, v, tgt_ready[v])
+                else:
+                    pix(r, k, v)
                 s.wait_event(prev)
                 gau(r, k, v)
                 prev = s.record_event()
         for s in self.streams:
             main.wait_stream(s)
+        if host is not None:
+            main.wait_stream(self.copy_stream)
         if self.allreduce is not None:
             self.allreduce(self.grads.buf)
+        if host is not None:
+            host.loss.copy_(self.losses, non_blocking=True)
         return self.grads
 
     def launches_per_step(self):
@@ -110,25 +164,11 @@ class MapStep:
         return len(self.mine) * kernels_per_view(self.r.cam)
 
 
-def sort_passes(cam):
-    """Depth radix passes of gs_bin_sort (9-bit digits over bits(z) - bits(z_near))."""
-    import numpy as np
-    zb = int(np.float32(cam.z_near).view(np.uint32))
-    ze = int(np.float32(cam.z_far).view(np.uint32))
-    bits = max(1, (ze - zb + 1).bit_length())
-    return (bits + 8) // 9
-
-
-def tile_passes(cam):
-    T = ((cam.width + 15) // 16) * ((cam.height + 15) // 16)
-    return (max(1, (T - 1).bit_length()) + 6) // 7
-
-
 def kernels_per_view(cam, loss=True, bwd=True):
     """Kernels of ours per view (the sort's memset is a copy-engine node, not a kernel):
-    project 1; bin_sort: prep, tile counts, 3 per depth pass, scan, emit, 3 per
-    tile pass, gather; render 1 + tile order 1; loss 3; backward 2."""
-    n = 1 + (2 + 3 * sort_passes(cam) + 2 + 3 * tile_passes(cam) + 1) + 2
+    project 1; bin_sort: prep, tile counts, emit, tile sort, long-list sort = 5;
+    render 1 + backward tile order 1; loss 3; backward 2."""
+    n = 1 + 5 + 2
     if loss:
         n += 3
     if bwd:
