@@ -305,6 +305,7 @@ def bench_ours(a):
         dist.barrier()
     if rank == 0 and world == 1 and not a.profile and not a.no_tracking:
         line["tracking"] = bench_tracking(device)
+        line["tracking_masked"] = bench_tracking(device, masked=(0.5, 50.0))
     if rank == 0 and world == 1 and not a.profile and not a.no_cpu_baseline:
         line["cpu_baseline"] = cpu_baseline(a, s)
     if rank == 0:
@@ -342,8 +343,9 @@ def e2e_ours(a, s, ms, device, world=1):
             "d2h_bytes_per_step": int(host.d2h_bytes()), "ms_per_step": ms_step}
 
 
-def bench_tracking(device):
-    """BJ.configs[2]: 200k Gaussians, 1200x680, 100 pose iterations in one CUDA graph."""
+def bench_tracking(device, masked=None):
+    """BJ.configs[2]: 200k Gaussians, 1200x680, 100 pose iterations in one CUDA graph
+    (masked = (lambda_c, inlier_mult): the Eq. 15 masked loss instead of L1)."""
     import torch
     from paper_2312_10070_b200 import Params, Rasterizer, inputs
     from paper_2312_10070_b200.pipeline import TrackingLoop
@@ -355,7 +357,8 @@ def bench_tracking(device):
     r.forward(P, gt)
     tc, td = r.frame.color.clone(), r.frame.depth.clone()
     del r
-    loop = TrackingLoop(P, s.cam, tc, td, torch.as_tensor(s.extra["start_view"], device=device), iters=100)
+    loop = TrackingLoop(P, s.cam, tc, td, torch.as_tensor(s.extra["start_view"], device=device), iters=100,
+                        masked=masked)
     loop.size()
     loop.capture()
     for _ in range(2):
@@ -377,6 +380,8 @@ def bench_tracking(device):
     sv = s.extra["start_view"].astype(np.float64)
     rot0 = np.degrees(np.arccos(np.clip((np.trace(sv[:9].reshape(3, 3)) - 1) / 2, -1, 1)))
     return {"metric": "tracking iterations/s (BJ.configs[2], 200k Gaussians, 1200x680)",
+            "loss": "L1 colour + L1 depth (BJ.configs[2])" if masked is None else
+                    "Eq. 15 masked: alpha^3 x inlier (50 x median), lambda_c = %g" % masked[0],
             "value": 100 / (med * 1e-3), "unit": "iter/s", "ms_per_iter": med / 100,
             "graph": "100 iterations captured once (project, sort, render, loss, pose bwd, pose grad + Adam)",
             "gpu_launches_per_iter": loop.launches_per_iter(),

@@ -248,6 +248,34 @@ int gs_loss(gs_camera cam, const float *color, const float *depth,
             float lambda_color, float lambda_depth, void *ws, size_t ws_bytes,
             float *loss, float *dL_dcolor, float *dL_ddepth, void *stream);
 
+/* NEXT(1) — masked tracking loss (Eq. 15; S:286-294, S:425-438;
+ * DESIGN.md R29-R31).  Tracking only: gradients flow to the rendered colour
+ * and depth, the masks are constants (the 3-D Gaussians are frozen).
+ *
+ *   e_c = (|C^_r - C_r| + |C^_g - C_g| + |C^_b - C_b|) / 3,  e_d = |D^ - D*|
+ *         (fp32, each operation rounded to nearest, in this order)
+ *   valid pixels: D* > 0;  med_c, med_d = LOWER medians (rank floor((n-1)/2))
+ *   of e_c, e_d over the n valid pixels (exact order statistics);
+ *   M_inlier = valid & e_d <= fp32(mult med_d) & e_c <= fp32(mult med_c);
+ *   M_alpha = alpha^3 (fp32, from the rendered alpha map);
+ *   L = sum_px M_inlier M_alpha (lambda_c e_c + (1 - lambda_c) e_d)   (fp64 sum);
+ *   dL_dcolor = M_inlier M_alpha (lambda_c / 3) sign(C^ - C*);
+ *   dL_ddepth = M_inlier M_alpha (1 - lambda_c) sign(D^ - D*);  sign(0) = 0.
+ *   color, depth, alpha (device) rendered maps [3][H][W], [H][W], [H][W]
+ *   tgt_color, tgt_depth (device) RGB-D input frame, same layouts
+ *   lambda_c in [0, 1]; inlier_mult > 0 (50 in the paper's supplement)
+ *   ws     (device) >= gs_tracking_loss_workspace_bytes(cam)
+ *   loss   (device) [4] = (L, med_c, med_d, number of inlier pixels); with no
+ *          valid pixel every mask is empty and loss = (0, 0, 0, 0)
+ * The masks and medians are bit-deterministic; L is a fixed-order reduction.
+ * Errors: GS_ERR_INVALID_ARG (null, lambda_c outside [0,1], mult <= 0),
+ * GS_ERR_WORKSPACE. */
+size_t gs_tracking_loss_workspace_bytes(gs_camera cam);
+int gs_tracking_loss(gs_camera cam, const float *color, const float *depth, const float *alpha,
+                     const float *tgt_color, const float *tgt_depth, float lambda_c,
+                     float inlier_mult, void *ws, size_t ws_bytes, float *loss,
+                     float *dL_dcolor, float *dL_ddepth, void *stream);
+
 /* S5+S6 — backward (Eqs. 7-8; R16, R17).
  *
  * Per pixel, replays the composited entries back to front (same alpha

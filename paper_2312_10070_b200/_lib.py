@@ -65,6 +65,8 @@ _PROTOS = {
     "gs_render_fwd": (C.c_int, [GsProj, _VP, _VP, _VP, GsCamera, _VP, _VP, _VP, _VP, _VP, _VP, _VP, _VP]),
     "gs_tile_order": (C.c_int, [_VP, _I32, _VP, _VP]),
     "gs_loss": (C.c_int, [GsCamera, _VP, _VP, _VP, _VP, _VP, _F, _F, _VP, _SZ, _VP, _VP, _VP, _VP]),
+    "gs_tracking_loss_workspace_bytes": (_SZ, [GsCamera]),
+    "gs_tracking_loss": (C.c_int, [GsCamera, _VP, _VP, _VP, _VP, _VP, _F, _F, _VP, _SZ, _VP, _VP, _VP, _VP]),
     "gs_render_bwd": (C.c_int, [GsParams, _VP, GsCamera, GsProj, _VP, _VP, _VP, _VP, _VP, _VP, _VP, _VP, _U32, _VP,
                                 _SZ, _VP, _VP, _VP, _VP, _VP, _VP]),
     "gs_pose_grad": (C.c_int, [_VP, _VP, _I32, C.POINTER(GsPoseStep), _VP, _VP, _VP, _VP, _VP]),

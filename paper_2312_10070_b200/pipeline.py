@@ -180,7 +180,10 @@ class TrackingLoop:
     """K tracking iterations on one GPU, graph-captured."""
 
     def __init__(self, params: Params, cam, tgt_color, tgt_depth, start_view, iters=100, lambda_color=1.0,
-                 lambda_depth=1.0, step=(2e-3, 1e-3, 0.9, 0.999, 1e-8), device="cuda"):
+                 lambda_depth=1.0, step=(2e-3, 1e-3, 0.9, 0.999, 1e-8), device="cuda", masked=None):
+        """masked: None for the L1 colour + depth loss of BJ.configs[2], or
+        (lambda_c, inlier_mult) for the masked tracking loss of Eq. 15."""
+        self.masked = masked
         self.params = params
         self.r = Rasterizer(params.n, cam, device=device)
         self.tc, self.td = tgt_color, tgt_depth
@@ -201,7 +204,10 @@ class TrackingLoop:
     def iteration(self):
         r = self.r
         r.forward(self.params, self.view)
-        r.compute_loss(self.tc, self.td, None, self.lc, self.ld)
+        if self.masked is None:
+            r.compute_loss(self.tc, self.td, None, self.lc, self.ld)
+        else:
+            r.compute_tracking_loss(self.tc, self.td, *self.masked)
         r.backward(self.params, self.view, GS_GRAD_POSE)
         r.pose_grad(self.view, self.stepcfg, self.adam, dL_dtwist=self.dtwist)
 
@@ -235,4 +241,5 @@ class TrackingLoop:
             self.graph.replay()
 
     def launches_per_iter(self):
-        return kernels_per_view(self.r.cam) + 1
+        # masked loss: 6 kernels (residual + digit 0, 3 digit passes, apply, final) instead of 3
+        return kernels_per_view(self.r.cam) + 1 + (3 if self.masked is not None else 0)

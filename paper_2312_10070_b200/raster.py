@@ -19,7 +19,7 @@ from . import _lib
 from ._lib import GS_BWD_GAUSS_ONLY, GS_BWD_PIXELS_ONLY, GS_GRAD_PARAMS, GS_GRAD_POSE, GsCamera, GsError, GsParams, GsPoseStep, GsProj, check, lib
 
 __all__ = ["Params", "Grads", "Proj", "Frame", "Rasterizer", "camera", "gs_project", "gs_bin_sort",
-           "gs_render_fwd", "gs_tile_order", "gs_loss", "gs_render_bwd", "gs_pose_grad", "GS_GRAD_PARAMS", "GS_GRAD_POSE", "GS_BWD_PIXELS_ONLY", "GS_BWD_GAUSS_ONLY",
+           "gs_render_fwd", "gs_tile_order", "gs_loss", "gs_tracking_loss", "gs_render_bwd", "gs_pose_grad", "GS_GRAD_PARAMS", "GS_GRAD_POSE", "GS_BWD_PIXELS_ONLY", "GS_BWD_GAUSS_ONLY",
            "GsError", "device_check"]
 
 
@@ -166,6 +166,13 @@ def gs_loss(cam: GsCamera, color, depth, tgt_color, tgt_depth, weight, lambda_co
                         _p(dL_ddepth), _stream(stream)), "gs_loss")
 
 
+def gs_tracking_loss(cam: GsCamera, color, depth, alpha, tgt_color, tgt_depth, lambda_c, inlier_mult, ws, loss,
+                     dL_dcolor, dL_ddepth, stream=None):
+    check(lib().gs_tracking_loss(cam, _p(color), _p(depth), _p(alpha), _p(tgt_color), _p(tgt_depth), float(lambda_c),
+                                 float(inlier_mult), _p(ws), ws.numel() * ws.element_size(), _p(loss),
+                                 _p(dL_dcolor), _p(dL_ddepth), _stream(stream)), "gs_tracking_loss")
+
+
 def gs_render_bwd(params: Params, view, cam: GsCamera, proj: Proj, sorted_idx, tile_range, T_final, n_contrib,
                   dL_dcolor, dL_ddepth, dL_dalpha, flags, ws, grads: Grads = None, pose_partials=None,
                   stream=None, event_pair=None, tile_order=None):
@@ -222,6 +229,8 @@ class Rasterizer:
         self.loss_ws = torch.empty((L.gs_loss_workspace_bytes(self.cam) + 15) // 16 * 4, dtype=torch.float32,
                                    device=device)
         self.loss = torch.zeros(3, dtype=torch.float32, device=device)
+        self.tl_ws = None  # gs_tracking_loss workspace, allocated on first use
+        self.tl_loss = None
         self.dL_dcolor = torch.zeros(3, H, W, dtype=torch.float32, device=device)
         self.dL_ddepth = torch.zeros(H, W, dtype=torch.float32, device=device)
         # zeroed once; gs_render_bwd returns it zeroed (include/gs.h)
@@ -284,6 +293,18 @@ class Rasterizer:
         gs_loss(self.cam, self.frame.color, self.frame.depth, tgt_color, tgt_depth, weight, lambda_color,
                 lambda_depth, self.loss_ws, self.loss, self.dL_dcolor, self.dL_ddepth)
         return self.loss
+
+    def compute_tracking_loss(self, tgt_color, tgt_depth, lambda_c=0.5, inlier_mult=50.0):
+        """Eq. 15 masked tracking loss into self.tl_loss = (L, med_c, med_d,
+        inliers) and the gradient maps used by backward()."""
+        if self.tl_ws is None:
+            L = lib()
+            self.tl_ws = torch.empty((L.gs_tracking_loss_workspace_bytes(self.cam) + 15) // 16 * 4,
+                                     dtype=torch.float32, device=self.device)
+            self.tl_loss = torch.zeros(4, dtype=torch.float32, device=self.device)
+        gs_tracking_loss(self.cam, self.frame.color, self.frame.depth, self.frame.alpha, tgt_color, tgt_depth,
+                         lambda_c, inlier_mult, self.tl_ws, self.tl_loss, self.dL_dcolor, self.dL_ddepth)
+        return self.tl_loss
 
     def backward(self, params: Params, view, flags=GS_GRAD_PARAMS, grads: Grads = None, dL_dcolor=None,
                  dL_ddepth=None, dL_dalpha=None, event_pair=None):
