@@ -112,7 +112,8 @@ struct BwdPix {
 // (the 1/2 of dsigma/dA and dsigma/dC is applied once, by the writing lane)
 template <bool kParams>
 __device__ __forceinline__ void bwd_entry(BwdPix &s, const float2 e[2], const bool pass[kBPX], float4 c, float4 cn,
-                                          float2 ul, float fpy, const float2 fx[2], float *dst, float *red) {
+                                          float2 ul, float fpy, const float2 fx[2], float *dst, float *red, int rv,
+                                          int rp) {
   const float dy = ul.y - fpy;  // Delta = mu^I - pixel; one row: dy is shared
   // per-thread sums over its pixels (as pair sums) of ga = alpha dL/dalpha
   // (0 if clamped) and ga dx, ga dx^2; dsigma/d(u, v, A, B, C) and
@@ -181,23 +182,21 @@ __device__ __forceinline__ void bwd_entry(BwdPix &s, const float2 e[2], const bo
     // row l (stride 11: conflict-free both ways); lane 3v + p (v < 10, p < 3)
     // sums value v over the rows = p mod 3, the 3 partial sums meet by two
     // shuffles, lane 3v adds the total to grad2d
+    // (rv, rp) = (lane / 3, lane % 3); row 32 of the slab is zero, so every
+    // lane sums 11 rows without bounds checks (lanes 30, 31 sum column 10,
+    // the padding, and never write)
     const int lane = threadIdx.x & 31;
     float *row = red + lane * 11;
 #pragma unroll
     for (int v = 0; v < 10; ++v) row[v] = acc[v];
     __syncwarp();
-    const int v = lane / 3, p = lane - 3 * v;
     float part = 0.f;
-    if (lane < 30) {
+    const float *col = red + rp * 11 + rv;
 #pragma unroll
-      for (int t = 0; t < 11; ++t) {
-        const int i = p + 3 * t;
-        if (i < 32) part += red[i * 11 + v];
-      }
-    }
+    for (int t = 0; t < 11; ++t) part += col[t * 33];
     part += __shfl_down_sync(0xffffffffu, part, 1) + __shfl_down_sync(0xffffffffu, part, 2);
-    if (lane < 30 && p == 0 && (kParams || v < 6))
-      atomicAdd(dst + (v < 7 ? v : v + 1), (v == 2 || v == 4) ? 0.5f * part : part);
+    if (lane < 30 && rp == 0 && (kParams || rv < 6))
+      atomicAdd(dst + (rv < 7 ? rv : rv + 1), (rv == 2 || rv == 4) ? 0.5f * part : part);
     return;
   }
   int idx;
@@ -209,19 +208,25 @@ __device__ __forceinline__ void bwd_entry(BwdPix &s, const float2 e[2], const bo
   }
 }
 
+// one staged list entry of the backward
+struct __align__(16) BwdRec {
+  float4 p;      // entry terms (a', b', d', K)
+  float4 rgbz;   // colour, camera depth
+  float4 conic;  // (A, B, C, o)
+  float2 q;      // (DV, log2 o)
+  float2 uv;     // tile-local mean
+  int idx, pad[3];
+};
+
 template <bool kParams, bool kAlphaUp>
 __global__ void __launch_bounds__(BG::kThreads) k_bwd_pixels(BwdArgs a) {
-  // slot kBatch of s_p / s_q is a sentinel entry whose exponent is -inf
-  __shared__ int s_idx[kBatch];
-  __shared__ float4 s_p[kBatch + 1];
-  __shared__ float2 s_q[kBatch + 1];
-  __shared__ float2 s_uv[kBatch];
-  __shared__ float4 s_rgbz[kBatch];
-  __shared__ float4 s_conic[kBatch];
+  // one staged record per entry (one base address + immediate offsets);
+  // record kBatch is a sentinel entry whose exponent is -inf
+  __shared__ BwdRec s_rec[kBatch + 1];
   __shared__ unsigned char s_mask[kBatch];
   __shared__ unsigned char s_list[BG::kWarps][kBatch + 2];
   __shared__ int s_lmax;
-  __shared__ float s_red[BG::kWarps][2][32 * 11];  // per-warp reduction slabs (double-buffered)
+  __shared__ float s_red[BG::kWarps][2][33 * 11];  // per-warp reduction slabs (double-buffered; row 32 = 0)
   int rbuf = 0;
   const int tile = a.tile_order ? __ldg(a.tile_order + blockIdx.x) : int(blockIdx.x);
   const int tx = tile % a.TX, ty = tile / a.TX;
@@ -263,8 +268,12 @@ __global__ void __launch_bounds__(BG::kThreads) k_bwd_pixels(BwdArgs a) {
   }
   if (threadIdx.x == 0) {
     s_lmax = 0;
-    s_p[kBatch] = make_float4(0.f, 0.f, 0.f, 0.f);
-    s_q[kBatch] = make_float2(0.f, -INFINITY);
+    s_rec[kBatch].p = make_float4(0.f, 0.f, 0.f, 0.f);
+    s_rec[kBatch].q = make_float2(0.f, -INFINITY);
+  }
+  for (int i = threadIdx.x; i < BG::kWarps * 2 * 11; i += blockDim.x) {
+    const int ww = i / 22, bb = (i / 11) % 2, c = i % 11;
+    s_red[ww][bb][32 * 11 + c] = 0.f;
   }
   __syncthreads();
   // warp-level bound: entries at or beyond every lane's n_contrib are skipped
@@ -275,6 +284,7 @@ __global__ void __launch_bounds__(BG::kThreads) k_bwd_pixels(BwdArgs a) {
   __syncthreads();
   const int lmax = s_lmax;
   unsigned char *list = s_list[w];
+  const int rv = (threadIdx.x & 31) / 3, rp = (threadIdx.x & 31) % 3;  // reduction lane roles
   for (int end = lmax; end > 0; end -= kBatch) {
     const int beg = max(end - kBatch, 0);
     __syncthreads();
@@ -288,12 +298,13 @@ __global__ void __launch_bounds__(BG::kThreads) k_bwd_pixels(BwdArgs a) {
         const float4 cf = __ldg(a.coef + g);
         const float ul = float(u.x - ox), vl = float(u.y - oy);
         const EntryTerms et = entry_terms(cf, ul, vl);
-        s_idx[i] = g;
-        s_p[i] = et.p;
-        s_q[i] = et.q;
-        s_uv[i] = make_float2(ul, vl);
-        s_rgbz[i] = __ldg(a.rgbz + g);
-        s_conic[i] = __ldg(a.conic_o + g);
+        BwdRec &rc = s_rec[i];
+        rc.p = et.p;
+        rc.q = et.q;
+        rc.uv = make_float2(ul, vl);
+        rc.rgbz = __ldg(a.rgbz + g);
+        rc.conic = __ldg(a.conic_o + g);
+        rc.idx = g;
         s_mask[i] = (unsigned char)box_block_mask<BG>(entry_box(cf, ul, vl));
       }
     }
@@ -306,8 +317,8 @@ __global__ void __launch_bounds__(BG::kThreads) k_bwd_pixels(BwdArgs a) {
     const int nh = warp_hit_list(s_mask, min(end, wmax) - beg, list + 1, kBatch);
     for (int kk = nh; kk >= 1; kk -= 2) {
       const int ja = list[kk], jb = list[kk - 1];
-      const RowTerms ra = row_terms(s_p[ja], s_q[ja], pg.fpy);
-      const RowTerms rb = row_terms(s_p[jb], s_q[jb], pg.fpy);
+      const RowTerms ra = row_terms(s_rec[ja].p, s_rec[ja].q, pg.fpy);
+      const RowTerms rb = row_terms(s_rec[jb].p, s_rec[jb].q, pg.fpy);
       float2 ea[2], eb[2];
 #pragma unroll
       for (int h = 0; h < 2; ++h) {
@@ -326,8 +337,9 @@ __global__ void __launch_bounds__(BG::kThreads) k_bwd_pixels(BwdArgs a) {
           pass[2 * h + 1] = pos < s.last[2 * h + 1] && e[h].y >= kExpSkip;
         }
         if (!__any_sync(0xffffffffu, pass[0] || pass[1] || pass[2] || pass[3])) continue;
-        bwd_entry<kParams>(s, e, pass, s_rgbz[j], s_conic[j], s_uv[j], pg.fpy, fx, a.grad2d + size_t(s_idx[j]) * kG2,
-                           s_red[w][rbuf]);
+        const BwdRec &rc = s_rec[j];
+        bwd_entry<kParams>(s, e, pass, rc.rgbz, rc.conic, rc.uv, pg.fpy, fx, a.grad2d + size_t(rc.idx) * kG2,
+                           s_red[w][rbuf], rv, rp);
         rbuf ^= 1;
       }
     }

@@ -67,12 +67,18 @@ __device__ __forceinline__ void fwd_blend(FwdPix &s, float2 e, bool p0, bool p1,
   }
 }
 
+// one staged list entry of the forward
+struct __align__(16) FwdRec {
+  float4 p;     // entry terms (a', b', d', K)
+  float4 rgbz;  // colour, camera depth
+  float2 q;     // (DV, log2 o)
+  float2 pad;
+};
+
 template <bool kStats>
 __global__ void __launch_bounds__(FG::kThreads) k_render_fwd(FwdArgs a) {
-  // slot kBatch of s_p / s_q is a sentinel entry whose exponent is -inf
-  __shared__ float4 s_p[kBatch + 1];
-  __shared__ float2 s_q[kBatch + 1];
-  __shared__ float4 s_rgbz[kBatch];
+  // one staged record per entry; record kBatch is a sentinel entry whose exponent is -inf
+  __shared__ FwdRec s_rec[kBatch + 1];
   __shared__ unsigned char s_mask[kBatch];
   __shared__ unsigned char s_list[FG::kWarps][kBatch + 2];
   const int tile = a.tile_order ? __ldg(a.tile_order + blockIdx.x) : int(blockIdx.x);
@@ -83,8 +89,8 @@ __global__ void __launch_bounds__(FG::kThreads) k_render_fwd(FwdArgs a) {
   const int2 range = a.tile_range[tile];
   const float2 fx = make_float2(pg.fpx0, pg.fpx0 + 1.f);
   if (threadIdx.x == 0) {
-    s_p[kBatch] = make_float4(0.f, 0.f, 0.f, 0.f);
-    s_q[kBatch] = make_float2(0.f, -INFINITY);
+    s_rec[kBatch].p = make_float4(0.f, 0.f, 0.f, 0.f);
+    s_rec[kBatch].q = make_float2(0.f, -INFINITY);
   }
   // a pixel composites while T >= 1e-4 (include, then stop: T < 1e-4 happens
   // exactly at the stopping entry); pixels outside the image start with T = 0
@@ -106,9 +112,10 @@ __global__ void __launch_bounds__(FG::kThreads) k_render_fwd(FwdArgs a) {
         const float4 cf = __ldg(a.coef + g);
         const float ul = float(u.x - ox), vl = float(u.y - oy);
         const EntryTerms et = entry_terms(cf, ul, vl);
-        s_p[threadIdx.x] = et.p;
-        s_q[threadIdx.x] = et.q;
-        s_rgbz[threadIdx.x] = __ldg(a.rgbz + g);
+        FwdRec &rc = s_rec[threadIdx.x];
+        rc.p = et.p;
+        rc.q = et.q;
+        rc.rgbz = __ldg(a.rgbz + g);
         s_mask[threadIdx.x] = (unsigned char)box_block_mask<FG>(entry_box(cf, ul, vl));
       }
     }
@@ -123,15 +130,15 @@ __global__ void __launch_bounds__(FG::kThreads) k_render_fwd(FwdArgs a) {
     for (int k = 0; k < nh; k += 2) {
       if ((k & 31) == 0 && !__any_sync(0xffffffffu, s.live0 || s.live1)) break;
       const int ja = list[k], jb = list[k + 1];
-      const float2 ea = pair_exponent(row_terms(s_p[ja], s_q[ja], pg.fpy), fx);
-      const float2 eb = pair_exponent(row_terms(s_p[jb], s_q[jb], pg.fpy), fx);
+      const float2 ea = pair_exponent(row_terms(s_rec[ja].p, s_rec[ja].q, pg.fpy), fx);
+      const float2 eb = pair_exponent(row_terms(s_rec[jb].p, s_rec[jb].q, pg.fpy), fx);
       {
         const bool p0 = s.live0 && ea.x >= kExpSkip, p1 = s.live1 && ea.y >= kExpSkip;
-        if (__any_sync(0xffffffffu, p0 || p1)) fwd_blend<kStats>(s, ea, p0, p1, s_rgbz[ja], base + ja);
+        if (__any_sync(0xffffffffu, p0 || p1)) fwd_blend<kStats>(s, ea, p0, p1, s_rec[ja].rgbz, base + ja);
       }
       {
         const bool p0 = s.live0 && eb.x >= kExpSkip, p1 = s.live1 && eb.y >= kExpSkip;
-        if (__any_sync(0xffffffffu, p0 || p1)) fwd_blend<kStats>(s, eb, p0, p1, s_rgbz[jb], base + jb);
+        if (__any_sync(0xffffffffu, p0 || p1)) fwd_blend<kStats>(s, eb, p0, p1, s_rec[jb].rgbz, base + jb);
       }
     }
   }
