@@ -85,6 +85,7 @@ __device__ __forceinline__ void red_add_v4(float *addr, float x, float y, float 
 
 constexpr int kBPX = 4;   // pixels per thread in the backward (two fp32x2 pairs)
 constexpr bool kSmemReduce = true;  // per-entry warp sums through shared memory (else shuffles)
+constexpr int kBwdMinBlocks = 1;    // resident CTAs per SM the register budget must allow
 using BG = Geo<kBPX, 16>;  // 2 warps, 16x8 pixel strips
 
 __device__ __forceinline__ float rcp_approx(float x) {
@@ -187,6 +188,7 @@ __device__ __forceinline__ void bwd_entry(BwdPix &s, const float2 e[2], const bo
     // the padding, and never write)
     const int lane = threadIdx.x & 31;
     float *row = red + lane * 11;
+    __syncwarp();  // the previous entry's reads of the slab are done
 #pragma unroll
     for (int v = 0; v < 10; ++v) row[v] = acc[v];
     __syncwarp();
@@ -219,15 +221,14 @@ struct __align__(16) BwdRec {
 };
 
 template <bool kParams, bool kAlphaUp>
-__global__ void __launch_bounds__(BG::kThreads) k_bwd_pixels(BwdArgs a) {
+__global__ void __launch_bounds__(BG::kThreads, kBwdMinBlocks) k_bwd_pixels(BwdArgs a) {
   // one staged record per entry (one base address + immediate offsets);
   // record kBatch is a sentinel entry whose exponent is -inf
   __shared__ BwdRec s_rec[kBatch + 1];
   __shared__ unsigned char s_mask[kBatch];
   __shared__ unsigned char s_list[BG::kWarps][kBatch + 2];
   __shared__ int s_lmax;
-  __shared__ float s_red[BG::kWarps][2][33 * 11];  // per-warp reduction slabs (double-buffered; row 32 = 0)
-  int rbuf = 0;
+  __shared__ float s_red[BG::kWarps][33 * 11];  // per-warp reduction slabs (row 32 = 0)
   const int tile = a.tile_order ? __ldg(a.tile_order + blockIdx.x) : int(blockIdx.x);
   const int tx = tile % a.TX, ty = tile / a.TX;
   const int w = threadIdx.x >> 5;
@@ -271,10 +272,7 @@ __global__ void __launch_bounds__(BG::kThreads) k_bwd_pixels(BwdArgs a) {
     s_rec[kBatch].p = make_float4(0.f, 0.f, 0.f, 0.f);
     s_rec[kBatch].q = make_float2(0.f, -INFINITY);
   }
-  for (int i = threadIdx.x; i < BG::kWarps * 2 * 11; i += blockDim.x) {
-    const int ww = i / 22, bb = (i / 11) % 2, c = i % 11;
-    s_red[ww][bb][32 * 11 + c] = 0.f;
-  }
+  for (int i = threadIdx.x; i < BG::kWarps * 11; i += blockDim.x) s_red[i / 11][32 * 11 + i % 11] = 0.f;
   __syncthreads();
   // warp-level bound: entries at or beyond every lane's n_contrib are skipped
   int wmax = tmax;
@@ -339,8 +337,7 @@ __global__ void __launch_bounds__(BG::kThreads) k_bwd_pixels(BwdArgs a) {
         if (!__any_sync(0xffffffffu, pass[0] || pass[1] || pass[2] || pass[3])) continue;
         const BwdRec &rc = s_rec[j];
         bwd_entry<kParams>(s, e, pass, rc.rgbz, rc.conic, rc.uv, pg.fpy, fx, a.grad2d + size_t(rc.idx) * kG2,
-                           s_red[w][rbuf], rv, rp);
-        rbuf ^= 1;
+                           s_red[w], rv, rp);
       }
     }
   }
