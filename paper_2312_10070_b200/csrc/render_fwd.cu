@@ -76,7 +76,7 @@ struct __align__(16) FwdRec {
 };
 
 template <bool kStats>
-__global__ void __launch_bounds__(FG::kThreads) k_render_fwd(FwdArgs a) {
+__global__ void __launch_bounds__(FG::kThreads, 1) k_render_fwd(FwdArgs a) {
   // one staged record per entry; record kBatch is a sentinel entry whose exponent is -inf
   __shared__ FwdRec s_rec[kBatch + 1];
   __shared__ unsigned char s_mask[kBatch];
