@@ -14,17 +14,25 @@ struct ViewD {
   double R[9], t[3];
 };
 
+// camera fields promoted to fp64 once on the host (exact)
+struct CamD {
+  double fx, fy, cx, cy, zn, zf;
+};
+
 __global__ void __launch_bounds__(256) k_project(gs_params p, const gs_view *__restrict__ view,
-                                                 gs_camera cam, int TX, int TY, gs_proj out,
+                                                 CamD cam, int TX, int TY, gs_proj out,
                                                  gs_counters *cnt) {
+  // the view, promoted to fp64 once per block (exact)
+  __shared__ ViewD sV;
+  if (threadIdx.x < 12) {
+    const float f = __ldg(threadIdx.x < 9 ? &view->R[threadIdx.x] : &view->t[threadIdx.x - 9]);
+    (threadIdx.x < 9 ? sV.R[threadIdx.x] : sV.t[threadIdx.x - 9]) = (double)f;
+  }
+  __syncthreads();
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   bool culled = true, nonfinite = false;
   if (i < p.n) {
-    ViewD V;
-#pragma unroll
-    for (int k = 0; k < 9; ++k) V.R[k] = (double)__ldg(&view->R[k]);
-#pragma unroll
-    for (int k = 0; k < 3; ++k) V.t[k] = (double)__ldg(&view->t[k]);
+    const ViewD &V = sV;
     const float4 mo = __ldg(reinterpret_cast<const float4 *>(p.mean_opa) + i);
     const float4 qf = __ldg(reinterpret_cast<const float4 *>(p.quat) + i);
     const float4 lf = __ldg(reinterpret_cast<const float4 *>(p.logscale) + i);
@@ -37,7 +45,7 @@ __global__ void __launch_bounds__(256) k_project(gs_params p, const gs_view *__r
       pc[r] = ((V.R[3 * r] * mu[0] + V.R[3 * r + 1] * mu[1]) + V.R[3 * r + 2] * mu[2]) + V.t[r];
     const double qn = sqrt(((qin[0] * qin[0] + qin[1] * qin[1]) + qin[2] * qin[2]) + qin[3] * qin[3]);
     const double x = pc[0], y = pc[1], z = pc[2];
-    const double zn = (double)cam.z_near, zf = (double)cam.z_far;
+    const double zn = cam.zn, zf = cam.zf;
     if (!isfinite(x) || !isfinite(y) || !isfinite(z) || !isfinite(qn) || !(qn > 0.0)) {
       nonfinite = true;
     } else if (z >= zn && z <= zf) {  // near/far cull (R5)
@@ -67,8 +75,8 @@ __global__ void __launch_bounds__(256) k_project(gs_params p, const gs_view *__r
           Sig[3 * r + c] = (M[3 * r] * M[3 * c] + M[3 * r + 1] * M[3 * c + 1]) + M[3 * r + 2] * M[3 * c + 2];
       // pinhole pi (R4): u = fx x / z + cx
       const double fx = cam.fx, fy = cam.fy;
-      const double u = (fx * x) / z + (double)cam.cx;
-      const double v = (fy * y) / z + (double)cam.cy;
+      const double u = (fx * x) / z + cam.cx;
+      const double v = (fy * y) / z + cam.cy;
       // unclamped EWA Jacobian (Eq. 2, R6)
       const double z2 = z * z;
       const double J0 = fx / z, J2 = -(fx * x) / z2, J4 = fy / z, J5 = -(fy * y) / z2;
@@ -175,6 +183,7 @@ extern "C" int gs_project(gs_params p, const gs_view *view, gs_camera cam, gs_pr
   }
   const int threads = 256;
   const int blocks = (p.n + threads - 1) / threads;
-  k_project<<<blocks, threads, 0, as_stream(stream)>>>(p, view, cam, tiles_x(cam), tiles_y(cam), out, cnt);
+  const CamD cd{cam.fx, cam.fy, cam.cx, cam.cy, cam.z_near, cam.z_far};
+  k_project<<<blocks, threads, 0, as_stream(stream)>>>(p, view, cd, tiles_x(cam), tiles_y(cam), out, cnt);
   return check_launch("gs_project");
 }
