@@ -47,7 +47,7 @@ def parse():
     ap.add_argument("--no-tracking", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--profile", action="store_true", help="short run for ncu (no clocks/cpu/e2e/tracking)")
-    ap.add_argument("--lanes", type=int, default=4, help="CUDA streams the views are pipelined over")
+    ap.add_argument("--lanes", type=int, default=8, help="CUDA streams the views are pipelined over")
     return ap.parse_args()
 
 

@@ -530,10 +530,12 @@ __global__ void __launch_bounds__(kBucketThreads, 4) k_tile_sort(TileSortArgs a)
   for (int b = threadIdx.x; b < kBuckets; b += kBucketThreads) s.cnt[b] = 0u;
   if (threadIdx.x == 0) s.flag = 0;
   constexpr int kIt = kChunk / kBucketThreads;
+  const int items = (n + kBucketThreads - 1) / kBucketThreads;
   uint32_t key[kIt], val[kIt];
   uint32_t kmin = 0xffffffffu, kmax = 0u;
 #pragma unroll
   for (int k = 0; k < kIt; ++k) {
+    if (k >= items) break;  // block-uniform: only the rounds this list needs
     const int i = threadIdx.x + k * kBucketThreads;
     if (i < n) {
       val[k] = uint32_t(a.ids[r.x + i]);
@@ -562,6 +564,7 @@ __global__ void __launch_bounds__(kBucketThreads, 4) k_tile_sort(TileSortArgs a)
   uint16_t slot[kIt];
 #pragma unroll
   for (int k = 0; k < kIt; ++k) {
+    if (k >= items) break;  // block-uniform: only the rounds this list needs
     const int i = threadIdx.x + k * kBucketThreads;
     if (i < n) slot[k] = uint16_t(atomicAdd(&s.cnt[(key[k] - kmin) >> shift], 1u));
   }
@@ -591,6 +594,7 @@ __global__ void __launch_bounds__(kBucketThreads, 4) k_tile_sort(TileSortArgs a)
   // scatter into the buckets (unordered inside a bucket)
 #pragma unroll
   for (int k = 0; k < kIt; ++k) {
+    if (k >= items) break;  // block-uniform: only the rounds this list needs
     const int i = threadIdx.x + k * kBucketThreads;
     if (i < n) {
       const uint32_t pos = s.cnt[(key[k] - kmin) >> shift] + slot[k];
@@ -603,6 +607,7 @@ __global__ void __launch_bounds__(kBucketThreads, 4) k_tile_sort(TileSortArgs a)
   // exact key (depth bits, id): O(bucket size) per entry, no serial chain
 #pragma unroll
   for (int k = 0; k < kIt; ++k) {
+    if (k >= items) break;  // block-uniform: only the rounds this list needs
     const int i = threadIdx.x + k * kBucketThreads;
     if (i < n) {
       const uint32_t b = (key[k] - kmin) >> shift;

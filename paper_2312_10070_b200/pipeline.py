@@ -48,7 +48,7 @@ def shard_views(n_views, rank, world):
 class MapStep:
     """One mapping iteration over this rank's views.
 
-    Views are pipelined over `lanes` CUDA streams, each with its own
+    Views are pipelined over `lanes` CUDA streams (default 8: every view of a BJ.configs[3] step in flight), each with its own
     Rasterizer buffers: the latency-bound sort / loss kernels of one view
     overlap the compute-bound compositing kernels of another.  Only the
     per-Gaussian phase of gs_render_bwd (a read-modify-write of the shared
@@ -56,7 +56,7 @@ class MapStep:
     """
 
     def __init__(self, params: Params, views, cam, tgt_color, tgt_depth, rank=0, world=1, group=None,
-                 lambda_color=1.0, lambda_depth=1.0, device="cuda", lanes=4, allreduce=None):
+                 lambda_color=1.0, lambda_depth=1.0, device="cuda", lanes=8, allreduce=None):
         self.params = params
         self.views = views                  # [V, 12] device tensor (all views)
         self.V = views.shape[0]
