@@ -114,6 +114,33 @@ __device__ uint32_t block_excl_scan(uint32_t v, uint32_t *sh /* >= 33 */, uint32
   return r;
 }
 
+// In-place 2-D inclusive prefix (rows, then columns) of the TX x TY corner of
+// a shared (TY+1) x W1 difference array: per-tile counts.  One warp per row /
+// column, 32 elements per step (warp scan + carry).
+__device__ void prefix2d(uint32_t *c, int W1, int TX, int TY) {
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  for (int y = w; y < TY; y += nw) {
+    uint32_t carry = 0;
+    for (int x0 = 0; x0 < TX; x0 += 32) {
+      const int x = x0 + lane;
+      const uint32_t inc = warp_incl_scan(x < TX ? c[y * W1 + x] : 0u) + carry;
+      if (x < TX) c[y * W1 + x] = inc;
+      carry = __shfl_sync(0xffffffffu, inc, 31);
+    }
+  }
+  __syncthreads();
+  for (int x = w; x < TX; x += nw) {
+    uint32_t carry = 0;
+    for (int y0 = 0; y0 < TY; y0 += 32) {
+      const int y = y0 + lane;
+      const uint32_t inc = warp_incl_scan(y < TY ? c[y * W1 + x] : 0u) + carry;
+      if (y < TY) c[y * W1 + x] = inc;
+      carry = __shfl_sync(0xffffffffu, inc, 31);
+    }
+  }
+  __syncthreads();
+}
+
 // Lanes of `act` whose digit equals this lane's: one ballot per digit bit.
 // Every lane of the warp must call it.
 __device__ __forceinline__ unsigned peer_mask(unsigned act, uint32_t d) {
@@ -180,23 +207,7 @@ __global__ void __launch_bounds__(1024) k_tile_counts(TileArgs a) {
   if (threadIdx.x == 0) s_max = 0;
   if (threadIdx.x < 64) s_b[threadIdx.x] = 0;
   __syncthreads();
-  // rows, then columns: diff -> per-tile counts
-  for (int y = threadIdx.x; y < a.TY; y += blockDim.x) {
-    uint32_t run = 0;
-    for (int x = 0; x < a.TX; ++x) {
-      run += s_c[y * W1 + x];
-      s_c[y * W1 + x] = run;
-    }
-  }
-  __syncthreads();
-  for (int x = threadIdx.x; x < a.TX; x += blockDim.x) {
-    uint32_t run = 0;
-    for (int y = 0; y < a.TY; ++y) {
-      run += s_c[y * W1 + x];
-      s_c[y * W1 + x] = run;
-    }
-  }
-  __syncthreads();
+  prefix2d(s_c, W1, a.TX, a.TY);  // diff -> per-tile counts
   // exclusive scan over tiles (tile id = y*TX + x), PER consecutive tiles per thread
   const int PER = (a.T + blockDim.x - 1) / blockDim.x;
   uint32_t s = 0;
@@ -287,27 +298,25 @@ __global__ void __launch_bounds__(kEmitThreads) k_emit(const int32_t *__restrict
     }
   }
   __syncthreads();
-  for (int y = threadIdx.x; y < TY; y += blockDim.x) {
-    uint32_t run = 0;
-    for (int x = 0; x < TX; ++x) {
-      run += s_cur[y * W1 + x];
-      s_cur[y * W1 + x] = run;
+  prefix2d(s_cur, W1, TX, TY);
+  // one reservation per (block, tile); four independent atomics in flight per thread
+  for (int t0 = threadIdx.x; t0 < T; t0 += 4 * blockDim.x) {
+    uint32_t cnt[4], base[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int t = t0 + u * blockDim.x;
+      cnt[u] = t < T ? s_cur[(t / TX) * W1 + t % TX] : 0u;
     }
-  }
-  __syncthreads();
-  for (int x = threadIdx.x; x < TX; x += blockDim.x) {
-    uint32_t run = 0;
-    for (int y = 0; y < TY; ++y) {
-      run += s_cur[y * W1 + x];
-      s_cur[y * W1 + x] = run;
+#pragma unroll
+    for (int u = 0; u < 4; ++u) base[u] = cnt[u] ? atomicAdd(cursor + t0 + u * blockDim.x, cnt[u]) : 0u;
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int t = t0 + u * blockDim.x;
+      if (t < T) {
+        s_base[t] = base[u];
+        s_cur[(t / TX) * W1 + t % TX] = 0;
+      }
     }
-  }
-  __syncthreads();
-  for (int t = threadIdx.x; t < T; t += blockDim.x) {
-    const int c = (t / TX) * W1 + t % TX;
-    const uint32_t cnt = s_cur[c];
-    if (cnt) s_base[t] = atomicAdd(cursor + t, cnt);
-    s_cur[c] = 0;
   }
   __syncthreads();
 #pragma unroll
@@ -318,6 +327,8 @@ __global__ void __launch_bounds__(kEmitThreads) k_emit(const int32_t *__restrict
     const int incl = int(warp_incl_scan(uint32_t(nt)));
     const int total = __shfl_sync(0xffffffffu, incl, 31);
     const int xy = (int(r[k].x) & 0xffff) | (int(r[k].y) << 16);
+    // row = local / wdt as a multiply-high (exact for local, wdt < 2^16)
+    const uint32_t magic = wdt > 1 ? uint32_t((0x100000000ull + uint64_t(wdt) - 1) / uint64_t(wdt)) : 0u;
     for (int p0 = 0; p0 < total; p0 += 32) {
       const int p = p0 + lane;
       // j = number of lanes whose inclusive prefix is <= p
@@ -330,9 +341,11 @@ __global__ void __launch_bounds__(kEmitThreads) k_emit(const int32_t *__restrict
       j = min(j, 31);
       const int ij = __shfl_sync(0xffffffffu, incl, j), nj = __shfl_sync(0xffffffffu, nt, j);
       const int wj = __shfl_sync(0xffffffffu, wdt, j), xyj = __shfl_sync(0xffffffffu, xy, j);
+      const uint32_t mj = __shfl_sync(0xffffffffu, magic, j);
       if (p < total) {
         const int local = p - (ij - nj);
-        const int row = local / wj, col = local - row * wj;
+        const int row = wj == 1 ? local : (nj < 65536 ? int(__umulhi(uint32_t(local), mj)) : local / wj);
+        const int col = local - row * wj;
         const int x = (xyj & 0xffff) + col, y = (xyj >> 16) + row;
         const uint32_t pos = s_base[y * TX + x] + atomicAdd(s_cur + y * W1 + x, 1u);
         ids[pos] = i - lane + j;
