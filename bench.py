@@ -47,7 +47,9 @@ def parse():
     ap.add_argument("--no-tracking", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--profile", action="store_true", help="short run for ncu (no clocks/cpu/e2e/tracking)")
-    ap.add_argument("--lanes", type=int, default=8, help="CUDA streams the views are pipelined over")
+    ap.add_argument("--lanes", type=int, default=8, help="per-view buffer sets (and lane streams)")
+    ap.add_argument("--schedule", default="lanes", choices=["stages", "lanes"],
+                    help="stages: one stream per stage (software pipeline); lanes: one stream per view")
     return ap.parse_args()
 
 
@@ -136,7 +138,31 @@ def make_workload(cfg, device, rank, world):
     return s, P, views, tc, td
 
 
-def roofline_for(step, stats_views, peaks, sm_mhz, fwd_ms, bwd_ms):
+def union_ms(intervals):
+    """Length of the union of [t0, t1] intervals (ms)."""
+    tot, end = 0.0, None
+    for t0, t1 in sorted(intervals):
+        if end is None or t0 > end:
+            tot += t1 - t0
+            end = t1
+        elif t1 > end:
+            tot += t1 - end
+            end = t1
+    return tot
+
+
+def active_ms(step_ms, evs, per_step):
+    """Per step, the time at least one launch of a kernel is running: the
+    union of its launches' CUDA-event intervals (on their lane streams),
+    placed on the step's timeline by the step-start event."""
+    out = []
+    for i, (s0, _) in enumerate(step_ms):
+        iv = [(s0.elapsed_time(e0), s0.elapsed_time(e1)) for e0, e1 in evs[i * per_step:(i + 1) * per_step]]
+        out.append(union_ms(iv))
+    return statistics.mean(out)
+
+
+def roofline_for(step, stats_views, peaks, sm_mhz, fwd_ms, bwd_ms, fwd_active=None, bwd_active=None):
     """FP32-pipe roofline of the compositing kernels.
 
     Algorithmic flops: forward 10 s + 11 c per pixel, backward
@@ -156,12 +182,21 @@ def roofline_for(step, stats_views, peaks, sm_mhz, fwd_ms, bwd_ms):
     tp = os.path.join(ROOT, "profiles", "traffic.json")
     if os.path.exists(tp):  # dram bytes of the dominant kernel from the committed ncu --set full capture
         traffic = json.load(open(tp)).get("dram_bytes_per_launch")
-    for name, fl, ms in (("render_bwd_pixels", bwd_flops, bwd_ms), ("render_fwd", fwd_flops, fwd_ms)):
-        ach = fl / (ms * 1e-3) / 1e12 if ms else None
+    for name, fl, ms, act in (("render_bwd_pixels", bwd_flops, bwd_ms, bwd_active),
+                              ("render_fwd", fwd_flops, fwd_ms, fwd_active)):
+        if act is not None:  # in-step: all launches of the step over the time any of them runs
+            ach = fl * nv / (act * 1e-3) / 1e12 if act else None
+        else:  # one launch alone
+            ach = fl / (ms * 1e-3) / 1e12 if ms else None
         out[name] = {"bound": "alu", "achieved": ach, "peak": peak, "unit": "TFLOP/s",
                      "frac": ach / peak if ach else None,
                      "traffic": traffic if name == "render_bwd_pixels" else None, "flops_per_launch": fl,
                      "ms_per_launch": ms}
+        if act is not None:
+            out[name].update({"launches_per_step": nv, "ms_active_per_step": act,
+                              "method": "algorithmic flops of the step's launches of this kernel / the time at "
+                                        "least one of them runs (union of their CUDA-event intervals on the lane "
+                                        "streams); launches of different views overlap in the step"})
     return out
 
 
@@ -183,7 +218,7 @@ def bench_ours(a):
     sm_count = raster.device_check(local)
     s, P, views, tc, td = make_workload(a.config, device, rank, world)
     V = views.shape[0]
-    ms = MapStep(P, views, s.cam, tc, td, rank, world, group, device=device, lanes=a.lanes)
+    ms = MapStep(P, views, s.cam, tc, td, rank, world, group, device=device, lanes=a.lanes, schedule=a.schedule)
     ms.size()
     # per-view work counts for the roofline (untimed)
     stats_views = []
@@ -200,25 +235,27 @@ def bench_ours(a):
     # events around the dominant kernels inside the timed steps (on their lane stream)
     ev_fwd, ev_bwd = [], []
 
-    def timed_pixels(m, r, k, v):
+    def timed_fwd(r, k, v, tgt_ready=None):
         st = torch.cuda.current_stream()
-        r.project(m.params, m.views[v])
-        r.bin_sort()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record(st)
         raster.gs_render_fwd(r.proj, r.sorted_idx, r.tile_range, r.cam, r.frame, False, tile_order=r.tile_order,
                              tile_work=r.tile_work)
         e1.record(st)
         ev_fwd.append((e0, e1))
-        r.compute_loss(m.tgt_color[v], m.tgt_depth[v], None, m.lc, m.ld)
-        m.losses[k].copy_(r.loss)
-        b0, b1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         raster.gs_tile_order(r.tile_work, r.T, r.bwd_order)
-        r.backward(m.params, m.views[v], raster.GS_GRAD_PARAMS | raster.GS_BWD_PIXELS_ONLY, m.grads,
+        if tgt_ready is not None:
+            st.wait_event(tgt_ready)
+        r.compute_loss(ms.tgt_color[v], ms.tgt_depth[v], None, ms.lc, ms.ld)
+        ms.losses[k].copy_(r.loss)
+
+    def timed_bwd(r, k, v):
+        b0, b1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        r.backward(ms.params, ms.views[v], raster.GS_GRAD_PARAMS | raster.GS_BWD_PIXELS_ONLY, ms.grads,
                    event_pair=(b0, b1))
         ev_bwd.append((b0, b1))
 
-    hooks = (lambda r, k, v: timed_pixels(ms, r, k, v), ms.view_gauss)
+    hooks = {"fwd": timed_fwd, "bwd": timed_bwd}
 
     for _ in range(max(a.warmup, 3)):
         ms.step(hooks)
@@ -255,7 +292,9 @@ def bench_ours(a):
     value = mp / (ms_per_step * 1e-3)
     peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))) if os.path.exists(
         os.path.join(ROOT, "MEASURED_PEAKS.json")) else {}
-    roof = roofline_for(ms, stats_views, peaks, clocks.get("sm_mhz"), fwd_ms, bwd_ms)
+    nvw = len(ms.mine)
+    roof = roofline_for(ms, stats_views, peaks, clocks.get("sm_mhz"), fwd_ms, bwd_ms,
+                        active_ms(step_ms, ev_fwd, nvw), active_ms(step_ms, ev_bwd, nvw))
     # the same kernels timed alone (one view at a time, no other stream active)
     iso_f, iso_b = [], []
     r0 = ms.lanes[0]
@@ -293,7 +332,7 @@ def bench_ours(a):
                    "contrib_per_px": sum(x["contrib"] for x in stats_views) / (len(stats_views) * W * H)},
         "roofline": roof["render_bwd_pixels"],
         "roofline_other": {"render_fwd": roof["render_fwd"],
-                           "note": "in-step event times include sharing the GPU with the other pipeline lanes; "
+                           "note": "in-step: the lane streams run the views' launches concurrently; "
                                    "*_isolated = the same launch timed alone (median of 3 x views)",
                            "render_bwd_pixels_isolated": roof_iso["render_bwd_pixels"],
                            "render_fwd_isolated": roof_iso["render_fwd"]},

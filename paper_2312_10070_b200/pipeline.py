@@ -56,7 +56,7 @@ class MapStep:
     """
 
     def __init__(self, params: Params, views, cam, tgt_color, tgt_depth, rank=0, world=1, group=None,
-                 lambda_color=1.0, lambda_depth=1.0, device="cuda", lanes=8, allreduce=None):
+                 lambda_color=1.0, lambda_depth=1.0, device="cuda", lanes=8, allreduce=None, schedule="lanes"):
         self.params = params
         self.views = views                  # [V, 12] device tensor (all views)
         self.V = views.shape[0]
@@ -78,6 +78,8 @@ class MapStep:
         self.grads = Grads.zeros(params.n, device)
         self.losses = torch.zeros(max(len(self.mine), 1), 3, dtype=torch.float32, device=device)
         self.copy_stream = None
+        self.schedule = schedule
+        self.stage_streams = [torch.cuda.Stream(device=device) for _ in range(3)] if schedule == "stages" else []
 
     def size(self, slack=1.25):
         """Setup only (host sync): pair capacity = slack x max pairs over my views."""
@@ -93,39 +95,62 @@ class MapStep:
             r.set_capacity(int(best * slack) + 1024)
         return best
 
-    def view_pixels(self, r, k, v, tgt_ready=None):
-        """Everything of view v up to the per-pixel backward phase
-        (tgt_ready: event after which this view's targets are on the device)."""
-        r.forward(self.params, self.views[v])
+    # -- the four stages of one view ---------------------------------------------
+    def stage_front(self, r, k, v):
+        """S1 + S2: projection and binning."""
+        r.project(self.params, self.views[v])
+        r.bin_sort()
+
+    def stage_fwd(self, r, k, v, tgt_ready=None):
+        """S3 + S4: compositing, then the loss once the view's targets are on
+        the device (tgt_ready)."""
+        r.render()
         if tgt_ready is not None:
             torch.cuda.current_stream().wait_event(tgt_ready)
         r.compute_loss(self.tgt_color[v], self.tgt_depth[v], None, self.lc, self.ld)
         self.losses[k].copy_(r.loss)
+
+    def stage_bwd(self, r, k, v):
+        """S5: the per-pixel backward phase."""
         r.backward(self.params, self.views[v], GS_GRAD_PARAMS | GS_BWD_PIXELS_ONLY, self.grads)
 
-    def view_gauss(self, r, k, v):
+    def stage_gauss(self, r, k, v):
+        """S6: the per-Gaussian phase (+= into the shared gradient buffer)."""
         r.backward(self.params, self.views[v], GS_GRAD_PARAMS | GS_BWD_GAUSS_ONLY, self.grads)
 
     def step(self, hooks=None, host=None):
-        """hooks: optional (pixels_fn, gauss_fn) replacing view_pixels / view_gauss.
+        """One mapping iteration.  hooks: optional dict overriding stages
+        ("front", "fwd", "bwd", "gauss") with functions of the same signature.
+
+        Schedule "lanes" (default): view k runs all its stages on lane stream
+        k % lanes (8 lanes: every view of a BJ.configs[3] step in flight), so
+        the latency-bound binning of some views and the tails of the
+        compositing launches of others fill each other's idle SMs; only the
+        per-Gaussian phase is serialised (events) in view order.
+        Schedule "stages": front stages on the lane streams, then one stream
+        each for the forward, the per-pixel and the per-Gaussian backward (a
+        software pipeline: no two compositing launches of one kind overlap;
+        measured 8% slower on BJ.configs[3] because the compositing tails
+        then stay idle).
 
         host: optional HostInputs (pinned host buffers of this step's inputs).
         A copy stream uploads the parameters and poses, then every view's
-        RGB-D targets in view order; a lane waits for the parameters before
-        projecting and for its view's targets only before the loss, so the
-        target uploads overlap the projection, binning and compositing of the
-        views ahead.  The per-view losses are read back into host.loss."""
-        pix, gau = hooks if hooks is not None else (self.view_pixels, self.view_gauss)
+        RGB-D targets in view order; the front stage waits for the
+        parameters, the loss only for its view's targets, so the uploads
+        overlap compute.  The per-view losses are read back into host.loss."""
+        st = {"front": self.stage_front, "fwd": self.stage_fwd, "bwd": self.stage_bwd, "gauss": self.stage_gauss}
+        if hooks:
+            st.update(hooks)
         main = torch.cuda.current_stream()
-        tgt_ready = {}
+        tgt_ready = {v: None for v in self.mine}
         if host is not None:
             if self.copy_stream is None:
                 self.copy_stream = torch.cuda.Stream(device=self.params.mean_opa.device)
             cs = self.copy_stream
             cs.wait_stream(main)  # the previous step no longer reads these buffers
             with torch.cuda.stream(cs):
-                for k in ("mean_opa", "quat", "logscale", "rgb"):
-                    getattr(self.params, k).copy_(host.params[k], non_blocking=True)
+                for name in ("mean_opa", "quat", "logscale", "rgb"):
+                    getattr(self.params, name).copy_(host.params[name], non_blocking=True)
                 self.views.copy_(host.views, non_blocking=True)
                 params_ready = cs.record_event()
                 for v in self.mine:
@@ -135,21 +160,38 @@ class MapStep:
             main.wait_event(params_ready)
         self.grads.zero_()
         start = main.record_event()
-        for s in self.streams:
+        for s in self.streams + self.stage_streams:
             s.wait_event(start)
-        prev = start
-        for k, v in enumerate(self.mine):
-            lane = k % len(self.lanes)
-            s, r = self.streams[lane], self.lanes[lane]
-            with torch.cuda.stream(s):
-                if host is not None:
-                    pix(r, k, v, tgt_ready[v])
-                else:
-                    pix(r, k, v)
-                s.wait_event(prev)
-                gau(r, k, v)
-                prev = s.record_event()
-        for s in self.streams:
+        if self.schedule == "stages":
+            done = {}  # buffer set -> event after the last stage of the view that used it
+            for k, v in enumerate(self.mine):
+                lane = k % len(self.lanes)
+                r = self.lanes[lane]
+                ev = done.get(lane)  # view k reuses the buffers of view k - lanes
+                for i, name in enumerate(("front", "fwd", "bwd", "gauss")):
+                    s = self.streams[lane] if i == 0 else self.stage_streams[i - 1]
+                    if ev is not None:
+                        s.wait_event(ev)
+                    with torch.cuda.stream(s):
+                        if name == "fwd":
+                            st[name](r, k, v, tgt_ready[v])
+                        else:
+                            st[name](r, k, v)
+                        ev = s.record_event()
+                done[lane] = ev
+        else:
+            prev = start
+            for k, v in enumerate(self.mine):
+                lane = k % len(self.lanes)
+                s, r = self.streams[lane], self.lanes[lane]
+                with torch.cuda.stream(s):
+                    st["front"](r, k, v)
+                    st["fwd"](r, k, v, tgt_ready[v])
+                    st["bwd"](r, k, v)
+                    s.wait_event(prev)
+                    st["gauss"](r, k, v)
+                    prev = s.record_event()
+        for s in self.streams + self.stage_streams:
             main.wait_stream(s)
         if host is not None:
             main.wait_stream(self.copy_stream)

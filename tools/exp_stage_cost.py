@@ -13,28 +13,33 @@ import bench  # noqa: E402
 
 dev = torch.device("cuda")
 s, P, views, tc, td = bench.make_workload(3, dev, 0, 1)
-lanes = int(sys.argv[1]) if len(sys.argv) > 1 else 4
-ms = MapStep(P, views, s.cam, tc, td, device=dev, lanes=lanes)
+lanes = int(sys.argv[1]) if len(sys.argv) > 1 else 8
+sched = sys.argv[2] if len(sys.argv) > 2 else "lanes"
+ms = MapStep(P, views, s.cam, tc, td, device=dev, lanes=lanes, schedule=sched)
 ms.size()
 
 
 def make(skip):
-    def pix(r, k, v):
-        if "project" not in skip:
-            r.project(ms.params, ms.views[v])
-        if "sort" not in skip:
-            r.bin_sort()
+    noop = lambda *args: None
+    hooks = {}
+    if "project" in skip and "sort" in skip:
+        hooks["front"] = noop
+    elif "sort" in skip:
+        hooks["front"] = lambda r, k, v: r.project(ms.params, ms.views[v])
+    elif "project" in skip:
+        hooks["front"] = lambda r, k, v: r.bin_sort()
+
+    def fwd(r, k, v, tgt=None):
         if "fwd" not in skip:
             r.render()
         if "loss" not in skip:
             r.compute_loss(ms.tgt_color[v], ms.tgt_depth[v], None, ms.lc, ms.ld)
-        if "bwd" not in skip:
-            r.backward(ms.params, ms.views[v], raster.GS_GRAD_PARAMS | raster.GS_BWD_PIXELS_ONLY, ms.grads)
-
-    def gau(r, k, v):
-        if "gauss" not in skip:
-            ms.view_gauss(r, k, v)
-    return pix, gau
+    hooks["fwd"] = fwd
+    if "bwd" in skip:
+        hooks["bwd"] = noop
+    if "gauss" in skip:
+        hooks["gauss"] = noop
+    return hooks
 
 
 def timeit(hooks, n=20):
@@ -51,7 +56,7 @@ def timeit(hooks, n=20):
 
 
 base = timeit(make(set()))
-print(f"lanes {lanes}: full step {base:.3f} ms ({base / 8 * 1e3:.0f} us/view)")
+print(f"{sched} lanes {lanes}: full step {base:.3f} ms ({base / 8 * 1e3:.0f} us/view)")
 for sk in (["sort"], ["project", "sort"], ["loss"], ["gauss"], ["fwd"], ["bwd"], ["fwd", "bwd"],
            ["project", "sort", "loss", "gauss"]):
     t = timeit(make(set(sk)))

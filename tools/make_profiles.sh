@@ -1,18 +1,20 @@
 #!/bin/bash
 # On the GPU box: bench line, ncu launch list of the bench command, full ncu
-# captures of the two compositing kernels and the top binning kernel.
+# captures of the compositing kernels and the per-tile sort / emission.
 #   tools/make_profiles.sh <round-tag>
 set -u
 tag=${1:-r01}
 mkdir -p gpurun_out
 B="python bench.py --steps 3 --warmup 3 --no-cpu-baseline --no-tracking --no-e2e"
-timeout 600 python bench.py --steps 50 --warmup 5 > gpurun_out/${tag}_bench.json 2> gpurun_out/${tag}_bench.err
+timeout 900 python bench.py --steps 50 --warmup 5 > gpurun_out/${tag}_bench.json 2> gpurun_out/${tag}_bench.err
 echo "bench rc=$?"
 timeout 300 $B > gpurun_out/${tag}_plain.log 2>&1 && \
   timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv \
     --log-file gpurun_out/${tag}_launches.csv $B > gpurun_out/${tag}_ncu_list.log 2>&1
 echo "launch list rc=$?"
-for k in k_bwd_pixels k_render_fwd; do
-  timeout 400 tools/ncu_full.sh ${tag}_$k $k --reps 6; echo "$k rc=$?"
+for k in k_bwd_pixels k_render_fwd "^k_tile_sort$" "^k_emit$"; do
+  n=$(echo $k | tr -d '^$')
+  timeout 400 tools/ncu_full.sh ${tag}_$n "$k" --reps 6; echo "$n rc=$?"
+  python tools/ncu_summary.py gpurun_out/prof_${tag}_$n.ncu-rep 30 > gpurun_out/sum_${tag}_$n.txt 2>&1
 done
-SKIP=8 timeout 400 tools/ncu_full.sh ${tag}_k_rs_downsweep k_rs_downsweep --reps 3; echo "rs rc=$?"
+python tools/launches.py gpurun_out/${tag}_launches.csv > gpurun_out/${tag}_launches_one_view.txt 2>&1
