@@ -246,7 +246,7 @@ def bench_ours(a):
         raster.gs_tile_order(r.tile_work, r.T, r.bwd_order)
         if tgt_ready is not None:
             st.wait_event(tgt_ready)
-        r.compute_loss(ms.tgt_color[v], ms.tgt_depth[v], None, ms.lc, ms.ld)
+        r.compute_loss(ms.tgt_color[v], ms.tgt_depth[v], None, ms.lc, ms.ld, ms.ssim)
         ms.losses[k].copy_(r.loss)
 
     def timed_bwd(r, k, v):
@@ -338,6 +338,25 @@ def bench_ours(a):
                            "render_fwd_isolated": roof_iso["render_fwd"]},
         "clocks": clocks, "gpu_launches": launches, "sm_count": sm_count,
     }
+    if not a.profile:  # the same step with Eq. 10's SSIM colour term (lambda = 0.2), every rank
+        ms.ssim = 0.2
+        for _ in range(3):
+            ms.step()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        nss = max(3, a.steps // 2)
+        for _ in range(nss):
+            ms.step()
+        e1.record(stream)
+        torch.cuda.synchronize()
+        ms.ssim = 0.0
+        t_ss = torch.tensor([e0.elapsed_time(e1) / nss], dtype=torch.float64, device=device)
+        if world > 1:
+            dist.all_reduce(t_ss, op=dist.ReduceOp.MAX)
+        line["mapping_ssim"] = {"metric": METRIC + ", colour loss with Eq. 10's SSIM term (lambda = 0.2)",
+                                "value": mp / (float(t_ss.item()) * 1e-3), "unit": UNIT,
+                                "ms_per_step": float(t_ss.item())}
     if not a.profile and not a.no_e2e:  # every rank: the step contains the all-reduce
         line["e2e"] = e2e_ours(a, s, ms, device, world)
     if world > 1:

@@ -276,6 +276,28 @@ int gs_tracking_loss(gs_camera cam, const float *color, const float *depth, cons
                      float inlier_mult, void *ws, size_t ws_bytes, float *loss,
                      float *dL_dcolor, float *dL_ddepth, void *stream);
 
+/* NEXT(2) — SSIM term of the colour loss (Eq. 10: L_color =
+ * (1 - lambda) |C^ - C*|_1 + lambda (1 - SSIM(C^, C*)), lambda = 0.2;
+ * S:266-274; R32-R33).
+ *
+ * SSIM per Wang et al. 2004 (the paper's [wang2004image]): per channel and
+ * pixel, local means / variances / covariance under an 11x11 Gaussian window
+ * (sigma 1.5, normalised) applied as a zero-padded "same" correlation,
+ * C1 = 0.01^2, C2 = 0.03^2; SSIM = the mean of the SSIM map over 3HW.
+ *   color, tgt_color (device) [3][H][W]
+ *   weight   the loss weight w of the SSIM term (lambda_color * lambda)
+ *   ws       (device) >= gs_ssim_workspace_bytes(cam)
+ *   loss     (device) [4]: loss[0] += w (1 - SSIM), loss[3] = SSIM
+ *   dL_dcolor (device) [3][H][W]: += -w dSSIM/dC^ (analytic, through the
+ *            local statistics)
+ * Call it after gs_loss with lambda_color * (1 - lambda) as gs_loss's colour
+ * weight to get Eq. 10 + Eq. 12 (R33).  The SSIM value is a fixed-order
+ * reduction (deterministic); the gradient is per-pixel (no atomics).
+ * Errors: GS_ERR_INVALID_ARG (null, weight < 0), GS_ERR_WORKSPACE. */
+size_t gs_ssim_workspace_bytes(gs_camera cam);
+int gs_ssim(gs_camera cam, const float *color, const float *tgt_color, float weight, void *ws,
+            size_t ws_bytes, float *loss, float *dL_dcolor, void *stream);
+
 /* S5+S6 — backward (Eqs. 7-8; R16, R17).
  *
  * Per pixel, replays the composited entries back to front (same alpha

@@ -66,6 +66,8 @@ _PROTOS = {
     "gs_tile_order": (C.c_int, [_VP, _I32, _VP, _VP]),
     "gs_loss": (C.c_int, [GsCamera, _VP, _VP, _VP, _VP, _VP, _F, _F, _VP, _SZ, _VP, _VP, _VP, _VP]),
     "gs_tracking_loss_workspace_bytes": (_SZ, [GsCamera]),
+    "gs_ssim_workspace_bytes": (_SZ, [GsCamera]),
+    "gs_ssim": (C.c_int, [GsCamera, _VP, _VP, _F, _VP, _SZ, _VP, _VP, _VP]),
     "gs_tracking_loss": (C.c_int, [GsCamera, _VP, _VP, _VP, _VP, _VP, _F, _F, _VP, _SZ, _VP, _VP, _VP, _VP]),
     "gs_render_bwd": (C.c_int, [GsParams, _VP, GsCamera, GsProj, _VP, _VP, _VP, _VP, _VP, _VP, _VP, _VP, _U32, _VP,
                                 _SZ, _VP, _VP, _VP, _VP, _VP, _VP]),

@@ -30,7 +30,7 @@ class HostInputs:
         self.views = pin(views)
         self.tgt_color = {v: pin(tgt_color[v]) for v in mine}
         self.tgt_depth = {v: pin(tgt_depth[v]) for v in mine}
-        self.loss = torch.empty(n_losses, 3, dtype=torch.float32).pin_memory()
+        self.loss = torch.empty(n_losses, 4, dtype=torch.float32).pin_memory()
 
     def h2d_bytes(self):
         b = sum(t.numel() * t.element_size() for t in self.params.values()) + self.views.numel() * 4
@@ -56,7 +56,11 @@ class MapStep:
     """
 
     def __init__(self, params: Params, views, cam, tgt_color, tgt_depth, rank=0, world=1, group=None,
-                 lambda_color=1.0, lambda_depth=1.0, device="cuda", lanes=8, allreduce=None, schedule="lanes"):
+                 lambda_color=1.0, lambda_depth=1.0, device="cuda", lanes=8, allreduce=None, schedule="lanes",
+                 ssim=0.0):
+        """ssim: the lambda of Eq. 10's colour loss (0: L1 colour only, as
+        BJ.configs[3]; the paper uses 0.2)."""
+        self.ssim = ssim
         self.params = params
         self.views = views                  # [V, 12] device tensor (all views)
         self.V = views.shape[0]
@@ -76,7 +80,8 @@ class MapStep:
         self.streams = [torch.cuda.Stream(device=device) for _ in range(nl)]
         self.r = self.lanes[0]
         self.grads = Grads.zeros(params.n, device)
-        self.losses = torch.zeros(max(len(self.mine), 1), 3, dtype=torch.float32, device=device)
+        # per view: (total, L1 colour, L1 depth, SSIM if ssim > 0)
+        self.losses = torch.zeros(max(len(self.mine), 1), 4, dtype=torch.float32, device=device)
         self.copy_stream = None
         self.schedule = schedule
         self.stage_streams = [torch.cuda.Stream(device=device) for _ in range(3)] if schedule == "stages" else []
@@ -107,7 +112,7 @@ class MapStep:
         r.render()
         if tgt_ready is not None:
             torch.cuda.current_stream().wait_event(tgt_ready)
-        r.compute_loss(self.tgt_color[v], self.tgt_depth[v], None, self.lc, self.ld)
+        r.compute_loss(self.tgt_color[v], self.tgt_depth[v], None, self.lc, self.ld, self.ssim)
         self.losses[k].copy_(r.loss)
 
     def stage_bwd(self, r, k, v):

@@ -19,7 +19,7 @@ from . import _lib
 from ._lib import GS_BWD_GAUSS_ONLY, GS_BWD_PIXELS_ONLY, GS_GRAD_PARAMS, GS_GRAD_POSE, GsCamera, GsError, GsParams, GsPoseStep, GsProj, check, lib
 
 __all__ = ["Params", "Grads", "Proj", "Frame", "Rasterizer", "camera", "gs_project", "gs_bin_sort",
-           "gs_render_fwd", "gs_tile_order", "gs_loss", "gs_tracking_loss", "gs_render_bwd", "gs_pose_grad", "GS_GRAD_PARAMS", "GS_GRAD_POSE", "GS_BWD_PIXELS_ONLY", "GS_BWD_GAUSS_ONLY",
+           "gs_render_fwd", "gs_tile_order", "gs_loss", "gs_tracking_loss", "gs_ssim", "gs_render_bwd", "gs_pose_grad", "GS_GRAD_PARAMS", "GS_GRAD_POSE", "GS_BWD_PIXELS_ONLY", "GS_BWD_GAUSS_ONLY",
            "GsError", "device_check"]
 
 
@@ -173,6 +173,11 @@ def gs_tracking_loss(cam: GsCamera, color, depth, alpha, tgt_color, tgt_depth, l
                                  _p(dL_dcolor), _p(dL_ddepth), _stream(stream)), "gs_tracking_loss")
 
 
+def gs_ssim(cam: GsCamera, color, tgt_color, weight, ws, loss, dL_dcolor, stream=None):
+    check(lib().gs_ssim(cam, _p(color), _p(tgt_color), float(weight), _p(ws), ws.numel() * ws.element_size(),
+                        _p(loss), _p(dL_dcolor), _stream(stream)), "gs_ssim")
+
+
 def gs_render_bwd(params: Params, view, cam: GsCamera, proj: Proj, sorted_idx, tile_range, T_final, n_contrib,
                   dL_dcolor, dL_ddepth, dL_dalpha, flags, ws, grads: Grads = None, pose_partials=None,
                   stream=None, event_pair=None, tile_order=None):
@@ -228,7 +233,8 @@ class Rasterizer:
         self.frame = Frame(H, W, device)
         self.loss_ws = torch.empty((L.gs_loss_workspace_bytes(self.cam) + 15) // 16 * 4, dtype=torch.float32,
                                    device=device)
-        self.loss = torch.zeros(3, dtype=torch.float32, device=device)
+        self.loss = torch.zeros(4, dtype=torch.float32, device=device)  # total, L1 colour, depth, SSIM
+        self.ssim_ws = None
         self.tl_ws = None  # gs_tracking_loss workspace, allocated on first use
         self.tl_loss = None
         self.dL_dcolor = torch.zeros(3, H, W, dtype=torch.float32, device=device)
@@ -289,9 +295,18 @@ class Rasterizer:
         self.render(stats)
         return self.frame
 
-    def compute_loss(self, tgt_color, tgt_depth, weight=None, lambda_color=1.0, lambda_depth=1.0):
-        gs_loss(self.cam, self.frame.color, self.frame.depth, tgt_color, tgt_depth, weight, lambda_color,
-                lambda_depth, self.loss_ws, self.loss, self.dL_dcolor, self.dL_ddepth)
+    def compute_loss(self, tgt_color, tgt_depth, weight=None, lambda_color=1.0, lambda_depth=1.0, ssim=0.0):
+        """Eq. 12 with the L1 colour term (ssim = 0, BJ.configs) or Eq. 10's
+        (1 - ssim) L1 + ssim (1 - SSIM) colour loss (ssim = 0.2 in the paper).
+        self.loss = (total, L1 colour, L1 depth, SSIM)."""
+        gs_loss(self.cam, self.frame.color, self.frame.depth, tgt_color, tgt_depth, weight,
+                lambda_color * (1.0 - ssim), lambda_depth, self.loss_ws, self.loss, self.dL_dcolor, self.dL_ddepth)
+        if ssim > 0.0:
+            if self.ssim_ws is None:
+                self.ssim_ws = torch.empty((lib().gs_ssim_workspace_bytes(self.cam) + 15) // 16 * 4,
+                                           dtype=torch.float32, device=self.device)
+            gs_ssim(self.cam, self.frame.color, tgt_color, lambda_color * ssim, self.ssim_ws, self.loss,
+                    self.dL_dcolor)
         return self.loss
 
     def compute_tracking_loss(self, tgt_color, tgt_depth, lambda_c=0.5, inlier_mult=50.0):

@@ -122,7 +122,7 @@ def test_tracking_first_iteration_pose_gradient():
     dview = torch.zeros(12, device=d)
     r.pose_grad(v, dL_dview=dview)
     torch.cuda.synchronize()
-    assert np.allclose(to_np(r.loss), L, rtol=1e-5)
+    assert np.allclose(to_np(r.loss)[:3], L, rtol=1e-5)
     ok, st = grad_check(to_np(dview), ob["pose"], ob["mpose"])
     assert ok.all(), (st, to_np(dview), ob["pose"])
 

@@ -1,0 +1,92 @@
+"""Parity of gs_ssim (Eq. 10's SSIM term, NEXT(2)) with the fp64 oracle on the
+same fp32 images: SSIM within 2e-6 absolute (fp32 local statistics), the
+gradient map within 1e-4 of its largest entry (fp32 two-pass separable
+correlation vs fp64)."""
+import numpy as np
+import pytest
+import torch
+
+from oracle import ssim as OS
+from paper_2312_10070_b200 import Params, Rasterizer, inputs
+from paper_2312_10070_b200.raster import camera, gs_ssim, lib
+
+pytestmark = pytest.mark.gpu
+
+
+def _gpu_ssim(x, y, weight=1.0):
+    dev = torch.device("cuda:0")
+    _, H, W = x.shape
+    cam = camera(inputs.Camera(W, H, 1.0, 1.0, 0.0, 0.0))
+    ws = torch.empty((lib().gs_ssim_workspace_bytes(cam) + 15) // 16 * 4, dtype=torch.float32, device=dev)
+    loss = torch.zeros(4, dtype=torch.float32, device=dev)
+    g = torch.zeros(3, H, W, dtype=torch.float32, device=dev)
+    t = lambda a: torch.as_tensor(np.ascontiguousarray(a, np.float32), device=dev)
+    gs_ssim(cam, t(x), t(y), weight, ws, loss, g)
+    torch.cuda.synchronize()
+    return loss.cpu().numpy(), g.cpu().numpy()
+
+
+def _check(x, y, w=0.7):
+    x32, y32 = x.astype(np.float32), y.astype(np.float32)
+    loss, g = _gpu_ssim(x32, y32, w)
+    s = OS.ssim(x32, y32)
+    assert abs(loss[3] - s) <= 2e-6
+    assert abs(loss[0] - w * (1 - s)) <= 2e-6
+    want = -w * OS.ssim_grad(x32, y32)
+    scale = max(np.abs(want).max(), w / x.size)  # at a stationary point (x = y) the floor is w / 3HW
+    assert np.abs(g - want).max() <= 1e-4 * scale
+    return s
+
+
+@pytest.mark.parametrize("shape", [(48, 64), (29, 37), (16, 16), (5, 7)])
+def test_ssim_parity_random(shape):
+    rng = np.random.default_rng(shape[0])
+    x = rng.uniform(0, 1, (3,) + shape)
+    y = np.clip(x + rng.normal(0, 0.1, x.shape), 0, 1)
+    _check(x, y)
+
+
+def test_ssim_parity_identical_and_constant():
+    rng = np.random.default_rng(7)
+    x = rng.uniform(0, 1, (3, 40, 40))
+    assert abs(_check(x, x) - 1.0) < 2e-6
+    _check(np.full((3, 33, 35), 0.25), np.full((3, 33, 35), 0.75))
+
+
+def test_ssim_parity_rendered_full_size():
+    """BJ.configs[1] (640x480): the render of the scene vs a perturbed copy's."""
+    s = inputs.config1()
+    dev = torch.device("cuda:0")
+    P = Params.from_numpy(*s.params(), device=dev)
+    v = torch.as_tensor(s.views[0], device=dev)
+    r = Rasterizer(s.n, s.cam, device=dev)
+    r.size_for(P, v)
+    r.forward(P, v)
+    x = r.frame.color.cpu().numpy()
+    rng = np.random.default_rng(3)
+    y = np.clip(x + rng.normal(0, 0.05, x.shape), 0, None).astype(np.float32)
+    _check(x, y, 0.2)
+
+
+def test_color_loss_with_ssim_matches_eq10():
+    """Rasterizer.compute_loss(ssim=0.2) = Eq. 12 with Eq. 10's colour term."""
+    s = inputs.config0()
+    dev = torch.device("cuda:0")
+    P = Params.from_numpy(*s.params(), device=dev)
+    v = torch.as_tensor(s.views[0], device=dev)
+    r = Rasterizer(s.n, s.cam, device=dev)
+    r.size_for(P, v)
+    r.forward(P, v)
+    tc = torch.as_tensor(s.extra["tgt_color"][0], device=dev)
+    td = torch.as_tensor(s.extra["tgt_depth"][0], device=dev)
+    lc, ld = 0.9, 0.5
+    loss = r.compute_loss(tc, td, None, lc, ld, ssim=0.2).cpu().numpy()
+    x = r.frame.color.cpu().numpy()
+    Lc, l1, ssim, gc = OS.color_loss(x, tc.cpu().numpy(), 0.2)
+    d, t = r.frame.depth.cpu().numpy().astype(np.float64), td.cpu().numpy().astype(np.float64)
+    valid = t > 0
+    Ld = np.abs(d - t)[valid].mean() if valid.any() else 0.0
+    assert abs(loss[0] - (lc * Lc + ld * Ld)) <= 2e-6 * max(1.0, abs(loss[0]))
+    assert abs(loss[3] - ssim) <= 2e-6
+    g = r.dL_dcolor.cpu().numpy()
+    assert np.abs(g - lc * gc).max() <= 1e-4 * np.abs(lc * gc).max()

@@ -16,4 +16,5 @@ for k in ("render_fwd_isolated", "render_bwd_pixels_isolated"):
     print("%-28s %.1f us  frac %.3f" % (k, ro[k]["ms_per_launch"] * 1e3, ro[k]["frac"]))
 print("roofline(in-step) frac %.3f  %.1f us active of %.1f per step" % (d["roofline"]["frac"], d["roofline"].get("ms_active_per_step", 0) * 1e3, d["ms_per_step"] * 1e3))
 if "tracking" in d: print("tracking it/s %.1f" % d["tracking"]["value"])
+if "mapping_ssim" in d: print("mapping+SSIM MP/s %.1f" % d["mapping_ssim"]["value"])
 PY
