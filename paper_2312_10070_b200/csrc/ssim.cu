@@ -10,19 +10,25 @@
 // image x (y = target):
 //   dSSIM/dx(q) = [G*A + 2 x G*B + y G*Cc](q) / 3HW,
 //   A = dS/dmu_x - 2 mu_x dS/ds_xx - mu_y dS/ds_xy, B = dS/ds_xx, Cc = dS/ds_xy.
-// Two separable passes, each one CTA per (16x16 tile, channel) with a 26x26
-// halo in shared memory: k_ssim_stats (the five local moments -> S, A, B, Cc)
-// and k_ssim_grad (the three blurred maps -> the gradient, added to
-// dL_dcolor); fp64 block partials of S, reduced in a fixed order.
+// Two separable passes, each one CTA per (32x32 tile, channel) with a 42x42
+// halo in shared memory, the window sliding over register-held rows (8
+// outputs per horizontal task, 4 per vertical one): k_ssim_stats (the five
+// local moments -> S, A, B, Cc) and k_ssim_grad (the three blurred maps ->
+// the gradient, added to dL_dcolor); fp64 block partials of S, reduced in a
+// fixed order.
 #include <cmath>
 
 #include "gs_internal.cuh"
 
 namespace gs {
 
-constexpr int kSR = 5;                 // window radius
-constexpr int kSW = 2 * kSR + 1;       // 11 taps
-constexpr int kSH = kTile + 2 * kSR;   // 26: halo tile side
+constexpr int kSR = 5;                  // window radius
+constexpr int kSW = 2 * kSR + 1;        // 11 taps
+constexpr int kST = 32;                 // output tile side (32 x 32 per CTA)
+constexpr int kSH = kST + 2 * kSR;      // 42: halo tile side
+constexpr int kSThreads = 256;
+constexpr int kHSeg = 8;                // horizontal pass: 8 outputs per thread task (sliding window)
+constexpr int kVSeg = 4;                // vertical pass: 4 outputs per thread
 constexpr float kC1 = 0.01f * 0.01f, kC2 = 0.03f * 0.03f;
 
 struct SsimTaps {
@@ -31,21 +37,36 @@ struct SsimTaps {
 
 struct SsimArgs {
   const float *x, *y;  // rendered [3][H][W], target [3][H][W]
-  int W, H, TX;
+  int W, H, TX;        // TX = tiles of kST columns
   float *A, *B, *Cc;   // [3][H][W] each
   double *part;        // [3 * tiles]
   float weight;        // dL_dcolor += -weight * dSSIM/dx
   float *g_color, *loss;
 };
 
-// Zero-padded halo tile of a [H][W] map around tile (tx, ty), in-image
-// values shifted by `shift`.
+// Zero-padded kSH x kSH halo of a [H][W] map around output tile (tx, ty),
+// in-image values shifted by `shift`.
 __device__ __forceinline__ void load_halo(float (*s)[kSH], const float *m, int tx, int ty, int W, int H,
                                           float shift = 0.f) {
-  for (int i = threadIdx.x; i < kSH * kSH; i += blockDim.x) {
-    const int r = i / kSH, c = i % kSH;
-    const int gy = ty * kTile - kSR + r, gx = tx * kTile - kSR + c;
-    s[r][c] = (gy >= 0 && gy < H && gx >= 0 && gx < W) ? __ldg(m + size_t(gy) * W + gx) - shift : 0.f;
+  // 64 threads per row (42 used), 4 rows per pass: all 11 loads of a thread
+  // are issued before the first store (latency-bound otherwise)
+  constexpr int kRowsPer = (kSH + kSThreads / 64 - 1) / (kSThreads / 64);  // 11
+  const int gy0 = ty * kST - kSR, gx0 = tx * kST - kSR;
+  const int c = threadIdx.x % 64, r0 = threadIdx.x / 64;
+  const int gx = gx0 + c;
+  const bool colin = c < kSH && gx >= 0 && gx < W;
+  float v[kRowsPer];
+#pragma unroll
+  for (int i = 0; i < kRowsPer; ++i) {
+    const int r = r0 + i * (kSThreads / 64), gy = gy0 + r;
+    v[i] = (colin && r < kSH && gy >= 0 && gy < H) ? __ldg(m + size_t(gy) * W + gx) - shift : 0.f;
+  }
+  if (c < kSH) {
+#pragma unroll
+    for (int i = 0; i < kRowsPer; ++i) {
+      const int r = r0 + i * (kSThreads / 64);
+      if (r < kSH) s[r][c] = v[i];
+    }
   }
 }
 
@@ -57,131 +78,167 @@ __device__ __forceinline__ float axis_mass(const SsimTaps &t, int p, int n) {
   return m;
 }
 
-__global__ void __launch_bounds__(256) k_ssim_stats(SsimArgs a, SsimTaps t) {
-  __shared__ float sx[kSH][kSH], sy[kSH][kSH];
-  __shared__ float h[5][kSH][kTile];
-  __shared__ double sh[256];
+// Horizontal pass of NM maps over the halo: out[q][r][c] = sum_k g_k in_q(r, c + k)
+// for r < kSH, c < kST.  A task = one row and kHSeg consecutive outputs: the
+// kHSeg + 10 inputs are read once into registers and the window slides.
+template <int NM, class F>
+__device__ __forceinline__ void hpass(const SsimTaps &t, F in, float (*out)[kSH][kST]) {
+  constexpr int kTasks = kSH * (kST / kHSeg);  // 168
+  for (int task = threadIdx.x; task < kTasks; task += kSThreads) {
+    const int r = task / (kST / kHSeg), c0 = (task % (kST / kHSeg)) * kHSeg;
+    float v[NM][kHSeg + 2 * kSR];
+#pragma unroll
+    for (int k = 0; k < kHSeg + 2 * kSR; ++k) in(r, c0 + k, v, k);
+#pragma unroll
+    for (int o = 0; o < kHSeg; ++o) {
+      float acc[NM];
+#pragma unroll
+      for (int q = 0; q < NM; ++q) acc[q] = 0.f;
+#pragma unroll
+      for (int k = 0; k < kSW; ++k)
+#pragma unroll
+        for (int q = 0; q < NM; ++q) acc[q] = fmaf(t.g[k], v[q][o + k], acc[q]);
+#pragma unroll
+      for (int q = 0; q < NM; ++q) out[q][r][c0 + o] = acc[q];
+    }
+  }
+}
+
+// Vertical pass for this thread's kVSeg outputs of column c, rows r0..r0+3.
+template <int NM>
+__device__ __forceinline__ void vpass(const SsimTaps &t, const float (*h)[kSH][kST], int r0, int c,
+                                      float res[kVSeg][NM]) {
+#pragma unroll
+  for (int o = 0; o < kVSeg; ++o)
+#pragma unroll
+    for (int q = 0; q < NM; ++q) res[o][q] = 0.f;
+#pragma unroll
+  for (int k = 0; k < kVSeg + 2 * kSR; ++k) {
+#pragma unroll
+    for (int q = 0; q < NM; ++q) {
+      const float v = h[q][r0 + k][c];
+#pragma unroll
+      for (int o = 0; o < kVSeg; ++o)
+        if (k - o >= 0 && k - o < kSW) res[o][q] = fmaf(t.g[k - o], v, res[o][q]);
+    }
+  }
+}
+
+struct StatsSmem {
+  float sx[kSH][kSH], sy[kSH][kSH];
+  float h[5][kSH][kST];
+  double red[kSThreads / 32];
+};
+
+__global__ void __launch_bounds__(kSThreads) k_ssim_stats(SsimArgs a, SsimTaps t) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  StatsSmem &S = *reinterpret_cast<StatsSmem *>(smem_raw);
   const int tx = blockIdx.x % a.TX, ty = blockIdx.x / a.TX, ch = blockIdx.y;
   const size_t HW = size_t(a.W) * a.H;
   // moments of the in-image values shifted by the tile's first pixel (cx, cy):
   // the variances / covariance then carry no cancellation of the squared
   // means (exact zeros on flat patches); the mass m = G*1_image restores the
   // zero-padded statistics exactly (see below)
-  const size_t o = ch * HW + size_t(ty * kTile) * a.W + tx * kTile;
-  const float cx = __ldg(a.x + o), cy = __ldg(a.y + o);
-  load_halo(sx, a.x + ch * HW, tx, ty, a.W, a.H, cx);
-  load_halo(sy, a.y + ch * HW, tx, ty, a.W, a.H, cy);
+  const size_t o0 = ch * HW + size_t(ty * kST) * a.W + tx * kST;
+  const float cx = __ldg(a.x + o0), cy = __ldg(a.y + o0);
+  load_halo(S.sx, a.x + ch * HW, tx, ty, a.W, a.H, cx);
+  load_halo(S.sy, a.y + ch * HW, tx, ty, a.W, a.H, cy);
   __syncthreads();
-  // horizontal pass: the five moments over 26 rows x 16 columns
-  for (int i = threadIdx.x; i < kSH * kTile; i += blockDim.x) {
-    const int r = i / kTile, c = i % kTile;
-    float m0 = 0.f, m1 = 0.f, m2 = 0.f, m3 = 0.f, m4 = 0.f;
-#pragma unroll
-    for (int k = 0; k < kSW; ++k) {
-      const float xv = sx[r][c + k], yv = sy[r][c + k], g = t.g[k];
-      m0 = fmaf(g, xv, m0);
-      m1 = fmaf(g, yv, m1);
-      m2 = fmaf(g, xv * xv, m2);
-      m3 = fmaf(g, yv * yv, m3);
-      m4 = fmaf(g, xv * yv, m4);
-    }
-    h[0][r][c] = m0;
-    h[1][r][c] = m1;
-    h[2][r][c] = m2;
-    h[3][r][c] = m3;
-    h[4][r][c] = m4;
-  }
+  hpass<5>(t, [&](int r, int c, float (*v)[kHSeg + 2 * kSR], int k) {
+    const float xv = S.sx[r][c], yv = S.sy[r][c];
+    v[0][k] = xv;
+    v[1][k] = yv;
+    v[2][k] = xv * xv;
+    v[3][k] = yv * yv;
+    v[4][k] = xv * yv;
+  }, S.h);
   __syncthreads();
-  const int i = threadIdx.x / kTile, j = threadIdx.x % kTile;
-  float m[5] = {0.f, 0.f, 0.f, 0.f, 0.f};
-#pragma unroll
-  for (int k = 0; k < kSW; ++k) {
-    const float g = t.g[k];
-#pragma unroll
-    for (int q = 0; q < 5; ++q) m[q] = fmaf(g, h[q][i + k][j], m[q]);
-  }
-  const int px = tx * kTile + j, py = ty * kTile + i;
+  const int c = threadIdx.x % kST, r0 = (threadIdx.x / kST) * kVSeg;
+  float m[kVSeg][5];
+  vpass<5>(t, S.h, r0, c, m);
   double s_acc = 0.0;
-  if (px < a.W && py < a.H) {
+  const int px = tx * kST + c;
+  const float massx = axis_mass(t, px, a.W);
+#pragma unroll
+  for (int o = 0; o < kVSeg; ++o) {
+    const int py = ty * kST + r0 + o;
+    if (px >= a.W || py >= a.H) continue;
     // shifted moments G1 = G*x', G2 = G*y' with x' = (x - cx) 1_image:
     //   mu_x = G1 + cx m,  s_xx = G*x'^2 - G1^2 + (2 cx G1 + cx^2 m)(1 - m),
     //   s_xy = G*x'y' - G1 G2 + (cx G2 + cy G1 + cx cy m)(1 - m)
-    const float mass = axis_mass(t, px, a.W) * axis_mass(t, py, a.H), om = 1.f - mass;
-    const float G1 = m[0], G2 = m[1];
+    const float mass = massx * axis_mass(t, py, a.H), om = 1.f - mass;
+    const float G1 = m[o][0], G2 = m[o][1];
     const float mx = fmaf(cx, mass, G1), my = fmaf(cy, mass, G2);
-    const float sxx = (m[2] - G1 * G1) + (2.f * cx * G1 + cx * cx * mass) * om;
-    const float syy = (m[3] - G2 * G2) + (2.f * cy * G2 + cy * cy * mass) * om;
-    const float sxy = (m[4] - G1 * G2) + (cx * G2 + cy * G1 + cx * cy * mass) * om;
+    const float sxx = (m[o][2] - G1 * G1) + (2.f * cx * G1 + cx * cx * mass) * om;
+    const float syy = (m[o][3] - G2 * G2) + (2.f * cy * G2 + cy * cy * mass) * om;
+    const float sxy = (m[o][4] - G1 * G2) + (cx * G2 + cy * G1 + cx * cy * mass) * om;
     const float n1 = 2.f * mx * my + kC1, n2 = 2.f * sxy + kC2;
     const float d1 = mx * mx + my * my + kC1, d2 = sxx + syy + kC2;
-    const float D = d1 * d2, iD = 1.f / D;
-    const float S = n1 * n2 * iD;
-    const float dmx = 2.f * my * n2 * iD - 2.f * mx * S / d1;
-    const float dsxx = -S / d2, dsxy = 2.f * n1 * iD;
+    const float iD = 1.f / (d1 * d2);
+    const float Sv = n1 * n2 * iD;
+    const float dmx = 2.f * my * n2 * iD - 2.f * mx * Sv / d1;
+    const float dsxx = -Sv / d2, dsxy = 2.f * n1 * iD;
     const size_t q = ch * HW + size_t(py) * a.W + px;
     a.A[q] = dmx - 2.f * mx * dsxx - my * dsxy;
     a.B[q] = dsxx;
     a.Cc[q] = dsxy;
-    s_acc = double(S);
+    s_acc += double(Sv);
   }
-  // fixed-shape block tree: deterministic
-  sh[threadIdx.x] = s_acc;
+  // fixed-order block sum: warp tree, then the 8 warp sums in order
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) s_acc += __shfl_xor_sync(0xffffffffu, s_acc, off);
+  if ((threadIdx.x & 31) == 0) S.red[threadIdx.x >> 5] = s_acc;
   __syncthreads();
-  for (int s = 128; s > 0; s >>= 1) {
-    if (threadIdx.x < s) sh[threadIdx.x] += sh[threadIdx.x + s];
-    __syncthreads();
+  if (threadIdx.x == 0) {
+    double b = 0.0;
+    for (int w = 0; w < kSThreads / 32; ++w) b += S.red[w];
+    a.part[blockIdx.y * gridDim.x + blockIdx.x] = b;
   }
-  if (threadIdx.x == 0) a.part[blockIdx.y * gridDim.x + blockIdx.x] = sh[0];
 }
 
-__global__ void __launch_bounds__(256) k_ssim_grad(SsimArgs a, SsimTaps t) {
-  __shared__ float sm[3][kSH][kSH];
-  __shared__ float h[3][kSH][kTile];
+struct GradSmem {
+  float sm[3][kSH][kSH];
+  float h[3][kSH][kST];
+};
+
+__global__ void __launch_bounds__(kSThreads) k_ssim_grad(SsimArgs a, SsimTaps t) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  GradSmem &S = *reinterpret_cast<GradSmem *>(smem_raw);
   const int tx = blockIdx.x % a.TX, ty = blockIdx.x / a.TX, ch = blockIdx.y;
   const size_t HW = size_t(a.W) * a.H;
-  load_halo(sm[0], a.A + ch * HW, tx, ty, a.W, a.H);
-  load_halo(sm[1], a.B + ch * HW, tx, ty, a.W, a.H);
-  load_halo(sm[2], a.Cc + ch * HW, tx, ty, a.W, a.H);
+  load_halo(S.sm[0], a.A + ch * HW, tx, ty, a.W, a.H);
+  load_halo(S.sm[1], a.B + ch * HW, tx, ty, a.W, a.H);
+  load_halo(S.sm[2], a.Cc + ch * HW, tx, ty, a.W, a.H);
   __syncthreads();
-  for (int i = threadIdx.x; i < kSH * kTile; i += blockDim.x) {
-    const int r = i / kTile, c = i % kTile;
-    float m0 = 0.f, m1 = 0.f, m2 = 0.f;
-#pragma unroll
-    for (int k = 0; k < kSW; ++k) {
-      const float g = t.g[k];
-      m0 = fmaf(g, sm[0][r][c + k], m0);
-      m1 = fmaf(g, sm[1][r][c + k], m1);
-      m2 = fmaf(g, sm[2][r][c + k], m2);
-    }
-    h[0][r][c] = m0;
-    h[1][r][c] = m1;
-    h[2][r][c] = m2;
-  }
+  hpass<3>(t, [&](int r, int c, float (*v)[kHSeg + 2 * kSR], int k) {
+    v[0][k] = S.sm[0][r][c];
+    v[1][k] = S.sm[1][r][c];
+    v[2][k] = S.sm[2][r][c];
+  }, S.h);
   __syncthreads();
-  const int i = threadIdx.x / kTile, j = threadIdx.x % kTile;
-  const int px = tx * kTile + j, py = ty * kTile + i;
-  if (px >= a.W || py >= a.H) return;
-  float bA = 0.f, bB = 0.f, bC = 0.f;
+  const int c = threadIdx.x % kST, r0 = (threadIdx.x / kST) * kVSeg;
+  float m[kVSeg][3];
+  vpass<3>(t, S.h, r0, c, m);
+  const int px = tx * kST + c;
+  const float sc = -a.weight / float(3 * HW);
 #pragma unroll
-  for (int k = 0; k < kSW; ++k) {
-    const float g = t.g[k];
-    bA = fmaf(g, h[0][i + k][j], bA);
-    bB = fmaf(g, h[1][i + k][j], bB);
-    bC = fmaf(g, h[2][i + k][j], bC);
+  for (int o = 0; o < kVSeg; ++o) {
+    const int py = ty * kST + r0 + o;
+    if (px >= a.W || py >= a.H) continue;
+    const size_t q = ch * HW + size_t(py) * a.W + px;
+    const float xv = __ldg(a.x + q), yv = __ldg(a.y + q);
+    const float grad = m[o][0] + 2.f * xv * m[o][1] + yv * m[o][2];  // 3HW x dSSIM/dx
+    a.g_color[q] += sc * grad;
   }
-  const size_t q = ch * HW + size_t(py) * a.W + px;
-  const float xv = __ldg(a.x + q), yv = __ldg(a.y + q);
-  const float grad = bA + 2.f * xv * bB + yv * bC;  // 3HW x dSSIM/dx
-  a.g_color[q] += -a.weight / float(3 * HW) * grad;
 }
 
-__global__ void __launch_bounds__(256) k_ssim_final(SsimArgs a, int nblk) {
-  __shared__ double sh[256];
+__global__ void __launch_bounds__(1024) k_ssim_final(SsimArgs a, int nblk) {
+  __shared__ double sh[1024];
   double s = 0.0;
   for (int b = threadIdx.x; b < nblk; b += blockDim.x) s += a.part[b];  // fixed order per thread
   sh[threadIdx.x] = s;
   __syncthreads();
-  for (int k = 128; k > 0; k >>= 1) {
+  for (int k = 512; k > 0; k >>= 1) {
     if (threadIdx.x < k) sh[threadIdx.x] += sh[threadIdx.x + k];
     __syncthreads();
   }
@@ -192,9 +249,12 @@ __global__ void __launch_bounds__(256) k_ssim_final(SsimArgs a, int nblk) {
   }
 }
 
+static int ssim_tiles_x(const gs_camera &c) { return (c.width + kST - 1) / kST; }
+static int ssim_tiles_y(const gs_camera &c) { return (c.height + kST - 1) / kST; }
+
 static size_t ssim_ws_bytes(const gs_camera &cam) {
   const size_t HW = size_t(cam.width) * cam.height;
-  const size_t nblk = size_t(3) * tiles_x(cam) * tiles_y(cam);
+  const size_t nblk = size_t(3) * ssim_tiles_x(cam) * ssim_tiles_y(cam);
   return 3 * 3 * HW * sizeof(float) + nblk * sizeof(double) + 256;
 }
 
@@ -218,8 +278,8 @@ extern "C" int gs_ssim(gs_camera cam, const float *color, const float *tgt_color
   }
   const size_t HW = size_t(cam.width) * cam.height;
   float *A = static_cast<float *>(ws);
-  const int T = tiles_x(cam) * tiles_y(cam);
-  SsimArgs a{color, tgt_color, cam.width, cam.height, tiles_x(cam), A, A + 3 * HW, A + 6 * HW,
+  const int T = ssim_tiles_x(cam) * ssim_tiles_y(cam);
+  SsimArgs a{color, tgt_color, cam.width, cam.height, ssim_tiles_x(cam), A, A + 3 * HW, A + 6 * HW,
              reinterpret_cast<double *>(A + 9 * HW + (9 * HW & 1)), weight, dL_dcolor, loss};
   SsimTaps t;
   double g[kSW], sum = 0.0;
@@ -229,9 +289,15 @@ extern "C" int gs_ssim(gs_camera cam, const float *color, const float *tgt_color
   }
   for (int k = 0; k < kSW; ++k) t.g[k] = float(g[k] / sum);
   cudaStream_t s = as_stream(stream);
+  static thread_local bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(k_ssim_stats, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sizeof(StatsSmem)));
+    cudaFuncSetAttribute(k_ssim_grad, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sizeof(GradSmem)));
+    attr = true;
+  }
   const dim3 grid(T, 3);
-  k_ssim_stats<<<grid, 256, 0, s>>>(a, t);
-  k_ssim_grad<<<grid, 256, 0, s>>>(a, t);
-  k_ssim_final<<<1, 256, 0, s>>>(a, 3 * T);
+  k_ssim_stats<<<grid, kSThreads, sizeof(StatsSmem), s>>>(a, t);
+  k_ssim_grad<<<grid, kSThreads, sizeof(GradSmem), s>>>(a, t);
+  k_ssim_final<<<1, 1024, 0, s>>>(a, 3 * T);
   return check_launch("gs_ssim");
 }
