@@ -357,6 +357,28 @@ def bench_ours(a):
         line["mapping_ssim"] = {"metric": METRIC + ", colour loss with Eq. 10's SSIM term (lambda = 0.2)",
                                 "value": mp / (float(t_ss.item()) * 1e-3), "unit": UNIT,
                                 "ms_per_step": float(t_ss.item())}
+    if not a.profile:  # NEXT(3) epilogue: Eq. 11 + Adam over all Gaussians (after the all-reduce)
+        from paper_2312_10070_b200.raster import Optimizer
+        opt = Optimizer(s.n, device)
+        Pc = type(P)(*[getattr(P, k).clone() for k in ("mean_opa", "quat", "logscale", "rgb")])
+        for _ in range(3):
+            opt.regularize(Pc, ms.grads, 1.0)
+            opt.step(Pc, ms.grads)
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(20):
+            opt.regularize(Pc, ms.grads, 1.0)
+            opt.step(Pc, ms.grads)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        t_opt = e0.elapsed_time(e1) / 20
+        # algorithmic bytes: Eq. 11 reads log-scales and read-modify-writes their gradients (48 B);
+        # Adam reads 4 gradients (64 B) and read-modify-writes 4 parameters (128 B) and 8 moments (256 B)
+        nbytes = s.n * (48 + 64 + 128 + 256)
+        line["optimizer"] = {"what": "Eq. 11 regulariser + one Adam step over all %d Gaussians" % s.n,
+                             "ms": t_opt, "achieved_gbs": nbytes / (t_opt * 1e-3) / 1e9,
+                             "hbm_peak_gbs": peaks.get("hbm_gbs"), "bytes": nbytes}
     if not a.profile and not a.no_e2e:  # every rank: the step contains the all-reduce
         line["e2e"] = e2e_ours(a, s, ms, device, world)
     if world > 1:

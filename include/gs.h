@@ -298,6 +298,54 @@ size_t gs_ssim_workspace_bytes(gs_camera cam);
 int gs_ssim(gs_camera cam, const float *color, const float *tgt_color, float weight, void *ws,
             size_t ws_bytes, float *loss, float *dL_dcolor, void *stream);
 
+/* NEXT(3) — device epilogue of a mapping iteration ("jointly
+ * optimized ... minimizing the loss (12)"; Eq. 11; P:624 pruning;
+ * S:205-241; R34-R36).  All calls are asynchronous. */
+
+/* Adam hyper-parameters (host, by pointer).  Learning rates per parameter
+ * group (S:231 defaults: mean 1e-4, quaternion 1e-3, log-scale 1e-3, opacity
+ * logit 5e-2, colour 2.5e-3; beta 0.9 / 0.999, eps 1e-8); step = t >= 1 (bias
+ * correction 1 - beta^t). */
+typedef struct {
+  float lr_mean, lr_quat, lr_logscale, lr_opacity, lr_rgb;
+  double beta1, beta2, eps; /* fp64: 1 - beta is formed without fp32 cancellation */
+  int32_t step;
+} gs_adam_cfg;
+
+/* Workspace bytes gs_iso_reg / gs_prune need for n Gaussians. */
+size_t gs_opt_workspace_bytes(int32_t n);
+
+/* Eq. 11: L_reg = sum_k |s_k - s^bar_k|_1 / |K|, s_k = exp(logscale_k)
+ * (3 components), s^bar_k = the mean of s_k's components (R34).
+ *   g_logscale (device) [n][4]: += lambda_reg dL_reg/dlogscale (w unused)
+ *   loss       (device) [2]: loss[0] += lambda_reg L_reg, loss[1] = L_reg
+ * Fixed-order reduction (deterministic). */
+int gs_iso_reg(gs_params p, float lambda_reg, float *g_logscale, void *ws, size_t ws_bytes,
+               float *loss, void *stream);
+
+/* One Adam step over the four parameter arrays of p, IN PLACE (the arrays of
+ * p are written although gs_params declares them const): per component
+ * m = b1 m + (1 - b1) g, v = b2 v + (1 - b2) g^2, p -= lr (m / (1 - b1^t)) /
+ * (sqrt(v / (1 - b2^t)) + eps); quaternions renormalised after the step
+ * (S:220); a Gaussian with any non-finite gradient is left untouched and
+ * counted in cnt->n_nonfinite.
+ *   g_*      (device) [n][4] gradients (gs_render_bwd's layout)
+ *   moments  (device) [n][8][4]: m of (mean_opa, quat, logscale, rgb), then
+ *            v; zero-initialise (new Gaussians start from zero)
+ *   cnt      (device, nullable) */
+int gs_adam_step(gs_params p, const float *g_mean_opa, const float *g_quat,
+                 const float *g_logscale, const float *g_rgb, float *moments,
+                 const gs_adam_cfg *cfg, gs_counters *cnt, void *stream);
+
+/* Opacity pruning ("prune Gaussians having opacity values lower than a
+ * threshold o_thre"): keeps the Gaussians with sigmoid(logit) >= o_thre
+ * (decided in fp64, R35), compacted in their original order into `out`
+ * (and their moments into moments_out when moments != NULL); *n_out (device)
+ * = the kept count.  out / moments_out must not alias the inputs.
+ *   ws (device) >= gs_opt_workspace_bytes(p.n) */
+int gs_prune(gs_params p, const float *moments, float o_thre, gs_params out,
+             float *moments_out, void *ws, size_t ws_bytes, int32_t *n_out, void *stream);
+
 /* S5+S6 — backward (Eqs. 7-8; R16, R17).
  *
  * Per pixel, replays the composited entries back to front (same alpha

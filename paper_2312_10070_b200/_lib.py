@@ -45,6 +45,12 @@ class GsPoseStep(C.Structure):
                 ("eps", C.c_float)]
 
 
+class GsAdamCfg(C.Structure):
+    _fields_ = [("lr_mean", C.c_float), ("lr_quat", C.c_float), ("lr_logscale", C.c_float),
+                ("lr_opacity", C.c_float), ("lr_rgb", C.c_float), ("beta1", C.c_double), ("beta2", C.c_double),
+                ("eps", C.c_double), ("step", C.c_int32)]
+
+
 class GsError(RuntimeError):
     pass
 
@@ -67,6 +73,10 @@ _PROTOS = {
     "gs_loss": (C.c_int, [GsCamera, _VP, _VP, _VP, _VP, _VP, _F, _F, _VP, _SZ, _VP, _VP, _VP, _VP]),
     "gs_tracking_loss_workspace_bytes": (_SZ, [GsCamera]),
     "gs_ssim_workspace_bytes": (_SZ, [GsCamera]),
+    "gs_opt_workspace_bytes": (_SZ, [_I32]),
+    "gs_iso_reg": (C.c_int, [GsParams, _F, _VP, _VP, _SZ, _VP, _VP]),
+    "gs_adam_step": (C.c_int, [GsParams, _VP, _VP, _VP, _VP, _VP, C.POINTER(GsAdamCfg), _VP, _VP]),
+    "gs_prune": (C.c_int, [GsParams, _VP, _F, GsParams, _VP, _VP, _SZ, _VP, _VP]),
     "gs_ssim": (C.c_int, [GsCamera, _VP, _VP, _F, _VP, _SZ, _VP, _VP, _VP]),
     "gs_tracking_loss": (C.c_int, [GsCamera, _VP, _VP, _VP, _VP, _VP, _F, _F, _VP, _SZ, _VP, _VP, _VP, _VP]),
     "gs_render_bwd": (C.c_int, [GsParams, _VP, GsCamera, GsProj, _VP, _VP, _VP, _VP, _VP, _VP, _VP, _VP, _U32, _VP,

@@ -16,10 +16,11 @@ from dataclasses import dataclass
 import torch
 
 from . import _lib
-from ._lib import GS_BWD_GAUSS_ONLY, GS_BWD_PIXELS_ONLY, GS_GRAD_PARAMS, GS_GRAD_POSE, GsCamera, GsError, GsParams, GsPoseStep, GsProj, check, lib
+from ._lib import (GS_BWD_GAUSS_ONLY, GS_BWD_PIXELS_ONLY, GS_GRAD_PARAMS, GS_GRAD_POSE, GsAdamCfg, GsCamera, GsError,
+                   GsParams, GsPoseStep, GsProj, check, lib)
 
 __all__ = ["Params", "Grads", "Proj", "Frame", "Rasterizer", "camera", "gs_project", "gs_bin_sort",
-           "gs_render_fwd", "gs_tile_order", "gs_loss", "gs_tracking_loss", "gs_ssim", "gs_render_bwd", "gs_pose_grad", "GS_GRAD_PARAMS", "GS_GRAD_POSE", "GS_BWD_PIXELS_ONLY", "GS_BWD_GAUSS_ONLY",
+           "gs_render_fwd", "gs_tile_order", "gs_loss", "gs_tracking_loss", "gs_ssim", "gs_iso_reg", "gs_adam_step", "gs_prune", "Optimizer", "gs_render_bwd", "gs_pose_grad", "GS_GRAD_PARAMS", "GS_GRAD_POSE", "GS_BWD_PIXELS_ONLY", "GS_BWD_GAUSS_ONLY",
            "GsError", "device_check"]
 
 
@@ -176,6 +177,62 @@ def gs_tracking_loss(cam: GsCamera, color, depth, alpha, tgt_color, tgt_depth, l
 def gs_ssim(cam: GsCamera, color, tgt_color, weight, ws, loss, dL_dcolor, stream=None):
     check(lib().gs_ssim(cam, _p(color), _p(tgt_color), float(weight), _p(ws), ws.numel() * ws.element_size(),
                         _p(loss), _p(dL_dcolor), _stream(stream)), "gs_ssim")
+
+
+def gs_iso_reg(params: Params, lambda_reg, g_logscale, ws, loss, stream=None):
+    check(lib().gs_iso_reg(params.c(), float(lambda_reg), _p(g_logscale), _p(ws), ws.numel() * ws.element_size(),
+                           _p(loss), _stream(stream)), "gs_iso_reg")
+
+
+def gs_adam_step(params: Params, grads: "Grads", moments, cfg: GsAdamCfg, counters=None, stream=None):
+    check(lib().gs_adam_step(params.c(), _p(grads.mean_opa), _p(grads.quat), _p(grads.logscale), _p(grads.rgb),
+                             _p(moments), C.byref(cfg), _p(counters), _stream(stream)), "gs_adam_step")
+
+
+def gs_prune(params: Params, moments, o_thre, out: Params, moments_out, ws, n_out, stream=None):
+    check(lib().gs_prune(params.c(), _p(moments), float(o_thre), out.c(), _p(moments_out), _p(ws),
+                         ws.numel() * ws.element_size(), _p(n_out), _stream(stream)), "gs_prune")
+
+
+class Optimizer:
+    """Device-side mapping optimiser (NEXT(3)): Adam over the four float4
+    parameter arrays with per-group learning rates (S:231 defaults), the
+    Eq. 11 isotropic regulariser folded into the gradient before the step,
+    and opacity pruning as a stable compaction of parameters and
+    moments.  The moments are one [n][8][4] buffer."""
+
+    DEFAULT_LR = dict(lr_mean=1e-4, lr_quat=1e-3, lr_logscale=1e-3, lr_opacity=5e-2, lr_rgb=2.5e-3)
+
+    def __init__(self, n, device="cuda", betas=(0.9, 0.999), eps=1e-8, **lr):
+        self.lr = dict(self.DEFAULT_LR, **lr)
+        self.betas, self.eps = betas, eps
+        self.t = 0
+        self.moments = torch.zeros(max(n, 1), 8, 4, dtype=torch.float32, device=device)
+        self.ws = torch.empty((lib().gs_opt_workspace_bytes(max(n, 1)) + 15) // 16 * 4, dtype=torch.float32,
+                              device=device)
+        self.reg_loss = torch.zeros(2, dtype=torch.float32, device=device)
+        self.n_out = torch.zeros(1, dtype=torch.int32, device=device)
+
+    def cfg(self):
+        return GsAdamCfg(self.lr["lr_mean"], self.lr["lr_quat"], self.lr["lr_logscale"], self.lr["lr_opacity"],
+                         self.lr["lr_rgb"], self.betas[0], self.betas[1], self.eps, self.t)
+
+    def regularize(self, params: Params, grads: "Grads", lambda_reg=1.0):
+        """Eq. 11 (x lambda_reg): self.reg_loss = (lambda_reg L_reg, L_reg) and the
+        log-scale gradients += its gradient."""
+        self.reg_loss.zero_()
+        gs_iso_reg(params, lambda_reg, grads.logscale, self.ws, self.reg_loss)
+        return self.reg_loss
+
+    def step(self, params: Params, grads: "Grads", counters=None):
+        self.t += 1
+        gs_adam_step(params, grads, self.moments, self.cfg(), counters)
+
+    def prune(self, params: Params, o_thre, out: Params, moments_out):
+        """Kept Gaussians -> out (same capacity), moments -> moments_out;
+        self.n_out (device) = kept count."""
+        gs_prune(params, self.moments, o_thre, out, moments_out, self.ws, self.n_out)
+        return self.n_out
 
 
 def gs_render_bwd(params: Params, view, cam: GsCamera, proj: Proj, sorted_idx, tile_range, T_final, n_contrib,

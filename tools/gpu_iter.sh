@@ -17,4 +17,5 @@ for k in ("render_fwd_isolated", "render_bwd_pixels_isolated"):
 print("roofline(in-step) frac %.3f  %.1f us active of %.1f per step" % (d["roofline"]["frac"], d["roofline"].get("ms_active_per_step", 0) * 1e3, d["ms_per_step"] * 1e3))
 if "tracking" in d: print("tracking it/s %.1f" % d["tracking"]["value"])
 if "mapping_ssim" in d: print("mapping+SSIM MP/s %.1f" % d["mapping_ssim"]["value"])
+if "optimizer" in d: print("optimizer %.1f us  %.0f GB/s" % (d["optimizer"]["ms"] * 1e3, d["optimizer"]["achieved_gbs"]))
 PY
