@@ -123,22 +123,22 @@ __device__ __forceinline__ unsigned box_block_mask(float4 b) {
   return m;
 }
 
-// This warp's hit list over a staged batch: the indices (ascending) of the
-// entries j < cnt whose mask has bit w, written to list[0..n), followed by
-// `sentinel` at list[n].  Returns n.
-__device__ __forceinline__ int warp_hit_list(const unsigned char *s_mask, int cnt, unsigned char *list,
-                                             int sentinel) {
+// This warp's hit list over a staged batch of B entries: the indices
+// (ascending) of the entries j < cnt whose mask has bit w, written to
+// list[0..n), followed by `sentinel` at list[n].  Returns n.
+template <int B = kBatch, class L>
+__device__ __forceinline__ int warp_hit_list(const unsigned char *s_mask, int cnt, L *list, int sentinel) {
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   int n = 0;
 #pragma unroll
-  for (int h = 0; h < kBatch / 32; ++h) {
+  for (int h = 0; h < B / 32; ++h) {
     const int j = h * 32 + lane;
     const bool hit = j < cnt && ((s_mask[j] >> w) & 1u);
     const unsigned b = __ballot_sync(0xffffffffu, hit);
-    if (hit) list[n + __popc(b & lanemask_lt())] = (unsigned char)j;
+    if (hit) list[n + __popc(b & lanemask_lt())] = (L)j;
     n += __popc(b);
   }
-  if (lane == 0) list[n] = (unsigned char)sentinel;
+  if (lane == 0) list[n] = (L)sentinel;
   __syncwarp();
   return n;
 }
