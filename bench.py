@@ -379,6 +379,33 @@ def bench_ours(a):
         line["optimizer"] = {"what": "Eq. 11 regulariser + one Adam step over all %d Gaussians" % s.n,
                              "ms": t_opt, "achieved_gbs": nbytes / (t_opt * 1e-3) / 1e9,
                              "hbm_peak_gbs": peaks.get("hbm_gbs"), "bytes": nbytes}
+    if not a.profile:  # NEXT(4): seeding one keyframe against the 500k-Gaussian sub-map
+        from paper_2312_10070_b200.raster import gs_seed, lib as _gslib
+        r0 = ms.lanes[0]
+        r0.forward(P, views[0])
+        alpha = r0.frame.alpha.clone()
+        depth = (r0.frame.depth / alpha.clamp_min(1e-6)).contiguous()
+        H_, W_ = alpha.shape
+        alpha[H_ // 4:3 * H_ // 4, W_ // 4:3 * W_ // 4] = 0.0  # an unmapped window: every pixel a candidate
+        cap = s.n + 50000
+        Ps = type(P)(*[torch.cat([getattr(P, k), torch.zeros(50000, 4, device=device)]).contiguous()
+                       for k in ("mean_opa", "quat", "logscale", "rgb")])
+        sws = torch.empty((_gslib().gs_seed_workspace_bytes(r0.cam, s.n, 50000) + 15) // 16 * 4,
+                          dtype=torch.float32, device=device)
+        n_new = torch.zeros(1, dtype=torch.int32, device=device)
+        vh = views[0].cpu()
+        for _ in range(2):
+            gs_seed(r0.cam, vh, r0.frame.color, depth, alpha, 0.6, 0.01, 50000, 1, Ps, s.n, sws, n_new)
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(10):
+            gs_seed(r0.cam, vh, r0.frame.color, depth, alpha, 0.6, 0.01, 50000, 1, Ps, s.n, sws, n_new)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        line["seeding"] = {"what": "gs_seed: M_k = 50000 alpha-gated samples of a 1200x680 keyframe against "
+                                   "%d existing Gaussians (rho = 1 cm)" % s.n,
+                           "ms": e0.elapsed_time(e1) / 10, "accepted": int(n_new.item()), "capacity": cap}
     if not a.profile and not a.no_e2e:  # every rank: the step contains the all-reduce
         line["e2e"] = e2e_ours(a, s, ms, device, world)
     if world > 1:

@@ -346,6 +346,36 @@ int gs_adam_step(gs_params p, const float *g_mean_opa, const float *g_quat,
 int gs_prune(gs_params p, const float *moments, float o_thre, gs_params out,
              float *moments_out, void *ws, size_t ws_bytes, int32_t *n_out, void *stream);
 
+/* NEXT(4) — sub-map seeding from a keyframe ("we sample M_k points
+ * uniformly from the regions with the rendered alpha values lower than a
+ * threshold alpha_n ... that have no neighbors within a search radius rho
+ * ... scales ... based on the nearest neighbor distance"; P:230 alpha_n = 0.6,
+ * rho = 0.01 m; P:624 opacity 0.5; R37-R41).
+ *
+ *   candidates: the first max_new pixels with depth > 0 and alpha < alpha_n in
+ *     the order of the seeded bijective permutation of the pixel indices of
+ *     R38 (oracle/seed.py writes it out);
+ *   points: p_c = ((i - cx) D / fx, (j - cy) D / fy, D), world = R^T (p_c - t)
+ *     in fp64, rounded to fp32;
+ *   a candidate is rejected if an existing mean or an earlier candidate lies
+ *     within rho (squared fp64 distance < rho^2);
+ *   accepted points are appended at p.mean_opa / quat / logscale / rgb
+ *     [n, n + n_new) in sample order: mean, opacity logit 0 (o = 0.5),
+ *     rotation (1, 0, 0, 0), log-scales ln(clamp(nearest-neighbour distance
+ *     among existing + accepted points, rho / 2, 0.1 m)), colour of the pixel.
+ *   view_host (host) T_wc of the keyframe
+ *   color, depth, alpha (device) the keyframe RGB-D and the rendered alpha
+ *   capacity  length of the parameter arrays (appends beyond it are dropped;
+ *             *n_new still counts them)
+ *   n_new     (device) [1] accepted count
+ *   ws        (device) >= gs_seed_workspace_bytes(cam, p.n, max_new)
+ * Deterministic for a given seed.  Errors: GS_ERR_INVALID_ARG (null, rho
+ * not in (0, 0.1], capacity < n), GS_ERR_WORKSPACE. */
+size_t gs_seed_workspace_bytes(gs_camera cam, int32_t n, int32_t max_new);
+int gs_seed(gs_camera cam, const gs_view *view_host, const float *color, const float *depth,
+            const float *alpha, float alpha_n, float rho, int32_t max_new, uint32_t seed,
+            gs_params p, int32_t capacity, void *ws, size_t ws_bytes, int32_t *n_new, void *stream);
+
 /* S5+S6 — backward (Eqs. 7-8; R16, R17).
  *
  * Per pixel, replays the composited entries back to front (same alpha

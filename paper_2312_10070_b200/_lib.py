@@ -45,6 +45,10 @@ class GsPoseStep(C.Structure):
                 ("eps", C.c_float)]
 
 
+class GsView(C.Structure):
+    _fields_ = [("R", C.c_float * 9), ("t", C.c_float * 3)]
+
+
 class GsAdamCfg(C.Structure):
     _fields_ = [("lr_mean", C.c_float), ("lr_quat", C.c_float), ("lr_logscale", C.c_float),
                 ("lr_opacity", C.c_float), ("lr_rgb", C.c_float), ("beta1", C.c_double), ("beta2", C.c_double),
@@ -74,6 +78,8 @@ _PROTOS = {
     "gs_tracking_loss_workspace_bytes": (_SZ, [GsCamera]),
     "gs_ssim_workspace_bytes": (_SZ, [GsCamera]),
     "gs_opt_workspace_bytes": (_SZ, [_I32]),
+    "gs_seed_workspace_bytes": (_SZ, [GsCamera, _I32, _I32]),
+    "gs_seed": (C.c_int, [GsCamera, _VP, _VP, _VP, _VP, _F, _F, _I32, _U32, GsParams, _I32, _VP, _SZ, _VP, _VP]),
     "gs_iso_reg": (C.c_int, [GsParams, _F, _VP, _VP, _SZ, _VP, _VP]),
     "gs_adam_step": (C.c_int, [GsParams, _VP, _VP, _VP, _VP, _VP, C.POINTER(GsAdamCfg), _VP, _VP]),
     "gs_prune": (C.c_int, [GsParams, _VP, _F, GsParams, _VP, _VP, _SZ, _VP, _VP]),

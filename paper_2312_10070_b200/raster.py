@@ -17,10 +17,10 @@ import torch
 
 from . import _lib
 from ._lib import (GS_BWD_GAUSS_ONLY, GS_BWD_PIXELS_ONLY, GS_GRAD_PARAMS, GS_GRAD_POSE, GsAdamCfg, GsCamera, GsError,
-                   GsParams, GsPoseStep, GsProj, check, lib)
+                   GsParams, GsPoseStep, GsProj, GsView, check, lib)
 
 __all__ = ["Params", "Grads", "Proj", "Frame", "Rasterizer", "camera", "gs_project", "gs_bin_sort",
-           "gs_render_fwd", "gs_tile_order", "gs_loss", "gs_tracking_loss", "gs_ssim", "gs_iso_reg", "gs_adam_step", "gs_prune", "Optimizer", "gs_render_bwd", "gs_pose_grad", "GS_GRAD_PARAMS", "GS_GRAD_POSE", "GS_BWD_PIXELS_ONLY", "GS_BWD_GAUSS_ONLY",
+           "gs_render_fwd", "gs_tile_order", "gs_loss", "gs_tracking_loss", "gs_ssim", "gs_iso_reg", "gs_adam_step", "gs_prune", "gs_seed", "Optimizer", "gs_render_bwd", "gs_pose_grad", "GS_GRAD_PARAMS", "GS_GRAD_POSE", "GS_BWD_PIXELS_ONLY", "GS_BWD_GAUSS_ONLY",
            "GsError", "device_check"]
 
 
@@ -192,6 +192,21 @@ def gs_adam_step(params: Params, grads: "Grads", moments, cfg: GsAdamCfg, counte
 def gs_prune(params: Params, moments, o_thre, out: Params, moments_out, ws, n_out, stream=None):
     check(lib().gs_prune(params.c(), _p(moments), float(o_thre), out.c(), _p(moments_out), _p(ws),
                          ws.numel() * ws.element_size(), _p(n_out), _stream(stream)), "gs_prune")
+
+
+def gs_seed(cam: GsCamera, view, color, depth, alpha, alpha_n, rho, max_new, seed, params: Params, n, ws, n_new,
+            stream=None):
+    """NEXT(4): append the seeded Gaussians of one keyframe to params (arrays of
+    capacity >= n + max_new) after the first n; n_new (device) = accepted count.
+    view: the keyframe's T_wc as 12 host floats (R row-major, t)."""
+    import numpy as np
+    v = np.asarray(view.detach().cpu() if hasattr(view, "detach") else view, np.float32).ravel()
+    gv = GsView((C.c_float * 9)(*v[:9]), (C.c_float * 3)(*v[9:12]))
+    cap = params.mean_opa.shape[0]
+    P = GsParams(_p(params.mean_opa), _p(params.quat), _p(params.logscale), _p(params.rgb), int(n))
+    check(lib().gs_seed(cam, C.byref(gv), _p(color), _p(depth), _p(alpha), float(alpha_n), float(rho), int(max_new),
+                        int(seed) & 0xFFFFFFFF, P, int(cap), _p(ws), ws.numel() * ws.element_size(), _p(n_new),
+                        _stream(stream)), "gs_seed")
 
 
 class Optimizer:

@@ -18,4 +18,5 @@ print("roofline(in-step) frac %.3f  %.1f us active of %.1f per step" % (d["roofl
 if "tracking" in d: print("tracking it/s %.1f" % d["tracking"]["value"])
 if "mapping_ssim" in d: print("mapping+SSIM MP/s %.1f" % d["mapping_ssim"]["value"])
 if "optimizer" in d: print("optimizer %.1f us  %.0f GB/s" % (d["optimizer"]["ms"] * 1e3, d["optimizer"]["achieved_gbs"]))
+if "seeding" in d: print("seeding %.1f us  accepted %d" % (d["seeding"]["ms"] * 1e3, d["seeding"]["accepted"]))
 PY
