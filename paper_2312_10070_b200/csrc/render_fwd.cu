@@ -30,17 +30,27 @@ struct FwdArgs {
   int32_t *n_contrib, *stats, *tile_work;
 };
 
-constexpr int kFPX = 2;  // pixels per thread in the forward (one fp32x2 pair)
-using FG = Geo<kFPX, 8>;  // 4 warps, 8x8 pixel blocks
+#ifndef FWD_NP
+#define FWD_NP 1
+#endif
+#ifndef FWD_WX
+#define FWD_WX 8
+#endif
+// Forward geometry: NP fp32x2 pixel pairs per thread on WX-wide warp blocks.
+//   NP = 1, WX = 8:  4 warps on 8x8 blocks, 2 px / thread
+//   NP = 2, WX = 16: 2 warps on 16x8 strips, 4 px / thread
+constexpr int kFNP = FWD_NP;
+constexpr int kFWX = FWD_WX;
+using FG = Geo<2 * kFNP, kFWX>;
 
-// per-thread compositing state of its pixel pair
+// per-thread compositing state of one pixel pair
 struct FwdPix {
   float2 T, c0, c1, c2, D, A;
   bool live0, live1;
   int last0, last1, ncon0, ncon1, term0, term1;
 };
 
-// One list entry at the pixel pair: alpha decision (R11) and the blend of
+// One list entry at a pixel pair: alpha decision (R11) and the blend of
 // Eqs. 3, 6 and R14, branch-free (alpha = 0 leaves the state bit-identical).
 template <bool kStats>
 __device__ __forceinline__ void fwd_blend(FwdPix &s, float2 e, bool p0, bool p1, float4 c, int pos) {
@@ -75,6 +85,29 @@ struct __align__(16) FwdRec {
   float2 pad;
 };
 
+__device__ __forceinline__ bool any_live(const FwdPix s[kFNP]) {
+  bool l = false;
+#pragma unroll
+  for (int h = 0; h < kFNP; ++h) l |= s[h].live0 || s[h].live1;
+  return l;
+}
+
+// one hit at all of the thread's pairs: returns the pass test, blends if any lane passes
+template <bool kStats>
+__device__ __forceinline__ void fwd_entry(FwdPix s[kFNP], const float2 e[kFNP], const FwdRec &rc, int pos) {
+  bool p[kFNP][2], any = false;
+#pragma unroll
+  for (int h = 0; h < kFNP; ++h) {
+    p[h][0] = s[h].live0 && e[h].x >= kExpSkip;
+    p[h][1] = s[h].live1 && e[h].y >= kExpSkip;
+    any |= p[h][0] || p[h][1];
+  }
+  if (!__any_sync(0xffffffffu, any)) return;
+  const float4 c = rc.rgbz;
+#pragma unroll
+  for (int h = 0; h < kFNP; ++h) fwd_blend<kStats>(s[h], e[h], p[h][0], p[h][1], c, pos);
+}
+
 template <bool kStats>
 __global__ void __launch_bounds__(FG::kThreads, 1) k_render_fwd(FwdArgs a) {
   // one staged record per entry; record kBatch is a sentinel entry whose exponent is -inf
@@ -87,36 +120,43 @@ __global__ void __launch_bounds__(FG::kThreads, 1) k_render_fwd(FwdArgs a) {
   const PixGeom pg = pix_geom<FG>(tx, ty, a.H);
   const double ox = double(tx * kTile), oy = double(ty * kTile);
   const int2 range = a.tile_range[tile];
-  const float2 fx = make_float2(pg.fpx0, pg.fpx0 + 1.f);
+  float2 fx[kFNP];
+#pragma unroll
+  for (int h = 0; h < kFNP; ++h) fx[h] = make_float2(pg.fpx0 + 2.f * h, pg.fpx0 + 2.f * h + 1.f);
   if (threadIdx.x == 0) {
     s_rec[kBatch].p = make_float4(0.f, 0.f, 0.f, 0.f);
     s_rec[kBatch].q = make_float2(0.f, -INFINITY);
   }
   // a pixel composites while T >= 1e-4 (include, then stop: T < 1e-4 happens
   // exactly at the stopping entry); pixels outside the image start with T = 0
-  FwdPix s;
-  s.T = make_float2((pg.row_in && pg.px0 < a.W) ? 1.f : 0.f, (pg.row_in && pg.px0 + 1 < a.W) ? 1.f : 0.f);
-  s.c0 = s.c1 = s.c2 = s.D = s.A = make_float2(0.f, 0.f);
-  s.live0 = s.T.x >= kTEps;
-  s.live1 = s.T.y >= kTEps;
-  s.last0 = s.last1 = s.ncon0 = s.ncon1 = 0;
-  s.term0 = s.term1 = range.y - range.x;  // entries scanned if the pixel never terminates
+  FwdPix s[kFNP];
+#pragma unroll
+  for (int h = 0; h < kFNP; ++h) {
+    s[h].T = make_float2((pg.row_in && pg.px0 + 2 * h < a.W) ? 1.f : 0.f,
+                         (pg.row_in && pg.px0 + 2 * h + 1 < a.W) ? 1.f : 0.f);
+    s[h].c0 = s[h].c1 = s[h].c2 = s[h].D = s[h].A = make_float2(0.f, 0.f);
+    s[h].live0 = s[h].T.x >= kTEps;
+    s[h].live1 = s[h].T.y >= kTEps;
+    s[h].last0 = s[h].last1 = s[h].ncon0 = s[h].ncon1 = 0;
+    s[h].term0 = s[h].term1 = range.y - range.x;  // entries scanned if the pixel never terminates
+  }
   for (int start = range.x; start < range.y; start += kBatch) {
-    if (__syncthreads_count(s.live0 || s.live1) == 0) break;
-    static_assert(FG::kRecPerThread == 1, "one staged record per thread");
-    {
-      const int k = start + threadIdx.x;
+    if (__syncthreads_count(any_live(s)) == 0) break;
+#pragma unroll
+    for (int r = 0; r < FG::kRecPerThread; ++r) {
+      const int i = r * FG::kThreads + threadIdx.x;
+      const int k = start + i;
       if (k < range.y) {
         const int g = __ldg(a.sorted_idx + k);
         const double2 u = __ldg(a.uv + g);
         const float4 cf = __ldg(a.coef + g);
         const float ul = float(u.x - ox), vl = float(u.y - oy);
         const EntryTerms et = entry_terms(cf, ul, vl);
-        FwdRec &rc = s_rec[threadIdx.x];
+        FwdRec &rc = s_rec[i];
         rc.p = et.p;
         rc.q = et.q;
         rc.rgbz = __ldg(a.rgbz + g);
-        s_mask[threadIdx.x] = (unsigned char)box_block_mask<FG>(entry_box(cf, ul, vl));
+        s_mask[i] = (unsigned char)box_block_mask<FG>(entry_box(cf, ul, vl));
       }
     }
     __syncthreads();
@@ -128,25 +168,27 @@ __global__ void __launch_bounds__(FG::kThreads, 1) k_render_fwd(FwdArgs a) {
     const int nh = warp_hit_list(s_mask, min(kBatch, range.y - start), list, kBatch);
     const int base = start - range.x + 1;
     for (int k = 0; k < nh; k += 2) {
-      if ((k & 31) == 0 && !__any_sync(0xffffffffu, s.live0 || s.live1)) break;
+      if ((k & 31) == 0 && !__any_sync(0xffffffffu, any_live(s))) break;
       const int ja = list[k], jb = list[k + 1];
-      const float2 ea = pair_exponent(row_terms(s_rec[ja].p, s_rec[ja].q, pg.fpy), fx);
-      const float2 eb = pair_exponent(row_terms(s_rec[jb].p, s_rec[jb].q, pg.fpy), fx);
-      {
-        const bool p0 = s.live0 && ea.x >= kExpSkip, p1 = s.live1 && ea.y >= kExpSkip;
-        if (__any_sync(0xffffffffu, p0 || p1)) fwd_blend<kStats>(s, ea, p0, p1, s_rec[ja].rgbz, base + ja);
+      const RowTerms ra = row_terms(s_rec[ja].p, s_rec[ja].q, pg.fpy);
+      const RowTerms rb = row_terms(s_rec[jb].p, s_rec[jb].q, pg.fpy);
+      float2 ea[kFNP], eb[kFNP];
+#pragma unroll
+      for (int h = 0; h < kFNP; ++h) {
+        ea[h] = pair_exponent(ra, fx[h]);
+        eb[h] = pair_exponent(rb, fx[h]);
       }
-      {
-        const bool p0 = s.live0 && eb.x >= kExpSkip, p1 = s.live1 && eb.y >= kExpSkip;
-        if (__any_sync(0xffffffffu, p0 || p1)) fwd_blend<kStats>(s, eb, p0, p1, s_rec[jb].rgbz, base + jb);
-      }
+      fwd_entry<kStats>(s, ea, s_rec[ja], base + ja);
+      fwd_entry<kStats>(s, eb, s_rec[jb], base + jb);
     }
   }
   if (a.tile_work) {  // the backward's work on this tile: sum of n_contrib
     __shared__ int s_work;
     if (threadIdx.x == 0) s_work = 0;
     __syncthreads();
-    int wk = s.last0 + s.last1;
+    int wk = 0;
+#pragma unroll
+    for (int h = 0; h < kFNP; ++h) wk += s[h].last0 + s[h].last1;
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) wk += __shfl_xor_sync(0xffffffffu, wk, o);
     if ((threadIdx.x & 31) == 0) atomicAdd(&s_work, wk);
@@ -155,23 +197,26 @@ __global__ void __launch_bounds__(FG::kThreads, 1) k_render_fwd(FwdArgs a) {
   }
   if (!pg.row_in) return;
   const size_t HW = size_t(a.W) * a.H;
-  const float cc0[2] = {s.c0.x, s.c0.y}, cc1[2] = {s.c1.x, s.c1.y}, cc2[2] = {s.c2.x, s.c2.y},
-              DD[2] = {s.D.x, s.D.y}, AA[2] = {s.A.x, s.A.y}, TT[2] = {s.T.x, s.T.y};
-  const int ll[2] = {s.last0, s.last1}, nc[2] = {s.ncon0, s.ncon1}, tm[2] = {s.term0, s.term1};
 #pragma unroll
-  for (int k = 0; k < kFPX; ++k) {
-    if (pg.px0 + k >= a.W) break;
-    const size_t q = size_t(pg.py) * a.W + pg.px0 + k;
-    a.color[q] = cc0[k];
-    a.color[HW + q] = cc1[k];
-    a.color[2 * HW + q] = cc2[k];
-    a.depth[q] = DD[k];
-    a.alpha[q] = AA[k];
-    a.T_final[q] = TT[k];
-    a.n_contrib[q] = ll[k];
-    if (kStats) {
-      a.stats[q] = tm[k];  // entries scanned = termination position or list length
-      a.stats[HW + q] = nc[k];
+  for (int h = 0; h < kFNP; ++h) {
+    const float cc0[2] = {s[h].c0.x, s[h].c0.y}, cc1[2] = {s[h].c1.x, s[h].c1.y}, cc2[2] = {s[h].c2.x, s[h].c2.y},
+                DD[2] = {s[h].D.x, s[h].D.y}, AA[2] = {s[h].A.x, s[h].A.y}, TT[2] = {s[h].T.x, s[h].T.y};
+    const int ll[2] = {s[h].last0, s[h].last1}, nc[2] = {s[h].ncon0, s[h].ncon1}, tm[2] = {s[h].term0, s[h].term1};
+#pragma unroll
+    for (int k = 0; k < 2; ++k) {
+      if (pg.px0 + 2 * h + k >= a.W) break;
+      const size_t q = size_t(pg.py) * a.W + pg.px0 + 2 * h + k;
+      a.color[q] = cc0[k];
+      a.color[HW + q] = cc1[k];
+      a.color[2 * HW + q] = cc2[k];
+      a.depth[q] = DD[k];
+      a.alpha[q] = AA[k];
+      a.T_final[q] = TT[k];
+      a.n_contrib[q] = ll[k];
+      if (kStats) {
+        a.stats[q] = tm[k];  // entries scanned = termination position or list length
+        a.stats[HW + q] = nc[k];
+      }
     }
   }
 }
