@@ -404,6 +404,22 @@ int gs_render_bwd(gs_params p, const gs_view *view, gs_camera cam, gs_proj pr,
                   float *g_mean_opa, float *g_quat, float *g_logscale, float *g_rgb,
                   float *pose_partials, void *stream);
 
+/* S6 for several views at once (mapping, Eq. 12 summed over the keyframes of
+ * an iteration): for every Gaussian, the camera part of the chain
+ * of gs_render_bwd's Gaussian phase for each of the V views (each view's
+ * grad2d scratch from a GS_BWD_PIXELS_ONLY call), summed in fp64, then the
+ * scale / quaternion part once on the sum and one += into the gradient
+ * arrays.  Equal to V GS_BWD_GAUSS_ONLY calls up to fp32 rounding; reads
+ * the parameters and writes the gradients once instead of V times.
+ *   V in [1, 16]; views, conic_o, tiles_touched, ws: host arrays of V device
+ *   pointers (each view's gs_view, gs_proj.conic_o, gs_proj.tiles_touched and
+ *   gs_render_bwd workspace); every grad2d record read is zeroed.
+ *   g_* (device) [n][4] gradients, += (GS_GRAD_PARAMS layout). */
+int gs_render_bwd_gauss_views(gs_params p, int32_t V, const gs_view *const *views, gs_camera cam,
+                              const float *const *conic_o, const int32_t *const *tiles_touched,
+                              float *const *ws, float *g_mean_opa, float *g_quat, float *g_logscale,
+                              float *g_rgb, void *stream);
+
 /* S7 — camera-pose gradient (Eq. 14; R22).
  *
  * Reduces the pose partials in a fixed order to dL/dR, dL/dt and converts

@@ -87,6 +87,8 @@ _PROTOS = {
     "gs_tracking_loss": (C.c_int, [GsCamera, _VP, _VP, _VP, _VP, _VP, _F, _F, _VP, _SZ, _VP, _VP, _VP, _VP]),
     "gs_render_bwd": (C.c_int, [GsParams, _VP, GsCamera, GsProj, _VP, _VP, _VP, _VP, _VP, _VP, _VP, _VP, _U32, _VP,
                                 _SZ, _VP, _VP, _VP, _VP, _VP, _VP]),
+    "gs_render_bwd_gauss_views": (C.c_int, [GsParams, _I32, C.POINTER(_VP), GsCamera, C.POINTER(_VP), C.POINTER(_VP),
+                                             C.POINTER(_VP), _VP, _VP, _VP, _VP, _VP]),
     "gs_pose_grad": (C.c_int, [_VP, _VP, _I32, C.POINTER(GsPoseStep), _VP, _VP, _VP, _VP, _VP]),
 }
 

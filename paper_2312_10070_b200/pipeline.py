@@ -17,7 +17,8 @@ from __future__ import annotations
 
 import torch
 
-from .raster import GS_BWD_GAUSS_ONLY, GS_BWD_PIXELS_ONLY, GS_GRAD_PARAMS, GS_GRAD_POSE, Grads, Params, Rasterizer, lib
+from .raster import (GS_BWD_GAUSS_ONLY, GS_BWD_PIXELS_ONLY, GS_GRAD_PARAMS, GS_GRAD_POSE, Grads, Params, Rasterizer,
+                     gs_render_bwd_gauss_views, lib)
 
 
 class HostInputs:
@@ -57,9 +58,14 @@ class MapStep:
 
     def __init__(self, params: Params, views, cam, tgt_color, tgt_depth, rank=0, world=1, group=None,
                  lambda_color=1.0, lambda_depth=1.0, device="cuda", lanes=8, allreduce=None, schedule="lanes",
-                 ssim=0.0):
+                 ssim=0.0, fused_gauss=False):
         """ssim: the lambda of Eq. 10's colour loss (0: L1 colour only, as
-        BJ.configs[3]; the paper uses 0.2)."""
+        BJ.configs[3]; the paper uses 0.2).  fused_gauss: when every view has
+        its own lane, run ONE per-Gaussian phase over all views
+        (gs_render_bwd_gauss_views) instead of a per-view S6 on each lane;
+        off by default: it sits on the step's critical path and measured
+        3.61 ms per BJ.configs[3] step against 3.15 ms for the overlapped
+        per-view phases (profiles/r01/README.md)."""
         self.ssim = ssim
         self.params = params
         self.views = views                  # [V, 12] device tensor (all views)
@@ -84,6 +90,7 @@ class MapStep:
         self.losses = torch.zeros(max(len(self.mine), 1), 4, dtype=torch.float32, device=device)
         self.copy_stream = None
         self.schedule = schedule
+        self.fused_gauss = fused_gauss
         self.stage_streams = [torch.cuda.Stream(device=device) for _ in range(3)] if schedule == "stages" else []
 
     def size(self, slack=1.25):
@@ -184,6 +191,20 @@ class MapStep:
                             st[name](r, k, v)
                         ev = s.record_event()
                 done[lane] = ev
+        elif self.fused_gauss and len(self.mine) <= len(self.lanes) and "gauss" not in (hooks or {}):
+            # every view has its own buffers: the per-pixel phases run on the
+            # lanes, then ONE per-Gaussian phase over all views
+            # (gs_render_bwd_gauss_views: parameters read and gradients written once)
+            for k, v in enumerate(self.mine):
+                s, r = self.streams[k], self.lanes[k]
+                with torch.cuda.stream(s):
+                    st["front"](r, k, v)
+                    st["fwd"](r, k, v, tgt_ready[v])
+                    st["bwd"](r, k, v)
+            for s in self.streams:
+                main.wait_stream(s)
+            gs_render_bwd_gauss_views(self.params, [self.views[v] for v in self.mine], self.r.cam,
+                                      self.lanes[:len(self.mine)], self.grads)
         else:
             prev = start
             for k, v in enumerate(self.mine):
@@ -208,6 +229,8 @@ class MapStep:
 
     def launches_per_step(self):
         """Kernels of ours launched per step."""
+        if self.schedule == "lanes" and self.fused_gauss and len(self.mine) <= len(self.lanes):
+            return len(self.mine) * (kernels_per_view(self.r.cam) - 1) + 1
         return len(self.mine) * kernels_per_view(self.r.cam)
 
 

@@ -20,7 +20,7 @@ from ._lib import (GS_BWD_GAUSS_ONLY, GS_BWD_PIXELS_ONLY, GS_GRAD_PARAMS, GS_GRA
                    GsParams, GsPoseStep, GsProj, GsView, check, lib)
 
 __all__ = ["Params", "Grads", "Proj", "Frame", "Rasterizer", "camera", "gs_project", "gs_bin_sort",
-           "gs_render_fwd", "gs_tile_order", "gs_loss", "gs_tracking_loss", "gs_ssim", "gs_iso_reg", "gs_adam_step", "gs_prune", "gs_seed", "Optimizer", "gs_render_bwd", "gs_pose_grad", "GS_GRAD_PARAMS", "GS_GRAD_POSE", "GS_BWD_PIXELS_ONLY", "GS_BWD_GAUSS_ONLY",
+           "gs_render_fwd", "gs_tile_order", "gs_loss", "gs_tracking_loss", "gs_ssim", "gs_iso_reg", "gs_adam_step", "gs_prune", "gs_seed", "Optimizer", "gs_render_bwd", "gs_render_bwd_gauss_views", "gs_pose_grad", "GS_GRAD_PARAMS", "GS_GRAD_POSE", "GS_BWD_PIXELS_ONLY", "GS_BWD_GAUSS_ONLY",
            "GsError", "device_check"]
 
 
@@ -266,6 +266,18 @@ def gs_render_bwd(params: Params, view, cam: GsCamera, proj: Proj, sorted_idx, t
                               _p(pose_partials), _stream(stream)), "gs_render_bwd")
     if event_pair is not None:
         event_pair[1].record(torch.cuda.current_stream() if stream is None else stream)
+
+
+def gs_render_bwd_gauss_views(params: Params, views, cam: GsCamera, rasterizers, grads: "Grads", stream=None):
+    """S6 over several views: views = list of device view tensors [12] (one per
+    rasterizer, after its GS_BWD_PIXELS_ONLY backward)."""
+    V = len(views)
+    arr = lambda xs: (C.c_void_p * V)(*[x.value if isinstance(x, C.c_void_p) else x for x in xs])
+    check(lib().gs_render_bwd_gauss_views(
+        params.c(), V, arr([v.data_ptr() for v in views]), cam,
+        arr([r.proj.conic_o.data_ptr() for r in rasterizers]), arr([r.proj.tiles_touched.data_ptr() for r in rasterizers]),
+        arr([r.bwd_ws.data_ptr() for r in rasterizers]), _p(grads.mean_opa), _p(grads.quat), _p(grads.logscale),
+        _p(grads.rgb), _stream(stream)), "gs_render_bwd_gauss_views")
 
 
 def gs_pose_grad(view, pose_partials, n_partials, step=None, adam_state=None, dL_dview=None, dL_dtwist=None,

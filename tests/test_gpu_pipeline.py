@@ -49,14 +49,20 @@ def test_mapstep_equals_sum_of_views_for_any_lanes():
     torch.cuda.synchronize()
     ref_np = ref.buf.cpu().numpy()
     scale = np.abs(ref_np).max()
-    for lanes in (1, 2, 3):
-        ms = MapStep(P, views, s.cam, tc, td, lanes=lanes, device=d)
+    # per-view Gaussian phases in view order; fused (lanes >= V): one
+    # multi-view Gaussian phase (gs_render_bwd_gauss_views); "stages": stage streams
+    for lanes, sched, fused in ((1, "lanes", False), (2, "lanes", False), (3, "lanes", False), (4, "lanes", False),
+                                (4, "lanes", True), (8, "lanes", True), (2, "stages", False), (4, "stages", False)):
+        ms = MapStep(P, views, s.cam, tc, td, lanes=lanes, device=d, schedule=sched, fused_gauss=fused)
         ms.size()
         g = ms.step()
         torch.cuda.synchronize()
         got = g.buf.cpu().numpy()
-        assert np.allclose(got, ref_np, rtol=1e-4, atol=1e-5 * scale), lanes
+        assert np.allclose(got, ref_np, rtol=1e-4, atol=1e-5 * scale), (lanes, sched, fused)
         assert np.allclose(ms.losses.cpu().numpy(), torch.stack(losses).cpu().numpy(), rtol=1e-6)
+        g2 = ms.step()  # the grad2d scratches were left zeroed: a second step gives the same
+        torch.cuda.synchronize()
+        assert np.allclose(g2.buf.cpu().numpy(), got, rtol=1e-5, atol=1e-6 * scale), (lanes, sched, fused)
 
 
 def test_sharded_sum_equals_unsharded():
