@@ -56,6 +56,9 @@ extern "C" {
 #define GS_GRAD_POSE 2u   /* camera-pose partials (tracking)           */
 #define GS_BWD_PIXELS_ONLY 4u /* run only the per-pixel phase (S5)                 */
 #define GS_BWD_GAUSS_ONLY 8u  /* run only the per-Gaussian phase (S6)              */
+#define GS_BWD_ATOMIC_ACC 16u /* S6 adds into g_* with atomic vector adds:  calls on
+                                 several streams may accumulate into the same arrays
+                                 concurrently (summation order unspecified)        */
 
 /* Pinhole camera, passed by value (R4, R5). */
 typedef struct gs_camera {
@@ -389,7 +392,9 @@ int gs_seed(gs_camera cam, const gs_view *view_host, const float *color, const f
  *   flags     GS_GRAD_PARAMS and/or GS_GRAD_POSE, optionally one of
  *             GS_BWD_PIXELS_ONLY (accumulate grad2d only; it then holds the
  *             2-D gradients) / GS_BWD_GAUSS_ONLY (chain an accumulated grad2d
- *             and re-zero it); the two split calls equal one full call
+ *             and re-zero it); the two split calls equal one full call;
+ *             GS_BWD_ATOMIC_ACC: the += into g_* below is an atomic add, so
+ *             per-view calls on different streams need no ordering
  *   ws        (device) >= gs_bwd_workspace_bytes(n), zero on entry
  *   g_mean_opa, g_quat, g_logscale, g_rgb (device) [n][4], ACCUMULATED (+=)
  *             in the layout of gs_params; required iff GS_GRAD_PARAMS

@@ -53,7 +53,7 @@ def build(verbose=False, force=False):
         obj = os.path.join(BUILD, src + ".o")
         objs.append(obj)
         if force or _stale(obj, [path] + hdrs):
-            cmd = [nvcc()] + ARCH + NVCC_FLAGS + PER_FILE.get(src, [])
+            cmd = [nvcc()] + ARCH + NVCC_FLAGS + PER_FILE.get(src, []) + os.environ.get("GS_EXTRA_NVCC", "").split()
             if src.endswith(".cpp"):
                 cmd += ["-x", "cu"]
             cmd += ["-c", path, "-o", obj]

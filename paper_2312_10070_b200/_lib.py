@@ -23,6 +23,7 @@ GS_GRAD_PARAMS = 1
 GS_GRAD_POSE = 2
 GS_BWD_PIXELS_ONLY = 4
 GS_BWD_GAUSS_ONLY = 8
+GS_BWD_ATOMIC_ACC = 16
 
 
 class GsCamera(C.Structure):

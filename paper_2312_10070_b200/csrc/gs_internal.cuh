@@ -15,8 +15,15 @@ constexpr int kTilePx = kTile * kTile;  // 256 pixels per tile
 constexpr float kAlphaMax = GS_ALPHA_MAX;
 constexpr float kAlphaMin = GS_ALPHA_MIN;
 constexpr float kTEps = GS_T_EPS;
-// exponent pre-test: for e < kExpSkip, 2^e < 1/255 by a relative gap of
-// 4e-4 >> MUFU.EX2 error (2^-22), so the pre-test never changes a decision.
+// The alpha decisions of R11 are taken on the fp32 exponent e (log2 alpha~,
+// raster_common.cuh), in both render kernels (R2'):
+//   alpha~ >= 1/255 (GS_ALPHA_MIN)  <=>  e >= kExpMin
+//   alpha~ >= 0.999 (GS_ALPHA_MAX)  <=>  e >= kExpClamp
+// each constant the smallest float >= log2 of the (fp32) threshold, so the
+// test is the exact decision for 2^e; no MUFU.EX2 rounding enters it.
+constexpr float kExpMin = -7.994353294373e+00f;    // 0xc0ffd1be, log2(1/255f) = -7.99435335...
+constexpr float kExpClamp = -1.443398185074e-03f;  // 0xbabd3068, log2(0.999f) = -0.00144339827...
+// conservative bound for the entry boxes (below kExpMin by 6.5e-4)
 constexpr float kExpSkip = -7.9950f;
 // 0.5 * log2(e): sigma * log2(e) = (a' dx + b' dy)^2 + (d' dy)^2 (H2b)
 constexpr double kHalfLog2e = 0.72134752044448170368;

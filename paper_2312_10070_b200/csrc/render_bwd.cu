@@ -85,7 +85,10 @@ __device__ __forceinline__ void red_add_v4(float *addr, float x, float y, float 
 
 constexpr int kBPX = 4;   // pixels per thread in the backward (two fp32x2 pairs)
 constexpr bool kSmemReduce = true;  // per-entry warp sums through shared memory (else shuffles)
-constexpr int kBwdMinBlocks = 1;    // resident CTAs per SM the register budget must allow
+#ifndef BWD_MINB
+#define BWD_MINB 1
+#endif
+constexpr int kBwdMinBlocks = BWD_MINB;  // resident CTAs per SM the register budget must allow
 using BG = Geo<kBPX, 16>;  // 2 warps, 16x8 pixel strips
 
 __device__ __forceinline__ float rcp_approx(float x) {
@@ -105,75 +108,85 @@ struct BwdPix {
   int last[kBPX];
 };
 
+// per-lane roles in the shared-memory reduction of bwd_entry: lane 3v + p
+// (v < 10, p < 3) sums value v over the slab rows = p mod 3; lane 3v writes
+// the total, scaled by wsc, to grad2d[woff]
+struct RedRole {
+  const float *col;  // first slab row of this lane's column
+  int woff;          // grad2d record offset of value v
+  float wsc;         // sign of the value and the 1/2 of dsigma/dA, dsigma/dC
+  bool writer;
+};
+
 // One list entry j at the thread's pixels: alpha replay (H5), T by division
 // (R16), Eq. 8 through Q, per-thread sums, then the warp reduction into
 // grad2d.  Branch-free per pixel: alpha = 0 leaves T and Q unchanged and
-// contributes exact zeros.
-// acc layout: 0 u, 1 v, 2 2*A-term, 3 B, 4 2*C-term, 5 p_z, 6 logit, 7 r, 8 g, 9 b
-// (the 1/2 of dsigma/dA and dsigma/dC is applied once, by the writing lane)
+// contributes exact zeros.  pass[k]: the pixel's decision (entry inside its
+// n_contrib and alpha~ >= 1/255, the forward's e >= kExpMin, R2'); any: one
+// of this lane's pixels passes; ball: the warp's ballot of `any` (nonzero).
+// acc layout (before the writer's sign/scale): 0 u, 1 v, 2 A-term, 3 B,
+// 4 C-term, 5 p_z, 6 logit, 7 r, 8 g, 9 b
 template <bool kParams>
-__device__ __forceinline__ void bwd_entry(BwdPix &s, const float2 e[2], const bool pass[kBPX], float4 c, float4 cn,
-                                          float2 ul, float fpy, const float2 fx[2], float *dst, float *red, int rv,
-                                          int rp) {
+__device__ __forceinline__ void bwd_entry(BwdPix &s, const float2 e[2], const bool pass[kBPX], bool any,
+                                          unsigned ball, float4 c, float4 cn, float2 ul, float fpy,
+                                          const float2 fx[2], float *dst, float *red, const RedRole &rr) {
   const float dy = ul.y - fpy;  // Delta = mu^I - pixel; one row: dy is shared
   // per-thread sums over its pixels (as pair sums) of ga = alpha dL/dalpha
   // (0 if clamped) and ga dx, ga dx^2; dsigma/d(u, v, A, B, C) and
   // dalpha/dlogit are formed once per (thread, entry) from them, the conic,
   // dy and o (entry constants)
-  float2 sga = make_float2(0.f, 0.f), sgx = sga, sgxx = sga, sz = sga, sr = sga, sg = sga, sb = sga;
-  bool any = false;
+  float2 ga[2], t[2], wt[2], dx[2];
 #pragma unroll
   for (int h = 0; h < 2; ++h) {
-    const float at0 = ex2_approx(e[h].x), at1 = ex2_approx(e[h].y);
-    const float m0 = fminf(at0, kAlphaMax), m1 = fminf(at1, kAlphaMax);
-    const bool q0 = pass[2 * h] && m0 >= kAlphaMin, q1 = pass[2 * h + 1] && m1 >= kAlphaMin;
-    const float a0 = q0 ? m0 : 0.f, a1 = q1 ? m1 : 0.f;  // same decision as the forward (H5)
-    any |= q0 || q1;
+    // a skipped pixel's exponent becomes -inf: alpha = 0 (the forward's value, H5)
+    const float a0 = fminf(ex2_approx(pass[2 * h] ? e[h].x : -INFINITY), kAlphaMax);
+    const float a1 = fminf(ex2_approx(pass[2 * h + 1] ? e[h].y : -INFINITY), kAlphaMax);
     const float2 al = make_float2(a0, a1);
     // T_j = T_{j+1} / (1 - alpha_j) (R16)
     s.T[h] = __fmul2_rn(s.T[h], make_float2(rcp_approx(1.f - a0), rcp_approx(1.f - a1)));
-    const float2 wt = __fmul2_rn(al, s.T[h]);
+    wt[h] = __fmul2_rn(al, s.T[h]);
     // Eq. 8 chained with Eq. 7 through the suffix scalar Q
     const float2 gx = __ffma2_rn(
         s.G0[h], bcast(c.x), __ffma2_rn(s.G1[h], bcast(c.y), __ffma2_rn(s.G2[h], bcast(c.z), __ffma2_rn(s.GD[h], bcast(c.w), s.GA[h]))));
     const float2 d = __fadd2_rn(gx, make_float2(-s.Q[h].x, -s.Q[h].y));
     const float2 galpha = __fmul2_rn(s.T[h], d);
     s.Q[h] = __ffma2_rn(al, d, s.Q[h]);
-    sz = __ffma2_rn(wt, s.GD[h], sz);  // dD/dz_j = alpha_j T_j
-    if (kParams) {
-      sr = __ffma2_rn(wt, s.G0[h], sr);  // dC/dc_j = alpha_j T_j
-      sg = __ffma2_rn(wt, s.G1[h], sg);
-      sb = __ffma2_rn(wt, s.G2[h], sb);
-    }
-    // clamped alpha: no gradient (R17)
-    const float2 ga = __fmul2_rn(make_float2(at0 < kAlphaMax ? a0 : 0.f, at1 < kAlphaMax ? a1 : 0.f), galpha);
-    const float2 dx = __fadd2_rn(bcast(ul.x), make_float2(-fx[h].x, -fx[h].y));
-    const float2 t = __fmul2_rn(ga, dx);
-    sga = __fadd2_rn(sga, ga);
-    sgx = __fadd2_rn(sgx, t);
-    sgxx = __ffma2_rn(t, dx, sgxx);
+    // clamped alpha (alpha~ >= 0.999: e >= kExpClamp): no gradient (R17)
+    ga[h] = __fmul2_rn(make_float2(e[h].x < kExpClamp ? a0 : 0.f, e[h].y < kExpClamp ? a1 : 0.f), galpha);
+    dx[h] = __fadd2_rn(bcast(ul.x), make_float2(-fx[h].x, -fx[h].y));
+    t[h] = __fmul2_rn(ga[h], dx[h]);
   }
-  const unsigned ball = __ballot_sync(0xffffffffu, any);
-  if (!ball) return;
+  const float2 sga = __fadd2_rn(ga[0], ga[1]);
+  const float2 sgx = __fadd2_rn(t[0], t[1]);
+  const float2 sgxx = __ffma2_rn(t[1], dx[1], __fmul2_rn(t[0], dx[0]));
+  const float2 sz = __ffma2_rn(wt[1], s.GD[1], __fmul2_rn(wt[0], s.GD[0]));  // dD/dz_j = alpha_j T_j
   const float Sga = sga.x + sga.y, Sgx = sgx.x + sgx.y;
   // dalpha/dsigma = -alpha, dsigma/du = A dx + B dy, dsigma/dv = B dx + C dy,
-  // dsigma/d(A, B, C) = (dx^2/2, dx dy, dy^2/2), dalpha/dlogit = alpha (1 - o)
+  // dsigma/d(A, B, C) = (dx^2/2, dx dy, dy^2/2), dalpha/dlogit = alpha (1 - o);
+  // the signs of values 0-4 and the halves are applied by the writer (wsc)
   float acc[10];
-  acc[0] = -fmaf(cn.x, Sgx, cn.y * dy * Sga);
-  acc[1] = -fmaf(cn.y, Sgx, cn.z * dy * Sga);
-  acc[2] = -(sgxx.x + sgxx.y);  // x2 (the writer applies 1/2)
-  acc[3] = -dy * Sgx;
-  acc[4] = -dy * dy * Sga;  // x2
+  acc[0] = fmaf(cn.x, Sgx, cn.y * dy * Sga);
+  acc[1] = fmaf(cn.y, Sgx, cn.z * dy * Sga);
+  acc[2] = sgxx.x + sgxx.y;
+  acc[3] = dy * Sgx;
+  acc[4] = dy * dy * Sga;
   acc[5] = sz.x + sz.y;
   acc[6] = kParams ? (1.f - cn.w) * Sga : 0.f;
-  acc[7] = sr.x + sr.y;
-  acc[8] = sg.x + sg.y;
-  acc[9] = sb.x + sb.y;
+  if (kParams) {  // dC/dc_j = alpha_j T_j
+    const float2 sr = __ffma2_rn(wt[1], s.G0[1], __fmul2_rn(wt[0], s.G0[0]));
+    const float2 sg = __ffma2_rn(wt[1], s.G1[1], __fmul2_rn(wt[0], s.G1[0]));
+    const float2 sb = __ffma2_rn(wt[1], s.G2[1], __fmul2_rn(wt[0], s.G2[0]));
+    acc[7] = sr.x + sr.y;
+    acc[8] = sg.x + sg.y;
+    acc[9] = sb.x + sb.y;
+  } else {
+    acc[7] = acc[8] = acc[9] = 0.f;
+  }
   if (__popc(ball) <= 2) {  // few contributing lanes: write directly, skip the reduction
     if (any) {
       // grad2d record: (u, v, A, B), (C, p_z, logit, 0), (r, g, b, 0)
-      red_add_v4(dst, acc[0], acc[1], 0.5f * acc[2], acc[3]);
-      red_add_v4(dst + 4, 0.5f * acc[4], acc[5], acc[6], 0.f);
+      red_add_v4(dst, -acc[0], -acc[1], -0.5f * acc[2], -acc[3]);
+      red_add_v4(dst + 4, -0.5f * acc[4], acc[5], acc[6], 0.f);
       if (kParams) red_add_v4(dst + 8, acc[7], acc[8], acc[9], 0.f);
     }
     return;
@@ -182,32 +195,31 @@ __device__ __forceinline__ void bwd_entry(BwdPix &s, const float2 e[2], const bo
     // through this warp's shared-memory slab: lane l stores its 10 values in
     // row l (stride 11: conflict-free both ways); lane 3v + p (v < 10, p < 3)
     // sums value v over the rows = p mod 3, the 3 partial sums meet by two
-    // shuffles, lane 3v adds the total to grad2d
-    // (rv, rp) = (lane / 3, lane % 3); row 32 of the slab is zero, so every
-    // lane sums 11 rows without bounds checks (lanes 30, 31 sum column 10,
-    // the padding, and never write)
+    // shuffles, lane 3v adds the total to grad2d.  Row 32 of the slab is
+    // zero, so every lane sums 11 rows without bounds checks (lanes 30, 31
+    // sum column 10, the padding, and never write)
     const int lane = threadIdx.x & 31;
     float *row = red + lane * 11;
     __syncwarp();  // the previous entry's reads of the slab are done
 #pragma unroll
     for (int v = 0; v < 10; ++v) row[v] = acc[v];
     __syncwarp();
-    float part = 0.f;
-    const float *col = red + rp * 11 + rv;
+    float c[11];
 #pragma unroll
-    for (int t = 0; t < 11; ++t) part += col[t * 33];
+    for (int t = 0; t < 11; ++t) c[t] = rr.col[t * 33];
+    // pairwise (depth 4, not a chain of 10 dependent adds)
+    float part = (((c[0] + c[1]) + (c[2] + c[3])) + ((c[4] + c[5]) + (c[6] + c[7]))) + ((c[8] + c[9]) + c[10]);
     part += __shfl_down_sync(0xffffffffu, part, 1) + __shfl_down_sync(0xffffffffu, part, 2);
-    if (lane < 30 && rp == 0 && (kParams || rv < 6))
-      atomicAdd(dst + (rv < 7 ? rv : rv + 1), (rv == 2 || rv == 4) ? 0.5f * part : part);
+    if (rr.writer) atomicAdd(dst + rr.woff, rr.wsc * part);
     return;
   }
+  const float sgn[10] = {-1.f, -1.f, -0.5f, -1.f, -0.5f, 1.f, 1.f, 1.f, 1.f, 1.f};
+#pragma unroll
+  for (int v = 0; v < 10; ++v) acc[v] *= sgn[v];
   int idx;
   bool writer;
   const float tot = warp_reduce10(acc, idx, writer);
-  if (writer && (kParams || idx < 6)) {
-    const int off = idx < 7 ? idx : idx + 1;
-    atomicAdd(dst + off, (idx == 2 || idx == 4) ? 0.5f * tot : tot);
-  }
+  if (writer && (kParams || idx < 6)) atomicAdd(dst + (idx < 7 ? idx : idx + 1), tot);
 }
 
 // one staged list entry of the backward
@@ -282,7 +294,14 @@ __global__ void __launch_bounds__(BG::kThreads, kBwdMinBlocks) k_bwd_pixels(BwdA
   __syncthreads();
   const int lmax = s_lmax;
   unsigned char *list = s_list[w];
-  const int rv = (threadIdx.x & 31) / 3, rp = (threadIdx.x & 31) % 3;  // reduction lane roles
+  RedRole rr;
+  {
+    const int lane = threadIdx.x & 31, rv = lane / 3, rp = lane % 3;
+    rr.col = s_red[w] + rp * 11 + rv;
+    rr.woff = rv < 7 ? rv : rv + 1;
+    rr.wsc = (rv == 2 || rv == 4) ? -0.5f : (rv < 4 ? -1.f : 1.f);
+    rr.writer = lane < 30 && rp == 0 && (kParams || rv < 6);
+  }
   for (int end = lmax; end > 0; end -= kBatch) {
     const int beg = max(end - kBatch, 0);
     __syncthreads();
@@ -313,10 +332,21 @@ __global__ void __launch_bounds__(BG::kThreads, kBwdMinBlocks) k_bwd_pixels(BwdA
     // Hits are list[1..nh]; list[0] is the sentinel.
     if ((threadIdx.x & 31) == 0) list[0] = (unsigned char)kBatch;
     const int nh = warp_hit_list(s_mask, min(end, wmax) - beg, list + 1, kBatch);
+    // the next pair's list indices and entry terms are loaded one step ahead
+    // (list[0] is the sentinel: indices below 0 are clamped to it)
+    int ja = list[nh], jb = list[max(nh - 1, 0)];
+    float4 pa = s_rec[ja].p, pb = s_rec[jb].p;
+    float2 qa = s_rec[ja].q, qb = s_rec[jb].q;
     for (int kk = nh; kk >= 1; kk -= 2) {
-      const int ja = list[kk], jb = list[kk - 1];
-      const RowTerms ra = row_terms(s_rec[ja].p, s_rec[ja].q, pg.fpy);
-      const RowTerms rb = row_terms(s_rec[jb].p, s_rec[jb].q, pg.fpy);
+      const RowTerms ra = row_terms(pa, qa, pg.fpy);
+      const RowTerms rb = row_terms(pb, qb, pg.fpy);
+      const int ja_ = ja, jb_ = jb;
+      ja = list[max(kk - 2, 0)];
+      jb = list[max(kk - 3, 0)];
+      pa = s_rec[ja].p;
+      pb = s_rec[jb].p;
+      qa = s_rec[ja].q;
+      qb = s_rec[jb].q;
       float2 ea[2], eb[2];
 #pragma unroll
       for (int h = 0; h < 2; ++h) {
@@ -325,19 +355,21 @@ __global__ void __launch_bounds__(BG::kThreads, kBwdMinBlocks) k_bwd_pixels(BwdA
       }
 #pragma unroll
       for (int u = 0; u < 2; ++u) {
-        const int j = u ? jb : ja;
+        const int j = u ? jb_ : ja_;
         const float2 *e = u ? eb : ea;
         const int pos = beg + j;  // entry position in the tile list
         bool pass[kBPX];
 #pragma unroll
         for (int h = 0; h < 2; ++h) {
-          pass[2 * h] = pos < s.last[2 * h] && e[h].x >= kExpSkip;
-          pass[2 * h + 1] = pos < s.last[2 * h + 1] && e[h].y >= kExpSkip;
+          pass[2 * h] = pos < s.last[2 * h] && e[h].x >= kExpMin;
+          pass[2 * h + 1] = pos < s.last[2 * h + 1] && e[h].y >= kExpMin;
         }
-        if (!__any_sync(0xffffffffu, pass[0] || pass[1] || pass[2] || pass[3])) continue;
+        const bool any = pass[0] || pass[1] || pass[2] || pass[3];
+        const unsigned ball = __ballot_sync(0xffffffffu, any);
+        if (!ball) continue;
         const BwdRec &rc = s_rec[j];
-        bwd_entry<kParams>(s, e, pass, rc.rgbz, rc.conic, rc.uv, pg.fpy, fx, a.grad2d + size_t(rc.idx) * kG2,
-                           s_red[w], rv, rp);
+        bwd_entry<kParams>(s, e, pass, any, ball, rc.rgbz, rc.conic, rc.uv, pg.fpy, fx,
+                           a.grad2d + size_t(rc.idx) * kG2, s_red[w], rr);
       }
     }
   }
@@ -352,6 +384,7 @@ struct GaussArgs {
   float *grad2d;
   float4 *g_mean_opa, *g_quat, *g_logscale, *g_rgb;
   float *pose_partials;
+  bool atomic_acc;  // GS_BWD_ATOMIC_ACC: g_* += by red.global.add.v4
 };
 
 template <bool kParams, bool kPose>
@@ -375,10 +408,12 @@ __global__ void __launch_bounds__(kGaussThreads, 4) k_bwd_gauss(GaussArgs a) {
     gb = g2[1];
     if (kParams) {
       gc = g2[2];
-      old_m = a.g_mean_opa[i];
-      old_q = a.g_quat[i];
-      old_l = a.g_logscale[i];
-      old_c = a.g_rgb[i];
+      if (!a.atomic_acc) {
+        old_m = a.g_mean_opa[i];
+        old_q = a.g_quat[i];
+        old_l = a.g_logscale[i];
+        old_c = a.g_rgb[i];
+      }
     }
   }
   if (tt > 0) {
@@ -508,12 +543,20 @@ __global__ void __launch_bounds__(kGaussThreads, 4) k_bwd_gauss(GaussArgs a) {
                                 qy * GRq[5] + qx * GRq[6] + qy * GRq[7]);
       const double dot = gw * qw + gx * qx + gy * qy + gzq * qz;
       // q^ = q / |q| (R18)
-      a.g_mean_opa[i] = make_float4(float(old_m.x + gmu[0]), float(old_m.y + gmu[1]), float(old_m.z + gmu[2]),
-                                    old_m.w + gb.z);
-      a.g_quat[i] = make_float4(float(old_q.x + (gw - qw * dot) * iq), float(old_q.y + (gx - qx * dot) * iq),
-                                float(old_q.z + (gy - qy * dot) * iq), float(old_q.w + (gzq - qz * dot) * iq));
-      a.g_logscale[i] = make_float4(float(old_l.x + gls[0]), float(old_l.y + gls[1]), float(old_l.z + gls[2]), old_l.w);
-      a.g_rgb[i] = make_float4(old_c.x + gc.x, old_c.y + gc.y, old_c.z + gc.z, old_c.w);
+      if (a.atomic_acc) {
+        red_add_v4(reinterpret_cast<float *>(a.g_mean_opa + i), float(gmu[0]), float(gmu[1]), float(gmu[2]), gb.z);
+        red_add_v4(reinterpret_cast<float *>(a.g_quat + i), float((gw - qw * dot) * iq), float((gx - qx * dot) * iq),
+                   float((gy - qy * dot) * iq), float((gzq - qz * dot) * iq));
+        red_add_v4(reinterpret_cast<float *>(a.g_logscale + i), float(gls[0]), float(gls[1]), float(gls[2]), 0.f);
+        red_add_v4(reinterpret_cast<float *>(a.g_rgb + i), gc.x, gc.y, gc.z, 0.f);
+      } else {
+        a.g_mean_opa[i] = make_float4(float(old_m.x + gmu[0]), float(old_m.y + gmu[1]), float(old_m.z + gmu[2]),
+                                      old_m.w + gb.z);
+        a.g_quat[i] = make_float4(float(old_q.x + (gw - qw * dot) * iq), float(old_q.y + (gx - qx * dot) * iq),
+                                  float(old_q.z + (gy - qy * dot) * iq), float(old_q.w + (gzq - qz * dot) * iq));
+        a.g_logscale[i] = make_float4(float(old_l.x + gls[0]), float(old_l.y + gls[1]), float(old_l.z + gls[2]), old_l.w);
+        a.g_rgb[i] = make_float4(old_c.x + gc.x, old_c.y + gc.y, old_c.z + gc.z, old_c.w);
+      }
     }
     if (kPose) {
       // dL/dt = dL/dp; dL/dR = dL/dp mu^T + 2 G_Sc R Sigma
@@ -746,7 +789,7 @@ extern "C" int gs_render_bwd(gs_params p, const gs_view *view, gs_camera cam, gs
   const bool want_params = flags & GS_GRAD_PARAMS, want_pose = flags & GS_GRAD_POSE;
   const bool run_pixels = !(flags & GS_BWD_GAUSS_ONLY), run_gauss = !(flags & GS_BWD_PIXELS_ONLY);
   if (p.n < 0 || !view || !camera_ok(cam) || !tile_range || !T_final || !n_contrib || !dL_dcolor || !dL_ddepth ||
-      (flags & ~(GS_GRAD_PARAMS | GS_GRAD_POSE | GS_BWD_PIXELS_ONLY | GS_BWD_GAUSS_ONLY)) ||
+      (flags & ~(GS_GRAD_PARAMS | GS_GRAD_POSE | GS_BWD_PIXELS_ONLY | GS_BWD_GAUSS_ONLY | GS_BWD_ATOMIC_ACC)) ||
       !(want_params || want_pose) || !(run_pixels || run_gauss)) {
     set_error("gs_render_bwd: invalid argument");
     return GS_ERR_INVALID_ARG;
@@ -795,7 +838,8 @@ extern "C" int gs_render_bwd(gs_params p, const gs_view *view, gs_camera cam, gs
   if (!run_gauss) return check_launch("gs_render_bwd");
   GaussArgs g{p, view, cam.fx, cam.fy, reinterpret_cast<const float4 *>(pr.conic_o), pr.tiles_touched, grad2d,
               reinterpret_cast<float4 *>(g_mean_opa), reinterpret_cast<float4 *>(g_quat),
-              reinterpret_cast<float4 *>(g_logscale), reinterpret_cast<float4 *>(g_rgb), pose_partials};
+              reinterpret_cast<float4 *>(g_logscale), reinterpret_cast<float4 *>(g_rgb), pose_partials,
+              (flags & GS_BWD_ATOMIC_ACC) != 0};
   const int blocks = gs_pose_partials_count(p.n);
   if (want_params && want_pose)
     k_bwd_gauss<true, true><<<blocks, kGaussThreads, 0, s>>>(g);

@@ -53,11 +53,11 @@ struct FwdPix {
 // One list entry at a pixel pair: alpha decision (R11) and the blend of
 // Eqs. 3, 6 and R14, branch-free (alpha = 0 leaves the state bit-identical).
 template <bool kStats>
-__device__ __forceinline__ void fwd_blend(FwdPix &s, float2 e, bool p0, bool p1, float4 c, int pos) {
-  float a0 = fminf(ex2_approx(e.x), kAlphaMax), a1 = fminf(ex2_approx(e.y), kAlphaMax);
-  const bool q0 = p0 && a0 >= kAlphaMin, q1 = p1 && a1 >= kAlphaMin;  // skip (R11)
-  a0 = q0 ? a0 : 0.f;
-  a1 = q1 ? a1 : 0.f;
+__device__ __forceinline__ void fwd_blend(FwdPix &s, float2 e, bool q0, bool q1, float4 c, int pos) {
+  // q: live and alpha~ >= 1/255 (e >= kExpMin, R2'); a skipped pixel's
+  // exponent becomes -inf, so alpha = 2^-inf = 0 (R11)
+  const float a0 = fminf(ex2_approx(q0 ? e.x : -INFINITY), kAlphaMax);
+  const float a1 = fminf(ex2_approx(q1 ? e.y : -INFINITY), kAlphaMax);
   s.last0 = q0 ? pos : s.last0;
   s.last1 = q1 ? pos : s.last1;
   const float2 wt = __fmul2_rn(make_float2(a0, a1), s.T);           // alpha_j T_j
@@ -98,8 +98,8 @@ __device__ __forceinline__ void fwd_entry(FwdPix s[kFNP], const float2 e[kFNP], 
   bool p[kFNP][2], any = false;
 #pragma unroll
   for (int h = 0; h < kFNP; ++h) {
-    p[h][0] = s[h].live0 && e[h].x >= kExpSkip;
-    p[h][1] = s[h].live1 && e[h].y >= kExpSkip;
+    p[h][0] = s[h].live0 && e[h].x >= kExpMin;
+    p[h][1] = s[h].live1 && e[h].y >= kExpMin;
     any |= p[h][0] || p[h][1];
   }
   if (!__any_sync(0xffffffffu, any)) return;

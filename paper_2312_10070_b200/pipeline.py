@@ -17,7 +17,7 @@ from __future__ import annotations
 
 import torch
 
-from .raster import (GS_BWD_GAUSS_ONLY, GS_BWD_PIXELS_ONLY, GS_GRAD_PARAMS, GS_GRAD_POSE, Grads, Params, Rasterizer,
+from .raster import (GS_BWD_ATOMIC_ACC, GS_BWD_GAUSS_ONLY, GS_BWD_PIXELS_ONLY, GS_GRAD_PARAMS, GS_GRAD_POSE, Grads, Params, Rasterizer,
                      gs_render_bwd_gauss_views, lib)
 
 
@@ -58,14 +58,17 @@ class MapStep:
 
     def __init__(self, params: Params, views, cam, tgt_color, tgt_depth, rank=0, world=1, group=None,
                  lambda_color=1.0, lambda_depth=1.0, device="cuda", lanes=8, allreduce=None, schedule="lanes",
-                 ssim=0.0, fused_gauss=False):
+                 ssim=0.0, fused_gauss=False, atomic_gauss=True):
         """ssim: the lambda of Eq. 10's colour loss (0: L1 colour only, as
         BJ.configs[3]; the paper uses 0.2).  fused_gauss: when every view has
         its own lane, run ONE per-Gaussian phase over all views
         (gs_render_bwd_gauss_views) instead of a per-view S6 on each lane;
         off by default: it sits on the step's critical path and measured
         3.61 ms per BJ.configs[3] step against 3.15 ms for the overlapped
-        per-view phases (profiles/r01/README.md)."""
+        per-view phases (profiles/r01/README.md).  atomic_gauss: the
+        per-view S6 adds into the gradient buffer atomically
+        (GS_BWD_ATOMIC_ACC), so the views' Gaussian phases need no ordering;
+        else they are serialised in view order (events)."""
         self.ssim = ssim
         self.params = params
         self.views = views                  # [V, 12] device tensor (all views)
@@ -91,6 +94,7 @@ class MapStep:
         self.copy_stream = None
         self.schedule = schedule
         self.fused_gauss = fused_gauss
+        self.atomic_gauss = atomic_gauss
         self.stage_streams = [torch.cuda.Stream(device=device) for _ in range(3)] if schedule == "stages" else []
 
     def size(self, slack=1.25):
@@ -128,7 +132,8 @@ class MapStep:
 
     def stage_gauss(self, r, k, v):
         """S6: the per-Gaussian phase (+= into the shared gradient buffer)."""
-        r.backward(self.params, self.views[v], GS_GRAD_PARAMS | GS_BWD_GAUSS_ONLY, self.grads)
+        r.backward(self.params, self.views[v],
+                   GS_GRAD_PARAMS | GS_BWD_GAUSS_ONLY | (GS_BWD_ATOMIC_ACC if self.atomic_gauss else 0), self.grads)
 
     def step(self, hooks=None, host=None):
         """One mapping iteration.  hooks: optional dict overriding stages
@@ -137,8 +142,9 @@ class MapStep:
         Schedule "lanes" (default): view k runs all its stages on lane stream
         k % lanes (8 lanes: every view of a BJ.configs[3] step in flight), so
         the latency-bound binning of some views and the tails of the
-        compositing launches of others fill each other's idle SMs; only the
-        per-Gaussian phase is serialised (events) in view order.
+        compositing launches of others fill each other's idle SMs; the
+        per-Gaussian phases add atomically into the gradient buffer (or, with
+        atomic_gauss=False, are serialised in view order by events).
         Schedule "stages": front stages on the lane streams, then one stream
         each for the forward, the per-pixel and the per-Gaussian backward (a
         software pipeline: no two compositing launches of one kind overlap;
@@ -214,7 +220,8 @@ class MapStep:
                     st["front"](r, k, v)
                     st["fwd"](r, k, v, tgt_ready[v])
                     st["bwd"](r, k, v)
-                    s.wait_event(prev)
+                    if not self.atomic_gauss:
+                        s.wait_event(prev)
                     st["gauss"](r, k, v)
                     prev = s.record_event()
         for s in self.streams + self.stage_streams:

@@ -51,18 +51,23 @@ def test_mapstep_equals_sum_of_views_for_any_lanes():
     scale = np.abs(ref_np).max()
     # per-view Gaussian phases in view order; fused (lanes >= V): one
     # multi-view Gaussian phase (gs_render_bwd_gauss_views); "stages": stage streams
-    for lanes, sched, fused in ((1, "lanes", False), (2, "lanes", False), (3, "lanes", False), (4, "lanes", False),
-                                (4, "lanes", True), (8, "lanes", True), (2, "stages", False), (4, "stages", False)):
-        ms = MapStep(P, views, s.cam, tc, td, lanes=lanes, device=d, schedule=sched, fused_gauss=fused)
+    # atomic: per-view Gaussian phases add atomically (GS_BWD_ATOMIC_ACC, unordered)
+    for lanes, sched, fused, atomic in ((1, "lanes", False, True), (2, "lanes", False, True),
+                                        (3, "lanes", False, True), (4, "lanes", False, True),
+                                        (4, "lanes", False, False), (2, "lanes", False, False),
+                                        (4, "lanes", True, True), (8, "lanes", True, True),
+                                        (2, "stages", False, True), (4, "stages", False, False)):
+        ms = MapStep(P, views, s.cam, tc, td, lanes=lanes, device=d, schedule=sched, fused_gauss=fused,
+                     atomic_gauss=atomic)
         ms.size()
         g = ms.step()
         torch.cuda.synchronize()
         got = g.buf.cpu().numpy()
-        assert np.allclose(got, ref_np, rtol=1e-4, atol=1e-5 * scale), (lanes, sched, fused)
+        assert np.allclose(got, ref_np, rtol=1e-4, atol=1e-5 * scale), (lanes, sched, fused, atomic)
         assert np.allclose(ms.losses.cpu().numpy(), torch.stack(losses).cpu().numpy(), rtol=1e-6)
         g2 = ms.step()  # the grad2d scratches were left zeroed: a second step gives the same
         torch.cuda.synchronize()
-        assert np.allclose(g2.buf.cpu().numpy(), got, rtol=1e-5, atol=1e-6 * scale), (lanes, sched, fused)
+        assert np.allclose(g2.buf.cpu().numpy(), got, rtol=1e-5, atol=1e-6 * scale), (lanes, sched, fused, atomic)
 
 
 def test_sharded_sum_equals_unsharded():
