@@ -423,10 +423,11 @@ def bench_ours(a):
 
 def e2e_ours(a, s, ms, device, world=1):
     """Same metric through the public API with HOST buffers: every step copies
-    its inputs (Gaussian parameters, view poses, this rank's RGB-D targets)
-    from pinned host memory and reads the per-view losses back
-    (MapStep.step(host=...): the targets of later views upload while earlier
-    views compute)."""
+    its inputs (Gaussian parameters, view poses, this rank's RGB-D frames as
+    8-bit RGB + 16-bit depth, R42) from pinned host memory and reads the
+    per-view losses back (MapStep.step(host=...): the frames of later views
+    upload while earlier views compute, and a step's uploads overlap the
+    previous step's compute through two alternating device input sets)."""
     import torch
     from paper_2312_10070_b200.pipeline import HostInputs
     host = HostInputs(ms.params, ms.views, ms.tgt_color, ms.tgt_depth, ms.mine, ms.losses.shape[0])

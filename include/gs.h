@@ -379,6 +379,20 @@ int gs_seed(gs_camera cam, const gs_view *view_host, const float *color, const f
             const float *alpha, float alpha_n, float rho, int32_t max_new, uint32_t seed,
             gs_params p, int32_t capacity, void *ws, size_t ws_bytes, int32_t *n_new, void *stream);
 
+/* Input frames ("the RGBD frame", "the input color and depth map
+ * at frame i", "an RGBD sensor"): unpacks a frame in the sensors' and
+ * datasets' format, 8-bit RGB and 16-bit depth, into the fp32 planar targets
+ * of gs_loss / gs_tracking_loss / gs_seed:
+ *   tgt_color[c][q] = rgb[q][c] / 255   (IEEE fp32 division)
+ *   tgt_depth[q]    = depth16[q] * depth_scale   (fp32; 0 stays 0 = invalid)
+ *   rgb        (device) [H][W][3] uint8, interleaved
+ *   depth16    (device) [H][W] uint16, in units of depth_scale metres
+ *              (e.g. 1/5000 for TUM-RGBD, 1/6553.5 for Replica)
+ *   tgt_color  (device) [3][H][W] fp32;  tgt_depth (device) [H][W] fp32
+ * Errors: GS_ERR_INVALID_ARG (null, bad camera, depth_scale <= 0). */
+int gs_unpack_rgbd(gs_camera cam, const uint8_t *rgb, const uint16_t *depth16, float depth_scale,
+                   float *tgt_color, float *tgt_depth, void *stream);
+
 /* S5+S6 — backward (Eqs. 7-8; R16, R17).
  *
  * Per pixel, replays the composited entries back to front (same alpha

@@ -25,7 +25,7 @@ ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NVCC_FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-I", INCLUDE, "-I", CSRC,
               "--expt-relaxed-constexpr", "-Xptxas", "-warn-spills"]
 PER_FILE = {"project.cu": ["--fmad=false"]}
-SOURCES = ["abi.cpp", "project.cu", "binsort.cu", "render_fwd.cu", "loss.cu", "tracking_loss.cu", "ssim.cu", "optim.cu", "seed.cu", "render_bwd.cu",
+SOURCES = ["abi.cpp", "project.cu", "binsort.cu", "render_fwd.cu", "loss.cu", "tracking_loss.cu", "ssim.cu", "optim.cu", "seed.cu", "rgbd.cu", "render_bwd.cu",
            "pose.cu"]
 HEADERS = ["gs_internal.cuh", "raster_common.cuh"]
 

@@ -275,4 +275,20 @@ def upstream_maps(seed, cam: Camera):
     return gc, gd, ga
 
 
+# depth unit of the synthetic sensor frames: 0.2 mm (TUM-RGBD's factor 5000;
+# DESIGN.md R42)
+DEPTH_SCALE = 1.0 / 5000.0
+
+
+def quantize_rgbd(color, depth, scale=DEPTH_SCALE):
+    """A synthetic RGB-D frame in the sensors' format (R42):
+    rgb8 = round(clip(C, 0, 1) * 255) as [H, W, 3] uint8 and
+    depth16 = round(D / scale) clipped to [0, 65535] as [H, W] uint16, from
+    fp32 planar colour [3, H, W] and depth [H, W] (e.g. a target render)."""
+    c = np.clip(np.asarray(color, np.float64), 0.0, 1.0)
+    rgb8 = np.rint(c * 255.0).astype(np.uint8).transpose(1, 2, 0).copy()
+    d16 = np.clip(np.rint(np.asarray(depth, np.float64) / float(np.float32(scale))), 0, 65535).astype(np.uint16)
+    return rgb8, d16
+
+
 CONFIGS = {0: config0, 1: config1, 2: config2, 3: config3, 4: config4}

@@ -15,26 +15,61 @@ order of calls.
 """
 from __future__ import annotations
 
+import numpy as np
 import torch
 
 from .raster import (GS_BWD_ATOMIC_ACC, GS_BWD_GAUSS_ONLY, GS_BWD_PIXELS_ONLY, GS_GRAD_PARAMS, GS_GRAD_POSE, Grads, Params, Rasterizer,
-                     gs_render_bwd_gauss_views, lib)
+                     gs_render_bwd_gauss_views, gs_unpack_rgbd, lib)
 
 
 class HostInputs:
     """Pinned host buffers of one mapping step's inputs (parameters, view
-    poses, this rank's RGB-D targets) and its per-view loss output."""
+    poses, this rank's RGB-D targets) and its per-view loss output.
 
-    def __init__(self, params: Params, views, tgt_color, tgt_depth, mine, n_losses):
+    frames="rgbd16" (default): the targets are held as the sensors' frames,
+    8-bit RGB [H][W][3] + 16-bit depth [H][W] in units of depth_scale
+    (R42), uploaded as such and unpacked on the
+    device (gs_unpack_rgbd); frames="f32": fp32 planar targets, uploaded as is."""
+
+    def __init__(self, params: Params, views, tgt_color, tgt_depth, mine, n_losses, frames="rgbd16",
+                 depth_scale=None):
+        from . import inputs
         pin = lambda t: t.detach().cpu().contiguous().pin_memory()
         self.params = {k: pin(getattr(params, k)) for k in ("mean_opa", "quat", "logscale", "rgb")}
         self.views = pin(views)
-        self.tgt_color = {v: pin(tgt_color[v]) for v in mine}
-        self.tgt_depth = {v: pin(tgt_depth[v]) for v in mine}
+        self.frames = frames
+        self.depth_scale = inputs.DEPTH_SCALE if depth_scale is None else depth_scale
+        if frames == "rgbd16":
+            self.rgb8, self.d16, self.dev_rgb8, self.dev_d16 = {}, {}, {}, {}
+            for v in mine:
+                r8, d16 = inputs.quantize_rgbd(tgt_color[v].cpu().numpy(), tgt_depth[v].cpu().numpy(),
+                                               self.depth_scale)
+                self.rgb8[v] = torch.from_numpy(r8).pin_memory()
+                self.d16[v] = torch.from_numpy(d16.view(np.int16)).pin_memory()
+                self.dev_rgb8[v] = torch.empty_like(self.rgb8[v], device=tgt_color[v].device)
+                self.dev_d16[v] = torch.empty_like(self.d16[v], device=tgt_color[v].device)
+        elif frames == "f32":
+            self.tgt_color = {v: pin(tgt_color[v]) for v in mine}
+            self.tgt_depth = {v: pin(tgt_depth[v]) for v in mine}
+        else:
+            raise ValueError(frames)
+        self.mine = list(mine)
         self.loss = torch.empty(n_losses, 4, dtype=torch.float32).pin_memory()
+
+    def upload_targets(self, v, cam, tgt_color, tgt_depth):
+        """On the current (copy) stream: view v's frame into its device targets."""
+        if self.frames == "rgbd16":
+            self.dev_rgb8[v].copy_(self.rgb8[v], non_blocking=True)
+            self.dev_d16[v].copy_(self.d16[v], non_blocking=True)
+            gs_unpack_rgbd(cam, self.dev_rgb8[v], self.dev_d16[v], self.depth_scale, tgt_color, tgt_depth)
+        else:
+            tgt_color.copy_(self.tgt_color[v], non_blocking=True)
+            tgt_depth.copy_(self.tgt_depth[v], non_blocking=True)
 
     def h2d_bytes(self):
         b = sum(t.numel() * t.element_size() for t in self.params.values()) + self.views.numel() * 4
+        if self.frames == "rgbd16":
+            return b + sum(self.rgb8[v].numel() + 2 * self.d16[v].numel() for v in self.mine)
         return b + sum(t.numel() * 4 for t in self.tgt_color.values()) + sum(t.numel() * 4 for t in self.tgt_depth.values())
 
     def d2h_bytes(self):
@@ -51,9 +86,9 @@ class MapStep:
 
     Views are pipelined over `lanes` CUDA streams (default 8: every view of a BJ.configs[3] step in flight), each with its own
     Rasterizer buffers: the latency-bound sort / loss kernels of one view
-    overlap the compute-bound compositing kernels of another.  Only the
-    per-Gaussian phase of gs_render_bwd (a read-modify-write of the shared
-    gradient buffer) is serialised across views, by events, in view order.
+    overlap the compute-bound compositing kernels of another.  The
+    per-Gaussian phases of gs_render_bwd add into the shared gradient buffer
+    atomically (GS_BWD_ATOMIC_ACC), so no view waits for another.
     """
 
     def __init__(self, params: Params, views, cam, tgt_color, tgt_depth, rank=0, world=1, group=None,
@@ -91,7 +126,8 @@ class MapStep:
         self.grads = Grads.zeros(params.n, device)
         # per view: (total, L1 colour, L1 depth, SSIM if ssim > 0)
         self.losses = torch.zeros(max(len(self.mine), 1), 4, dtype=torch.float32, device=device)
-        self.copy_stream = None
+        self.copy_stream = None  # host-input uploads (created on the first step(host=...))
+        self._slots = None
         self.schedule = schedule
         self.fused_gauss = fused_gauss
         self.atomic_gauss = atomic_gauss
@@ -161,20 +197,42 @@ class MapStep:
             st.update(hooks)
         main = torch.cuda.current_stream()
         tgt_ready = {v: None for v in self.mine}
+        rgb_ready = None
+
+        def fwd(r, k, v):  # the forward reads the colours: wait for their upload
+            if rgb_ready is not None:
+                torch.cuda.current_stream().wait_event(rgb_ready)
+            st["fwd"](r, k, v, tgt_ready[v])
+        slot = None
         if host is not None:
             if self.copy_stream is None:
                 self.copy_stream = torch.cuda.Stream(device=self.params.mean_opa.device)
+                # two device input sets used alternately: the uploads of step
+                # k + 1 overlap the compute of step k (they wait only for the
+                # step that last read their set, k - 1)
+                clone = Params(*(getattr(self.params, n).clone() for n in ("mean_opa", "quat", "logscale", "rgb")))
+                self._slots = [(self.params, self.views, self.tgt_color, self.tgt_depth),
+                               (clone, self.views.clone(), {v: t.clone() for v, t in self.tgt_color.items()},
+                                {v: t.clone() for v, t in self.tgt_depth.items()})]
+                self._released = [main.record_event(), main.record_event()]
+                self._slot = 0
+            slot = self._slot
+            self._slot ^= 1
+            self.params, self.views, self.tgt_color, self.tgt_depth = self._slots[slot]
             cs = self.copy_stream
-            cs.wait_stream(main)  # the previous step no longer reads these buffers
+            cs.wait_event(self._released[slot])  # the step that last read this set is done
             with torch.cuda.stream(cs):
-                for name in ("mean_opa", "quat", "logscale", "rgb"):
+                # the projection's inputs first; the colours (read from the
+                # forward on) and the frames follow while the fronts run
+                for name in ("mean_opa", "quat", "logscale"):
                     getattr(self.params, name).copy_(host.params[name], non_blocking=True)
                 self.views.copy_(host.views, non_blocking=True)
                 params_ready = cs.record_event()
+                self.params.rgb.copy_(host.params["rgb"], non_blocking=True)
+                rgb_ready = cs.record_event()
                 for v in self.mine:
-                    self.tgt_color[v].copy_(host.tgt_color[v], non_blocking=True)
-                    self.tgt_depth[v].copy_(host.tgt_depth[v], non_blocking=True)
-                    tgt_ready[v] = cs.record_event()
+                    host.upload_targets(v, self.r.cam, self.tgt_color[v], self.tgt_depth[v])
+                    tgt_ready[v] = cs.record_event()  # also orders the colours before every loss
             main.wait_event(params_ready)
         self.grads.zero_()
         start = main.record_event()
@@ -192,7 +250,7 @@ class MapStep:
                         s.wait_event(ev)
                     with torch.cuda.stream(s):
                         if name == "fwd":
-                            st[name](r, k, v, tgt_ready[v])
+                            fwd(r, k, v)
                         else:
                             st[name](r, k, v)
                         ev = s.record_event()
@@ -205,7 +263,7 @@ class MapStep:
                 s, r = self.streams[k], self.lanes[k]
                 with torch.cuda.stream(s):
                     st["front"](r, k, v)
-                    st["fwd"](r, k, v, tgt_ready[v])
+                    fwd(r, k, v)
                     st["bwd"](r, k, v)
             for s in self.streams:
                 main.wait_stream(s)
@@ -218,7 +276,7 @@ class MapStep:
                 s, r = self.streams[lane], self.lanes[lane]
                 with torch.cuda.stream(s):
                     st["front"](r, k, v)
-                    st["fwd"](r, k, v, tgt_ready[v])
+                    fwd(r, k, v)
                     st["bwd"](r, k, v)
                     if not self.atomic_gauss:
                         s.wait_event(prev)
@@ -232,6 +290,7 @@ class MapStep:
             self.allreduce(self.grads.buf)
         if host is not None:
             host.loss.copy_(self.losses, non_blocking=True)
+            self._released[slot] = main.record_event()
         return self.grads
 
     def launches_per_step(self):

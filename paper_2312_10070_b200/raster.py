@@ -20,7 +20,7 @@ from ._lib import (GS_BWD_ATOMIC_ACC, GS_BWD_GAUSS_ONLY, GS_BWD_PIXELS_ONLY, GS_
                    GsParams, GsPoseStep, GsProj, GsView, check, lib)
 
 __all__ = ["Params", "Grads", "Proj", "Frame", "Rasterizer", "camera", "gs_project", "gs_bin_sort",
-           "gs_render_fwd", "gs_tile_order", "gs_loss", "gs_tracking_loss", "gs_ssim", "gs_iso_reg", "gs_adam_step", "gs_prune", "gs_seed", "Optimizer", "gs_render_bwd", "gs_render_bwd_gauss_views", "gs_pose_grad", "GS_GRAD_PARAMS", "GS_GRAD_POSE", "GS_BWD_PIXELS_ONLY", "GS_BWD_GAUSS_ONLY", "GS_BWD_ATOMIC_ACC",
+           "gs_render_fwd", "gs_tile_order", "gs_loss", "gs_tracking_loss", "gs_ssim", "gs_iso_reg", "gs_adam_step", "gs_prune", "gs_seed", "gs_unpack_rgbd", "Optimizer", "gs_render_bwd", "gs_render_bwd_gauss_views", "gs_pose_grad", "GS_GRAD_PARAMS", "GS_GRAD_POSE", "GS_BWD_PIXELS_ONLY", "GS_BWD_GAUSS_ONLY", "GS_BWD_ATOMIC_ACC",
            "GsError", "device_check"]
 
 
@@ -207,6 +207,13 @@ def gs_seed(cam: GsCamera, view, color, depth, alpha, alpha_n, rho, max_new, see
     check(lib().gs_seed(cam, C.byref(gv), _p(color), _p(depth), _p(alpha), float(alpha_n), float(rho), int(max_new),
                         int(seed) & 0xFFFFFFFF, P, int(cap), _p(ws), ws.numel() * ws.element_size(), _p(n_new),
                         _stream(stream)), "gs_seed")
+
+
+def gs_unpack_rgbd(cam: GsCamera, rgb8, depth16, depth_scale, tgt_color, tgt_depth, stream=None):
+    """An 8-bit RGB [H][W][3] + 16-bit depth [H][W] frame (device tensors,
+    uint8 / int16 or uint16 storage) into fp32 planar targets [3][H][W], [H][W]."""
+    check(lib().gs_unpack_rgbd(cam, _p(rgb8), _p(depth16), float(depth_scale), _p(tgt_color), _p(tgt_depth),
+                               _stream(stream)), "gs_unpack_rgbd")
 
 
 class Optimizer:

@@ -89,3 +89,46 @@ def test_sharded_sum_equals_unsharded():
     torch.cuda.synchronize()
     scale = g1.abs().max().item()
     assert torch.allclose(acc, g1, rtol=1e-4, atol=1e-5 * scale)
+
+
+@pytest.mark.parametrize("frames", ["f32", "rgbd16"])
+def test_mapstep_with_host_inputs(frames):
+    """MapStep.step(host=HostInputs): inputs uploaded from pinned host memory
+    inside the step (parameters in two parts, the frames view by view, as
+    8-bit RGB + 16-bit depth unpacked by gs_unpack_rgbd for "rgbd16") give
+    the step of device-resident inputs holding the same values; the per-view
+    losses are read back into host.loss."""
+    from oracle import rgbd
+    from paper_2312_10070_b200.pipeline import HostInputs
+    d = torch.device("cuda")
+    s = _small_submap(seed=6)
+    P = Params.from_numpy(*s.params(), device=d)
+    views = torch.as_tensor(s.views, device=d)
+    tc, td = _targets(s, d)
+    V = views.shape[0]
+    if frames == "rgbd16":  # the device-resident reference holds the unpacked sensor frames
+        for v in range(V):
+            r8, d16 = inputs.quantize_rgbd(tc[v].cpu().numpy(), td[v].cpu().numpy())
+            c, z = rgbd.unpack(r8, d16, inputs.DEPTH_SCALE)
+            tc[v], td[v] = torch.as_tensor(c, device=d), torch.as_tensor(z, device=d)
+    ms = MapStep(P, views, s.cam, tc, td, lanes=4, device=d)
+    ms.size()
+    ref = ms.step().buf.clone()
+    ref_loss = ms.losses.clone()
+    torch.cuda.synchronize()
+    host = HostInputs(ms.params, ms.views, ms.tgt_color, ms.tgt_depth, ms.mine, ms.losses.shape[0], frames=frames)
+    # scribble over the device copies: the step must bring everything from the host
+    for name in ("mean_opa", "quat", "logscale", "rgb"):
+        getattr(ms.params, name).fill_(float("nan"))
+    ms.views.zero_()
+    for v in range(V):
+        ms.tgt_color[v].fill_(-1.0)
+        ms.tgt_depth[v].fill_(-1.0)
+    for _ in range(2):
+        g = ms.step(host=host)
+    torch.cuda.synchronize()
+    scale = ref.abs().max()
+    assert torch.allclose(g.buf, ref, rtol=1e-4, atol=1e-5 * scale)
+    assert torch.allclose(host.loss, ref_loss.cpu(), rtol=1e-6, atol=0)
+    assert host.h2d_bytes() == 4 * s.n * 16 + V * 48 + (
+        V * s.cam.width * s.cam.height * (5 if frames == "rgbd16" else 16))
