@@ -387,8 +387,11 @@ struct GaussArgs {
   bool atomic_acc;  // GS_BWD_ATOMIC_ACC: g_* += by red.global.add.v4
 };
 
+#ifndef GAUSS_MINB
+#define GAUSS_MINB 4
+#endif
 template <bool kParams, bool kPose>
-__global__ void __launch_bounds__(kGaussThreads, 4) k_bwd_gauss(GaussArgs a) {
+__global__ void __launch_bounds__(kGaussThreads, GAUSS_MINB) k_bwd_gauss(GaussArgs a) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   float pose[12];
 #pragma unroll
