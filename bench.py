@@ -491,7 +491,9 @@ def bench_tracking(device, masked=None):
             "loss": "L1 colour + L1 depth (BJ.configs[2])" if masked is None else
                     "Eq. 15 masked: alpha^3 x inlier (50 x median), lambda_c = %g" % masked[0],
             "value": 100 / (med * 1e-3), "unit": "iter/s", "ms_per_iter": med / 100,
-            "graph": "100 iterations captured once (project, sort, render, loss, pose bwd, pose grad + Adam)",
+            "graph": ("100 iterations captured once (project, sort, render with the L1 gradient maps fused "
+                      "(gs_render_fwd_l1; scales once per frame), pose bwd, pose grad + Adam)") if masked is None else
+                     "100 iterations captured once (project, sort, render, loss, pose bwd, pose grad + Adam)",
             "gpu_launches_per_iter": loop.launches_per_iter(),
             "start_err": {"rot_deg": float(rot0), "trans_cm": float(np.linalg.norm(sv[9:]) * 100)},
             "final_err": {"rot_deg": float(rot_err), "trans_cm": float(np.linalg.norm(t) * 100)}}

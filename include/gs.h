@@ -229,6 +229,22 @@ int gs_render_fwd(gs_proj pr, const int32_t *sorted_idx, const int32_t *tile_ran
                   float *alpha, float *T_final, int32_t *n_contrib, int32_t *stats,
                   int32_t *tile_work, void *stream);
 
+/* S3 with S4's gradient fused (tracking, BJ.configs[2]; SURVEY S4 "fusable"):
+ * gs_render_fwd, then in the same kernel, per pixel, the gradient maps of
+ * gs_loss with weight 1:  dL_dcolor = scales[0] sign(C^ - C*),
+ * dL_ddepth = scales[1] sign(D^ - D*) where D* > 0, else 0 (sign(0) = 0) —
+ * the same fp32 values gs_loss writes.  The loss VALUE is not computed (the
+ * tracking update needs only the gradient).  Arguments as gs_render_fwd
+ * (no stats) plus:
+ *   tgt_color [3][H][W], tgt_depth [H][W] (device) the frame's targets
+ *   scales    (device) [2] from gs_loss_scales for this target frame
+ *   dL_dcolor [3][H][W], dL_ddepth [H][W] (device) written */
+int gs_render_fwd_l1(gs_proj pr, const int32_t *sorted_idx, const int32_t *tile_range,
+                     const int32_t *tile_order, gs_camera cam, float *color, float *depth,
+                     float *alpha, float *T_final, int32_t *n_contrib, int32_t *tile_work,
+                     const float *tgt_color, const float *tgt_depth, const float *scales,
+                     float *dL_dcolor, float *dL_ddepth, void *stream);
+
 /* Scheduling utility: tile ids by descending work (64 buckets of max/64, order
  * inside a bucket unspecified), e.g. from gs_render_fwd's tile_work for
  * gs_render_bwd.  work (device) [T] >= 0; order (device) [T]. */
@@ -250,6 +266,13 @@ int gs_loss(gs_camera cam, const float *color, const float *depth,
             const float *tgt_color, const float *tgt_depth, const float *weight,
             float lambda_color, float lambda_depth, void *ws, size_t ws_bytes,
             float *loss, float *dL_dcolor, float *dL_ddepth, void *stream);
+
+/* The two gradient scales of gs_loss for a target frame (weight 1):
+ * scales[0] = lambda_color / (3HW), scales[1] = lambda_depth / |V| (0 if
+ * |V| = 0), |V| = #{D* > 0}; computed once per frame for gs_render_fwd_l1.
+ *   ws (device) >= gs_loss_workspace_bytes(cam); scales (device) [2]. */
+int gs_loss_scales(gs_camera cam, const float *tgt_depth, float lambda_color, float lambda_depth,
+                   void *ws, size_t ws_bytes, float *scales, void *stream);
 
 /* NEXT(1) — masked tracking loss (Eq. 15; S:286-294, S:425-438;
  * DESIGN.md R29-R31).  Tracking only: gradients flow to the rendered colour

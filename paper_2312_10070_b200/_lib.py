@@ -76,6 +76,9 @@ _PROTOS = {
     "gs_render_fwd": (C.c_int, [GsProj, _VP, _VP, _VP, GsCamera, _VP, _VP, _VP, _VP, _VP, _VP, _VP, _VP]),
     "gs_tile_order": (C.c_int, [_VP, _I32, _VP, _VP]),
     "gs_loss": (C.c_int, [GsCamera, _VP, _VP, _VP, _VP, _VP, _F, _F, _VP, _SZ, _VP, _VP, _VP, _VP]),
+    "gs_loss_scales": (C.c_int, [GsCamera, _VP, _F, _F, _VP, _SZ, _VP, _VP]),
+    "gs_render_fwd_l1": (C.c_int, [GsProj, _VP, _VP, _VP, GsCamera, _VP, _VP, _VP, _VP, _VP, _VP, _VP, _VP, _VP, _VP,
+                                   _VP, _VP]),
     "gs_tracking_loss_workspace_bytes": (_SZ, [GsCamera]),
     "gs_ssim_workspace_bytes": (_SZ, [GsCamera]),
     "gs_opt_workspace_bytes": (_SZ, [_I32]),

@@ -115,7 +115,40 @@ __global__ void __launch_bounds__(kLossThreads) k_loss_final(const double *part,
   }
 }
 
+// gs_loss_scales: the two gradient scales of k_loss_main, from the partial
+// counts of k_loss_count
+__global__ void __launch_bounds__(32) k_loss_scales(const uint32_t *__restrict__ cnt_part, int nblk, int64_t HW,
+                                                    float lc, float ld, float *scales) {
+  uint32_t nv = 0;
+  for (int b = threadIdx.x; b < nblk; b += 32) nv += cnt_part[b];
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) nv += __shfl_xor_sync(0xffffffffu, nv, o);
+  if (threadIdx.x == 0) {
+    scales[0] = float(double(lc) / (3.0 * double(HW)));
+    scales[1] = nv ? float(double(ld) / double(nv)) : 0.f;
+  }
+}
+
 }  // namespace gs
+
+extern "C" int gs_loss_scales(gs_camera cam, const float *tgt_depth, float lambda_color, float lambda_depth,
+                              void *ws, size_t ws_bytes, float *scales, void *stream) {
+  using namespace gs;
+  if (!camera_ok(cam) || !tgt_depth || !scales || !(lambda_color >= 0.f) || !(lambda_depth >= 0.f)) {
+    set_error("gs_loss_scales: invalid argument");
+    return GS_ERR_INVALID_ARG;
+  }
+  if (!ws || ws_bytes < loss_ws_bytes()) {
+    set_error("gs_loss_scales: workspace %zu < %zu bytes", ws_bytes, loss_ws_bytes());
+    return GS_ERR_WORKSPACE;
+  }
+  cudaStream_t s = as_stream(stream);
+  const int64_t HW = int64_t(cam.width) * cam.height;
+  uint32_t *cnt_part = reinterpret_cast<uint32_t *>(static_cast<double *>(ws) + 2 * kLossBlocks);
+  k_loss_count<<<kLossBlocks, kLossThreads, 0, s>>>(tgt_depth, HW, cnt_part);
+  k_loss_scales<<<1, 32, 0, s>>>(cnt_part, kLossBlocks, HW, lambda_color, lambda_depth, scales);
+  return check_launch("gs_loss_scales");
+}
 
 extern "C" size_t gs_loss_workspace_bytes(gs_camera cam) {
   if (!gs::camera_ok(cam)) return 0;

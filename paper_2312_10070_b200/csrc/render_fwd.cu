@@ -28,6 +28,10 @@ struct FwdArgs {
   int W, H, TX;
   float *color, *depth, *alpha, *T_final;
   int32_t *n_contrib, *stats, *tile_work;
+  // fused L1 gradient epilogue (gs_render_fwd_l1): targets, device scales
+  // (lambda_c / 3HW, lambda_d / |V|) from gs_loss_scales, gradient maps
+  const float *tc, *td, *scales;
+  float *gC, *gD;
 };
 
 #ifndef FWD_NP
@@ -108,7 +112,7 @@ __device__ __forceinline__ void fwd_entry(FwdPix s[kFNP], const float2 e[kFNP], 
   for (int h = 0; h < kFNP; ++h) fwd_blend<kStats>(s[h], e[h], p[h][0], p[h][1], c, pos);
 }
 
-template <bool kStats>
+template <bool kStats, bool kL1 = false>
 __global__ void __launch_bounds__(FG::kThreads, 1) k_render_fwd(FwdArgs a) {
   // one staged record per entry; record kBatch is a sentinel entry whose exponent is -inf
   __shared__ FwdRec s_rec[kBatch + 1];
@@ -217,6 +221,18 @@ __global__ void __launch_bounds__(FG::kThreads, 1) k_render_fwd(FwdArgs a) {
         a.stats[q] = tm[k];  // entries scanned = termination position or list length
         a.stats[HW + q] = nc[k];
       }
+      if (kL1) {  // gs_loss's gradient maps, the same fp32 values (weight 1, sign(0) = 0, R21)
+        const float sc = __ldg(a.scales), sd = __ldg(a.scales + 1);
+        const float cc[3] = {cc0[k], cc1[k], cc2[k]};
+#pragma unroll
+        for (int ch = 0; ch < 3; ++ch) {
+          const float r = cc[ch] - __ldg(a.tc + ch * HW + q);
+          a.gC[ch * HW + q] = sc * 1.f * float((r > 0.f) - (r < 0.f));
+        }
+        const float t = __ldg(a.td + q);
+        const float r = DD[k] - t;
+        a.gD[q] = t > 0.f ? sd * 1.f * float((r > 0.f) - (r < 0.f)) : 0.f;
+      }
     }
   }
 }
@@ -239,11 +255,36 @@ extern "C" int gs_render_fwd(gs_proj pr, const int32_t *sorted_idx, const int32_
   FwdArgs a{reinterpret_cast<const double2 *>(pr.uv), reinterpret_cast<const float4 *>(pr.coef),
             reinterpret_cast<const float4 *>(pr.rgbz), sorted_idx, reinterpret_cast<const int2 *>(tile_range),
             tile_order, cam.width, cam.height, tiles_x(cam), color, depth, alpha, T_final, n_contrib, stats,
-            tile_work};
+            tile_work, nullptr, nullptr, nullptr, nullptr, nullptr};
   const int T = tiles_x(cam) * tiles_y(cam);
   if (stats)
     k_render_fwd<true><<<T, FG::kThreads, 0, as_stream(stream)>>>(a);
   else
     k_render_fwd<false><<<T, FG::kThreads, 0, as_stream(stream)>>>(a);
   return check_launch("gs_render_fwd");
+}
+
+extern "C" int gs_render_fwd_l1(gs_proj pr, const int32_t *sorted_idx, const int32_t *tile_range,
+                                const int32_t *tile_order, gs_camera cam, float *color, float *depth, float *alpha,
+                                float *T_final, int32_t *n_contrib, int32_t *tile_work, const float *tgt_color,
+                                const float *tgt_depth, const float *scales, float *dL_dcolor, float *dL_ddepth,
+                                void *stream) {
+  using namespace gs;
+  if (!camera_ok(cam) || !tile_range || !color || !depth || !alpha || !T_final || !n_contrib || !tgt_color ||
+      !tgt_depth || !scales || !dL_dcolor || !dL_ddepth) {
+    set_error("gs_render_fwd_l1: invalid argument");
+    return GS_ERR_INVALID_ARG;
+  }
+  if (!pr.uv || !pr.coef || !pr.rgbz || !aligned16(pr.uv) || !aligned16(pr.coef) || !aligned16(pr.rgbz) ||
+      (reinterpret_cast<uintptr_t>(tile_range) & 7u)) {
+    set_error("gs_render_fwd_l1: null or misaligned projection arrays");
+    return GS_ERR_INVALID_ARG;
+  }
+  FwdArgs a{reinterpret_cast<const double2 *>(pr.uv), reinterpret_cast<const float4 *>(pr.coef),
+            reinterpret_cast<const float4 *>(pr.rgbz), sorted_idx, reinterpret_cast<const int2 *>(tile_range),
+            tile_order, cam.width, cam.height, tiles_x(cam), color, depth, alpha, T_final, n_contrib, nullptr,
+            tile_work, tgt_color, tgt_depth, scales, dL_dcolor, dL_ddepth};
+  const int T = tiles_x(cam) * tiles_y(cam);
+  k_render_fwd<false, true><<<T, FG::kThreads, 0, as_stream(stream)>>>(a);
+  return check_launch("gs_render_fwd_l1");
 }

@@ -316,10 +316,15 @@ class TrackingLoop:
     """K tracking iterations on one GPU, graph-captured."""
 
     def __init__(self, params: Params, cam, tgt_color, tgt_depth, start_view, iters=100, lambda_color=1.0,
-                 lambda_depth=1.0, step=(2e-3, 1e-3, 0.9, 0.999, 1e-8), device="cuda", masked=None):
+                 lambda_depth=1.0, step=(2e-3, 1e-3, 0.9, 0.999, 1e-8), device="cuda", masked=None,
+                 fused_loss=True):
         """masked: None for the L1 colour + depth loss of BJ.configs[2], or
-        (lambda_c, inlier_mult) for the masked tracking loss of Eq. 15."""
+        (lambda_c, inlier_mult) for the masked tracking loss of Eq. 15.
+        fused_loss (L1 only): the gradient maps are written by the forward
+        kernel (gs_render_fwd_l1, the same values as gs_loss) and no loss value
+        is computed per iteration; else gs_loss runs after the forward."""
         self.masked = masked
+        self.fused_loss = fused_loss
         self.params = params
         self.r = Rasterizer(params.n, cam, device=device)
         self.tc, self.td = tgt_color, tgt_depth
@@ -337,13 +342,22 @@ class TrackingLoop:
         self.r.set_capacity(int(P * slack) + 4096)
         return P
 
+    def prepare(self):
+        """Once per target frame: the L1 gradient scales (fused mode)."""
+        if self.masked is None and self.fused_loss:
+            self.r.loss_scales(self.td, self.lc, self.ld)
+
     def iteration(self):
         r = self.r
-        r.forward(self.params, self.view)
-        if self.masked is None:
-            r.compute_loss(self.tc, self.td, None, self.lc, self.ld)
+        if self.masked is None and self.fused_loss:
+            # S1-S3 with the L1 gradient maps written by the forward (gs_render_fwd_l1)
+            r.forward_l1(self.params, self.view, self.tc, self.td)
         else:
-            r.compute_tracking_loss(self.tc, self.td, *self.masked)
+            r.forward(self.params, self.view)
+            if self.masked is None:
+                r.compute_loss(self.tc, self.td, None, self.lc, self.ld)
+            else:
+                r.compute_tracking_loss(self.tc, self.td, *self.masked)
         r.backward(self.params, self.view, GS_GRAD_POSE)
         r.pose_grad(self.view, self.stepcfg, self.adam, dL_dtwist=self.dtwist)
 
@@ -356,6 +370,7 @@ class TrackingLoop:
         s = torch.cuda.Stream()
         s.wait_stream(torch.cuda.current_stream())
         with torch.cuda.stream(s):
+            self.prepare()
             for _ in range(2):  # warm-up outside capture (lazy attributes, module load)
                 self.iteration()
         torch.cuda.current_stream().wait_stream(s)
@@ -363,6 +378,7 @@ class TrackingLoop:
         self.reset()
         g = torch.cuda.CUDAGraph()
         with torch.cuda.graph(g):
+            self.prepare()  # once per target frame, inside the timed graph
             for _ in range(self.iters):
                 self.iteration()
         self.graph = g
@@ -371,11 +387,15 @@ class TrackingLoop:
     def run(self):
         self.reset()
         if self.graph is None:
+            self.prepare()
             for _ in range(self.iters):
                 self.iteration()
         else:
             self.graph.replay()
 
     def launches_per_iter(self):
-        # masked loss: 6 kernels (residual + digit 0, 3 digit passes, apply, final) instead of 3
+        # masked loss: 6 kernels (residual + digit 0, 3 digit passes, apply, final) instead of 3;
+        # fused L1: none (the forward writes the maps; + 2 per graph for the scales)
+        if self.masked is None and self.fused_loss:
+            return kernels_per_view(self.r.cam) + 1 - 3
         return kernels_per_view(self.r.cam) + 1 + (3 if self.masked is not None else 0)
