@@ -97,23 +97,25 @@ struct PoseArgs {
   float *dL_dview, *dL_dtwist, *dL_dqt;
 };
 
-__global__ void __launch_bounds__(256) k_pose_grad(PoseArgs a) {
-  __shared__ double sh[256][13];
-  double acc[12];
-#pragma unroll
-  for (int c = 0; c < 12; ++c) acc[c] = 0.0;
-  for (int k = threadIdx.x; k < a.n_partials; k += blockDim.x)
-#pragma unroll
-    for (int c = 0; c < 12; ++c) acc[c] += double(a.partials[size_t(k) * 12 + c]);
-#pragma unroll
-  for (int c = 0; c < 12; ++c) sh[threadIdx.x][c] = acc[c];
+constexpr int kPoseThreads = 384;  // 32 record lanes x 12 components
+
+__global__ void __launch_bounds__(kPoseThreads) k_pose_grad(PoseArgs a) {
+  // fixed-order fp64 reduction of the [n][12] partials: thread t owns
+  // component c = t % 12 of the records k = t / 12 (mod 32) -> consecutive
+  // threads read consecutive floats (coalesced); then the 32 lane sums of
+  // each component are added in lane order
+  __shared__ double sh[32][13];
+  const int c = threadIdx.x % 12, l = threadIdx.x / 12;
+  double acc = 0.0;
+  for (int k = l; k < a.n_partials; k += 32) acc += double(a.partials[size_t(k) * 12 + c]);
+  sh[l][c] = acc;
   __syncthreads();
-  for (int s = 128; s > 0; s >>= 1) {
-    if (threadIdx.x < s)
-#pragma unroll
-      for (int c = 0; c < 12; ++c) sh[threadIdx.x][c] += sh[threadIdx.x + s][c];
-    __syncthreads();
+  if (threadIdx.x < 12) {
+    double v = 0.0;
+    for (int k = 0; k < 32; ++k) v += sh[k][threadIdx.x];
+    sh[0][threadIdx.x] = v;  // row 0 is only read by thread 0 after the barrier
   }
+  __syncthreads();
   if (threadIdx.x != 0) return;
   double gR[9], gt[3], R[9], t[3];
   for (int c = 0; c < 9; ++c) gR[c] = sh[0][c];
@@ -206,6 +208,6 @@ extern "C" int gs_pose_grad(gs_view *view, const float *pose_partials, int32_t n
   }
   PoseArgs a{view, pose_partials, n_partials, step != nullptr, step ? *step : gs_pose_step{0, 0, 0, 0, 1},
              adam_state, dL_dview, dL_dtwist, dL_dqt};
-  k_pose_grad<<<1, 256, 0, as_stream(stream)>>>(a);
+  k_pose_grad<<<1, kPoseThreads, 0, as_stream(stream)>>>(a);
   return check_launch("gs_pose_grad");
 }

@@ -19,6 +19,7 @@ r.forward(P, gt)
 tc, td = r.frame.color.clone(), r.frame.depth.clone()
 loop = TrackingLoop(P, s.cam, tc, td, torch.as_tensor(s.extra["start_view"], device=d), iters=3)
 loop.size()
+loop.prepare()
 for _ in range(int(sys.argv[1]) if len(sys.argv) > 1 else 3):
     loop.iteration()
 torch.cuda.synchronize()
