@@ -108,8 +108,21 @@ struct BwdPix {
   int last[kBPX];
 };
 
-// per-lane roles in the shared-memory reduction of bwd_entry: lane 3v + p
-// (v < 10, p < 3) sums value v over the slab rows = p mod 3; lane 3v writes
+// Geometry of the per-warp reduction slab of bwd_entry: NV values per entry
+// (10 for mapping; 6 = u, v, A, B, C, p_z for the pose-only backward), L
+// lanes per value, each summing R rows (row stride NV + 1, odd: conflict-free
+// stores); rows 32 .. L R - 1 are zero padding.
+template <bool kParams>
+struct Slab {
+  static constexpr int NV = kParams ? 10 : 6;
+  static constexpr int L = 32 / NV;
+  static constexpr int R = (32 + L - 1) / L;
+  static constexpr int S = NV + 1;
+  static constexpr int SIZE = L * R * S;
+};
+
+// per-lane roles in the shared-memory reduction of bwd_entry: lane L v + p
+// (v < NV, p < L) sums value v over the slab rows = p mod L; lane L v writes
 // the total, scaled by wsc, to grad2d[woff]
 struct RedRole {
   const float *col;  // first slab row of this lane's column
@@ -192,24 +205,35 @@ __device__ __forceinline__ void bwd_entry(BwdPix &s, const float2 e[2], const bo
     return;
   }
   if (kSmemReduce) {
-    // through this warp's shared-memory slab: lane l stores its 10 values in
-    // row l (stride 11: conflict-free both ways); lane 3v + p (v < 10, p < 3)
-    // sums value v over the rows = p mod 3, the 3 partial sums meet by two
-    // shuffles, lane 3v adds the total to grad2d.  Row 32 of the slab is
-    // zero, so every lane sums 11 rows without bounds checks (lanes 30, 31
-    // sum column 10, the padding, and never write)
+    // through this warp's shared-memory slab (Slab): lane l stores its NV
+    // values in row l; lane L v + p sums value v over the rows = p mod L
+    // (zero rows past 32: no bounds checks), the L partial sums meet by
+    // shuffles, lane L v adds the total to grad2d
+    using SL = Slab<kParams>;
     const int lane = threadIdx.x & 31;
-    float *row = red + lane * 11;
+    float *row = red + lane * SL::S;
     __syncwarp();  // the previous entry's reads of the slab are done
 #pragma unroll
-    for (int v = 0; v < 10; ++v) row[v] = acc[v];
+    for (int v = 0; v < SL::NV; ++v) row[v] = acc[v];
     __syncwarp();
-    float c[11];
+    float c[SL::R];
 #pragma unroll
-    for (int t = 0; t < 11; ++t) c[t] = rr.col[t * 33];
-    // pairwise (depth 4, not a chain of 10 dependent adds)
-    float part = (((c[0] + c[1]) + (c[2] + c[3])) + ((c[4] + c[5]) + (c[6] + c[7]))) + ((c[8] + c[9]) + c[10]);
-    part += __shfl_down_sync(0xffffffffu, part, 1) + __shfl_down_sync(0xffffffffu, part, 2);
+    for (int t = 0; t < SL::R; ++t) c[t] = rr.col[t * SL::L * SL::S];
+    float part;
+    if (SL::R == 11) {  // pairwise (depth 4, not a chain of dependent adds)
+      part = (((c[0] + c[1]) + (c[2] + c[3])) + ((c[4] + c[5]) + (c[6] + c[7]))) + ((c[8] + c[9]) + c[10]);
+    } else {
+      part = c[0];
+#pragma unroll
+      for (int t = 1; t < SL::R; t += 2) part += t + 1 < SL::R ? c[t] + c[t + 1] : c[t];
+    }
+    if (SL::L == 3) {
+      part += __shfl_down_sync(0xffffffffu, part, 1) + __shfl_down_sync(0xffffffffu, part, 2);
+    } else {  // L = 5: (x0 + x1) + (x2 + x3) + x4 on the group's first lane
+      float q = part + __shfl_down_sync(0xffffffffu, part, 1);
+      q += __shfl_down_sync(0xffffffffu, q, 2);
+      part = q + __shfl_down_sync(0xffffffffu, part, 4);
+    }
     if (rr.writer) atomicAdd(dst + rr.woff, rr.wsc * part);
     return;
   }
@@ -240,7 +264,7 @@ __global__ void __launch_bounds__(BG::kThreads, kBwdMinBlocks) k_bwd_pixels(BwdA
   __shared__ unsigned char s_mask[kBatch];
   __shared__ unsigned char s_list[BG::kWarps][kBatch + 2];
   __shared__ int s_lmax;
-  __shared__ float s_red[BG::kWarps][33 * 11];  // per-warp reduction slabs (row 32 = 0)
+  __shared__ float s_red[BG::kWarps][Slab<kParams>::SIZE];  // per-warp reduction slabs (rows >= 32 are 0)
   const int tile = a.tile_order ? __ldg(a.tile_order + blockIdx.x) : int(blockIdx.x);
   const int tx = tile % a.TX, ty = tile / a.TX;
   const int w = threadIdx.x >> 5;
@@ -284,7 +308,11 @@ __global__ void __launch_bounds__(BG::kThreads, kBwdMinBlocks) k_bwd_pixels(BwdA
     s_rec[kBatch].p = make_float4(0.f, 0.f, 0.f, 0.f);
     s_rec[kBatch].q = make_float2(0.f, -INFINITY);
   }
-  for (int i = threadIdx.x; i < BG::kWarps * 11; i += blockDim.x) s_red[i / 11][32 * 11 + i % 11] = 0.f;
+  {
+    using SL = Slab<kParams>;
+    constexpr int kPad = SL::SIZE - 32 * SL::S;
+    for (int i = threadIdx.x; i < BG::kWarps * kPad; i += blockDim.x) s_red[i / kPad][32 * SL::S + i % kPad] = 0.f;
+  }
   __syncthreads();
   // warp-level bound: entries at or beyond every lane's n_contrib are skipped
   int wmax = tmax;
@@ -296,11 +324,12 @@ __global__ void __launch_bounds__(BG::kThreads, kBwdMinBlocks) k_bwd_pixels(BwdA
   unsigned char *list = s_list[w];
   RedRole rr;
   {
-    const int lane = threadIdx.x & 31, rv = lane / 3, rp = lane % 3;
-    rr.col = s_red[w] + rp * 11 + rv;
+    using SL = Slab<kParams>;
+    const int lane = threadIdx.x & 31, rv = lane / SL::L, rp = lane % SL::L;
+    rr.col = s_red[w] + rp * SL::S + rv;  // lanes past NV L read the padding column and never write
     rr.woff = rv < 7 ? rv : rv + 1;
     rr.wsc = (rv == 2 || rv == 4) ? -0.5f : (rv < 4 ? -1.f : 1.f);
-    rr.writer = lane < 30 && rp == 0 && (kParams || rv < 6);
+    rr.writer = lane < SL::NV * SL::L && rp == 0;
   }
   for (int end = lmax; end > 0; end -= kBatch) {
     const int beg = max(end - kBatch, 0);

@@ -10,7 +10,7 @@ import torch  # noqa: E402
 
 from paper_2312_10070_b200 import Params, Rasterizer, inputs  # noqa: E402
 
-s = inputs.config3()
+s = inputs.CONFIGS[int(sys.argv[1]) if len(sys.argv) > 1 else 3]()
 d = torch.device("cuda")
 P = Params.from_numpy(*s.params(), device=d)
 v = torch.as_tensor(s.views[0], device=d)
