@@ -1,5 +1,5 @@
-"""Parity at BASELINE.json's full sizes, in the launch configuration bench.py
-times: bit-exact projection rects/keys and binning of all
+"""Parity at BASELINE.json's full sizes (configs [1], [3] and the largest, [4]),
+in the launch configuration bench.py times: bit-exact projection rects/keys and binning of all
 Gaussians; compositing and gradients on a random sample of tiles the oracle
 computes pixel by pixel (upstream maps are zero outside the sample, so the
 GPU's gradient over the whole frame equals the oracle's sampled gradient)."""
@@ -31,10 +31,13 @@ def _pixel_mask(cam, tmask):
     return px
 
 
-@pytest.fixture(scope="module", params=["config3_view0", "config3_view5", "config1"])
+@pytest.fixture(scope="module", params=["config3_view0", "config3_view5", "config1", "config4_view0"])
 def full(request):
     if request.param.startswith("config3"):
         s = inputs.config3()
+        view = s.views[int(request.param[-1])]
+    elif request.param.startswith("config4"):  # the largest config: 2M Gaussians, 1920x1080, ~20M pairs
+        s = inputs.config4()
         view = s.views[int(request.param[-1])]
     else:
         s = inputs.config1()
