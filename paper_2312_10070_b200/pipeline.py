@@ -145,7 +145,24 @@ class MapStep:
             best = max(best, int(r.n_pairs.item()))
         for r in self.lanes:
             r.set_capacity(int(best * slack) + 1024)
+            r.counters[2].zero_()  # the sizing passes' own overflows
         return best
+
+    def overflowed(self):
+        """Host sync: pair-capacity overflows the lanes' gs_bin_sort calls
+        recorded (gs_counters.n_overflow; an overflowing view is rendered
+        empty) since the lanes' counters were last zeroed."""
+        return sum(int(r.counters[2].item()) for r in self.lanes)
+
+    def step_checked(self, hooks=None, host=None, slack=1.25):
+        """step(); then, if a view overflowed its pair capacity, re-size the
+        lanes and run the step again (host sync).  For loops whose Gaussians
+        change between steps (mapping with the optimiser)."""
+        g = self.step(hooks, host)
+        if self.overflowed():
+            self.size(slack)
+            g = self.step(hooks, host)
+        return g
 
     # -- the four stages of one view ---------------------------------------------
     def stage_front(self, r, k, v):

@@ -132,3 +132,28 @@ def test_mapstep_with_host_inputs(frames):
     assert torch.allclose(host.loss, ref_loss.cpu(), rtol=1e-6, atol=0)
     assert host.h2d_bytes() == 4 * s.n * 16 + V * 48 + (
         V * s.cam.width * s.cam.height * (5 if frames == "rgbd16" else 16))
+
+
+def test_step_checked_resizes_on_overflow():
+    """Gaussians that grow after sizing overflow the pair capacity (the view
+    renders empty and n_overflow counts it); step_checked re-sizes and
+    repeats the step, matching a step sized for the grown Gaussians."""
+    d = torch.device("cuda")
+    s = _small_submap(seed=7)
+    P = Params.from_numpy(*s.params(), device=d)
+    views = torch.as_tensor(s.views, device=d)
+    tc, td = _targets(s, d)
+    ms = MapStep(P, views, s.cam, tc, td, lanes=2, device=d)
+    ms.size(slack=1.0)
+    P.logscale[:, :3] += 0.7  # ~2x larger splats: many more (tile, Gaussian) pairs
+    ms.step()
+    torch.cuda.synchronize()
+    assert ms.overflowed() > 0  # the unchecked step lost views
+    g = ms.step_checked().buf.clone()
+    torch.cuda.synchronize()
+    ref_ms = MapStep(P, views, s.cam, tc, td, lanes=2, device=d)
+    ref_ms.size()
+    ref = ref_ms.step().buf.clone()
+    torch.cuda.synchronize()
+    assert ms.overflowed() == 0 and ref_ms.overflowed() == 0
+    assert np.allclose(g.cpu().numpy(), ref.cpu().numpy(), rtol=1e-4, atol=1e-5 * ref.abs().max().item())
