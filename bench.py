@@ -236,17 +236,31 @@ def bench_ours(a):
     ev_fwd, ev_bwd = [], []
 
     def timed_fwd(r, k, v, tgt_ready=None):
+        # MapStep.stage_fwd with CUDA events around the compositing launch
         st = torch.cuda.current_stream()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        e0.record(st)
-        raster.gs_render_fwd(r.proj, r.sorted_idx, r.tile_range, r.cam, r.frame, False, tile_order=r.tile_order,
-                             tile_work=r.tile_work)
-        e1.record(st)
+        if ms.fused_loss and ms.ssim == 0.0:
+            if tgt_ready is not None:
+                st.wait_event(tgt_ready)
+            if r.loss_part is None:
+                r.loss_part = torch.empty(2 * r.T, dtype=torch.float64, device=r.device)
+            e0.record(st)
+            raster.gs_render_fwd_l1(r.proj, r.sorted_idx, r.tile_range, r.cam, r.frame, ms.tgt_color[v],
+                                    ms.tgt_depth[v], ms.tgt_scales[v], r.dL_dcolor, r.dL_ddepth,
+                                    tile_order=r.tile_order, tile_work=r.tile_work, loss_part=r.loss_part)
+            e1.record(st)
+            raster.gs_tile_order(r.tile_work, r.T, r.bwd_order)
+            raster.gs_loss_from_tiles(r.cam, r.loss_part, ms.tgt_scales[v], ms.lc, ms.ld, r.loss)
+        else:
+            e0.record(st)
+            raster.gs_render_fwd(r.proj, r.sorted_idx, r.tile_range, r.cam, r.frame, False, tile_order=r.tile_order,
+                                 tile_work=r.tile_work)
+            e1.record(st)
+            raster.gs_tile_order(r.tile_work, r.T, r.bwd_order)
+            if tgt_ready is not None:
+                st.wait_event(tgt_ready)
+            r.compute_loss(ms.tgt_color[v], ms.tgt_depth[v], None, ms.lc, ms.ld, ms.ssim)
         ev_fwd.append((e0, e1))
-        raster.gs_tile_order(r.tile_work, r.T, r.bwd_order)
-        if tgt_ready is not None:
-            st.wait_event(tgt_ready)
-        r.compute_loss(ms.tgt_color[v], ms.tgt_depth[v], None, ms.lc, ms.ld, ms.ssim)
         ms.losses[k].copy_(r.loss)
 
     def timed_bwd(r, k, v):

@@ -237,13 +237,16 @@ int gs_render_fwd(gs_proj pr, const int32_t *sorted_idx, const int32_t *tile_ran
  * tracking update needs only the gradient).  Arguments as gs_render_fwd
  * (no stats) plus:
  *   tgt_color [3][H][W], tgt_depth [H][W] (device) the frame's targets
- *   scales    (device) [2] from gs_loss_scales for this target frame
- *   dL_dcolor [3][H][W], dL_ddepth [H][W] (device) written */
+ *   scales    (device) [4] from gs_loss_scales for this target frame
+ *   dL_dcolor [3][H][W], dL_ddepth [H][W] (device) written
+ *   loss_part (device, nullable) [T][2] fp64: per tile, sum |C^ - C*| over
+ *             its pixels and channels, sum |D^ - D*| over its valid pixels
+ *             (fixed order); gs_loss_from_tiles turns them into the loss. */
 int gs_render_fwd_l1(gs_proj pr, const int32_t *sorted_idx, const int32_t *tile_range,
                      const int32_t *tile_order, gs_camera cam, float *color, float *depth,
                      float *alpha, float *T_final, int32_t *n_contrib, int32_t *tile_work,
                      const float *tgt_color, const float *tgt_depth, const float *scales,
-                     float *dL_dcolor, float *dL_ddepth, void *stream);
+                     float *dL_dcolor, float *dL_ddepth, double *loss_part, void *stream);
 
 /* Scheduling utility: tile ids by descending work (64 buckets of max/64, order
  * inside a bucket unspecified), e.g. from gs_render_fwd's tile_work for
@@ -269,10 +272,19 @@ int gs_loss(gs_camera cam, const float *color, const float *depth,
 
 /* The two gradient scales of gs_loss for a target frame (weight 1):
  * scales[0] = lambda_color / (3HW), scales[1] = lambda_depth / |V| (0 if
- * |V| = 0), |V| = #{D* > 0}; computed once per frame for gs_render_fwd_l1.
- *   ws (device) >= gs_loss_workspace_bytes(cam); scales (device) [2]. */
+ * |V| = 0), scales[2] = |V| = #{D* > 0} (exact in fp32: HW < 2^24),
+ * scales[3] = 0; computed once per frame for gs_render_fwd_l1.
+ *   ws (device) >= gs_loss_workspace_bytes(cam); scales (device) [4]. */
 int gs_loss_scales(gs_camera cam, const float *tgt_depth, float lambda_color, float lambda_depth,
                    void *ws, size_t ws_bytes, float *scales, void *stream);
+
+/* gs_loss's value from gs_render_fwd_l1's per-tile sums: loss[3] =
+ * (lambda_color Lc + lambda_depth Ld, Lc, Ld), Lc = sum / (3HW), Ld = sum / |V|
+ * (0 if |V| = 0), fp64, fixed-order (bit-deterministic; equal to gs_loss's up
+ * to the fp64 summation order).  loss_part (device) [T][2]; scales (device)
+ * [4] from gs_loss_scales; loss (device) [3]. */
+int gs_loss_from_tiles(gs_camera cam, const double *loss_part, const float *scales, float lambda_color,
+                       float lambda_depth, float *loss, void *stream);
 
 /* NEXT(1) — masked tracking loss (Eq. 15; S:286-294, S:425-438;
  * DESIGN.md R29-R31).  Tracking only: gradients flow to the rendered colour

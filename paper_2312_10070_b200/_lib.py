@@ -78,7 +78,8 @@ _PROTOS = {
     "gs_loss": (C.c_int, [GsCamera, _VP, _VP, _VP, _VP, _VP, _F, _F, _VP, _SZ, _VP, _VP, _VP, _VP]),
     "gs_loss_scales": (C.c_int, [GsCamera, _VP, _F, _F, _VP, _SZ, _VP, _VP]),
     "gs_render_fwd_l1": (C.c_int, [GsProj, _VP, _VP, _VP, GsCamera, _VP, _VP, _VP, _VP, _VP, _VP, _VP, _VP, _VP, _VP,
-                                   _VP, _VP]),
+                                   _VP, _VP, _VP]),
+    "gs_loss_from_tiles": (C.c_int, [GsCamera, _VP, _VP, _F, _F, _VP, _VP]),
     "gs_tracking_loss_workspace_bytes": (_SZ, [GsCamera]),
     "gs_ssim_workspace_bytes": (_SZ, [GsCamera]),
     "gs_opt_workspace_bytes": (_SZ, [_I32]),

@@ -126,6 +126,31 @@ __global__ void __launch_bounds__(32) k_loss_scales(const uint32_t *__restrict__
   if (threadIdx.x == 0) {
     scales[0] = float(double(lc) / (3.0 * double(HW)));
     scales[1] = nv ? float(double(ld) / double(nv)) : 0.f;
+    scales[2] = float(nv);  // exact: |V| <= HW < 2^24
+    scales[3] = 0.f;
+  }
+}
+
+// gs_loss_from_tiles: loss[3] from the per-tile |residual| sums of
+// gs_render_fwd_l1, fixed-order (deterministic) fp64 reduction
+__global__ void __launch_bounds__(kLossThreads) k_loss_tiles(const double *__restrict__ part, int T, int64_t HW,
+                                                             const float *__restrict__ scales, float lc, float ld,
+                                                             float *loss) {
+  __shared__ double sh[kLossThreads];
+  double ac = 0.0, ad = 0.0;
+  for (int t = threadIdx.x; t < T; t += blockDim.x) {  // fixed order per thread
+    ac += part[2 * t];
+    ad += part[2 * t + 1];
+  }
+  ac = block_sum_d(ac, sh);
+  ad = block_sum_d(ad, sh);
+  if (threadIdx.x == 0) {
+    const double nv = double(scales[2]);
+    const double Lc = ac / (3.0 * double(HW));
+    const double Ld = nv > 0.0 ? ad / nv : 0.0;
+    loss[0] = float(double(lc) * Lc + double(ld) * Ld);
+    loss[1] = float(Lc);
+    loss[2] = float(Ld);
   }
 }
 
@@ -148,6 +173,19 @@ extern "C" int gs_loss_scales(gs_camera cam, const float *tgt_depth, float lambd
   k_loss_count<<<kLossBlocks, kLossThreads, 0, s>>>(tgt_depth, HW, cnt_part);
   k_loss_scales<<<1, 32, 0, s>>>(cnt_part, kLossBlocks, HW, lambda_color, lambda_depth, scales);
   return check_launch("gs_loss_scales");
+}
+
+extern "C" int gs_loss_from_tiles(gs_camera cam, const double *loss_part, const float *scales, float lambda_color,
+                                  float lambda_depth, float *loss, void *stream) {
+  using namespace gs;
+  if (!camera_ok(cam) || !loss_part || !scales || !loss || !(lambda_color >= 0.f) || !(lambda_depth >= 0.f)) {
+    set_error("gs_loss_from_tiles: invalid argument");
+    return GS_ERR_INVALID_ARG;
+  }
+  const int T = tiles_x(cam) * tiles_y(cam);
+  k_loss_tiles<<<1, kLossThreads, 0, as_stream(stream)>>>(loss_part, T, int64_t(cam.width) * cam.height, scales,
+                                                          lambda_color, lambda_depth, loss);
+  return check_launch("gs_loss_from_tiles");
 }
 
 extern "C" size_t gs_loss_workspace_bytes(gs_camera cam) {

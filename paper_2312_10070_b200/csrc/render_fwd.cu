@@ -29,9 +29,11 @@ struct FwdArgs {
   float *color, *depth, *alpha, *T_final;
   int32_t *n_contrib, *stats, *tile_work;
   // fused L1 gradient epilogue (gs_render_fwd_l1): targets, device scales
-  // (lambda_c / 3HW, lambda_d / |V|) from gs_loss_scales, gradient maps
+  // (lambda_c / 3HW, lambda_d / |V|, |V|) from gs_loss_scales, gradient maps,
+  // per-tile fp64 sums of |C - C*| and of |D - D*| over valid pixels (nullable)
   const float *tc, *td, *scales;
   float *gC, *gD;
+  double *loss_part;
 };
 
 #ifndef FWD_NP
@@ -199,10 +201,11 @@ __global__ void __launch_bounds__(FG::kThreads, 1) k_render_fwd(FwdArgs a) {
     __syncthreads();
     if (threadIdx.x == 0) a.tile_work[tile] = s_work;
   }
-  if (!pg.row_in) return;
   const size_t HW = size_t(a.W) * a.H;
+  double l1c = 0.0, l1d = 0.0;  // this thread's |residual| sums (kL1)
 #pragma unroll
   for (int h = 0; h < kFNP; ++h) {
+    if (!pg.row_in) break;
     const float cc0[2] = {s[h].c0.x, s[h].c0.y}, cc1[2] = {s[h].c1.x, s[h].c1.y}, cc2[2] = {s[h].c2.x, s[h].c2.y},
                 DD[2] = {s[h].D.x, s[h].D.y}, AA[2] = {s[h].A.x, s[h].A.y}, TT[2] = {s[h].T.x, s[h].T.y};
     const int ll[2] = {s[h].last0, s[h].last1}, nc[2] = {s[h].ncon0, s[h].ncon1}, tm[2] = {s[h].term0, s[h].term1};
@@ -228,11 +231,35 @@ __global__ void __launch_bounds__(FG::kThreads, 1) k_render_fwd(FwdArgs a) {
         for (int ch = 0; ch < 3; ++ch) {
           const float r = cc[ch] - __ldg(a.tc + ch * HW + q);
           a.gC[ch * HW + q] = sc * 1.f * float((r > 0.f) - (r < 0.f));
+          l1c += fabs(double(r));
         }
         const float t = __ldg(a.td + q);
         const float r = DD[k] - t;
         a.gD[q] = t > 0.f ? sd * 1.f * float((r > 0.f) - (r < 0.f)) : 0.f;
+        if (t > 0.f) l1d += fabs(double(r));
       }
+    }
+  }
+  if (kL1 && a.loss_part) {  // the tile's sums, fixed order: warp shuffles, then warps in order
+    __shared__ double s_l1[FG::kWarps][2];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      l1c += __shfl_xor_sync(0xffffffffu, l1c, o);
+      l1d += __shfl_xor_sync(0xffffffffu, l1d, o);
+    }
+    if ((threadIdx.x & 31) == 0) {
+      s_l1[w][0] = l1c;
+      s_l1[w][1] = l1d;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      double c = 0.0, d = 0.0;
+      for (int k = 0; k < FG::kWarps; ++k) {
+        c += s_l1[k][0];
+        d += s_l1[k][1];
+      }
+      a.loss_part[2 * size_t(tile)] = c;
+      a.loss_part[2 * size_t(tile) + 1] = d;
     }
   }
 }
@@ -255,7 +282,7 @@ extern "C" int gs_render_fwd(gs_proj pr, const int32_t *sorted_idx, const int32_
   FwdArgs a{reinterpret_cast<const double2 *>(pr.uv), reinterpret_cast<const float4 *>(pr.coef),
             reinterpret_cast<const float4 *>(pr.rgbz), sorted_idx, reinterpret_cast<const int2 *>(tile_range),
             tile_order, cam.width, cam.height, tiles_x(cam), color, depth, alpha, T_final, n_contrib, stats,
-            tile_work, nullptr, nullptr, nullptr, nullptr, nullptr};
+            tile_work, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};
   const int T = tiles_x(cam) * tiles_y(cam);
   if (stats)
     k_render_fwd<true><<<T, FG::kThreads, 0, as_stream(stream)>>>(a);
@@ -268,7 +295,7 @@ extern "C" int gs_render_fwd_l1(gs_proj pr, const int32_t *sorted_idx, const int
                                 const int32_t *tile_order, gs_camera cam, float *color, float *depth, float *alpha,
                                 float *T_final, int32_t *n_contrib, int32_t *tile_work, const float *tgt_color,
                                 const float *tgt_depth, const float *scales, float *dL_dcolor, float *dL_ddepth,
-                                void *stream) {
+                                double *loss_part, void *stream) {
   using namespace gs;
   if (!camera_ok(cam) || !tile_range || !color || !depth || !alpha || !T_final || !n_contrib || !tgt_color ||
       !tgt_depth || !scales || !dL_dcolor || !dL_ddepth) {
@@ -283,7 +310,7 @@ extern "C" int gs_render_fwd_l1(gs_proj pr, const int32_t *sorted_idx, const int
   FwdArgs a{reinterpret_cast<const double2 *>(pr.uv), reinterpret_cast<const float4 *>(pr.coef),
             reinterpret_cast<const float4 *>(pr.rgbz), sorted_idx, reinterpret_cast<const int2 *>(tile_range),
             tile_order, cam.width, cam.height, tiles_x(cam), color, depth, alpha, T_final, n_contrib, nullptr,
-            tile_work, tgt_color, tgt_depth, scales, dL_dcolor, dL_ddepth};
+            tile_work, tgt_color, tgt_depth, scales, dL_dcolor, dL_ddepth, loss_part};
   const int T = tiles_x(cam) * tiles_y(cam);
   k_render_fwd<false, true><<<T, FG::kThreads, 0, as_stream(stream)>>>(a);
   return check_launch("gs_render_fwd_l1");

@@ -19,7 +19,7 @@ import numpy as np
 import torch
 
 from .raster import (GS_BWD_ATOMIC_ACC, GS_BWD_GAUSS_ONLY, GS_BWD_PIXELS_ONLY, GS_GRAD_PARAMS, GS_GRAD_POSE, Grads, Params, Rasterizer,
-                     gs_render_bwd_gauss_views, gs_unpack_rgbd, lib)
+                     gs_loss_scales, gs_render_bwd_gauss_views, gs_unpack_rgbd, lib)
 
 
 class HostInputs:
@@ -93,7 +93,7 @@ class MapStep:
 
     def __init__(self, params: Params, views, cam, tgt_color, tgt_depth, rank=0, world=1, group=None,
                  lambda_color=1.0, lambda_depth=1.0, device="cuda", lanes=8, allreduce=None, schedule="lanes",
-                 ssim=0.0, fused_gauss=False, atomic_gauss=True):
+                 ssim=0.0, fused_gauss=False, atomic_gauss=True, fused_loss=True):
         """ssim: the lambda of Eq. 10's colour loss (0: L1 colour only, as
         BJ.configs[3]; the paper uses 0.2).  fused_gauss: when every view has
         its own lane, run ONE per-Gaussian phase over all views
@@ -103,7 +103,9 @@ class MapStep:
         per-view phases (profiles/r01/README.md).  atomic_gauss: the
         per-view S6 adds into the gradient buffer atomically
         (GS_BWD_ATOMIC_ACC), so the views' Gaussian phases need no ordering;
-        else they are serialised in view order (events)."""
+        else they are serialised in view order (events).  fused_loss (L1
+        loss, ssim = 0): the loss is computed by the compositing kernel
+        (gs_render_fwd_l1, per-view scales from prepare_targets)."""
         self.ssim = ssim
         self.params = params
         self.views = views                  # [V, 12] device tensor (all views)
@@ -130,6 +132,8 @@ class MapStep:
         self._slots = None
         self.schedule = schedule
         self.fused_gauss = fused_gauss
+        self.fused_loss = fused_loss  # used while self.ssim == 0 (the L1 loss is pixel-local)
+        self.tgt_scales = {}
         self.atomic_gauss = atomic_gauss
         self.stage_streams = [torch.cuda.Stream(device=device) for _ in range(3)] if schedule == "stages" else []
 
@@ -146,6 +150,8 @@ class MapStep:
         for r in self.lanes:
             r.set_capacity(int(best * slack) + 1024)
             r.counters[2].zero_()  # the sizing passes' own overflows
+        if self.fused_loss:
+            self.prepare_targets()
         return best
 
     def overflowed(self):
@@ -171,13 +177,29 @@ class MapStep:
         r.bin_sort()
 
     def stage_fwd(self, r, k, v, tgt_ready=None):
-        """S3 + S4: compositing, then the loss once the view's targets are on
-        the device (tgt_ready)."""
-        r.render()
-        if tgt_ready is not None:
-            torch.cuda.current_stream().wait_event(tgt_ready)
-        r.compute_loss(self.tgt_color[v], self.tgt_depth[v], None, self.lc, self.ld, self.ssim)
+        """S3 + S4 once the view's targets are on the device (tgt_ready):
+        with fused_loss (L1, ssim = 0) one compositing kernel also writes the
+        loss gradient maps and per-tile loss sums (gs_render_fwd_l1 +
+        gs_loss_from_tiles); else compositing, then gs_loss (+ gs_ssim)."""
+        if self.fused_loss and self.ssim == 0.0:
+            if tgt_ready is not None:
+                torch.cuda.current_stream().wait_event(tgt_ready)
+            r.render_l1(self.tgt_color[v], self.tgt_depth[v], self.lc, self.ld, self.tgt_scales[v])
+        else:
+            r.render()
+            if tgt_ready is not None:
+                torch.cuda.current_stream().wait_event(tgt_ready)
+            r.compute_loss(self.tgt_color[v], self.tgt_depth[v], None, self.lc, self.ld, self.ssim)
         self.losses[k].copy_(r.loss)
+
+    def prepare_targets(self):
+        """The per-view gradient scales of the fused L1 loss (gs_loss_scales,
+        once per target frame): call again after changing the targets."""
+        self.tgt_scales = {v: self.tgt_scales.get(v) if self.tgt_scales else None for v in self.mine}
+        for v in self.mine:
+            if self.tgt_scales[v] is None:
+                self.tgt_scales[v] = torch.zeros(4, dtype=torch.float32, device=self.tgt_depth[v].device)
+            self.lanes[0].loss_scales(self.tgt_depth[v], self.lc, self.ld, out=self.tgt_scales[v])
 
     def stage_bwd(self, r, k, v):
         """S5: the per-pixel backward phase."""
@@ -228,14 +250,18 @@ class MapStep:
                 # k + 1 overlap the compute of step k (they wait only for the
                 # step that last read their set, k - 1)
                 clone = Params(*(getattr(self.params, n).clone() for n in ("mean_opa", "quat", "logscale", "rgb")))
-                self._slots = [(self.params, self.views, self.tgt_color, self.tgt_depth),
+                if self.fused_loss and not self.tgt_scales:
+                    self.prepare_targets()
+                self._slots = [(self.params, self.views, self.tgt_color, self.tgt_depth, self.tgt_scales),
                                (clone, self.views.clone(), {v: t.clone() for v, t in self.tgt_color.items()},
-                                {v: t.clone() for v, t in self.tgt_depth.items()})]
+                                {v: t.clone() for v, t in self.tgt_depth.items()},
+                                {v: t.clone() for v, t in self.tgt_scales.items()})]
+                self.scale_ws = torch.empty_like(self.lanes[0].loss_ws)
                 self._released = [main.record_event(), main.record_event()]
                 self._slot = 0
             slot = self._slot
             self._slot ^= 1
-            self.params, self.views, self.tgt_color, self.tgt_depth = self._slots[slot]
+            self.params, self.views, self.tgt_color, self.tgt_depth, self.tgt_scales = self._slots[slot]
             cs = self.copy_stream
             cs.wait_event(self._released[slot])  # the step that last read this set is done
             with torch.cuda.stream(cs):
@@ -249,6 +275,9 @@ class MapStep:
                 rgb_ready = cs.record_event()
                 for v in self.mine:
                     host.upload_targets(v, self.r.cam, self.tgt_color[v], self.tgt_depth[v])
+                    if self.fused_loss:  # the new frame's gradient scales (gs_loss_scales)
+                        gs_loss_scales(self.r.cam, self.tgt_depth[v], self.lc, self.ld, self.scale_ws,
+                                       self.tgt_scales[v])
                     tgt_ready[v] = cs.record_event()  # also orders the colours before every loss
             main.wait_event(params_ready)
         self.grads.zero_()
@@ -311,10 +340,12 @@ class MapStep:
         return self.grads
 
     def launches_per_step(self):
-        """Kernels of ours launched per step."""
+        """Kernels of ours launched per step; the fused L1
+        loss takes 1 launch (gs_loss_from_tiles) instead of gs_loss's 3."""
+        per_view = kernels_per_view(self.r.cam) - (2 if self.fused_loss and self.ssim == 0.0 else 0)
         if self.schedule == "lanes" and self.fused_gauss and len(self.mine) <= len(self.lanes):
-            return len(self.mine) * (kernels_per_view(self.r.cam) - 1) + 1
-        return len(self.mine) * kernels_per_view(self.r.cam)
+            return len(self.mine) * (per_view - 1) + 1
+        return len(self.mine) * per_view
 
 
 def kernels_per_view(cam, loss=True, bwd=True):

@@ -20,7 +20,7 @@ from ._lib import (GS_BWD_ATOMIC_ACC, GS_BWD_GAUSS_ONLY, GS_BWD_PIXELS_ONLY, GS_
                    GsParams, GsPoseStep, GsProj, GsView, check, lib)
 
 __all__ = ["Params", "Grads", "Proj", "Frame", "Rasterizer", "camera", "gs_project", "gs_bin_sort",
-           "gs_render_fwd", "gs_render_fwd_l1", "gs_loss_scales", "gs_tile_order", "gs_loss", "gs_tracking_loss", "gs_ssim", "gs_iso_reg", "gs_adam_step", "gs_prune", "gs_seed", "gs_unpack_rgbd", "Optimizer", "gs_render_bwd", "gs_render_bwd_gauss_views", "gs_pose_grad", "GS_GRAD_PARAMS", "GS_GRAD_POSE", "GS_BWD_PIXELS_ONLY", "GS_BWD_GAUSS_ONLY", "GS_BWD_ATOMIC_ACC",
+           "gs_render_fwd", "gs_render_fwd_l1", "gs_loss_scales", "gs_loss_from_tiles", "gs_tile_order", "gs_loss", "gs_tracking_loss", "gs_ssim", "gs_iso_reg", "gs_adam_step", "gs_prune", "gs_seed", "gs_unpack_rgbd", "Optimizer", "gs_render_bwd", "gs_render_bwd_gauss_views", "gs_pose_grad", "GS_GRAD_PARAMS", "GS_GRAD_POSE", "GS_BWD_PIXELS_ONLY", "GS_BWD_GAUSS_ONLY", "GS_BWD_ATOMIC_ACC",
            "GsError", "device_check"]
 
 
@@ -157,11 +157,16 @@ def gs_render_fwd(proj: Proj, sorted_idx, tile_range, cam: GsCamera, frame: Fram
 
 
 def gs_render_fwd_l1(proj: Proj, sorted_idx, tile_range, cam: GsCamera, frame: Frame, tgt_color, tgt_depth, scales,
-                     dL_dcolor, dL_ddepth, stream=None, tile_order=None, tile_work=None):
+                     dL_dcolor, dL_ddepth, stream=None, tile_order=None, tile_work=None, loss_part=None):
     check(lib().gs_render_fwd_l1(proj.c(), _p(sorted_idx), _p(tile_range), _p(tile_order), cam, _p(frame.color),
                                  _p(frame.depth), _p(frame.alpha), _p(frame.T_final), _p(frame.n_contrib),
                                  _p(tile_work), _p(tgt_color), _p(tgt_depth), _p(scales), _p(dL_dcolor),
-                                 _p(dL_ddepth), _stream(stream)), "gs_render_fwd_l1")
+                                 _p(dL_ddepth), _p(loss_part), _stream(stream)), "gs_render_fwd_l1")
+
+
+def gs_loss_from_tiles(cam: GsCamera, loss_part, scales, lambda_color, lambda_depth, loss, stream=None):
+    check(lib().gs_loss_from_tiles(cam, _p(loss_part), _p(scales), float(lambda_color), float(lambda_depth), _p(loss),
+                                   _stream(stream)), "gs_loss_from_tiles")
 
 
 def gs_loss_scales(cam: GsCamera, tgt_depth, lambda_color, lambda_depth, ws, scales, stream=None):
@@ -341,6 +346,7 @@ class Rasterizer:
         self.ssim_ws = None
         self.tl_ws = None  # gs_tracking_loss workspace, allocated on first use
         self.scales = None  # gs_loss_scales output (forward_l1)
+        self.loss_part = None  # per-tile |residual| sums (render_l1)
         self.tl_loss = None
         self.dL_dcolor = torch.zeros(3, H, W, dtype=torch.float32, device=device)
         self.dL_ddepth = torch.zeros(H, W, dtype=torch.float32, device=device)
@@ -400,12 +406,29 @@ class Rasterizer:
         self.render(stats)
         return self.frame
 
-    def loss_scales(self, tgt_depth, lambda_color=1.0, lambda_depth=1.0):
-        """gs_loss_scales of a target frame into self.scales (for forward_l1)."""
-        if self.scales is None:
-            self.scales = torch.zeros(2, dtype=torch.float32, device=self.device)
-        gs_loss_scales(self.cam, tgt_depth, lambda_color, lambda_depth, self.loss_ws, self.scales)
-        return self.scales
+    def loss_scales(self, tgt_depth, lambda_color=1.0, lambda_depth=1.0, out=None):
+        """gs_loss_scales of a target frame into out (default self.scales, for
+        forward_l1 / render_l1)."""
+        if out is None:
+            if self.scales is None:
+                self.scales = torch.zeros(4, dtype=torch.float32, device=self.device)
+            out = self.scales
+        gs_loss_scales(self.cam, tgt_depth, lambda_color, lambda_depth, self.loss_ws, out)
+        return out
+
+    def render_l1(self, tgt_color, tgt_depth, lambda_color, lambda_depth, scales):
+        """S3 + S4 fused (after project + bin_sort): gs_render_fwd_l1 writes the
+        frame and gs_loss's gradient maps and per-tile |residual| sums, then
+        gs_loss_from_tiles -> self.loss[:3]; scales from loss_scales (same
+        lambdas)."""
+        if self.loss_part is None:
+            self.loss_part = torch.empty(2 * self.T, dtype=torch.float64, device=self.device)
+        gs_render_fwd_l1(self.proj, self.sorted_idx, self.tile_range, self.cam, self.frame, tgt_color, tgt_depth,
+                         scales, self.dL_dcolor, self.dL_ddepth, tile_order=self.tile_order,
+                         tile_work=self.tile_work, loss_part=self.loss_part)
+        gs_tile_order(self.tile_work, self.T, self.bwd_order)
+        gs_loss_from_tiles(self.cam, self.loss_part, scales, lambda_color, lambda_depth, self.loss)
+        return self.loss
 
     def forward_l1(self, params: Params, view, tgt_color, tgt_depth):
         """S1-S3 with the L1 gradient maps fused into the forward

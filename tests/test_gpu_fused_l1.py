@@ -1,7 +1,8 @@
-"""gs_render_fwd_l1 (S3 with S4's gradient fused, tracking) against the
-separate calls: the frame is bit-identical to gs_render_fwd's and the
-gradient maps to gs_loss's (weight 1); gs_loss_scales gives gs_loss's
-scales; the fused tracking loop follows the unfused one."""
+"""gs_render_fwd_l1 (S3 with S4 fused: tracking, and mapping with the L1
+loss) against the separate calls: the frame is bit-identical to
+gs_render_fwd's and the gradient maps to gs_loss's (weight 1);
+gs_loss_scales gives gs_loss's scales and gs_loss_from_tiles its value; the
+fused tracking loop follows the unfused one."""
 import numpy as np
 import pytest
 import torch
@@ -42,6 +43,35 @@ def test_fwd_l1_equals_fwd_then_loss(cfg, lc, ld, holes):
         assert torch.equal(getattr(r.frame, k), t), k
     assert torch.equal(r.dL_dcolor, gc)
     assert torch.equal(r.dL_ddepth, gd)
+    assert sc[2].item() == nv
+    # the loss value from the forward's per-tile sums (mapping's fused S3 + S4)
+    ref_loss = r.loss[:3].clone()
+    r.dL_dcolor.fill_(7.0)
+    r.loss.fill_(-1.0)
+    r.render_l1(tc, td, lc, ld, sc)
+    torch.cuda.synchronize()
+    assert torch.equal(r.dL_dcolor, gc)
+    assert np.allclose(r.loss[:3].cpu().numpy(), ref_loss.cpu().numpy(), rtol=1e-6, atol=0)
+
+
+def test_fused_loss_no_valid_depth():
+    s = inputs.config0()
+    P = Params.from_numpy(*s.params(), device=DEV)
+    v = torch.as_tensor(s.views[0], device=DEV)
+    r = Rasterizer(s.n, s.cam, device=DEV)
+    r.size_for(P, v)
+    H, W = s.cam.height, s.cam.width
+    tc = torch.rand(3, H, W, device=DEV)
+    td = torch.zeros(H, W, device=DEV)  # |V| = 0: L_d = 0 and a zero depth gradient
+    r.forward(P, v)
+    r.compute_loss(tc, td, None, 1.0, 1.0)
+    ref = r.loss[:3].clone()
+    sc = r.loss_scales(td, 1.0, 1.0)
+    r.render_l1(tc, td, 1.0, 1.0, sc)
+    torch.cuda.synchronize()
+    assert sc[1].item() == 0.0 and sc[2].item() == 0.0
+    assert r.loss[2].item() == 0.0 and (r.dL_ddepth == 0).all()
+    assert np.allclose(r.loss[:3].cpu().numpy(), ref.cpu().numpy(), rtol=1e-6, atol=0)
 
 
 def test_fused_tracking_follows_unfused():

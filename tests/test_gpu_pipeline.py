@@ -57,8 +57,9 @@ def test_mapstep_equals_sum_of_views_for_any_lanes():
                                         (4, "lanes", False, False), (2, "lanes", False, False),
                                         (4, "lanes", True, True), (8, "lanes", True, True),
                                         (2, "stages", False, True), (4, "stages", False, False)):
+        # the fused L1 loss (default) everywhere but the 2-lane serialised case
         ms = MapStep(P, views, s.cam, tc, td, lanes=lanes, device=d, schedule=sched, fused_gauss=fused,
-                     atomic_gauss=atomic)
+                     atomic_gauss=atomic, fused_loss=(lanes, atomic) != (2, False))
         ms.size()
         g = ms.step()
         torch.cuda.synchronize()
