@@ -139,8 +139,29 @@ struct RedRole {
 // of this lane's pixels passes; ball: the warp's ballot of `any` (nonzero).
 // acc layout (before the writer's sign/scale): 0 u, 1 v, 2 A-term, 3 B,
 // 4 C-term, 5 p_z, 6 logit, 7 r, 8 g, 9 b
+// alpha of an entry at the thread's pixel pairs (the forward's value, H5; a
+// skipped pixel's exponent becomes -inf: alpha = 0), 1 / (1 - alpha) (R16) and
+// the alpha that carries a gradient (0 where clamped, R17): independent of
+// the T / Q chain, so computed for both entries of a step up front
+struct AlphaPrep {
+  float2 al[2], ir[2], ag[2];
+};
+
+__device__ __forceinline__ AlphaPrep alpha_prep(const float2 e[2], const bool pass[kBPX]) {
+  AlphaPrep p;
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+    const float a0 = fminf(ex2_approx(pass[2 * h] ? e[h].x : -INFINITY), kAlphaMax);
+    const float a1 = fminf(ex2_approx(pass[2 * h + 1] ? e[h].y : -INFINITY), kAlphaMax);
+    p.al[h] = make_float2(a0, a1);
+    p.ir[h] = make_float2(rcp_approx(1.f - a0), rcp_approx(1.f - a1));
+    p.ag[h] = make_float2(e[h].x < kExpClamp ? a0 : 0.f, e[h].y < kExpClamp ? a1 : 0.f);
+  }
+  return p;
+}
+
 template <bool kParams>
-__device__ __forceinline__ void bwd_entry(BwdPix &s, const float2 e[2], const bool pass[kBPX], bool any,
+__device__ __forceinline__ void bwd_entry(BwdPix &s, const AlphaPrep &ap, bool any,
                                           unsigned ball, float4 c, float4 cn, float2 ul, float fpy,
                                           const float2 fx[2], float *dst, float *red, const RedRole &rr) {
   const float dy = ul.y - fpy;  // Delta = mu^I - pixel; one row: dy is shared
@@ -151,12 +172,9 @@ __device__ __forceinline__ void bwd_entry(BwdPix &s, const float2 e[2], const bo
   float2 ga[2], t[2], wt[2], dx[2];
 #pragma unroll
   for (int h = 0; h < 2; ++h) {
-    // a skipped pixel's exponent becomes -inf: alpha = 0 (the forward's value, H5)
-    const float a0 = fminf(ex2_approx(pass[2 * h] ? e[h].x : -INFINITY), kAlphaMax);
-    const float a1 = fminf(ex2_approx(pass[2 * h + 1] ? e[h].y : -INFINITY), kAlphaMax);
-    const float2 al = make_float2(a0, a1);
+    const float2 al = ap.al[h];
     // T_j = T_{j+1} / (1 - alpha_j) (R16)
-    s.T[h] = __fmul2_rn(s.T[h], make_float2(rcp_approx(1.f - a0), rcp_approx(1.f - a1)));
+    s.T[h] = __fmul2_rn(s.T[h], ap.ir[h]);
     wt[h] = __fmul2_rn(al, s.T[h]);
     // Eq. 8 chained with Eq. 7 through the suffix scalar Q
     const float2 gx = __ffma2_rn(
@@ -165,7 +183,7 @@ __device__ __forceinline__ void bwd_entry(BwdPix &s, const float2 e[2], const bo
     const float2 galpha = __fmul2_rn(s.T[h], d);
     s.Q[h] = __ffma2_rn(al, d, s.Q[h]);
     // clamped alpha (alpha~ >= 0.999: e >= kExpClamp): no gradient (R17)
-    ga[h] = __fmul2_rn(make_float2(e[h].x < kExpClamp ? a0 : 0.f, e[h].y < kExpClamp ? a1 : 0.f), galpha);
+    ga[h] = __fmul2_rn(ap.ag[h], galpha);
     dx[h] = __fadd2_rn(bcast(ul.x), make_float2(-fx[h].x, -fx[h].y));
     t[h] = __fmul2_rn(ga[h], dx[h]);
   }
@@ -382,22 +400,28 @@ __global__ void __launch_bounds__(BG::kThreads, kBwdMinBlocks) k_bwd_pixels(BwdA
         ea[h] = pair_exponent(ra, fx[h]);
         eb[h] = pair_exponent(rb, fx[h]);
       }
+      // decisions and alphas of both entries first (independent of the T / Q chain)
+      bool pass[2][kBPX], any[2];
+      unsigned ball[2];
+      AlphaPrep ap[2];
 #pragma unroll
       for (int u = 0; u < 2; ++u) {
-        const int j = u ? jb_ : ja_;
+        const int pos = beg + (u ? jb_ : ja_);  // entry position in the tile list
         const float2 *e = u ? eb : ea;
-        const int pos = beg + j;  // entry position in the tile list
-        bool pass[kBPX];
 #pragma unroll
         for (int h = 0; h < 2; ++h) {
-          pass[2 * h] = pos < s.last[2 * h] && e[h].x >= kExpMin;
-          pass[2 * h + 1] = pos < s.last[2 * h + 1] && e[h].y >= kExpMin;
+          pass[u][2 * h] = pos < s.last[2 * h] && e[h].x >= kExpMin;
+          pass[u][2 * h + 1] = pos < s.last[2 * h + 1] && e[h].y >= kExpMin;
         }
-        const bool any = pass[0] || pass[1] || pass[2] || pass[3];
-        const unsigned ball = __ballot_sync(0xffffffffu, any);
-        if (!ball) continue;
-        const BwdRec &rc = s_rec[j];
-        bwd_entry<kParams>(s, e, pass, any, ball, rc.rgbz, rc.conic, rc.uv, pg.fpy, fx,
+        any[u] = pass[u][0] || pass[u][1] || pass[u][2] || pass[u][3];
+        ball[u] = __ballot_sync(0xffffffffu, any[u]);
+        ap[u] = alpha_prep(e, pass[u]);
+      }
+#pragma unroll
+      for (int u = 0; u < 2; ++u) {
+        if (!ball[u]) continue;
+        const BwdRec &rc = s_rec[u ? jb_ : ja_];
+        bwd_entry<kParams>(s, ap[u], any[u], ball[u], rc.rgbz, rc.conic, rc.uv, pg.fpy, fx,
                            a.grad2d + size_t(rc.idx) * kG2, s_red[w], rr);
       }
     }
