@@ -320,3 +320,35 @@ def test_large_splat_covers_image():
     assert to_np(r.proj.tiles_touched)[0] == 7 * 5
     ok = fr["margin"] > AMBIG
     assert np.abs(g["color"] - fr["color"])[:, ok].max() <= 1e-4
+
+
+@pytest.mark.parametrize("T", [1, 5, 1200, 3225, 8160, 20000])
+def test_tile_orders_are_heaviest_first_permutations(T):
+    """gs_tile_order (and gs_bin_sort's tile_order): a permutation of the
+    tiles, bucket-major by 64 buckets of max / 64, heaviest bucket first."""
+    import torch
+    from paper_2312_10070_b200.raster import gs_tile_order
+    rng = np.random.default_rng(T)
+    work = rng.integers(0, 5000, T).astype(np.int32)
+    work[rng.uniform(size=T) < 0.1] = 0
+    w = torch.as_tensor(work, device="cuda")
+    order = torch.full((T,), -1, dtype=torch.int32, device="cuda")
+    gs_tile_order(w, T, order)
+    torch.cuda.synchronize()
+    o = order.cpu().numpy()
+    assert np.array_equal(np.sort(o), np.arange(T))
+    b = 63 - (work[o].astype(np.int64) * 64) // (int(work.max()) + 1)
+    assert (np.diff(b) >= 0).all()
+
+
+def test_bin_sort_tile_order_by_list_length():
+    s = inputs.config1()
+    r, P, v = gpu_forward(s)
+    import torch
+    torch.cuda.synchronize()
+    o = r.tile_order.cpu().numpy()
+    rng_ = r.tile_range.cpu().numpy().reshape(-1, 2)
+    L = (rng_[:, 1] - rng_[:, 0]).astype(np.int64)
+    assert np.array_equal(np.sort(o), np.arange(len(L)))
+    b = 63 - (L[o] * 64) // (int(L.max()) + 1)
+    assert (np.diff(b) >= 0).all()
