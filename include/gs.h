@@ -414,6 +414,27 @@ int gs_seed(gs_camera cam, const gs_view *view_host, const float *color, const f
             const float *alpha, float alpha_n, float rho, int32_t max_new, uint32_t seed,
             gs_params p, int32_t capacity, void *ws, size_t ws_bytes, int32_t *n_new, void *stream);
 
+/* First keyframe of a sub-map, M_c batch ("M_c points from the
+ * keyframe point cloud in high color gradient regions"; R43): the
+ * high-colour-gradient candidate set as a pseudo-alpha map for gs_seed
+ * (alpha_n = 0.5 then samples exactly that set):
+ *   grey = (0.299 r + 0.587 g) + 0.114 b, 3x3 Sobel gx, gy on interior
+ *   pixels (0 on the border), m2 = gx^2 + gy^2, all IEEE fp64 in this order;
+ *   t = the nearest-rank q-percentile of m2 over all pixels (the
+ *   ceil(q HW)-th smallest, exact); pseudo_alpha = 0 where m2 > t and
+ *   depth > 0, else 1.
+ *   color [3][H][W], depth [H][W] (device) the keyframe
+ *   q             in (0, 1] (0.95)
+ *   pseudo_alpha  (device) [H][W] written
+ *   threshold_m2  (device, nullable) [1] fp64: t
+ *   ws (device, 8-byte aligned) >= gs_gradient_mask_workspace_bytes(cam)
+ * The M_u batch is gs_seed with the empty sub-map's alpha (all 0); the M_c
+ * batch then runs against the sub-map holding the M_u Gaussians. */
+size_t gs_gradient_mask_workspace_bytes(gs_camera cam);
+int gs_gradient_mask(gs_camera cam, const float *color, const float *depth, double q,
+                     float *pseudo_alpha, double *threshold_m2, void *ws, size_t ws_bytes,
+                     void *stream);
+
 /* Input frames ("the RGBD frame", "the input color and depth map
  * at frame i", "an RGBD sensor"): unpacks a frame in the sensors' and
  * datasets' format, 8-bit RGB and 16-bit depth, into the fp32 planar targets

@@ -28,6 +28,16 @@ distances.  Readings R37-R41:
       logit 0 (o = 0.5), rotation (1, 0, 0, 0), log-scales = ln(clamp(d_nn,
       rho / 2, 0.1 m)) on all three axes, d_nn = distance to the nearest other
       point among the existing means and the accepted new points.
+  R43 the first keyframe of a sub-map ("we sample M_u uniformly and M_c
+      points from the keyframe point cloud in high color gradient regions"):
+      a batch of M_u uniform samples (valid depth; the empty sub-map renders
+      alpha 0), then a batch of M_c samples from the high-colour-gradient set
+      against the sub-map that now holds the first batch.  High colour
+      gradient: grey = (0.299 r + 0.587 g) + 0.114 b, 3x3
+      Sobel gx, gy on interior pixels (0 on the border), m2 = gx^2 + gy^2, all
+      in fp64 in this order; the set = valid-depth pixels with m2 strictly
+      above the nearest-rank percentile (the ceil(q HW)-th smallest m2 over
+      all pixels, q = 0.95).
 """
 from __future__ import annotations
 
@@ -116,3 +126,44 @@ def seed(color, depth, alpha, view, cam, means, alpha_n=0.6, rho=0.01, max_new=1
                 quat=np.tile(np.array([1, 0, 0, 0], np.float32), (n, 1)),
                 logscale=np.concatenate([np.repeat(s[:, None], 3, axis=1), np.zeros((n, 1))], axis=1),
                 rgb=np.concatenate([cols, np.zeros((n, 1), np.float32)], axis=1))
+
+
+def gradient_m2(color):
+    """R43: squared Sobel magnitude of the grey image, fp64 [H, W]."""
+    c = np.asarray(color, np.float32).astype(np.float64)
+    g = (0.299 * c[0] + 0.587 * c[1]) + 0.114 * c[2]
+    H, W = g.shape
+    m2 = np.zeros((H, W))
+    if H < 3 or W < 3:
+        return m2
+    up, mid, dn = g[:-2], g[1:-1], g[2:]
+    # gx = right column - left column, gy = bottom row - top row, (1, 2, 1) weights, in this order
+    gx = ((up[:, 2:] + 2.0 * mid[:, 2:]) + dn[:, 2:]) - ((up[:, :-2] + 2.0 * mid[:, :-2]) + dn[:, :-2])
+    gy = ((dn[:, :-2] + 2.0 * dn[:, 1:-1]) + dn[:, 2:]) - ((up[:, :-2] + 2.0 * up[:, 1:-1]) + up[:, 2:])
+    m2[1:-1, 1:-1] = gx * gx + gy * gy
+    return m2
+
+
+def gradient_threshold(m2, q=0.95):
+    """R43: the nearest-rank q-percentile of m2 over all pixels."""
+    v = np.sort(np.asarray(m2, np.float64).ravel())
+    k = max(int(np.ceil(q * v.size)), 1)
+    return float(v[k - 1])
+
+
+def gradient_mask(color, depth, q=0.95):
+    """R43: the high-colour-gradient candidate set (bool [H, W])."""
+    m2 = gradient_m2(color)
+    return (m2 > gradient_threshold(m2, q)) & (np.asarray(depth, np.float32) > 0)
+
+
+def first_keyframe(color, depth, view, cam, M_u, M_c, rho=0.01, seed_=0, q=0.95):
+    """R43: the two insertion batches of a new sub-map's first keyframe;
+    returns the two seed() results (the second against the first's Gaussians)."""
+    H, W = np.asarray(depth).shape
+    r1 = seed(color, depth, np.zeros((H, W), np.float32), view, cam, np.zeros((0, 4), np.float32),
+              rho=rho, max_new=M_u, seed_=seed_)
+    pseudo = np.where(gradient_mask(color, depth, q), 0.0, 1.0).astype(np.float32)
+    r2 = seed(color, depth, pseudo, view, cam, r1["mean_opa"], alpha_n=0.5, rho=rho, max_new=M_c,
+              seed_=seed_ + 1)
+    return r1, r2

@@ -16,7 +16,15 @@
 // prunes the brute-force search (points within 0.1 m lie in adjacent cells).
 // Compactions are block counts + one-CTA scan + ballot scatter: the output
 // order is deterministic (sample order).
+//
+// gs_gradient_mask (the first keyframe's M_c batch, R43): the grey image's
+// squared Sobel magnitude in fp64 (the oracle's operation order, no
+// contraction), its exact nearest-rank percentile by an 8-pass MSB radix
+// select over the fp64 bit patterns, and a pseudo-alpha map (0 on the
+// high-gradient valid-depth pixels, 1 elsewhere) that gs_seed's alpha gate
+// turns into that candidate set.
 #include <algorithm>
+#include <cmath>
 
 #include "gs_internal.cuh"
 
@@ -376,7 +384,125 @@ __global__ void __launch_bounds__(kSdThreads) k_sd_emit(SeedArgs a) {
   a.o_rgb[o] = make_float4(__ldg(a.color + p), __ldg(a.color + a.HW + p), __ldg(a.color + 2 * a.HW + p), 0.f);
 }
 
+// ---- R43: high-colour-gradient mask --------------------------------------------
+constexpr int kGmThreads = 256;
+
+__global__ void __launch_bounds__(kGmThreads) k_gm_grey(const float *__restrict__ color, int64_t HW, double *grey) {
+  const int64_t q = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (q >= HW) return;
+  const double r = __ldg(color + q), g = __ldg(color + HW + q), b = __ldg(color + 2 * HW + q);
+  grey[q] = __dadd_rn(__dadd_rn(__dmul_rn(0.299, r), __dmul_rn(0.587, g)), __dmul_rn(0.114, b));
+}
+
+__global__ void __launch_bounds__(kGmThreads) k_gm_m2(const double *__restrict__ grey, int W, int H,
+                                                      uint64_t *keys) {
+  const int64_t q = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (q >= int64_t(W) * H) return;
+  const int i = int(q % W), j = int(q / W);
+  double m2 = 0.0;
+  if (i > 0 && j > 0 && i < W - 1 && j < H - 1) {
+    auto G = [&](int y, int x) { return grey[int64_t(y) * W + x]; };
+    // gx = right - left column, gy = bottom - top row, weights (1, 2, 1), the oracle's order
+    const double gx = __dsub_rn(__dadd_rn(__dadd_rn(G(j - 1, i + 1), __dmul_rn(2.0, G(j, i + 1))), G(j + 1, i + 1)),
+                                __dadd_rn(__dadd_rn(G(j - 1, i - 1), __dmul_rn(2.0, G(j, i - 1))), G(j + 1, i - 1)));
+    const double gy = __dsub_rn(__dadd_rn(__dadd_rn(G(j + 1, i - 1), __dmul_rn(2.0, G(j + 1, i))), G(j + 1, i + 1)),
+                                __dadd_rn(__dadd_rn(G(j - 1, i - 1), __dmul_rn(2.0, G(j - 1, i))), G(j - 1, i + 1)));
+    m2 = __dadd_rn(__dmul_rn(gx, gx), __dmul_rn(gy, gy));
+  }
+  keys[q] = uint64_t(__double_as_longlong(m2));  // m2 >= +0: bit order = value order
+}
+
+// select state: [0] prefix of the k-th key, [1] k (1-based rank among the
+// keys matching the prefix); hist [256]
+__global__ void __launch_bounds__(kGmThreads) k_gm_hist(const uint64_t *__restrict__ keys, int64_t HW, int shift,
+                                                        const unsigned long long *state, unsigned *hist) {
+  __shared__ unsigned sh[256];
+  sh[threadIdx.x] = 0u;
+  __syncthreads();
+  const uint64_t prefix = state[0];
+  const uint64_t hi_mask = shift >= 56 ? 0ull : ~((uint64_t(1) << (shift + 8)) - 1);
+  for (int64_t q = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; q < HW; q += int64_t(gridDim.x) * blockDim.x) {
+    const uint64_t k = keys[q];
+    if ((k & hi_mask) == (prefix & hi_mask)) atomicAdd(&sh[(k >> shift) & 255u], 1u);
+  }
+  __syncthreads();
+  if (sh[threadIdx.x]) atomicAdd(&hist[threadIdx.x], sh[threadIdx.x]);
+}
+
+__global__ void __launch_bounds__(256) k_gm_pick(int shift, unsigned long long *state, unsigned *hist) {
+  __shared__ unsigned sh[256];
+  const unsigned c = hist[threadIdx.x];
+  sh[threadIdx.x] = c;
+  __syncthreads();
+  if (threadIdx.x == 0) {  // the digit whose cumulative count reaches k (fixed order)
+    unsigned long long k = state[1], cum = 0;
+    int d = 0;
+    for (; d < 255; ++d) {
+      if (cum + sh[d] >= k) break;
+      cum += sh[d];
+    }
+    state[0] |= (unsigned long long)d << shift;
+    state[1] = k - cum;
+  }
+  hist[threadIdx.x] = 0u;  // for the next pass
+}
+
+__global__ void __launch_bounds__(256) k_gm_init(unsigned long long *state, unsigned *hist, unsigned long long k) {
+  if (threadIdx.x == 0) {
+    state[0] = 0ull;
+    state[1] = k;
+  }
+  hist[threadIdx.x] = 0u;
+}
+
+__global__ void __launch_bounds__(kGmThreads) k_gm_mask(const uint64_t *__restrict__ keys,
+                                                        const float *__restrict__ depth, int64_t HW,
+                                                        const unsigned long long *state, float *pseudo_alpha) {
+  const int64_t q = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (q >= HW) return;
+  pseudo_alpha[q] = (keys[q] > state[0] && __ldg(depth + q) > 0.f) ? 0.f : 1.f;
+}
+
 }  // namespace gs
+
+extern "C" size_t gs_gradient_mask_workspace_bytes(gs_camera cam) {
+  if (!gs::camera_ok(cam)) return 0;
+  return 16 * size_t(cam.width) * cam.height + 2048;  // grey + keys (fp64 / uint64 per pixel), state, histogram
+}
+
+extern "C" int gs_gradient_mask(gs_camera cam, const float *color, const float *depth, double q, float *pseudo_alpha,
+                                double *threshold_m2, void *ws, size_t ws_bytes, void *stream) {
+  using namespace gs;
+  if (!camera_ok(cam) || !color || !depth || !pseudo_alpha || !(q > 0.0 && q <= 1.0)) {
+    set_error("gs_gradient_mask: invalid argument");
+    return GS_ERR_INVALID_ARG;
+  }
+  const int64_t HW = int64_t(cam.width) * cam.height;
+  if (!ws || ws_bytes < gs_gradient_mask_workspace_bytes(cam) || (reinterpret_cast<uintptr_t>(ws) & 7u)) {
+    set_error("gs_gradient_mask: workspace too small or misaligned");
+    return GS_ERR_WORKSPACE;
+  }
+  cudaStream_t s = as_stream(stream);
+  char *w = static_cast<char *>(ws);
+  double *grey = reinterpret_cast<double *>(w);
+  uint64_t *keys = reinterpret_cast<uint64_t *>(w + 8 * size_t(HW));
+  unsigned long long *state = reinterpret_cast<unsigned long long *>(w + 16 * size_t(HW));
+  unsigned *hist = reinterpret_cast<unsigned *>(w + 16 * size_t(HW) + 64);
+  // nearest rank: the ceil(q HW)-th smallest (fp64 product, as the oracle)
+  const unsigned long long k = (unsigned long long)std::max<double>(1.0, std::ceil(q * double(HW)));
+  k_gm_init<<<1, 256, 0, s>>>(state, hist, k);
+  const int nb = int((HW + kGmThreads - 1) / kGmThreads);
+  k_gm_grey<<<nb, kGmThreads, 0, s>>>(color, HW, grey);
+  k_gm_m2<<<nb, kGmThreads, 0, s>>>(grey, cam.width, cam.height, keys);
+  const int nh = std::min(nb, 148 * 8);
+  for (int shift = 56; shift >= 0; shift -= 8) {
+    k_gm_hist<<<nh, kGmThreads, 0, s>>>(keys, HW, shift, state, hist);
+    k_gm_pick<<<1, 256, 0, s>>>(shift, state, hist);
+  }
+  k_gm_mask<<<nb, kGmThreads, 0, s>>>(keys, depth, HW, state, pseudo_alpha);
+  if (threshold_m2) cudaMemcpyAsync(threshold_m2, state, sizeof(double), cudaMemcpyDeviceToDevice, s);
+  return check_launch("gs_gradient_mask");
+}
 
 extern "C" size_t gs_seed_workspace_bytes(gs_camera cam, int32_t n, int32_t max_new) {
   if (!gs::camera_ok(cam) || n < 0 || max_new < 0) return 0;

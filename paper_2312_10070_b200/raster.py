@@ -20,7 +20,7 @@ from ._lib import (GS_BWD_ATOMIC_ACC, GS_BWD_GAUSS_ONLY, GS_BWD_PIXELS_ONLY, GS_
                    GsParams, GsPoseStep, GsProj, GsView, check, lib)
 
 __all__ = ["Params", "Grads", "Proj", "Frame", "Rasterizer", "camera", "gs_project", "gs_bin_sort",
-           "gs_render_fwd", "gs_render_fwd_l1", "gs_loss_scales", "gs_loss_from_tiles", "gs_tile_order", "gs_loss", "gs_tracking_loss", "gs_ssim", "gs_iso_reg", "gs_adam_step", "gs_prune", "gs_seed", "gs_unpack_rgbd", "Optimizer", "gs_render_bwd", "gs_render_bwd_gauss_views", "gs_pose_grad", "GS_GRAD_PARAMS", "GS_GRAD_POSE", "GS_BWD_PIXELS_ONLY", "GS_BWD_GAUSS_ONLY", "GS_BWD_ATOMIC_ACC",
+           "gs_render_fwd", "gs_render_fwd_l1", "gs_loss_scales", "gs_loss_from_tiles", "gs_tile_order", "gs_loss", "gs_tracking_loss", "gs_ssim", "gs_iso_reg", "gs_adam_step", "gs_prune", "gs_seed", "gs_gradient_mask", "seed_first_keyframe", "gs_unpack_rgbd", "Optimizer", "gs_render_bwd", "gs_render_bwd_gauss_views", "gs_pose_grad", "GS_GRAD_PARAMS", "GS_GRAD_POSE", "GS_BWD_PIXELS_ONLY", "GS_BWD_GAUSS_ONLY", "GS_BWD_ATOMIC_ACC",
            "GsError", "device_check"]
 
 
@@ -225,6 +225,34 @@ def gs_seed(cam: GsCamera, view, color, depth, alpha, alpha_n, rho, max_new, see
     check(lib().gs_seed(cam, C.byref(gv), _p(color), _p(depth), _p(alpha), float(alpha_n), float(rho), int(max_new),
                         int(seed) & 0xFFFFFFFF, P, int(cap), _p(ws), ws.numel() * ws.element_size(), _p(n_new),
                         _stream(stream)), "gs_seed")
+
+
+def gs_gradient_mask(cam: GsCamera, color, depth, q, pseudo_alpha, ws, threshold_m2=None, stream=None):
+    """R43: pseudo_alpha (device [H, W]) = 0 on the high-colour-gradient
+    valid-depth pixels of the keyframe, 1 elsewhere (gs_seed with alpha_n 0.5)."""
+    check(lib().gs_gradient_mask(cam, _p(color), _p(depth), float(q), _p(pseudo_alpha), _p(threshold_m2), _p(ws),
+                                 ws.numel() * ws.element_size(), _stream(stream)), "gs_gradient_mask")
+
+
+def seed_first_keyframe(cam: GsCamera, view, color, depth, params: Params, n, M_u, M_c, seed, rho=0.01, q=0.95):
+    """The first keyframe of a sub-map (R43): M_u uniform samples, then
+    M_c samples of the high-colour-gradient set against the sub-map holding
+    the first batch; params (capacity >= n + M_u + M_c) gets both batches
+    after the first n.  Host-synchronising (the second batch starts after the
+    first's count).  Returns (n_u, n_c)."""
+    import numpy as np  # noqa: F401
+    d = color.device
+    H, W = depth.shape
+    ws = torch.empty((max(lib().gs_seed_workspace_bytes(cam, n + M_u, max(M_u, M_c)),
+                          lib().gs_gradient_mask_workspace_bytes(cam)) + 15) // 16 * 4, dtype=torch.float32, device=d)
+    n_new = torch.zeros(1, dtype=torch.int32, device=d)
+    gs_seed(cam, view, color, depth, torch.zeros(H, W, dtype=torch.float32, device=d), 0.6, rho, M_u, seed, params,
+            n, ws, n_new)
+    n_u = int(n_new.item())
+    pseudo = torch.empty(H, W, dtype=torch.float32, device=d)
+    gs_gradient_mask(cam, color, depth, q, pseudo, ws)
+    gs_seed(cam, view, color, depth, pseudo, 0.5, rho, M_c, seed + 1, params, n + n_u, ws, n_new)
+    return n_u, int(n_new.item())
 
 
 def gs_unpack_rgbd(cam: GsCamera, rgb8, depth16, depth_scale, tgt_color, tgt_depth, stream=None):

@@ -90,3 +90,58 @@ def test_seed_from_rendered_alpha_full_size():
     c = r.frame.color.cpu().numpy()
     o = _check(c, d, a, s.views[0], s.cam, s.params()[0][:20000], max_new=4000, seed=7)
     assert o["accepted"].sum() > 0
+
+
+@pytest.mark.parametrize("W,H,q", [(37, 23, 0.95), (64, 48, 0.9), (2, 2, 0.95), (1200, 680, 0.95)])
+def test_gradient_mask_parity(W, H, q):
+    """R43: the high-colour-gradient set and its nearest-rank threshold,
+    bit-exact (fp64 Sobel in the oracle's order, exact radix select)."""
+    from paper_2312_10070_b200.raster import gs_gradient_mask
+    rng = np.random.default_rng(W + H)
+    color = rng.uniform(0, 1, (3, H, W)).astype(np.float32)
+    color[:, :, W // 2:] *= 0.3
+    color[:, ::7] = 0.5  # ties in m2
+    depth = rng.uniform(0.5, 4.0, (H, W)).astype(np.float32)
+    depth[rng.uniform(size=(H, W)) < 0.1] = 0.0
+    cam = camera(inputs.Camera(W, H, 100.0, 100.0, W / 2, H / 2))
+    ws = torch.empty((lib().gs_gradient_mask_workspace_bytes(cam) + 15) // 16 * 4, dtype=torch.float32, device=DEV)
+    pa = torch.full((H, W), -1.0, device=DEV)
+    thr = torch.zeros(1, dtype=torch.float64, device=DEV)
+    t = lambda a: torch.as_tensor(a, device=DEV)
+    gs_gradient_mask(cam, t(color), t(depth), q, pa, ws, threshold_m2=thr)
+    torch.cuda.synchronize()
+    m2 = S.gradient_m2(color)
+    assert thr.item() == S.gradient_threshold(m2, q)
+    mask = S.gradient_mask(color, depth, q)
+    assert np.array_equal(pa.cpu().numpy(), np.where(mask, 0.0, 1.0).astype(np.float32))
+
+
+def test_first_keyframe_parity():
+    """P:156 / R43: the M_u uniform batch, then the M_c gradient batch against
+    it, equal to the oracle's two batches (counts, means, colours, rotations
+    bit-exact; log-scales within 1e-6)."""
+    from paper_2312_10070_b200.raster import seed_first_keyframe
+    H, W = 60, 80
+    rng = np.random.default_rng(9)
+    color = rng.uniform(0, 1, (3, H, W)).astype(np.float32)
+    color[:, 20:40, 30:50] = 0.9  # a bright square: strong edges
+    depth = (2.0 + 0.05 * rng.standard_normal((H, W))).astype(np.float32)
+    depth[rng.uniform(size=(H, W)) < 0.05] = 0.0
+    cam_py = inputs.Camera(W, H, 400.0, 400.0, (W - 1) / 2, (H - 1) / 2)
+    view = np.array([0.98, -0.2, 0, 0.2, 0.98, 0, 0, 0, 1, 0.01, -0.02, 0.03], np.float32)
+    M_u, M_c = 1200, 300
+    r1, r2 = S.first_keyframe(color, depth, view, cam_py, M_u, M_c, seed_=4)
+    cap = M_u + M_c
+    z = np.zeros((cap, 4), np.float32)
+    P = Params.from_numpy(z, z, z, z, device=DEV)
+    t = lambda a: torch.as_tensor(a, device=DEV)
+    n_u, n_c = seed_first_keyframe(camera(cam_py), view, t(color), t(depth), P, 0, M_u, M_c, 4)
+    torch.cuda.synchronize()
+    assert n_u == int(r1["accepted"].sum()) and n_c == int(r2["accepted"].sum()) and n_c > 0
+    for name, k0, k1, o in (("mean_opa", 0, n_u, r1), ("mean_opa", n_u, n_u + n_c, r2)):
+        assert np.array_equal(P.mean_opa.cpu().numpy()[k0:k1], o["mean_opa"])
+    got = {k: getattr(P, k).cpu().numpy() for k in ("quat", "rgb", "logscale")}
+    for k0, k1, o in ((0, n_u, r1), (n_u, n_u + n_c, r2)):
+        assert np.array_equal(got["quat"][k0:k1], o["quat"])
+        assert np.array_equal(got["rgb"][k0:k1], o["rgb"])
+        np.testing.assert_allclose(got["logscale"][k0:k1], o["logscale"], rtol=1e-6, atol=1e-7)

@@ -100,3 +100,63 @@ def test_new_gaussian_init():
     ex = np.array([[p[0] + 0.03, p[1], p[2], 0.0]], np.float32)
     r2 = S.seed(color, depth, alpha, I12, cam, ex)
     assert abs(np.exp(r2["logscale"][0, 0]) - 0.03) < 1e-6
+
+
+def test_sobel_step_edge_and_border():
+    """A vertical step of height d in grey: gx = 4 d on the two columns next
+    to the edge, gy = 0; the border is 0 (R43)."""
+    H, W = 6, 8
+    c = np.zeros((3, H, W), np.float32)
+    c[:, :, 4:] = 0.5  # grey = 0.5 (0.299 + 0.587 + 0.114 = 1)
+    m2 = S.gradient_m2(c)
+    g = (0.299 * 0.5 + 0.587 * 0.5) + 0.114 * 0.5
+    assert np.allclose(m2[1:-1, 3], (4 * g) ** 2) and np.allclose(m2[1:-1, 4], (4 * g) ** 2)
+    assert (m2[1:-1, [1, 2, 5, 6]] == 0).all()
+    assert (m2[0] == 0).all() and (m2[-1] == 0).all() and (m2[:, 0] == 0).all() and (m2[:, -1] == 0).all()
+    # a horizontal ramp of slope s: gx = 8 s everywhere inside, gy = 0
+    r = np.tile(np.arange(W, dtype=np.float32) * 0.01, (H, 1))
+    m2 = S.gradient_m2(np.stack([r, r, r]))
+    assert np.allclose(m2[1:-1, 1:-1], (8 * 0.01) ** 2, rtol=1e-9)
+
+
+def test_grey_weights_and_sobel_brute_force():
+    rng = np.random.default_rng(4)
+    c = rng.uniform(0, 1, (3, 7, 9)).astype(np.float32)
+    m2 = S.gradient_m2(c)
+    g = c.astype(np.float64)
+    grey = 0.299 * g[0] + 0.587 * g[1] + 0.114 * g[2]
+    kx = np.array([[-1, 0, 1], [-2, 0, 2], [-1, 0, 1]], np.float64)
+    for j in range(1, 6):
+        for i in range(1, 8):
+            win = grey[j - 1:j + 2, i - 1:i + 2]
+            gx, gy = (win * kx).sum(), (win * kx.T).sum()
+            assert abs(m2[j, i] - (gx * gx + gy * gy)) < 1e-12
+
+
+def test_percentile_nearest_rank():
+    v = np.arange(1, 101, dtype=np.float64)  # 1..100
+    assert S.gradient_threshold(v, 0.95) == 95.0
+    assert S.gradient_threshold(v, 0.951) == 96.0
+    assert S.gradient_threshold(np.array([3.0]), 0.95) == 3.0
+    m = np.zeros(100)
+    m[:7] = 5.0  # ties: 93 zeros, 7 fives -> threshold 5, nothing strictly above
+    assert S.gradient_threshold(m, 0.95) == 5.0
+
+
+def test_first_keyframe_batches():
+    """Uniform batch, then the gradient batch against it: the gradient
+    candidates all come from the high-gradient set, and the union stays
+    rho-separated (R40, R43)."""
+    H, W = 40, 48
+    rng = np.random.default_rng(5)
+    color = rng.uniform(0, 1, (3, H, W)).astype(np.float32)
+    color[:, :, 24:] *= 0.2  # a strong edge
+    depth = (2.0 + 0.1 * rng.uniform(size=(H, W))).astype(np.float32)
+    cam = inputs.Camera(W, H, 300.0, 300.0, (W - 1) / 2, (H - 1) / 2)
+    r1, r2 = S.first_keyframe(color, depth, I12, cam, M_u=200, M_c=60, seed_=3)
+    mask = S.gradient_mask(color, depth)
+    assert mask.sum() <= int(np.ceil(0.05 * H * W)) + 1 and mask.sum() > 0
+    assert mask.ravel()[r2["idx"]].all()
+    A = np.concatenate([r1["mean_opa"][:, :3], r2["mean_opa"][:, :3]]).astype(np.float64)
+    d = np.sqrt(((A[:, None] - A[None]) ** 2).sum(-1)) + np.eye(len(A))
+    assert d.min() >= 0.01 - 1e-9
