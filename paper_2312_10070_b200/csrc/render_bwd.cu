@@ -7,11 +7,12 @@
 // reconstructing T_j = T_{j+1}/(1-alpha_j) and carrying the suffix form of
 // Eq. 8 (one scalar Q = G . S per pixel).  The per-pixel arithmetic runs on
 // fp32x2 pixel pairs (FFMA2).  Each warp walks, back to front, the compacted
-// list of staged entries that meet its strip; per (thread, entry) the 2-D
-// gradients are summed over the thread's pixels, then across the warp by a
-// transposed reduce-scatter (skipped when no lane composited the entry, and
-// replaced by direct vector reds when <= 2 lanes did) and added to the
-// grad2d scratch.
+// list of staged entries that meet its strip, two entries per step (their
+// decisions, alphas and reciprocals first, then the T / Q chain of each);
+// per (thread, entry) the 2-D gradients are summed over the thread's pixels,
+// then across the warp through a per-warp shared-memory slab (skipped when no
+// lane composited the entry, replaced by direct vector reds when <= 2 lanes
+// did) and added to the grad2d scratch.
 //
 // S6 (k_bwd_gauss): one thread per visible Gaussian chains the 2-D gradients
 // to mean, quaternion, log-scales, opacity logit and colour ("derived as in
@@ -39,52 +40,12 @@ struct BwdArgs {
   float *grad2d;
 };
 
-// Transposed warp reduce-scatter of 10 values (u, v, A, B, C, z, logit, r, g, b):
-// 12 shuffles instead of 5 x 10.  Each stage halves the lanes' value sets;
-// on return this lane holds the warp total of value `idx`, and `writer` is
-// set on exactly one lane per value.
-__device__ __forceinline__ float warp_reduce10(const float v[10], int &idx, bool &writer) {
-  const unsigned F = 0xffffffffu;
-  const int lane = threadIdx.x & 31;
-  const bool h16 = lane & 16, h8 = lane & 8, h4 = lane & 4, h2 = lane & 2, h1 = lane & 1;
-  float a[5];
-#pragma unroll
-  for (int k = 0; k < 5; ++k) {  // A (xor 16): low half keeps 0..4, high half 5..9
-    const float snd = h16 ? v[k] : v[k + 5];
-    a[k] = (h16 ? v[k + 5] : v[k]) + __shfl_xor_sync(F, snd, 16);
-  }
-  float b[3];
-#pragma unroll
-  for (int k = 0; k < 3; ++k) {  // B (xor 8): !h8 keeps a0..a2, h8 keeps a3, a4
-    const float snd = h8 ? a[k] : (k < 2 ? a[3 + k] : 0.f);
-    const float r = __shfl_xor_sync(F, snd, 8);
-    b[k] = h8 ? (k < 2 ? a[3 + k] + r : 0.f) : a[k] + r;
-  }
-  // C (xor 4): (!h8,!h4) keeps b0,b1; (!h8,h4) keeps b2; (h8,!h4) keeps b0; (h8,h4) keeps b1
-  const float s1 = !h8 ? (!h4 ? b[2] : b[0]) : (!h4 ? b[1] : b[0]);
-  const float s2 = (!h8 && h4) ? b[1] : 0.f;
-  const float r1 = __shfl_xor_sync(F, s1, 4);
-  const float r2 = __shfl_xor_sync(F, s2, 4);
-  const bool two = !h8 && !h4;
-  const float c0 = (!h8 ? (!h4 ? b[0] : b[2]) : (!h4 ? b[0] : b[1])) + r1;
-  const float c1 = b[1] + r2;  // meaningful only when `two`
-  // D (xor 2): lanes holding two values split them; others add their pair
-  const float sd = two ? (h2 ? c0 : c1) : c0;
-  const float d0 = (two ? (h2 ? c1 : c0) : c0) + __shfl_xor_sync(F, sd, 2);
-  const float e0 = d0 + __shfl_xor_sync(F, d0, 1);  // E (xor 1)
-  const int sub = two ? (h2 ? 1 : 0) : (!h8 ? 2 : (!h4 ? 3 : 4));
-  idx = (h16 ? 5 : 0) + sub;
-  writer = !h1 && (two || !h2);
-  return e0;
-}
-
 __device__ __forceinline__ void red_add_v4(float *addr, float x, float y, float z, float w) {
   asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(addr), "f"(x), "f"(y), "f"(z), "f"(w)
                : "memory");
 }
 
 constexpr int kBPX = 4;   // pixels per thread in the backward (two fp32x2 pairs)
-constexpr bool kSmemReduce = true;  // per-entry warp sums through shared memory (else shuffles)
 #ifndef BWD_MINB
 #define BWD_MINB 1
 #endif
@@ -222,46 +183,36 @@ __device__ __forceinline__ void bwd_entry(BwdPix &s, const AlphaPrep &ap, bool a
     }
     return;
   }
-  if (kSmemReduce) {
-    // through this warp's shared-memory slab (Slab): lane l stores its NV
-    // values in row l; lane L v + p sums value v over the rows = p mod L
-    // (zero rows past 32: no bounds checks), the L partial sums meet by
-    // shuffles, lane L v adds the total to grad2d
-    using SL = Slab<kParams>;
-    const int lane = threadIdx.x & 31;
-    float *row = red + lane * SL::S;
-    __syncwarp();  // the previous entry's reads of the slab are done
+  // through this warp's shared-memory slab (Slab): lane l stores its NV
+  // values in row l; lane L v + p sums value v over the rows = p mod L
+  // (zero rows past 32: no bounds checks), the L partial sums meet by
+  // shuffles, lane L v adds the total to grad2d
+  using SL = Slab<kParams>;
+  const int lane = threadIdx.x & 31;
+  float *row = red + lane * SL::S;
+  __syncwarp();  // the previous entry's reads of the slab are done
 #pragma unroll
-    for (int v = 0; v < SL::NV; ++v) row[v] = acc[v];
-    __syncwarp();
-    float c[SL::R];
+  for (int v = 0; v < SL::NV; ++v) row[v] = acc[v];
+  __syncwarp();
+  float cs[SL::R];
 #pragma unroll
-    for (int t = 0; t < SL::R; ++t) c[t] = rr.col[t * SL::L * SL::S];
-    float part;
-    if (SL::R == 11) {  // pairwise (depth 4, not a chain of dependent adds)
-      part = (((c[0] + c[1]) + (c[2] + c[3])) + ((c[4] + c[5]) + (c[6] + c[7]))) + ((c[8] + c[9]) + c[10]);
-    } else {
-      part = c[0];
+  for (int t = 0; t < SL::R; ++t) cs[t] = rr.col[t * SL::L * SL::S];
+  float part;
+  if (SL::R == 11) {  // pairwise (depth 4, not a chain of dependent adds)
+    part = (((cs[0] + cs[1]) + (cs[2] + cs[3])) + ((cs[4] + cs[5]) + (cs[6] + cs[7]))) + ((cs[8] + cs[9]) + cs[10]);
+  } else {
+    part = cs[0];
 #pragma unroll
-      for (int t = 1; t < SL::R; t += 2) part += t + 1 < SL::R ? c[t] + c[t + 1] : c[t];
-    }
-    if (SL::L == 3) {
-      part += __shfl_down_sync(0xffffffffu, part, 1) + __shfl_down_sync(0xffffffffu, part, 2);
-    } else {  // L = 5: (x0 + x1) + (x2 + x3) + x4 on the group's first lane
-      float q = part + __shfl_down_sync(0xffffffffu, part, 1);
-      q += __shfl_down_sync(0xffffffffu, q, 2);
-      part = q + __shfl_down_sync(0xffffffffu, part, 4);
-    }
-    if (rr.writer) atomicAdd(dst + rr.woff, rr.wsc * part);
-    return;
+    for (int t = 1; t < SL::R; t += 2) part += t + 1 < SL::R ? cs[t] + cs[t + 1] : cs[t];
   }
-  const float sgn[10] = {-1.f, -1.f, -0.5f, -1.f, -0.5f, 1.f, 1.f, 1.f, 1.f, 1.f};
-#pragma unroll
-  for (int v = 0; v < 10; ++v) acc[v] *= sgn[v];
-  int idx;
-  bool writer;
-  const float tot = warp_reduce10(acc, idx, writer);
-  if (writer && (kParams || idx < 6)) atomicAdd(dst + (idx < 7 ? idx : idx + 1), tot);
+  if (SL::L == 3) {
+    part += __shfl_down_sync(0xffffffffu, part, 1) + __shfl_down_sync(0xffffffffu, part, 2);
+  } else {  // L = 5: (x0 + x1) + (x2 + x3) + x4 on the group's first lane
+    float q = part + __shfl_down_sync(0xffffffffu, part, 1);
+    q += __shfl_down_sync(0xffffffffu, q, 2);
+    part = q + __shfl_down_sync(0xffffffffu, part, 4);
+  }
+  if (rr.writer) atomicAdd(dst + rr.woff, rr.wsc * part);
 }
 
 // one staged list entry of the backward
