@@ -2,7 +2,7 @@
 
     python tools/profile_view.py [--config 3] [--reps 2]
 
-Runs `reps` untimed passes of project -> bin_sort -> render -> loss -> bwd on
+Runs `reps` untimed passes of project -> bin_sort -> render + loss (fused) -> bwd on
 view 0 after setup, so `ncu -k regex:<kernel> -s <reps-1> -c 1` captures one
 steady-state launch of each kernel.
 """
@@ -37,9 +37,14 @@ def main():
         r.forward(P, v)
     tc, td = r.frame.color.clone(), r.frame.depth.clone()
     g = Grads.zeros(s.n, d)
+    sc = r.loss_scales(td)
     torch.cuda.synchronize()
     for _ in range(a.reps):
-        r.forward(P, v)
+        # the step's path: S3 + S4 fused (gs_render_fwd_l1 + gs_loss_from_tiles);
+        # gs_loss once more for its own capture (the SSIM step's loss kernels)
+        r.project(P, v)
+        r.bin_sort()
+        r.render_l1(tc, td, 1.0, 1.0, sc)
         r.compute_loss(tc, td)
         r.backward(P, v, GS_GRAD_POSE if a.pose else GS_GRAD_PARAMS, None if a.pose else g)
         if a.pose:
