@@ -133,17 +133,36 @@ __global__ void __launch_bounds__(32) k_loss_scales(const uint32_t *__restrict__
 
 // gs_loss_from_tiles: loss[3] from the per-tile |residual| sums of
 // gs_render_fwd_l1, fixed-order (deterministic) fp64 reduction
-__global__ void __launch_bounds__(kLossThreads) k_loss_tiles(const double *__restrict__ part, int T, int64_t HW,
-                                                             const float *__restrict__ scales, float lc, float ld,
-                                                             float *loss) {
-  __shared__ double sh[kLossThreads];
+__global__ void __launch_bounds__(1024) k_loss_tiles(const double *__restrict__ part, int T, int64_t HW,
+                                                     const float *__restrict__ scales, float lc, float ld,
+                                                     float *loss) {
+  __shared__ double sw[2][32];
   double ac = 0.0, ad = 0.0;
   for (int t = threadIdx.x; t < T; t += blockDim.x) {  // fixed order per thread
-    ac += part[2 * t];
-    ad += part[2 * t + 1];
+    const double2 p = reinterpret_cast<const double2 *>(part)[t];
+    ac += p.x;
+    ad += p.y;
   }
-  ac = block_sum_d(ac, sh);
-  ad = block_sum_d(ad, sh);
+  // fixed-shape reduction: warp shuffles, then the 32 warp sums by warp 0
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    ac += __shfl_xor_sync(0xffffffffu, ac, o);
+    ad += __shfl_xor_sync(0xffffffffu, ad, o);
+  }
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  if (lane == 0) {
+    sw[0][w] = ac;
+    sw[1][w] = ad;
+  }
+  __syncthreads();
+  if (w != 0) return;
+  ac = lane < int(blockDim.x >> 5) ? sw[0][lane] : 0.0;
+  ad = lane < int(blockDim.x >> 5) ? sw[1][lane] : 0.0;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    ac += __shfl_xor_sync(0xffffffffu, ac, o);
+    ad += __shfl_xor_sync(0xffffffffu, ad, o);
+  }
   if (threadIdx.x == 0) {
     const double nv = double(scales[2]);
     const double Lc = ac / (3.0 * double(HW));
@@ -183,8 +202,8 @@ extern "C" int gs_loss_from_tiles(gs_camera cam, const double *loss_part, const 
     return GS_ERR_INVALID_ARG;
   }
   const int T = tiles_x(cam) * tiles_y(cam);
-  k_loss_tiles<<<1, kLossThreads, 0, as_stream(stream)>>>(loss_part, T, int64_t(cam.width) * cam.height, scales,
-                                                          lambda_color, lambda_depth, loss);
+  k_loss_tiles<<<1, 1024, 0, as_stream(stream)>>>(loss_part, T, int64_t(cam.width) * cam.height, scales,
+                                                  lambda_color, lambda_depth, loss);
   return check_launch("gs_loss_from_tiles");
 }
 
