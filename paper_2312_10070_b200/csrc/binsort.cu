@@ -51,7 +51,7 @@ struct SortLayout {
   int n, T, TX, TY;
   int64_t capacity;
   size_t diff, misc, zero_end;  // zeroed region (one memset per call)
-  size_t cursor, slow, key_a, key_b, val_b, total;
+  size_t cursor, slow, mid, key_a, key_b, val_b, total;
 };
 
 static size_t align_up(size_t x) { return (x + 255) & ~size_t(255); }
@@ -70,10 +70,11 @@ static bool make_layout(int32_t n, int64_t capacity, const gs_camera &cam, SortL
     return o;
   };
   L.diff = take(4 * size_t(L.TX + 1) * (L.TY + 1));
-  L.misc = take(64);  // [1] P, [2] overflow, [3] slow-list length
+  L.misc = take(64);  // [1] P, [2] overflow, [3] slow-list length, [4] mid-list length
   L.zero_end = off;
   L.cursor = take(4 * size_t(L.T));
   L.slow = take(4 * size_t(L.T));
+  L.mid = take(4 * size_t(L.T));
   const size_t cc = size_t(capacity > 0 ? capacity : 1);
   L.key_a = take(4 * cc);  // scratch of the chunked (long-segment) sort
   L.key_b = take(4 * cc);
@@ -509,6 +510,7 @@ struct TileSortArgs {
   int32_t *ids;  // sorted_idx
   uint32_t *key_a, *key_b, *val_b;
   int32_t *slow;  // [T] tiles left to k_tile_sort_big
+  int32_t *mid;   // [T] tiles of kSmallCap+1 .. kChunk entries (k_tile_sort_mid)
 };
 
 // Tiles with <= kChunk entries, one CTA each, one pass: a counting sort on
@@ -519,30 +521,34 @@ struct TileSortArgs {
 // entries).  A tile whose buckets
 // exceed kMaxBucket entries (a dense cluster of depths next to a far
 // outlier), or whose list exceeds kChunk, is appended to the slow list.
+// Two instances: kCap = kSmallCap (every tile, in launch order; more CTAs
+// per SM: half the shared memory and registers) passes longer lists to the
+// mid list, which kCap = kChunk sorts (grid-stride); longer ones, and
+// dense-bucket tiles, go to the slow list.
+#ifndef TS_SMALL
+#define TS_SMALL 2048
+#endif
+#ifndef TS_SMALL_MINB
+#define TS_SMALL_MINB 5
+#endif
+constexpr int kSmallCap = TS_SMALL;
+
+template <int kCap>
 struct BucketSmem {
-  uint32_t key[kChunk];
-  uint32_t val[kChunk];
+  uint32_t key[kCap];
+  uint32_t val[kCap];
   uint32_t cnt[kBuckets];  // counts, then bucket starts
   uint32_t sh[33];
   uint32_t red[2][kBucketThreads / 32];
   int flag;
 };
 
-__global__ void __launch_bounds__(kBucketThreads, 4) k_tile_sort(TileSortArgs a) {
-  __shared__ BucketSmem s;
-  if (a.misc[2]) return;
-  const int tile = a.order ? __ldg(a.order + blockIdx.x) : int(blockIdx.x);
-  const int2 r = reinterpret_cast<const int2 *>(a.tile_range)[tile];
-  const int n = r.y - r.x;
-  if (n <= 1) return;
-  if (n > kChunk) {
-    if (threadIdx.x == 0) a.slow[atomicAdd(&a.misc[3], 1u)] = tile;
-    return;
-  }
+template <int kCap>
+__device__ __forceinline__ void tile_sort_one(const TileSortArgs &a, BucketSmem<kCap> &s, int tile, int2 r, int n) {
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   for (int b = threadIdx.x; b < kBuckets; b += kBucketThreads) s.cnt[b] = 0u;
   if (threadIdx.x == 0) s.flag = 0;
-  constexpr int kIt = kChunk / kBucketThreads;
+  constexpr int kIt = kCap / kBucketThreads;
   const int items = (n + kBucketThreads - 1) / kBucketThreads;
   uint32_t key[kIt], val[kIt];
   uint32_t kmin = 0xffffffffu, kmax = 0u;
@@ -633,6 +639,37 @@ __global__ void __launch_bounds__(kBucketThreads, 4) k_tile_sort(TileSortArgs a)
       }
       a.ids[r.x + b0 + rank] = int32_t(val[k]);
     }
+  }
+}
+
+__global__ void __launch_bounds__(kBucketThreads, TS_SMALL_MINB) k_tile_sort(TileSortArgs a) {
+  __shared__ BucketSmem<kSmallCap> s;
+  if (a.misc[2]) return;
+  const int tile = a.order ? __ldg(a.order + blockIdx.x) : int(blockIdx.x);
+  const int2 r = reinterpret_cast<const int2 *>(a.tile_range)[tile];
+  const int n = r.y - r.x;
+  if (n <= 1) return;
+  if (n > kSmallCap) {
+    if (threadIdx.x == 0) {
+      if (n > kChunk)
+        a.slow[atomicAdd(&a.misc[3], 1u)] = tile;
+      else
+        a.mid[atomicAdd(&a.misc[4], 1u)] = tile;
+    }
+    return;
+  }
+  tile_sort_one<kSmallCap>(a, s, tile, r, n);
+}
+
+__global__ void __launch_bounds__(kBucketThreads, 4) k_tile_sort_mid(TileSortArgs a) {
+  __shared__ BucketSmem<kChunk> s;
+  if (a.misc[2]) return;
+  const int nmid = int(a.misc[4]);
+  for (int q = blockIdx.x; q < nmid; q += gridDim.x) {
+    const int tile = a.mid[q];
+    const int2 r = reinterpret_cast<const int2 *>(a.tile_range)[tile];
+    tile_sort_one<kChunk>(a, s, tile, r, r.y - r.x);
+    __syncthreads();  // the shared buffers are reused by the next tile
   }
 }
 
@@ -801,8 +838,9 @@ extern "C" int gs_bin_sort(gs_proj pr, int32_t n, gs_camera cam, void *ws, size_
     k_emit<<<(n + per_block - 1) / per_block, kEmitThreads, emit_bytes, s>>>(
         pr.tiles_touched, rect, n, L.TX, L.TY, U(L.cursor), misc, sorted_idx);
     TileSortArgs a{pr.depth, tile_range, tile_order, misc, L.T, sorted_idx, U(L.key_a), U(L.key_b), U(L.val_b),
-                   reinterpret_cast<int32_t *>(U(L.slow))};
+                   reinterpret_cast<int32_t *>(U(L.slow)), reinterpret_cast<int32_t *>(U(L.mid))};
     k_tile_sort<<<L.T, kBucketThreads, 0, s>>>(a);
+    k_tile_sort_mid<<<std::min(L.T, 4 * kBigBlocks), kBucketThreads, 0, s>>>(a);
     k_tile_sort_big<<<std::min(L.T, kBigBlocks), kSortThreads, 0, s>>>(a);
   }
   return check_launch("gs_bin_sort");

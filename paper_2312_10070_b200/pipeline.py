@@ -350,9 +350,9 @@ class MapStep:
 
 def kernels_per_view(cam, loss=True, bwd=True):
     """Kernels of ours per view (the sort's memset is a copy-engine node, not a kernel):
-    project 1; bin_sort: prep, tile counts, emit, tile sort, long-list sort = 5;
+    project 1; bin_sort: prep, tile counts, emit, tile sort, mid-list sort, long-list sort = 6;
     render 1 + backward tile order 1; loss 3; backward 2."""
-    n = 1 + 5 + 2
+    n = 1 + 6 + 2
     if loss:
         n += 3
     if bwd:
