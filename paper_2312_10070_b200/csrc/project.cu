@@ -19,7 +19,10 @@ struct CamD {
   double fx, fy, cx, cy, zn, zf;
 };
 
-__global__ void __launch_bounds__(256) k_project(gs_params p, const gs_view *__restrict__ view,
+#ifndef PROJ_MINB
+#define PROJ_MINB 4
+#endif
+__global__ void __launch_bounds__(256, PROJ_MINB) k_project(gs_params p, const gs_view *__restrict__ view,
                                                  CamD cam, int TX, int TY, gs_proj out,
                                                  gs_counters *cnt) {
   // the view, promoted to fp64 once per block (exact)

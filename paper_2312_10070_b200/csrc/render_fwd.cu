@@ -45,6 +45,9 @@ struct FwdArgs {
 // Forward geometry: NP fp32x2 pixel pairs per thread on WX-wide warp blocks.
 //   NP = 1, WX = 8:  4 warps on 8x8 blocks, 2 px / thread
 //   NP = 2, WX = 16: 2 warps on 16x8 strips, 4 px / thread
+#ifndef FWD_MINB
+#define FWD_MINB 1
+#endif
 constexpr int kFNP = FWD_NP;
 constexpr int kFWX = FWD_WX;
 using FG = Geo<2 * kFNP, kFWX>;
@@ -115,7 +118,7 @@ __device__ __forceinline__ void fwd_entry(FwdPix s[kFNP], const float2 e[kFNP], 
 }
 
 template <bool kStats, bool kL1 = false>
-__global__ void __launch_bounds__(FG::kThreads, 1) k_render_fwd(FwdArgs a) {
+__global__ void __launch_bounds__(FG::kThreads, FWD_MINB) k_render_fwd(FwdArgs a) {
   // one staged record per entry; record kBatch is a sentinel entry whose exponent is -inf
   __shared__ FwdRec s_rec[kBatch + 1];
   __shared__ unsigned char s_mask[kBatch];
