@@ -373,6 +373,8 @@ class TrackingLoop:
         is computed per iteration; else gs_loss runs after the forward."""
         self.masked = masked
         self.fused_loss = fused_loss
+        self.reuse_order = True  # launch orders from the previous iteration (scheduling only)
+        self.order_every = 8     # ... refreshed from the forward's work every 8 iterations
         self.params = params
         self.r = Rasterizer(params.n, cam, device=device)
         self.tc, self.td = tgt_color, tgt_depth
@@ -395,11 +397,12 @@ class TrackingLoop:
         if self.masked is None and self.fused_loss:
             self.r.loss_scales(self.td, self.lc, self.ld)
 
-    def iteration(self):
+    def iteration(self, i=0):
         r = self.r
         if self.masked is None and self.fused_loss:
             # S1-S3 with the L1 gradient maps written by the forward (gs_render_fwd_l1)
-            r.forward_l1(self.params, self.view, self.tc, self.td)
+            r.forward_l1(self.params, self.view, self.tc, self.td, reuse_order=self.reuse_order,
+                         refresh_order=not self.reuse_order or i % self.order_every == 0)
         else:
             r.forward(self.params, self.view)
             if self.masked is None:
@@ -427,8 +430,8 @@ class TrackingLoop:
         g = torch.cuda.CUDAGraph()
         with torch.cuda.graph(g):
             self.prepare()  # once per target frame, inside the timed graph
-            for _ in range(self.iters):
-                self.iteration()
+            for i in range(self.iters):
+                self.iteration(i)
         self.graph = g
         return g
 
@@ -436,8 +439,8 @@ class TrackingLoop:
         self.reset()
         if self.graph is None:
             self.prepare()
-            for _ in range(self.iters):
-                self.iteration()
+            for i in range(self.iters):
+                self.iteration(i)
         else:
             self.graph.replay()
 

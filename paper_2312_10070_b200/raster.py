@@ -364,7 +364,8 @@ class Rasterizer:
         self.tile_range = torch.empty(self.T, 2, dtype=torch.int32, device=device)
         self.tile_order = torch.empty(self.T, dtype=torch.int32, device=device)
         self.tile_work = torch.empty(self.T, dtype=torch.int32, device=device)
-        self.bwd_order = torch.empty(self.T, dtype=torch.int32, device=device)
+        # a valid launch order from the start (forward_l1(reuse_order=True) may launch with it)
+        self.bwd_order = torch.arange(self.T, dtype=torch.int32, device=device)
         self.n_pairs = torch.zeros(1, dtype=torch.int64, device=device)
         self.counters = torch.zeros(4, dtype=torch.int64, device=device)
         self.frame = Frame(H, W, device)
@@ -458,16 +459,25 @@ class Rasterizer:
         gs_loss_from_tiles(self.cam, self.loss_part, scales, lambda_color, lambda_depth, self.loss)
         return self.loss
 
-    def forward_l1(self, params: Params, view, tgt_color, tgt_depth):
+    def forward_l1(self, params: Params, view, tgt_color, tgt_depth, reuse_order=False, refresh_order=True):
         """S1-S3 with the L1 gradient maps fused into the forward
         (gs_render_fwd_l1, scales from loss_scales): self.dL_dcolor /
-        self.dL_ddepth hold gs_loss's maps; no loss value."""
+        self.dL_ddepth hold gs_loss's maps; no loss value.  reuse_order: the
+        forward is launched in the previous call's work order (tracking: the
+        pose moves little between iterations) and gs_bin_sort skips its own
+        launch order; refresh_order=False keeps the previous work order for
+        the backward too; launch orders never change results."""
         self.project(params, view)
-        self.bin_sort()
+        if reuse_order:
+            gs_bin_sort(self.proj, self.n, self.cam, self.sort_ws, self.capacity, self.sorted_idx, self.tile_range,
+                        self.n_pairs, self.counters, tile_order=None)
+        else:
+            self.bin_sort()
         gs_render_fwd_l1(self.proj, self.sorted_idx, self.tile_range, self.cam, self.frame, tgt_color, tgt_depth,
-                         self.scales, self.dL_dcolor, self.dL_ddepth, tile_order=self.tile_order,
-                         tile_work=self.tile_work)
-        gs_tile_order(self.tile_work, self.T, self.bwd_order)
+                         self.scales, self.dL_dcolor, self.dL_ddepth,
+                         tile_order=self.bwd_order if reuse_order else self.tile_order, tile_work=self.tile_work)
+        if refresh_order or not reuse_order:
+            gs_tile_order(self.tile_work, self.T, self.bwd_order)
         return self.frame
 
     def compute_loss(self, tgt_color, tgt_depth, weight=None, lambda_color=1.0, lambda_depth=1.0, ssim=0.0):
