@@ -74,9 +74,11 @@ __device__ void se3_exp_d(const double *xi, double *R, double *t) {
     B = 0.5 - th2 / 24.0;
     Cc = 1.0 / 6.0 - th2 / 120.0;
   } else {
-    A = sin(th) / th;
-    B = (1.0 - cos(th)) / th2;
-    Cc = (th - sin(th)) / (th2 * th);
+    double sn, cs;
+    sincos(th, &sn, &cs);
+    A = sn / th;
+    B = (1.0 - cs) / th2;
+    Cc = (th - sn) / (th2 * th);
   }
   double V[9];
   for (int i = 0; i < 9; ++i) {
@@ -170,12 +172,13 @@ __global__ void __launch_bounds__(kPoseThreads) k_pose_grad(PoseArgs a) {
     const double stp = double(a.adam[12]) + 1.0;
     a.adam[12] = float(stp);
     double d[6];
+    const double c1 = 1.0 - pow(b1, stp), c2 = 1.0 - pow(b2, stp);  // bias corrections, once
     for (int i = 0; i < 6; ++i) {
       const double m = b1 * double(a.adam[i]) + (1.0 - b1) * tw[i];
       const double v = b2 * double(a.adam[6 + i]) + (1.0 - b2) * tw[i] * tw[i];
       a.adam[i] = float(m);
       a.adam[6 + i] = float(v);
-      const double mh = m / (1.0 - pow(b1, stp)), vh = v / (1.0 - pow(b2, stp));
+      const double mh = m / c1, vh = v / c2;
       d[i] = -(i < 3 ? double(a.step.lr_trans) : double(a.step.lr_rot)) * mh / (sqrt(vh) + eps);
     }
     double dR[9], dt[3], R2[9], t2[3];
