@@ -241,12 +241,19 @@ int gs_render_fwd(gs_proj pr, const int32_t *sorted_idx, const int32_t *tile_ran
  *   dL_dcolor [3][H][W], dL_ddepth [H][W] (device) written
  *   loss_part (device, nullable) [T][2] fp64: per tile, sum |C^ - C*| over
  *             its pixels and channels, sum |D^ - D*| over its valid pixels
- *             (fixed order); gs_loss_from_tiles turns them into the loss. */
+ *             (fixed order); gs_loss_from_tiles turns them into the loss.
+ *   tile_done (device, nullable) [T] uint32, zero on first use: per-tile
+ *             completion flags for the NEXT call on the stream being a
+ *             gs_render_bwd with the same tile_done (it then starts while
+ *             this forward finishes, each tile after its own forward tile;
+ *             the backward re-arms the flags).  Every call given tile_done
+ *             must be followed by exactly one such backward. */
 int gs_render_fwd_l1(gs_proj pr, const int32_t *sorted_idx, const int32_t *tile_range,
                      const int32_t *tile_order, gs_camera cam, float *color, float *depth,
                      float *alpha, float *T_final, int32_t *n_contrib, int32_t *tile_work,
                      const float *tgt_color, const float *tgt_depth, const float *scales,
-                     float *dL_dcolor, float *dL_ddepth, double *loss_part, void *stream);
+                     float *dL_dcolor, float *dL_ddepth, double *loss_part, uint32_t *tile_done,
+                     void *stream);
 
 /* Scheduling utility: tile ids by descending work (64 buckets of max/64, order
  * inside a bucket unspecified), e.g. from gs_render_fwd's tile_work for
@@ -470,14 +477,19 @@ int gs_unpack_rgbd(gs_camera cam, const uint8_t *rgb, const uint16_t *depth16, f
  *             in the layout of gs_params; required iff GS_GRAD_PARAMS
  *   pose_partials (device) [gs_pose_partials_count(n)][12] =
  *             (dL/dR row-major 9, dL/dt 3) per block; required iff
- *             GS_GRAD_POSE, overwritten. */
+ *             GS_GRAD_POSE, overwritten.
+ *   tile_done (device, nullable) the flags given to the immediately
+ *             preceding gs_render_fwd_l1 on this stream: the per-pixel phase
+ *             is launched as a programmatic dependent of that forward (PDL)
+ *             and each tile waits for its forward tile; NULL: ordinary
+ *             stream order. */
 int gs_render_bwd(gs_params p, const gs_view *view, gs_camera cam, gs_proj pr,
                   const int32_t *sorted_idx, const int32_t *tile_range,
                   const int32_t *tile_order, const float *T_final, const int32_t *n_contrib,
                   const float *dL_dcolor, const float *dL_ddepth,
                   const float *dL_dalpha, uint32_t flags, void *ws, size_t ws_bytes,
                   float *g_mean_opa, float *g_quat, float *g_logscale, float *g_rgb,
-                  float *pose_partials, void *stream);
+                  float *pose_partials, uint32_t *tile_done, void *stream);
 
 /* S6 for several views at once (mapping, Eq. 12 summed over the keyframes of
  * an iteration): for every Gaussian, the camera part of the chain

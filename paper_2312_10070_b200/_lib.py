@@ -78,7 +78,7 @@ _PROTOS = {
     "gs_loss": (C.c_int, [GsCamera, _VP, _VP, _VP, _VP, _VP, _F, _F, _VP, _SZ, _VP, _VP, _VP, _VP]),
     "gs_loss_scales": (C.c_int, [GsCamera, _VP, _F, _F, _VP, _SZ, _VP, _VP]),
     "gs_render_fwd_l1": (C.c_int, [GsProj, _VP, _VP, _VP, GsCamera, _VP, _VP, _VP, _VP, _VP, _VP, _VP, _VP, _VP, _VP,
-                                   _VP, _VP, _VP]),
+                                   _VP, _VP, _VP, _VP]),
     "gs_loss_from_tiles": (C.c_int, [GsCamera, _VP, _VP, _F, _F, _VP, _VP]),
     "gs_tracking_loss_workspace_bytes": (_SZ, [GsCamera]),
     "gs_ssim_workspace_bytes": (_SZ, [GsCamera]),
@@ -94,7 +94,7 @@ _PROTOS = {
     "gs_ssim": (C.c_int, [GsCamera, _VP, _VP, _F, _VP, _SZ, _VP, _VP, _VP]),
     "gs_tracking_loss": (C.c_int, [GsCamera, _VP, _VP, _VP, _VP, _VP, _F, _F, _VP, _SZ, _VP, _VP, _VP, _VP]),
     "gs_render_bwd": (C.c_int, [GsParams, _VP, GsCamera, GsProj, _VP, _VP, _VP, _VP, _VP, _VP, _VP, _VP, _U32, _VP,
-                                _SZ, _VP, _VP, _VP, _VP, _VP, _VP]),
+                                _SZ, _VP, _VP, _VP, _VP, _VP, _VP, _VP]),
     "gs_render_bwd_gauss_views": (C.c_int, [GsParams, _I32, C.POINTER(_VP), GsCamera, C.POINTER(_VP), C.POINTER(_VP),
                                              C.POINTER(_VP), _VP, _VP, _VP, _VP, _VP]),
     "gs_pose_grad": (C.c_int, [_VP, _VP, _I32, C.POINTER(GsPoseStep), _VP, _VP, _VP, _VP, _VP]),

@@ -38,6 +38,7 @@ struct BwdArgs {
   const float *dL_dcolor, *dL_ddepth, *dL_dalpha;
   int W, H, TX;
   float *grad2d;
+  uint32_t *tile_done;  // nullable: wait for (and re-arm) the forward's per-tile flag
 };
 
 __device__ __forceinline__ void red_add_v4(float *addr, float x, float y, float z, float w) {
@@ -235,6 +236,21 @@ __global__ void __launch_bounds__(BG::kThreads, kBwdMinBlocks) k_bwd_pixels(BwdA
   __shared__ int s_lmax;
   __shared__ float s_red[BG::kWarps][Slab<kParams>::SIZE];  // per-warp reduction slabs (rows >= 32 are 0)
   const int tile = a.tile_order ? __ldg(a.tile_order + blockIdx.x) : int(blockIdx.x);
+  if (a.tile_done) {
+    // launched programmatically dependent on gs_render_fwd_l1: every forward
+    // CTA has started (launch_dependents), so this tile's flag is set in
+    // bounded time; the wait is capped (~0.5 s) so a misuse cannot hang
+    if (threadIdx.x == 0) {
+      uint32_t f = 0;
+      for (long long it = 0; it < (1ll << 22); ++it) {
+        asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(f) : "l"(a.tile_done + tile) : "memory");
+        if (f) break;
+        __nanosleep(100);
+      }
+      a.tile_done[tile] = 0u;  // re-armed for the next forward
+    }
+    __syncthreads();
+  }
   const int tx = tile % a.TX, ty = tile / a.TX;
   const int w = threadIdx.x >> 5;
   const PixGeom pg = pix_geom<BG>(tx, ty, a.H);
@@ -791,7 +807,7 @@ extern "C" int gs_render_bwd(gs_params p, const gs_view *view, gs_camera cam, gs
                              const int32_t *tile_range, const int32_t *tile_order, const float *T_final, const int32_t *n_contrib,
                              const float *dL_dcolor, const float *dL_ddepth, const float *dL_dalpha, uint32_t flags,
                              void *ws, size_t ws_bytes, float *g_mean_opa, float *g_quat, float *g_logscale,
-                             float *g_rgb, float *pose_partials, void *stream) {
+                             float *g_rgb, float *pose_partials, uint32_t *tile_done, void *stream) {
   using namespace gs;
   const bool want_params = flags & GS_GRAD_PARAMS, want_pose = flags & GS_GRAD_POSE;
   const bool run_pixels = !(flags & GS_BWD_GAUSS_ONLY), run_gauss = !(flags & GS_BWD_PIXELS_ONLY);
@@ -832,15 +848,25 @@ extern "C" int gs_render_bwd(gs_params p, const gs_view *view, gs_camera cam, gs
   BwdArgs b{reinterpret_cast<const double2 *>(pr.uv), reinterpret_cast<const float4 *>(pr.coef),
             reinterpret_cast<const float4 *>(pr.rgbz), reinterpret_cast<const float4 *>(pr.conic_o), sorted_idx,
             reinterpret_cast<const int2 *>(tile_range), tile_order, T_final, n_contrib, dL_dcolor, dL_ddepth, dL_dalpha,
-            cam.width, cam.height, tiles_x(cam), grad2d};
+            cam.width, cam.height, tiles_x(cam), grad2d, tile_done};
   const int T = tiles_x(cam) * tiles_y(cam);
   if (run_pixels) {
-    if (want_params)
-      dL_dalpha ? k_bwd_pixels<true, true><<<T, BG::kThreads, 0, s>>>(b)
-                : k_bwd_pixels<true, false><<<T, BG::kThreads, 0, s>>>(b);
-    else
-      dL_dalpha ? k_bwd_pixels<false, true><<<T, BG::kThreads, 0, s>>>(b)
-                : k_bwd_pixels<false, false><<<T, BG::kThreads, 0, s>>>(b);
+    void (*kern)(BwdArgs) = want_params ? (dL_dalpha ? k_bwd_pixels<true, true> : k_bwd_pixels<true, false>)
+                                        : (dL_dalpha ? k_bwd_pixels<false, true> : k_bwd_pixels<false, false>);
+    if (tile_done) {  // programmatic dependent launch: overlaps the forward's tail tile by tile
+      cudaLaunchConfig_t cfg{};
+      cfg.gridDim = dim3(T);
+      cfg.blockDim = dim3(BG::kThreads);
+      cfg.stream = s;
+      cudaLaunchAttribute attr[1];
+      attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+      attr[0].val.programmaticStreamSerializationAllowed = 1;
+      cfg.attrs = attr;
+      cfg.numAttrs = 1;
+      cudaLaunchKernelEx(&cfg, kern, b);
+    } else {
+      kern<<<T, BG::kThreads, 0, s>>>(b);
+    }
   }
   if (!run_gauss) return check_launch("gs_render_bwd");
   GaussArgs g{p, view, cam.fx, cam.fy, reinterpret_cast<const float4 *>(pr.conic_o), pr.tiles_touched, grad2d,

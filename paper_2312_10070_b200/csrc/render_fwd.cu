@@ -34,6 +34,9 @@ struct FwdArgs {
   const float *tc, *td, *scales;
   float *gC, *gD;
   double *loss_part;
+  // per-tile completion flags for a programmatically dependent backward
+  // (gs_render_bwd with the same tile_done); nullable
+  uint32_t *tile_done;
 };
 
 #ifndef FWD_NP
@@ -123,6 +126,7 @@ __global__ void __launch_bounds__(FG::kThreads, FWD_MINB) k_render_fwd(FwdArgs a
   __shared__ FwdRec s_rec[kBatch + 1];
   __shared__ unsigned char s_mask[kBatch];
   __shared__ unsigned char s_list[FG::kWarps][kBatch + 2];
+  if (kL1 && a.tile_done) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");  // the backward may launch
   const int tile = a.tile_order ? __ldg(a.tile_order + blockIdx.x) : int(blockIdx.x);
   const int tx = tile % a.TX, ty = tile / a.TX;
   const int w = threadIdx.x >> 5;
@@ -265,6 +269,11 @@ __global__ void __launch_bounds__(FG::kThreads, FWD_MINB) k_render_fwd(FwdArgs a
       a.loss_part[2 * size_t(tile) + 1] = d;
     }
   }
+  if (kL1 && a.tile_done) {  // this tile's outputs are complete: release its flag
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(a.tile_done + tile), "r"(1u) : "memory");
+  }
 }
 
 }  // namespace gs
@@ -285,7 +294,7 @@ extern "C" int gs_render_fwd(gs_proj pr, const int32_t *sorted_idx, const int32_
   FwdArgs a{reinterpret_cast<const double2 *>(pr.uv), reinterpret_cast<const float4 *>(pr.coef),
             reinterpret_cast<const float4 *>(pr.rgbz), sorted_idx, reinterpret_cast<const int2 *>(tile_range),
             tile_order, cam.width, cam.height, tiles_x(cam), color, depth, alpha, T_final, n_contrib, stats,
-            tile_work, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};
+            tile_work, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};
   const int T = tiles_x(cam) * tiles_y(cam);
   if (stats)
     k_render_fwd<true><<<T, FG::kThreads, 0, as_stream(stream)>>>(a);
@@ -298,7 +307,7 @@ extern "C" int gs_render_fwd_l1(gs_proj pr, const int32_t *sorted_idx, const int
                                 const int32_t *tile_order, gs_camera cam, float *color, float *depth, float *alpha,
                                 float *T_final, int32_t *n_contrib, int32_t *tile_work, const float *tgt_color,
                                 const float *tgt_depth, const float *scales, float *dL_dcolor, float *dL_ddepth,
-                                double *loss_part, void *stream) {
+                                double *loss_part, uint32_t *tile_done, void *stream) {
   using namespace gs;
   if (!camera_ok(cam) || !tile_range || !color || !depth || !alpha || !T_final || !n_contrib || !tgt_color ||
       !tgt_depth || !scales || !dL_dcolor || !dL_ddepth) {
@@ -313,7 +322,7 @@ extern "C" int gs_render_fwd_l1(gs_proj pr, const int32_t *sorted_idx, const int
   FwdArgs a{reinterpret_cast<const double2 *>(pr.uv), reinterpret_cast<const float4 *>(pr.coef),
             reinterpret_cast<const float4 *>(pr.rgbz), sorted_idx, reinterpret_cast<const int2 *>(tile_range),
             tile_order, cam.width, cam.height, tiles_x(cam), color, depth, alpha, T_final, n_contrib, nullptr,
-            tile_work, tgt_color, tgt_depth, scales, dL_dcolor, dL_ddepth, loss_part};
+            tile_work, tgt_color, tgt_depth, scales, dL_dcolor, dL_ddepth, loss_part, tile_done};
   const int T = tiles_x(cam) * tiles_y(cam);
   k_render_fwd<false, true><<<T, FG::kThreads, 0, as_stream(stream)>>>(a);
   return check_launch("gs_render_fwd_l1");

@@ -375,6 +375,7 @@ class TrackingLoop:
         self.fused_loss = fused_loss
         self.reuse_order = True  # launch orders from the previous iteration (scheduling only)
         self.order_every = 8     # ... refreshed from the forward's work every 8 iterations
+        self.overlap = True      # the backward starts tile by tile as the forward finishes (PDL)
         self.params = params
         self.r = Rasterizer(params.n, cam, device=device)
         self.tc, self.td = tgt_color, tgt_depth
@@ -402,14 +403,14 @@ class TrackingLoop:
         if self.masked is None and self.fused_loss:
             # S1-S3 with the L1 gradient maps written by the forward (gs_render_fwd_l1)
             r.forward_l1(self.params, self.view, self.tc, self.td, reuse_order=self.reuse_order,
-                         refresh_order=not self.reuse_order or i % self.order_every == 0)
+                         refresh_order=not self.reuse_order or i % self.order_every == 0, overlap=self.overlap)
         else:
             r.forward(self.params, self.view)
             if self.masked is None:
                 r.compute_loss(self.tc, self.td, None, self.lc, self.ld)
             else:
                 r.compute_tracking_loss(self.tc, self.td, *self.masked)
-        r.backward(self.params, self.view, GS_GRAD_POSE)
+        r.backward(self.params, self.view, GS_GRAD_POSE, overlap=self.overlap and self.masked is None and self.fused_loss)
         r.pose_grad(self.view, self.stepcfg, self.adam, dL_dtwist=self.dtwist)
 
     def reset(self):

@@ -157,11 +157,12 @@ def gs_render_fwd(proj: Proj, sorted_idx, tile_range, cam: GsCamera, frame: Fram
 
 
 def gs_render_fwd_l1(proj: Proj, sorted_idx, tile_range, cam: GsCamera, frame: Frame, tgt_color, tgt_depth, scales,
-                     dL_dcolor, dL_ddepth, stream=None, tile_order=None, tile_work=None, loss_part=None):
+                     dL_dcolor, dL_ddepth, stream=None, tile_order=None, tile_work=None, loss_part=None,
+                     tile_done=None):
     check(lib().gs_render_fwd_l1(proj.c(), _p(sorted_idx), _p(tile_range), _p(tile_order), cam, _p(frame.color),
                                  _p(frame.depth), _p(frame.alpha), _p(frame.T_final), _p(frame.n_contrib),
                                  _p(tile_work), _p(tgt_color), _p(tgt_depth), _p(scales), _p(dL_dcolor),
-                                 _p(dL_ddepth), _p(loss_part), _stream(stream)), "gs_render_fwd_l1")
+                                 _p(dL_ddepth), _p(loss_part), _p(tile_done), _stream(stream)), "gs_render_fwd_l1")
 
 
 def gs_loss_from_tiles(cam: GsCamera, loss_part, scales, lambda_color, lambda_depth, loss, stream=None):
@@ -305,7 +306,7 @@ class Optimizer:
 
 def gs_render_bwd(params: Params, view, cam: GsCamera, proj: Proj, sorted_idx, tile_range, T_final, n_contrib,
                   dL_dcolor, dL_ddepth, dL_dalpha, flags, ws, grads: Grads = None, pose_partials=None,
-                  stream=None, event_pair=None, tile_order=None):
+                  stream=None, event_pair=None, tile_order=None, tile_done=None):
     """event_pair: optional (start, end) torch.cuda.Event recorded around the call."""
     g = grads
     if event_pair is not None:
@@ -316,7 +317,7 @@ def gs_render_bwd(params: Params, view, cam: GsCamera, proj: Proj, sorted_idx, t
                               ws.numel() * ws.element_size(),
                               _p(g.mean_opa) if g is not None else None, _p(g.quat) if g is not None else None,
                               _p(g.logscale) if g is not None else None, _p(g.rgb) if g is not None else None,
-                              _p(pose_partials), _stream(stream)), "gs_render_bwd")
+                              _p(pose_partials), _p(tile_done), _stream(stream)), "gs_render_bwd")
     if event_pair is not None:
         event_pair[1].record(torch.cuda.current_stream() if stream is None else stream)
 
@@ -376,6 +377,7 @@ class Rasterizer:
         self.tl_ws = None  # gs_tracking_loss workspace, allocated on first use
         self.scales = None  # gs_loss_scales output (forward_l1)
         self.loss_part = None  # per-tile |residual| sums (render_l1)
+        self.tile_done = None  # per-tile forward -> backward flags (overlap)
         self.tl_loss = None
         self.dL_dcolor = torch.zeros(3, H, W, dtype=torch.float32, device=device)
         self.dL_ddepth = torch.zeros(H, W, dtype=torch.float32, device=device)
@@ -459,14 +461,22 @@ class Rasterizer:
         gs_loss_from_tiles(self.cam, self.loss_part, scales, lambda_color, lambda_depth, self.loss)
         return self.loss
 
-    def forward_l1(self, params: Params, view, tgt_color, tgt_depth, reuse_order=False, refresh_order=True):
+    def _tile_done(self):
+        if self.tile_done is None:
+            self.tile_done = torch.zeros(self.T, dtype=torch.int32, device=self.device)
+        return self.tile_done
+
+    def forward_l1(self, params: Params, view, tgt_color, tgt_depth, reuse_order=False, refresh_order=True,
+                   overlap=False):
         """S1-S3 with the L1 gradient maps fused into the forward
         (gs_render_fwd_l1, scales from loss_scales): self.dL_dcolor /
         self.dL_ddepth hold gs_loss's maps; no loss value.  reuse_order: the
         forward is launched in the previous call's work order (tracking: the
         pose moves little between iterations) and gs_bin_sort skips its own
         launch order; refresh_order=False keeps the previous work order for
-        the backward too; launch orders never change results."""
+        the backward too; launch orders never change results.  overlap: the
+        next backward(overlap=True) starts while this forward finishes, tile
+        by tile (per-tile flags + programmatic dependent launch)."""
         self.project(params, view)
         if reuse_order:
             gs_bin_sort(self.proj, self.n, self.cam, self.sort_ws, self.capacity, self.sorted_idx, self.tile_range,
@@ -475,7 +485,8 @@ class Rasterizer:
             self.bin_sort()
         gs_render_fwd_l1(self.proj, self.sorted_idx, self.tile_range, self.cam, self.frame, tgt_color, tgt_depth,
                          self.scales, self.dL_dcolor, self.dL_ddepth,
-                         tile_order=self.bwd_order if reuse_order else self.tile_order, tile_work=self.tile_work)
+                         tile_order=self.bwd_order if reuse_order else self.tile_order, tile_work=self.tile_work,
+                         tile_done=self._tile_done() if overlap else None)
         if refresh_order or not reuse_order:
             gs_tile_order(self.tile_work, self.T, self.bwd_order)
         return self.frame
@@ -507,12 +518,13 @@ class Rasterizer:
         return self.tl_loss
 
     def backward(self, params: Params, view, flags=GS_GRAD_PARAMS, grads: Grads = None, dL_dcolor=None,
-                 dL_ddepth=None, dL_dalpha=None, event_pair=None):
+                 dL_ddepth=None, dL_dalpha=None, event_pair=None, overlap=False):
+        """overlap: right after forward_l1(overlap=True) (see there)."""
         gs_render_bwd(params, view, self.cam, self.proj, self.sorted_idx, self.tile_range, self.frame.T_final,
                       self.frame.n_contrib, self.dL_dcolor if dL_dcolor is None else dL_dcolor,
                       self.dL_ddepth if dL_ddepth is None else dL_ddepth, dL_dalpha, flags, self.bwd_ws, grads,
                       self.pose_partials if flags & GS_GRAD_POSE else None, event_pair=event_pair,
-                      tile_order=self.bwd_order)
+                      tile_order=self.bwd_order, tile_done=self._tile_done() if overlap else None)
 
     def pose_grad(self, view, step=None, adam_state=None, dL_dview=None, dL_dtwist=None, dL_dqt=None):
         gs_pose_grad(view, self.pose_partials, self.n_partials, step, adam_state, dL_dview, dL_dtwist, dL_dqt)

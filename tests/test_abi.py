@@ -62,7 +62,7 @@ def test_invalid_arguments_rejected_on_host():
     assert L.gs_loss(cam, None, None, None, None, None, 1.0, 1.0, None, 0, None, None, None, None) == _lib.GS_ERR_INVALID_ARG
     assert L.gs_render_bwd(p, C.c_void_p(16), cam, pr, None, C.c_void_p(16), None, C.c_void_p(16), C.c_void_p(16),
                            C.c_void_p(16), C.c_void_p(16), None, 0, None, 0, None, None, None, None, None,
-                           None) == _lib.GS_ERR_INVALID_ARG  # flags = 0
+                           None, None) == _lib.GS_ERR_INVALID_ARG  # flags = 0
     assert L.gs_pose_grad(None, None, 0, None, None, None, None, None, None) == _lib.GS_ERR_INVALID_ARG
 
 

@@ -93,3 +93,53 @@ def test_fused_tracking_follows_unfused():
         views.append(loop.view.cpu().numpy())
     # same gradient maps; only the fp32 atomic order of the backward differs
     assert np.allclose(views[0], views[1], rtol=0, atol=2e-5), views
+
+
+def test_overlapped_backward_matches_and_rearms_flags():
+    """forward_l1(overlap) -> backward(overlap): the per-pixel backward is a
+    programmatic dependent of the forward and waits per tile; the gradients
+    equal the stream-ordered path's (up to fp32 atomic order) and every tile
+    flag is re-armed (0) afterwards; repeated pairs stay correct."""
+    from paper_2312_10070_b200 import GS_GRAD_PARAMS, Grads
+    s = inputs.config1()
+    P = Params.from_numpy(*s.params(), device=DEV)
+    v = torch.as_tensor(s.views[0], device=DEV)
+    r = Rasterizer(s.n, s.cam, device=DEV)
+    r.size_for(P, v)
+    rng = np.random.default_rng(3)
+    H, W = s.cam.height, s.cam.width
+    tc = torch.as_tensor(rng.uniform(0, 1, (3, H, W)).astype(np.float32), device=DEV)
+    td = torch.as_tensor(rng.uniform(0.5, 5, (H, W)).astype(np.float32), device=DEV)
+    r.loss_scales(td)
+    ref = Grads.zeros(s.n, DEV)
+    r.forward_l1(P, v, tc, td)
+    r.backward(P, v, GS_GRAD_PARAMS, ref)
+    for _ in range(3):
+        g = Grads.zeros(s.n, DEV)
+        r.forward_l1(P, v, tc, td, overlap=True)
+        r.backward(P, v, GS_GRAD_PARAMS, g, overlap=True)
+        torch.cuda.synchronize()
+        assert int(r.tile_done.abs().sum()) == 0
+        scale = ref.buf.abs().max().item()
+        assert torch.allclose(g.buf, ref.buf, rtol=1e-4, atol=1e-6 * scale)
+
+
+def test_overlapped_tracking_follows_stream_ordered():
+    from paper_2312_10070_b200.pipeline import TrackingLoop
+    s = inputs.config2(n=40_000)
+    P = Params.from_numpy(*s.params(), device=DEV)
+    gt = torch.as_tensor(s.extra["gt_view"], device=DEV)
+    r = Rasterizer(s.n, s.cam, device=DEV)
+    r.size_for(P, gt)
+    r.forward(P, gt)
+    tc, td = r.frame.color.clone(), r.frame.depth.clone()
+    views = []
+    for overlap in (True, False):
+        loop = TrackingLoop(P, s.cam, tc, td, torch.as_tensor(s.extra["start_view"], device=DEV), iters=10)
+        loop.overlap = overlap
+        loop.size()
+        loop.capture()
+        loop.run()
+        torch.cuda.synchronize()
+        views.append(loop.view.cpu().numpy())
+    assert np.allclose(views[0], views[1], rtol=0, atol=2e-5), views
