@@ -162,6 +162,7 @@ __device__ __forceinline__ unsigned peer_mask(unsigned act, uint32_t d) {
 __global__ void __launch_bounds__(256) k_bin_prep(const int32_t *__restrict__ tiles_touched,
                                                   const short4 *__restrict__ rect, int n, int TX, int TY,
                                                   uint32_t *diff) {
+  pdl_begin();
   extern __shared__ uint32_t s_diff[];
   const int W1 = TX + 1, cells = W1 * (TY + 1);
   for (int i = threadIdx.x; i < cells; i += blockDim.x) s_diff[i] = 0;
@@ -199,6 +200,7 @@ struct TileArgs {
 };
 
 __global__ void __launch_bounds__(1024) k_tile_counts(TileArgs a) {
+  pdl_begin();
   extern __shared__ uint32_t s_c[];  // (TY+1) x (TX+1)
   __shared__ uint32_t sh[33];
   __shared__ int s_max;
@@ -278,6 +280,7 @@ __global__ void __launch_bounds__(kEmitThreads) k_emit(const int32_t *__restrict
                                                        const short4 *__restrict__ rect, int n, int TX, int TY,
                                                        uint32_t *cursor, const uint32_t *__restrict__ misc,
                                                        int32_t *ids) {
+  pdl_begin();
   extern __shared__ uint32_t s_e[];  // [(TY+1)(TX+1)] diff -> counts -> cursors, [T] bases
   if (misc[2]) return;               // overflow: leave sorted_idx untouched
   const int W1 = TX + 1, cells = W1 * (TY + 1), T = TX * TY;
@@ -643,6 +646,7 @@ __device__ __forceinline__ void tile_sort_one(const TileSortArgs &a, BucketSmem<
 }
 
 __global__ void __launch_bounds__(kBucketThreads, TS_SMALL_MINB) k_tile_sort(TileSortArgs a) {
+  pdl_begin();
   __shared__ BucketSmem<kSmallCap> s;
   if (a.misc[2]) return;
   const int tile = a.order ? __ldg(a.order + blockIdx.x) : int(blockIdx.x);
@@ -662,6 +666,7 @@ __global__ void __launch_bounds__(kBucketThreads, TS_SMALL_MINB) k_tile_sort(Til
 }
 
 __global__ void __launch_bounds__(kBucketThreads, 4) k_tile_sort_mid(TileSortArgs a) {
+  pdl_begin();
   __shared__ BucketSmem<kChunk> s;
   if (a.misc[2]) return;
   const int nmid = int(a.misc[4]);
@@ -679,6 +684,7 @@ __global__ void __launch_bounds__(kBucketThreads, 4) k_tile_sort_mid(TileSortArg
 // digit counters), digit bases carried across chunks from a per-pass
 // histogram.
 __global__ void __launch_bounds__(kSortThreads) k_tile_sort_big(TileSortArgs a) {
+  pdl_begin();
   __shared__ SortSmem s;
   if (a.misc[2]) return;
   const int nslow = int(a.misc[3]);
@@ -743,6 +749,9 @@ __global__ void __launch_bounds__(kSortThreads) k_tile_sort_big(TileSortArgs a) 
 
 // Tiles by descending work, 64 buckets of max/64 (single CTA).
 __global__ void __launch_bounds__(1024) k_order_by_work(const int32_t *__restrict__ work, int T, int32_t *order) {
+  // no early trigger: a backward launched after this kernel with tile_done
+  // does not wait for its predecessor grid, and it reads this order
+  pdl_wait();
   __shared__ int s_max;
   __shared__ unsigned s_b[64];
   if (threadIdx.x == 0) s_max = 0;
@@ -777,7 +786,7 @@ extern "C" int gs_tile_order(const int32_t *work, int32_t T, int32_t *order, voi
     set_error("gs_tile_order: invalid argument");
     return GS_ERR_INVALID_ARG;
   }
-  k_order_by_work<<<1, 1024, 0, as_stream(stream)>>>(work, T, order);
+  launch_pdl(k_order_by_work, dim3(1), dim3(1024), 0, as_stream(stream), work, T, order);
   return check_launch("gs_tile_order");
 }
 
@@ -827,21 +836,21 @@ extern "C" int gs_bin_sort(gs_proj pr, int32_t n, gs_camera cam, void *ws, size_
   }
   if (n > 0) {
     const int blocks = std::max(1, std::min(2 * 148, (n + 255) / 256));
-    k_bin_prep<<<blocks, 256, diff_bytes, s>>>(pr.tiles_touched, rect, n, L.TX, L.TY, U(L.diff));
+    launch_pdl(k_bin_prep, dim3(blocks), dim3(256), diff_bytes, s, pr.tiles_touched, rect, n, L.TX, L.TY, U(L.diff));
   }
   {
     TileArgs a{U(L.diff), L.TX, L.TY, L.T, capacity, tile_range, tile_order, U(L.cursor), n_pairs, misc, cnt};
-    k_tile_counts<<<1, 1024, diff_bytes, s>>>(a);
+    launch_pdl(k_tile_counts, dim3(1), dim3(1024), diff_bytes, s, a);
   }
   if (n > 0 && capacity > 0) {
     const int per_block = kEmitThreads * kEmitPer;
-    k_emit<<<(n + per_block - 1) / per_block, kEmitThreads, emit_bytes, s>>>(
+    launch_pdl(k_emit, dim3((n + per_block - 1) / per_block), dim3(kEmitThreads), emit_bytes, s,
         pr.tiles_touched, rect, n, L.TX, L.TY, U(L.cursor), misc, sorted_idx);
     TileSortArgs a{pr.depth, tile_range, tile_order, misc, L.T, sorted_idx, U(L.key_a), U(L.key_b), U(L.val_b),
                    reinterpret_cast<int32_t *>(U(L.slow)), reinterpret_cast<int32_t *>(U(L.mid))};
-    k_tile_sort<<<L.T, kBucketThreads, 0, s>>>(a);
-    k_tile_sort_mid<<<std::min(L.T, 4 * kBigBlocks), kBucketThreads, 0, s>>>(a);
-    k_tile_sort_big<<<std::min(L.T, kBigBlocks), kSortThreads, 0, s>>>(a);
+    launch_pdl(k_tile_sort, dim3(L.T), dim3(kBucketThreads), 0, s, a);
+    launch_pdl(k_tile_sort_mid, dim3(std::min(L.T, 4 * kBigBlocks)), dim3(kBucketThreads), 0, s, a);
+    launch_pdl(k_tile_sort_big, dim3(std::min(L.T, kBigBlocks)), dim3(kSortThreads), 0, s, a);
   }
   return check_launch("gs_bin_sort");
 }

@@ -102,6 +102,7 @@ struct PoseArgs {
 constexpr int kPoseThreads = 384;  // 32 record lanes x 12 components
 
 __global__ void __launch_bounds__(kPoseThreads) k_pose_grad(PoseArgs a) {
+  pdl_begin();
   // fixed-order fp64 reduction of the [n][12] partials: thread t owns
   // component c = t % 12 of the records k = t / 12 (mod 32) -> consecutive
   // threads read consecutive floats (coalesced); then the 32 lane sums of
@@ -211,6 +212,6 @@ extern "C" int gs_pose_grad(gs_view *view, const float *pose_partials, int32_t n
   }
   PoseArgs a{view, pose_partials, n_partials, step != nullptr, step ? *step : gs_pose_step{0, 0, 0, 0, 1},
              adam_state, dL_dview, dL_dtwist, dL_dqt};
-  k_pose_grad<<<1, kPoseThreads, 0, as_stream(stream)>>>(a);
+  launch_pdl(k_pose_grad, dim3(1), dim3(kPoseThreads), 0, as_stream(stream), a);
   return check_launch("gs_pose_grad");
 }

@@ -25,6 +25,7 @@ struct CamD {
 __global__ void __launch_bounds__(256, PROJ_MINB) k_project(gs_params p, const gs_view *__restrict__ view,
                                                  CamD cam, int TX, int TY, gs_proj out,
                                                  gs_counters *cnt) {
+  pdl_begin();
   // the view, promoted to fp64 once per block (exact)
   __shared__ ViewD sV;
   if (threadIdx.x < 12) {
@@ -187,6 +188,7 @@ extern "C" int gs_project(gs_params p, const gs_view *view, gs_camera cam, gs_pr
   const int threads = 256;
   const int blocks = (p.n + threads - 1) / threads;
   const CamD cd{cam.fx, cam.fy, cam.cx, cam.cy, cam.z_near, cam.z_far};
-  k_project<<<blocks, threads, 0, as_stream(stream)>>>(p, view, cd, tiles_x(cam), tiles_y(cam), out, cnt);
+  launch_pdl(k_project, dim3(blocks), dim3(threads), 0, as_stream(stream), p, view, cd, tiles_x(cam), tiles_y(cam),
+             out, cnt);
   return check_launch("gs_project");
 }

@@ -235,6 +235,10 @@ __global__ void __launch_bounds__(BG::kThreads, kBwdMinBlocks) k_bwd_pixels(BwdA
   __shared__ unsigned char s_list[BG::kWarps][kBatch + 2];
   __shared__ int s_lmax;
   __shared__ float s_red[BG::kWarps][Slab<kParams>::SIZE];  // per-warp reduction slabs (rows >= 32 are 0)
+  // with tile_done the forward's per-tile flags order this kernel after its
+  // tile; else wait for the preceding grid (PDL; a no-op without it)
+  if (!a.tile_done) pdl_wait();
+  pdl_trigger();
   const int tile = a.tile_order ? __ldg(a.tile_order + blockIdx.x) : int(blockIdx.x);
   if (a.tile_done) {
     // launched programmatically dependent on gs_render_fwd_l1: every forward
@@ -412,6 +416,7 @@ struct GaussArgs {
 #endif
 template <bool kParams, bool kPose>
 __global__ void __launch_bounds__(kGaussThreads, GAUSS_MINB) k_bwd_gauss(GaussArgs a) {
+  pdl_begin();
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   float pose[12];
 #pragma unroll
@@ -853,20 +858,9 @@ extern "C" int gs_render_bwd(gs_params p, const gs_view *view, gs_camera cam, gs
   if (run_pixels) {
     void (*kern)(BwdArgs) = want_params ? (dL_dalpha ? k_bwd_pixels<true, true> : k_bwd_pixels<true, false>)
                                         : (dL_dalpha ? k_bwd_pixels<false, true> : k_bwd_pixels<false, false>);
-    if (tile_done) {  // programmatic dependent launch: overlaps the forward's tail tile by tile
-      cudaLaunchConfig_t cfg{};
-      cfg.gridDim = dim3(T);
-      cfg.blockDim = dim3(BG::kThreads);
-      cfg.stream = s;
-      cudaLaunchAttribute attr[1];
-      attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-      attr[0].val.programmaticStreamSerializationAllowed = 1;
-      cfg.attrs = attr;
-      cfg.numAttrs = 1;
-      cudaLaunchKernelEx(&cfg, kern, b);
-    } else {
-      kern<<<T, BG::kThreads, 0, s>>>(b);
-    }
+    // programmatic dependent launch (with tile_done: overlaps the forward's
+    // tail tile by tile)
+    launch_pdl(kern, dim3(T), dim3(BG::kThreads), 0, s, b);
   }
   if (!run_gauss) return check_launch("gs_render_bwd");
   GaussArgs g{p, view, cam.fx, cam.fy, reinterpret_cast<const float4 *>(pr.conic_o), pr.tiles_touched, grad2d,
@@ -875,11 +869,11 @@ extern "C" int gs_render_bwd(gs_params p, const gs_view *view, gs_camera cam, gs
               (flags & GS_BWD_ATOMIC_ACC) != 0};
   const int blocks = gs_pose_partials_count(p.n);
   if (want_params && want_pose)
-    k_bwd_gauss<true, true><<<blocks, kGaussThreads, 0, s>>>(g);
+    launch_pdl(k_bwd_gauss<true, true>, dim3(blocks), dim3(kGaussThreads), 0, s, g);
   else if (want_params)
-    k_bwd_gauss<true, false><<<blocks, kGaussThreads, 0, s>>>(g);
+    launch_pdl(k_bwd_gauss<true, false>, dim3(blocks), dim3(kGaussThreads), 0, s, g);
   else
-    k_bwd_gauss<false, true><<<blocks, kGaussThreads, 0, s>>>(g);
+    launch_pdl(k_bwd_gauss<false, true>, dim3(blocks), dim3(kGaussThreads), 0, s, g);
   return check_launch("gs_render_bwd");
 }
 

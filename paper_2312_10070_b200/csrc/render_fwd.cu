@@ -126,7 +126,7 @@ __global__ void __launch_bounds__(FG::kThreads, FWD_MINB) k_render_fwd(FwdArgs a
   __shared__ FwdRec s_rec[kBatch + 1];
   __shared__ unsigned char s_mask[kBatch];
   __shared__ unsigned char s_list[FG::kWarps][kBatch + 2];
-  if (kL1 && a.tile_done) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");  // the backward may launch
+  pdl_begin();  // (the dependent backward of gs_render_fwd_l1(tile_done) may launch now)
   const int tile = a.tile_order ? __ldg(a.tile_order + blockIdx.x) : int(blockIdx.x);
   const int tx = tile % a.TX, ty = tile / a.TX;
   const int w = threadIdx.x >> 5;
@@ -297,9 +297,9 @@ extern "C" int gs_render_fwd(gs_proj pr, const int32_t *sorted_idx, const int32_
             tile_work, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};
   const int T = tiles_x(cam) * tiles_y(cam);
   if (stats)
-    k_render_fwd<true><<<T, FG::kThreads, 0, as_stream(stream)>>>(a);
+    launch_pdl(k_render_fwd<true>, dim3(T), dim3(FG::kThreads), 0, as_stream(stream), a);
   else
-    k_render_fwd<false><<<T, FG::kThreads, 0, as_stream(stream)>>>(a);
+    launch_pdl(k_render_fwd<false>, dim3(T), dim3(FG::kThreads), 0, as_stream(stream), a);
   return check_launch("gs_render_fwd");
 }
 
@@ -324,6 +324,6 @@ extern "C" int gs_render_fwd_l1(gs_proj pr, const int32_t *sorted_idx, const int
             tile_order, cam.width, cam.height, tiles_x(cam), color, depth, alpha, T_final, n_contrib, nullptr,
             tile_work, tgt_color, tgt_depth, scales, dL_dcolor, dL_ddepth, loss_part, tile_done};
   const int T = tiles_x(cam) * tiles_y(cam);
-  k_render_fwd<false, true><<<T, FG::kThreads, 0, as_stream(stream)>>>(a);
+  launch_pdl(k_render_fwd<false, true>, dim3(T), dim3(FG::kThreads), 0, as_stream(stream), a);
   return check_launch("gs_render_fwd_l1");
 }
