@@ -202,11 +202,20 @@ int gs_project(gs_params p, const gs_view *view, gs_camera cam, gs_proj out,
  *                 then start the heaviest tiles first (no effect on results)
  *   n_pairs       (device) [1] int64 total pair count P
  *   cnt           (device) counters, nullable
+ *   sort_order    (device, nullable) [T] the per-tile sort's launch order
+ *                 (default: tile_order, else tile id); scheduling only
+ *   tile_sorted   (device, nullable) [T] uint32, zero on first use: a
+ *                 flag per tile, released once its list is sorted, for the
+ *                 NEXT call on the stream being gs_render_fwd_l1 with the same
+ *                 tile_sorted (it then starts each tile as soon as that tile
+ *                 is sorted and re-arms the flag); every call given
+ *                 tile_sorted must be followed by exactly one such forward
  * If P > capacity, n_overflow is incremented, every tile range is set empty
  * and sorted_idx is left untouched (the caller re-sizes and repeats). */
 int gs_bin_sort(gs_proj pr, int32_t n, gs_camera cam, void *ws, size_t ws_bytes,
                 int64_t capacity, int32_t *sorted_idx, int32_t *tile_range,
-                int32_t *tile_order, int64_t *n_pairs, gs_counters *cnt, void *stream);
+                int32_t *tile_order, int64_t *n_pairs, gs_counters *cnt,
+                const int32_t *sort_order, uint32_t *tile_sorted, void *stream);
 
 /* S3 — front-to-back alpha compositing (Eqs. 3, 4, 6; P:133-141, P:161-166;
  * S:129-138; R11-R15).
@@ -247,13 +256,16 @@ int gs_render_fwd(gs_proj pr, const int32_t *sorted_idx, const int32_t *tile_ran
  *             gs_render_bwd with the same tile_done (it then starts while
  *             this forward finishes, each tile after its own forward tile;
  *             the backward re-arms the flags).  Every call given tile_done
- *             must be followed by exactly one such backward. */
+ *             must be followed by exactly one such backward.
+ *   tile_sorted (device, nullable) the flags given to the immediately
+ *             preceding gs_bin_sort: each tile starts once its list is sorted
+ *             (see gs_bin_sort). */
 int gs_render_fwd_l1(gs_proj pr, const int32_t *sorted_idx, const int32_t *tile_range,
                      const int32_t *tile_order, gs_camera cam, float *color, float *depth,
                      float *alpha, float *T_final, int32_t *n_contrib, int32_t *tile_work,
                      const float *tgt_color, const float *tgt_depth, const float *scales,
                      float *dL_dcolor, float *dL_ddepth, double *loss_part, uint32_t *tile_done,
-                     void *stream);
+                     uint32_t *tile_sorted, void *stream);
 
 /* Scheduling utility: tile ids by descending work (64 buckets of max/64, order
  * inside a bucket unspecified), e.g. from gs_render_fwd's tile_work for

@@ -72,13 +72,13 @@ _PROTOS = {
     "gs_bwd_workspace_bytes": (_SZ, [_I32]),
     "gs_pose_partials_count": (_I32, [_I32]),
     "gs_project": (C.c_int, [GsParams, _VP, GsCamera, GsProj, _VP, _VP]),
-    "gs_bin_sort": (C.c_int, [GsProj, _I32, GsCamera, _VP, _SZ, _I64, _VP, _VP, _VP, _VP, _VP, _VP]),
+    "gs_bin_sort": (C.c_int, [GsProj, _I32, GsCamera, _VP, _SZ, _I64, _VP, _VP, _VP, _VP, _VP, _VP, _VP, _VP]),
     "gs_render_fwd": (C.c_int, [GsProj, _VP, _VP, _VP, GsCamera, _VP, _VP, _VP, _VP, _VP, _VP, _VP, _VP]),
     "gs_tile_order": (C.c_int, [_VP, _I32, _VP, _VP]),
     "gs_loss": (C.c_int, [GsCamera, _VP, _VP, _VP, _VP, _VP, _F, _F, _VP, _SZ, _VP, _VP, _VP, _VP]),
     "gs_loss_scales": (C.c_int, [GsCamera, _VP, _F, _F, _VP, _SZ, _VP, _VP]),
     "gs_render_fwd_l1": (C.c_int, [GsProj, _VP, _VP, _VP, GsCamera, _VP, _VP, _VP, _VP, _VP, _VP, _VP, _VP, _VP, _VP,
-                                   _VP, _VP, _VP, _VP]),
+                                   _VP, _VP, _VP, _VP, _VP]),
     "gs_loss_from_tiles": (C.c_int, [GsCamera, _VP, _VP, _F, _F, _VP, _VP]),
     "gs_tracking_loss_workspace_bytes": (_SZ, [GsCamera]),
     "gs_ssim_workspace_bytes": (_SZ, [GsCamera]),

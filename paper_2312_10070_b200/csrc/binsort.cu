@@ -514,7 +514,17 @@ struct TileSortArgs {
   uint32_t *key_a, *key_b, *val_b;
   int32_t *slow;  // [T] tiles left to k_tile_sort_big
   int32_t *mid;   // [T] tiles of kSmallCap+1 .. kChunk entries (k_tile_sort_mid)
+  uint32_t *tile_sorted;  // nullable: per-tile "list sorted" flags for a flag-waiting forward
 };
+
+// release this tile's flag once every thread's writes of its list are done
+__device__ __forceinline__ void mark_sorted(const TileSortArgs &a, int tile) {
+  if (!a.tile_sorted) return;
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0)
+    asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(a.tile_sorted + tile), "r"(1u) : "memory");
+}
 
 // Tiles with <= kChunk entries, one CTA each, one pass: a counting sort on
 // the top kBucketBits bits of (depth bits - tile min) into shared memory
@@ -547,7 +557,7 @@ struct BucketSmem {
 };
 
 template <int kCap>
-__device__ __forceinline__ void tile_sort_one(const TileSortArgs &a, BucketSmem<kCap> &s, int tile, int2 r, int n) {
+__device__ __forceinline__ bool tile_sort_one(const TileSortArgs &a, BucketSmem<kCap> &s, int tile, int2 r, int n) {
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   for (int b = threadIdx.x; b < kBuckets; b += kBucketThreads) s.cnt[b] = 0u;
   if (threadIdx.x == 0) s.flag = 0;
@@ -611,7 +621,7 @@ __device__ __forceinline__ void tile_sort_one(const TileSortArgs &a, BucketSmem<
   __syncthreads();
   if (s.flag) {  // dense buckets: exact two-key path
     if (threadIdx.x == 0) a.slow[atomicAdd(&a.misc[3], 1u)] = tile;
-    return;
+    return false;
   }
   // scatter into the buckets (unordered inside a bucket)
 #pragma unroll
@@ -643,17 +653,24 @@ __device__ __forceinline__ void tile_sort_one(const TileSortArgs &a, BucketSmem<
       a.ids[r.x + b0 + rank] = int32_t(val[k]);
     }
   }
+  return true;
 }
 
 __global__ void __launch_bounds__(kBucketThreads, TS_SMALL_MINB) k_tile_sort(TileSortArgs a) {
   pdl_begin();
   __shared__ BucketSmem<kSmallCap> s;
-  if (a.misc[2]) return;
   const int tile = a.order ? __ldg(a.order + blockIdx.x) : int(blockIdx.x);
+  if (a.misc[2]) {  // overflow: every range is empty
+    mark_sorted(a, tile);
+    return;
+  }
   const int2 r = reinterpret_cast<const int2 *>(a.tile_range)[tile];
   const int n = r.y - r.x;
-  if (n <= 1) return;
-  if (n > kSmallCap) {
+  if (n <= 1) {
+    mark_sorted(a, tile);
+    return;
+  }
+  if (n > kSmallCap) {  // k_tile_sort_mid / _big sort it (and mark it)
     if (threadIdx.x == 0) {
       if (n > kChunk)
         a.slow[atomicAdd(&a.misc[3], 1u)] = tile;
@@ -662,18 +679,22 @@ __global__ void __launch_bounds__(kBucketThreads, TS_SMALL_MINB) k_tile_sort(Til
     }
     return;
   }
-  tile_sort_one<kSmallCap>(a, s, tile, r, n);
+  if (tile_sort_one<kSmallCap>(a, s, tile, r, n)) mark_sorted(a, tile);
 }
 
+// (the mid and long-list kernels let their dependents launch BEFORE waiting
+// for their predecessor: a flag-waiting forward can then start on the tiles
+// k_tile_sort has finished; dependents that wait for the grid are unaffected)
 __global__ void __launch_bounds__(kBucketThreads, 4) k_tile_sort_mid(TileSortArgs a) {
-  pdl_begin();
+  pdl_trigger();
+  pdl_wait();
   __shared__ BucketSmem<kChunk> s;
   if (a.misc[2]) return;
   const int nmid = int(a.misc[4]);
   for (int q = blockIdx.x; q < nmid; q += gridDim.x) {
     const int tile = a.mid[q];
     const int2 r = reinterpret_cast<const int2 *>(a.tile_range)[tile];
-    tile_sort_one<kChunk>(a, s, tile, r, r.y - r.x);
+    if (tile_sort_one<kChunk>(a, s, tile, r, r.y - r.x)) mark_sorted(a, tile);
     __syncthreads();  // the shared buffers are reused by the next tile
   }
 }
@@ -684,7 +705,8 @@ __global__ void __launch_bounds__(kBucketThreads, 4) k_tile_sort_mid(TileSortArg
 // digit counters), digit bases carried across chunks from a per-pass
 // histogram.
 __global__ void __launch_bounds__(kSortThreads) k_tile_sort_big(TileSortArgs a) {
-  pdl_begin();
+  pdl_trigger();
+  pdl_wait();
   __shared__ SortSmem s;
   if (a.misc[2]) return;
   const int nslow = int(a.misc[3]);
@@ -743,8 +765,16 @@ __global__ void __launch_bounds__(kSortThreads) k_tile_sort_big(TileSortArgs a) 
     uint32_t *dst = reinterpret_cast<uint32_t *>(a.ids) + r.x;
     if (vA != dst)
       for (int i = threadIdx.x; i < n; i += kSortThreads) dst[i] = vA[i];
+    mark_sorted(a, tile);
     __syncthreads();
   }
+}
+
+// flags only (nothing to sort: no pairs or no capacity)
+__global__ void k_mark_all_sorted(uint32_t *tile_sorted, int T) {
+  pdl_begin();
+  for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < T; t += gridDim.x * blockDim.x)
+    asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(tile_sorted + t), "r"(1u) : "memory");
 }
 
 // Tiles by descending work, 64 buckets of max/64 (single CTA).
@@ -798,7 +828,7 @@ extern "C" size_t gs_binsort_workspace_bytes(int32_t n, int64_t capacity, gs_cam
 
 extern "C" int gs_bin_sort(gs_proj pr, int32_t n, gs_camera cam, void *ws, size_t ws_bytes, int64_t capacity,
                            int32_t *sorted_idx, int32_t *tile_range, int32_t *tile_order, int64_t *n_pairs,
-                           gs_counters *cnt, void *stream) {
+                           gs_counters *cnt, const int32_t *sort_order, uint32_t *tile_sorted, void *stream) {
   using namespace gs;
   if (n < 0 || !camera_ok(cam) || !tile_range || !n_pairs || capacity < 0 || (capacity > 0 && !sorted_idx)) {
     set_error("gs_bin_sort: invalid argument");
@@ -846,11 +876,14 @@ extern "C" int gs_bin_sort(gs_proj pr, int32_t n, gs_camera cam, void *ws, size_
     const int per_block = kEmitThreads * kEmitPer;
     launch_pdl(k_emit, dim3((n + per_block - 1) / per_block), dim3(kEmitThreads), emit_bytes, s,
         pr.tiles_touched, rect, n, L.TX, L.TY, U(L.cursor), misc, sorted_idx);
-    TileSortArgs a{pr.depth, tile_range, tile_order, misc, L.T, sorted_idx, U(L.key_a), U(L.key_b), U(L.val_b),
-                   reinterpret_cast<int32_t *>(U(L.slow)), reinterpret_cast<int32_t *>(U(L.mid))};
+    TileSortArgs a{pr.depth, tile_range, sort_order ? sort_order : tile_order, misc, L.T, sorted_idx, U(L.key_a),
+                   U(L.key_b), U(L.val_b), reinterpret_cast<int32_t *>(U(L.slow)),
+                   reinterpret_cast<int32_t *>(U(L.mid)), tile_sorted};
     launch_pdl(k_tile_sort, dim3(L.T), dim3(kBucketThreads), 0, s, a);
     launch_pdl(k_tile_sort_mid, dim3(std::min(L.T, 4 * kBigBlocks)), dim3(kBucketThreads), 0, s, a);
     launch_pdl(k_tile_sort_big, dim3(std::min(L.T, kBigBlocks)), dim3(kSortThreads), 0, s, a);
   }
+  else if (tile_sorted)
+    launch_pdl(k_mark_all_sorted, dim3(std::max(1, std::min(L.T / 256 + 1, 148))), dim3(256), 0, s, tile_sorted, L.T);
   return check_launch("gs_bin_sort");
 }

@@ -11,6 +11,7 @@ calls together; ``Params`` / ``Grads`` hold the four float4 SoA arrays.
 from __future__ import annotations
 
 import ctypes as C
+import os
 from dataclasses import dataclass
 
 import torch
@@ -142,10 +143,10 @@ def gs_project(params: Params, view, cam: GsCamera, proj: Proj, counters=None, s
 
 
 def gs_bin_sort(proj: Proj, n, cam: GsCamera, ws, capacity, sorted_idx, tile_range, n_pairs, counters=None,
-                stream=None, tile_order=None):
+                stream=None, tile_order=None, sort_order=None, tile_sorted=None):
     check(lib().gs_bin_sort(proj.c(), int(n), cam, _p(ws), ws.numel() * ws.element_size(), int(capacity),
                             _p(sorted_idx), _p(tile_range), _p(tile_order), _p(n_pairs), _p(counters),
-                            _stream(stream)), "gs_bin_sort")
+                            _p(sort_order), _p(tile_sorted), _stream(stream)), "gs_bin_sort")
 
 
 def gs_render_fwd(proj: Proj, sorted_idx, tile_range, cam: GsCamera, frame: Frame, stats=False, stream=None,
@@ -158,11 +159,12 @@ def gs_render_fwd(proj: Proj, sorted_idx, tile_range, cam: GsCamera, frame: Fram
 
 def gs_render_fwd_l1(proj: Proj, sorted_idx, tile_range, cam: GsCamera, frame: Frame, tgt_color, tgt_depth, scales,
                      dL_dcolor, dL_ddepth, stream=None, tile_order=None, tile_work=None, loss_part=None,
-                     tile_done=None):
+                     tile_done=None, tile_sorted=None):
     check(lib().gs_render_fwd_l1(proj.c(), _p(sorted_idx), _p(tile_range), _p(tile_order), cam, _p(frame.color),
                                  _p(frame.depth), _p(frame.alpha), _p(frame.T_final), _p(frame.n_contrib),
                                  _p(tile_work), _p(tgt_color), _p(tgt_depth), _p(scales), _p(dL_dcolor),
-                                 _p(dL_ddepth), _p(loss_part), _p(tile_done), _stream(stream)), "gs_render_fwd_l1")
+                                 _p(dL_ddepth), _p(loss_part), _p(tile_done), _p(tile_sorted), _stream(stream)),
+          "gs_render_fwd_l1")
 
 
 def gs_loss_from_tiles(cam: GsCamera, loss_part, scales, lambda_color, lambda_depth, loss, stream=None):
@@ -378,6 +380,13 @@ class Rasterizer:
         self.scales = None  # gs_loss_scales output (forward_l1)
         self.loss_part = None  # per-tile |residual| sums (render_l1)
         self.tile_done = None  # per-tile forward -> backward flags (overlap)
+        self.tile_sorted = None  # per-tile sort -> forward flags (overlap)
+        # forward_l1(reuse_order, overlap): also start the forward tile by tile
+        # as the sort finishes (gs_bin_sort tile_sorted) / run the sort in the
+        # forward's order; both measured slower on BJ.configs[2] (2457 vs
+        # 2502 it/s: the waiting CTAs hold SM slots), so off by default
+        self.sort_overlap = False
+        self.sort_in_fwd_order = False
         self.tl_loss = None
         self.dL_dcolor = torch.zeros(3, H, W, dtype=torch.float32, device=device)
         self.dL_ddepth = torch.zeros(H, W, dtype=torch.float32, device=device)
@@ -478,15 +487,23 @@ class Rasterizer:
         next backward(overlap=True) starts while this forward finishes, tile
         by tile (per-tile flags + programmatic dependent launch)."""
         self.project(params, view)
+        sorted_flags = None
         if reuse_order:
+            # the sort runs in the forward's launch order; with overlap the
+            # forward starts every tile as soon as its list is sorted
+            if overlap and self.sort_overlap:
+                if self.tile_sorted is None:
+                    self.tile_sorted = torch.zeros(self.T, dtype=torch.int32, device=self.device)
+                sorted_flags = self.tile_sorted
             gs_bin_sort(self.proj, self.n, self.cam, self.sort_ws, self.capacity, self.sorted_idx, self.tile_range,
-                        self.n_pairs, self.counters, tile_order=None)
+                        self.n_pairs, self.counters, tile_order=None,
+                        sort_order=self.bwd_order if self.sort_in_fwd_order else None, tile_sorted=sorted_flags)
         else:
             self.bin_sort()
         gs_render_fwd_l1(self.proj, self.sorted_idx, self.tile_range, self.cam, self.frame, tgt_color, tgt_depth,
                          self.scales, self.dL_dcolor, self.dL_ddepth,
                          tile_order=self.bwd_order if reuse_order else self.tile_order, tile_work=self.tile_work,
-                         tile_done=self._tile_done() if overlap else None)
+                         tile_done=self._tile_done() if overlap else None, tile_sorted=sorted_flags)
         if refresh_order or not reuse_order:
             gs_tile_order(self.tile_work, self.T, self.bwd_order)
         return self.frame

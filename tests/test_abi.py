@@ -58,7 +58,7 @@ def test_invalid_arguments_rejected_on_host():
                            None) == _lib.GS_ERR_INVALID_ARG
     assert L.gs_tile_order(None, 10, None, None) == _lib.GS_ERR_INVALID_ARG
     assert L.gs_bin_sort(pr, 10, cam, None, 0, 100, C.c_void_p(16), C.c_void_p(16), None, C.c_void_p(16), None,
-                         None) == _lib.GS_ERR_INVALID_ARG  # null projection arrays
+                         None, None, None) == _lib.GS_ERR_INVALID_ARG  # null projection arrays
     assert L.gs_loss(cam, None, None, None, None, None, 1.0, 1.0, None, 0, None, None, None, None) == _lib.GS_ERR_INVALID_ARG
     assert L.gs_render_bwd(p, C.c_void_p(16), cam, pr, None, C.c_void_p(16), None, C.c_void_p(16), C.c_void_p(16),
                            C.c_void_p(16), C.c_void_p(16), None, 0, None, 0, None, None, None, None, None,

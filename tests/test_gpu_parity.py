@@ -352,3 +352,37 @@ def test_bin_sort_tile_order_by_list_length():
     assert np.array_equal(np.sort(o), np.arange(len(L)))
     b = 63 - (L[o] * 64) // (int(L.max()) + 1)
     assert (np.diff(b) >= 0).all()
+
+
+@pytest.mark.parametrize("case", ["config1", "overflow", "empty"])
+def test_bin_sort_sorted_flags_and_launch_order(case):
+    """gs_bin_sort(sort_order, tile_sorted): the same bins as the plain call
+    (bit-exact), every tile flag released (also on overflow and with no
+    pairs), for a flag-waiting forward."""
+    import torch
+    from paper_2312_10070_b200 import Params, Rasterizer
+    from paper_2312_10070_b200.raster import gs_bin_sort
+    s = inputs.config1() if case != "empty" else inputs.random_scene(61, 0, 64, 48)
+    d = torch.device("cuda")
+    P = Params.from_numpy(*s.params(), device=d)
+    v = torch.as_tensor(s.views[0], device=d)
+    r = Rasterizer(s.n, s.cam, device=d)
+    r.size_for(P, v)
+    if case == "overflow":
+        r.set_capacity(1000)
+    r.project(P, v)
+    r.bin_sort()
+    torch.cuda.synchronize()
+    ref_idx, ref_rng = r.sorted_idx.clone(), r.tile_range.clone()
+    T = r.T
+    order = torch.as_tensor(np.random.default_rng(1).permutation(T).astype(np.int32), device=d)
+    flags = torch.zeros(T, dtype=torch.int32, device=d)
+    r.sorted_idx.fill_(-1)
+    gs_bin_sort(r.proj, r.n, r.cam, r.sort_ws, r.capacity, r.sorted_idx, r.tile_range, r.n_pairs, r.counters,
+                tile_order=None, sort_order=order, tile_sorted=flags)
+    torch.cuda.synchronize()
+    assert int(flags.sum()) == T
+    assert torch.equal(r.tile_range, ref_rng)
+    if case == "config1":
+        P_ = int(r.n_pairs.item())
+        assert torch.equal(r.sorted_idx[:P_], ref_idx[:P_])
