@@ -5,8 +5,10 @@
 
 One *step* = one multi-view sub-map mapping iteration of BJ.configs[3]
 (500k Gaussians, 1200x680, 8 keyframe views): per view gs_project ->
-gs_bin_sort -> gs_render_fwd -> gs_loss -> gs_render_bwd (all parameters), and
-for N > 1 one NCCL all-reduce of the gradient buffer.  Views are sharded
+gs_bin_sort -> gs_render_fwd_l1 (compositing with the L1 loss gradient and
+tile loss sums fused) -> gs_loss_from_tiles -> gs_render_bwd (all
+parameters), the views on 8 concurrent streams, and for N > 1 one NCCL
+all-reduce of the gradient buffer.  Views are sharded
 round-robin across ranks (strong scaling: 8 views in total for every N).
 Metric: fwd+bwd megapixels/s = (8 x 1200 x 680 / 1e6) / step time, max over
 ranks.  Also reported: tracking iterations/s (BJ.configs[2], 100 iterations
