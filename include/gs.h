@@ -464,9 +464,14 @@ int gs_gradient_mask(gs_camera cam, const float *color, const float *depth, doub
  *   depth16    (device) [H][W] uint16, in units of depth_scale metres
  *              (e.g. 1/5000 for TUM-RGBD, 1/6553.5 for Replica)
  *   tgt_color  (device) [3][H][W] fp32;  tgt_depth (device) [H][W] fp32
- * Errors: GS_ERR_INVALID_ARG (null, bad camera, depth_scale <= 0). */
+ *   scales     (device, nullable) [4]: also written as gs_loss_scales(cam,
+ *              tgt_depth, lambda_color, lambda_depth) would (the valid-depth
+ *              count taken during the unpacking, no second pass)
+ * Errors: GS_ERR_INVALID_ARG (null, bad camera, depth_scale <= 0, negative
+ * lambdas with scales). */
 int gs_unpack_rgbd(gs_camera cam, const uint8_t *rgb, const uint16_t *depth16, float depth_scale,
-                   float *tgt_color, float *tgt_depth, void *stream);
+                   float *tgt_color, float *tgt_depth, float *scales, float lambda_color,
+                   float lambda_depth, void *stream);
 
 /* S5+S6 — backward (Eqs. 7-8; R16, R17).
  *

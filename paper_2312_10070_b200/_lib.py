@@ -85,7 +85,7 @@ _PROTOS = {
     "gs_opt_workspace_bytes": (_SZ, [_I32]),
     "gs_seed_workspace_bytes": (_SZ, [GsCamera, _I32, _I32]),
     "gs_seed": (C.c_int, [GsCamera, _VP, _VP, _VP, _VP, _F, _F, _I32, _U32, GsParams, _I32, _VP, _SZ, _VP, _VP]),
-    "gs_unpack_rgbd": (C.c_int, [GsCamera, _VP, _VP, _F, _VP, _VP, _VP]),
+    "gs_unpack_rgbd": (C.c_int, [GsCamera, _VP, _VP, _F, _VP, _VP, _VP, _F, _F, _VP]),
     "gs_gradient_mask_workspace_bytes": (_SZ, [GsCamera]),
     "gs_gradient_mask": (C.c_int, [GsCamera, _VP, _VP, C.c_double, _VP, _VP, _VP, _SZ, _VP]),
     "gs_iso_reg": (C.c_int, [GsParams, _F, _VP, _VP, _SZ, _VP, _VP]),

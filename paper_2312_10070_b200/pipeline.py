@@ -56,15 +56,18 @@ class HostInputs:
         self.mine = list(mine)
         self.loss = torch.empty(n_losses, 4, dtype=torch.float32).pin_memory()
 
-    def upload_targets(self, v, cam, tgt_color, tgt_depth):
-        """On the current (copy) stream: view v's frame into its device targets."""
+    def upload_targets(self, v, cam, tgt_color, tgt_depth, scales=None, lambda_color=1.0, lambda_depth=1.0):
+        """On the current (copy) stream: view v's frame into its device targets
+        (and, if given, its gs_loss_scales into scales; returns whether it did)."""
         if self.frames == "rgbd16":
             self.dev_rgb8[v].copy_(self.rgb8[v], non_blocking=True)
             self.dev_d16[v].copy_(self.d16[v], non_blocking=True)
-            gs_unpack_rgbd(cam, self.dev_rgb8[v], self.dev_d16[v], self.depth_scale, tgt_color, tgt_depth)
-        else:
-            tgt_color.copy_(self.tgt_color[v], non_blocking=True)
-            tgt_depth.copy_(self.tgt_depth[v], non_blocking=True)
+            gs_unpack_rgbd(cam, self.dev_rgb8[v], self.dev_d16[v], self.depth_scale, tgt_color, tgt_depth,
+                           scales=scales, lambda_color=lambda_color, lambda_depth=lambda_depth)
+            return scales is not None
+        tgt_color.copy_(self.tgt_color[v], non_blocking=True)
+        tgt_depth.copy_(self.tgt_depth[v], non_blocking=True)
+        return False
 
     def h2d_bytes(self):
         b = sum(t.numel() * t.element_size() for t in self.params.values()) + self.views.numel() * 4
@@ -274,8 +277,10 @@ class MapStep:
                 self.params.rgb.copy_(host.params["rgb"], non_blocking=True)
                 rgb_ready = cs.record_event()
                 for v in self.mine:
-                    host.upload_targets(v, self.r.cam, self.tgt_color[v], self.tgt_depth[v])
-                    if self.fused_loss:  # the new frame's gradient scales (gs_loss_scales)
+                    # the new frame and (fused loss) its gradient scales, in the unpacking pass
+                    done = host.upload_targets(v, self.r.cam, self.tgt_color[v], self.tgt_depth[v],
+                                               self.tgt_scales[v] if self.fused_loss else None, self.lc, self.ld)
+                    if self.fused_loss and not done:
                         gs_loss_scales(self.r.cam, self.tgt_depth[v], self.lc, self.ld, self.scale_ws,
                                        self.tgt_scales[v])
                     tgt_ready[v] = cs.record_event()  # also orders the colours before every loss

@@ -258,11 +258,14 @@ def seed_first_keyframe(cam: GsCamera, view, color, depth, params: Params, n, M_
     return n_u, int(n_new.item())
 
 
-def gs_unpack_rgbd(cam: GsCamera, rgb8, depth16, depth_scale, tgt_color, tgt_depth, stream=None):
+def gs_unpack_rgbd(cam: GsCamera, rgb8, depth16, depth_scale, tgt_color, tgt_depth, stream=None, scales=None,
+                   lambda_color=1.0, lambda_depth=1.0):
     """An 8-bit RGB [H][W][3] + 16-bit depth [H][W] frame (device tensors,
-    uint8 / int16 or uint16 storage) into fp32 planar targets [3][H][W], [H][W]."""
+    uint8 / int16 or uint16 storage) into fp32 planar targets [3][H][W], [H][W];
+    scales (device [4], optional): the frame's gs_loss_scales in the same pass."""
     check(lib().gs_unpack_rgbd(cam, _p(rgb8), _p(depth16), float(depth_scale), _p(tgt_color), _p(tgt_depth),
-                               _stream(stream)), "gs_unpack_rgbd")
+                               _p(scales), float(lambda_color), float(lambda_depth), _stream(stream)),
+          "gs_unpack_rgbd")
 
 
 class Optimizer:

@@ -19,7 +19,7 @@ def timeit(fn, n=30):
 print("device-resident  %.3f" % timeit(ms.step))
 host = HostInputs(ms.params, ms.views, ms.tgt_color, ms.tgt_depth, ms.mine, ms.losses.shape[0])
 print("host all         %.3f" % timeit(lambda: ms.step(host=host)))
-def copies_only(v, cam, c, d):
+def copies_only(v, cam, c, d, *rest):
     host.dev_rgb8[v].copy_(host.rgb8[v], non_blocking=True)
     host.dev_d16[v].copy_(host.d16[v], non_blocking=True)
 orig = host.upload_targets
