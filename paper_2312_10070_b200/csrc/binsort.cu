@@ -656,9 +656,13 @@ __device__ __forceinline__ bool tile_sort_one(const TileSortArgs &a, BucketSmem<
   return true;
 }
 
-__global__ void __launch_bounds__(kBucketThreads, TS_SMALL_MINB) k_tile_sort(TileSortArgs a) {
+// One CTA per tile.  kCap = kSmallCap: lists of kSmallCap+1 .. kChunk go to
+// the mid list (k_tile_sort_mid); kCap = kChunk: every list <= kChunk here.
+// Longer lists go to the slow list.
+template <int kCap, int kMinB>
+__global__ void __launch_bounds__(kBucketThreads, kMinB) k_tile_sort(TileSortArgs a) {
   pdl_begin();
-  __shared__ BucketSmem<kSmallCap> s;
+  __shared__ BucketSmem<kCap> s;
   const int tile = a.order ? __ldg(a.order + blockIdx.x) : int(blockIdx.x);
   if (a.misc[2]) {  // overflow: every range is empty
     mark_sorted(a, tile);
@@ -670,7 +674,7 @@ __global__ void __launch_bounds__(kBucketThreads, TS_SMALL_MINB) k_tile_sort(Til
     mark_sorted(a, tile);
     return;
   }
-  if (n > kSmallCap) {  // k_tile_sort_mid / _big sort it (and mark it)
+  if (n > kCap) {  // k_tile_sort_mid / _big sort it (and mark it)
     if (threadIdx.x == 0) {
       if (n > kChunk)
         a.slow[atomicAdd(&a.misc[3], 1u)] = tile;
@@ -679,7 +683,7 @@ __global__ void __launch_bounds__(kBucketThreads, TS_SMALL_MINB) k_tile_sort(Til
     }
     return;
   }
-  if (tile_sort_one<kSmallCap>(a, s, tile, r, n)) mark_sorted(a, tile);
+  if (tile_sort_one<kCap>(a, s, tile, r, n)) mark_sorted(a, tile);
 }
 
 // (the mid and long-list kernels let their dependents launch BEFORE waiting
@@ -879,8 +883,15 @@ extern "C" int gs_bin_sort(gs_proj pr, int32_t n, gs_camera cam, void *ws, size_
     TileSortArgs a{pr.depth, tile_range, sort_order ? sort_order : tile_order, misc, L.T, sorted_idx, U(L.key_a),
                    U(L.key_b), U(L.val_b), reinterpret_cast<int32_t *>(U(L.slow)),
                    reinterpret_cast<int32_t *>(U(L.mid)), tile_sorted};
-    launch_pdl(k_tile_sort, dim3(L.T), dim3(kBucketThreads), 0, s, a);
-    launch_pdl(k_tile_sort_mid, dim3(std::min(L.T, 4 * kBigBlocks)), dim3(kBucketThreads), 0, s, a);
+    // lists averaging <= 1800 entries: the half-size instance (more CTAs per
+    // SM) with the rare longer lists on the mid path; longer averages (e.g.
+    // BJ.configs[4]): every list <= kChunk in one pass
+    if (capacity <= int64_t(1800) * L.T) {
+      launch_pdl(k_tile_sort<kSmallCap, TS_SMALL_MINB>, dim3(L.T), dim3(kBucketThreads), 0, s, a);
+      launch_pdl(k_tile_sort_mid, dim3(std::min(L.T, 4 * kBigBlocks)), dim3(kBucketThreads), 0, s, a);
+    } else {
+      launch_pdl(k_tile_sort<kChunk, 4>, dim3(L.T), dim3(kBucketThreads), 0, s, a);
+    }
     launch_pdl(k_tile_sort_big, dim3(std::min(L.T, kBigBlocks)), dim3(kSortThreads), 0, s, a);
   }
   else if (tile_sorted)

@@ -347,17 +347,20 @@ class MapStep:
     def launches_per_step(self):
         """Kernels of ours launched per step; the fused L1
         loss takes 1 launch (gs_loss_from_tiles) instead of gs_loss's 3."""
-        per_view = kernels_per_view(self.r.cam) - (2 if self.fused_loss and self.ssim == 0.0 else 0)
+        per_view = kernels_per_view(self.r.cam, capacity=self.r.capacity) - (
+            2 if self.fused_loss and self.ssim == 0.0 else 0)
         if self.schedule == "lanes" and self.fused_gauss and len(self.mine) <= len(self.lanes):
             return len(self.mine) * (per_view - 1) + 1
         return len(self.mine) * per_view
 
 
-def kernels_per_view(cam, loss=True, bwd=True):
+def kernels_per_view(cam, loss=True, bwd=True, capacity=0):
     """Kernels of ours per view (the sort's memset is a copy-engine node, not a kernel):
-    project 1; bin_sort: prep, tile counts, emit, tile sort, mid-list sort, long-list sort = 6;
+    project 1; bin_sort: prep, tile counts, emit, tile sort, [mid-list sort when the
+    pair capacity averages <= 1800 per tile,] long-list sort = 5 or 6;
     render 1 + backward tile order 1; loss 3; backward 2."""
-    n = 1 + 6 + 2
+    T = ((cam.width + 15) // 16) * ((cam.height + 15) // 16)
+    n = 1 + (6 if capacity <= 1800 * T else 5) + 2
     if loss:
         n += 3
     if bwd:
@@ -454,5 +457,5 @@ class TrackingLoop:
         # masked loss: 6 kernels (residual + digit 0, 3 digit passes, apply, final) instead of 3;
         # fused L1: none (the forward writes the maps; + 2 per graph for the scales)
         if self.masked is None and self.fused_loss:
-            return kernels_per_view(self.r.cam) + 1 - 3
-        return kernels_per_view(self.r.cam) + 1 + (3 if self.masked is not None else 0)
+            return kernels_per_view(self.r.cam, capacity=self.r.capacity) + 1 - 3
+        return kernels_per_view(self.r.cam, capacity=self.r.capacity) + 1 + (3 if self.masked is not None else 0)
