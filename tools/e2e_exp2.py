@@ -1,3 +1,4 @@
+"""Experiment: the end-to-end step with parts of the upload / unpack path disabled (copies only, no gradient scales)."""
 import os, sys
 sys.path.insert(0, os.getcwd())
 import torch
