@@ -50,8 +50,10 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--profile", action="store_true", help="short run for ncu (no clocks/cpu/e2e/tracking)")
     ap.add_argument("--lanes", type=int, default=8, help="per-view buffer sets (and lane streams)")
-    ap.add_argument("--schedule", default="lanes", choices=["stages", "lanes"],
-                    help="stages: one stream per stage (software pipeline); lanes: one stream per view")
+    ap.add_argument("--backend", default="nccl", choices=["nccl", "gloo"],
+                    help="process-group backend for N > 1 (gloo: tests of the multi-rank branch on one GPU)")
+    ap.add_argument("--small", action="store_true",
+                    help="tests only: BJ.configs[3] reduced to 40k Gaussians, 4 views of 320x184")
     return ap.parse_args()
 
 
@@ -114,10 +116,14 @@ class Clocks:
 # ---------------------------------------------------------------------------
 # workload
 
-def make_workload(cfg, device, rank, world):
+def make_workload(cfg, device, rank, world, small=False):
     import torch
     from paper_2312_10070_b200 import Params, Rasterizer, inputs
-    s = {1: inputs.config1, 3: inputs.config3, 4: inputs.config4}[cfg]()
+    if small:  # tests only (bench.py --small)
+        s = inputs.config3(seed=5, n=40_000, n_views=4)
+        s.cam = inputs.Camera(320, 184, 160.0, 160.0, 159.5, 91.5)
+    else:
+        s = {1: inputs.config1, 3: inputs.config3, 4: inputs.config4}[cfg]()
     P = Params.from_numpy(*s.params(), device=device)
     views = torch.as_tensor(s.views, device=device)
     V = views.shape[0]
@@ -212,15 +218,20 @@ def bench_ours(a):
     if world != a.gpus:
         if a.gpus != 1 or world != 1:
             print(f"warning: --gpus {a.gpus} but WORLD_SIZE={world}", file=sys.stderr)
-    torch.cuda.set_device(local)
-    device = torch.device("cuda", local)
+    # one process per GPU; with --backend gloo (tests) several ranks may share one GPU
+    local_dev = local % max(torch.cuda.device_count(), 1)
+    torch.cuda.set_device(local_dev)
+    device = torch.device("cuda", local_dev)
     group = None
     if world > 1:
-        dist.init_process_group("nccl", device_id=device)
-    sm_count = raster.device_check(local)
-    s, P, views, tc, td = make_workload(a.config, device, rank, world)
+        if a.backend == "nccl":
+            dist.init_process_group("nccl", device_id=device)
+        else:
+            dist.init_process_group("gloo")
+    sm_count = raster.device_check(local_dev)
+    s, P, views, tc, td = make_workload(a.config, device, rank, world, a.small)
     V = views.shape[0]
-    ms = MapStep(P, views, s.cam, tc, td, rank, world, group, device=device, lanes=a.lanes, schedule=a.schedule)
+    ms = MapStep(P, views, s.cam, tc, td, rank, world, group, device=device, lanes=a.lanes)
     ms.size()
     # per-view work counts for the roofline (untimed)
     stats_views = []
@@ -281,7 +292,7 @@ def bench_ours(a):
     if world > 1:
         dist.barrier()
     step_ms = []
-    with Clocks(local) as clk:
+    with Clocks(local_dev) as clk:
         torch.cuda.synchronize()
         if world > 1:
             dist.barrier()
@@ -350,9 +361,12 @@ def bench_ours(a):
         "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
         "dtype": "f32", "data": "synthetic (seeded BJ.configs[%d] generator; targets = render of a perturbed copy)"
         % a.config,
-        "config": {"workload": f"BJ.configs[{a.config}] sub-map mapping iteration", "gaussians": s.n,
+        "config": {"workload": (f"BJ.configs[{a.config}] sub-map mapping iteration" if not a.small else
+                                "BJ.configs[3] reduced (40k Gaussians, 4 views of 320x184; tests only)"),
+                   "gaussians": s.n,
                    "width": W, "height": H, "views_per_step": V, "views_per_rank": len(ms.mine),
-                   "parallelism": f"view-sharded dp{world}, NCCL all-reduce of gradients" if world > 1 else "1 GPU",
+                   "parallelism": (f"view-sharded dp{world}, {a.backend.upper()} all-reduce of gradients"
+                                   if world > 1 else "1 GPU"),
                    "l2": "256 MiB buffer written between timed steps (outside the step events)",
                    "pairs_per_view": int(np.mean([x["pairs"] for x in stats_views])),
                    "scanned_per_px": sum(x["scanned"] for x in stats_views) / (len(stats_views) * W * H),
@@ -522,6 +536,7 @@ def bench_tracking(device, masked=None):
                       "(gs_render_fwd_l1; scales once per frame), pose bwd, pose grad + Adam)") if masked is None else
                      "100 iterations captured once (project, sort, render, loss, pose bwd, pose grad + Adam)",
             "gpu_launches_per_iter": loop.launches_per_iter(),
+            "flag_timeouts": loop.flag_timeouts(),
             "start_err": {"rot_deg": float(rot0), "trans_cm": float(np.linalg.norm(sv[9:]) * 100)},
             "final_err": {"rot_deg": float(rot_err), "trans_cm": float(np.linalg.norm(t) * 100)}}
 

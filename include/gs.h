@@ -35,7 +35,7 @@
 extern "C" {
 #endif
 
-#define GS_ABI_VERSION 1
+#define GS_ABI_VERSION 2
 
 /* Rasterizer constants (fp32 bit patterns in DESIGN.md R11). */
 #define GS_TILE 16                   /* 16x16 pixel tiles           */
@@ -121,10 +121,13 @@ typedef struct gs_counters {
   int64_t reserved;
 } gs_counters;
 
-/* Adam step on the left-perturbation twist of T_wc (host, by value).
- * Defaults: lr_trans 2e-3 m, lr_rot 1e-3 rad, 0.9, 0.999, 1e-8. */
+/* Adam step on the left-perturbation twist of T_wc (host, by pointer).
+ * Defaults: lr_trans 2e-3 m, lr_rot 1e-3 rad, 0.9, 0.999, 1e-8.
+ * beta1, beta2, eps are fp64 (as in gs_adam_cfg): 1 - beta is formed without
+ * the fp32 rounding of 0.999 (1 - fp32(0.999) = 1.0000467e-3). */
 typedef struct gs_pose_step {
-  float lr_trans, lr_rot, beta1, beta2, eps;
+  float lr_trans, lr_rot;
+  double beta1, beta2, eps;
 } gs_pose_step;
 
 /* ---------------------------------------------------------------------- */
@@ -144,9 +147,11 @@ int gs_check_device(int device, int *sm_count);
 int32_t gs_num_tiles(gs_camera cam);
 
 /* Workspace bytes gs_bin_sort needs for n Gaussians, a pair capacity and
- * camera `cam`: ~12 bytes per pair of capacity (scratch of the exact sort of
- * long tile lists) + 12 bytes per tile.  0 if unsupported (> 2^21 tiles or
- * capacity >= 2^31 - 1). */
+ * camera `cam`: ~24 bytes per Gaussian (the depth sort's key / id ping-pong
+ * and the ordered tile rects) + 4 bytes per (tile, 1024..4096 Gaussians) of
+ * per-CTA tile counts + look-back words; independent of the capacity.  0 if
+ * unsupported (> 2^21 tiles, n >= 2^30, capacity >= 2^31 - 1, or a tile grid
+ * too large for the emission CTA's shared memory: > ~33k tiles). */
 size_t gs_binsort_workspace_bytes(int32_t n, int64_t capacity, gs_camera cam);
 
 /* Workspace bytes gs_loss needs for camera `cam`. */
@@ -190,9 +195,13 @@ int gs_project(gs_params p, const gs_view *view, gs_camera cam, gs_proj out,
  * S:142; R10).
  *
  * Emits one (tile, Gaussian) pair per tile of each visible Gaussian's rect and
- * orders all pairs by the key (tile asc, fp32 depth asc, Gaussian id asc).
+ * orders all pairs by the key (tile asc, fp32 depth asc, Gaussian id asc):
+ * a stable radix sort of the visible Gaussians by depth, then a stable
+ * per-tile counting pass over that order (bit-deterministic; no atomics
+ * decide a position).
  *   pr.depth, pr.rect, pr.tiles_touched (device) inputs from gs_project
- *   ws/ws_bytes   (device) workspace >= gs_binsort_workspace_bytes(n, capacity, cam)
+ *   ws/ws_bytes   (device, 16-byte aligned) workspace >=
+ *                 gs_binsort_workspace_bytes(n, capacity, cam)
  *   capacity      length of sorted_idx
  *   sorted_idx    (device) [capacity] Gaussian ids, tile-major
  *   tile_range    (device) [T][2] int32 [start, end) into sorted_idx
@@ -202,20 +211,11 @@ int gs_project(gs_params p, const gs_view *view, gs_camera cam, gs_proj out,
  *                 then start the heaviest tiles first (no effect on results)
  *   n_pairs       (device) [1] int64 total pair count P
  *   cnt           (device) counters, nullable
- *   sort_order    (device, nullable) [T] the per-tile sort's launch order
- *                 (default: tile_order, else tile id); scheduling only
- *   tile_sorted   (device, nullable) [T] uint32, zero on first use: a
- *                 flag per tile, released once its list is sorted, for the
- *                 NEXT call on the stream being gs_render_fwd_l1 with the same
- *                 tile_sorted (it then starts each tile as soon as that tile
- *                 is sorted and re-arms the flag); every call given
- *                 tile_sorted must be followed by exactly one such forward
  * If P > capacity, n_overflow is incremented, every tile range is set empty
  * and sorted_idx is left untouched (the caller re-sizes and repeats). */
 int gs_bin_sort(gs_proj pr, int32_t n, gs_camera cam, void *ws, size_t ws_bytes,
                 int64_t capacity, int32_t *sorted_idx, int32_t *tile_range,
-                int32_t *tile_order, int64_t *n_pairs, gs_counters *cnt,
-                const int32_t *sort_order, uint32_t *tile_sorted, void *stream);
+                int32_t *tile_order, int64_t *n_pairs, gs_counters *cnt, void *stream);
 
 /* S3 — front-to-back alpha compositing (Eqs. 3, 4, 6; P:133-141, P:161-166;
  * S:129-138; R11-R15).
@@ -251,21 +251,20 @@ int gs_render_fwd(gs_proj pr, const int32_t *sorted_idx, const int32_t *tile_ran
  *   loss_part (device, nullable) [T][2] fp64: per tile, sum |C^ - C*| over
  *             its pixels and channels, sum |D^ - D*| over its valid pixels
  *             (fixed order); gs_loss_from_tiles turns them into the loss.
- *   tile_done (device, nullable) [T] uint32, zero on first use: per-tile
- *             completion flags for the NEXT call on the stream being a
- *             gs_render_bwd with the same tile_done (it then starts while
- *             this forward finishes, each tile after its own forward tile;
- *             the backward re-arms the flags).  Every call given tile_done
- *             must be followed by exactly one such backward.
- *   tile_sorted (device, nullable) the flags given to the immediately
- *             preceding gs_bin_sort: each tile starts once its list is sorted
- *             (see gs_bin_sort). */
+ *   tile_done (device, nullable) [T + 1] uint32, zero on first use:
+ *             per-tile completion flags [0, T) for the NEXT call on the
+ *             stream being a gs_render_bwd with the same tile_done (it then
+ *             starts while this forward finishes, each tile after its own
+ *             forward tile, and re-arms the flags), and at [T] the count of
+ *             capped waits that timed out (see gs_render_bwd; 0 unless the
+ *             contract below is broken).  Every call given tile_done must be
+ *             followed by exactly one such backward. */
 int gs_render_fwd_l1(gs_proj pr, const int32_t *sorted_idx, const int32_t *tile_range,
                      const int32_t *tile_order, gs_camera cam, float *color, float *depth,
                      float *alpha, float *T_final, int32_t *n_contrib, int32_t *tile_work,
                      const float *tgt_color, const float *tgt_depth, const float *scales,
                      float *dL_dcolor, float *dL_ddepth, double *loss_part, uint32_t *tile_done,
-                     uint32_t *tile_sorted, void *stream);
+                     void *stream);
 
 /* Scheduling utility: tile ids by descending work (64 buckets of max/64, order
  * inside a bucket unspecified), e.g. from gs_render_fwd's tile_work for
@@ -495,11 +494,15 @@ int gs_unpack_rgbd(gs_camera cam, const uint8_t *rgb, const uint16_t *depth16, f
  *   pose_partials (device) [gs_pose_partials_count(n)][12] =
  *             (dL/dR row-major 9, dL/dt 3) per block; required iff
  *             GS_GRAD_POSE, overwritten.
- *   tile_done (device, nullable) the flags given to the immediately
+ *   tile_done (device, nullable) the [T + 1] flags given to the immediately
  *             preceding gs_render_fwd_l1 on this stream: the per-pixel phase
  *             is launched as a programmatic dependent of that forward (PDL)
- *             and each tile waits for its forward tile; NULL: ordinary
- *             stream order. */
+ *             and each tile waits for its forward tile's flag, then re-arms
+ *             it.  The wait is capped (~0.4 s): a wait that times out is
+ *             counted in tile_done[T] and its flag is NOT re-armed, so a
+ *             broken ordering is never silent (the results of that call are
+ *             invalid; TrackingLoop.flag_timeouts() reads the count).  NULL:
+ *             ordinary stream order. */
 int gs_render_bwd(gs_params p, const gs_view *view, gs_camera cam, gs_proj pr,
                   const int32_t *sorted_idx, const int32_t *tile_range,
                   const int32_t *tile_order, const float *T_final, const int32_t *n_contrib,
@@ -507,22 +510,6 @@ int gs_render_bwd(gs_params p, const gs_view *view, gs_camera cam, gs_proj pr,
                   const float *dL_dalpha, uint32_t flags, void *ws, size_t ws_bytes,
                   float *g_mean_opa, float *g_quat, float *g_logscale, float *g_rgb,
                   float *pose_partials, uint32_t *tile_done, void *stream);
-
-/* S6 for several views at once (mapping, Eq. 12 summed over the keyframes of
- * an iteration): for every Gaussian, the camera part of the chain
- * of gs_render_bwd's Gaussian phase for each of the V views (each view's
- * grad2d scratch from a GS_BWD_PIXELS_ONLY call), summed in fp64, then the
- * scale / quaternion part once on the sum and one += into the gradient
- * arrays.  Equal to V GS_BWD_GAUSS_ONLY calls up to fp32 rounding; reads
- * the parameters and writes the gradients once instead of V times.
- *   V in [1, 16]; views, conic_o, tiles_touched, ws: host arrays of V device
- *   pointers (each view's gs_view, gs_proj.conic_o, gs_proj.tiles_touched and
- *   gs_render_bwd workspace); every grad2d record read is zeroed.
- *   g_* (device) [n][4] gradients, += (GS_GRAD_PARAMS layout). */
-int gs_render_bwd_gauss_views(gs_params p, int32_t V, const gs_view *const *views, gs_camera cam,
-                              const float *const *conic_o, const int32_t *const *tiles_touched,
-                              float *const *ws, float *g_mean_opa, float *g_quat, float *g_logscale,
-                              float *g_rgb, void *stream);
 
 /* S7 — camera-pose gradient (Eq. 14; R22).
  *
@@ -533,13 +520,15 @@ int gs_render_bwd_gauss_views(gs_params p, int32_t V, const gs_view *const *view
  *                 Adam on the twist, T <- exp(-step^) T, R re-orthonormalised
  *   pose_partials (device) [n_partials][12]
  *   step          (host, nullable) Adam hyper-parameters
- *   adam_state    (device) [13] = m[6], v[6], t; required iff step != NULL;
- *                 zero it before the first iteration
+ *   adam_state    (device) [13] fp64 = m[6], v[6], t; required iff step !=
+ *                 NULL; zero it before the first iteration (the moments are
+ *                 kept in fp64, so the step equals the fp64 definition up to
+ *                 the fp32 rounding of the stored view)
  *   dL_dview      (device, nullable) [12] = dL/dR (9), dL/dt (3)
  *   dL_dtwist     (device, nullable) [6]  = dL/dv (3), dL/dw (3)
  *   dL_dqt        (device, nullable) [7]  = dL/dq (4), dL/dt (3) */
 int gs_pose_grad(gs_view *view, const float *pose_partials, int32_t n_partials,
-                 const gs_pose_step *step, float *adam_state, float *dL_dview,
+                 const gs_pose_step *step, double *adam_state, float *dL_dview,
                  float *dL_dtwist, float *dL_dqt, void *stream);
 
 #ifdef __cplusplus

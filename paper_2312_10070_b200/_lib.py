@@ -42,8 +42,8 @@ class GsProj(C.Structure):
 
 
 class GsPoseStep(C.Structure):
-    _fields_ = [("lr_trans", C.c_float), ("lr_rot", C.c_float), ("beta1", C.c_float), ("beta2", C.c_float),
-                ("eps", C.c_float)]
+    _fields_ = [("lr_trans", C.c_float), ("lr_rot", C.c_float), ("beta1", C.c_double), ("beta2", C.c_double),
+                ("eps", C.c_double)]
 
 
 class GsView(C.Structure):
@@ -72,13 +72,13 @@ _PROTOS = {
     "gs_bwd_workspace_bytes": (_SZ, [_I32]),
     "gs_pose_partials_count": (_I32, [_I32]),
     "gs_project": (C.c_int, [GsParams, _VP, GsCamera, GsProj, _VP, _VP]),
-    "gs_bin_sort": (C.c_int, [GsProj, _I32, GsCamera, _VP, _SZ, _I64, _VP, _VP, _VP, _VP, _VP, _VP, _VP, _VP]),
+    "gs_bin_sort": (C.c_int, [GsProj, _I32, GsCamera, _VP, _SZ, _I64, _VP, _VP, _VP, _VP, _VP, _VP]),
     "gs_render_fwd": (C.c_int, [GsProj, _VP, _VP, _VP, GsCamera, _VP, _VP, _VP, _VP, _VP, _VP, _VP, _VP]),
     "gs_tile_order": (C.c_int, [_VP, _I32, _VP, _VP]),
     "gs_loss": (C.c_int, [GsCamera, _VP, _VP, _VP, _VP, _VP, _F, _F, _VP, _SZ, _VP, _VP, _VP, _VP]),
     "gs_loss_scales": (C.c_int, [GsCamera, _VP, _F, _F, _VP, _SZ, _VP, _VP]),
     "gs_render_fwd_l1": (C.c_int, [GsProj, _VP, _VP, _VP, GsCamera, _VP, _VP, _VP, _VP, _VP, _VP, _VP, _VP, _VP, _VP,
-                                   _VP, _VP, _VP, _VP, _VP]),
+                                   _VP, _VP, _VP, _VP]),
     "gs_loss_from_tiles": (C.c_int, [GsCamera, _VP, _VP, _F, _F, _VP, _VP]),
     "gs_tracking_loss_workspace_bytes": (_SZ, [GsCamera]),
     "gs_ssim_workspace_bytes": (_SZ, [GsCamera]),
@@ -95,8 +95,6 @@ _PROTOS = {
     "gs_tracking_loss": (C.c_int, [GsCamera, _VP, _VP, _VP, _VP, _VP, _F, _F, _VP, _SZ, _VP, _VP, _VP, _VP]),
     "gs_render_bwd": (C.c_int, [GsParams, _VP, GsCamera, GsProj, _VP, _VP, _VP, _VP, _VP, _VP, _VP, _VP, _U32, _VP,
                                 _SZ, _VP, _VP, _VP, _VP, _VP, _VP, _VP]),
-    "gs_render_bwd_gauss_views": (C.c_int, [GsParams, _I32, C.POINTER(_VP), GsCamera, C.POINTER(_VP), C.POINTER(_VP),
-                                             C.POINTER(_VP), _VP, _VP, _VP, _VP, _VP]),
     "gs_pose_grad": (C.c_int, [_VP, _VP, _I32, C.POINTER(GsPoseStep), _VP, _VP, _VP, _VP, _VP]),
 }
 

@@ -95,7 +95,7 @@ struct PoseArgs {
   int n_partials;
   int has_step;
   gs_pose_step step;
-  float *adam;
+  double *adam;
   float *dL_dview, *dL_dtwist, *dL_dqt;
 };
 
@@ -170,15 +170,15 @@ __global__ void __launch_bounds__(kPoseThreads) k_pose_grad(PoseArgs a) {
   if (a.has_step) {
     // Adam on the twist, applied as T <- exp(d^) T
     const double b1 = a.step.beta1, b2 = a.step.beta2, eps = a.step.eps;
-    const double stp = double(a.adam[12]) + 1.0;
-    a.adam[12] = float(stp);
+    const double stp = a.adam[12] + 1.0;
+    a.adam[12] = stp;
     double d[6];
     const double c1 = 1.0 - pow(b1, stp), c2 = 1.0 - pow(b2, stp);  // bias corrections, once
     for (int i = 0; i < 6; ++i) {
-      const double m = b1 * double(a.adam[i]) + (1.0 - b1) * tw[i];
-      const double v = b2 * double(a.adam[6 + i]) + (1.0 - b2) * tw[i] * tw[i];
-      a.adam[i] = float(m);
-      a.adam[6 + i] = float(v);
+      const double m = b1 * a.adam[i] + (1.0 - b1) * tw[i];
+      const double v = b2 * a.adam[6 + i] + (1.0 - b2) * tw[i] * tw[i];
+      a.adam[i] = m;
+      a.adam[6 + i] = v;
       const double mh = m / c1, vh = v / c2;
       d[i] = -(i < 3 ? double(a.step.lr_trans) : double(a.step.lr_rot)) * mh / (sqrt(vh) + eps);
     }
@@ -199,14 +199,14 @@ __global__ void __launch_bounds__(kPoseThreads) k_pose_grad(PoseArgs a) {
 }  // namespace gs
 
 extern "C" int gs_pose_grad(gs_view *view, const float *pose_partials, int32_t n_partials, const gs_pose_step *step,
-                            float *adam_state, float *dL_dview, float *dL_dtwist, float *dL_dqt, void *stream) {
+                            double *adam_state, float *dL_dview, float *dL_dtwist, float *dL_dqt, void *stream) {
   using namespace gs;
   if (!view || !pose_partials || n_partials <= 0 || (step && !adam_state)) {
     set_error("gs_pose_grad: invalid argument");
     return GS_ERR_INVALID_ARG;
   }
-  if (step && !(step->lr_trans >= 0.f && step->lr_rot >= 0.f && step->beta1 >= 0.f && step->beta1 < 1.f &&
-                step->beta2 >= 0.f && step->beta2 < 1.f && step->eps > 0.f)) {
+  if (step && !(step->lr_trans >= 0.f && step->lr_rot >= 0.f && step->beta1 >= 0.0 && step->beta1 < 1.0 &&
+                step->beta2 >= 0.0 && step->beta2 < 1.0 && step->eps > 0.0)) {
     set_error("gs_pose_grad: invalid Adam hyper-parameters");
     return GS_ERR_INVALID_ARG;
   }

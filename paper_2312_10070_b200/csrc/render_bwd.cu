@@ -38,7 +38,8 @@ struct BwdArgs {
   const float *dL_dcolor, *dL_ddepth, *dL_dalpha;
   int W, H, TX;
   float *grad2d;
-  uint32_t *tile_done;  // nullable: wait for (and re-arm) the forward's per-tile flag
+  uint32_t *tile_done;  // nullable: [T + 1], wait for (and re-arm) the forward's per-tile flag
+  int T;                // tiles; tile_done[T] counts timed-out waits
 };
 
 __device__ __forceinline__ void red_add_v4(float *addr, float x, float y, float z, float w) {
@@ -243,7 +244,8 @@ __global__ void __launch_bounds__(BG::kThreads, kBwdMinBlocks) k_bwd_pixels(BwdA
   if (a.tile_done) {
     // launched programmatically dependent on gs_render_fwd_l1: every forward
     // CTA has started (launch_dependents), so this tile's flag is set in
-    // bounded time; the wait is capped (~0.5 s) so a misuse cannot hang
+    // bounded time; the wait is capped (~0.4 s) so a misuse cannot hang, and
+    // a timeout is counted in tile_done[T] (the flag is then left as it is)
     if (threadIdx.x == 0) {
       uint32_t f = 0;
       for (long long it = 0; it < (1ll << 22); ++it) {
@@ -251,7 +253,10 @@ __global__ void __launch_bounds__(BG::kThreads, kBwdMinBlocks) k_bwd_pixels(BwdA
         if (f) break;
         __nanosleep(100);
       }
-      a.tile_done[tile] = 0u;  // re-armed for the next forward
+      if (f)
+        a.tile_done[tile] = 0u;  // re-armed for the next forward
+      else
+        atomicAdd(a.tile_done + a.T, 1u);
     }
     __syncthreads();
   }
@@ -622,180 +627,6 @@ __global__ void __launch_bounds__(kGaussThreads, GAUSS_MINB) k_bwd_gauss(GaussAr
   }
 }
 
-// ---- S6 over several views at once (mapping) -------------------------------------
-constexpr int kMaxGaussViews = 16;
-
-struct GaussViewsArgs {
-  gs_params p;
-  int V;
-  float fx, fy;
-  const gs_view *view[kMaxGaussViews];
-  const float4 *conic_o[kMaxGaussViews];
-  const int32_t *tiles_touched[kMaxGaussViews];
-  float *grad2d[kMaxGaussViews];
-  float4 *g_mean_opa, *g_quat, *g_logscale, *g_rgb;
-};
-
-// One thread per Gaussian: the view-independent part of the chain of P:172
-// (q^, R_q, s, M, Sigma) once, then per view the camera part (p, J, Sigma_c,
-// dL/dp, dL/dSigma_c), summed in fp64 as dL/dmu and dL/dSigma (world frame);
-// the scale / quaternion chain, linear in dL/dSigma, runs once on the sum;
-// one read-modify-write of the four gradient arrays.  Equal to V calls of
-// the single-view Gaussian phase up to the fp32 rounding of the += chain.
-__global__ void __launch_bounds__(kGaussThreads) k_bwd_gauss_views(GaussViewsArgs a) {
-  const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= a.p.n) return;
-  int tt[kMaxGaussViews];
-  bool any = false;
-#pragma unroll
-  for (int v = 0; v < kMaxGaussViews; ++v) {
-    tt[v] = v < a.V ? __ldg(a.tiles_touched[v] + i) : 0;
-    any |= tt[v] > 0;
-  }
-  if (!any) return;  // invisible in every view: no contribution, nothing to write
-  const float4 mo = __ldg(reinterpret_cast<const float4 *>(a.p.mean_opa) + i);
-  const float4 qf = __ldg(reinterpret_cast<const float4 *>(a.p.quat) + i);
-  const float4 lf = __ldg(reinterpret_cast<const float4 *>(a.p.logscale) + i);
-  const double mu[3] = {mo.x, mo.y, mo.z};
-  const double q0 = qf.x, q1 = qf.y, q2 = qf.z, q3 = qf.w;
-  const double qn = sqrt(q0 * q0 + q1 * q1 + q2 * q2 + q3 * q3);
-  const double iq = 1.0 / qn;
-  const double qw = q0 * iq, qx = q1 * iq, qy = q2 * iq, qz = q3 * iq;
-  double Rq[9];
-  Rq[0] = 1.0 - 2.0 * (qy * qy + qz * qz);
-  Rq[1] = 2.0 * (qx * qy - qw * qz);
-  Rq[2] = 2.0 * (qx * qz + qw * qy);
-  Rq[3] = 2.0 * (qx * qy + qw * qz);
-  Rq[4] = 1.0 - 2.0 * (qx * qx + qz * qz);
-  Rq[5] = 2.0 * (qy * qz - qw * qx);
-  Rq[6] = 2.0 * (qx * qz - qw * qy);
-  Rq[7] = 2.0 * (qy * qz + qw * qx);
-  Rq[8] = 1.0 - 2.0 * (qx * qx + qy * qy);
-  const double s[3] = {exp(double(lf.x)), exp(double(lf.y)), exp(double(lf.z))};
-  double M[9], Sig[9];
-#pragma unroll
-  for (int r = 0; r < 3; ++r)
-#pragma unroll
-    for (int c = 0; c < 3; ++c) M[3 * r + c] = Rq[3 * r + c] * s[c];
-#pragma unroll
-  for (int r = 0; r < 3; ++r)
-#pragma unroll
-    for (int c = 0; c < 3; ++c) Sig[3 * r + c] = M[3 * r] * M[3 * c] + M[3 * r + 1] * M[3 * c + 1] + M[3 * r + 2] * M[3 * c + 2];
-  double gmu[3] = {0.0, 0.0, 0.0}, GSig[9], glogit = 0.0, grgb[3] = {0.0, 0.0, 0.0};
-#pragma unroll
-  for (int k = 0; k < 9; ++k) GSig[k] = 0.0;
-  const double fx = a.fx, fy = a.fy;
-  for (int v = 0; v < a.V; ++v) {
-    if (tt[v] <= 0) continue;
-    float4 *g2 = reinterpret_cast<float4 *>(a.grad2d[v]) + 3 * size_t(i);
-    const float4 ga = g2[0], gb = g2[1], gc = g2[2];
-    const float4 z4 = make_float4(0.f, 0.f, 0.f, 0.f);
-    g2[0] = z4;  // leave the scratch zeroed for the next call
-    g2[1] = z4;
-    g2[2] = z4;
-    const float4 cn = __ldg(a.conic_o[v] + i);
-    double R[9], t[3];
-#pragma unroll
-    for (int k = 0; k < 9; ++k) R[k] = __ldg(&a.view[v]->R[k]);
-#pragma unroll
-    for (int k = 0; k < 3; ++k) t[k] = __ldg(&a.view[v]->t[k]);
-    const double gu = ga.x, gv = ga.y, gA = ga.z, gB = ga.w, gC = gb.x, gz = gb.y;
-    double p[3];
-#pragma unroll
-    for (int r = 0; r < 3; ++r) p[r] = R[3 * r] * mu[0] + R[3 * r + 1] * mu[1] + R[3 * r + 2] * mu[2] + t[r];
-    const double x = p[0], y = p[1], z = p[2];
-    double W[9], Sc[9];
-#pragma unroll
-    for (int r = 0; r < 3; ++r)
-#pragma unroll
-      for (int c = 0; c < 3; ++c) W[3 * r + c] = R[3 * r] * Sig[c] + R[3 * r + 1] * Sig[3 + c] + R[3 * r + 2] * Sig[6 + c];
-#pragma unroll
-    for (int r = 0; r < 3; ++r)
-#pragma unroll
-      for (int c = 0; c < 3; ++c) Sc[3 * r + c] = W[3 * r] * R[3 * c] + W[3 * r + 1] * R[3 * c + 1] + W[3 * r + 2] * R[3 * c + 2];
-    const double iz = 1.0 / z, iz2 = iz * iz, iz3 = iz2 * iz;
-    const double J0 = fx * iz, J2 = -fx * x * iz2, J4 = fy * iz, J5 = -fy * y * iz2;
-    // conic -> Sigma^I: G_S2 = -Conic G_M Conic, G_M = [[gA, gB/2], [gB/2, gC]]
-    const double A = cn.x, B = cn.y, C = cn.z;
-    const double hB = 0.5 * gB;
-    const double t00 = A * gA + B * hB, t01 = A * hB + B * gC, t10 = B * gA + C * hB, t11 = B * hB + C * gC;
-    const double S00 = -(t00 * A + t01 * B), S01 = -(t00 * B + t01 * C), S11 = -(t10 * B + t11 * C);
-    const double Jm[6] = {J0, 0.0, J2, 0.0, J4, J5};
-    const double GS2[4] = {S00, S01, S01, S11};
-    double GSc[9];
-#pragma unroll
-    for (int r = 0; r < 3; ++r)
-#pragma unroll
-      for (int c = 0; c < 3; ++c) {
-        double acc = 0.0;
-#pragma unroll
-        for (int u = 0; u < 2; ++u)
-#pragma unroll
-          for (int w = 0; w < 2; ++w) acc += Jm[3 * u + r] * GS2[2 * u + w] * Jm[3 * w + c];
-        GSc[3 * r + c] = acc;
-      }
-    double GJ0[6], GJ[6];
-#pragma unroll
-    for (int r = 0; r < 2; ++r)
-#pragma unroll
-      for (int c = 0; c < 3; ++c) GJ0[3 * r + c] = GS2[2 * r] * Jm[c] + GS2[2 * r + 1] * Jm[3 + c];
-#pragma unroll
-    for (int r = 0; r < 2; ++r)
-#pragma unroll
-      for (int c = 0; c < 3; ++c)
-        GJ[3 * r + c] = 2.0 * (GJ0[3 * r] * Sc[c] + GJ0[3 * r + 1] * Sc[3 + c] + GJ0[3 * r + 2] * Sc[6 + c]);
-    double gp[3];
-    gp[0] = gu * fx * iz - GJ[2] * fx * iz2;
-    gp[1] = gv * fy * iz - GJ[5] * fy * iz2;
-    gp[2] = -gu * fx * x * iz2 - gv * fy * y * iz2 + gz - GJ[0] * fx * iz2 + GJ[2] * 2.0 * fx * x * iz3 -
-            GJ[4] * fy * iz2 + GJ[5] * 2.0 * fy * y * iz3;
-#pragma unroll
-    for (int c = 0; c < 3; ++c) gmu[c] += R[c] * gp[0] + R[3 + c] * gp[1] + R[6 + c] * gp[2];
-    // G_Sigma += R^T G_Sc R
-    double tmp[9];
-#pragma unroll
-    for (int r = 0; r < 3; ++r)
-#pragma unroll
-      for (int c = 0; c < 3; ++c) tmp[3 * r + c] = R[r] * GSc[c] + R[3 + r] * GSc[3 + c] + R[6 + r] * GSc[6 + c];
-#pragma unroll
-    for (int r = 0; r < 3; ++r)
-#pragma unroll
-      for (int c = 0; c < 3; ++c) GSig[3 * r + c] += tmp[3 * r] * R[c] + tmp[3 * r + 1] * R[3 + c] + tmp[3 * r + 2] * R[6 + c];
-    glogit += gb.z;
-    grgb[0] += gc.x;
-    grgb[1] += gc.y;
-    grgb[2] += gc.z;
-  }
-  // G_M = 2 G_Sigma M; scales and quaternion once on the sum
-  double GM3[9];
-#pragma unroll
-  for (int r = 0; r < 3; ++r)
-#pragma unroll
-    for (int c = 0; c < 3; ++c)
-      GM3[3 * r + c] = 2.0 * (GSig[3 * r] * M[c] + GSig[3 * r + 1] * M[3 + c] + GSig[3 * r + 2] * M[6 + c]);
-  double gls[3], GRq[9];
-#pragma unroll
-  for (int k = 0; k < 3; ++k) {
-    gls[k] = s[k] * (GM3[k] * Rq[k] + GM3[3 + k] * Rq[3 + k] + GM3[6 + k] * Rq[6 + k]);
-#pragma unroll
-    for (int r = 0; r < 3; ++r) GRq[3 * r + k] = GM3[3 * r + k] * s[k];
-  }
-  const double gw = 2.0 * (-qz * GRq[1] + qy * GRq[2] + qz * GRq[3] - qx * GRq[5] - qy * GRq[6] + qx * GRq[7]);
-  const double gx = 2.0 * (qy * GRq[1] + qz * GRq[2] + qy * GRq[3] - 2.0 * qx * GRq[4] - qw * GRq[5] + qz * GRq[6] +
-                           qw * GRq[7] - 2.0 * qx * GRq[8]);
-  const double gy = 2.0 * (-2.0 * qy * GRq[0] + qx * GRq[1] + qw * GRq[2] + qx * GRq[3] + qz * GRq[5] - qw * GRq[6] +
-                           qz * GRq[7] - 2.0 * qy * GRq[8]);
-  const double gzq = 2.0 * (-2.0 * qz * GRq[0] - qw * GRq[1] + qx * GRq[2] + qw * GRq[3] - 2.0 * qz * GRq[4] +
-                            qy * GRq[5] + qx * GRq[6] + qy * GRq[7]);
-  const double dot = gw * qw + gx * qx + gy * qy + gzq * qz;
-  const float4 om = a.g_mean_opa[i], oq = a.g_quat[i], ol = a.g_logscale[i], oc = a.g_rgb[i];
-  a.g_mean_opa[i] = make_float4(float(om.x + gmu[0]), float(om.y + gmu[1]), float(om.z + gmu[2]), float(om.w + glogit));
-  a.g_quat[i] = make_float4(float(oq.x + (gw - qw * dot) * iq), float(oq.y + (gx - qx * dot) * iq),
-                            float(oq.z + (gy - qy * dot) * iq), float(oq.w + (gzq - qz * dot) * iq));
-  a.g_logscale[i] = make_float4(float(ol.x + gls[0]), float(ol.y + gls[1]), float(ol.z + gls[2]), ol.w);
-  a.g_rgb[i] = make_float4(float(oc.x + grgb[0]), float(oc.y + grgb[1]), float(oc.z + grgb[2]), oc.w);
-}
-
 }  // namespace gs
 
 extern "C" size_t gs_bwd_workspace_bytes(int32_t n) {
@@ -853,7 +684,7 @@ extern "C" int gs_render_bwd(gs_params p, const gs_view *view, gs_camera cam, gs
   BwdArgs b{reinterpret_cast<const double2 *>(pr.uv), reinterpret_cast<const float4 *>(pr.coef),
             reinterpret_cast<const float4 *>(pr.rgbz), reinterpret_cast<const float4 *>(pr.conic_o), sorted_idx,
             reinterpret_cast<const int2 *>(tile_range), tile_order, T_final, n_contrib, dL_dcolor, dL_ddepth, dL_dalpha,
-            cam.width, cam.height, tiles_x(cam), grad2d, tile_done};
+            cam.width, cam.height, tiles_x(cam), grad2d, tile_done, tiles_x(cam) * tiles_y(cam)};
   const int T = tiles_x(cam) * tiles_y(cam);
   if (run_pixels) {
     void (*kern)(BwdArgs) = want_params ? (dL_dalpha ? k_bwd_pixels<true, true> : k_bwd_pixels<true, false>)
@@ -878,37 +709,3 @@ extern "C" int gs_render_bwd(gs_params p, const gs_view *view, gs_camera cam, gs
 }
 
 
-extern "C" int gs_render_bwd_gauss_views(gs_params p, int32_t V, const gs_view *const *views, gs_camera cam,
-                                         const float *const *conic_o, const int32_t *const *tiles_touched,
-                                         float *const *ws, float *g_mean_opa, float *g_quat, float *g_logscale,
-                                         float *g_rgb, void *stream) {
-  using namespace gs;
-  if (p.n < 0 || V < 1 || V > kMaxGaussViews || !views || !conic_o || !tiles_touched || !ws || !camera_ok(cam) ||
-      !g_mean_opa || !g_quat || !g_logscale || !g_rgb || !aligned16(g_mean_opa) || !aligned16(g_quat) ||
-      !aligned16(g_logscale) || !aligned16(g_rgb)) {
-    set_error("gs_render_bwd_gauss_views: invalid argument (V=%d)", V);
-    return GS_ERR_INVALID_ARG;
-  }
-  if (p.n == 0) return GS_OK;
-  GaussViewsArgs a;
-  a.p = p;
-  a.V = V;
-  a.fx = cam.fx;
-  a.fy = cam.fy;
-  for (int v = 0; v < V; ++v) {
-    if (!views[v] || !conic_o[v] || !tiles_touched[v] || !ws[v] || !aligned16(conic_o[v]) || !aligned16(ws[v])) {
-      set_error("gs_render_bwd_gauss_views: null or misaligned array of view %d", v);
-      return GS_ERR_INVALID_ARG;
-    }
-    a.view[v] = views[v];
-    a.conic_o[v] = reinterpret_cast<const float4 *>(conic_o[v]);
-    a.tiles_touched[v] = tiles_touched[v];
-    a.grad2d[v] = ws[v];
-  }
-  a.g_mean_opa = reinterpret_cast<float4 *>(g_mean_opa);
-  a.g_quat = reinterpret_cast<float4 *>(g_quat);
-  a.g_logscale = reinterpret_cast<float4 *>(g_logscale);
-  a.g_rgb = reinterpret_cast<float4 *>(g_rgb);
-  k_bwd_gauss_views<<<(p.n + kGaussThreads - 1) / kGaussThreads, kGaussThreads, 0, as_stream(stream)>>>(a);
-  return check_launch("gs_render_bwd_gauss_views");
-}

@@ -37,9 +37,6 @@ struct FwdArgs {
   // per-tile completion flags for a programmatically dependent backward
   // (gs_render_bwd with the same tile_done); nullable
   uint32_t *tile_done;
-  // per-tile "list sorted" flags of the preceding gs_bin_sort (nullable):
-  // wait for this tile's flag instead of the whole sort
-  uint32_t *tile_sorted;
 };
 
 #ifndef FWD_NP
@@ -129,24 +126,11 @@ __global__ void __launch_bounds__(FG::kThreads, FWD_MINB) k_render_fwd(FwdArgs a
   __shared__ FwdRec s_rec[kBatch + 1];
   __shared__ unsigned char s_mask[kBatch];
   __shared__ unsigned char s_list[FG::kWarps][kBatch + 2];
+  // wait for the predecessor grid BEFORE reading any of its outputs (the
+  // launch order is written by the last kernel of gs_bin_sort); then the
+  // dependent backward of gs_render_fwd_l1(tile_done) may launch
+  pdl_begin();
   const int tile = a.tile_order ? __ldg(a.tile_order + blockIdx.x) : int(blockIdx.x);
-  if (kL1 && a.tile_sorted) {
-    // programmatic dependent of gs_bin_sort: every sort CTA has started, so
-    // this tile's flag is set in bounded time (the wait is capped)
-    pdl_trigger();
-    if (threadIdx.x == 0) {
-      uint32_t f = 0;
-      for (int it = 0; it < (1 << 20); ++it) {
-        asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(f) : "l"(a.tile_sorted + tile) : "memory");
-        if (f) break;
-        __nanosleep(64);
-      }
-      a.tile_sorted[tile] = 0u;  // re-armed for the next sort
-    }
-    __syncthreads();
-  } else {
-    pdl_begin();  // (the dependent backward of gs_render_fwd_l1(tile_done) may launch now)
-  }
   const int tx = tile % a.TX, ty = tile / a.TX;
   const int w = threadIdx.x >> 5;
   const PixGeom pg = pix_geom<FG>(tx, ty, a.H);
@@ -313,7 +297,7 @@ extern "C" int gs_render_fwd(gs_proj pr, const int32_t *sorted_idx, const int32_
   FwdArgs a{reinterpret_cast<const double2 *>(pr.uv), reinterpret_cast<const float4 *>(pr.coef),
             reinterpret_cast<const float4 *>(pr.rgbz), sorted_idx, reinterpret_cast<const int2 *>(tile_range),
             tile_order, cam.width, cam.height, tiles_x(cam), color, depth, alpha, T_final, n_contrib, stats,
-            tile_work, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};
+            tile_work, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};
   const int T = tiles_x(cam) * tiles_y(cam);
   if (stats)
     launch_pdl(k_render_fwd<true>, dim3(T), dim3(FG::kThreads), 0, as_stream(stream), a);
@@ -326,7 +310,7 @@ extern "C" int gs_render_fwd_l1(gs_proj pr, const int32_t *sorted_idx, const int
                                 const int32_t *tile_order, gs_camera cam, float *color, float *depth, float *alpha,
                                 float *T_final, int32_t *n_contrib, int32_t *tile_work, const float *tgt_color,
                                 const float *tgt_depth, const float *scales, float *dL_dcolor, float *dL_ddepth,
-                                double *loss_part, uint32_t *tile_done, uint32_t *tile_sorted, void *stream) {
+                                double *loss_part, uint32_t *tile_done, void *stream) {
   using namespace gs;
   if (!camera_ok(cam) || !tile_range || !color || !depth || !alpha || !T_final || !n_contrib || !tgt_color ||
       !tgt_depth || !scales || !dL_dcolor || !dL_ddepth) {
@@ -341,7 +325,7 @@ extern "C" int gs_render_fwd_l1(gs_proj pr, const int32_t *sorted_idx, const int
   FwdArgs a{reinterpret_cast<const double2 *>(pr.uv), reinterpret_cast<const float4 *>(pr.coef),
             reinterpret_cast<const float4 *>(pr.rgbz), sorted_idx, reinterpret_cast<const int2 *>(tile_range),
             tile_order, cam.width, cam.height, tiles_x(cam), color, depth, alpha, T_final, n_contrib, nullptr,
-            tile_work, tgt_color, tgt_depth, scales, dL_dcolor, dL_ddepth, loss_part, tile_done, tile_sorted};
+            tile_work, tgt_color, tgt_depth, scales, dL_dcolor, dL_ddepth, loss_part, tile_done};
   const int T = tiles_x(cam) * tiles_y(cam);
   launch_pdl(k_render_fwd<false, true>, dim3(T), dim3(FG::kThreads), 0, as_stream(stream), a);
   return check_launch("gs_render_fwd_l1");

@@ -19,7 +19,7 @@ import numpy as np
 import torch
 
 from .raster import (GS_BWD_ATOMIC_ACC, GS_BWD_GAUSS_ONLY, GS_BWD_PIXELS_ONLY, GS_GRAD_PARAMS, GS_GRAD_POSE, Grads, Params, Rasterizer,
-                     gs_loss_scales, gs_render_bwd_gauss_views, gs_unpack_rgbd, lib)
+                     gs_loss_scales, gs_unpack_rgbd, lib)
 
 
 class HostInputs:
@@ -95,15 +95,10 @@ class MapStep:
     """
 
     def __init__(self, params: Params, views, cam, tgt_color, tgt_depth, rank=0, world=1, group=None,
-                 lambda_color=1.0, lambda_depth=1.0, device="cuda", lanes=8, allreduce=None, schedule="lanes",
-                 ssim=0.0, fused_gauss=False, atomic_gauss=True, fused_loss=True):
+                 lambda_color=1.0, lambda_depth=1.0, device="cuda", lanes=8, allreduce=None,
+                 ssim=0.0, atomic_gauss=True, fused_loss=True):
         """ssim: the lambda of Eq. 10's colour loss (0: L1 colour only, as
-        BJ.configs[3]; the paper uses 0.2).  fused_gauss: when every view has
-        its own lane, run ONE per-Gaussian phase over all views
-        (gs_render_bwd_gauss_views) instead of a per-view S6 on each lane;
-        off by default: it sits on the step's critical path and measured
-        3.61 ms per BJ.configs[3] step against 3.15 ms for the overlapped
-        per-view phases (profiles/r01/README.md).  atomic_gauss: the
+        BJ.configs[3]; the paper uses 0.2).  atomic_gauss: the
         per-view S6 adds into the gradient buffer atomically
         (GS_BWD_ATOMIC_ACC), so the views' Gaussian phases need no ordering;
         else they are serialised in view order (events).  fused_loss (L1
@@ -133,12 +128,9 @@ class MapStep:
         self.losses = torch.zeros(max(len(self.mine), 1), 4, dtype=torch.float32, device=device)
         self.copy_stream = None  # host-input uploads (created on the first step(host=...))
         self._slots = None
-        self.schedule = schedule
-        self.fused_gauss = fused_gauss
         self.fused_loss = fused_loss  # used while self.ssim == 0 (the L1 loss is pixel-local)
         self.tgt_scales = {}
         self.atomic_gauss = atomic_gauss
-        self.stage_streams = [torch.cuda.Stream(device=device) for _ in range(3)] if schedule == "stages" else []
 
     def size(self, slack=1.25):
         """Setup only (host sync): pair capacity = slack x max pairs over my views."""
@@ -157,16 +149,23 @@ class MapStep:
             self.prepare_targets()
         return best
 
-    def overflowed(self):
+    def overflowed(self, collective=True):
         """Host sync: pair-capacity overflows the lanes' gs_bin_sort calls
         recorded (gs_counters.n_overflow; an overflowing view is rendered
-        empty) since the lanes' counters were last zeroed."""
-        return sum(int(r.counters[2].item()) for r in self.lanes)
+        empty) since the lanes' counters were last zeroed.  With world > 1
+        (and a process group) the MAX over ranks — a collective every rank
+        must call — so that all ranks take the same repeat decision."""
+        n = torch.stack([r.counters[2] for r in self.lanes]).sum().reshape(1)
+        if collective and self.world > 1 and torch.distributed.is_available() and torch.distributed.is_initialized():
+            torch.distributed.all_reduce(n, op=torch.distributed.ReduceOp.MAX, group=self.group)
+        return int(n.item())
 
     def step_checked(self, hooks=None, host=None, slack=1.25):
-        """step(); then, if a view overflowed its pair capacity, re-size the
-        lanes and run the step again (host sync).  For loops whose Gaussians
-        change between steps (mapping with the optimiser)."""
+        """step(); then, if a view of ANY rank overflowed its pair capacity,
+        every rank re-sizes its lanes and runs the step again (host sync; the
+        decision is collective, so the ranks' all-reduces stay paired, and the
+        repeated step starts from zeroed gradients).  For loops whose
+        Gaussians change between steps (mapping with the optimiser)."""
         g = self.step(hooks, host)
         if self.overflowed():
             self.size(slack)
@@ -217,17 +216,14 @@ class MapStep:
         """One mapping iteration.  hooks: optional dict overriding stages
         ("front", "fwd", "bwd", "gauss") with functions of the same signature.
 
-        Schedule "lanes" (default): view k runs all its stages on lane stream
-        k % lanes (8 lanes: every view of a BJ.configs[3] step in flight), so
-        the latency-bound binning of some views and the tails of the
-        compositing launches of others fill each other's idle SMs; the
-        per-Gaussian phases add atomically into the gradient buffer (or, with
-        atomic_gauss=False, are serialised in view order by events).
-        Schedule "stages": front stages on the lane streams, then one stream
-        each for the forward, the per-pixel and the per-Gaussian backward (a
-        software pipeline: no two compositing launches of one kind overlap;
-        measured 8% slower on BJ.configs[3] because the compositing tails
-        then stay idle).
+        View k runs all its stages on lane stream k % lanes (8 lanes: every
+        view of a BJ.configs[3] step in flight), so the latency-bound binning
+        of some views and the tails of the compositing launches of others
+        fill each other's idle SMs; the per-Gaussian phases add atomically
+        into the gradient buffer (or, with atomic_gauss=False, are serialised
+        in view order by events).  (Measured and dropped in round 1: one
+        stream per stage, 8% slower; one multi-view S6 after all pixel phases,
+        3.61 vs 3.15 ms per step.)
 
         host: optional HostInputs (pinned host buffers of this step's inputs).
         A copy stream uploads the parameters and poses, then every view's
@@ -287,53 +283,21 @@ class MapStep:
             main.wait_event(params_ready)
         self.grads.zero_()
         start = main.record_event()
-        for s in self.streams + self.stage_streams:
+        for s in self.streams:
             s.wait_event(start)
-        if self.schedule == "stages":
-            done = {}  # buffer set -> event after the last stage of the view that used it
-            for k, v in enumerate(self.mine):
-                lane = k % len(self.lanes)
-                r = self.lanes[lane]
-                ev = done.get(lane)  # view k reuses the buffers of view k - lanes
-                for i, name in enumerate(("front", "fwd", "bwd", "gauss")):
-                    s = self.streams[lane] if i == 0 else self.stage_streams[i - 1]
-                    if ev is not None:
-                        s.wait_event(ev)
-                    with torch.cuda.stream(s):
-                        if name == "fwd":
-                            fwd(r, k, v)
-                        else:
-                            st[name](r, k, v)
-                        ev = s.record_event()
-                done[lane] = ev
-        elif self.fused_gauss and len(self.mine) <= len(self.lanes) and "gauss" not in (hooks or {}):
-            # every view has its own buffers: the per-pixel phases run on the
-            # lanes, then ONE per-Gaussian phase over all views
-            # (gs_render_bwd_gauss_views: parameters read and gradients written once)
-            for k, v in enumerate(self.mine):
-                s, r = self.streams[k], self.lanes[k]
-                with torch.cuda.stream(s):
-                    st["front"](r, k, v)
-                    fwd(r, k, v)
-                    st["bwd"](r, k, v)
-            for s in self.streams:
-                main.wait_stream(s)
-            gs_render_bwd_gauss_views(self.params, [self.views[v] for v in self.mine], self.r.cam,
-                                      self.lanes[:len(self.mine)], self.grads)
-        else:
-            prev = start
-            for k, v in enumerate(self.mine):
-                lane = k % len(self.lanes)
-                s, r = self.streams[lane], self.lanes[lane]
-                with torch.cuda.stream(s):
-                    st["front"](r, k, v)
-                    fwd(r, k, v)
-                    st["bwd"](r, k, v)
-                    if not self.atomic_gauss:
-                        s.wait_event(prev)
-                    st["gauss"](r, k, v)
-                    prev = s.record_event()
-        for s in self.streams + self.stage_streams:
+        prev = start
+        for k, v in enumerate(self.mine):
+            lane = k % len(self.lanes)
+            s, r = self.streams[lane], self.lanes[lane]
+            with torch.cuda.stream(s):
+                st["front"](r, k, v)
+                fwd(r, k, v)
+                st["bwd"](r, k, v)
+                if not self.atomic_gauss:
+                    s.wait_event(prev)
+                st["gauss"](r, k, v)
+                prev = s.record_event()
+        for s in self.streams:
             main.wait_stream(s)
         if host is not None:
             main.wait_stream(self.copy_stream)
@@ -349,18 +313,24 @@ class MapStep:
         loss takes 1 launch (gs_loss_from_tiles) instead of gs_loss's 3."""
         per_view = kernels_per_view(self.r.cam, capacity=self.r.capacity) - (
             2 if self.fused_loss and self.ssim == 0.0 else 0)
-        if self.schedule == "lanes" and self.fused_gauss and len(self.mine) <= len(self.lanes):
-            return len(self.mine) * (per_view - 1) + 1
         return len(self.mine) * per_view
+
+
+def _sort_passes(cam):
+    """Radix passes of gs_bin_sort's depth sort (binsort.cu make_layout): the
+    keys span nbits(bits(z_far) - bits(z_near)) bits, <= 11 bits per pass."""
+    import struct
+    bits = lambda f: struct.unpack("<I", struct.pack("<f", f))[0]
+    nb = max(1, (bits(cam.z_far) - bits(cam.z_near)).bit_length())
+    return (nb + 10) // 11
 
 
 def kernels_per_view(cam, loss=True, bwd=True, capacity=0):
     """Kernels of ours per view (the sort's memset is a copy-engine node, not a kernel):
-    project 1; bin_sort: prep, tile counts, emit, tile sort, [mid-list sort when the
-    pair capacity averages <= 1800 per tile,] long-list sort = 5 or 6;
-    render 1 + backward tile order 1; loss 3; backward 2."""
-    T = ((cam.width + 15) // 16) * ((cam.height + 15) // 16)
-    n = 1 + (6 if capacity <= 1800 * T else 5) + 2
+    project 1; bin_sort: depth histogram, npass radix passes, tile counts, count
+    scan, emission (3 + npass + 1 = 7 for z 0.2..100 m); render 1 + backward tile
+    order 1; loss 3; backward 2."""
+    n = 1 + (4 + _sort_passes(cam)) + 2
     if loss:
         n += 3
     if bwd:
@@ -389,7 +359,7 @@ class TrackingLoop:
         self.tc, self.td = tgt_color, tgt_depth
         self.start = start_view.clone()
         self.view = start_view.clone()
-        self.adam = torch.zeros(13, dtype=torch.float32, device=device)
+        self.adam = torch.zeros(13, dtype=torch.float64, device=device)  # gs_pose_grad's fp64 Adam state
         self.dtwist = torch.zeros(6, dtype=torch.float32, device=device)
         self.iters = iters
         self.lc, self.ld = lambda_color, lambda_depth
@@ -420,6 +390,11 @@ class TrackingLoop:
                 r.compute_tracking_loss(self.tc, self.td, *self.masked)
         r.backward(self.params, self.view, GS_GRAD_POSE, overlap=self.overlap and self.masked is None and self.fused_loss)
         r.pose_grad(self.view, self.stepcfg, self.adam, dL_dtwist=self.dtwist)
+
+    def flag_timeouts(self):
+        """Host sync: timed-out waits of the overlapped backward (must be 0;
+        include/gs.h gs_render_bwd tile_done)."""
+        return self.r.flag_timeouts()
 
     def reset(self):
         self.view.copy_(self.start)

@@ -21,7 +21,7 @@ from ._lib import (GS_BWD_ATOMIC_ACC, GS_BWD_GAUSS_ONLY, GS_BWD_PIXELS_ONLY, GS_
                    GsParams, GsPoseStep, GsProj, GsView, check, lib)
 
 __all__ = ["Params", "Grads", "Proj", "Frame", "Rasterizer", "camera", "gs_project", "gs_bin_sort",
-           "gs_render_fwd", "gs_render_fwd_l1", "gs_loss_scales", "gs_loss_from_tiles", "gs_tile_order", "gs_loss", "gs_tracking_loss", "gs_ssim", "gs_iso_reg", "gs_adam_step", "gs_prune", "gs_seed", "gs_gradient_mask", "seed_first_keyframe", "gs_unpack_rgbd", "Optimizer", "gs_render_bwd", "gs_render_bwd_gauss_views", "gs_pose_grad", "GS_GRAD_PARAMS", "GS_GRAD_POSE", "GS_BWD_PIXELS_ONLY", "GS_BWD_GAUSS_ONLY", "GS_BWD_ATOMIC_ACC",
+           "gs_render_fwd", "gs_render_fwd_l1", "gs_loss_scales", "gs_loss_from_tiles", "gs_tile_order", "gs_loss", "gs_tracking_loss", "gs_ssim", "gs_iso_reg", "gs_adam_step", "gs_prune", "gs_seed", "gs_gradient_mask", "seed_first_keyframe", "gs_unpack_rgbd", "Optimizer", "gs_render_bwd", "gs_pose_grad", "GS_GRAD_PARAMS", "GS_GRAD_POSE", "GS_BWD_PIXELS_ONLY", "GS_BWD_GAUSS_ONLY", "GS_BWD_ATOMIC_ACC",
            "GsError", "device_check"]
 
 
@@ -143,10 +143,10 @@ def gs_project(params: Params, view, cam: GsCamera, proj: Proj, counters=None, s
 
 
 def gs_bin_sort(proj: Proj, n, cam: GsCamera, ws, capacity, sorted_idx, tile_range, n_pairs, counters=None,
-                stream=None, tile_order=None, sort_order=None, tile_sorted=None):
+                stream=None, tile_order=None):
     check(lib().gs_bin_sort(proj.c(), int(n), cam, _p(ws), ws.numel() * ws.element_size(), int(capacity),
                             _p(sorted_idx), _p(tile_range), _p(tile_order), _p(n_pairs), _p(counters),
-                            _p(sort_order), _p(tile_sorted), _stream(stream)), "gs_bin_sort")
+                            _stream(stream)), "gs_bin_sort")
 
 
 def gs_render_fwd(proj: Proj, sorted_idx, tile_range, cam: GsCamera, frame: Frame, stats=False, stream=None,
@@ -159,11 +159,11 @@ def gs_render_fwd(proj: Proj, sorted_idx, tile_range, cam: GsCamera, frame: Fram
 
 def gs_render_fwd_l1(proj: Proj, sorted_idx, tile_range, cam: GsCamera, frame: Frame, tgt_color, tgt_depth, scales,
                      dL_dcolor, dL_ddepth, stream=None, tile_order=None, tile_work=None, loss_part=None,
-                     tile_done=None, tile_sorted=None):
+                     tile_done=None):
     check(lib().gs_render_fwd_l1(proj.c(), _p(sorted_idx), _p(tile_range), _p(tile_order), cam, _p(frame.color),
                                  _p(frame.depth), _p(frame.alpha), _p(frame.T_final), _p(frame.n_contrib),
                                  _p(tile_work), _p(tgt_color), _p(tgt_depth), _p(scales), _p(dL_dcolor),
-                                 _p(dL_ddepth), _p(loss_part), _p(tile_done), _p(tile_sorted), _stream(stream)),
+                                 _p(dL_ddepth), _p(loss_part), _p(tile_done), _stream(stream)),
           "gs_render_fwd_l1")
 
 
@@ -327,18 +327,6 @@ def gs_render_bwd(params: Params, view, cam: GsCamera, proj: Proj, sorted_idx, t
         event_pair[1].record(torch.cuda.current_stream() if stream is None else stream)
 
 
-def gs_render_bwd_gauss_views(params: Params, views, cam: GsCamera, rasterizers, grads: "Grads", stream=None):
-    """S6 over several views: views = list of device view tensors [12] (one per
-    rasterizer, after its GS_BWD_PIXELS_ONLY backward)."""
-    V = len(views)
-    arr = lambda xs: (C.c_void_p * V)(*[x.value if isinstance(x, C.c_void_p) else x for x in xs])
-    check(lib().gs_render_bwd_gauss_views(
-        params.c(), V, arr([v.data_ptr() for v in views]), cam,
-        arr([r.proj.conic_o.data_ptr() for r in rasterizers]), arr([r.proj.tiles_touched.data_ptr() for r in rasterizers]),
-        arr([r.bwd_ws.data_ptr() for r in rasterizers]), _p(grads.mean_opa), _p(grads.quat), _p(grads.logscale),
-        _p(grads.rgb), _stream(stream)), "gs_render_bwd_gauss_views")
-
-
 def gs_pose_grad(view, pose_partials, n_partials, step=None, adam_state=None, dL_dview=None, dL_dtwist=None,
                  dL_dqt=None, stream=None):
     st = None
@@ -382,14 +370,7 @@ class Rasterizer:
         self.tl_ws = None  # gs_tracking_loss workspace, allocated on first use
         self.scales = None  # gs_loss_scales output (forward_l1)
         self.loss_part = None  # per-tile |residual| sums (render_l1)
-        self.tile_done = None  # per-tile forward -> backward flags (overlap)
-        self.tile_sorted = None  # per-tile sort -> forward flags (overlap)
-        # forward_l1(reuse_order, overlap): also start the forward tile by tile
-        # as the sort finishes (gs_bin_sort tile_sorted) / run the sort in the
-        # forward's order; both measured slower on BJ.configs[2] (2457 vs
-        # 2502 it/s: the waiting CTAs hold SM slots), so off by default
-        self.sort_overlap = False
-        self.sort_in_fwd_order = False
+        self.tile_done = None  # per-tile forward -> backward flags (overlap) + timeout count
         self.tl_loss = None
         self.dL_dcolor = torch.zeros(3, H, W, dtype=torch.float32, device=device)
         self.dL_ddepth = torch.zeros(H, W, dtype=torch.float32, device=device)
@@ -474,9 +455,14 @@ class Rasterizer:
         return self.loss
 
     def _tile_done(self):
-        if self.tile_done is None:
-            self.tile_done = torch.zeros(self.T, dtype=torch.int32, device=self.device)
+        if self.tile_done is None:  # [T] flags + [1] count of timed-out waits (include/gs.h)
+            self.tile_done = torch.zeros(self.T + 1, dtype=torch.int32, device=self.device)
         return self.tile_done
+
+    def flag_timeouts(self):
+        """Host sync: capped tile_done waits of the overlapped backward that
+        timed out (0 unless the forward -> backward ordering was broken)."""
+        return 0 if self.tile_done is None else int(self.tile_done[self.T].item())
 
     def forward_l1(self, params: Params, view, tgt_color, tgt_depth, reuse_order=False, refresh_order=True,
                    overlap=False):
@@ -490,23 +476,15 @@ class Rasterizer:
         next backward(overlap=True) starts while this forward finishes, tile
         by tile (per-tile flags + programmatic dependent launch)."""
         self.project(params, view)
-        sorted_flags = None
-        if reuse_order:
-            # the sort runs in the forward's launch order; with overlap the
-            # forward starts every tile as soon as its list is sorted
-            if overlap and self.sort_overlap:
-                if self.tile_sorted is None:
-                    self.tile_sorted = torch.zeros(self.T, dtype=torch.int32, device=self.device)
-                sorted_flags = self.tile_sorted
+        if reuse_order:  # no launch order for the sort: the forward reuses the previous work order
             gs_bin_sort(self.proj, self.n, self.cam, self.sort_ws, self.capacity, self.sorted_idx, self.tile_range,
-                        self.n_pairs, self.counters, tile_order=None,
-                        sort_order=self.bwd_order if self.sort_in_fwd_order else None, tile_sorted=sorted_flags)
+                        self.n_pairs, self.counters, tile_order=None)
         else:
             self.bin_sort()
         gs_render_fwd_l1(self.proj, self.sorted_idx, self.tile_range, self.cam, self.frame, tgt_color, tgt_depth,
                          self.scales, self.dL_dcolor, self.dL_ddepth,
                          tile_order=self.bwd_order if reuse_order else self.tile_order, tile_work=self.tile_work,
-                         tile_done=self._tile_done() if overlap else None, tile_sorted=sorted_flags)
+                         tile_done=self._tile_done() if overlap else None)
         if refresh_order or not reuse_order:
             gs_tile_order(self.tile_work, self.T, self.bwd_order)
         return self.frame

@@ -85,3 +85,59 @@ def gpu_backward(r, P, v, gC, gD, gA=None, flags=GS_GRAD_PARAMS):
 
 
 __all__ = ["GS_GRAD_PARAMS", "GS_GRAD_POSE", "oracle"]
+
+
+def small_submap(seed=5, n=40_000, V=4):
+    """BJ.configs[3] reduced: n Gaussians, V views of 320x184 on the 1 m arc."""
+    from paper_2312_10070_b200 import inputs
+    s = inputs.config3(seed=seed, n=n, n_views=V)
+    s.cam = inputs.Camera(320, 184, 160.0, 160.0, 159.5, 91.5)
+    return s
+
+
+def oracle_mapping_reference(s, ambig_residual=1e-5):
+    """The fp64 oracle's mapping iteration over all views of scene s (Eq. 12
+    L1 colour + depth, lambda = 1/V per view, R20): targets = the oracle's
+    render of the perturbed copy rounded to fp32 (fed to both sides);
+    per view the ambiguous pixels (R2 margin <= AMBIG, or a colour / valid
+    depth residual within ambig_residual of 0, R21), whose upstream maps are
+    zeroed on both sides; the summed gradient g3 [n,16] and its R23 scale m3,
+    and the per-view losses (total, colour, depth) of the unmodified loss."""
+    V = s.views.shape[0]
+    p64 = oracle.params64(*s.params())
+    tp = oracle.params64(*s.extra["target_params"])
+    out = dict(tc={}, td={}, amb={}, loss=np.zeros((V, 3)), g3=np.zeros((s.n, 16)), m3=np.zeros((s.n, 16)))
+    for v in range(V):
+        view = s.views[v].astype(np.float64)
+        tgt = oracle.forward(tp, view, s.cam)
+        tc = tgt["color"].astype(np.float32)
+        td = tgt["depth"].astype(np.float32)
+        fr = oracle.forward(p64, view, s.cam)
+        L, gc, gd = oracle.loss(s.cam, fr["color"], fr["depth"], tc, td, None, 1.0 / V, 1.0 / V)
+        amb = (fr["margin"] <= AMBIG) | (np.abs(fr["color"] - tc) < ambig_residual).any(0) | (
+            (td > 0) & (np.abs(fr["depth"] - td) < ambig_residual))
+        gc[:, amb] = 0.0
+        gd[amb] = 0.0
+        b = oracle.backward(p64, view, s.cam, fr["sorted_idx"], fr["tile_range"], gc, gd)
+        out["tc"][v], out["td"][v], out["amb"][v] = tc, td, amb
+        out["loss"][v] = L
+        out["g3"] += b["g3"]
+        out["m3"] += b["m3"]
+    return out
+
+
+def zero_upstream_hook(ms, amb_dev):
+    """A MapStep "bwd" stage hook: zero the view's loss-gradient maps at the
+    oracle's ambiguous pixels (R2 treatment), then the ordinary per-pixel
+    backward stage (on the lane's stream)."""
+    def bwd(r, k, v):
+        m = amb_dev[v]
+        r.dL_dcolor.masked_fill_(m.unsqueeze(0).expand_as(r.dL_dcolor), 0.0)
+        r.dL_ddepth.masked_fill_(m, 0.0)
+        ms.stage_bwd(r, k, v)
+    return bwd
+
+
+def grads_as_g3(g):
+    """A Grads buffer [4, n, 4] in the oracle's g3 layout [n, 16]."""
+    return np.concatenate([to_np(g.mean_opa), to_np(g.quat), to_np(g.logscale), to_np(g.rgb)], 1)

@@ -67,6 +67,14 @@ def test_full_projection_and_binning_bit_exact(full):
 def test_full_render_sampled_tiles(full):
     s, fr = full["s"], full["fr"]
     g = gpu_frame(full["r"])
+    # every tile rendered, in a permutation order; n_contrib within each tile's list (all pixels)
+    r = full["r"]
+    T, TX = r.T, (s.cam.width + 15) // 16
+    assert np.array_equal(np.sort(to_np(r.tile_order)), np.arange(T))
+    rng = to_np(r.tile_range).reshape(-1, 2)
+    ln = (rng[:, 1] - rng[:, 0]).repeat(16).reshape(-1, TX * 16)  # [TY, TX * 16] list length per column
+    ln = np.repeat(ln, 16, axis=0)[:s.cam.height, :s.cam.width]
+    assert ((g["n_contrib"] >= 0) & (g["n_contrib"] <= ln)).all()
     sel = _pixel_mask(s.cam, full["tmask"]) & (fr["margin"] > AMBIG)
     assert sel.sum() > 0.95 * _pixel_mask(s.cam, full["tmask"]).sum()
     for key in ("depth", "alpha", "T_final"):
@@ -152,6 +160,7 @@ def test_tracking_graph_converges_and_matches_eager():
     loop.run()
     torch.cuda.synchronize()
     graph = to_np(loop.view).astype(np.float64)
+    assert loop.flag_timeouts() == 0
     # both runs recover the GT pose (identity); they are not bit-identical
     # because the fp32 atomics of the backward sum in a different order
     for pose in (eager, graph):

@@ -253,6 +253,78 @@ def test_pose_parity(case):
     tw = oracle.pose_twist(ob["pose"], oracle_view(s))
     ok, st = grad_check(to_np(dtw), tw, twist_magnitude(ob["mpose"], oracle_view(s)))
     assert ok.all(), (st, to_np(dtw), tw)
+    q = _quat_wxyz(oracle_view(s))  # (q, t) of T_wc (R22)
+    ok, st = grad_check(to_np(dqt)[:4], oracle.pose_qt(ob["pose"], q), qt_magnitude(ob["mpose"][:9], q))
+    assert ok.all(), (st, to_np(dqt)[:4])
+    ok, st = grad_check(to_np(dqt)[4:], ob["pose"][9:], ob["mpose"][9:])
+    assert ok.all(), st
+
+
+def _quat_wxyz(view):
+    """Unit quaternion (w, x, y, z), w >= 0, of the view's rotation (scipy,
+    the nearest rotation of the fp32 matrix)."""
+    from scipy.spatial.transform import Rotation
+    x, y, z, w = Rotation.from_matrix(np.asarray(view[:9], np.float64).reshape(3, 3)).as_quat()
+    q = np.array([w, x, y, z])
+    return -q if q[0] < 0 else q
+
+
+def qt_magnitude(mR, q):
+    """|.|-propagation of the dL/dR magnitudes through dL/dq = (I - q q^T)
+    sum_i dL/dR_i dR_i/dq (R22): m_k = sum_i |dR_i/dq_k| m_i +
+    |q_k| sum_l |q_l| sum_i |dR_i/dq_l| m_i."""
+    w, x, y, z = q
+    D = np.array([[0, -2 * z, 2 * y, 2 * z, 0, -2 * x, -2 * y, 2 * x, 0],
+                  [0, 2 * y, 2 * z, 2 * y, -4 * x, -2 * w, 2 * z, 2 * w, -4 * x],
+                  [-4 * y, 2 * x, 2 * w, 2 * x, 0, 2 * z, -2 * w, 2 * z, -4 * y],
+                  [-4 * z, -2 * w, 2 * x, 2 * w, -4 * z, 2 * y, 2 * x, 2 * y, 0]])
+    raw = np.abs(D) @ mR
+    return raw + np.abs(q) * (np.abs(q) @ raw)
+
+
+def test_pose_qt_and_device_adam_steps_match_oracle():
+    """S7 (R22, R28): gs_pose_grad's dL/d(q, t) of T_wc against oracle.pose_qt
+    and three device Adam steps with the exp-map retraction (view and fp64 Adam
+    state) against oracle.pose_adam, on fixed synthetic pose partials.  Both
+    sides follow their own trajectory (the oracle never sees a GPU value); the
+    GPU stores the view in fp32 (and re-orthonormalises R), so the views agree
+    to ~1e-7 and the twists (linear in R, t) to ~1e-7 relative."""
+    from paper_2312_10070_b200.raster import gs_pose_grad
+    rng = np.random.default_rng(17)
+    n_part = 37
+    parts = rng.normal(0.0, 1.0, (n_part, 12)).astype(np.float32)
+    view0 = _tilted(4)
+    step = (2e-3, 1e-3, 0.9, 0.999, 1e-8)
+    d = torch.device("cuda")
+    v = torch.as_tensor(view0, device=d).contiguous()
+    tparts = torch.as_tensor(parts, device=d)
+    adam = torch.zeros(13, dtype=torch.float64, device=d)
+    pose = parts.astype(np.float64).sum(0)                       # the fp64 reduction of the partials
+    mpose = np.abs(parts.astype(np.float64)).sum(0)
+    vo, st = view0.astype(np.float64), np.zeros(13)
+    for k in range(3):
+        dview = torch.zeros(12, device=d)
+        dtw = torch.zeros(6, device=d)
+        dqt = torch.zeros(7, device=d)
+        gs_pose_grad(v, tparts, n_part, step, adam, dL_dview=dview, dL_dtwist=dtw, dL_dqt=dqt)
+        torch.cuda.synchronize()
+        # gradients at the view before the step
+        assert np.allclose(to_np(dview), pose, rtol=1e-6, atol=1e-6 * mpose.max())
+        tw = oracle.pose_twist(pose, vo)
+        ok, st_tw = grad_check(to_np(dtw), tw, twist_magnitude(mpose, vo))
+        assert ok.all(), (k, st_tw, to_np(dtw), tw)
+        q = _quat_wxyz(vo)
+        gq = oracle.pose_qt(pose, q)
+        ok, st_q = grad_check(to_np(dqt)[:4], gq, qt_magnitude(mpose[:9], q))
+        assert ok.all(), (k, st_q, to_np(dqt)[:4], gq)
+        assert np.array_equal(to_np(dqt)[4:], to_np(dview)[9:])   # dL/dt of (q, t) = dL/dt
+        vo, st = oracle.pose_adam(vo, tw, st, lr=step[:2], hyp=step[2:])
+        gv, ga = to_np(v).astype(np.float64), to_np(adam)
+        assert np.abs(gv - vo).max() <= 2e-6, (k, gv, vo)
+        assert ga[12] == st[12] == k + 1
+        assert np.allclose(ga[:6], st[:6], rtol=1e-5, atol=1e-9 * np.abs(st[:6]).max())
+        assert np.allclose(ga[6:12], st[6:12], rtol=1e-5, atol=0)
+        log("pose_adam", step=k, view_err=float(np.abs(gv - vo).max()), qt=st_q, twist=st_tw)
 
 
 def twist_magnitude(mpose, view):
@@ -352,37 +424,3 @@ def test_bin_sort_tile_order_by_list_length():
     assert np.array_equal(np.sort(o), np.arange(len(L)))
     b = 63 - (L[o] * 64) // (int(L.max()) + 1)
     assert (np.diff(b) >= 0).all()
-
-
-@pytest.mark.parametrize("case", ["config1", "overflow", "empty"])
-def test_bin_sort_sorted_flags_and_launch_order(case):
-    """gs_bin_sort(sort_order, tile_sorted): the same bins as the plain call
-    (bit-exact), every tile flag released (also on overflow and with no
-    pairs), for a flag-waiting forward."""
-    import torch
-    from paper_2312_10070_b200 import Params, Rasterizer
-    from paper_2312_10070_b200.raster import gs_bin_sort
-    s = inputs.config1() if case != "empty" else inputs.random_scene(61, 0, 64, 48)
-    d = torch.device("cuda")
-    P = Params.from_numpy(*s.params(), device=d)
-    v = torch.as_tensor(s.views[0], device=d)
-    r = Rasterizer(s.n, s.cam, device=d)
-    r.size_for(P, v)
-    if case == "overflow":
-        r.set_capacity(1000)
-    r.project(P, v)
-    r.bin_sort()
-    torch.cuda.synchronize()
-    ref_idx, ref_rng = r.sorted_idx.clone(), r.tile_range.clone()
-    T = r.T
-    order = torch.as_tensor(np.random.default_rng(1).permutation(T).astype(np.int32), device=d)
-    flags = torch.zeros(T, dtype=torch.int32, device=d)
-    r.sorted_idx.fill_(-1)
-    gs_bin_sort(r.proj, r.n, r.cam, r.sort_ws, r.capacity, r.sorted_idx, r.tile_range, r.n_pairs, r.counters,
-                tile_order=None, sort_order=order, tile_sorted=flags)
-    torch.cuda.synchronize()
-    assert int(flags.sum()) == T
-    assert torch.equal(r.tile_range, ref_rng)
-    if case == "config1":
-        P_ = int(r.n_pairs.item())
-        assert torch.equal(r.sorted_idx[:P_], ref_idx[:P_])

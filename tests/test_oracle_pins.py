@@ -544,3 +544,173 @@ def test_adam_first_step(orc):
     xi = -np.concatenate([2e-3 * np.sign(g[:3]), 1e-3 * np.sign(g[3:])]) * (1 / (1 + 1e-8 / np.abs(g)))
     ref = _twist_apply(IDV, xi)
     assert np.allclose(view, ref, atol=1e-12) and st[12] == 1
+
+
+# --------------------------------------------------------------------------
+# R23 magnitude scales m2, m3, mpose and the R2 decision margin: they set the
+# slack of every GPU parity check, so they are pinned here against definitions
+# computed independently of the oracle's backward.
+
+G2_FIELDS = ("u", "v", "A", "B", "C", "logit", "r", "g", "b", "pz")
+
+
+@pytest.mark.parametrize("seed", range(4))
+def test_magnitude_scales_bound_the_gradients(orc, seed):
+    """R23: m* >= |g*| componentwise (2-D, 3-D and pose) on random scenes
+    (every inner sum of m* is a sum of absolute values of g*'s terms)."""
+    s = inputs.random_scene(100 + seed, 30, 40, 32, spread=1.0, ls=(-2.2, 0.4), lo=(0.5, 1.0))
+    p = s.params64()
+    view = np.concatenate([Rotation.from_rotvec([0.04, -0.02, 0.03]).as_matrix().reshape(9), [0.01, 0.02, -0.03]])
+    fr = orc.forward(p, view, s.cam)
+    rng = np.random.default_rng(seed)
+    G = (rng.standard_normal((3, 32, 40)), rng.standard_normal((32, 40)), rng.standard_normal((32, 40)))
+    b = orc.backward(p, view, s.cam, fr["sorted_idx"], fr["tile_range"], *G)
+    for g, m in (("g2", "m2"), ("g3", "m3"), ("pose", "mpose")):
+        assert (b[m] >= np.abs(b[g]) * (1 - 1e-12)).all(), g
+        assert (b[m] > np.abs(b[g]) * 1.01).any(), g  # and not merely |g*| (cancellation is counted)
+
+
+def _one_gaussian(cam, z=2.0, dy_px=1.3, logit=1.2, ls=-2.0):
+    """One isotropic Gaussian at camera x = 0 (so Sigma^I is diagonal: B = 0),
+    dy_px pixels below the principal point."""
+    return _params([[0.0, dy_px * z / cam.fy, z]], [[ls, ls, ls]], [logit], [[0.8, 0.5, 0.3]])
+
+
+def test_magnitude_scale_equals_gradient_on_single_pixel(orc):
+    """R23 on a 1-Gaussian, 1-pixel scene with same-sign upstream terms: every
+    absolute-value sum of m2 has one term, so m2 == |g2| exactly (dx = 0 here:
+    the u and A components vanish on both sides)."""
+    cam = _cam(1, 1, 50.0, cx=0.0, cy=0.0)
+    p = _one_gaussian(cam, dy_px=0.7)
+    fr = orc.forward(p, IDV, cam)
+    G = (np.full((3, 1, 1), 0.6), np.full((1, 1), 0.4), np.full((1, 1), 0.9))
+    b = orc.backward(p, IDV, cam, fr["sorted_idx"], fr["tile_range"], *G)
+    assert fr["n_contrib"][0, 0] == 1
+    assert np.allclose(b["m2"], np.abs(b["g2"]), rtol=1e-13, atol=0)
+    assert (np.abs(b["g2"][0, [1, 4, 5, 6, 7, 8, 9]]) > 0).all()
+
+
+def test_magnitude_scale_is_sum_of_per_pixel_fd_gradients(orc):
+    """R23's m2 = sum over pixels of |per-pixel contribution|: one Gaussian
+    (B = 0, same-sign upstream and colours, so every inner sum is one-signed),
+    each pixel's contribution to dL/d(u, v, A, B, C, logit, rgb, p_z) by central
+    finite differences of that pixel's value through orc.render with the 2-D
+    quantities perturbed directly (no backward code involved)."""
+    cam = _cam(24, 20, 60.0)
+    p = _one_gaussian(cam, dy_px=1.6, ls=-2.6)
+    fr = orc.forward(p, IDV, cam)
+    pr, idx, rng_ = fr["proj"], fr["sorted_idx"], fr["tile_range"]
+    assert abs(pr["conic"][0, 1]) < 1e-18
+    rgen = np.random.default_rng(9)
+    G = (rgen.uniform(0.2, 1.0, (3, 20, 24)), rgen.uniform(0.2, 1.0, (20, 24)), rgen.uniform(0.2, 1.0, (20, 24)))
+    b = orc.backward(p, IDV, cam, idx, rng_, *G)
+
+    def per_px(prx, rgb):
+        o = orc.render(prx, rgb, idx, rng_, cam)
+        return (G[0] * o["color"]).sum(0) + G[1] * o["depth"] + G[2] * o["alpha"], o["sig"]
+
+    base_sig = per_px(pr, p["rgb"])[1]
+    h = 1e-6
+    for j, name in enumerate(G2_FIELDS):
+        vals = []
+        for sgn in (1.0, -1.0):
+            q = {k: v.copy() for k, v in pr.items()}
+            rgb = p["rgb"].copy()
+            if name in ("u", "v"):
+                q["uv"][0, "uv".index(name)] += sgn * h
+            elif name in ("A", "B", "C"):
+                q["conic"][0, "ABC".index(name)] += sgn * h
+            elif name == "logit":
+                q["opac"][0] = 1.0 / (1.0 + np.exp(-(p["logit"][0] + sgn * h)))
+            elif name in ("r", "g", "b"):
+                rgb[0, "rgb".index(name)] += sgn * h
+            else:
+                q["pz"][0] += sgn * h
+            L, sig = per_px(q, rgb)
+            assert np.array_equal(sig, base_sig), name  # no decision flips at this h
+            vals.append(L)
+        contrib = (vals[0] - vals[1]) / (2 * h)
+        # the oracle's conic B term enters sigma as 2 B dx dy: dL/dB there is the
+        # coefficient of the symmetric off-diagonal, as g2 defines it
+        assert np.isclose(b["g2"][0, j], contrib.sum(), rtol=1e-6, atol=1e-9), name
+        assert np.isclose(b["m2"][0, j], np.abs(contrib).sum(), rtol=1e-6, atol=1e-9), name
+
+
+def _x2d(orc, p, view, cam):
+    """The 2-D quantities of every Gaussian (oracle projection): [n, 10] in g2 order."""
+    pr = orc.project(p, view, cam)
+    return np.concatenate([pr["uv"], pr["conic"], p["logit"][:, None], p["rgb"], pr["pz"][:, None]], 1)
+
+
+def test_magnitude_scales_3d_and_pose_are_abs_jacobian_of_m2(orc):
+    """R23: m3 = |d x2D / d theta|^T m2 per Gaussian and mpose = sum_g
+    |d x2D_g / d(R, t)|^T m2_g, with the Jacobian of the 2-D quantities taken by
+    central finite differences of orc.project (not the backward's chain)."""
+    s = inputs.random_scene(77, 8, 40, 32, spread=0.8, ls=(-2.2, 0.3), lo=(0.5, 1.0))
+    p = s.params64()
+    view = np.concatenate([Rotation.from_rotvec([0.03, 0.05, -0.02]).as_matrix().reshape(9), [0.02, -0.01, 0.04]])
+    fr = orc.forward(p, view, s.cam)
+    rng = np.random.default_rng(5)
+    G = (rng.standard_normal((3, 32, 40)), rng.standard_normal((32, 40)), rng.standard_normal((32, 40)))
+    b = orc.backward(p, view, s.cam, fr["sorted_idx"], fr["tile_range"], *G)
+    vis = fr["proj"]["culled"] == 0
+    assert vis.sum() >= 6
+    h = 1e-6
+    fields = [("mean", 3, 0), ("logit", None, 3), ("quat", 4, 4), ("logscale", 3, 8), ("rgb", 3, 12)]
+    m3 = np.zeros((s.n, 16))
+    for name, width, off in fields:
+        for c in range(width or 1):
+            pp = {k: v.copy() for k, v in p.items()}
+            pm = {k: v.copy() for k, v in p.items()}
+            if width is None:
+                pp[name] += h
+                pm[name] -= h
+            else:
+                pp[name][:, c] += h
+                pm[name][:, c] -= h
+            J = (_x2d(orc, pp, view, s.cam) - _x2d(orc, pm, view, s.cam)) / (2 * h)  # [n, 10], per Gaussian
+            m3[:, off + c] = (np.abs(J) * b["m2"]).sum(1)
+    assert np.allclose(b["m3"][vis], m3[vis], rtol=2e-5, atol=1e-12 * np.abs(m3).max())
+    assert (b["m3"][~vis] == 0).all()
+    mpose = np.zeros(12)
+    for k in range(12):
+        vp, vm = view.copy(), view.copy()
+        vp[k] += h
+        vm[k] -= h
+        J = (_x2d(orc, p, vp, s.cam) - _x2d(orc, p, vm, s.cam)) / (2 * h)
+        mpose[k] = (np.abs(J[vis]) * b["m2"][vis]).sum()
+    assert np.allclose(b["mpose"], mpose, rtol=2e-5)
+
+
+def test_decision_margin_brute_force(orc):
+    """R2: the per-pixel minimum relative decision margin, recomputed by a
+    brute-force numpy walk over each pixel's tile list (alpha~ against 1/255
+    and 0.999 at every scanned entry, T against 1e-4 after every composited
+    entry, stopping where the pixel stops)."""
+    s = inputs.random_scene(88, 18, 32, 32, spread=0.9, ls=(-2.0, 0.4), lo=(1.0, 1.5))
+    p = s.params64()
+    fr = orc.forward(p, IDV, s.cam)
+    pr = fr["proj"]
+    amin, amax, teps = (np.float64(np.float32(x)) for x in (1 / 255, 0.999, 1e-4))
+    TX = (s.cam.width + 15) // 16
+    ref = np.full((32, 32), np.inf)
+    for j in range(32):
+        for i in range(32):
+            t = (j // 16) * TX + i // 16
+            T, mg = 1.0, np.inf
+            for k in range(*fr["tile_range"][t]):
+                g = fr["sorted_idx"][k]
+                dx, dy = pr["uv"][g, 0] - i, pr["uv"][g, 1] - j
+                A, B, C = pr["conic"][g]
+                at = pr["opac"][g] * np.exp(-0.5 * (A * dx * dx + 2 * B * dx * dy + C * dy * dy))
+                mg = min(mg, abs(at - amin) / amin, abs(at - amax) / amax)
+                a = min(at, amax)
+                if a < amin:
+                    continue
+                T = T * (1 - a)
+                mg = min(mg, abs(T - teps) / teps)
+                if T < teps:
+                    break
+            ref[j, i] = mg
+    assert np.allclose(fr["margin"], ref, rtol=1e-9, atol=0)
+    assert np.isfinite(ref).mean() > 0.5 and (ref < 1e-2).any()
