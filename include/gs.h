@@ -148,9 +148,9 @@ int32_t gs_num_tiles(gs_camera cam);
 
 /* Workspace bytes gs_bin_sort needs for n Gaussians, a pair capacity and
  * camera `cam`: ~24 bytes per Gaussian (the depth sort's key / id ping-pong
- * and the ordered tile rects) + 4 bytes per (tile, 1024..4096 Gaussians) of
- * per-CTA tile counts + look-back words; independent of the capacity.  0 if
- * unsupported (> 2^21 tiles, n >= 2^30, capacity >= 2^31 - 1, or a tile grid
+ * the ordered tile rects and the pair prefix) + 4 bytes per (tile, 32768 pairs
+ * of capacity) of per-CTA tile counts + look-back words.  0 if
+ * unsupported (> 2^21 tiles, n >= 2^30, capacity >= 2^30, or a tile grid
  * too large for the emission CTA's shared memory: > ~33k tiles). */
 size_t gs_binsort_workspace_bytes(int32_t n, int64_t capacity, gs_camera cam);
 

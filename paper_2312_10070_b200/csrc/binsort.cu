@@ -16,18 +16,23 @@
 //      and the radix sort is stable on ascending ids: the result is the
 //      (depth, id) order.  The last pass also scatters the Gaussians' tile
 //      rects into that order.
-//   2. k_bin_count: CTA b takes the b-th run of 256 x wb Gaussians of that
-//      order and counts its pairs per tile (shared-memory counters).
-//   3. k_bin_scan: per tile, the exclusive scan of the CTA counts (a warp per
+//   2. k_bin_prefix: the exclusive prefix of the tile counts over that order
+//      (decoupled look-back), i.e. the position of every Gaussian's first pair
+//      in the flat list F of all pairs in (Gaussian order, rect row-major)
+//      order, P = |F|, and for every warp of the next kernels the Gaussian
+//      holding its first slot: the pairs, not the Gaussians, are split evenly
+//      (near splats have large rects and come first in the order).
+//   3. k_bin_count: warp g takes the slots [g C, (g + 1) C) of F (C = 32768 /
+//      wb), its CTA counts its pairs per tile (shared-memory counters).
+//   4. k_bin_scan: per tile, the exclusive scan of the CTA counts (a warp per
 //      tile) and the tile total.
-//   4. k_bin_emit: per CTA, the tile starts (scan of the totals), the pair
-//      count and capacity check, per-warp per-tile offsets (each warp counts
-//      its own 256 Gaussians again), then every warp walks its Gaussians in
-//      order, 32 (Gaussian, tile) pairs per step; pairs of one step that hit
-//      the same tile come from increasing positions in the order and are
-//      ranked by __match_any_sync, so every tile's list receives its
-//      Gaussians exactly in (depth, id) order.  CTA 0 also writes the tile
-//      ranges, P, the overflow counter and the heaviest-first tile order.
+//   5. k_bin_emit: per CTA, the tile starts (scan of the totals), the capacity
+//      check, per-warp per-tile offsets (each warp counts its own slots
+//      again), then every warp walks its slots in order, 32 per step; slots
+//      of one step that hit the same tile come from increasing positions in
+//      the order and are ranked by __match_any_sync, so every tile's list
+//      receives its Gaussians exactly in (depth, id) order.  CTA 0 also writes
+//      the tile ranges, P, the overflow counter and the heaviest-first order.
 // Everything is integer arithmetic on the fp32 depth bits: the output is
 // bit-deterministic (no atomics decide a position).
 #include <algorithm>
@@ -43,7 +48,7 @@ constexpr int kDsItems = 8;                     // keys per thread
 constexpr int kDsTile = kDsThreads * kDsItems;  // 4096 keys per sort-pass CTA
 constexpr int kDsMaxBits = 11;                  // digit bits per pass (<= 2048 digits)
 constexpr int kHistThreads = 256;
-constexpr int kWarpGauss = 256;                 // Gaussians per warp in count / emit
+constexpr int kBlockPairs = 32768;              // pair slots per count / emit CTA (wb warps)
 constexpr uint32_t kFlagAgg = 1u << 30, kFlagInc = 2u << 30, kValMask = (1u << 30) - 1u;
 
 struct BinLayout {
@@ -53,9 +58,9 @@ struct BinLayout {
   int npass, dbits, ndig;
   int gsort;  // sort-pass CTAs (from n)
   int wb;     // warps per count / emit CTA
-  int gbin;   // count / emit CTAs (from n)
-  size_t hist, ctr, status, zero_end;
-  size_t key0, val0, key1, val1, srect, cnt, totals, total;
+  int gbin;   // count / emit CTAs (from the capacity)
+  size_t hist, ctr, status, pstatus, misc, zero_end;
+  size_t key0, val0, key1, val1, srect, pre, wstart, cnt, totals, total;
 };
 
 static size_t align_up(size_t x) { return (x + 255) & ~size_t(255); }
@@ -88,7 +93,7 @@ static bool make_layout(int32_t n, int64_t capacity, const gs_camera &cam, BinLa
   L.TX = tiles_x(cam);
   L.TY = tiles_y(cam);
   L.T = L.TX * L.TY;
-  if (L.T > (1 << 21) || capacity >= (int64_t(1) << 31) - 1 || n >= (1 << 30)) return false;
+  if (L.T > (1 << 21) || capacity >= (int64_t(1) << 30) || n >= (1 << 30)) return false;
   L.wb = bin_warps(L.T);
   if (L.wb == 0) return false;
   L.kbase = f2u(cam.z_near);
@@ -99,7 +104,8 @@ static bool make_layout(int32_t n, int64_t capacity, const gs_camera &cam, BinLa
   L.ndig = 1 << L.dbits;
   const int nn = n > 0 ? n : 1;
   L.gsort = (nn + kDsTile - 1) / kDsTile;
-  L.gbin = (nn + L.wb * kWarpGauss - 1) / (L.wb * kWarpGauss);
+  const int64_t cap = capacity > 0 ? capacity : 1;
+  L.gbin = int((cap + kBlockPairs - 1) / kBlockPairs);
   size_t off = 0;
   auto take = [&](size_t bytes) {
     size_t o = off;
@@ -109,12 +115,16 @@ static bool make_layout(int32_t n, int64_t capacity, const gs_camera &cam, BinLa
   L.hist = take(size_t(4) * L.npass * L.ndig);
   L.ctr = take(4 * 8);
   L.status = take(size_t(4) * L.npass * L.gsort * L.ndig);
+  L.pstatus = take(size_t(4) * L.gsort);  // k_bin_prefix look-back words
+  L.misc = take(4 * 8);                   // [0] P
   L.zero_end = off;
   L.key0 = take(size_t(4) * nn);
   L.val0 = take(size_t(4) * nn);
   L.key1 = take(size_t(4) * nn);
   L.val1 = take(size_t(4) * nn);
   L.srect = take(size_t(8) * nn);
+  L.pre = take(size_t(4) * nn);
+  L.wstart = take(size_t(4) * L.gbin * L.wb);
   L.cnt = take(size_t(4) * L.T * L.gbin);
   L.totals = take(size_t(4) * L.T);
   L.total = off;
@@ -345,7 +355,13 @@ struct BinArgs {
   int ndig;
   const uint32_t *ids;    // [nvis] Gaussian ids in (depth, id) order
   const short4 *srect;    // [nvis] their rects
-  int TX, TY, T, gbin;
+  uint32_t *pre;          // [nvis] flat position of each Gaussian's first pair
+  uint32_t *wstart;       // [gbin wb] per warp: the Gaussian holding its first slot
+  uint32_t *pstatus;      // [gsort] k_bin_prefix look-back words
+  uint32_t *ctr;          // virtual CTA counter of k_bin_prefix
+  uint32_t *misc;         // [0] P
+  int TX, TY, T, gbin, wb;
+  uint32_t cw;            // pair slots per warp (kBlockPairs / wb)
   uint32_t *cnt;          // [T][gbin]: CTA counts -> exclusive prefix over CTAs
   uint32_t *totals;       // [T]
   int64_t capacity;
@@ -362,78 +378,146 @@ __device__ __forceinline__ uint32_t visible_count(const BinArgs &a, uint32_t *sh
   return total;
 }
 
-// The (Gaussian, tile) pairs of one warp round: lane j's Gaussian has rect
-// r (x0 > x1: none).  Every pair slot p of the round's flat list (lane j's
-// tiles in row-major rect order, lanes in order) is handed to f(j, tile, valid)
-// 32 at a time; all lanes call f every step (valid = false past the end).
-template <class F>
-__device__ __forceinline__ void for_round_pairs(short4 r, int TX, F &&f) {
-  const int lane = threadIdx.x & 31;
-  const int wdt = r.z - r.x + 1;
-  const int nt = (r.z >= r.x && r.w >= r.y) ? wdt * (r.w - r.y + 1) : 0;
-  const int incl = int(warp_incl_scan(uint32_t(nt)));
-  const int total = __shfl_sync(0xffffffffu, incl, 31);
-  const int xy = (int(r.x) & 0xffff) | (int(r.y) << 16);
-  // row = local / wdt as a multiply-high (exact for local, wdt < 2^16)
-  const uint32_t magic = wdt > 1 ? uint32_t((0x100000000ull + uint64_t(wdt) - 1) / uint64_t(wdt)) : 0u;
-  for (int p0 = 0; p0 < total; p0 += 32) {
-    const int p = p0 + lane;
-    // j = number of lanes whose inclusive prefix is <= p
-    int j = 0;
+__device__ __forceinline__ uint32_t rect_area(short4 r) {
+  return (r.z >= r.x && r.w >= r.y) ? uint32_t(r.z - r.x + 1) * uint32_t(r.w - r.y + 1) : 0u;
+}
+
+// Exclusive prefix of the tile counts over the (depth, id) order: 4096
+// Gaussians per CTA (512 threads x 8 consecutive), decoupled look-back on the
+// CTA sums; also the first Gaussian of every warp's slot range and P.
+__global__ void __launch_bounds__(kDsThreads) k_bin_prefix(BinArgs a) {
+  pdl_begin();
+  __shared__ uint32_t sh[33];
+  __shared__ int s_vb;
+  __shared__ uint32_t s_ex;
+  const uint32_t nvis = visible_count(a, sh);
+  if (threadIdx.x == 0) s_vb = int(atomicAdd(a.ctr, 1u));
+  __syncthreads();
+  const int vb = s_vb;
+  if (vb * kDsTile >= int(nvis)) return;
+  const int k0 = vb * kDsTile + threadIdx.x * kDsItems;
+  uint32_t c[kDsItems], sum = 0;
 #pragma unroll
-    for (int b = 16; b > 0; b >>= 1) {
-      const int v = __shfl_sync(0xffffffffu, incl, j + b - 1);
-      j += v <= p ? b : 0;
+  for (int k = 0; k < kDsItems; ++k) {
+    c[k] = k0 + k < int(nvis) ? rect_area(a.srect[k0 + k]) : 0u;
+    sum += c[k];
+  }
+  uint32_t tot;
+  uint32_t ex = block_excl_scan(sum, sh, tot);
+  if (threadIdx.x == 0) {
+    uint32_t e = 0;
+    if (vb == 0) {
+      st_release(a.pstatus, kFlagInc | tot);
+    } else {
+      st_release(a.pstatus + vb, kFlagAgg | tot);
+      for (int j = vb - 1; j >= 0;) {
+        const uint32_t s = ld_acquire(a.pstatus + j);
+        if (!(s & ~kValMask)) continue;  // not published yet: spin
+        e += s & kValMask;
+        if (s & kFlagInc) break;
+        --j;
+      }
+      st_release(a.pstatus + vb, kFlagInc | (e + tot));
     }
-    j = min(j, 31);
-    const int ij = __shfl_sync(0xffffffffu, incl, j), nj = __shfl_sync(0xffffffffu, nt, j);
-    const int wj = __shfl_sync(0xffffffffu, wdt, j), xyj = __shfl_sync(0xffffffffu, xy, j);
-    const uint32_t mj = __shfl_sync(0xffffffffu, magic, j);
-    int tile = 0;
-    const bool valid = p < total;
-    if (valid) {
-      const int local = p - (ij - nj);
-      const int row = wj == 1 ? local : (nj < 65536 ? int(__umulhi(uint32_t(local), mj)) : local / wj);
-      const int col = local - row * wj;
-      tile = ((xyj >> 16) + row) * TX + (xyj & 0xffff) + col;
-    }
-    f(j, tile, valid);
+    s_ex = e;
+    if ((vb + 1) * kDsTile >= int(nvis)) a.misc[0] = e + tot;  // the last CTA: P
+  }
+  __syncthreads();
+  ex += s_ex;
+#pragma unroll
+  for (int k = 0; k < kDsItems; ++k) {
+    if (k0 + k >= int(nvis)) break;
+    a.pre[k0 + k] = ex;
+    // warp slot ranges starting inside this Gaussian's pairs
+    for (uint32_t q = (ex + a.cw - 1) / a.cw * a.cw; q < ex + c[k]; q += a.cw) a.wstart[q / a.cw] = uint32_t(k0 + k);
+    ex += c[k];
   }
 }
 
-// this warp's Gaussians: positions [(b wb + w) 256, + 256) of the order
-__device__ __forceinline__ int warp_first(int wb) {
-  return (int(blockIdx.x) * wb + int(threadIdx.x >> 5)) * kWarpGauss;
+// The pairs of flat slots [q0, q1) of F, warp-wide, 32 per step, starting at
+// Gaussian k (the one holding slot q0): f(j, tile, valid, kw) per step, where
+// lane j of the current window of 32 Gaussians (kw = its first) holds the
+// slot's Gaussian; all lanes call f every step (valid = false past the end).
+template <class F>
+__device__ __forceinline__ void for_warp_pairs(const BinArgs &a, uint32_t nvis, uint32_t q0, uint32_t q1, int k,
+                                               F &&f) {
+  const int lane = threadIdx.x & 31;
+  for (;; k += 32) {
+    const int kk = k + lane;
+    const short4 r = kk < int(nvis) ? a.srect[kk] : make_short4(0, 0, -1, -1);
+    const uint32_t Q = a.pre[k];
+    const int wdt = r.z - r.x + 1;
+    const int nt = int(rect_area(r));
+    const int incl = int(warp_incl_scan(uint32_t(nt)));
+    const uint32_t total = uint32_t(__shfl_sync(0xffffffffu, incl, 31));
+    const int xy = (int(r.x) & 0xffff) | (int(r.y) << 16);
+    // row = floor(local / wdt) as floor((local + 0.5) (1 / wdt)) in fp32: exact
+    // (local < 2^22; the quotient is >= 0.5 / wdt away from an integer)
+    const float iw = 1.0f / float(max(wdt, 1));
+    const uint32_t pa = q0 > Q ? q0 - Q : 0u, pb = min(q1 - Q, total);
+    for (uint32_t p0 = pa; p0 < pb; p0 += 32) {
+      const int p = int(p0) + lane;
+      // j = number of lanes whose inclusive prefix is <= p
+      int j = 0;
+#pragma unroll
+      for (int b = 16; b > 0; b >>= 1) {
+        const int v = __shfl_sync(0xffffffffu, incl, j + b - 1);
+        j += v <= p ? b : 0;
+      }
+      j = min(j, 31);
+      const int ij = __shfl_sync(0xffffffffu, incl, j), nj = __shfl_sync(0xffffffffu, nt, j);
+      const int xyj = __shfl_sync(0xffffffffu, xy, j), wj = __shfl_sync(0xffffffffu, wdt, j);
+      const float iwj = __shfl_sync(0xffffffffu, iw, j);
+      int tile = 0;
+      const bool valid = uint32_t(p) < pb;
+      if (valid) {
+        const int local = p - (ij - nj);
+        const int row = int((float(local) + 0.5f) * iwj);
+        const int col = local - row * wj;
+        tile = ((xyj >> 16) + row) * a.TX + (xyj & 0xffff) + col;
+      }
+      f(j, tile, valid, k);
+    }
+    if (Q + total >= q1) break;
+  }
+}
+
+// P and this warp's slot range [q0, q1) (empty past P)
+__device__ __forceinline__ void warp_slots(const BinArgs &a, uint32_t P, uint32_t &q0, uint32_t &q1, int &k) {
+  const uint32_t g = blockIdx.x * a.wb + (threadIdx.x >> 5);
+  q0 = g * a.cw;
+  q1 = min(q0 + a.cw, P);
+  k = q0 < P ? int(a.wstart[g]) : 0;
 }
 
 __global__ void __launch_bounds__(512) k_bin_count(BinArgs a) {
   pdl_begin();
   extern __shared__ uint32_t s_c[];  // [T]
   __shared__ uint32_t sh[33];
-  const int wb = blockDim.x >> 5, lane = threadIdx.x & 31;
   const uint32_t nvis = visible_count(a, sh);
-  if (int(blockIdx.x) * wb * kWarpGauss >= int(nvis)) return;  // k_bin_scan reads only the CTAs holding Gaussians
+  const uint32_t P = nvis ? a.misc[0] : 0u;
+  if (uint64_t(blockIdx.x) * kBlockPairs >= P) return;  // k_bin_scan reads only the CTAs holding pairs
   for (int t = threadIdx.x; t < a.T; t += blockDim.x) s_c[t] = 0;
   __syncthreads();
-  const int g0 = warp_first(wb);
-  for (int r0 = 0; r0 < kWarpGauss; r0 += 32) {
-    const int k = g0 + r0 + lane;
-    const short4 r = k < int(nvis) ? a.srect[k] : make_short4(0, 0, -1, -1);
-    for_round_pairs(r, a.TX, [&](int, int tile, bool valid) {
+  uint32_t q0, q1;
+  int k;
+  warp_slots(a, P, q0, q1, k);
+  if (q0 < q1)
+    for_warp_pairs(a, nvis, q0, q1, k, [&](int, int tile, bool valid, int) {
       if (valid) atomicAdd(&s_c[tile], 1u);
     });
-  }
   __syncthreads();
   for (int t = threadIdx.x; t < a.T; t += blockDim.x) a.cnt[size_t(t) * a.gbin + blockIdx.x] = s_c[t];
 }
 
 // one warp per tile: exclusive scan of its CTA counts, the tile total
-__global__ void __launch_bounds__(256) k_bin_scan(BinArgs a, int wb) {
+__global__ void __launch_bounds__(256) k_bin_scan(BinArgs a) {
   pdl_begin();
   __shared__ uint32_t sh[33];
   const int lane = threadIdx.x & 31;
   const uint32_t nvis = visible_count(a, sh);
-  const int nb = (int(nvis) + wb * kWarpGauss - 1) / (wb * kWarpGauss);
+  const uint32_t P = nvis ? a.misc[0] : 0u;
+  const int nb = min(int((uint64_t(P) + kBlockPairs - 1) / kBlockPairs), a.gbin);
   const int t = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   if (t >= a.T) return;
   uint32_t *c = a.cnt + size_t(t) * a.gbin;
@@ -454,45 +538,47 @@ __global__ void __launch_bounds__(512) k_bin_emit(BinArgs a) {
   __shared__ uint32_t sh[33];
   __shared__ unsigned s_b[64];
   __shared__ uint32_t s_max;
-  const int wb = blockDim.x >> 5, lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int wb = a.wb, lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const int T = a.T;
   uint32_t *s_base = s_e;
   uint16_t *s_off = reinterpret_cast<uint16_t *>(s_e + T);
   const uint32_t nvis = visible_count(a, sh);
-  const bool has = int(blockIdx.x) * wb * kWarpGauss < int(nvis);
-  if (!has && blockIdx.x != 0) return;
-  // tile starts: exclusive scan of the totals; P
-  for (int t = threadIdx.x; t < T; t += blockDim.x) s_base[t] = a.totals[t];
-  __syncthreads();
-  const uint32_t P = block_excl_scan_array(s_base, T, sh);
+  const uint32_t P = nvis ? a.misc[0] : 0u;
   const bool over = int64_t(P) > a.capacity;
+  const bool has = !over && uint64_t(blockIdx.x) * kBlockPairs < P;
+  if (!has && blockIdx.x != 0) return;
+  // the tile totals (no pair: never computed; overflow: the lists stay empty)
+  auto total_of = [&](int t) { return (over || P == 0) ? 0u : a.totals[t]; };
+  // tile starts: exclusive scan of the totals
+  for (int t = threadIdx.x; t < T; t += blockDim.x) s_base[t] = total_of(t);
+  __syncthreads();
+  block_excl_scan_array(s_base, T, sh);
   if (blockIdx.x == 0) {
     for (int t = threadIdx.x; t < T; t += blockDim.x) {
       const int st = int(s_base[t]);
-      reinterpret_cast<int2 *>(a.tile_range)[t] = over ? make_int2(0, 0) : make_int2(st, st + int(a.totals[t]));
+      reinterpret_cast<int2 *>(a.tile_range)[t] = make_int2(st, st + int(total_of(t)));
     }
     if (threadIdx.x == 0) {
       *a.n_pairs = int64_t(P);
       if (over && a.cntrs) atomicAdd(reinterpret_cast<unsigned long long *>(&a.cntrs->n_overflow), 1ull);
     }
   }
-  if (!over && has) {
+  if (has) {
     // this CTA's base per tile, per-warp counts (each warp its own row)
     for (int t = threadIdx.x; t < T; t += blockDim.x) s_base[t] += a.cnt[size_t(t) * a.gbin + blockIdx.x];
     for (int i = threadIdx.x; i < (wb * T + 1) / 2; i += blockDim.x) reinterpret_cast<uint32_t *>(s_off)[i] = 0u;
     __syncthreads();
     uint16_t *row = s_off + w * T;
-    const int g0 = warp_first(wb);
-    for (int r0 = 0; r0 < kWarpGauss; r0 += 32) {
-      const int k = g0 + r0 + lane;
-      const short4 r = k < int(nvis) ? a.srect[k] : make_short4(0, 0, -1, -1);
-      for_round_pairs(r, a.TX, [&](int, int tile, bool valid) {
+    uint32_t q0, q1;
+    int k;
+    warp_slots(a, P, q0, q1, k);
+    if (q0 < q1)
+      for_warp_pairs(a, nvis, q0, q1, k, [&](int, int tile, bool valid, int) {
         // lanes of one step that hit the same tile form a match group
         const unsigned g = __match_any_sync(0xffffffffu, valid ? tile : -1);
         if (valid && lane == __ffs(g) - 1) row[tile] = uint16_t(row[tile] + __popc(g));
         __syncwarp();
       });
-    }
     __syncthreads();
     // per tile: exclusive prefix over the warps
     for (int t = threadIdx.x; t < T; t += blockDim.x) {
@@ -507,18 +593,16 @@ __global__ void __launch_bounds__(512) k_bin_emit(BinArgs a) {
     // emission in order: position = tile base + warp offset + pairs of this
     // tile earlier in the warp's walk (earlier steps: the running offset;
     // this step: lanes below in the match group, which hold earlier Gaussians)
-    for (int r0 = 0; r0 < kWarpGauss; r0 += 32) {
-      const int k = g0 + r0 + lane;
-      const bool in = k < int(nvis);
-      const short4 r = in ? a.srect[k] : make_short4(0, 0, -1, -1);
-      const int id = in ? int(a.ids[k]) : 0;
-      for_round_pairs(r, a.TX, [&](int j, int tile, bool valid) {
+    if (q0 < q1) {
+      int kw = -1, id = 0;
+      for_warp_pairs(a, nvis, q0, q1, k, [&](int j, int tile, bool valid, int kwin) {
+        if (kwin != kw) {  // a new window of 32 Gaussians: their ids
+          kw = kwin;
+          id = kw + lane < int(nvis) ? int(a.ids[kw + lane]) : 0;
+        }
         const int gid = __shfl_sync(0xffffffffu, id, j);
         const unsigned g = __match_any_sync(0xffffffffu, valid ? tile : -1);
-        if (valid) {
-          const uint32_t pos = s_base[tile] + row[tile] + __popc(g & lanemask_lt());
-          a.sorted_idx[pos] = gid;
-        }
+        if (valid) a.sorted_idx[s_base[tile] + row[tile] + __popc(g & lanemask_lt())] = gid;
         __syncwarp();
         if (valid && lane == __ffs(g) - 1) row[tile] = uint16_t(row[tile] + __popc(g));
         __syncwarp();
@@ -533,11 +617,12 @@ __global__ void __launch_bounds__(512) k_bin_emit(BinArgs a) {
   if (threadIdx.x < 64) s_b[threadIdx.x] = 0;
   __syncthreads();
   uint32_t m = 0;
-  for (int t = threadIdx.x; t < T; t += blockDim.x) m = max(m, a.totals[t]);
+  for (int t = threadIdx.x; t < T; t += blockDim.x) m = max(m, total_of(t));
   atomicMax(&s_max, m);
   __syncthreads();
   const int64_t den = int64_t(s_max) + 1;
-  for (int t = threadIdx.x; t < T; t += blockDim.x) atomicAdd(&s_b[63 - int(int64_t(a.totals[t]) * 64 / den)], 1u);
+  for (int t = threadIdx.x; t < T; t += blockDim.x)
+    atomicAdd(&s_b[63 - int(int64_t(total_of(t)) * 64 / den)], 1u);
   __syncthreads();
   if (threadIdx.x == 0) {
     unsigned run = 0;
@@ -549,7 +634,7 @@ __global__ void __launch_bounds__(512) k_bin_emit(BinArgs a) {
   }
   __syncthreads();
   for (int t = threadIdx.x; t < T; t += blockDim.x)
-    a.tile_order[atomicAdd(&s_b[63 - int(int64_t(a.totals[t]) * 64 / den)], 1u)] = t;
+    a.tile_order[atomicAdd(&s_b[63 - int(int64_t(total_of(t)) * 64 / den)], 1u)] = t;
 }
 
 // Tiles by descending work, 64 buckets of max/64 (single CTA).
@@ -642,16 +727,16 @@ extern "C" int gs_bin_sort(gs_proj pr, int32_t n, gs_camera cam, void *ws, size_
     cudaFuncSetAttribute(k_bin_emit, cudaFuncAttributeMaxDynamicSharedMemorySize, int(std::max(emit_smem, size_t(48) << 10)));
     smem_set = need;
   }
-  BinArgs b{U(L.hist), L.ndig, ids, reinterpret_cast<const short4 *>(w + L.srect), L.TX, L.TY, L.T, L.gbin,
+  BinArgs b{U(L.hist), L.ndig, ids, reinterpret_cast<const short4 *>(w + L.srect), U(L.pre), U(L.wstart),
+            U(L.pstatus), U(L.ctr) + 4, U(L.misc), L.TX, L.TY, L.T, L.gbin, L.wb, uint32_t(kBlockPairs / L.wb),
             U(L.cnt), U(L.totals), capacity, sorted_idx, tile_range, tile_order, n_pairs, cnt};
   if (n > 0) {
     const int hb = std::max(1, std::min(2 * 148, (n + 4 * kHistThreads - 1) / (4 * kHistThreads)));
     launch_pdl(k_ds_hist, dim3(hb), dim3(kHistThreads), size_t(4) * L.npass * L.ndig, s, d);
     for (int p = 0; p < L.npass; ++p) launch_pdl(k_ds_pass, dim3(L.gsort), dim3(kDsThreads), ds_smem, s, d, p);
+    launch_pdl(k_bin_prefix, dim3(L.gsort), dim3(kDsThreads), 0, s, b);
     launch_pdl(k_bin_count, dim3(L.gbin), dim3(32 * L.wb), cnt_smem, s, b);
-    launch_pdl(k_bin_scan, dim3((L.T + 7) / 8), dim3(256), 0, s, b, L.wb);
-  } else {
-    cudaMemsetAsync(w + L.totals, 0, size_t(4) * L.T, s);
+    launch_pdl(k_bin_scan, dim3((L.T + 7) / 8), dim3(256), 0, s, b);
   }
   launch_pdl(k_bin_emit, dim3(L.gbin), dim3(32 * L.wb), emit_smem, s, b);
   return check_launch("gs_bin_sort");

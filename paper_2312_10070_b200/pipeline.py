@@ -327,10 +327,10 @@ def _sort_passes(cam):
 
 def kernels_per_view(cam, loss=True, bwd=True, capacity=0):
     """Kernels of ours per view (the sort's memset is a copy-engine node, not a kernel):
-    project 1; bin_sort: depth histogram, npass radix passes, tile counts, count
-    scan, emission (3 + npass + 1 = 7 for z 0.2..100 m); render 1 + backward tile
-    order 1; loss 3; backward 2."""
-    n = 1 + (4 + _sort_passes(cam)) + 2
+    project 1; bin_sort: depth histogram, npass radix passes, pair prefix, tile
+    counts, count scan, emission (5 + npass = 8 for z 0.2..100 m); render 1 +
+    backward tile order 1; loss 3; backward 2."""
+    n = 1 + (5 + _sort_passes(cam)) + 2
     if loss:
         n += 3
     if bwd:
