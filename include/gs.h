@@ -147,11 +147,9 @@ int gs_check_device(int device, int *sm_count);
 int32_t gs_num_tiles(gs_camera cam);
 
 /* Workspace bytes gs_bin_sort needs for n Gaussians, a pair capacity and
- * camera `cam`: ~24 bytes per Gaussian (the depth sort's key / id ping-pong
- * the ordered tile rects and the pair prefix) + 4 bytes per (tile, 32768 pairs
- * of capacity) of per-CTA tile counts + look-back words.  0 if
- * unsupported (> 2^21 tiles, n >= 2^30, capacity >= 2^30, or a tile grid
- * too large for the emission CTA's shared memory: > ~33k tiles). */
+ * camera `cam`: ~12 bytes per pair of capacity (scratch of the exact sort of
+ * long tile lists) + 12 bytes per tile.  0 if unsupported (> 2^21 tiles or
+ * capacity >= 2^31 - 1). */
 size_t gs_binsort_workspace_bytes(int32_t n, int64_t capacity, gs_camera cam);
 
 /* Workspace bytes gs_loss needs for camera `cam`. */
@@ -196,12 +194,11 @@ int gs_project(gs_params p, const gs_view *view, gs_camera cam, gs_proj out,
  *
  * Emits one (tile, Gaussian) pair per tile of each visible Gaussian's rect and
  * orders all pairs by the key (tile asc, fp32 depth asc, Gaussian id asc):
- * a stable radix sort of the visible Gaussians by depth, then a stable
- * per-tile counting pass over that order (bit-deterministic; no atomics
- * decide a position).
+ * pairs are emitted into per-tile segments, then every segment is sorted
+ * exactly on (depth bits, id) (bit-deterministic whatever the order of the
+ * emission's atomics).
  *   pr.depth, pr.rect, pr.tiles_touched (device) inputs from gs_project
- *   ws/ws_bytes   (device, 16-byte aligned) workspace >=
- *                 gs_binsort_workspace_bytes(n, capacity, cam)
+ *   ws/ws_bytes   (device) workspace >= gs_binsort_workspace_bytes(n, capacity, cam)
  *   capacity      length of sorted_idx
  *   sorted_idx    (device) [capacity] Gaussian ids, tile-major
  *   tile_range    (device) [T][2] int32 [start, end) into sorted_idx

@@ -2,39 +2,30 @@
 // ("m ordered Gaussians"; R10).
 //
 // Result = every (tile, Gaussian) pair ordered by the composite key
-// (tile asc, fp32 depth asc, Gaussian id asc).  No per-tile sort: the
-// visible Gaussians are put in (depth, id) order ONCE, then every tile's list
-// is filled by a stable counting pass over that order.
-//   1. k_ds_hist + k_ds_pass x npass: stable LSD radix sort of the visible
-//      Gaussians (tiles_touched > 0) by their fp32 depth bits relative to
-//      bits(z_near) (visible depths lie in [z_near, z_far], so the keys span
-//      nbits(bits(z_far) - bits(z_near)) bits: 27 for 0.2 / 100 m -> 3
-//      passes of 9-bit digits).  One histogram kernel for all passes; every
-//      pass ranks its 4096-key tile stably per warp (ballot-sliced peer
-//      masks), gets its digit offsets from the earlier tiles by decoupled
-//      look-back, and scatters.  Positive floats order as their bit patterns
-//      and the radix sort is stable on ascending ids: the result is the
-//      (depth, id) order.  The last pass also scatters the Gaussians' tile
-//      rects into that order.
-//   2. k_bin_prefix: the exclusive prefix of the tile counts over that order
-//      (decoupled look-back), i.e. the position of every Gaussian's first pair
-//      in the flat list F of all pairs in (Gaussian order, rect row-major)
-//      order, P = |F|, and for every warp of the next kernels the Gaussian
-//      holding its first slot: the pairs, not the Gaussians, are split evenly
-//      (near splats have large rects and come first in the order).
-//   3. k_bin_count: warp g takes the slots [g C, (g + 1) C) of F (C = 32768 /
-//      wb), its CTA counts its pairs per tile (shared-memory counters).
-//   4. k_bin_scan: per tile, the exclusive scan of the CTA counts (a warp per
-//      tile) and the tile total.
-//   5. k_bin_emit: per CTA, the tile starts (scan of the totals), the capacity
-//      check, per-warp per-tile offsets (each warp counts its own slots
-//      again), then every warp walks its slots in order, 32 per step; slots
-//      of one step that hit the same tile come from increasing positions in
-//      the order and are ranked by __match_any_sync, so every tile's list
-//      receives its Gaussians exactly in (depth, id) order.  CTA 0 also writes
-//      the tile ranges, P, the overflow counter and the heaviest-first order.
-// Everything is integer arithmetic on the fp32 depth bits: the output is
-// bit-deterministic (no atomics decide a position).
+// (tile asc, fp32 depth asc, Gaussian id asc).  Built tile by tile, with no
+// global sort and no pass whose blocks wait on each other:
+//   1. k_bin_prep: per-tile pair counts from a 2-D difference array of the
+//      tile rects (4 shared-memory updates per visible Gaussian, merged into
+//      one global array per block);
+//   2. k_tile_counts (one CTA): 2-D prefix -> counts -> tile ranges (scan),
+//      the capacity check, per-tile write cursors and the heaviest-first
+//      launch order;
+//   3. k_emit: every visible Gaussian appends its id to the segment of each
+//      tile of its rect (block-aggregated: shared-memory counts, one global
+//      cursor reservation per (block, tile), warp-balanced pair expansion);
+//      the order inside a segment is arbitrary at this point;
+//   4. k_tile_sort: one CTA per tile sorts its segment in shared memory in
+//      one pass: a counting sort on the top 11 bits of (depth bits - tile
+//      minimum), then every entry ranked inside its bucket (~n / 2048
+//      entries) on the exact key (depth bits, id).  Segments longer than 4096
+//      entries, or with a bucket of more than 128 (a dense cluster of depths
+//      next to a far outlier), are left to k_tile_sort_big: an exact two-key
+//      stable LSD radix sort (id digits, then depth digits; 9-bit digits,
+//      warp ranks from ballot-sliced peer masks) chunk by chunk over global
+//      memory.
+// Everything is integer arithmetic on the fp32 depth bits (positive floats
+// order as their bit patterns): the output is bit-deterministic whatever the
+// order of the atomics in step 3.
 #include <algorithm>
 #include <cstring>
 
@@ -42,91 +33,51 @@
 
 namespace gs {
 
-constexpr int kDsThreads = 512;                 // sort-pass CTA: 16 warps
-constexpr int kDsWarps = kDsThreads / 32;
-constexpr int kDsItems = 8;                     // keys per thread
-constexpr int kDsTile = kDsThreads * kDsItems;  // 4096 keys per sort-pass CTA
-constexpr int kDsMaxBits = 11;                  // digit bits per pass (<= 2048 digits)
-constexpr int kHistThreads = 256;
-constexpr int kBlockPairs = 32768;              // pair slots per count / emit CTA (wb warps)
-constexpr uint32_t kFlagAgg = 1u << 30, kFlagInc = 2u << 30, kValMask = (1u << 30) - 1u;
+constexpr int kSortThreads = 256;  // k_tile_sort CTA: 8 warps
+constexpr int kSortWarps = kSortThreads / 32;
+constexpr int kSortItems = 16;                          // keys per thread
+constexpr int kChunk = kSortThreads * kSortItems;       // 4096 keys sorted in shared memory at once
+constexpr int kDigitBits = 9;
+constexpr int kDigits = 1 << kDigitBits;
+constexpr int kBucketBits = 11;
+constexpr int kBuckets = 1 << kBucketBits;  // k_tile_sort counting-sort buckets
+constexpr int kBucketThreads = 256;  // k_tile_sort CTA
+constexpr int kMaxBucket = 128;     // fuller buckets -> exact two-key sort (k_tile_sort_big)
+constexpr int kEmitThreads = 512;
+constexpr int kBigBlocks = 148;    // k_tile_sort_big grid (grid-stride over the long tiles)
 
-struct BinLayout {
+struct SortLayout {
   int n, T, TX, TY;
   int64_t capacity;
-  uint32_t kbase, kmax;  // key = depth bits - kbase, in [0, kmax]
-  int npass, dbits, ndig;
-  int gsort;  // sort-pass CTAs (from n)
-  int wb;     // warps per count / emit CTA
-  int gbin;   // count / emit CTAs (from the capacity)
-  size_t hist, ctr, status, pstatus, misc, zero_end;
-  size_t key0, val0, key1, val1, srect, pre, wstart, cnt, totals, total;
+  size_t diff, misc, zero_end;  // zeroed region (one memset per call)
+  size_t cursor, slow, mid, key_a, key_b, val_b, total;
 };
 
 static size_t align_up(size_t x) { return (x + 255) & ~size_t(255); }
 
-static uint32_t f2u(float f) {
-  uint32_t u;
-  std::memcpy(&u, &f, 4);
-  return u;
-}
-
-static int host_nbits(uint32_t x) {
-  int b = 0;
-  while (x) {
-    ++b;
-    x >>= 1;
-  }
-  return b;
-}
-
-// warps per count / emit CTA: the emit CTA holds wb x T u16 offsets + T u32 bases
-static int bin_warps(int T) {
-  for (int wb = 16; wb >= 1; wb >>= 1)
-    if (size_t(wb) * T * 2 + size_t(T) * 4 + 1024 <= 200 * 1024) return wb;
-  return 0;
-}
-
-static bool make_layout(int32_t n, int64_t capacity, const gs_camera &cam, BinLayout &L) {
+static bool make_layout(int32_t n, int64_t capacity, const gs_camera &cam, SortLayout &L) {
   L.n = n;
   L.capacity = capacity;
   L.TX = tiles_x(cam);
   L.TY = tiles_y(cam);
   L.T = L.TX * L.TY;
-  if (L.T > (1 << 21) || capacity >= (int64_t(1) << 30) || n >= (1 << 30)) return false;
-  L.wb = bin_warps(L.T);
-  if (L.wb == 0) return false;
-  L.kbase = f2u(cam.z_near);
-  L.kmax = f2u(cam.z_far) - L.kbase;
-  const int nb = std::max(1, host_nbits(L.kmax));
-  L.npass = (nb + kDsMaxBits - 1) / kDsMaxBits;
-  L.dbits = (nb + L.npass - 1) / L.npass;
-  L.ndig = 1 << L.dbits;
-  const int nn = n > 0 ? n : 1;
-  L.gsort = (nn + kDsTile - 1) / kDsTile;
-  const int64_t cap = capacity > 0 ? capacity : 1;
-  L.gbin = int((cap + kBlockPairs - 1) / kBlockPairs);
+  if (L.T > (1 << 21) || capacity >= (int64_t(1) << 31) - 1) return false;
   size_t off = 0;
   auto take = [&](size_t bytes) {
     size_t o = off;
     off = align_up(off + bytes);
     return o;
   };
-  L.hist = take(size_t(4) * L.npass * L.ndig);
-  L.ctr = take(4 * 8);
-  L.status = take(size_t(4) * L.npass * L.gsort * L.ndig);
-  L.pstatus = take(size_t(4) * L.gsort);  // k_bin_prefix look-back words
-  L.misc = take(4 * 8);                   // [0] P
+  L.diff = take(4 * size_t(L.TX + 1) * (L.TY + 1));
+  L.misc = take(64);  // [1] P, [2] overflow, [3] slow-list length, [4] mid-list length
   L.zero_end = off;
-  L.key0 = take(size_t(4) * nn);
-  L.val0 = take(size_t(4) * nn);
-  L.key1 = take(size_t(4) * nn);
-  L.val1 = take(size_t(4) * nn);
-  L.srect = take(size_t(8) * nn);
-  L.pre = take(size_t(4) * nn);
-  L.wstart = take(size_t(4) * L.gbin * L.wb);
-  L.cnt = take(size_t(4) * L.T * L.gbin);
-  L.totals = take(size_t(4) * L.T);
+  L.cursor = take(4 * size_t(L.T));
+  L.slow = take(4 * size_t(L.T));
+  L.mid = take(4 * size_t(L.T));
+  const size_t cc = size_t(capacity > 0 ? capacity : 1);
+  L.key_a = take(4 * cc);  // scratch of the chunked (long-segment) sort
+  L.key_b = take(4 * cc);
+  L.val_b = take(4 * cc);
   L.total = off;
   return true;
 }
@@ -163,33 +114,39 @@ __device__ uint32_t block_excl_scan(uint32_t v, uint32_t *sh /* >= 33 */, uint32
   return r;
 }
 
-// In place: a[0..n) <- exclusive prefix sums (block-wide, blockDim threads,
-// n / blockDim consecutive entries per thread); returns the total.
-__device__ uint32_t block_excl_scan_array(uint32_t *a, int n, uint32_t *sh) {
-  const int per = (n + blockDim.x - 1) / blockDim.x;
-  const int b0 = threadIdx.x * per;
-  uint32_t s = 0;
-  for (int k = 0; k < per; ++k)
-    if (b0 + k < n) s += a[b0 + k];
-  uint32_t total;
-  uint32_t ex = block_excl_scan(s, sh, total);
-  for (int k = 0; k < per; ++k)
-    if (b0 + k < n) {
-      const uint32_t c = a[b0 + k];
-      a[b0 + k] = ex;
-      ex += c;
+// In-place 2-D inclusive prefix (rows, then columns) of the TX x TY corner of
+// a shared (TY+1) x W1 difference array: per-tile counts.  One warp per row /
+// column, 32 elements per step (warp scan + carry).
+__device__ void prefix2d(uint32_t *c, int W1, int TX, int TY) {
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  for (int y = w; y < TY; y += nw) {
+    uint32_t carry = 0;
+    for (int x0 = 0; x0 < TX; x0 += 32) {
+      const int x = x0 + lane;
+      const uint32_t inc = warp_incl_scan(x < TX ? c[y * W1 + x] : 0u) + carry;
+      if (x < TX) c[y * W1 + x] = inc;
+      carry = __shfl_sync(0xffffffffu, inc, 31);
     }
+  }
   __syncthreads();
-  return total;
+  for (int x = w; x < TX; x += nw) {
+    uint32_t carry = 0;
+    for (int y0 = 0; y0 < TY; y0 += 32) {
+      const int y = y0 + lane;
+      const uint32_t inc = warp_incl_scan(y < TY ? c[y * W1 + x] : 0u) + carry;
+      if (y < TY) c[y * W1 + x] = inc;
+      carry = __shfl_sync(0xffffffffu, inc, 31);
+    }
+  }
+  __syncthreads();
 }
 
 // Lanes of `act` whose digit equals this lane's: one ballot per digit bit.
 // Every lane of the warp must call it.
-__device__ __forceinline__ unsigned peer_mask(unsigned act, uint32_t d, int dbits) {
+__device__ __forceinline__ unsigned peer_mask(unsigned act, uint32_t d) {
   unsigned m = act;
 #pragma unroll
-  for (int b = 0; b < kDsMaxBits; ++b) {
-    if (b >= dbits) break;
+  for (int b = 0; b < kDigitBits; ++b) {
     const bool bit = (d >> b) & 1u;
     const unsigned bb = __ballot_sync(0xffffffffu, bit);
     m &= bit ? bb : ~bb;
@@ -197,432 +154,116 @@ __device__ __forceinline__ unsigned peer_mask(unsigned act, uint32_t d, int dbit
   return m;
 }
 
-__device__ __forceinline__ uint32_t ld_acquire(const uint32_t *p) {
-  uint32_t v;
-  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
-  return v;
+// floor(c * 64 / den) for c < 2^25, den >= 1, exact: a float estimate
+// corrected by one step (no 64-bit integer division on the hot path)
+__device__ __forceinline__ int bucket64(uint32_t c, uint32_t den, float inv_den) {
+  const uint32_t x = c * 64u;
+  int q = int(float(x) * inv_den);
+  if (uint64_t(q) * den > x) --q;
+  else if (uint64_t(q + 1) * den <= x) ++q;
+  return q;
 }
 
-__device__ __forceinline__ void st_release(uint32_t *p, uint32_t v) {
-  asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
-}
+// tile row t / TX for t < 2^22, TX < 2^12: floor((t + 0.5) / TX) in fp32 is exact
+__device__ __forceinline__ int tile_row(int t, float inv_tx) { return int((float(t) + 0.5f) * inv_tx); }
 
 // ---------------------------------------------------------------------------
-// Stage 1: stable LSD radix sort of the visible Gaussians by depth bits.
+// Step 1: tile-rect difference array (per-block in shared memory, merged with
+// one global atomic per nonzero cell).
 
-struct DsArgs {
-  const float *depth;
-  const int32_t *tiles_touched;
-  const short4 *rect;
-  int n;
-  uint32_t kbase, kmax;
-  int npass, dbits, ndig, gsort;
-  uint32_t *hist;    // [npass][ndig] global digit counts
-  uint32_t *ctr;     // [npass] virtual CTA counters
-  uint32_t *status;  // [npass][gsort][ndig] look-back words
-  uint32_t *key[2], *val[2];
-  short4 *srect;     // the rects in the final order
-};
-
-__device__ __forceinline__ uint32_t depth_key(const DsArgs &a, int i) {
-  // visible depths are RN(p_z) with z_near <= p_z <= z_far (gs_project), so
-  // the key lies in [0, kmax]; the clamp only guards the digit range
-  return min(__float_as_uint(__ldg(a.depth + i)) - a.kbase, a.kmax);
-}
-
-__global__ void __launch_bounds__(kHistThreads) k_ds_hist(DsArgs a) {
+__global__ void __launch_bounds__(256) k_bin_prep(const int32_t *__restrict__ tiles_touched,
+                                                  const short4 *__restrict__ rect, int n, int TX, int TY,
+                                                  uint32_t *diff) {
   pdl_begin();
-  extern __shared__ uint32_t s_h[];  // [npass][ndig]
-  const int nh = a.npass * a.ndig;
-  for (int i = threadIdx.x; i < nh; i += blockDim.x) s_h[i] = 0;
+  extern __shared__ uint32_t s_diff[];
+  const int W1 = TX + 1, cells = W1 * (TY + 1);
+  for (int i = threadIdx.x; i < cells; i += blockDim.x) s_diff[i] = 0;
   __syncthreads();
-  const uint32_t mask = uint32_t(a.ndig - 1);
-  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < a.n; i += gridDim.x * blockDim.x) {
-    if (__ldg(a.tiles_touched + i) > 0) {
-      const uint32_t k = depth_key(a, i);
-      for (int p = 0; p < a.npass; ++p) atomicAdd(&s_h[p * a.ndig + ((k >> (p * a.dbits)) & mask)], 1u);
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    if (__ldg(tiles_touched + i) > 0) {  // +1 over the rect [x0, x1] x [y0, y1]
+      const short4 r = __ldg(rect + i);
+      atomicAdd(s_diff + r.y * W1 + r.x, 1u);
+      atomicAdd(s_diff + r.y * W1 + r.z + 1, 0xffffffffu);
+      atomicAdd(s_diff + (r.w + 1) * W1 + r.x, 0xffffffffu);
+      atomicAdd(s_diff + (r.w + 1) * W1 + r.z + 1, 1u);
     }
   }
   __syncthreads();
-  for (int i = threadIdx.x; i < nh; i += blockDim.x)
-    if (s_h[i]) atomicAdd(a.hist + i, s_h[i]);
-}
-
-// One stable pass on digit p.  Keys are held "blocked": warp w owns the
-// positions [w 32 I, (w + 1) 32 I) of the CTA's tile, its k-th round the 32
-// positions w 32 I + 32 k + lane (I = kDsItems).
-__global__ void __launch_bounds__(kDsThreads) k_ds_pass(DsArgs a, int p) {
-  pdl_begin();
-  extern __shared__ uint32_t s_dyn[];
-  uint16_t *s_cnt = reinterpret_cast<uint16_t *>(s_dyn);            // [kDsWarps][ndig]: counts -> warp offsets
-  uint32_t *s_off = s_dyn + (kDsWarps * a.ndig) / 2;               // [ndig]: global digit base + earlier tiles
-  __shared__ uint32_t sh[33];
-  __shared__ int s_vb;
-  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  const int nd = a.ndig;
-  const uint32_t mask = uint32_t(nd - 1);
-  const int shift = p * a.dbits;
-  if (threadIdx.x == 0) s_vb = int(atomicAdd(a.ctr + p, 1u));  // virtual CTA id: predecessors have started
-  // global digit bases of this pass (exclusive scan of its histogram); the
-  // visible count = the total of any pass's histogram
-  for (int d = threadIdx.x; d < nd; d += blockDim.x) s_off[d] = a.hist[p * nd + d];
-  __syncthreads();
-  const uint32_t nvis = block_excl_scan_array(s_off, nd, sh);
-  const int vb = s_vb;
-  const int nin = p == 0 ? a.n : int(nvis);
-  if (vb * kDsTile >= nin) return;  // empty tile: no later tile reads its status
-  for (int i = threadIdx.x; i < kDsWarps * nd / 2; i += blockDim.x) s_dyn[i] = 0u;
-  __syncthreads();
-  // load (pass 0: the visible Gaussians of the index range, id = index)
-  const uint32_t *kin = a.key[p & 1], *vin = a.val[p & 1];
-  uint32_t key[kDsItems], val[kDsItems];
-  bool ok[kDsItems];
-  const int base = vb * kDsTile + w * 32 * kDsItems;
-#pragma unroll
-  for (int k = 0; k < kDsItems; ++k) {
-    const int i = base + 32 * k + lane;
-    if (p == 0) {
-      ok[k] = i < a.n && __ldg(a.tiles_touched + i) > 0;
-      key[k] = ok[k] ? depth_key(a, i) : 0u;
-      val[k] = uint32_t(i);
-    } else {
-      ok[k] = i < nin;
-      key[k] = ok[k] ? kin[i] : 0u;
-      val[k] = ok[k] ? vin[i] : 0u;
-    }
-  }
-  // per-warp stable ranks (rounds in order, lanes in order)
-  uint16_t rank[kDsItems];
-  uint16_t *cw = s_cnt + w * nd;
-#pragma unroll
-  for (int k = 0; k < kDsItems; ++k) {
-    const unsigned act = __ballot_sync(0xffffffffu, ok[k]);
-    const uint32_t d = (key[k] >> shift) & mask;
-    const unsigned peers = peer_mask(act, d, a.dbits);
-    const uint32_t before = ok[k] ? cw[d] : 0u;
-    rank[k] = uint16_t(before + __popc(peers & lanemask_lt()));
-    __syncwarp();
-    if (ok[k] && lane == 31 - __clz(peers)) cw[d] = uint16_t(before + __popc(peers));
-    __syncwarp();
-  }
-  __syncthreads();
-  // per digit: the tile's count (published for the look-back) and the warp offsets
-  uint32_t *st = a.status + (size_t(p) * a.gsort + vb) * nd;
-  for (int d = threadIdx.x; d < nd; d += blockDim.x) {
-    uint32_t run = 0;
-    for (int ww = 0; ww < kDsWarps; ++ww) {
-      const uint32_t c = s_cnt[ww * nd + d];
-      s_cnt[ww * nd + d] = uint16_t(run);
-      run += c;
-    }
-    if (vb == 0) {
-      st_release(st + d, kFlagInc | run);
-    } else {
-      st_release(st + d, kFlagAgg | run);
-      // decoupled look-back over the earlier tiles of this pass
-      uint32_t ex = 0;
-      for (int j = vb - 1; j >= 0;) {
-        const uint32_t s = ld_acquire(a.status + (size_t(p) * a.gsort + j) * nd + d);
-        if (!(s & ~kValMask)) continue;  // not published yet: spin
-        ex += s & kValMask;
-        if (s & kFlagInc) break;
-        --j;
-      }
-      st_release(st + d, kFlagInc | (ex + run));
-      s_off[d] += ex;
-    }
-  }
-  __syncthreads();
-  // scatter (the last pass also moves the rects into the final order)
-  const bool last = p == a.npass - 1;
-  uint32_t *kout = a.key[(p + 1) & 1], *vout = a.val[(p + 1) & 1];
-#pragma unroll
-  for (int k = 0; k < kDsItems; ++k) {
-    if (!ok[k]) continue;
-    const uint32_t d = (key[k] >> shift) & mask;
-    const uint32_t pos = s_off[d] + s_cnt[w * nd + d] + rank[k];
-    kout[pos] = key[k];
-    vout[pos] = val[k];
-    if (last) a.srect[pos] = __ldg(a.rect + val[k]);
+  for (int i = threadIdx.x; i < cells; i += blockDim.x) {
+    const uint32_t c = s_diff[i];
+    if (c) atomicAdd(diff + i, c);
   }
 }
 
 // ---------------------------------------------------------------------------
-// Stages 2-4: stable per-tile emission over the (depth, id) order.
+// Step 2: per-tile pair counts (2-D prefix of the difference array, in shared
+// memory), tile ranges, write cursors, P and the capacity check,
+// heaviest-first tile order.
 
-struct BinArgs {
-  const uint32_t *hist;   // pass-0 digit counts (their total = visible count)
-  int ndig;
-  const uint32_t *ids;    // [nvis] Gaussian ids in (depth, id) order
-  const short4 *srect;    // [nvis] their rects
-  uint32_t *pre;          // [nvis] flat position of each Gaussian's first pair
-  uint32_t *wstart;       // [gbin wb] per warp: the Gaussian holding its first slot
-  uint32_t *pstatus;      // [gsort] k_bin_prefix look-back words
-  uint32_t *ctr;          // virtual CTA counter of k_bin_prefix
-  uint32_t *misc;         // [0] P
-  int TX, TY, T, gbin, wb;
-  uint32_t cw;            // pair slots per warp (kBlockPairs / wb)
-  uint32_t *cnt;          // [T][gbin]: CTA counts -> exclusive prefix over CTAs
-  uint32_t *totals;       // [T]
+struct TileArgs {
+  const uint32_t *diff;  // (TY+1) x (TX+1)
+  int TX, TY, T;
   int64_t capacity;
-  int32_t *sorted_idx, *tile_range, *tile_order;
+  int32_t *tile_range, *tile_order;
+  uint32_t *cursor;
   int64_t *n_pairs;
-  gs_counters *cntrs;
+  uint32_t *misc;  // [1] P, [2] overflow
+  gs_counters *cnt;
 };
 
-__device__ __forceinline__ uint32_t visible_count(const BinArgs &a, uint32_t *sh) {
-  uint32_t s = 0;
-  for (int d = threadIdx.x; d < a.ndig; d += blockDim.x) s += a.hist[d];
-  uint32_t total;
-  block_excl_scan(s, sh, total);
-  return total;
-}
-
-__device__ __forceinline__ uint32_t rect_area(short4 r) {
-  return (r.z >= r.x && r.w >= r.y) ? uint32_t(r.z - r.x + 1) * uint32_t(r.w - r.y + 1) : 0u;
-}
-
-// Exclusive prefix of the tile counts over the (depth, id) order: 4096
-// Gaussians per CTA (512 threads x 8 consecutive), decoupled look-back on the
-// CTA sums; also the first Gaussian of every warp's slot range and P.
-__global__ void __launch_bounds__(kDsThreads) k_bin_prefix(BinArgs a) {
+__global__ void __launch_bounds__(1024) k_tile_counts(TileArgs a) {
   pdl_begin();
+  extern __shared__ uint32_t s_c[];  // (TY+1) x (TX+1)
   __shared__ uint32_t sh[33];
-  __shared__ int s_vb;
-  __shared__ uint32_t s_ex;
-  const uint32_t nvis = visible_count(a, sh);
-  if (threadIdx.x == 0) s_vb = int(atomicAdd(a.ctr, 1u));
-  __syncthreads();
-  const int vb = s_vb;
-  if (vb * kDsTile >= int(nvis)) return;
-  const int k0 = vb * kDsTile + threadIdx.x * kDsItems;
-  uint32_t c[kDsItems], sum = 0;
-#pragma unroll
-  for (int k = 0; k < kDsItems; ++k) {
-    c[k] = k0 + k < int(nvis) ? rect_area(a.srect[k0 + k]) : 0u;
-    sum += c[k];
-  }
-  uint32_t tot;
-  uint32_t ex = block_excl_scan(sum, sh, tot);
-  if (threadIdx.x == 0) {
-    uint32_t e = 0;
-    if (vb == 0) {
-      st_release(a.pstatus, kFlagInc | tot);
-    } else {
-      st_release(a.pstatus + vb, kFlagAgg | tot);
-      for (int j = vb - 1; j >= 0;) {
-        const uint32_t s = ld_acquire(a.pstatus + j);
-        if (!(s & ~kValMask)) continue;  // not published yet: spin
-        e += s & kValMask;
-        if (s & kFlagInc) break;
-        --j;
-      }
-      st_release(a.pstatus + vb, kFlagInc | (e + tot));
-    }
-    s_ex = e;
-    if ((vb + 1) * kDsTile >= int(nvis)) a.misc[0] = e + tot;  // the last CTA: P
-  }
-  __syncthreads();
-  ex += s_ex;
-#pragma unroll
-  for (int k = 0; k < kDsItems; ++k) {
-    if (k0 + k >= int(nvis)) break;
-    a.pre[k0 + k] = ex;
-    // warp slot ranges starting inside this Gaussian's pairs
-    for (uint32_t q = (ex + a.cw - 1) / a.cw * a.cw; q < ex + c[k]; q += a.cw) a.wstart[q / a.cw] = uint32_t(k0 + k);
-    ex += c[k];
-  }
-}
-
-// The pairs of flat slots [q0, q1) of F, warp-wide, 32 per step, starting at
-// Gaussian k (the one holding slot q0): f(j, tile, valid, kw) per step, where
-// lane j of the current window of 32 Gaussians (kw = its first) holds the
-// slot's Gaussian; all lanes call f every step (valid = false past the end).
-template <class F>
-__device__ __forceinline__ void for_warp_pairs(const BinArgs &a, uint32_t nvis, uint32_t q0, uint32_t q1, int k,
-                                               F &&f) {
-  const int lane = threadIdx.x & 31;
-  for (;; k += 32) {
-    const int kk = k + lane;
-    const short4 r = kk < int(nvis) ? a.srect[kk] : make_short4(0, 0, -1, -1);
-    const uint32_t Q = a.pre[k];
-    const int wdt = r.z - r.x + 1;
-    const int nt = int(rect_area(r));
-    const int incl = int(warp_incl_scan(uint32_t(nt)));
-    const uint32_t total = uint32_t(__shfl_sync(0xffffffffu, incl, 31));
-    const int xy = (int(r.x) & 0xffff) | (int(r.y) << 16);
-    // row = floor(local / wdt) as floor((local + 0.5) (1 / wdt)) in fp32: exact
-    // (local < 2^22; the quotient is >= 0.5 / wdt away from an integer)
-    const float iw = 1.0f / float(max(wdt, 1));
-    const uint32_t pa = q0 > Q ? q0 - Q : 0u, pb = min(q1 - Q, total);
-    for (uint32_t p0 = pa; p0 < pb; p0 += 32) {
-      const int p = int(p0) + lane;
-      // j = number of lanes whose inclusive prefix is <= p
-      int j = 0;
-#pragma unroll
-      for (int b = 16; b > 0; b >>= 1) {
-        const int v = __shfl_sync(0xffffffffu, incl, j + b - 1);
-        j += v <= p ? b : 0;
-      }
-      j = min(j, 31);
-      const int ij = __shfl_sync(0xffffffffu, incl, j), nj = __shfl_sync(0xffffffffu, nt, j);
-      const int xyj = __shfl_sync(0xffffffffu, xy, j), wj = __shfl_sync(0xffffffffu, wdt, j);
-      const float iwj = __shfl_sync(0xffffffffu, iw, j);
-      int tile = 0;
-      const bool valid = uint32_t(p) < pb;
-      if (valid) {
-        const int local = p - (ij - nj);
-        const int row = int((float(local) + 0.5f) * iwj);
-        const int col = local - row * wj;
-        tile = ((xyj >> 16) + row) * a.TX + (xyj & 0xffff) + col;
-      }
-      f(j, tile, valid, k);
-    }
-    if (Q + total >= q1) break;
-  }
-}
-
-// P and this warp's slot range [q0, q1) (empty past P)
-__device__ __forceinline__ void warp_slots(const BinArgs &a, uint32_t P, uint32_t &q0, uint32_t &q1, int &k) {
-  const uint32_t g = blockIdx.x * a.wb + (threadIdx.x >> 5);
-  q0 = g * a.cw;
-  q1 = min(q0 + a.cw, P);
-  k = q0 < P ? int(a.wstart[g]) : 0;
-}
-
-__global__ void __launch_bounds__(512) k_bin_count(BinArgs a) {
-  pdl_begin();
-  extern __shared__ uint32_t s_c[];  // [T]
-  __shared__ uint32_t sh[33];
-  const uint32_t nvis = visible_count(a, sh);
-  const uint32_t P = nvis ? a.misc[0] : 0u;
-  if (uint64_t(blockIdx.x) * kBlockPairs >= P) return;  // k_bin_scan reads only the CTAs holding pairs
-  for (int t = threadIdx.x; t < a.T; t += blockDim.x) s_c[t] = 0;
-  __syncthreads();
-  uint32_t q0, q1;
-  int k;
-  warp_slots(a, P, q0, q1, k);
-  if (q0 < q1)
-    for_warp_pairs(a, nvis, q0, q1, k, [&](int, int tile, bool valid, int) {
-      if (valid) atomicAdd(&s_c[tile], 1u);
-    });
-  __syncthreads();
-  for (int t = threadIdx.x; t < a.T; t += blockDim.x) a.cnt[size_t(t) * a.gbin + blockIdx.x] = s_c[t];
-}
-
-// one warp per tile: exclusive scan of its CTA counts, the tile total
-__global__ void __launch_bounds__(256) k_bin_scan(BinArgs a) {
-  pdl_begin();
-  __shared__ uint32_t sh[33];
-  const int lane = threadIdx.x & 31;
-  const uint32_t nvis = visible_count(a, sh);
-  const uint32_t P = nvis ? a.misc[0] : 0u;
-  const int nb = min(int((uint64_t(P) + kBlockPairs - 1) / kBlockPairs), a.gbin);
-  const int t = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
-  if (t >= a.T) return;
-  uint32_t *c = a.cnt + size_t(t) * a.gbin;
-  uint32_t carry = 0;
-  for (int b0 = 0; b0 < nb; b0 += 32) {
-    const int b = b0 + lane;
-    const uint32_t v = b < nb ? c[b] : 0u;
-    const uint32_t inc = warp_incl_scan(v) + carry;
-    if (b < nb) c[b] = inc - v;
-    carry = __shfl_sync(0xffffffffu, inc, 31);
-  }
-  if (lane == 0) a.totals[t] = carry;
-}
-
-__global__ void __launch_bounds__(512) k_bin_emit(BinArgs a) {
-  pdl_begin();
-  extern __shared__ uint32_t s_e[];  // [T] tile bases, then [wb][T] u16 per-warp offsets
-  __shared__ uint32_t sh[33];
+  __shared__ int s_max;
   __shared__ unsigned s_b[64];
-  __shared__ uint32_t s_max;
-  const int wb = a.wb, lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  const int T = a.T;
-  uint32_t *s_base = s_e;
-  uint16_t *s_off = reinterpret_cast<uint16_t *>(s_e + T);
-  const uint32_t nvis = visible_count(a, sh);
-  const uint32_t P = nvis ? a.misc[0] : 0u;
-  const bool over = int64_t(P) > a.capacity;
-  const bool has = !over && uint64_t(blockIdx.x) * kBlockPairs < P;
-  if (!has && blockIdx.x != 0) return;
-  // the tile totals (no pair: never computed; overflow: the lists stay empty)
-  auto total_of = [&](int t) { return (over || P == 0) ? 0u : a.totals[t]; };
-  // tile starts: exclusive scan of the totals
-  for (int t = threadIdx.x; t < T; t += blockDim.x) s_base[t] = total_of(t);
-  __syncthreads();
-  block_excl_scan_array(s_base, T, sh);
-  if (blockIdx.x == 0) {
-    for (int t = threadIdx.x; t < T; t += blockDim.x) {
-      const int st = int(s_base[t]);
-      reinterpret_cast<int2 *>(a.tile_range)[t] = make_int2(st, st + int(total_of(t)));
-    }
-    if (threadIdx.x == 0) {
-      *a.n_pairs = int64_t(P);
-      if (over && a.cntrs) atomicAdd(reinterpret_cast<unsigned long long *>(&a.cntrs->n_overflow), 1ull);
-    }
-  }
-  if (has) {
-    // this CTA's base per tile, per-warp counts (each warp its own row)
-    for (int t = threadIdx.x; t < T; t += blockDim.x) s_base[t] += a.cnt[size_t(t) * a.gbin + blockIdx.x];
-    for (int i = threadIdx.x; i < (wb * T + 1) / 2; i += blockDim.x) reinterpret_cast<uint32_t *>(s_off)[i] = 0u;
-    __syncthreads();
-    uint16_t *row = s_off + w * T;
-    uint32_t q0, q1;
-    int k;
-    warp_slots(a, P, q0, q1, k);
-    if (q0 < q1)
-      for_warp_pairs(a, nvis, q0, q1, k, [&](int, int tile, bool valid, int) {
-        // lanes of one step that hit the same tile form a match group
-        const unsigned g = __match_any_sync(0xffffffffu, valid ? tile : -1);
-        if (valid && lane == __ffs(g) - 1) row[tile] = uint16_t(row[tile] + __popc(g));
-        __syncwarp();
-      });
-    __syncthreads();
-    // per tile: exclusive prefix over the warps
-    for (int t = threadIdx.x; t < T; t += blockDim.x) {
-      uint32_t run = 0;
-      for (int ww = 0; ww < wb; ++ww) {
-        const uint32_t c = s_off[ww * T + t];
-        s_off[ww * T + t] = uint16_t(run);
-        run += c;
-      }
-    }
-    __syncthreads();
-    // emission in order: position = tile base + warp offset + pairs of this
-    // tile earlier in the warp's walk (earlier steps: the running offset;
-    // this step: lanes below in the match group, which hold earlier Gaussians)
-    if (q0 < q1) {
-      int kw = -1, id = 0;
-      for_warp_pairs(a, nvis, q0, q1, k, [&](int j, int tile, bool valid, int kwin) {
-        if (kwin != kw) {  // a new window of 32 Gaussians: their ids
-          kw = kwin;
-          id = kw + lane < int(nvis) ? int(a.ids[kw + lane]) : 0;
-        }
-        const int gid = __shfl_sync(0xffffffffu, id, j);
-        const unsigned g = __match_any_sync(0xffffffffu, valid ? tile : -1);
-        if (valid) a.sorted_idx[s_base[tile] + row[tile] + __popc(g & lanemask_lt())] = gid;
-        __syncwarp();
-        if (valid && lane == __ffs(g) - 1) row[tile] = uint16_t(row[tile] + __popc(g));
-        __syncwarp();
-      });
-    }
-  }
-  if (blockIdx.x != 0 || !a.tile_order) return;
-  // CTA 0: tiles by descending list length, 64 buckets of max/64 (order
-  // inside a bucket unspecified), a scheduling hint for the compositing
-  __syncthreads();
+  const int W1 = a.TX + 1, cells = W1 * (a.TY + 1);
+  const float itx = 1.0f / float(a.TX);
+  for (int i = threadIdx.x; i < cells; i += blockDim.x) s_c[i] = a.diff[i];
   if (threadIdx.x == 0) s_max = 0;
   if (threadIdx.x < 64) s_b[threadIdx.x] = 0;
   __syncthreads();
-  uint32_t m = 0;
-  for (int t = threadIdx.x; t < T; t += blockDim.x) m = max(m, total_of(t));
+  prefix2d(s_c, W1, a.TX, a.TY);  // diff -> per-tile counts
+  // exclusive scan over tiles (tile id = y*TX + x), PER consecutive tiles per thread
+  const int PER = (a.T + blockDim.x - 1) / blockDim.x;
+  uint32_t s = 0;
+  int m = 0;
+  for (int k = 0; k < PER; ++k) {
+    const int t = threadIdx.x * PER + k;
+    if (t < a.T) {
+      const uint32_t c = s_c[t + tile_row(t, itx)];  // (t / TX) W1 + t % TX
+      s += c;
+      m = max(m, int(c));
+    }
+  }
+  uint32_t P;
+  uint32_t ex = block_excl_scan(s, sh, P);
+  const bool over = int64_t(P) > a.capacity;
   atomicMax(&s_max, m);
+  for (int k = 0; k < PER; ++k) {
+    const int t = threadIdx.x * PER + k;
+    if (t < a.T) {
+      const uint32_t c = s_c[t + tile_row(t, itx)];  // (t / TX) W1 + t % TX
+      reinterpret_cast<int2 *>(a.tile_range)[t] = over ? make_int2(0, 0) : make_int2(int(ex), int(ex + c));
+      a.cursor[t] = ex;
+      ex += c;
+    }
+  }
+  if (threadIdx.x == 0) {
+    a.misc[1] = P;
+    a.misc[2] = over ? 1u : 0u;
+    *a.n_pairs = int64_t(P);
+    if (over && a.cnt) atomicAdd(reinterpret_cast<unsigned long long *>(&a.cnt->n_overflow), 1ull);
+  }
+  if (!a.tile_order) return;
   __syncthreads();
-  const int64_t den = int64_t(s_max) + 1;
-  for (int t = threadIdx.x; t < T; t += blockDim.x)
-    atomicAdd(&s_b[63 - int(int64_t(total_of(t)) * 64 / den)], 1u);
+  // heaviest first: 64 buckets of maxlen/64 (order inside a bucket unspecified)
+  const uint32_t den = uint32_t(s_max) + 1u;
+  const float iden = 1.0f / float(den);
+  for (int t = threadIdx.x; t < a.T; t += blockDim.x) {
+    const uint32_t c = s_c[t + tile_row(t, itx)];  // (t / TX) W1 + t % TX
+    atomicAdd(&s_b[63 - bucket64(c, den, iden)], 1u);
+  }
   __syncthreads();
   if (threadIdx.x == 0) {
     unsigned run = 0;
@@ -633,8 +274,498 @@ __global__ void __launch_bounds__(512) k_bin_emit(BinArgs a) {
     }
   }
   __syncthreads();
-  for (int t = threadIdx.x; t < T; t += blockDim.x)
-    a.tile_order[atomicAdd(&s_b[63 - int(int64_t(total_of(t)) * 64 / den)], 1u)] = t;
+  for (int t = threadIdx.x; t < a.T; t += blockDim.x) {
+    const uint32_t c = s_c[t + tile_row(t, itx)];  // (t / TX) W1 + t % TX
+    a.tile_order[atomicAdd(&s_b[63 - bucket64(c, den, iden)], 1u)] = t;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Step 3: pair emission into the tile segments (unordered inside a segment).
+// Per block of kEmitThreads * kEmitPer Gaussians: the block's per-tile counts
+// from a shared-memory 2-D difference array (4 updates per Gaussian), one
+// global cursor reservation per (block, tile), then the pairs: every warp
+// expands the rects of 32 Gaussians into one flat list of (Gaussian, tile)
+// pairs walked 32 at a time (a lane finds its Gaussian by a binary search of
+// the warp's inclusive prefix of tile counts), so lanes stay busy whatever
+// the mix of rect sizes.
+
+template <int kEmitPer>  // Gaussians per thread
+__global__ void __launch_bounds__(kEmitThreads) k_emit(const int32_t *__restrict__ tiles_touched,
+                                                       const short4 *__restrict__ rect, int n, int TX, int TY,
+                                                       uint32_t *cursor, const uint32_t *__restrict__ misc,
+                                                       int32_t *ids) {
+  pdl_begin();
+  extern __shared__ uint32_t s_e[];  // [(TY+1)(TX+1)] diff -> counts -> cursors, [T] bases
+  if (misc[2]) return;               // overflow: leave sorted_idx untouched
+  const int W1 = TX + 1, cells = W1 * (TY + 1), T = TX * TY;
+  const float itx = 1.0f / float(TX);
+  uint32_t *s_cur = s_e, *s_base = s_e + cells;
+  const int lane = threadIdx.x & 31;
+  for (int c = threadIdx.x; c < cells; c += blockDim.x) s_cur[c] = 0;
+  __syncthreads();
+  short4 r[kEmitPer];
+#pragma unroll
+  for (int k = 0; k < kEmitPer; ++k) {
+    const int i = (blockIdx.x * kEmitPer + k) * kEmitThreads + threadIdx.x;
+    const bool vis = i < n && __ldg(tiles_touched + i) > 0;
+    r[k] = vis ? __ldg(rect + i) : make_short4(0, 0, -1, -1);
+    if (vis) {
+      atomicAdd(s_cur + r[k].y * W1 + r[k].x, 1u);
+      atomicAdd(s_cur + r[k].y * W1 + r[k].z + 1, 0xffffffffu);
+      atomicAdd(s_cur + (r[k].w + 1) * W1 + r[k].x, 0xffffffffu);
+      atomicAdd(s_cur + (r[k].w + 1) * W1 + r[k].z + 1, 1u);
+    }
+  }
+  __syncthreads();
+  prefix2d(s_cur, W1, TX, TY);
+  // one reservation per (block, tile); four independent atomics in flight per thread
+  for (int t0 = threadIdx.x; t0 < T; t0 += 4 * blockDim.x) {
+    uint32_t cnt[4], base[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int t = t0 + u * blockDim.x;
+      cnt[u] = t < T ? s_cur[t + tile_row(t, itx)] : 0u;
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) base[u] = cnt[u] ? atomicAdd(cursor + t0 + u * blockDim.x, cnt[u]) : 0u;
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int t = t0 + u * blockDim.x;
+      if (t < T) {
+        s_base[t] = base[u];
+        s_cur[t + tile_row(t, itx)] = 0;
+      }
+    }
+  }
+  __syncthreads();
+#pragma unroll
+  for (int k = 0; k < kEmitPer; ++k) {
+    const int i = (blockIdx.x * kEmitPer + k) * kEmitThreads + threadIdx.x;
+    const int wdt = r[k].z - r[k].x + 1;
+    const int nt = wdt * (r[k].w - r[k].y + 1);  // 0 when not visible
+    const int incl = int(warp_incl_scan(uint32_t(nt)));
+    const int total = __shfl_sync(0xffffffffu, incl, 31);
+    const int xy = (int(r[k].x) & 0xffff) | (int(r[k].y) << 16);
+    // row = local / wdt as a multiply-high (exact for local, wdt < 2^16)
+    const uint32_t magic = wdt > 1 ? uint32_t((0x100000000ull + uint64_t(wdt) - 1) / uint64_t(wdt)) : 0u;
+    for (int p0 = 0; p0 < total; p0 += 32) {
+      const int p = p0 + lane;
+      // j = number of lanes whose inclusive prefix is <= p
+      int j = 0;
+#pragma unroll
+      for (int b = 16; b > 0; b >>= 1) {
+        const int v = __shfl_sync(0xffffffffu, incl, j + b - 1);
+        j += v <= p ? b : 0;
+      }
+      j = min(j, 31);
+      const int ij = __shfl_sync(0xffffffffu, incl, j), nj = __shfl_sync(0xffffffffu, nt, j);
+      const int wj = __shfl_sync(0xffffffffu, wdt, j), xyj = __shfl_sync(0xffffffffu, xy, j);
+      const uint32_t mj = __shfl_sync(0xffffffffu, magic, j);
+      if (p < total) {
+        const int local = p - (ij - nj);
+        const int row = wj == 1 ? local : (nj < 65536 ? int(__umulhi(uint32_t(local), mj)) : local / wj);
+        const int col = local - row * wj;
+        const int x = (xyj & 0xffff) + col, y = (xyj >> 16) + row;
+        const uint32_t pos = s_base[y * TX + x] + atomicAdd(s_cur + y * W1 + x, 1u);
+        ids[pos] = i - lane + j;
+      }
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Step 4: per-tile sort.  Keys are held "blocked": warp w owns the positions
+// [w*32*items, (w+1)*32*items) of the current order, its k-th round the 32
+// positions w*32*items + 32k + lane.  One stable LSD pass:
+//   ranks    per warp round, ballot-sliced peer masks (stable: rounds in
+//            order, lanes in order) and per-warp digit counters s_cnt[w][d];
+//   offsets  digit-major, warp-minor: s_off[d] (digit base) + the warps
+//            before w in digit d;
+//   scatter  into the shared-memory buffers, reload blocked.
+
+struct SortSmem {
+  uint32_t key[kChunk];
+  uint32_t val[kChunk];
+  uint16_t cnt[kSortWarps][kDigits];
+  uint32_t off[kDigits];
+  uint32_t sh[33];
+  int flag;
+  uint32_t red[3][kSortWarps];
+};
+
+// Per-warp stable ranks of the digits of one chunk; leaves the per-warp digit
+// counts in s.cnt (zeroed here) and returns the ranks in rank[].
+__device__ __forceinline__ void chunk_rank(const uint32_t key[kSortItems], const uint32_t val[kSortItems], int n,
+                                           int items, bool by_val, int shift, SortSmem &s,
+                                           uint16_t rank[kSortItems]) {
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  for (int i = threadIdx.x; i < kSortWarps * kDigits / 2; i += kSortThreads)
+    reinterpret_cast<uint32_t *>(&s.cnt[0][0])[i] = 0u;
+  __syncthreads();
+  const int base = w * 32 * items;
+#pragma unroll
+  for (int k = 0; k < kSortItems; ++k) {
+    if (k >= items) break;
+    const bool ok = base + 32 * k + lane < n;
+    const unsigned act = __ballot_sync(0xffffffffu, ok);
+    const uint32_t d = ((by_val ? val[k] : key[k]) >> shift) & (kDigits - 1);
+    const unsigned peers = peer_mask(act, d);
+    const uint32_t before = ok ? s.cnt[w][d] : 0u;
+    rank[k] = uint16_t(before + __popc(peers & lanemask_lt()));
+    __syncwarp();
+    if (ok && lane == 31 - __clz(peers)) s.cnt[w][d] = uint16_t(before + __popc(peers));
+    __syncwarp();
+  }
+  __syncthreads();
+}
+
+// s.cnt[w][d] <- sum of the counts of warps < w in digit d; returns the digit
+// totals of digits 2t and 2t+1 (thread t).
+__device__ __forceinline__ uint2 warp_prefix(SortSmem &s) {
+  uint32_t tot[2];
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+    const int d = 2 * threadIdx.x + h;
+    uint32_t run = 0;
+#pragma unroll
+    for (int w = 0; w < kSortWarps; ++w) {
+      const uint32_t c = s.cnt[w][d];
+      s.cnt[w][d] = uint16_t(run);
+      run += c;
+    }
+    tot[h] = run;
+  }
+  return make_uint2(tot[0], tot[1]);
+}
+
+// One stable pass over a chunk held blocked in registers, scattered to
+// out_key/out_val at s.off[d] + (warps before) + rank.  `local`: the chunk is
+// the whole sequence, s.off = exclusive scan of its digit totals; otherwise
+// s.off holds running global digit bases and is advanced by the totals.
+template <bool kGlobalOut>
+__device__ __forceinline__ void chunk_pass(const uint32_t key[kSortItems], const uint32_t val[kSortItems], int n,
+                                           int items, bool by_val, int shift, bool local, SortSmem &s,
+                                           uint32_t *out_key, uint32_t *out_val) {
+  static_assert(kDigits == 2 * kSortThreads, "two digits per thread in the offset scan");
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  uint16_t rank[kSortItems];
+  chunk_rank(key, val, n, items, by_val, shift, s, rank);
+  const uint2 tot = warp_prefix(s);
+  if (local) {
+    uint32_t all;
+    const uint32_t ex = block_excl_scan(tot.x + tot.y, s.sh, all);
+    s.off[2 * threadIdx.x] = ex;
+    s.off[2 * threadIdx.x + 1] = ex + tot.x;
+  }
+  __syncthreads();
+  const int base = w * 32 * items;
+#pragma unroll
+  for (int k = 0; k < kSortItems; ++k) {
+    if (k >= items) break;
+    if (base + 32 * k + lane < n) {
+      const uint32_t d = ((by_val ? val[k] : key[k]) >> shift) & (kDigits - 1);
+      const uint32_t pos = s.off[d] + s.cnt[w][d] + rank[k];
+      out_key[pos] = key[k];
+      out_val[pos] = val[k];
+    }
+  }
+  __syncthreads();
+  if (!local) {
+    s.off[2 * threadIdx.x] += tot.x;
+    s.off[2 * threadIdx.x + 1] += tot.y;
+    __syncthreads();
+  }
+}
+
+__device__ __forceinline__ void load_blocked(uint32_t key[kSortItems], uint32_t val[kSortItems], const uint32_t *k_src,
+                                             const uint32_t *v_src, int n, int items) {
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int base = w * 32 * items;
+#pragma unroll
+  for (int k = 0; k < kSortItems; ++k) {
+    if (k >= items) break;
+    const int i = base + 32 * k + lane;
+    key[k] = i < n ? k_src[i] : 0u;
+    val[k] = i < n ? v_src[i] : 0u;
+  }
+}
+
+// Bits needed for values <= x.
+__device__ __forceinline__ int nbits(uint32_t x) { return x ? 32 - __clz(x) : 0; }
+
+// Block max of three values (s.red scratch); all threads get the results.
+__device__ __forceinline__ uint3 block_max3(uint3 v, SortSmem &s) {
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    v.x = max(v.x, __shfl_xor_sync(0xffffffffu, v.x, o));
+    v.y = max(v.y, __shfl_xor_sync(0xffffffffu, v.y, o));
+    v.z = max(v.z, __shfl_xor_sync(0xffffffffu, v.z, o));
+  }
+  if (lane == 0) {
+    s.red[0][w] = v.x;
+    s.red[1][w] = v.y;
+    s.red[2][w] = v.z;
+  }
+  __syncthreads();
+  uint3 r = make_uint3(0u, 0u, 0u);
+#pragma unroll
+  for (int k = 0; k < kSortWarps; ++k) {
+    r.x = max(r.x, s.red[0][k]);
+    r.y = max(r.y, s.red[1][k]);
+    r.z = max(r.z, s.red[2][k]);
+  }
+  __syncthreads();
+  return r;
+}
+
+struct TileSortArgs {
+  const float *depth;
+  const int32_t *tile_range;
+  const int32_t *order;  // tile launch order (nullable)
+  uint32_t *misc;        // [2] overflow, [3] length of the slow-path tile list
+  int T;
+  int32_t *ids;  // sorted_idx
+  uint32_t *key_a, *key_b, *val_b;
+  int32_t *slow;  // [T] tiles left to k_tile_sort_big
+  int32_t *mid;   // [T] tiles of kSmallCap+1 .. kChunk entries (k_tile_sort_mid)
+};
+
+// Tiles with <= kChunk entries, one CTA each, one pass: a counting sort on
+// the top kBucketBits bits of (depth bits - tile min) into shared memory
+// (positions within a bucket from shared-memory atomics, i.e. unordered),
+// then every entry placed at its bucket start + the number of entries of its
+// bucket with a smaller exact key (depth bits, id) (buckets hold ~n / 2048
+// entries).  A tile whose buckets
+// exceed kMaxBucket entries (a dense cluster of depths next to a far
+// outlier), or whose list exceeds kChunk, is appended to the slow list.
+// Two instances: kCap = kSmallCap (every tile, in launch order; more CTAs
+// per SM: half the shared memory and registers) passes longer lists to the
+// mid list, which kCap = kChunk sorts (grid-stride); longer ones, and
+// dense-bucket tiles, go to the slow list.
+#ifndef TS_SMALL
+#define TS_SMALL 2048
+#endif
+#ifndef TS_SMALL_MINB
+#define TS_SMALL_MINB 5
+#endif
+constexpr int kSmallCap = TS_SMALL;
+
+template <int kCap>
+struct BucketSmem {
+  uint32_t key[kCap];
+  uint32_t val[kCap];
+  uint32_t cnt[kBuckets];  // counts, then bucket starts
+  uint32_t sh[33];
+  uint32_t red[2][kBucketThreads / 32];
+  int flag;
+};
+
+template <int kCap>
+__device__ __forceinline__ bool tile_sort_one(const TileSortArgs &a, BucketSmem<kCap> &s, int tile, int2 r, int n) {
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  for (int b = threadIdx.x; b < kBuckets; b += kBucketThreads) s.cnt[b] = 0u;
+  if (threadIdx.x == 0) s.flag = 0;
+  constexpr int kIt = kCap / kBucketThreads;
+  const int items = (n + kBucketThreads - 1) / kBucketThreads;
+  uint32_t key[kIt], val[kIt];
+  uint32_t kmin = 0xffffffffu, kmax = 0u;
+#pragma unroll
+  for (int k = 0; k < kIt; ++k) {
+    if (k >= items) break;  // block-uniform: only the rounds this list needs
+    const int i = threadIdx.x + k * kBucketThreads;
+    if (i < n) {
+      val[k] = uint32_t(a.ids[r.x + i]);
+      key[k] = __float_as_uint(__ldg(a.depth + val[k]));
+      kmin = min(kmin, key[k]);
+      kmax = max(kmax, key[k]);
+    }
+  }
+  // block min / max of the depth bits
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    kmin = min(kmin, __shfl_xor_sync(0xffffffffu, kmin, o));
+    kmax = max(kmax, __shfl_xor_sync(0xffffffffu, kmax, o));
+  }
+  if (lane == 0) {
+    s.red[0][w] = kmin;
+    s.red[1][w] = kmax;
+  }
+  __syncthreads();
+#pragma unroll
+  for (int k = 0; k < (kBucketThreads / 32); ++k) {
+    kmin = min(kmin, s.red[0][k]);
+    kmax = max(kmax, s.red[1][k]);
+  }
+  const int shift = max(0, nbits(kmax - kmin) - kBucketBits);
+  uint16_t slot[kIt];
+#pragma unroll
+  for (int k = 0; k < kIt; ++k) {
+    if (k >= items) break;  // block-uniform: only the rounds this list needs
+    const int i = threadIdx.x + k * kBucketThreads;
+    if (i < n) slot[k] = uint16_t(atomicAdd(&s.cnt[(key[k] - kmin) >> shift], 1u));
+  }
+  __syncthreads();
+  // bucket starts (exclusive scan, kBuckets / kBucketThreads buckets per thread)
+  constexpr int kPer = kBuckets / kBucketThreads;
+  uint32_t c[kPer], sum = 0, big = 0;
+#pragma unroll
+  for (int k = 0; k < kPer; ++k) {
+    c[k] = s.cnt[threadIdx.x * kPer + k];
+    sum += c[k];
+    big |= c[k] > kMaxBucket;
+  }
+  if (big) s.flag = 1;
+  uint32_t all;
+  uint32_t ex = block_excl_scan(sum, s.sh, all);
+#pragma unroll
+  for (int k = 0; k < kPer; ++k) {
+    s.cnt[threadIdx.x * kPer + k] = ex;
+    ex += c[k];
+  }
+  __syncthreads();
+  if (s.flag) {  // dense buckets: exact two-key path
+    if (threadIdx.x == 0) a.slow[atomicAdd(&a.misc[3], 1u)] = tile;
+    return false;
+  }
+  // scatter into the buckets (unordered inside a bucket)
+#pragma unroll
+  for (int k = 0; k < kIt; ++k) {
+    if (k >= items) break;  // block-uniform: only the rounds this list needs
+    const int i = threadIdx.x + k * kBucketThreads;
+    if (i < n) {
+      const uint32_t pos = s.cnt[(key[k] - kmin) >> shift] + slot[k];
+      s.key[pos] = key[k];
+      s.val[pos] = val[k];
+    }
+  }
+  __syncthreads();
+  // final position = bucket start + number of bucket entries with a smaller
+  // exact key (depth bits, id): O(bucket size) per entry, no serial chain
+#pragma unroll
+  for (int k = 0; k < kIt; ++k) {
+    if (k >= items) break;  // block-uniform: only the rounds this list needs
+    const int i = threadIdx.x + k * kBucketThreads;
+    if (i < n) {
+      const uint32_t b = (key[k] - kmin) >> shift;
+      const uint32_t b0 = s.cnt[b];
+      const uint32_t be = b + 1 < kBuckets ? s.cnt[b + 1] : uint32_t(n);
+      uint32_t rank = 0;
+      for (uint32_t j = b0; j < be; ++j) {
+        const uint32_t kj = s.key[j], vj = s.val[j];
+        rank += (kj < key[k]) || (kj == key[k] && vj < val[k]);
+      }
+      a.ids[r.x + b0 + rank] = int32_t(val[k]);
+    }
+  }
+  return true;
+}
+
+// One CTA per tile.  kCap = kSmallCap: lists of kSmallCap+1 .. kChunk go to
+// the mid list (k_tile_sort_mid); kCap = kChunk: every list <= kChunk here.
+// Longer lists go to the slow list.
+template <int kCap, int kMinB>
+__global__ void __launch_bounds__(kBucketThreads, kMinB) k_tile_sort(TileSortArgs a) {
+  pdl_begin();
+  __shared__ BucketSmem<kCap> s;
+  const int tile = a.order ? __ldg(a.order + blockIdx.x) : int(blockIdx.x);
+  if (a.misc[2]) return;  // overflow: every range is empty
+  const int2 r = reinterpret_cast<const int2 *>(a.tile_range)[tile];
+  const int n = r.y - r.x;
+  if (n <= 1) return;
+  if (n > kCap) {  // k_tile_sort_mid / _big sort it (and mark it)
+    if (threadIdx.x == 0) {
+      if (n > kChunk)
+        a.slow[atomicAdd(&a.misc[3], 1u)] = tile;
+      else
+        a.mid[atomicAdd(&a.misc[4], 1u)] = tile;
+    }
+    return;
+  }
+  tile_sort_one<kCap>(a, s, tile, r, n);
+}
+
+__global__ void __launch_bounds__(kBucketThreads, 4) k_tile_sort_mid(TileSortArgs a) {
+  pdl_begin();
+  __shared__ BucketSmem<kChunk> s;
+  if (a.misc[2]) return;
+  const int nmid = int(a.misc[4]);
+  for (int q = blockIdx.x; q < nmid; q += gridDim.x) {
+    const int tile = a.mid[q];
+    const int2 r = reinterpret_cast<const int2 *>(a.tile_range)[tile];
+    tile_sort_one<kChunk>(a, s, tile, r, r.y - r.x);
+    __syncthreads();  // the shared buffers are reused by the next tile
+  }
+}
+
+// Tiles of the slow list (grid-stride): exact two-key LSD (id digits, then
+// depth digits) over global memory, chunk by chunk: each chunk of kChunk
+// entries ranked stably per warp round (ballot-sliced peer masks, per-warp
+// digit counters), digit bases carried across chunks from a per-pass
+// histogram.
+__global__ void __launch_bounds__(kSortThreads) k_tile_sort_big(TileSortArgs a) {
+  pdl_begin();
+  __shared__ SortSmem s;
+  if (a.misc[2]) return;
+  const int nslow = int(a.misc[3]);
+  for (int q = blockIdx.x; q < nslow; q += gridDim.x) {
+    const int tile = a.slow[q];
+    const int2 r = reinterpret_cast<const int2 *>(a.tile_range)[tile];
+    const int n = r.y - r.x;
+    uint32_t *vA = reinterpret_cast<uint32_t *>(a.ids) + r.x, *kA = a.key_a + r.x;
+    uint32_t *vB = a.val_b + r.x, *kB = a.key_b + r.x;
+    uint32_t kmin = 0xffffffffu, kmax = 0u, vmax = 0u;
+    for (int i = threadIdx.x; i < n; i += kSortThreads) {
+      const uint32_t v = vA[i];
+      const uint32_t k = __float_as_uint(__ldg(a.depth + v));
+      kA[i] = k;
+      kmin = min(kmin, k);
+      kmax = max(kmax, k);
+      vmax = max(vmax, v);
+    }
+    const uint3 m = block_max3(make_uint3(~kmin, kmax, vmax), s);
+    kmin = ~m.x;
+    for (int i = threadIdx.x; i < n; i += kSortThreads) kA[i] -= kmin;
+    __syncthreads();
+    const int kbits = nbits(m.y - kmin), vbits = nbits(m.z);
+    const int npass_v = (vbits + kDigitBits - 1) / kDigitBits, npass_k = (kbits + kDigitBits - 1) / kDigitBits;
+    for (int p = 0; p < npass_v + npass_k; ++p) {
+      const bool by_val = p < npass_v;
+      const int shift = (by_val ? p : p - npass_v) * kDigitBits;
+      // digit histogram of the whole segment -> global digit bases
+      for (int d = threadIdx.x; d < kDigits; d += kSortThreads) s.off[d] = 0;
+      __syncthreads();
+      for (int i = threadIdx.x; i < n; i += kSortThreads)
+        atomicAdd(&s.off[((by_val ? vA[i] : kA[i]) >> shift) & (kDigits - 1)], 1u);
+      __syncthreads();
+      {
+        const uint32_t c0 = s.off[2 * threadIdx.x], c1 = s.off[2 * threadIdx.x + 1];
+        uint32_t all;
+        const uint32_t ex = block_excl_scan(c0 + c1, s.sh, all);
+        s.off[2 * threadIdx.x] = ex;
+        s.off[2 * threadIdx.x + 1] = ex + c0;
+        __syncthreads();
+      }
+      for (int c0 = 0; c0 < n; c0 += kChunk) {
+        const int cn = min(kChunk, n - c0);
+        const int items = (cn + kSortThreads - 1) / kSortThreads;
+        uint32_t key[kSortItems], val[kSortItems];
+        load_blocked(key, val, kA + c0, vA + c0, cn, items);
+        chunk_pass<true>(key, val, cn, items, by_val, shift, false, s, kB, vB);
+      }
+      uint32_t *t0 = kA, *t1 = vA;
+      kA = kB;
+      vA = vB;
+      kB = t0;
+      vB = t1;
+      __syncthreads();
+    }
+    uint32_t *dst = reinterpret_cast<uint32_t *>(a.ids) + r.x;
+    if (vA != dst)
+      for (int i = threadIdx.x; i < n; i += kSortThreads) dst[i] = vA[i];
+    __syncthreads();
+  }
 }
 
 // Tiles by descending work, 64 buckets of max/64 (single CTA).
@@ -651,9 +782,9 @@ __global__ void __launch_bounds__(1024) k_order_by_work(const int32_t *__restric
   for (int t = threadIdx.x; t < T; t += blockDim.x) m = max(m, work[t]);
   atomicMax(&s_max, m);
   __syncthreads();
-  const int64_t den = int64_t(s_max) + 1;
-  for (int t = threadIdx.x; t < T; t += blockDim.x)
-    atomicAdd(&s_b[63 - int(int64_t(max(work[t], 0)) * 64 / den)], 1u);
+  const uint32_t den = uint32_t(s_max) + 1u;
+  const float iden = 1.0f / float(den);
+  for (int t = threadIdx.x; t < T; t += blockDim.x) atomicAdd(&s_b[63 - bucket64(uint32_t(max(work[t], 0)), den, iden)], 1u);
   __syncthreads();
   if (threadIdx.x == 0) {
     unsigned run = 0;
@@ -665,7 +796,7 @@ __global__ void __launch_bounds__(1024) k_order_by_work(const int32_t *__restric
   }
   __syncthreads();
   for (int t = threadIdx.x; t < T; t += blockDim.x)
-    order[atomicAdd(&s_b[63 - int(int64_t(max(work[t], 0)) * 64 / den)], 1u)] = t;
+    order[atomicAdd(&s_b[63 - bucket64(uint32_t(max(work[t], 0)), den, iden)], 1u)] = t;
 }
 
 }  // namespace gs
@@ -681,7 +812,7 @@ extern "C" int gs_tile_order(const int32_t *work, int32_t T, int32_t *order, voi
 }
 
 extern "C" size_t gs_binsort_workspace_bytes(int32_t n, int64_t capacity, gs_camera cam) {
-  gs::BinLayout L;
+  gs::SortLayout L;
   if (n < 0 || capacity < 0 || !gs::camera_ok(cam) || !gs::make_layout(n, capacity, cam, L)) return 0;
   return L.total;
 }
@@ -698,46 +829,66 @@ extern "C" int gs_bin_sort(gs_proj pr, int32_t n, gs_camera cam, void *ws, size_
     set_error("gs_bin_sort: null or misaligned projection arrays");
     return GS_ERR_INVALID_ARG;
   }
-  BinLayout L;
+  SortLayout L;
   if (!make_layout(n, capacity, cam, L)) {
     set_error("gs_bin_sort: problem too large (n=%d, capacity=%lld, tiles=%d)", n, (long long)capacity,
               tiles_x(cam) * tiles_y(cam));
     return GS_ERR_UNSUPPORTED;
   }
-  if (!ws || ws_bytes < L.total || (reinterpret_cast<uintptr_t>(ws) & 15u)) {
-    set_error("gs_bin_sort: workspace %zu < %zu bytes (or misaligned)", ws_bytes, L.total);
+  if (!ws || ws_bytes < L.total) {
+    set_error("gs_bin_sort: workspace %zu < %zu bytes", ws_bytes, L.total);
     return GS_ERR_WORKSPACE;
   }
   cudaStream_t s = as_stream(stream);
   char *w = static_cast<char *>(ws);
   auto U = [&](size_t off) { return reinterpret_cast<uint32_t *>(w + off); };
+  uint32_t *misc = U(L.misc);
   cudaMemsetAsync(w, 0, L.zero_end, s);
-  DsArgs d{pr.depth, pr.tiles_touched, reinterpret_cast<const short4 *>(pr.rect), n, L.kbase, L.kmax, L.npass,
-           L.dbits, L.ndig, L.gsort, U(L.hist), U(L.ctr), U(L.status), {U(L.key0), U(L.key1)},
-           {U(L.val0), U(L.val1)}, reinterpret_cast<short4 *>(w + L.srect)};
-  const uint32_t *ids = (L.npass & 1) ? U(L.val1) : U(L.val0);  // pass p writes val[(p + 1) & 1]
-  const size_t ds_smem = size_t(kDsWarps) * L.ndig * 2 + size_t(L.ndig) * 4;
-  const size_t cnt_smem = size_t(L.T) * 4;
-  const size_t emit_smem = size_t(L.T) * 4 + ((size_t(L.wb) * L.T * 2 + 3) & ~size_t(3));
-  static thread_local size_t smem_set = 0;
-  const size_t need = std::max(std::max(ds_smem, emit_smem), cnt_smem);
+  const short4 *rect = reinterpret_cast<const short4 *>(pr.rect);
+  const size_t diff_bytes = size_t(4) * (L.TX + 1) * (L.TY + 1);
+  const size_t emit_bytes = diff_bytes + size_t(4) * L.T;
+  static thread_local size_t smem_set = 0, smem_set_emit[9] = {0};
+  const size_t need = std::max(diff_bytes, emit_bytes);
   if (need > 48 * 1024 && need > smem_set) {
-    cudaFuncSetAttribute(k_ds_pass, cudaFuncAttributeMaxDynamicSharedMemorySize, int(std::max(ds_smem, size_t(48) << 10)));
-    cudaFuncSetAttribute(k_bin_count, cudaFuncAttributeMaxDynamicSharedMemorySize, int(std::max(cnt_smem, size_t(48) << 10)));
-    cudaFuncSetAttribute(k_bin_emit, cudaFuncAttributeMaxDynamicSharedMemorySize, int(std::max(emit_smem, size_t(48) << 10)));
+    cudaFuncSetAttribute(k_bin_prep, cudaFuncAttributeMaxDynamicSharedMemorySize, int(diff_bytes));
+    cudaFuncSetAttribute(k_tile_counts, cudaFuncAttributeMaxDynamicSharedMemorySize, int(diff_bytes));
     smem_set = need;
   }
-  BinArgs b{U(L.hist), L.ndig, ids, reinterpret_cast<const short4 *>(w + L.srect), U(L.pre), U(L.wstart),
-            U(L.pstatus), U(L.ctr) + 4, U(L.misc), L.TX, L.TY, L.T, L.gbin, L.wb, uint32_t(kBlockPairs / L.wb),
-            U(L.cnt), U(L.totals), capacity, sorted_idx, tile_range, tile_order, n_pairs, cnt};
   if (n > 0) {
-    const int hb = std::max(1, std::min(2 * 148, (n + 4 * kHistThreads - 1) / (4 * kHistThreads)));
-    launch_pdl(k_ds_hist, dim3(hb), dim3(kHistThreads), size_t(4) * L.npass * L.ndig, s, d);
-    for (int p = 0; p < L.npass; ++p) launch_pdl(k_ds_pass, dim3(L.gsort), dim3(kDsThreads), ds_smem, s, d, p);
-    launch_pdl(k_bin_prefix, dim3(L.gsort), dim3(kDsThreads), 0, s, b);
-    launch_pdl(k_bin_count, dim3(L.gbin), dim3(32 * L.wb), cnt_smem, s, b);
-    launch_pdl(k_bin_scan, dim3((L.T + 7) / 8), dim3(256), 0, s, b);
+    const int blocks = std::max(1, std::min(2 * 148, (n + 255) / 256));
+    launch_pdl(k_bin_prep, dim3(blocks), dim3(256), diff_bytes, s, pr.tiles_touched, rect, n, L.TX, L.TY, U(L.diff));
   }
-  launch_pdl(k_bin_emit, dim3(L.gbin), dim3(32 * L.wb), emit_smem, s, b);
+  {
+    TileArgs a{U(L.diff), L.TX, L.TY, L.T, capacity, tile_range, tile_order, U(L.cursor), n_pairs, misc, cnt};
+    launch_pdl(k_tile_counts, dim3(1), dim3(1024), diff_bytes, s, a);
+  }
+  if (n > 0 && capacity > 0) {
+    // Gaussians per thread: the smallest of 1, 2, 4, 8 that fits the grid in
+    // one wave of 2 CTAs per SM (the per-CTA set-up, a 2-D prefix and one
+    // cursor reservation per tile, is then paid about twice per SM)
+    int per = 1;
+    while (per < 8 && (n + kEmitThreads * per - 1) / (kEmitThreads * per) > 2 * 148) per *= 2;
+    const int eb = (n + kEmitThreads * per - 1) / (kEmitThreads * per);
+    auto kern = per == 1 ? k_emit<1> : per == 2 ? k_emit<2> : per == 4 ? k_emit<4> : k_emit<8>;
+    if (need > 48 * 1024 && need > smem_set_emit[per]) {
+      cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(emit_bytes));
+      smem_set_emit[per] = need;
+    }
+    launch_pdl(kern, dim3(eb), dim3(kEmitThreads), emit_bytes, s, pr.tiles_touched, rect, n, L.TX, L.TY,
+               U(L.cursor), misc, sorted_idx);
+    TileSortArgs a{pr.depth, tile_range, tile_order, misc, L.T, sorted_idx, U(L.key_a),
+                   U(L.key_b), U(L.val_b), reinterpret_cast<int32_t *>(U(L.slow)),
+                   reinterpret_cast<int32_t *>(U(L.mid))};
+    // lists averaging <= 1800 entries: the half-size instance (more CTAs per
+    // SM) with the rare longer lists on the mid path; longer averages (e.g.
+    // BJ.configs[4]): every list <= kChunk in one pass
+    if (capacity <= int64_t(1800) * L.T) {
+      launch_pdl(k_tile_sort<kSmallCap, TS_SMALL_MINB>, dim3(L.T), dim3(kBucketThreads), 0, s, a);
+      launch_pdl(k_tile_sort_mid, dim3(std::min(L.T, 4 * kBigBlocks)), dim3(kBucketThreads), 0, s, a);
+    } else {
+      launch_pdl(k_tile_sort<kChunk, 4>, dim3(L.T), dim3(kBucketThreads), 0, s, a);
+    }
+    launch_pdl(k_tile_sort_big, dim3(std::min(L.T, kBigBlocks)), dim3(kSortThreads), 0, s, a);
+  }
   return check_launch("gs_bin_sort");
 }

@@ -316,21 +316,13 @@ class MapStep:
         return len(self.mine) * per_view
 
 
-def _sort_passes(cam):
-    """Radix passes of gs_bin_sort's depth sort (binsort.cu make_layout): the
-    keys span nbits(bits(z_far) - bits(z_near)) bits, <= 11 bits per pass."""
-    import struct
-    bits = lambda f: struct.unpack("<I", struct.pack("<f", f))[0]
-    nb = max(1, (bits(cam.z_far) - bits(cam.z_near)).bit_length())
-    return (nb + 10) // 11
-
-
 def kernels_per_view(cam, loss=True, bwd=True, capacity=0):
     """Kernels of ours per view (the sort's memset is a copy-engine node, not a kernel):
-    project 1; bin_sort: depth histogram, npass radix passes, pair prefix, tile
-    counts, count scan, emission (5 + npass = 8 for z 0.2..100 m); render 1 +
-    backward tile order 1; loss 3; backward 2."""
-    n = 1 + (5 + _sort_passes(cam)) + 2
+    project 1; bin_sort: prep, tile counts, emit, tile sort, [mid-list sort when the
+    pair capacity averages <= 1800 per tile,] long-list sort = 5 or 6;
+    render 1 + backward tile order 1; loss 3; backward 2."""
+    T = ((cam.width + 15) // 16) * ((cam.height + 15) // 16)
+    n = 1 + (6 if capacity <= 1800 * T else 5) + 2
     if loss:
         n += 3
     if bwd:
