@@ -38,9 +38,10 @@ struct PixGeom {
   bool row_in;  // py < H
 };
 
+// w: the warp block of the tile this warp owns (default: its warp index)
 template <class G>
-__device__ __forceinline__ PixGeom pix_geom(int tx, int ty, int H) {
-  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+__device__ __forceinline__ PixGeom pix_geom(int tx, int ty, int H, int w = int(threadIdx.x >> 5)) {
+  const int lane = threadIdx.x & 31;
   PixGeom g;
   const int lx = G::bx(w) + (lane % G::kLanesPerRow) * (kTilePx / G::kThreads);
   const int ly = G::by(w) + lane / G::kLanesPerRow;
@@ -124,11 +125,12 @@ __device__ __forceinline__ unsigned box_block_mask(float4 b) {
 }
 
 // This warp's hit list over a staged batch of B entries: the indices
-// (ascending) of the entries j < cnt whose mask has bit w, written to
-// list[0..n), followed by `sentinel` at list[n].  Returns n.
+// (ascending) of the entries j < cnt whose mask has bit w (default: the warp
+// index), written to list[0..n), followed by `sentinel` at list[n].  Returns n.
 template <int B = kBatch, class L>
-__device__ __forceinline__ int warp_hit_list(const unsigned char *s_mask, int cnt, L *list, int sentinel) {
-  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+__device__ __forceinline__ int warp_hit_list(const unsigned char *s_mask, int cnt, L *list, int sentinel,
+                                             int w = int(threadIdx.x >> 5)) {
+  const int lane = threadIdx.x & 31;
   int n = 0;
 #pragma unroll
   for (int h = 0; h < B / 32; ++h) {
