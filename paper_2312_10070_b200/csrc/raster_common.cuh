@@ -124,6 +124,52 @@ __device__ __forceinline__ unsigned box_block_mask(float4 b) {
   return m;
 }
 
+// Exact culling of an entry against the warp blocks (a refinement of the box
+// test): the minimum over the continuous block rectangle [x0, x1] x [y0, y1]
+// (tile-local pixel centres) of E = y1^2 + y2^2 = (a' dx + b' dy)^2 +
+// (d' dy)^2, dx = u_l - x, dy = v_l - y, compared with R^2 = log2 o -
+// kExpSkip.  The rectangle contains every pixel centre of the block, so a
+// block with min E > R^2 has e = log2 o - E < kExpSkip < kExpMin at all of its
+// pixels (the kExpSkip margin, 6.5e-4, covers the fp32 rounding of E there
+// and here): dropping it never changes a decision.  The minimum of the convex
+// E is 0 if (dx, dy) = 0 lies in the rectangle, else on an edge: on dy = Y at
+// dx = -b' Y / a', on dx = X at dy = -a' b' X / (b'^2 + d'^2), clamped.
+__device__ __forceinline__ float rect_min_E(float a, float b, float d, float ia, float ibd, float dx0, float dx1,
+                                            float dy0, float dy1) {
+  if (dx0 <= 0.f && dx1 >= 0.f && dy0 <= 0.f && dy1 >= 0.f) return 0.f;
+  const float d2 = d * d;
+  auto edge_y = [&](float y) {
+    const float x = fminf(fmaxf(-b * y * ia, dx0), dx1);
+    const float u = fmaf(a, x, b * y);
+    return fmaf(u, u, d2 * y * y);
+  };
+  auto edge_x = [&](float x) {
+    const float y = fminf(fmaxf(-a * b * x * ibd, dy0), dy1);
+    const float u = fmaf(a, x, b * y);
+    return fmaf(u, u, d2 * y * y);
+  };
+  return fminf(fminf(edge_y(dy0), edge_y(dy1)), fminf(edge_x(dx0), edge_x(dx1)));
+}
+
+// Bit w set iff the entry can pass the exponent pre-test at some pixel of
+// warp block w: the box test, then the exact rectangle test.
+template <class G>
+__device__ __forceinline__ unsigned entry_block_mask(float4 coef, float ul, float vl) {
+  const float R2 = coef.w - kExpSkip;
+  const unsigned m = box_block_mask<G>(entry_box(coef, ul, vl));
+  if (!m) return 0u;
+  const float ia = 1.0f / coef.x, ibd = 1.0f / fmaf(coef.y, coef.y, coef.z * coef.z);
+  unsigned r = 0u;
+#pragma unroll
+  for (int w = 0; w < G::kWarps; ++w) {
+    if (!((m >> w) & 1u)) continue;
+    const float x0 = float(G::bx(w)), y0 = float(G::by(w));
+    const float x1 = x0 + float(16 / G::kAcross - 1), y1 = y0 + float(G::kRows - 1);
+    if (rect_min_E(coef.x, coef.y, coef.z, ia, ibd, ul - x1, ul - x0, vl - y1, vl - y0) <= R2) r |= 1u << w;
+  }
+  return r;
+}
+
 // This warp's hit list over a staged batch of B entries: the indices
 // (ascending) of the entries j < cnt whose mask has bit w (default: the warp
 // index), written to list[0..n), followed by `sentinel` at list[n].  Returns n.

@@ -345,7 +345,7 @@ __global__ void __launch_bounds__(BG::kThreads, kBwdMinBlocks) k_bwd_pixels(BwdA
         rc.rgbz = __ldg(a.rgbz + g);
         rc.conic = __ldg(a.conic_o + g);
         rc.idx = g;
-        s_mask[i] = (unsigned char)box_block_mask<BG>(entry_box(cf, ul, vl));
+        s_mask[i] = (unsigned char)entry_block_mask<BG>(cf, ul, vl);
       }
     }
     __syncthreads();

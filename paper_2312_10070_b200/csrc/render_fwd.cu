@@ -172,7 +172,7 @@ __global__ void __launch_bounds__(FG::kThreads, FWD_MINB) k_render_fwd(FwdArgs a
         rc.p = et.p;
         rc.q = et.q;
         rc.rgbz = __ldg(a.rgbz + g);
-        s_mask[i] = (unsigned char)box_block_mask<FG>(entry_box(cf, ul, vl));
+        s_mask[i] = (unsigned char)entry_block_mask<FG>(cf, ul, vl);
       }
     }
     __syncthreads();
