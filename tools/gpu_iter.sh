@@ -12,9 +12,11 @@ import json
 d = json.load(open("gpurun_out/bench.json"))
 print("MP/s %.1f  ms/step %.3f  e2e %s" % (d["value"], d["ms_per_step"], d.get("e2e", {}).get("value")))
 ro = d["roofline_other"]
-for k in ("render_fwd_isolated", "render_bwd_pixels_isolated"):
-    print("%-28s %.1f us  frac %.3f" % (k, ro[k]["ms_per_launch"] * 1e3, ro[k]["frac"]))
-print("roofline(in-step) frac %.3f  %.1f us active of %.1f per step" % (d["roofline"]["frac"], d["roofline"].get("ms_active_per_step", 0) * 1e3, d["ms_per_step"] * 1e3))
+for k, v in (("render_fwd_isolated", ro["render_fwd_isolated"]), ("render_bwd_pixels_isolated", d["roofline"])):
+    print("%-28s %.1f us  frac %.3f" % (k, v["ms_per_launch"] * 1e3, v["frac"]))
+ins = ro["render_bwd_pixels_in_step"]
+print("bwd in-step frac %.3f  %.1f us active of %.1f per step; p10/50/90 %s" % (ins["frac"], ins.get("ms_active_per_step", 0) * 1e3, d["ms_per_step"] * 1e3, d.get("ms_per_step_p10_p50_p90")))
+if "single_view" in d: print("single view (config1) MP/s %.1f" % d["single_view"]["value"])
 if "tracking" in d: print("tracking it/s %.1f" % d["tracking"]["value"])
 if "mapping_ssim" in d: print("mapping+SSIM MP/s %.1f" % d["mapping_ssim"]["value"])
 if "optimizer" in d: print("optimizer %.1f us  %.0f GB/s" % (d["optimizer"]["ms"] * 1e3, d["optimizer"]["achieved_gbs"]))

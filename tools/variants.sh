@@ -12,6 +12,6 @@ d = json.load(open("gpurun_out/v.json"))
 ro = d["roofline_other"]
 print("%-28s MP/s %7.1f  ms %.3f  fwd %.1f us  bwd %.1f us  track %.0f it/s" % (
     sys.argv[1], d["value"], d["ms_per_step"], ro["render_fwd_isolated"]["ms_per_launch"] * 1e3,
-    ro["render_bwd_pixels_isolated"]["ms_per_launch"] * 1e3, d.get("tracking", {}).get("value", 0)))
+    d["roofline"]["ms_per_launch"] * 1e3, d.get("tracking", {}).get("value", 0)))
 PY
 done
