@@ -228,8 +228,9 @@ int gs_bin_sort(gs_proj pr, int32_t n, gs_camera cam, void *ws, size_t ws_bytes,
  *             composited entry) + 1, 0 if none
  *   stats     (device, nullable) [2][H][W] int32: entries scanned, entries
  *             composited — the per-pixel counts of SURVEY §8(d)
- *   tile_work (device, nullable) [T] int32: sum of n_contrib over the tile's
- *             pixels (the backward's work per tile, for gs_tile_order). */
+ *   tile_work (device, nullable) [T] int32: the backward's work proxy per
+ *             tile for gs_tile_order: the largest n_contrib of the tile
+ *             (the backward's warps walk back from their strip's largest). */
 int gs_render_fwd(gs_proj pr, const int32_t *sorted_idx, const int32_t *tile_range,
                   const int32_t *tile_order, gs_camera cam, float *color, float *depth,
                   float *alpha, float *T_final, int32_t *n_contrib, int32_t *stats,

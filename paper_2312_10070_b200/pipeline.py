@@ -131,6 +131,15 @@ class MapStep:
         self.fused_loss = fused_loss  # used while self.ssim == 0 (the L1 loss is pixel-local)
         self.tgt_scales = {}
         self.atomic_gauss = atomic_gauss
+        # the forward of a view is launched in its previous step's work order
+        # (the backward's heaviest-first order of the same view on the same
+        # lane: the parameters move little between steps); scheduling only
+        self.reuse_order = True
+        self._lane_view = {}
+
+    def fwd_order(self, r, v):
+        """Tile launch order for view v's forward on lane r (None: gs_bin_sort's)."""
+        return r.bwd_order if self.reuse_order and self._lane_view.get(id(r)) == v else None
 
     def size(self, slack=1.25):
         """Setup only (host sync): pair capacity = slack x max pairs over my views."""
@@ -186,7 +195,9 @@ class MapStep:
         if self.fused_loss and self.ssim == 0.0:
             if tgt_ready is not None:
                 torch.cuda.current_stream().wait_event(tgt_ready)
-            r.render_l1(self.tgt_color[v], self.tgt_depth[v], self.lc, self.ld, self.tgt_scales[v])
+            r.render_l1(self.tgt_color[v], self.tgt_depth[v], self.lc, self.ld, self.tgt_scales[v],
+                        order=self.fwd_order(r, v))
+            self._lane_view[id(r)] = v
         else:
             r.render()
             if tgt_ready is not None:

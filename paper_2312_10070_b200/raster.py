@@ -440,15 +440,16 @@ class Rasterizer:
         gs_loss_scales(self.cam, tgt_depth, lambda_color, lambda_depth, self.loss_ws, out)
         return out
 
-    def render_l1(self, tgt_color, tgt_depth, lambda_color, lambda_depth, scales):
+    def render_l1(self, tgt_color, tgt_depth, lambda_color, lambda_depth, scales, order=None):
         """S3 + S4 fused (after project + bin_sort): gs_render_fwd_l1 writes the
         frame and gs_loss's gradient maps and per-tile |residual| sums, then
         gs_loss_from_tiles -> self.loss[:3]; scales from loss_scales (same
-        lambdas)."""
+        lambdas).  order: the forward's tile launch order (default: gs_bin_sort's
+        list-length order); scheduling only."""
         if self.loss_part is None:
             self.loss_part = torch.empty(2 * self.T, dtype=torch.float64, device=self.device)
         gs_render_fwd_l1(self.proj, self.sorted_idx, self.tile_range, self.cam, self.frame, tgt_color, tgt_depth,
-                         scales, self.dL_dcolor, self.dL_ddepth, tile_order=self.tile_order,
+                         scales, self.dL_dcolor, self.dL_ddepth, tile_order=self.tile_order if order is None else order,
                          tile_work=self.tile_work, loss_part=self.loss_part)
         gs_tile_order(self.tile_work, self.T, self.bwd_order)
         gs_loss_from_tiles(self.cam, self.loss_part, scales, lambda_color, lambda_depth, self.loss)
