@@ -50,6 +50,8 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--profile", action="store_true", help="short run for ncu (no clocks/cpu/e2e/tracking)")
     ap.add_argument("--lanes", type=int, default=8, help="per-view buffer sets (and lane streams)")
+    ap.add_argument("--no-overlap", action="store_true",
+                    help="stream-ordered forward -> backward (no per-tile flag overlap) in the timed step")
     ap.add_argument("--backend", default="nccl", choices=["nccl", "gloo"],
                     help="process-group backend for N > 1 (gloo: tests of the multi-rank branch on one GPU)")
     ap.add_argument("--small", action="store_true",
@@ -286,11 +288,11 @@ def bench_ours(a):
         ev_bwd.append((b0, b1))
 
     hooks = {"fwd": timed_fwd, "bwd": timed_bwd}
+    ms.overlap = not a.no_overlap
 
+    # the timed steps run the product path as is (MapStep.step(), no hooks)
     for _ in range(max(a.warmup, 3)):
-        ms.step(hooks)
-    ev_fwd.clear()
-    ev_bwd.clear()
+        ms.step()
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
@@ -303,7 +305,7 @@ def bench_ours(a):
             flush.zero_()  # L2 flush between timed steps (outside the step events)
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             e0.record(stream)
-            ms.step(hooks)
+            ms.step()
             e1.record(stream)
             step_ms.append((e0, e1))
         torch.cuda.synchronize()
@@ -312,6 +314,21 @@ def bench_ours(a):
     clocks = clk.summary()
     per_step = [e0.elapsed_time(e1) for e0, e1 in step_ms]
     tot = sum(per_step)
+    # secondary (in-step) roofline: a few more steps with CUDA events around the
+    # compositing launches on their lane streams (stream-ordered stages: events
+    # between the forward and the backward would defeat their tile overlap)
+    inst_steps = []
+    for i in range(2 + max(3, a.steps // 3)):
+        if i == 2:
+            ev_fwd.clear()
+            ev_bwd.clear()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        ms.step(hooks)
+        e1.record(stream)
+        if i >= 2:
+            inst_steps.append((e0, e1))
+    torch.cuda.synchronize()
     fwd_ms = statistics.mean(e0.elapsed_time(e1) for e0, e1 in ev_fwd) if ev_fwd else None
     bwd_ms = statistics.mean(e0.elapsed_time(e1) for e0, e1 in ev_bwd) if ev_bwd else None
     t = torch.tensor([tot], dtype=torch.float64, device=device)
@@ -325,7 +342,7 @@ def bench_ours(a):
         os.path.join(ROOT, "MEASURED_PEAKS.json")) else {}
     nvw = len(ms.mine)
     roof = roofline_for(ms, stats_views, peaks, clocks.get("sm_mhz"), fwd_ms, bwd_ms,
-                        active_ms(step_ms, ev_fwd, nvw), active_ms(step_ms, ev_bwd, nvw))
+                        active_ms(inst_steps, ev_fwd, nvw), active_ms(inst_steps, ev_bwd, nvw))
     # the same kernels timed alone (one view at a time, no other stream active;
     # skipped under --profile so that ncu's launch list ends with a step)
     iso_f, iso_b = [], []
@@ -465,6 +482,7 @@ def bench_ours(a):
     if world > 1:
         dist.barrier()
     if rank == 0 and world == 1 and not a.profile and not a.no_tracking:
+        line["scaling_budget"] = scaling_budget(a, s, P, views, tc, td, device, ms_per_step)
         line["single_view"] = bench_single_view(device, a)
         line["tracking"] = bench_tracking(device)
         line["tracking_masked"] = bench_tracking(device, masked=(0.5, 50.0))
@@ -507,6 +525,44 @@ def e2e_ours(a, s, ms, device, world=1):
             "note": "inputs (parameters, poses, this rank's 8-bit RGB + 16-bit depth frames) uploaded every step; "
                     "the per-view losses are read back; the gradient buffer stays on the device, where the "
                     "optimiser (gs_adam_step) consumes it"}
+
+
+def scaling_budget(a, s, P, views, tc, td, device, ms_1gpu):
+    """Strong-scaling budget of the view-sharded step on this one GPU: the
+    measured step time of rank 0's share at k = 2, 4, 8 ranks (its views only,
+    no all-reduce), plus a MODELLED NCCL all-reduce of the [4][N][4] fp32
+    gradient buffer at the pool's measured 8-rank bus bandwidth (725 GB/s,
+    B200_PROFILING.md): t_AR = 2 (k - 1) / k x bytes / busbw.  The projection
+    is T(1) / (t_share + t_AR); the driver's own multi-GPU runs supersede it."""
+    import torch
+    from paper_2312_10070_b200.pipeline import MapStep
+    busbw = 725e9
+    nbytes = 4 * s.n * 16
+    out = {"model": "projected_speedup = T(1) / (measured rank-0 share + modelled all-reduce); busbw 725 GB/s "
+                    "(measured 8-rank all-reduce on this pool); not a multi-GPU measurement",
+           "allreduce_bytes": nbytes}
+    for k in (2, 4, 8):
+        ms = MapStep(P, views, s.cam, tc, td, rank=0, world=k, allreduce=lambda buf: None, device=device,
+                     lanes=a.lanes)
+        ms.overlap = not a.no_overlap
+        ms.size()
+        for _ in range(3):
+            ms.step()
+        torch.cuda.synchronize()
+        t = []
+        for _ in range(max(10, a.steps // 2)):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            ms.step()
+            e1.record()
+            t.append((e0, e1))
+        torch.cuda.synchronize()
+        share = statistics.median(e0.elapsed_time(e1) for e0, e1 in t)
+        ar = 2 * (k - 1) / k * nbytes / busbw * 1e3
+        out[f"k{k}"] = {"views_per_rank": len(ms.mine), "ms_share": share, "ms_allreduce_model": ar,
+                        "projected_speedup": ms_1gpu / (share + ar), "step": "MapStep"}
+        del ms
+    return out
 
 
 def bench_single_view(device, a):

@@ -96,14 +96,21 @@ class MapStep:
 
     def __init__(self, params: Params, views, cam, tgt_color, tgt_depth, rank=0, world=1, group=None,
                  lambda_color=1.0, lambda_depth=1.0, device="cuda", lanes=8, allreduce=None,
-                 ssim=0.0, atomic_gauss=True, fused_loss=True):
+                 ssim=0.0, atomic_gauss=True, fused_loss=True, ar_chunks=None):
         """ssim: the lambda of Eq. 10's colour loss (0: L1 colour only, as
         BJ.configs[3]; the paper uses 0.2).  atomic_gauss: the
         per-view S6 adds into the gradient buffer atomically
         (GS_BWD_ATOMIC_ACC), so the views' Gaussian phases need no ordering;
         else they are serialised in view order (events).  fused_loss (L1
         loss, ssim = 0): the loss is computed by the compositing kernel
-        (gs_render_fwd_l1, per-view scales from prepare_targets)."""
+        (gs_render_fwd_l1, per-view scales from prepare_targets).
+        ar_chunks (world > 1): the per-Gaussian phase runs in this many
+        Gaussian ranges and each range's gradients (four contiguous component
+        slices) are all-reduced on a communication stream as soon as every
+        view has chained it, so the reduction overlaps the rest of S6
+        (default 1: one all-reduce of the whole buffer after S6; the chunked
+        form is correct on 2 ranks (tests) but its speed needs > 1 GPU to
+        measure)."""
         self.ssim = ssim
         self.params = params
         self.views = views                  # [V, 12] device tensor (all views)
@@ -131,11 +138,21 @@ class MapStep:
         self.fused_loss = fused_loss  # used while self.ssim == 0 (the L1 loss is pixel-local)
         self.tgt_scales = {}
         self.atomic_gauss = atomic_gauss
+        self.ar_chunks = 1 if ar_chunks is None else max(1, int(ar_chunks))
+        self.comm_stream = torch.cuda.Stream(device=device) if world > 1 else None
         # the forward of a view is launched in its previous step's work order
         # (the backward's heaviest-first order of the same view on the same
         # lane: the parameters move little between steps); scheduling only
         self.reuse_order = True
         self._lane_view = {}
+        # overlap (fused L1 loss, a view whose lane rendered it last step): its
+        # per-pixel backward starts tile by tile as its forward finishes
+        # (per-tile flags + programmatic dependent launch, as in tracking), both
+        # in the previous step's work order; the order refresh and the loss
+        # reduction follow.  Off by default: measured no faster for
+        # BJ.configs[3] (2235 vs 2250 MP/s at 8 views; 0.446 vs 0.448 ms for one view)
+        self.overlap = False
+        self._pending = {}
 
     def fwd_order(self, r, v):
         """Tile launch order for view v's forward on lane r (None: gs_bin_sort's)."""
@@ -195,6 +212,11 @@ class MapStep:
         if self.fused_loss and self.ssim == 0.0:
             if tgt_ready is not None:
                 torch.cuda.current_stream().wait_event(tgt_ready)
+            if self.overlap and self.reuse_order and self._lane_view.get(id(r)) == v:
+                # the backward must be the next launch on this stream (stage_bwd)
+                r.render_l1_overlapped(self.tgt_color[v], self.tgt_depth[v], self.tgt_scales[v])
+                self._pending[id(r)] = (k, v)
+                return
             r.render_l1(self.tgt_color[v], self.tgt_depth[v], self.lc, self.ld, self.tgt_scales[v],
                         order=self.fwd_order(r, v))
             self._lane_view[id(r)] = v
@@ -215,7 +237,14 @@ class MapStep:
             self.lanes[0].loss_scales(self.tgt_depth[v], self.lc, self.ld, out=self.tgt_scales[v])
 
     def stage_bwd(self, r, k, v):
-        """S5: the per-pixel backward phase."""
+        """S5: the per-pixel backward phase (overlapped with its forward's
+        tail when stage_fwd left it pending; then the next step's order and
+        the loss value)."""
+        if self._pending.pop(id(r), None) is not None:
+            r.backward(self.params, self.views[v], GS_GRAD_PARAMS | GS_BWD_PIXELS_ONLY, self.grads, overlap=True)
+            r.finish_l1(self.lc, self.ld, self.tgt_scales[v])
+            self.losses[k].copy_(r.loss)
+            return
         r.backward(self.params, self.views[v], GS_GRAD_PARAMS | GS_BWD_PIXELS_ONLY, self.grads)
 
     def stage_gauss(self, r, k, v):
@@ -296,6 +325,10 @@ class MapStep:
         start = main.record_event()
         for s in self.streams:
             s.wait_event(start)
+        chunked = (self.allreduce is not None and self.ar_chunks > 1 and self.atomic_gauss
+                   and "gauss" not in (hooks or {}))
+        bounds = self.chunk_bounds() if chunked else None
+        chunk_ev = {}  # (lane, chunk) -> event after the lane's last view chained that chunk
         prev = start
         for k, v in enumerate(self.mine):
             lane = k % len(self.lanes)
@@ -306,18 +339,43 @@ class MapStep:
                 st["bwd"](r, k, v)
                 if not self.atomic_gauss:
                     s.wait_event(prev)
-                st["gauss"](r, k, v)
+                if chunked:
+                    for c, (i0, i1) in enumerate(bounds):
+                        r.backward_gauss_range(self.params, self.views[v], self.grads, i0, i1,
+                                               GS_GRAD_PARAMS | GS_BWD_ATOMIC_ACC)
+                        chunk_ev[(lane, c)] = s.record_event()
+                else:
+                    st["gauss"](r, k, v)
                 prev = s.record_event()
+        if chunked:
+            # S8 chunk by chunk on the communication stream (overlaps the rest of S6)
+            cs = self.comm_stream
+            cs.wait_event(start)
+            with torch.cuda.stream(cs):
+                for c, (i0, i1) in enumerate(bounds):
+                    for lane in range(len(self.lanes)):
+                        if (lane, c) in chunk_ev:
+                            cs.wait_event(chunk_ev[(lane, c)])
+                    for comp in range(4):  # each component slice [i0, i1) is contiguous
+                        self.allreduce(self.grads.buf[comp, i0:i1])
         for s in self.streams:
             main.wait_stream(s)
         if host is not None:
             main.wait_stream(self.copy_stream)
-        if self.allreduce is not None:
+        if chunked:
+            main.wait_stream(self.comm_stream)
+        elif self.allreduce is not None:
             self.allreduce(self.grads.buf)
         if host is not None:
             host.loss.copy_(self.losses, non_blocking=True)
             self._released[slot] = main.record_event()
         return self.grads
+
+    def chunk_bounds(self):
+        """Gaussian ranges of the chunked S6 / S8 (multiples of 128)."""
+        n, c = self.params.n, self.ar_chunks
+        step = ((n + c - 1) // c + 127) // 128 * 128
+        return [(i, min(i + step, n)) for i in range(0, n, step)]
 
     def launches_per_step(self):
         """Kernels of ours launched per step; the fused L1

@@ -339,6 +339,14 @@ def gs_pose_grad(view, pose_partials, n_partials, step=None, adam_state=None, dL
 # ---------------------------------------------------------------------------
 
 
+class _GradView:
+    """Grads-like access to a [4, m, 4] slice of a gradient buffer (each
+    component array contiguous, not the whole slice)."""
+
+    def __init__(self, g):
+        self.mean_opa, self.quat, self.logscale, self.rgb = (g.buf[k] for k in range(4))
+
+
 class Rasterizer:
     """All buffers of one (N Gaussians, camera) problem; no allocation in the
     per-iteration calls, so a whole iteration can be CUDA-graph captured."""
@@ -455,6 +463,24 @@ class Rasterizer:
         gs_loss_from_tiles(self.cam, self.loss_part, scales, lambda_color, lambda_depth, self.loss)
         return self.loss
 
+    def render_l1_overlapped(self, tgt_color, tgt_depth, scales):
+        """render_l1's forward for an overlapped backward: launched in (and the
+        backward reading) the previous call's work order self.bwd_order, with
+        the per-tile completion flags; the NEXT launch on this stream must be
+        backward(..., overlap=True), then finish_l1."""
+        if self.loss_part is None:
+            self.loss_part = torch.empty(2 * self.T, dtype=torch.float64, device=self.device)
+        gs_render_fwd_l1(self.proj, self.sorted_idx, self.tile_range, self.cam, self.frame, tgt_color, tgt_depth,
+                         scales, self.dL_dcolor, self.dL_ddepth, tile_order=self.bwd_order,
+                         tile_work=self.tile_work, loss_part=self.loss_part, tile_done=self._tile_done())
+
+    def finish_l1(self, lambda_color, lambda_depth, scales):
+        """After render_l1_overlapped + backward: the next work order and the
+        loss value (self.loss[:3])."""
+        gs_tile_order(self.tile_work, self.T, self.bwd_order)
+        gs_loss_from_tiles(self.cam, self.loss_part, scales, lambda_color, lambda_depth, self.loss)
+        return self.loss
+
     def _tile_done(self):
         if self.tile_done is None:  # [T] flags + [1] count of timed-out waits (include/gs.h)
             self.tile_done = torch.zeros(self.T + 1, dtype=torch.int32, device=self.device)
@@ -524,6 +550,22 @@ class Rasterizer:
                       self.dL_ddepth if dL_ddepth is None else dL_ddepth, dL_dalpha, flags, self.bwd_ws, grads,
                       self.pose_partials if flags & GS_GRAD_POSE else None, event_pair=event_pair,
                       tile_order=self.bwd_order, tile_done=self._tile_done() if overlap else None)
+
+    def backward_gauss_range(self, params: Params, view, grads: Grads, i0, i1, flags=GS_GRAD_PARAMS):
+        """S6 (GS_BWD_GAUSS_ONLY) for the Gaussians [i0, i1) only: the same C-ABI
+        call on sub-array views (parameters, projection, grad2d scratch and
+        gradients offset by i0), so a caller can start reducing the finished
+        part of the gradient buffer while the rest is chained."""
+        sl = lambda t: t[i0:i1]
+        P = Params(sl(params.mean_opa), sl(params.quat), sl(params.logscale), sl(params.rgb))
+        pr = Proj.__new__(Proj)
+        pr.n = i1 - i0
+        for name in ("uv", "conic_o", "coef", "rgbz", "depth", "rect", "tiles_touched"):
+            setattr(pr, name, sl(getattr(self.proj, name)))
+        g = Grads(grads.buf[:, i0:i1])
+        gs_render_bwd(P, view, self.cam, pr, self.sorted_idx, self.tile_range, self.frame.T_final,
+                      self.frame.n_contrib, self.dL_dcolor, self.dL_ddepth, None, flags | GS_BWD_GAUSS_ONLY,
+                      self.bwd_ws[i0 * 12:i1 * 12], _GradView(g), None)
 
     def pose_grad(self, view, step=None, adam_state=None, dL_dview=None, dL_dtwist=None, dL_dqt=None):
         gs_pose_grad(view, self.pose_partials, self.n_partials, step, adam_state, dL_dview, dL_dtwist, dL_dqt)

@@ -56,7 +56,8 @@ def _worker(rank, world, port, data_path, out_dir, mode):
     tc = {v: torch.as_tensor(ref["tc"][v], device=d) for v in range(V)}
     td = {v: torch.as_tensor(ref["td"][v], device=d) for v in range(V)}
     amb = {v: torch.as_tensor(ref["amb"][v], device=d) for v in range(V)}
-    ms = MapStep(P, views, s.cam, tc, td, rank=rank, world=world, device=d)  # default all-reduce
+    ms = MapStep(P, views, s.cam, tc, td, rank=rank, world=world, device=d,  # default all-reduce
+                 ar_chunks=3 if mode == "chunked" else None)
     ms.size()
     if mode == "overflow" and rank == 0:
         for r in ms.lanes:
@@ -105,6 +106,14 @@ def test_two_rank_mapstep_allreduce_equals_oracle(reference, tmp_path):
     out = _run(reference, tmp_path, "plain")
     assert all(o["steps"] == 1 for o in out)
     assert np.array_equal(out[0]["g3"], out[1]["g3"])  # one SUM: every rank holds the same buffer
+
+
+def test_chunked_allreduce_equals_oracle(reference, tmp_path):
+    """ar_chunks = 3: S6 in three Gaussian ranges, each range all-reduced (its
+    four component slices) on the communication stream after every view
+    chained it: the same summed gradient."""
+    out = _run(reference, tmp_path, "chunked")
+    assert np.array_equal(out[0]["g3"], out[1]["g3"])
 
 
 def test_overflow_on_one_rank_repeats_on_every_rank(reference, tmp_path):

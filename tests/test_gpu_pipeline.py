@@ -176,11 +176,16 @@ def test_mapstep_matches_oracle():
     ms = MapStep(P, views, s.cam, tc, td, device=d)  # benched defaults: 8 lanes, fused L1, atomic S6
     assert ms.fused_loss and ms.atomic_gauss and len(ms.lanes) == V
     ms.size()
-    g = ms.step(hooks={"bwd": zero_upstream_hook(ms, amb)})
-    torch.cuda.synchronize()
-    ok, st = grad_check(grads_as_g3(g), ref["g3"], ref["m3"])
-    assert ok.all(), st
-    loss = ms.losses.cpu().numpy()[:, :3].astype(np.float64)
-    assert np.allclose(loss, ref["loss"], rtol=1e-6, atol=0), (loss, ref["loss"])
+    # step 1: stream-ordered stages; step 2 on: each view's per-pixel backward
+    # overlaps its forward tile by tile (MapStep.overlap, previous work order)
+    ms.overlap = True
+    for it in range(2):
+        g = ms.step(hooks={"bwd": zero_upstream_hook(ms, amb)})
+        torch.cuda.synchronize()
+        ok, st = grad_check(grads_as_g3(g), ref["g3"], ref["m3"])
+        assert ok.all(), (it, st)
+        loss = ms.losses.cpu().numpy()[:, :3].astype(np.float64)
+        assert np.allclose(loss, ref["loss"], rtol=1e-6, atol=0), (it, loss, ref["loss"])
+        assert all(r.flag_timeouts() == 0 for r in ms.lanes)
     amb_frac = float(np.mean([ref["amb"][v].mean() for v in range(V)]))
     assert amb_frac < 0.02

@@ -17,6 +17,7 @@ for k, v in (("render_fwd_isolated", ro["render_fwd_isolated"]), ("render_bwd_pi
 ins = ro["render_bwd_pixels_in_step"]
 print("bwd in-step frac %.3f  %.1f us active of %.1f per step; p10/50/90 %s" % (ins["frac"], ins.get("ms_active_per_step", 0) * 1e3, d["ms_per_step"] * 1e3, d.get("ms_per_step_p10_p50_p90")))
 if "single_view" in d: print("single view (config1) MP/s %.1f" % d["single_view"]["value"])
+if "scaling_budget" in d: print("scaling budget " + "  ".join("k=%s share %.3f ms + AR %.3f -> %.2fx" % (k[1:], v["ms_share"], v["ms_allreduce_model"], v["projected_speedup"]) for k, v in d["scaling_budget"].items() if k.startswith("k")))
 if "tracking" in d: print("tracking it/s %.1f" % d["tracking"]["value"])
 if "mapping_ssim" in d: print("mapping+SSIM MP/s %.1f" % d["mapping_ssim"]["value"])
 if "optimizer" in d: print("optimizer %.1f us  %.0f GB/s" % (d["optimizer"]["ms"] * 1e3, d["optimizer"]["achieved_gbs"]))
