@@ -12,7 +12,15 @@ rows = list(csv.reader(out.splitlines()))
 hi = next(i for i, r in enumerate(rows) if "Instructions Executed" in r)
 h, data = rows[hi], rows[hi + 1:]
 ie, st = h.index("Instructions Executed"), h.index("Warp Stall Sampling (All Samples)")
-f = lambda x: float(x) if x not in ("", "-") else 0.0
+
+
+def f(x):
+    try:
+        return float(x)
+    except ValueError:
+        return 0.0
+
+
 agg, stall, src = collections.Counter(), collections.Counter(), {}
 for r in data:
     if len(r) < len(h):
