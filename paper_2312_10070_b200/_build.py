@@ -18,8 +18,11 @@ PKG = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 INCLUDE = os.path.join(ROOT, "include")
-BUILD = os.path.join(PKG, "build")
-LIB = os.path.join(PKG, "libgs.so")
+# GS_DEBUG=1: the debug build (device-side bounds checks, gs_internal.cuh
+# GS_ASSERT) into libgs_debug.so / build_debug/, loaded by _lib when GS_LIB_DEBUG=1
+DEBUG = os.environ.get("GS_DEBUG", "0") == "1"
+BUILD = os.path.join(PKG, "build_debug" if DEBUG else "build")
+LIB = os.path.join(PKG, "libgs_debug.so" if DEBUG else "libgs.so")
 
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NVCC_FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-I", INCLUDE, "-I", CSRC,
@@ -53,7 +56,8 @@ def build(verbose=False, force=False):
         obj = os.path.join(BUILD, src + ".o")
         objs.append(obj)
         if force or _stale(obj, [path] + hdrs):
-            cmd = [nvcc()] + ARCH + NVCC_FLAGS + PER_FILE.get(src, []) + os.environ.get("GS_EXTRA_NVCC", "").split()
+            cmd = ([nvcc()] + ARCH + NVCC_FLAGS + PER_FILE.get(src, []) + (["-DGS_DEBUG"] if DEBUG else []) +
+                   os.environ.get("GS_EXTRA_NVCC", "").split())
             if src.endswith(".cpp"):
                 cmd += ["-x", "cu"]
             cmd += ["-c", path, "-o", obj]

@@ -11,7 +11,8 @@ import os
 import re
 
 PKG = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(PKG, "libgs.so")
+# GS_LIB_DEBUG=1: the debug build with device-side bounds checks (tests only)
+LIB_PATH = os.path.join(PKG, "libgs_debug.so" if os.environ.get("GS_LIB_DEBUG", "0") == "1" else "libgs.so")
 HEADER = os.path.join(os.path.dirname(PKG), "include", "gs.h")
 
 GS_OK = 0

@@ -368,6 +368,7 @@ __global__ void __launch_bounds__(kEmitThreads) k_emit(const int32_t *__restrict
         const int col = local - row * wj;
         const int x = (xyj & 0xffff) + col, y = (xyj >> 16) + row;
         const uint32_t pos = s_base[y * TX + x] + atomicAdd(s_cur + y * W1 + x, 1u);
+        GS_ASSERT(pos < misc[1]);  // inside the P pairs (<= capacity)
         ids[pos] = i - lane + j;
       }
     }
@@ -656,6 +657,7 @@ __device__ __forceinline__ bool tile_sort_one(const TileSortArgs &a, BucketSmem<
         const uint32_t kj = s.key[j], vj = s.val[j];
         rank += (kj < key[k]) || (kj == key[k] && vj < val[k]);
       }
+      GS_ASSERT(int(b0 + rank) < n);
       a.ids[r.x + b0 + rank] = int32_t(val[k]);
     }
   }

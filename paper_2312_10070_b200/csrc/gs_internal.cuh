@@ -8,6 +8,24 @@
 
 #include "gs.h"
 
+// Device-side bounds checks of the debug build (libgs_debug.so, compiled with
+// -DGS_DEBUG by _build.py): a failed check prints its location and traps (the
+// launch fails with a CUDA error).  compute-sanitizer is closed on this pool;
+// these checks on every index that a kernel derives from another kernel's
+// output are the substitute (tests run under the debug build: profiles/r02).
+#ifdef GS_DEBUG
+#include <cstdio>
+#define GS_ASSERT(c)                                                        \
+  do {                                                                      \
+    if (!(c)) {                                                             \
+      printf("GS_ASSERT failed %s:%d: %s\n", __FILE__, __LINE__, #c);     \
+      __trap();                                                             \
+    }                                                                       \
+  } while (0)
+#else
+#define GS_ASSERT(c) ((void)0)
+#endif
+
 namespace gs {
 
 constexpr int kTile = GS_TILE;

@@ -40,6 +40,7 @@ struct BwdArgs {
   float *grad2d;
   uint32_t *tile_done;  // nullable: [T + 1], wait for (and re-arm) the forward's per-tile flag
   int T;                // tiles; tile_done[T] counts timed-out waits
+  int n;                // Gaussians (bounds checks of the debug build)
 };
 
 __device__ __forceinline__ void red_add_v4(float *addr, float x, float y, float z, float w) {
@@ -241,6 +242,7 @@ __global__ void __launch_bounds__(BG::kThreads, kBwdMinBlocks) k_bwd_pixels(BwdA
   if (!a.tile_done) pdl_wait();
   pdl_trigger();
   const int tile = a.tile_order ? __ldg(a.tile_order + blockIdx.x) : int(blockIdx.x);
+  GS_ASSERT(tile >= 0 && tile < a.T);
   if (a.tile_done) {
     // launched programmatically dependent on gs_render_fwd_l1: every forward
     // CTA has started (launch_dependents), so this tile's flag is set in
@@ -265,6 +267,7 @@ __global__ void __launch_bounds__(BG::kThreads, kBwdMinBlocks) k_bwd_pixels(BwdA
   const PixGeom pg = pix_geom<BG>(tx, ty, a.H);
   const double ox = double(tx * kTile), oy = double(ty * kTile);
   const int2 range = a.tile_range[tile];
+  GS_ASSERT(range.x >= 0 && range.x <= range.y);
   const size_t HW = size_t(a.W) * a.H;
   const float2 fx[2] = {make_float2(pg.fpx0, pg.fpx0 + 1.f), make_float2(pg.fpx0 + 2.f, pg.fpx0 + 3.f)};
   BwdPix s;
@@ -281,6 +284,7 @@ __global__ void __launch_bounds__(BG::kThreads, kBwdMinBlocks) k_bwd_pixels(BwdA
         const size_t q = size_t(pg.py) * a.W + pg.px0 + k;
         t[m] = a.T_final[q];
         s.last[k] = a.n_contrib[q];
+        GS_ASSERT(s.last[k] >= 0 && s.last[k] <= range.y - range.x);
         g0[m] = a.dL_dcolor[q];
         g1[m] = a.dL_dcolor[HW + q];
         g2[m] = a.dL_dcolor[2 * HW + q];
@@ -334,6 +338,7 @@ __global__ void __launch_bounds__(BG::kThreads, kBwdMinBlocks) k_bwd_pixels(BwdA
       const int k = beg + i;
       if (k < end) {
         const int g = __ldg(a.sorted_idx + range.x + k);
+        GS_ASSERT(g >= 0 && g < a.n);
         const double2 u = __ldg(a.uv + g);
         const float4 cf = __ldg(a.coef + g);
         const float ul = float(u.x - ox), vl = float(u.y - oy);
@@ -684,7 +689,7 @@ extern "C" int gs_render_bwd(gs_params p, const gs_view *view, gs_camera cam, gs
   BwdArgs b{reinterpret_cast<const double2 *>(pr.uv), reinterpret_cast<const float4 *>(pr.coef),
             reinterpret_cast<const float4 *>(pr.rgbz), reinterpret_cast<const float4 *>(pr.conic_o), sorted_idx,
             reinterpret_cast<const int2 *>(tile_range), tile_order, T_final, n_contrib, dL_dcolor, dL_ddepth, dL_dalpha,
-            cam.width, cam.height, tiles_x(cam), grad2d, tile_done, tiles_x(cam) * tiles_y(cam)};
+            cam.width, cam.height, tiles_x(cam), grad2d, tile_done, tiles_x(cam) * tiles_y(cam), p.n};
   const int T = tiles_x(cam) * tiles_y(cam);
   if (run_pixels) {
     void (*kern)(BwdArgs) = want_params ? (dL_dalpha ? k_bwd_pixels<true, true> : k_bwd_pixels<true, false>)

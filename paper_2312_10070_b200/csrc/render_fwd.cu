@@ -131,11 +131,13 @@ __global__ void __launch_bounds__(FG::kThreads, FWD_MINB) k_render_fwd(FwdArgs a
   // dependent backward of gs_render_fwd_l1(tile_done) may launch
   pdl_begin();
   const int tile = a.tile_order ? __ldg(a.tile_order + blockIdx.x) : int(blockIdx.x);
+  GS_ASSERT(tile >= 0 && tile < int(gridDim.x));
   const int tx = tile % a.TX, ty = tile / a.TX;
   const int w = threadIdx.x >> 5;
   const PixGeom pg = pix_geom<FG>(tx, ty, a.H);
   const double ox = double(tx * kTile), oy = double(ty * kTile);
   const int2 range = a.tile_range[tile];
+  GS_ASSERT(range.x >= 0 && range.x <= range.y);
   float2 fx[kFNP];
 #pragma unroll
   for (int h = 0; h < kFNP; ++h) fx[h] = make_float2(pg.fpx0 + 2.f * h, pg.fpx0 + 2.f * h + 1.f);
@@ -164,6 +166,7 @@ __global__ void __launch_bounds__(FG::kThreads, FWD_MINB) k_render_fwd(FwdArgs a
       const int k = start + i;
       if (k < range.y) {
         const int g = __ldg(a.sorted_idx + k);
+        GS_ASSERT(g >= 0);
         const double2 u = __ldg(a.uv + g);
         const float4 cf = __ldg(a.coef + g);
         const float ul = float(u.x - ox), vl = float(u.y - oy);
