@@ -167,3 +167,65 @@ def test_tracking_graph_converges_and_matches_eager():
         R = pose[:9].reshape(3, 3)
         rot = np.degrees(np.arccos(np.clip((np.trace(R) - 1) / 2, -1, 1)))
         assert rot < 0.2 and np.linalg.norm(pose[9:]) < 0.005, pose
+
+
+def test_tracking_trajectory_replay_against_oracle():
+    """SURVEY §8(d) [2]: the oracle replays the GPU tracking loop in fp64 — per
+    iteration forward, L1 colour + depth loss against the oracle's fp64 GT
+    render (rounded to fp32, fed to both sides), backward to the pose, the
+    twist of the left perturbation and the Adam step with the exp-map
+    retraction — on BJ.configs[2]'s 1200x680 camera and start perturbation with
+    30k Gaussians.  The first iteration's twist gradient must agree under R23;
+    the later trajectory compounds fp32-vs-fp64 differences through Adam's
+    normalised steps, so it is compared loosely (and both must move toward the
+    GT pose)."""
+    from test_gpu_parity import twist_magnitude
+    from paper_2312_10070_b200 import Params
+    from paper_2312_10070_b200.pipeline import TrackingLoop
+    s = inputs.config2(n=30_000)
+    cam = s.cam
+    p64 = oracle.params64(*s.params())
+    gt = s.extra["gt_view"].astype(np.float64)
+    frg = oracle.forward(p64, gt, cam)
+    tc = frg["color"].astype(np.float32)
+    td = frg["depth"].astype(np.float32)
+    start = s.extra["start_view"].astype(np.float32)
+    iters = 8
+    # oracle replay
+    view, st = start.astype(np.float64), np.zeros(13)
+    views, tw0, m0 = [], None, None
+    for it in range(iters):
+        fr = oracle.forward(p64, view, cam)
+        _, gc, gd = oracle.loss(cam, fr["color"], fr["depth"], tc, td)
+        ob = oracle.backward(p64, view, cam, fr["sorted_idx"], fr["tile_range"], gc, gd)
+        tw = oracle.pose_twist(ob["pose"], view)
+        if it == 0:
+            tw0, m0 = tw, twist_magnitude(ob["mpose"], view)
+        view, st = oracle.pose_adam(view, tw, st)
+        views.append(view.copy())
+    # GPU: the tracking loop (fused L1 gradient in the forward, overlapped pose backward, device Adam)
+    d = torch.device("cuda")
+    P = Params.from_numpy(*s.params(), device=d)
+    loop = TrackingLoop(P, cam, torch.as_tensor(tc, device=d), torch.as_tensor(td, device=d),
+                        torch.as_tensor(start, device=d), iters=1)
+    loop.size()
+    loop.run()
+    torch.cuda.synchronize()
+    ok, stt = grad_check(to_np(loop.dtwist), tw0, m0)
+    assert ok.all(), (stt, to_np(loop.dtwist), tw0)
+    assert np.abs(to_np(loop.view).astype(np.float64) - views[0]).max() < 2e-6
+    loop.iters = iters
+    loop.run()
+    torch.cuda.synchronize()
+    assert loop.flag_timeouts() == 0
+    g = to_np(loop.view).astype(np.float64)
+    err = np.abs(g - views[-1]).max()
+    assert err < 1e-4, (err, g, views[-1])
+
+    def dist(v):
+        R = v[:9].reshape(3, 3)
+        return np.degrees(np.arccos(np.clip((np.trace(R) - 1) / 2, -1, 1))), np.linalg.norm(v[9:])
+    r0, t0 = dist(start.astype(np.float64))
+    for v in (g, views[-1]):
+        rr, tt = dist(v)
+        assert rr < r0 and tt < t0
