@@ -83,6 +83,24 @@ def ssim_grad(img, tgt):
     return out / (C * H * W)
 
 
+def ssim_grad_mag(img, tgt):
+    """R23 magnitude scale of ssim_grad: the same chain with every product and
+    inner sum expanded in absolute value,
+    m(q) = sum_p G(p - q) [|dS/dmu_x| + 2 |mu_x| |dS/dsigma_xx| + |mu_y| |dS/dsigma_xy|](p)
+         + 2 |x(q)| sum_p G(p - q) |dS/dsigma_xx(p)| + |y(q)| sum_p G(p - q) |dS/dsigma_xy(p)|,
+    divided by 3HW (G >= 0), so m >= |ssim_grad| elementwise."""
+    img = np.asarray(img, np.float64)
+    tgt = np.asarray(tgt, np.float64)
+    C, H, W = img.shape
+    out = np.zeros_like(img)
+    for c in range(C):
+        x, y = img[c], tgt[c]
+        S, dmx, dsxx, dsxy, mx, my = ssim_terms(x, y)
+        A = np.abs(dmx) + 2 * np.abs(mx) * np.abs(dsxx) + np.abs(my) * np.abs(dsxy)
+        out[c] = blur(A) + 2 * np.abs(x) * blur(np.abs(dsxx)) + np.abs(y) * blur(np.abs(dsxy))
+    return out / (C * H * W)
+
+
 def color_loss(img, tgt, lam=0.2):
     """Eq. 10: (1 - lambda) mean|I^ - I| + lambda (1 - SSIM); returns
     (loss, l1, ssim, dL/dI^)."""

@@ -1,7 +1,7 @@
 """Parity of gs_ssim (Eq. 10's SSIM term, NEXT(2)) with the fp64 oracle on the
 same fp32 images: SSIM within 2e-6 absolute (fp32 local statistics), the
-gradient map within 1e-4 of its largest entry (fp32 two-pass separable
-correlation vs fp64)."""
+gradient map per element under R23 with the oracle's |.|-expanded magnitude
+scale (fp32 two-pass separable correlation vs fp64)."""
 import numpy as np
 import pytest
 import torch
@@ -11,6 +11,11 @@ from paper_2312_10070_b200 import Params, Rasterizer, inputs
 from paper_2312_10070_b200.raster import camera, gs_ssim, lib
 
 pytestmark = pytest.mark.gpu
+
+# R23's absolute slack relative to the magnitude scale: the north star's 1e-6
+# (the kernel's moments of tile-shifted fp32 values keep the cancellation of
+# the squared means out of the variance; the worst element is reported on failure).
+ATOL_REL = 1e-6
 
 
 def _gpu_ssim(x, y, weight=1.0):
@@ -27,14 +32,19 @@ def _gpu_ssim(x, y, weight=1.0):
 
 
 def _check(x, y, w=0.7):
+    """SSIM value within 2e-6 absolute; the gradient map per element under
+    R23: |g - g*| <= 1e-3 |g*| + ATOL_REL m*, m* the |.|-expanded chain of
+    oracle.ssim.ssim_grad_mag (pinned in tests/test_oracle_ssim.py)."""
     x32, y32 = x.astype(np.float32), y.astype(np.float32)
     loss, g = _gpu_ssim(x32, y32, w)
     s = OS.ssim(x32, y32)
     assert abs(loss[3] - s) <= 2e-6
     assert abs(loss[0] - w * (1 - s)) <= 2e-6
     want = -w * OS.ssim_grad(x32, y32)
-    scale = max(np.abs(want).max(), w / x.size)  # at a stationary point (x = y) the floor is w / 3HW
-    assert np.abs(g - want).max() <= 1e-4 * scale
+    m = w * OS.ssim_grad_mag(x32, y32)
+    err = np.abs(g - want)
+    ok = err <= 1e-3 * np.abs(want) + ATOL_REL * m
+    assert ok.all(), (int((~ok).sum()), float((err / np.maximum(m, 1e-300)).max()))
     return s
 
 
@@ -89,4 +99,9 @@ def test_color_loss_with_ssim_matches_eq10():
     assert abs(loss[0] - (lc * Lc + ld * Ld)) <= 2e-6 * max(1.0, abs(loss[0]))
     assert abs(loss[3] - ssim) <= 2e-6
     g = r.dL_dcolor.cpu().numpy()
-    assert np.abs(g - lc * gc).max() <= 1e-4 * np.abs(lc * gc).max()
+    # R23 per element with the magnitude of both terms of Eq. 10's gradient
+    t32 = tc.cpu().numpy()
+    m = lc * ((1 - 0.2) * np.abs(np.sign(x.astype(np.float64) - t32)) / x.size + 0.2 * OS.ssim_grad_mag(x, t32))
+    want = lc * gc
+    ok = np.abs(g - want) <= 1e-3 * np.abs(want) + ATOL_REL * m
+    assert ok.all(), int((~ok).sum())

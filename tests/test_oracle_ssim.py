@@ -95,3 +95,28 @@ def test_color_loss_gradient_finite_differences():
         e[c, i, j] = h
         fd = (S.color_loss(x + e, y)[0] - S.color_loss(x - e, y)[0]) / (2 * h)
         assert abs(fd - g[c, i, j]) <= 1e-6 * max(1e-3, abs(fd))
+
+
+def test_ssim_gradient_magnitude_scale_bounds():
+    """R23 magnitude scale of the SSIM gradient (ssim_grad_mag): an upper
+    bound of |ssim_grad| elementwise and of sum_p |dSSIM_p / dx_q| / 3HW (the
+    per-output-pixel contributions, by central finite differences of the
+    SSIM map, not the oracle's chain), and not merely |ssim_grad|."""
+    x, y = _imgs(11, 9, 10)
+    g = S.ssim_grad(x, y)
+    m = S.ssim_grad_mag(x, y)
+    assert (m >= np.abs(g) * (1 - 1e-12)).all()
+    assert (m > np.abs(g) * 1.01).any()
+    C, H, W = x.shape
+    h = 1e-6
+    rs = np.random.default_rng(3)
+    for _ in range(12):
+        c, i, j = rs.integers(C), rs.integers(H), rs.integers(W)
+        xp, xm = x.copy(), x.copy()
+        xp[c, i, j] += h
+        xm[c, i, j] -= h
+        Sp = S.ssim_terms(xp[c], y[c])[0]
+        Sm = S.ssim_terms(xm[c], y[c])[0]
+        contrib = np.abs((Sp - Sm) / (2 * h)).sum() / (C * H * W)
+        assert contrib <= m[c, i, j] * (1 + 1e-6) + 1e-12
+        assert np.isclose(((Sp - Sm) / (2 * h)).sum() / (C * H * W), g[c, i, j], rtol=1e-5, atol=1e-12)
