@@ -4,17 +4,15 @@
 // Result = every (tile, Gaussian) pair ordered by the composite key
 // (tile asc, fp32 depth asc, Gaussian id asc).  Built tile by tile, with no
 // global sort and no pass whose blocks wait on each other:
-//   1. k_bin_prep: per-tile pair counts as a 2-D difference array of the
+//   1. k_bin_prep: per-tile pair counts from a 2-D difference array of the
 //      tile rects (4 shared-memory updates per visible Gaussian, merged into
 //      one global array per block);
-//   2. (round 1: a single-CTA counts kernel; now inside step 3) the 2-D
-//      prefix -> per-tile counts -> tile starts (scan), P and the capacity
-//      check, computed by every emission CTA for itself;
+//   2. k_tile_counts (one CTA): 2-D prefix -> counts -> tile ranges (scan),
+//      the capacity check, per-tile write cursors and the heaviest-first
+//      launch order;
 //   3. k_emit: every visible Gaussian appends its id to the segment of each
 //      tile of its rect (block-aggregated: shared-memory counts, one global
 //      cursor reservation per (block, tile), warp-balanced pair expansion);
-//      CTA 0 writes the tile ranges, P, the overflow flag and the
-//      heaviest-first tile order;
 //      the order inside a segment is arbitrary at this point;
 //   4. k_tile_sort: one CTA per tile sorts its segment in shared memory in
 //      one pass: a counting sort on the top 11 bits of (depth bits - tile
@@ -72,8 +70,8 @@ static bool make_layout(int32_t n, int64_t capacity, const gs_camera &cam, SortL
   };
   L.diff = take(4 * size_t(L.TX + 1) * (L.TY + 1));
   L.misc = take(64);  // [1] P, [2] overflow, [3] slow-list length, [4] mid-list length
-  L.cursor = take(4 * size_t(L.T));  // per-tile emission cursors, relative to the tile start
   L.zero_end = off;
+  L.cursor = take(4 * size_t(L.T));
   L.slow = take(4 * size_t(L.T));
   L.mid = take(4 * size_t(L.T));
   const size_t cc = size_t(capacity > 0 ? capacity : 1);
@@ -114,26 +112,6 @@ __device__ uint32_t block_excl_scan(uint32_t v, uint32_t *sh /* >= 33 */, uint32
   total = sh[32];
   __syncthreads();
   return r;
-}
-
-// In place: a[0..n) <- exclusive prefix sums (block-wide, blockDim threads,
-// n / blockDim consecutive entries per thread); returns the total.
-__device__ uint32_t block_excl_scan_array(uint32_t *a, int n, uint32_t *sh) {
-  const int per = (n + blockDim.x - 1) / blockDim.x;
-  const int b0 = threadIdx.x * per;
-  uint32_t s = 0;
-  for (int k = 0; k < per; ++k)
-    if (b0 + k < n) s += a[b0 + k];
-  uint32_t total;
-  uint32_t ex = block_excl_scan(s, sh, total);
-  for (int k = 0; k < per; ++k)
-    if (b0 + k < n) {
-      const uint32_t c = a[b0 + k];
-      a[b0 + k] = ex;
-      ex += c;
-    }
-  __syncthreads();
-  return total;
 }
 
 // In-place 2-D inclusive prefix (rows, then columns) of the TX x TY corner of
@@ -218,6 +196,91 @@ __global__ void __launch_bounds__(256) k_bin_prep(const int32_t *__restrict__ ti
 }
 
 // ---------------------------------------------------------------------------
+// Step 2: per-tile pair counts (2-D prefix of the difference array, in shared
+// memory), tile ranges, write cursors, P and the capacity check,
+// heaviest-first tile order.
+
+struct TileArgs {
+  const uint32_t *diff;  // (TY+1) x (TX+1)
+  int TX, TY, T;
+  int64_t capacity;
+  int32_t *tile_range, *tile_order;
+  uint32_t *cursor;
+  int64_t *n_pairs;
+  uint32_t *misc;  // [1] P, [2] overflow
+  gs_counters *cnt;
+};
+
+__global__ void __launch_bounds__(1024) k_tile_counts(TileArgs a) {
+  pdl_begin();
+  extern __shared__ uint32_t s_c[];  // (TY+1) x (TX+1)
+  __shared__ uint32_t sh[33];
+  __shared__ int s_max;
+  __shared__ unsigned s_b[64];
+  const int W1 = a.TX + 1, cells = W1 * (a.TY + 1);
+  const float itx = 1.0f / float(a.TX);
+  for (int i = threadIdx.x; i < cells; i += blockDim.x) s_c[i] = a.diff[i];
+  if (threadIdx.x == 0) s_max = 0;
+  if (threadIdx.x < 64) s_b[threadIdx.x] = 0;
+  __syncthreads();
+  prefix2d(s_c, W1, a.TX, a.TY);  // diff -> per-tile counts
+  // exclusive scan over tiles (tile id = y*TX + x), PER consecutive tiles per thread
+  const int PER = (a.T + blockDim.x - 1) / blockDim.x;
+  uint32_t s = 0;
+  int m = 0;
+  for (int k = 0; k < PER; ++k) {
+    const int t = threadIdx.x * PER + k;
+    if (t < a.T) {
+      const uint32_t c = s_c[t + tile_row(t, itx)];  // (t / TX) W1 + t % TX
+      s += c;
+      m = max(m, int(c));
+    }
+  }
+  uint32_t P;
+  uint32_t ex = block_excl_scan(s, sh, P);
+  const bool over = int64_t(P) > a.capacity;
+  atomicMax(&s_max, m);
+  for (int k = 0; k < PER; ++k) {
+    const int t = threadIdx.x * PER + k;
+    if (t < a.T) {
+      const uint32_t c = s_c[t + tile_row(t, itx)];  // (t / TX) W1 + t % TX
+      reinterpret_cast<int2 *>(a.tile_range)[t] = over ? make_int2(0, 0) : make_int2(int(ex), int(ex + c));
+      a.cursor[t] = ex;
+      ex += c;
+    }
+  }
+  if (threadIdx.x == 0) {
+    a.misc[1] = P;
+    a.misc[2] = over ? 1u : 0u;
+    *a.n_pairs = int64_t(P);
+    if (over && a.cnt) atomicAdd(reinterpret_cast<unsigned long long *>(&a.cnt->n_overflow), 1ull);
+  }
+  if (!a.tile_order) return;
+  __syncthreads();
+  // heaviest first: 64 buckets of maxlen/64 (order inside a bucket unspecified)
+  const uint32_t den = uint32_t(s_max) + 1u;
+  const float iden = 1.0f / float(den);
+  for (int t = threadIdx.x; t < a.T; t += blockDim.x) {
+    const uint32_t c = s_c[t + tile_row(t, itx)];  // (t / TX) W1 + t % TX
+    atomicAdd(&s_b[63 - bucket64(c, den, iden)], 1u);
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    unsigned run = 0;
+    for (int b = 0; b < 64; ++b) {
+      const unsigned c = s_b[b];
+      s_b[b] = run;
+      run += c;
+    }
+  }
+  __syncthreads();
+  for (int t = threadIdx.x; t < a.T; t += blockDim.x) {
+    const uint32_t c = s_c[t + tile_row(t, itx)];  // (t / TX) W1 + t % TX
+    a.tile_order[atomicAdd(&s_b[63 - bucket64(c, den, iden)], 1u)] = t;
+  }
+}
+
+// ---------------------------------------------------------------------------
 // Step 3: pair emission into the tile segments (unordered inside a segment).
 // Per block of kEmitThreads * kEmitPer Gaussians: the block's per-tile counts
 // from a shared-memory 2-D difference array (4 updates per Gaussian), one
@@ -227,89 +290,18 @@ __global__ void __launch_bounds__(256) k_bin_prep(const int32_t *__restrict__ ti
 // the warp's inclusive prefix of tile counts), so lanes stay busy whatever
 // the mix of rect sizes.
 
-// Every CTA first turns the global difference array of k_bin_prep into the
-// per-tile counts and their exclusive scan (the tile starts, P) itself: a
-// 2-D prefix over (TX+1)(TY+1) cells and a scan over T tiles, a few µs of
-// redundant work per CTA in place of a single-CTA kernel on the critical
-// path.  CTA 0 also writes the tile ranges, P, the overflow flag / counter and
-// the heaviest-first tile order.
-struct EmitArgs {
-  const int32_t *tiles_touched;
-  const short4 *rect;
-  int n, TX, TY, T;
-  const uint32_t *diff;  // (TY+1) x (TX+1), from k_bin_prep
-  int64_t capacity;
-  uint32_t *cursor;      // [T] zeroed: pairs reserved so far per tile
-  uint32_t *misc;        // [1] P, [2] overflow
-  int32_t *ids;          // sorted_idx
-  int32_t *tile_range, *tile_order;
-  int64_t *n_pairs;
-  gs_counters *cnt;
-};
-
 template <int kEmitPer>  // Gaussians per thread
-__global__ void __launch_bounds__(kEmitThreads) k_emit(EmitArgs a) {
+__global__ void __launch_bounds__(kEmitThreads) k_emit(const int32_t *__restrict__ tiles_touched,
+                                                       const short4 *__restrict__ rect, int n, int TX, int TY,
+                                                       uint32_t *cursor, const uint32_t *__restrict__ misc,
+                                                       int32_t *ids) {
   pdl_begin();
-  extern __shared__ uint32_t s_e[];  // [(TY+1)(TX+1)] counts / cursors, [T] tile starts -> bases
-  __shared__ uint32_t sh[33];
-  __shared__ unsigned s_b[64];
-  __shared__ uint32_t s_max;
-  const int TX = a.TX, TY = a.TY, T = a.T, n = a.n;
-  const int W1 = TX + 1, cells = W1 * (TY + 1);
+  extern __shared__ uint32_t s_e[];  // [(TY+1)(TX+1)] diff -> counts -> cursors, [T] bases
+  if (misc[2]) return;               // overflow: leave sorted_idx untouched
+  const int W1 = TX + 1, cells = W1 * (TY + 1), T = TX * TY;
   const float itx = 1.0f / float(TX);
   uint32_t *s_cur = s_e, *s_base = s_e + cells;
   const int lane = threadIdx.x & 31;
-  // global per-tile counts -> tile starts, P
-  for (int c = threadIdx.x; c < cells; c += blockDim.x) s_cur[c] = a.diff[c];
-  __syncthreads();
-  prefix2d(s_cur, W1, TX, TY);
-  for (int t = threadIdx.x; t < T; t += blockDim.x) s_base[t] = s_cur[t + tile_row(t, itx)];
-  __syncthreads();
-  const uint32_t P = block_excl_scan_array(s_base, T, sh);
-  const bool over = int64_t(P) > a.capacity;
-  if (blockIdx.x == 0) {
-    auto count_of = [&](int t) { return (t + 1 < T ? s_base[t + 1] : P) - s_base[t]; };
-    for (int t = threadIdx.x; t < T; t += blockDim.x) {
-      const int st = int(s_base[t]);
-      reinterpret_cast<int2 *>(a.tile_range)[t] = over ? make_int2(0, 0) : make_int2(st, st + int(count_of(t)));
-    }
-    if (threadIdx.x == 0) {
-      a.misc[1] = P;
-      a.misc[2] = over ? 1u : 0u;
-      *a.n_pairs = int64_t(P);
-      if (over && a.cnt) atomicAdd(reinterpret_cast<unsigned long long *>(&a.cnt->n_overflow), 1ull);
-    }
-    if (a.tile_order) {  // heaviest first: 64 buckets of maxlen/64 (order inside a bucket unspecified)
-      if (threadIdx.x == 0) s_max = 0;
-      if (threadIdx.x < 64) s_b[threadIdx.x] = 0;
-      __syncthreads();
-      uint32_t m = 0;
-      for (int t = threadIdx.x; t < T; t += blockDim.x) m = max(m, count_of(t));
-      atomicMax(&s_max, m);
-      __syncthreads();
-      const uint32_t den = s_max + 1u;
-      const float iden = 1.0f / float(den);
-      for (int t = threadIdx.x; t < T; t += blockDim.x) atomicAdd(&s_b[63 - bucket64(count_of(t), den, iden)], 1u);
-      __syncthreads();
-      if (threadIdx.x == 0) {
-        unsigned run = 0;
-        for (int b = 0; b < 64; ++b) {
-          const unsigned c = s_b[b];
-          s_b[b] = run;
-          run += c;
-        }
-      }
-      __syncthreads();
-      for (int t = threadIdx.x; t < T; t += blockDim.x)
-        a.tile_order[atomicAdd(&s_b[63 - bucket64(count_of(t), den, iden)], 1u)] = t;
-    }
-  }
-  if (over || n == 0 || a.capacity == 0) return;  // overflow: leave sorted_idx untouched
-  const int32_t *tiles_touched = a.tiles_touched;
-  const short4 *rect = a.rect;
-  uint32_t *cursor = a.cursor;
-  int32_t *ids = a.ids;
-  __syncthreads();
   for (int c = threadIdx.x; c < cells; c += blockDim.x) s_cur[c] = 0;
   __syncthreads();
   short4 r[kEmitPer];
@@ -341,7 +333,7 @@ __global__ void __launch_bounds__(kEmitThreads) k_emit(EmitArgs a) {
     for (int u = 0; u < 4; ++u) {
       const int t = t0 + u * blockDim.x;
       if (t < T) {
-        s_base[t] += base[u];  // tile start + this CTA's reservation
+        s_base[t] = base[u];
         s_cur[t + tile_row(t, itx)] = 0;
       }
     }
@@ -376,7 +368,7 @@ __global__ void __launch_bounds__(kEmitThreads) k_emit(EmitArgs a) {
         const int col = local - row * wj;
         const int x = (xyj & 0xffff) + col, y = (xyj >> 16) + row;
         const uint32_t pos = s_base[y * TX + x] + atomicAdd(s_cur + y * W1 + x, 1u);
-        GS_ASSERT(pos < P);  // inside the P pairs (<= capacity)
+        GS_ASSERT(pos < misc[1]);  // inside the P pairs (<= capacity)
         ids[pos] = i - lane + j;
       }
     }
@@ -861,6 +853,7 @@ extern "C" int gs_bin_sort(gs_proj pr, int32_t n, gs_camera cam, void *ws, size_
   const size_t need = std::max(diff_bytes, emit_bytes);
   if (need > 48 * 1024 && need > smem_set) {
     cudaFuncSetAttribute(k_bin_prep, cudaFuncAttributeMaxDynamicSharedMemorySize, int(diff_bytes));
+    cudaFuncSetAttribute(k_tile_counts, cudaFuncAttributeMaxDynamicSharedMemorySize, int(diff_bytes));
     smem_set = need;
   }
   if (n > 0) {
@@ -868,23 +861,23 @@ extern "C" int gs_bin_sort(gs_proj pr, int32_t n, gs_camera cam, void *ws, size_
     launch_pdl(k_bin_prep, dim3(blocks), dim3(256), diff_bytes, s, pr.tiles_touched, rect, n, L.TX, L.TY, U(L.diff));
   }
   {
+    TileArgs a{U(L.diff), L.TX, L.TY, L.T, capacity, tile_range, tile_order, U(L.cursor), n_pairs, misc, cnt};
+    launch_pdl(k_tile_counts, dim3(1), dim3(1024), diff_bytes, s, a);
+  }
+  if (n > 0 && capacity > 0) {
     // Gaussians per thread: the smallest of 1, 2, 4, 8 that fits the grid in
-    // one wave of 2 CTAs per SM (the per-CTA set-up, two 2-D prefixes, a scan
-    // and one cursor reservation per tile, is then paid about twice per SM);
-    // at least one CTA (CTA 0 writes the ranges even with no pair)
+    // one wave of 2 CTAs per SM (the per-CTA set-up, a 2-D prefix and one
+    // cursor reservation per tile, is then paid about twice per SM)
     int per = 1;
     while (per < 8 && (n + kEmitThreads * per - 1) / (kEmitThreads * per) > 2 * 148) per *= 2;
-    const int eb = std::max(1, (n + kEmitThreads * per - 1) / (kEmitThreads * per));
+    const int eb = (n + kEmitThreads * per - 1) / (kEmitThreads * per);
     auto kern = per == 1 ? k_emit<1> : per == 2 ? k_emit<2> : per == 4 ? k_emit<4> : k_emit<8>;
     if (need > 48 * 1024 && need > smem_set_emit[per]) {
       cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(emit_bytes));
       smem_set_emit[per] = need;
     }
-    EmitArgs e{pr.tiles_touched, rect, n, L.TX, L.TY, L.T, U(L.diff), capacity, U(L.cursor), misc, sorted_idx,
-               tile_range, tile_order, n_pairs, cnt};
-    launch_pdl(kern, dim3(eb), dim3(kEmitThreads), emit_bytes, s, e);
-  }
-  if (n > 0 && capacity > 0) {
+    launch_pdl(kern, dim3(eb), dim3(kEmitThreads), emit_bytes, s, pr.tiles_touched, rect, n, L.TX, L.TY,
+               U(L.cursor), misc, sorted_idx);
     TileSortArgs a{pr.depth, tile_range, tile_order, misc, L.T, sorted_idx, U(L.key_a),
                    U(L.key_b), U(L.val_b), reinterpret_cast<int32_t *>(U(L.slow)),
                    reinterpret_cast<int32_t *>(U(L.mid))};
