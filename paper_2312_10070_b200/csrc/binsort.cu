@@ -884,7 +884,7 @@ extern "C" int gs_bin_sort(gs_proj pr, int32_t n, gs_camera cam, void *ws, size_
     // lists averaging <= 1800 entries: the half-size instance (more CTAs per
     // SM) with the rare longer lists on the mid path; longer averages (e.g.
     // BJ.configs[4]): every list <= kChunk in one pass
-    if (capacity <= int64_t(1800) * L.T) {
+    if (capacity <= int64_t(GS_SORT_LONG_AVG) * L.T) {
       launch_pdl(k_tile_sort<kSmallCap, TS_SMALL_MINB>, dim3(L.T), dim3(kBucketThreads), 0, s, a);
       launch_pdl(k_tile_sort_mid, dim3(std::min(L.T, 4 * kBigBlocks)), dim3(kBucketThreads), 0, s, a);
     } else {

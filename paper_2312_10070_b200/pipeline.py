@@ -18,6 +18,7 @@ from __future__ import annotations
 import numpy as np
 import torch
 
+from . import _lib
 from .raster import (GS_BWD_ATOMIC_ACC, GS_BWD_GAUSS_ONLY, GS_BWD_PIXELS_ONLY, GS_GRAD_PARAMS, GS_GRAD_POSE, Grads, Params, Rasterizer,
                      gs_loss_scales, gs_unpack_rgbd, lib)
 
@@ -391,7 +392,7 @@ def kernels_per_view(cam, loss=True, bwd=True, capacity=0):
     pair capacity averages <= 1800 per tile,] long-list sort = 5 or 6;
     render 1 + backward tile order 1; loss 3; backward 2."""
     T = ((cam.width + 15) // 16) * ((cam.height + 15) // 16)
-    n = 1 + (6 if capacity <= 1800 * T else 5) + 2
+    n = 1 + (6 if capacity <= _lib.GS_SORT_LONG_AVG * T else 5) + 2
     if loss:
         n += 3
     if bwd:
