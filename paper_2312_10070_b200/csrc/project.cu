@@ -111,7 +111,9 @@ __global__ void __launch_bounds__(256, PROJ_MINB) k_project(gs_params p, const g
       if (!(det > 0.0) || !isfinite(det) || !isfinite(u) || !isfinite(v)) {
         nonfinite = true;  // singular Sigma^I
       } else {
-        const double A = c / det, B = -b / det, C = a / det;
+        // conic (an output, not a decision): one reciprocal
+        const double idet = 1.0 / det;
+        const double A = c * idet, B = -b * idet, C = a * idet;
         // tile membership (R8'): tiles meeting the box of the region where
         // o exp(-sigma) >= 1/255, sigma <= tau = ln(o / alpha_min): half-widths
         // sqrt(2 tau a), sqrt(2 tau c); no tile when tau <= 0
@@ -132,9 +134,13 @@ __global__ void __launch_bounds__(256, PROJ_MINB) k_project(gs_params p, const g
           reinterpret_cast<float4 *>(out.conic_o)[i] = make_float4((float)A, (float)B, (float)C, (float)o);
           // H2b Cholesky coefficients, pre-scaled by sqrt(log2(e)/2):
           // a' = sqrt(K A), b' = a' B / A = K B / a', d' = sqrt(K (AC - B^2)/A) = sqrt(K / c)
-          const double ap = sqrt(kHalfLog2e * A);
+          // the compositing coefficients (outputs, not decisions; the forward
+          // and backward both read these same fp32 values) in fp32 from the
+          // fp64 conic: a' = sqrt(K A), b' = K B / a', d' = sqrt(K / c), log2 o
+          const float Kf = float(kHalfLog2e);
+          const float ap = sqrtf(Kf * float(A));
           reinterpret_cast<float4 *>(out.coef)[i] =
-              make_float4((float)ap, (float)(kHalfLog2e * B / ap), (float)sqrt(kHalfLog2e / c), (float)log2(o));
+              make_float4(ap, Kf * float(B) / ap, sqrtf(Kf / float(c)), log2f(float(o)));
           reinterpret_cast<float4 *>(out.rgbz)[i] = make_float4(cf.x, cf.y, cf.z, (float)z);
           out.depth[i] = (float)z;  // RN(p_z): the sort key (R10)
           reinterpret_cast<short4 *>(out.rect)[i] = make_short4((short)x0, (short)y0, (short)x1, (short)y1);
