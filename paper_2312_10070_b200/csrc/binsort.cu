@@ -41,7 +41,10 @@ constexpr int kDigitBits = 9;
 constexpr int kDigits = 1 << kDigitBits;
 constexpr int kBucketBits = 11;
 constexpr int kBuckets = 1 << kBucketBits;  // k_tile_sort counting-sort buckets
-constexpr int kBucketThreads = 256;  // k_tile_sort CTA
+#ifndef TS_THREADS
+#define TS_THREADS 256
+#endif
+constexpr int kBucketThreads = TS_THREADS;  // k_tile_sort CTA
 constexpr int kMaxBucket = 128;     // fuller buckets -> exact two-key sort (k_tile_sort_big)
 constexpr int kEmitThreads = 512;
 constexpr int kBigBlocks = 148;    // k_tile_sort_big grid (grid-stride over the long tiles)

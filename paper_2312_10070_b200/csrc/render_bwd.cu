@@ -52,7 +52,18 @@ constexpr int kBPX = 4;   // pixels per thread in the backward (two fp32x2 pairs
 #ifndef BWD_MINB
 #define BWD_MINB 1
 #endif
-constexpr int kBwdMinBlocks = BWD_MINB;  // resident CTAs per SM the register budget must allow
+constexpr int kBwdMinBlocks = BWD_MINB;
+// at most this many contributing lanes: per-lane vector reds instead of the
+// shared-memory slab (mapping: 4 — more lanes' reds contend in L2 when 8 views
+// run at once, measured 2264 / 2253 / 2166 MP/s for 4 / 2 / 8; pose-only: 16 —
+// 2 reds per lane, one view at a time: 2697 / 2675 / 2656 / 2410 it/s for
+// 16 / 12 / 8 / 32)
+#ifndef BWD_DIRECT
+#define BWD_DIRECT 4
+#endif
+#ifndef BWD_DIRECT_POSE
+#define BWD_DIRECT_POSE 16
+#endif  // resident CTAs per SM the register budget must allow
 using BG = Geo<kBPX, 16>;  // 2 warps, 16x8 pixel strips
 
 __device__ __forceinline__ float rcp_approx(float x) {
@@ -177,7 +188,7 @@ __device__ __forceinline__ void bwd_entry(BwdPix &s, const AlphaPrep &ap, bool a
   } else {
     acc[7] = acc[8] = acc[9] = 0.f;
   }
-  if (__popc(ball) <= 2) {  // few contributing lanes: write directly, skip the reduction
+  if (__popc(ball) <= (kParams ? BWD_DIRECT : BWD_DIRECT_POSE)) {  // few lanes: write directly
     if (any) {
       // grad2d record: (u, v, A, B), (C, p_z, logit, 0), (r, g, b, 0)
       red_add_v4(dst, -acc[0], -acc[1], -0.5f * acc[2], -acc[3]);
