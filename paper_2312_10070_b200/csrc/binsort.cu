@@ -342,32 +342,43 @@ __global__ void __launch_bounds__(kEmitThreads) k_emit(const int32_t *__restrict
     }
   }
   __syncthreads();
+  // the pairs: per warp round of 32 Gaussians (one per lane), the flat list of
+  // their tiles (lane-major, row-major inside a rect) walked 32 slots per step.
+  // The owner of slot p is the r-th Gaussian with tiles, r = (Gaussians started
+  // by the step's first slot) - 1 + (starts inside (p0, p]): a ballot, one OR
+  // reduction of the start bits and a popcount, then a lookup of r's lane
+  // (no dependent chain of shuffles as in a binary search).
+  __shared__ unsigned char s_own[kEmitThreads / 32][32];
+  unsigned char *own = s_own[threadIdx.x >> 5];
 #pragma unroll
   for (int k = 0; k < kEmitPer; ++k) {
     const int i = (blockIdx.x * kEmitPer + k) * kEmitThreads + threadIdx.x;
     const int wdt = r[k].z - r[k].x + 1;
     const int nt = wdt * (r[k].w - r[k].y + 1);  // 0 when not visible
     const int incl = int(warp_incl_scan(uint32_t(nt)));
+    const int excl = incl - nt;
     const int total = __shfl_sync(0xffffffffu, incl, 31);
     const int xy = (int(r[k].x) & 0xffff) | (int(r[k].y) << 16);
-    // row = local / wdt as a multiply-high (exact for local, wdt < 2^16)
-    const uint32_t magic = wdt > 1 ? uint32_t((0x100000000ull + uint64_t(wdt) - 1) / uint64_t(wdt)) : 0u;
+    // row = floor(local / wdt) as floor((local + 0.5) (1 / wdt)) in fp32: exact
+    // (local < 2^22, wdt < 2^12: the quotient is >= 0.5 / wdt from an integer)
+    const float iw = 1.0f / float(max(wdt, 1));
+    const bool has = nt > 0;
+    const unsigned hm = __ballot_sync(0xffffffffu, has);
+    __syncwarp();  // the previous round's lookups are done
+    if (has) own[__popc(hm & lanemask_lt())] = (unsigned char)lane;
+    __syncwarp();
     for (int p0 = 0; p0 < total; p0 += 32) {
       const int p = p0 + lane;
-      // j = number of lanes whose inclusive prefix is <= p
-      int j = 0;
-#pragma unroll
-      for (int b = 16; b > 0; b >>= 1) {
-        const int v = __shfl_sync(0xffffffffu, incl, j + b - 1);
-        j += v <= p ? b : 0;
-      }
-      j = min(j, 31);
-      const int ij = __shfl_sync(0xffffffffu, incl, j), nj = __shfl_sync(0xffffffffu, nt, j);
+      const int c0 = __popc(__ballot_sync(0xffffffffu, has && excl <= p0));
+      const unsigned M = __reduce_or_sync(0xffffffffu, (has && excl > p0 && excl < p0 + 32) ? 1u << (excl - p0) : 0u);
+      const int rank = min(c0 - 1 + __popc(M & (0xffffffffu >> (31 - lane))), 31);
+      const int j = own[rank];
+      const int ej = __shfl_sync(0xffffffffu, excl, j);
       const int wj = __shfl_sync(0xffffffffu, wdt, j), xyj = __shfl_sync(0xffffffffu, xy, j);
-      const uint32_t mj = __shfl_sync(0xffffffffu, magic, j);
+      const float iwj = __shfl_sync(0xffffffffu, iw, j);
       if (p < total) {
-        const int local = p - (ij - nj);
-        const int row = wj == 1 ? local : (nj < 65536 ? int(__umulhi(uint32_t(local), mj)) : local / wj);
+        const int local = p - ej;
+        const int row = int((float(local) + 0.5f) * iwj);
         const int col = local - row * wj;
         const int x = (xyj & 0xffff) + col, y = (xyj >> 16) + row;
         const uint32_t pos = s_base[y * TX + x] + atomicAdd(s_cur + y * W1 + x, 1u);
