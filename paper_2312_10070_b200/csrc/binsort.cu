@@ -39,8 +39,6 @@ constexpr int kSortItems = 16;                          // keys per thread
 constexpr int kChunk = kSortThreads * kSortItems;       // 4096 keys sorted in shared memory at once
 constexpr int kDigitBits = 9;
 constexpr int kDigits = 1 << kDigitBits;
-constexpr int kBucketBits = 11;
-constexpr int kBuckets = 1 << kBucketBits;  // k_tile_sort counting-sort buckets
 #ifndef TS_THREADS
 #define TS_THREADS 256
 #endif
@@ -566,12 +564,19 @@ struct TileSortArgs {
 #define TS_SMALL_MINB 5
 #endif
 constexpr int kSmallCap = TS_SMALL;
+#ifndef TS_BUCKET_BITS
+#define TS_BUCKET_BITS 11
+#endif
+// counting-sort buckets per tile: 2^11 (the kChunk instances: 48 KB of static
+// shared memory), TS_BUCKET_BITS for the small instance
+template <int kCap>
+constexpr int kBucketBitsOf = kCap == kSmallCap ? TS_BUCKET_BITS : 11;
 
 template <int kCap>
 struct BucketSmem {
-  uint32_t key[kCap];
-  uint32_t val[kCap];
-  uint32_t cnt[kBuckets];  // counts, then bucket starts
+  static constexpr int kBuckets = 1 << kBucketBitsOf<kCap>;
+  unsigned long long comp[kCap];  // (depth bits << 32) | id: the exact composite key
+  uint32_t cnt[kBuckets];         // counts, then bucket starts
   uint32_t sh[33];
   uint32_t red[2][kBucketThreads / 32];
   int flag;
@@ -580,6 +585,7 @@ struct BucketSmem {
 template <int kCap>
 __device__ __forceinline__ bool tile_sort_one(const TileSortArgs &a, BucketSmem<kCap> &s, int tile, int2 r, int n) {
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  constexpr int kBucketBits = kBucketBitsOf<kCap>, kBuckets = 1 << kBucketBits;
   for (int b = threadIdx.x; b < kBuckets; b += kBucketThreads) s.cnt[b] = 0u;
   if (threadIdx.x == 0) s.flag = 0;
   constexpr int kIt = kCap / kBucketThreads;
@@ -651,13 +657,13 @@ __device__ __forceinline__ bool tile_sort_one(const TileSortArgs &a, BucketSmem<
     const int i = threadIdx.x + k * kBucketThreads;
     if (i < n) {
       const uint32_t pos = s.cnt[(key[k] - kmin) >> shift] + slot[k];
-      s.key[pos] = key[k];
-      s.val[pos] = val[k];
+      s.comp[pos] = (static_cast<unsigned long long>(key[k]) << 32) | val[k];
     }
   }
   __syncthreads();
   // final position = bucket start + number of bucket entries with a smaller
-  // exact key (depth bits, id): O(bucket size) per entry, no serial chain
+  // exact key (depth bits, id): O(bucket size) per entry, no serial chain;
+  // one 64-bit load and compare per member (the composite key)
 #pragma unroll
   for (int k = 0; k < kIt; ++k) {
     if (k >= items) break;  // block-uniform: only the rounds this list needs
@@ -666,11 +672,9 @@ __device__ __forceinline__ bool tile_sort_one(const TileSortArgs &a, BucketSmem<
       const uint32_t b = (key[k] - kmin) >> shift;
       const uint32_t b0 = s.cnt[b];
       const uint32_t be = b + 1 < kBuckets ? s.cnt[b + 1] : uint32_t(n);
+      const unsigned long long me = (static_cast<unsigned long long>(key[k]) << 32) | val[k];
       uint32_t rank = 0;
-      for (uint32_t j = b0; j < be; ++j) {
-        const uint32_t kj = s.key[j], vj = s.val[j];
-        rank += (kj < key[k]) || (kj == key[k] && vj < val[k]);
-      }
+      for (uint32_t j = b0; j < be; ++j) rank += s.comp[j] < me;
       GS_ASSERT(int(b0 + rank) < n);
       a.ids[r.x + b0 + rank] = int32_t(val[k]);
     }
