@@ -15,9 +15,9 @@
 //      cursor reservation per (block, tile), warp-balanced pair expansion);
 //      the order inside a segment is arbitrary at this point;
 //   4. k_tile_sort: one CTA per tile sorts its segment in shared memory in
-//      one pass: a counting sort on the top 11 bits of (depth bits - tile
-//      minimum), then every entry ranked inside its bucket (~n / 2048
-//      entries) on the exact key (depth bits, id).  Segments longer than 4096
+//      one pass: a counting sort on the top 10 (lists <= 2048) or 11 bits
+//      of (depth bits - tile minimum), then every entry ranked inside its
+//      bucket on the exact key (depth bits, id).  Segments longer than 4096
 //      entries, or with a bucket of more than 128 (a dense cluster of depths
 //      next to a far outlier), are left to k_tile_sort_big: an exact two-key
 //      stable LSD radix sort (id digits, then depth digits; 9-bit digits,
@@ -565,10 +565,10 @@ struct TileSortArgs {
 #endif
 constexpr int kSmallCap = TS_SMALL;
 #ifndef TS_BUCKET_BITS
-#define TS_BUCKET_BITS 11
+#define TS_BUCKET_BITS 10
 #endif
-// counting-sort buckets per tile: 2^11 (the kChunk instances: 48 KB of static
-// shared memory), TS_BUCKET_BITS for the small instance
+// counting-sort buckets per tile: 2^11 for the kChunk instances, TS_BUCKET_BITS
+// (2^10: measured best with bucket-order ranking) for the 2048-entry instance
 template <int kCap>
 constexpr int kBucketBitsOf = kCap == kSmallCap ? TS_BUCKET_BITS : 11;
 
