@@ -180,13 +180,28 @@ __global__ void __launch_bounds__(256) k_bin_prep(const int32_t *__restrict__ ti
   const int W1 = TX + 1, cells = W1 * (TY + 1);
   for (int i = threadIdx.x; i < cells; i += blockDim.x) s_diff[i] = 0;
   __syncthreads();
-  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
-    if (__ldg(tiles_touched + i) > 0) {  // +1 over the rect [x0, x1] x [y0, y1]
-      const short4 r = __ldg(rect + i);
-      atomicAdd(s_diff + r.y * W1 + r.x, 1u);
-      atomicAdd(s_diff + r.y * W1 + r.z + 1, 0xffffffffu);
-      atomicAdd(s_diff + (r.w + 1) * W1 + r.x, 0xffffffffu);
-      atomicAdd(s_diff + (r.w + 1) * W1 + r.z + 1, 1u);
+  // kPrepPer Gaussians per thread and round, every load issued before the
+  // first use (the rect is loaded whatever tiles_touched says: no dependent
+  // second round trip)
+  constexpr int kPrepPer = 8;
+  const int stride = gridDim.x * blockDim.x;
+  for (int i0 = blockIdx.x * blockDim.x + threadIdx.x; i0 < n; i0 += kPrepPer * stride) {
+    int tt[kPrepPer];
+    short4 r[kPrepPer];
+#pragma unroll
+    for (int k = 0; k < kPrepPer; ++k) {
+      const int i = i0 + k * stride;
+      tt[k] = i < n ? __ldg(tiles_touched + i) : 0;
+      r[k] = i < n ? __ldg(rect + i) : make_short4(0, 0, -1, -1);
+    }
+#pragma unroll
+    for (int k = 0; k < kPrepPer; ++k) {
+      if (tt[k] > 0) {  // +1 over the rect [x0, x1] x [y0, y1]
+        atomicAdd(s_diff + r[k].y * W1 + r[k].x, 1u);
+        atomicAdd(s_diff + r[k].y * W1 + r[k].z + 1, 0xffffffffu);
+        atomicAdd(s_diff + (r[k].w + 1) * W1 + r[k].x, 0xffffffffu);
+        atomicAdd(s_diff + (r[k].w + 1) * W1 + r[k].z + 1, 1u);
+      }
     }
   }
   __syncthreads();
@@ -310,7 +325,8 @@ __global__ void __launch_bounds__(kEmitThreads) k_emit(const int32_t *__restrict
   for (int k = 0; k < kEmitPer; ++k) {
     const int i = (blockIdx.x * kEmitPer + k) * kEmitThreads + threadIdx.x;
     const bool vis = i < n && __ldg(tiles_touched + i) > 0;
-    r[k] = vis ? __ldg(rect + i) : make_short4(0, 0, -1, -1);
+    const short4 ri = i < n ? __ldg(rect + i) : make_short4(0, 0, -1, -1);  // not behind the visibility load
+    r[k] = vis ? ri : make_short4(0, 0, -1, -1);
     if (vis) {
       atomicAdd(s_cur + r[k].y * W1 + r[k].x, 1u);
       atomicAdd(s_cur + r[k].y * W1 + r[k].z + 1, 0xffffffffu);
