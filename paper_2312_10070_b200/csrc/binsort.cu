@@ -281,13 +281,11 @@ __global__ void __launch_bounds__(1024) k_tile_counts(TileArgs a) {
     atomicAdd(&s_b[63 - bucket64(c, den, iden)], 1u);
   }
   __syncthreads();
-  if (threadIdx.x == 0) {
-    unsigned run = 0;
-    for (int b = 0; b < 64; ++b) {
-      const unsigned c = s_b[b];
-      s_b[b] = run;
-      run += c;
-    }
+  if (threadIdx.x < 32) {  // exclusive scan of the 64 buckets (2 per lane)
+    const unsigned b0 = s_b[2 * threadIdx.x], b1 = s_b[2 * threadIdx.x + 1];
+    const unsigned ex = warp_incl_scan(b0 + b1) - b0 - b1;
+    s_b[2 * threadIdx.x] = ex;
+    s_b[2 * threadIdx.x + 1] = ex + b0;
   }
   __syncthreads();
   for (int t = threadIdx.x; t < a.T; t += blockDim.x) {
@@ -826,13 +824,11 @@ __global__ void __launch_bounds__(1024) k_order_by_work(const int32_t *__restric
   const float iden = 1.0f / float(den);
   for (int t = threadIdx.x; t < T; t += blockDim.x) atomicAdd(&s_b[63 - bucket64(uint32_t(max(work[t], 0)), den, iden)], 1u);
   __syncthreads();
-  if (threadIdx.x == 0) {
-    unsigned run = 0;
-    for (int b = 0; b < 64; ++b) {
-      const unsigned c = s_b[b];
-      s_b[b] = run;
-      run += c;
-    }
+  if (threadIdx.x < 32) {  // exclusive scan of the 64 buckets (2 per lane)
+    const unsigned b0 = s_b[2 * threadIdx.x], b1 = s_b[2 * threadIdx.x + 1];
+    const unsigned ex = warp_incl_scan(b0 + b1) - b0 - b1;
+    s_b[2 * threadIdx.x] = ex;
+    s_b[2 * threadIdx.x + 1] = ex + b0;
   }
   __syncthreads();
   for (int t = threadIdx.x; t < T; t += blockDim.x)
