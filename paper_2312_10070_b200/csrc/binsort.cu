@@ -578,6 +578,9 @@ struct TileSortArgs {
 #define TS_SMALL_MINB 5
 #endif
 constexpr int kSmallCap = TS_SMALL;
+#ifndef TS_PERSIST
+#define TS_PERSIST 1
+#endif
 #ifndef TS_BUCKET_BITS
 #define TS_BUCKET_BITS 10
 #endif
@@ -722,6 +725,166 @@ __global__ void __launch_bounds__(kBucketThreads, kMinB) k_tile_sort(TileSortArg
     return;
   }
   tile_sort_one<kCap>(a, s, tile, r, n);
+}
+
+// Persistent variant of k_tile_sort<kSmallCap> (TS_PERSIST): CTAs take list
+// positions from an atomic counter (misc[5]) and software-pipeline the global
+// loads: the next position's tile range is loaded while the current tile is
+// counted, its ids are loaded before the current tile's ranking phase (which
+// works in shared memory only), and its depth gather opens the next round.
+// One exposed global round trip per tile instead of four (order, range, ids,
+// depths); same arithmetic and result as tile_sort_one.
+template <int kCap, int kMinB>
+__global__ void __launch_bounds__(kBucketThreads, kMinB) k_tile_sort_p(TileSortArgs a) {
+  pdl_begin();
+  __shared__ BucketSmem<kCap> s;
+  __shared__ int s_q;
+  if (a.misc[2]) return;  // overflow: every range is empty
+  constexpr int kBucketBits = kBucketBitsOf<kCap>, kBuckets = 1 << kBucketBits;
+  constexpr int kIt = kCap / kBucketThreads;
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int2 *ranges = reinterpret_cast<const int2 *>(a.tile_range);
+  if (threadIdx.x == 0) s_q = int(atomicAdd(&a.misc[5], 1u));
+  __syncthreads();
+  int q = s_q, tile = 0;
+  int2 r = make_int2(0, 0);
+  if (q < a.T) {
+    tile = a.order ? __ldg(a.order + q) : q;
+    r = ranges[tile];
+  }
+  uint32_t key[kIt], val[kIt];
+  {
+    const int n = r.y - r.x;
+    if (n > 1 && n <= kCap) {
+#pragma unroll
+      for (int k = 0; k < kIt; ++k) {
+        const int i = threadIdx.x + k * kBucketThreads;
+        if (i < n) val[k] = uint32_t(a.ids[r.x + i]);
+      }
+    }
+  }
+  while (q < a.T) {
+    __syncthreads();  // every thread has read s_q; the shared buffers are free
+    if (threadIdx.x == 0) {
+      s_q = int(atomicAdd(&a.misc[5], 1u));
+      s.flag = 0;
+    }
+    const int n = r.y - r.x;
+    const bool sortable = n > 1 && n <= kCap;
+    if (n > kCap && threadIdx.x == 0) {  // k_tile_sort_mid / _big sort it
+      if (n > kChunk)
+        a.slow[atomicAdd(&a.misc[3], 1u)] = tile;
+      else
+        a.mid[atomicAdd(&a.misc[4], 1u)] = tile;
+    }
+    const int items = sortable ? (n + kBucketThreads - 1) / kBucketThreads : 0;
+    uint32_t kmin = 0xffffffffu, kmax = 0u;
+    for (int b = threadIdx.x; b < kBuckets; b += kBucketThreads) s.cnt[b] = 0u;
+#pragma unroll
+    for (int k = 0; k < kIt; ++k) {  // the depth gather of the ids loaded last round
+      if (k >= items) break;
+      const int i = threadIdx.x + k * kBucketThreads;
+      if (i < n) {
+        key[k] = __float_as_uint(__ldg(a.depth + val[k]));
+        kmin = min(kmin, key[k]);
+        kmax = max(kmax, key[k]);
+      }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      kmin = min(kmin, __shfl_xor_sync(0xffffffffu, kmin, o));
+      kmax = max(kmax, __shfl_xor_sync(0xffffffffu, kmax, o));
+    }
+    if (lane == 0) {
+      s.red[0][w] = kmin;
+      s.red[1][w] = kmax;
+    }
+    __syncthreads();  // s_q, s.red
+    // the next position's tile range (consumed after this tile's scatter)
+    const int qn = s_q;
+    int tile_n = 0;
+    int2 r_n = make_int2(0, 0);
+    if (qn < a.T) {
+      tile_n = a.order ? __ldg(a.order + qn) : qn;
+      r_n = ranges[tile_n];
+    }
+#pragma unroll
+    for (int k = 0; k < (kBucketThreads / 32); ++k) {
+      kmin = min(kmin, s.red[0][k]);
+      kmax = max(kmax, s.red[1][k]);
+    }
+    const int shift = max(0, nbits(kmax - kmin) - kBucketBits);
+    uint16_t slot[kIt];
+#pragma unroll
+    for (int k = 0; k < kIt; ++k) {
+      if (k >= items) break;
+      const int i = threadIdx.x + k * kBucketThreads;
+      if (i < n) slot[k] = uint16_t(atomicAdd(&s.cnt[(key[k] - kmin) >> shift], 1u));
+    }
+    __syncthreads();
+    constexpr int kPer = kBuckets / kBucketThreads;
+    uint32_t c[kPer], sum = 0, big = 0;
+#pragma unroll
+    for (int k = 0; k < kPer; ++k) {
+      c[k] = s.cnt[threadIdx.x * kPer + k];
+      sum += c[k];
+      big |= c[k] > kMaxBucket;
+    }
+    if (big && sortable) s.flag = 1;
+    uint32_t all;
+    uint32_t ex = block_excl_scan(sum, s.sh, all);
+#pragma unroll
+    for (int k = 0; k < kPer; ++k) {
+      s.cnt[threadIdx.x * kPer + k] = ex;
+      ex += c[k];
+    }
+    __syncthreads();
+    const bool ranked = sortable && !s.flag;
+    if (sortable && s.flag && threadIdx.x == 0) a.slow[atomicAdd(&a.misc[3], 1u)] = tile;  // dense buckets
+    if (ranked) {
+#pragma unroll
+      for (int k = 0; k < kIt; ++k) {
+        if (k >= items) break;
+        const int i = threadIdx.x + k * kBucketThreads;
+        if (i < n) {
+          const uint32_t pos = s.cnt[(key[k] - kmin) >> shift] + slot[k];
+          s.comp[pos] = (static_cast<unsigned long long>(key[k]) << 32) | val[k];
+        }
+      }
+    }
+    __syncthreads();
+    // the next tile's ids, in flight during this tile's ranking
+    {
+      const int nn = r_n.y - r_n.x;
+      if (nn > 1 && nn <= kCap) {
+#pragma unroll
+        for (int k = 0; k < kIt; ++k) {
+          const int i = threadIdx.x + k * kBucketThreads;
+          if (i < nn) val[k] = uint32_t(a.ids[r_n.x + i]);
+        }
+      }
+    }
+    if (ranked) {
+#pragma unroll
+      for (int k = 0; k < kIt; ++k) {
+        if (k >= items) break;
+        const int p = threadIdx.x + k * kBucketThreads;
+        if (p < n) {
+          const unsigned long long me = s.comp[p];
+          const uint32_t b = (uint32_t(me >> 32) - kmin) >> shift;
+          const uint32_t b0 = s.cnt[b];
+          const uint32_t be = b + 1 < kBuckets ? s.cnt[b + 1] : uint32_t(n);
+          uint32_t rank = 0;
+          for (uint32_t j = b0; j < be; ++j) rank += s.comp[j] < me;
+          GS_ASSERT(int(b0 + rank) < n);
+          a.ids[r.x + b0 + rank] = int32_t(uint32_t(me));
+        }
+      }
+    }  // (a single entry is in place already)
+    q = qn;
+    tile = tile_n;
+    r = r_n;
+  }
 }
 
 __global__ void __launch_bounds__(kBucketThreads, 4) k_tile_sort_mid(TileSortArgs a) {
@@ -919,7 +1082,12 @@ extern "C" int gs_bin_sort(gs_proj pr, int32_t n, gs_camera cam, void *ws, size_
     // SM) with the rare longer lists on the mid path; longer averages (e.g.
     // BJ.configs[4]): every list <= kChunk in one pass
     if (capacity <= int64_t(GS_SORT_LONG_AVG) * L.T) {
+#if TS_PERSIST
+      launch_pdl(k_tile_sort_p<kSmallCap, TS_SMALL_MINB>, dim3(std::min(L.T, 148 * TS_SMALL_MINB)),
+                 dim3(kBucketThreads), 0, s, a);
+#else
       launch_pdl(k_tile_sort<kSmallCap, TS_SMALL_MINB>, dim3(L.T), dim3(kBucketThreads), 0, s, a);
+#endif
       launch_pdl(k_tile_sort_mid, dim3(std::min(L.T, 4 * kBigBlocks)), dim3(kBucketThreads), 0, s, a);
     } else {
       launch_pdl(k_tile_sort<kChunk, 4>, dim3(L.T), dim3(kBucketThreads), 0, s, a);
