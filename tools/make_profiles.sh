@@ -17,7 +17,7 @@ python tools/launches.py gpurun_out/${tag}_launches.csv > gpurun_out/${tag}_laun
 timeout 300 python tools/profile_track.py 2 > /dev/null 2>&1 && \
   timeout 300 python tools/ncu_times.py "." python tools/profile_track.py 2 > gpurun_out/${tag}_tracking_launches.txt 2>&1
 echo "tracking list rc=$?"
-for k in "k_bwd_pixels" "k_render_fwd" "^k_tile_sort$" "^k_emit$" "^k_project$" "k_bwd_gauss" "^k_bin_prep$" "^k_tile_counts$"; do
+for k in "k_bwd_pixels" "k_render_fwd" "^k_tile_sort_p$" "^k_emit$" "^k_project$" "k_bwd_gauss" "^k_bin_prep$" "^k_tile_counts$"; do
   n=$(echo $k | tr -d '^$')
   SKIP=${SKIP:-2} timeout 400 tools/ncu_full.sh ${tag}_$n "$k" --reps 3; echo "$n rc=$?"
   python tools/ncu_summary.py gpurun_out/prof_${tag}_$n.ncu-rep 30 > gpurun_out/sum_${tag}_$n.txt 2>&1
