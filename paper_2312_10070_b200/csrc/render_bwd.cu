@@ -437,6 +437,10 @@ struct GaussArgs {
 #endif
 template <bool kParams, bool kPose>
 __global__ void __launch_bounds__(kGaussThreads, GAUSS_MINB) k_bwd_gauss(GaussArgs a) {
+  // the view in fp64, once per block (exact)
+  __shared__ double sV[12];
+  if (threadIdx.x < 12) sV[threadIdx.x] = double(__ldg(threadIdx.x < 9 ? &a.view->R[threadIdx.x] : &a.view->t[threadIdx.x - 9]));
+  __syncthreads();
   pdl_begin();
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   float pose[12];
@@ -475,9 +479,9 @@ __global__ void __launch_bounds__(kGaussThreads, GAUSS_MINB) k_bwd_gauss(GaussAr
     // log-scale term of small splats, the tangent projection of dL/dq).
     double R[9], t[3];
 #pragma unroll
-    for (int k = 0; k < 9; ++k) R[k] = __ldg(&a.view->R[k]);
+    for (int k = 0; k < 9; ++k) R[k] = sV[k];
 #pragma unroll
-    for (int k = 0; k < 3; ++k) t[k] = __ldg(&a.view->t[k]);
+    for (int k = 0; k < 3; ++k) t[k] = sV[9 + k];
     const double gu = ga.x, gv = ga.y, gA = ga.z, gB = ga.w, gC = gb.x, gz = gb.y;
     const double mu[3] = {mo.x, mo.y, mo.z};
     double p[3];
@@ -505,10 +509,12 @@ __global__ void __launch_bounds__(kGaussThreads, GAUSS_MINB) k_bwd_gauss(GaussAr
     for (int r = 0; r < 3; ++r)
 #pragma unroll
       for (int c = 0; c < 3; ++c) M[3 * r + c] = Rq[3 * r + c] * s[c];
+    // symmetric products are formed once per unordered pair (round 2)
 #pragma unroll
     for (int r = 0; r < 3; ++r)
 #pragma unroll
-      for (int c = 0; c < 3; ++c) Sig[3 * r + c] = M[3 * r] * M[3 * c] + M[3 * r + 1] * M[3 * c + 1] + M[3 * r + 2] * M[3 * c + 2];
+      for (int c = r; c < 3; ++c)
+        Sig[3 * r + c] = Sig[3 * c + r] = M[3 * r] * M[3 * c] + M[3 * r + 1] * M[3 * c + 1] + M[3 * r + 2] * M[3 * c + 2];
 #pragma unroll
     for (int r = 0; r < 3; ++r)
 #pragma unroll
@@ -516,7 +522,8 @@ __global__ void __launch_bounds__(kGaussThreads, GAUSS_MINB) k_bwd_gauss(GaussAr
 #pragma unroll
     for (int r = 0; r < 3; ++r)
 #pragma unroll
-      for (int c = 0; c < 3; ++c) Sc[3 * r + c] = W[3 * r] * R[3 * c] + W[3 * r + 1] * R[3 * c + 1] + W[3 * r + 2] * R[3 * c + 2];
+      for (int c = r; c < 3; ++c)
+        Sc[3 * r + c] = Sc[3 * c + r] = W[3 * r] * R[3 * c] + W[3 * r + 1] * R[3 * c + 1] + W[3 * r + 2] * R[3 * c + 2];
     const double fx = a.fx, fy = a.fy;
     const double iz = 1.0 / z, iz2 = iz * iz, iz3 = iz2 * iz;
     const double J0 = fx * iz, J2 = -fx * x * iz2, J4 = fy * iz, J5 = -fy * y * iz2;
@@ -526,25 +533,23 @@ __global__ void __launch_bounds__(kGaussThreads, GAUSS_MINB) k_bwd_gauss(GaussAr
     const double t00 = A * gA + B * hB, t01 = A * hB + B * gC, t10 = B * gA + C * hB, t11 = B * hB + C * gC;
     const double S00 = -(t00 * A + t01 * B), S01 = -(t00 * B + t01 * C), S11 = -(t10 * B + t11 * C);
     // Sigma^I = J Sigma_c J^T: G_Sc = J^T G_S2 J, G_J = 2 G_S2 J Sigma_c, J = [[J0, 0, J2], [0, J4, J5]]
-    const double Jm[6] = {J0, 0.0, J2, 0.0, J4, J5};
+    // G_Sc = J^T G_S2 J written out (the structural zeros of J dropped)
     const double GS2[4] = {S00, S01, S01, S11};
+    double GJ0[6], GJ[6];  // G_S2 J
+    GJ0[0] = S00 * J0;
+    GJ0[1] = S01 * J4;
+    GJ0[2] = S00 * J2 + S01 * J5;
+    GJ0[3] = S01 * J0;
+    GJ0[4] = S11 * J4;
+    GJ0[5] = S01 * J2 + S11 * J5;
     double GSc[9];
-#pragma unroll
-    for (int r = 0; r < 3; ++r)
-#pragma unroll
-      for (int c = 0; c < 3; ++c) {
-        double acc = 0.0;
-#pragma unroll
-        for (int u = 0; u < 2; ++u)
-#pragma unroll
-          for (int v = 0; v < 2; ++v) acc += Jm[3 * u + r] * GS2[2 * u + v] * Jm[3 * v + c];
-        GSc[3 * r + c] = acc;
-      }
-    double GJ0[6], GJ[6];
-#pragma unroll
-    for (int r = 0; r < 2; ++r)
-#pragma unroll
-      for (int c = 0; c < 3; ++c) GJ0[3 * r + c] = GS2[2 * r] * Jm[c] + GS2[2 * r + 1] * Jm[3 + c];
+    GSc[0] = J0 * GJ0[0];
+    GSc[1] = GSc[3] = J0 * GJ0[1];
+    GSc[2] = GSc[6] = J0 * GJ0[2];
+    GSc[4] = J4 * GJ0[4];
+    GSc[5] = GSc[7] = J4 * GJ0[5];
+    GSc[8] = J2 * GJ0[2] + J5 * GJ0[5];
+    (void)GS2;
 #pragma unroll
     for (int r = 0; r < 2; ++r)
 #pragma unroll
@@ -569,7 +574,8 @@ __global__ void __launch_bounds__(kGaussThreads, GAUSS_MINB) k_bwd_gauss(GaussAr
 #pragma unroll
       for (int r = 0; r < 3; ++r)
 #pragma unroll
-        for (int c = 0; c < 3; ++c) GSig[3 * r + c] = tmp[3 * r] * R[c] + tmp[3 * r + 1] * R[3 + c] + tmp[3 * r + 2] * R[6 + c];
+        for (int c = r; c < 3; ++c)
+          GSig[3 * r + c] = GSig[3 * c + r] = tmp[3 * r] * R[c] + tmp[3 * r + 1] * R[3 + c] + tmp[3 * r + 2] * R[6 + c];
 #pragma unroll
       for (int r = 0; r < 3; ++r)
 #pragma unroll
@@ -609,11 +615,7 @@ __global__ void __launch_bounds__(kGaussThreads, GAUSS_MINB) k_bwd_gauss(GaussAr
     }
     if (kPose) {
       // dL/dt = dL/dp; dL/dR = dL/dp mu^T + 2 G_Sc R Sigma
-      double RS[9];
-#pragma unroll
-      for (int r = 0; r < 3; ++r)
-#pragma unroll
-        for (int c = 0; c < 3; ++c) RS[3 * r + c] = R[3 * r] * Sig[c] + R[3 * r + 1] * Sig[3 + c] + R[3 * r + 2] * Sig[6 + c];
+      const double *RS = W;  // R Sigma
 #pragma unroll
       for (int r = 0; r < 3; ++r)
 #pragma unroll
