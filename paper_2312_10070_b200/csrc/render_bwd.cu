@@ -54,15 +54,17 @@ constexpr int kBPX = 4;   // pixels per thread in the backward (two fp32x2 pairs
 #endif
 constexpr int kBwdMinBlocks = BWD_MINB;
 // at most this many contributing lanes: per-lane vector reds instead of the
-// shared-memory slab (mapping: 4 — more lanes' reds contend in L2 when 8 views
-// run at once, measured 2264 / 2253 / 2166 MP/s for 4 / 2 / 8; pose-only: 16 —
-// 2 reds per lane, one view at a time: 2697 / 2675 / 2656 / 2410 it/s for
-// 16 / 12 / 8 / 32)
+// shared-memory slab.  Re-tuned at the end of round 2 (the faster binning
+// changed what overlaps the backward): mapping 20 — k_bwd_pixels alone 170 /
+// 168 / 164 / 164 µs and the step 2382 / 2398 / 2421 / 2420 MP/s for 4 / 8 /
+// 20 / 24, all 32 lanes direct 340 µs (every lane's reds on one record
+// contend in L2); pose-only 24 — 2765 / 2776 / 2788 / 2467 it/s for 16 / 20 /
+// 24 / 32)
 #ifndef BWD_DIRECT
-#define BWD_DIRECT 4
+#define BWD_DIRECT 20
 #endif
 #ifndef BWD_DIRECT_POSE
-#define BWD_DIRECT_POSE 16
+#define BWD_DIRECT_POSE 24
 #endif  // resident CTAs per SM the register budget must allow
 using BG = Geo<kBPX, 16>;  // 2 warps, 16x8 pixel strips
 
