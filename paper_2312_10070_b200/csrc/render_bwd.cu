@@ -434,8 +434,10 @@ struct GaussArgs {
   bool atomic_acc;  // GS_BWD_ATOMIC_ACC: g_* += by red.global.add.v4
 };
 
+// S6 CTAs per SM (128 threads): 5 (with the fp64 chain's spills) measured
+// best with FWD_MINB 8, 2446 -> 2458 MP/s; 6 slower
 #ifndef GAUSS_MINB
-#define GAUSS_MINB 4
+#define GAUSS_MINB 5
 #endif
 template <bool kParams, bool kPose>
 __global__ void __launch_bounds__(kGaussThreads, GAUSS_MINB) k_bwd_gauss(GaussArgs a) {

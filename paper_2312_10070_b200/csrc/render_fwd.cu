@@ -48,8 +48,11 @@ struct FwdArgs {
 // Forward geometry: NP fp32x2 pixel pairs per thread on WX-wide warp blocks.
 //   NP = 1, WX = 8:  4 warps on 8x8 blocks, 2 px / thread
 //   NP = 2, WX = 16: 2 warps on 16x8 strips, 4 px / thread
+// resident CTAs per SM the register budget must allow: 8 (64 registers, no
+// spills; 72 without the cap = 7 CTAs): 94.2 -> 91.0 µs alone, 2816 it/s;
+// 9 no change, 10 (48 registers) 106 µs
 #ifndef FWD_MINB
-#define FWD_MINB 1
+#define FWD_MINB 8
 #endif
 constexpr int kFNP = FWD_NP;
 constexpr int kFWX = FWD_WX;
