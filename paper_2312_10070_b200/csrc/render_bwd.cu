@@ -23,7 +23,10 @@ namespace gs {
 
 // grad2d record [n][12]: (u, v, A, B), (C, p_z, logit, 0), (r, g, b, 0)
 constexpr int kG2 = 12;
-constexpr int kGaussThreads = 128;  // k_bwd_gauss block (one pose-partial record per block)
+#ifndef GAUSS_THREADS
+#define GAUSS_THREADS 128
+#endif
+constexpr int kGaussThreads = GAUSS_THREADS;  // k_bwd_gauss block (one pose-partial record per block)
 
 struct BwdArgs {
   const double2 *uv;
