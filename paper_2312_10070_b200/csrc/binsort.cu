@@ -44,7 +44,10 @@ constexpr int kDigits = 1 << kDigitBits;
 #endif
 constexpr int kBucketThreads = TS_THREADS;  // k_tile_sort CTA
 constexpr int kMaxBucket = 128;     // fuller buckets -> exact two-key sort (k_tile_sort_big)
-constexpr int kEmitThreads = 512;
+#ifndef EMIT_THREADS
+#define EMIT_THREADS 512
+#endif
+constexpr int kEmitThreads = EMIT_THREADS;
 // grids: the emission takes the fewest Gaussians per thread (1, 2, 4, 8) that
 // keep it within EMIT_WAVES CTAs per SM, the prep at most PREP_WAVES CTAs per
 // SM (each merges a full difference array with global atomics); measured
