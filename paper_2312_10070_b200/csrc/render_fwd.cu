@@ -61,7 +61,6 @@ using FG = Geo<2 * kFNP, kFWX>;
 // per-thread compositing state of one pixel pair
 struct FwdPix {
   float2 T, c0, c1, c2, D, A;
-  bool live0, live1;
   int last0, last1, ncon0, ncon1, term0, term1;
 };
 
@@ -82,13 +81,11 @@ __device__ __forceinline__ void fwd_blend(FwdPix &s, float2 e, bool q0, bool q1,
   s.D = __ffma2_rn(make_float2(c.w, c.w), wt, s.D);                 // Eq. 6 (camera-frame z, R12)
   s.A = __fadd2_rn(s.A, wt);                                        // R14
   s.T = __ffma2_rn(make_float2(-a0, -a1), s.T, s.T);                // T_{j+1} = T_j (1 - alpha_j)
-  s.live0 = s.T.x >= kTEps;
-  s.live1 = s.T.y >= kTEps;
   if (kStats) {
     s.ncon0 += q0;
     s.ncon1 += q1;
-    s.term0 = (q0 && !s.live0) ? pos : s.term0;  // include, then stop (R11)
-    s.term1 = (q1 && !s.live1) ? pos : s.term1;
+    s.term0 = (q0 && !(s.T.x >= kTEps)) ? pos : s.term0;  // include, then stop (R11)
+    s.term1 = (q1 && !(s.T.y >= kTEps)) ? pos : s.term1;
   }
 }
 
@@ -103,7 +100,7 @@ struct __align__(16) FwdRec {
 __device__ __forceinline__ bool any_live(const FwdPix s[kFNP]) {
   bool l = false;
 #pragma unroll
-  for (int h = 0; h < kFNP; ++h) l |= s[h].live0 || s[h].live1;
+  for (int h = 0; h < kFNP; ++h) l |= s[h].T.x >= kTEps || s[h].T.y >= kTEps;
   return l;
 }
 
@@ -113,8 +110,10 @@ __device__ __forceinline__ void fwd_entry(FwdPix s[kFNP], const float2 e[kFNP], 
   bool p[kFNP][2], any = false;
 #pragma unroll
   for (int h = 0; h < kFNP; ++h) {
-    p[h][0] = s[h].live0 && e[h].x >= kExpMin;
-    p[h][1] = s[h].live1 && e[h].y >= kExpMin;
+    // live (T >= 1e-4, compared where it is used: no flag to keep) and
+    // alpha~ >= 1/255
+    p[h][0] = s[h].T.x >= kTEps && e[h].x >= kExpMin;
+    p[h][1] = s[h].T.y >= kTEps && e[h].y >= kExpMin;
     any |= p[h][0] || p[h][1];
   }
   if (!__any_sync(0xffffffffu, any)) return;
@@ -156,8 +155,6 @@ __global__ void __launch_bounds__(FG::kThreads, FWD_MINB) k_render_fwd(FwdArgs a
     s[h].T = make_float2((pg.row_in && pg.px0 + 2 * h < a.W) ? 1.f : 0.f,
                          (pg.row_in && pg.px0 + 2 * h + 1 < a.W) ? 1.f : 0.f);
     s[h].c0 = s[h].c1 = s[h].c2 = s[h].D = s[h].A = make_float2(0.f, 0.f);
-    s[h].live0 = s[h].T.x >= kTEps;
-    s[h].live1 = s[h].T.y >= kTEps;
     s[h].last0 = s[h].last1 = s[h].ncon0 = s[h].ncon1 = 0;
     s[h].term0 = s[h].term1 = range.y - range.x;  // entries scanned if the pixel never terminates
   }
