@@ -186,19 +186,23 @@ __global__ void __launch_bounds__(FG::kThreads, FWD_MINB) k_render_fwd(FwdArgs a
     unsigned char *list = s_list[w];
     const int nh = warp_hit_list(s_mask, min(kBatch, range.y - start), list, kBatch);
     const int base = start - range.x + 1;
-    for (int k = 0; k < nh; k += 2) {
-      if ((k & 31) == 0 && !__any_sync(0xffffffffu, any_live(s))) break;
-      const int ja = list[k], jb = list[k + 1];
-      const RowTerms ra = row_terms(s_rec[ja].p, s_rec[ja].q, pg.fpy);
-      const RowTerms rb = row_terms(s_rec[jb].p, s_rec[jb].q, pg.fpy);
-      float2 ea[kFNP], eb[kFNP];
+    // the warp's early exit is tested once per 32 hits (outer loop), not per step
+    for (int k0 = 0; k0 < nh; k0 += 32) {
+      if (!__any_sync(0xffffffffu, any_live(s))) break;
+      const int k1 = min(nh, k0 + 32);
+      for (int k = k0; k < k1; k += 2) {
+        const int ja = list[k], jb = list[k + 1];
+        const RowTerms ra = row_terms(s_rec[ja].p, s_rec[ja].q, pg.fpy);
+        const RowTerms rb = row_terms(s_rec[jb].p, s_rec[jb].q, pg.fpy);
+        float2 ea[kFNP], eb[kFNP];
 #pragma unroll
-      for (int h = 0; h < kFNP; ++h) {
-        ea[h] = pair_exponent(ra, fx[h]);
-        eb[h] = pair_exponent(rb, fx[h]);
+        for (int h = 0; h < kFNP; ++h) {
+          ea[h] = pair_exponent(ra, fx[h]);
+          eb[h] = pair_exponent(rb, fx[h]);
+        }
+        fwd_entry<kStats>(s, ea, s_rec[ja], base + ja);
+        fwd_entry<kStats>(s, eb, s_rec[jb], base + jb);
       }
-      fwd_entry<kStats>(s, ea, s_rec[ja], base + ja);
-      fwd_entry<kStats>(s, eb, s_rec[jb], base + jb);
     }
   }
   if (a.tile_work) {
