@@ -55,6 +55,9 @@ constexpr int kEmitThreads = EMIT_THREADS;
 #ifndef EMIT_WAVES
 #define EMIT_WAVES 3
 #endif
+#ifndef TILE_ROWS
+#define TILE_ROWS 1
+#endif
 #ifndef PREP_WAVES
 #define PREP_WAVES 1
 #endif
@@ -304,6 +307,113 @@ __global__ void __launch_bounds__(1024) k_tile_counts(TileArgs a) {
   for (int t = threadIdx.x; t < a.T; t += blockDim.x) {
     const uint32_t c = s_c[t + tile_row(t, itx)];  // (t / TX) W1 + t % TX
     a.tile_order[atomicAdd(&s_b[63 - bucket64(c, den, iden)], 1u)] = t;
+  }
+}
+
+// Step 2 without the heaviest-first order (what the pipelines request): one
+// CTA per tile row y and no communication between CTAs.  With d the
+// difference array (its extra row and column ignored) and, per column x',
+//   col_y(x') = sum_{y'' <= y} d(x', y''),  counts c(x, y) = sum_{x' <= x} col_y(x'),
+//   S(y) = sum_{y' < y} sum_x c(x, y') = sum_x' (TX - x') sum_{y'' < y} (y - y'') d(x', y''),
+//   P = S(TY),
+// every CTA reads the whole array (from L2), derives its row's counts, the
+// pairs before its row and the total, and writes its row's ranges and
+// cursors: the same values as k_tile_counts (integer arithmetic).
+constexpr int kRowThreads = 128, kRowCols = 4;  // TX <= 512
+
+__device__ __forceinline__ int block_incl_scan128(int v, int *sh, int &total) {
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int inc = int(warp_incl_scan(uint32_t(v)));
+  if (lane == 31) sh[w] = inc;
+  __syncthreads();
+  int before = 0;
+  total = 0;
+#pragma unroll
+  for (int k = 0; k < kRowThreads / 32; ++k) {
+    const int t = sh[k];
+    before += k < w ? t : 0;
+    total += t;
+  }
+  __syncthreads();
+  return before + inc;
+}
+
+__device__ __forceinline__ long long block_sum128(long long v, long long *sh) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  if ((threadIdx.x & 31) == 0) sh[threadIdx.x >> 5] = v;
+  __syncthreads();
+  long long t = 0;
+#pragma unroll
+  for (int k = 0; k < kRowThreads / 32; ++k) t += sh[k];
+  __syncthreads();
+  return t;
+}
+
+__global__ void __launch_bounds__(kRowThreads) k_tile_rows(TileArgs a) {
+  pdl_begin();
+  __shared__ int s_sc[kRowThreads / 32];
+  __shared__ long long s_ll[kRowThreads / 32];
+  const int y = blockIdx.x, W1 = a.TX + 1;
+  int col[kRowCols];
+  long long wa = 0, wb = 0;  // sum_x' (TX - x') * (the two row-weighted column sums)
+#pragma unroll
+  for (int k = 0; k < kRowCols; ++k) {
+    const int x = threadIdx.x + k * kRowThreads;
+    int cs = 0;
+    long long A = 0, B = 0;
+    if (x < a.TX) {
+      int yy = 0;
+      for (; yy + 16 <= a.TY; yy += 16) {  // sixteen independent L2 loads in flight
+        int d[16];
+#pragma unroll
+        for (int u = 0; u < 16; ++u) d[u] = int(__ldcg(a.diff + (yy + u) * W1 + x));
+#pragma unroll
+        for (int u = 0; u < 16; ++u) {
+          const int r = yy + u;
+          cs += r <= y ? d[u] : 0;
+          A += r < y ? (long long)(y - r) * d[u] : 0ll;
+          B += (long long)(a.TY - r) * d[u];
+        }
+      }
+      for (; yy < a.TY; ++yy) {
+        const int d = int(__ldcg(a.diff + yy * W1 + x));
+        cs += yy <= y ? d : 0;
+        A += yy < y ? (long long)(y - yy) * d : 0ll;
+        B += (long long)(a.TY - yy) * d;
+      }
+      wa += (long long)(a.TX - x) * A;
+      wb += (long long)(a.TX - x) * B;
+    }
+    col[k] = cs;
+  }
+  const long long S = block_sum128(wa, s_ll), P = block_sum128(wb, s_ll);
+  const bool over = P > a.capacity;
+  // counts c(x, y) = inclusive scan of col over x; the row's starts = their exclusive scan
+  int carry_c = 0, carry_s = 0;
+#pragma unroll
+  for (int k = 0; k < kRowCols; ++k) {
+    if (k * kRowThreads >= a.TX) break;  // block-uniform
+    const int x = threadIdx.x + k * kRowThreads;
+    int tot;
+    const int c = block_incl_scan128(col[k], s_sc, tot) + carry_c;
+    carry_c += tot;
+    const int cv = x < a.TX ? c : 0;
+    int tot2;
+    const int incl = block_incl_scan128(cv, s_sc, tot2) + carry_s;
+    carry_s += tot2;
+    if (x < a.TX) {
+      const int t = y * a.TX + x;
+      const long long start = S + (incl - cv);
+      reinterpret_cast<int2 *>(a.tile_range)[t] = over ? make_int2(0, 0) : make_int2(int(start), int(start + cv));
+      a.cursor[t] = uint32_t(start);
+    }
+  }
+  if (y == 0 && threadIdx.x == 0) {
+    a.misc[1] = uint32_t(P);
+    a.misc[2] = over ? 1u : 0u;
+    *a.n_pairs = P;
+    if (over && a.cnt) atomicAdd(reinterpret_cast<unsigned long long *>(&a.cnt->n_overflow), 1ull);
   }
 }
 
@@ -1072,7 +1182,10 @@ extern "C" int gs_bin_sort(gs_proj pr, int32_t n, gs_camera cam, void *ws, size_
   }
   {
     TileArgs a{U(L.diff), L.TX, L.TY, L.T, capacity, tile_range, tile_order, U(L.cursor), n_pairs, misc, cnt};
-    launch_pdl(k_tile_counts, dim3(1), dim3(1024), diff_bytes, s, a);
+    if (TILE_ROWS && !tile_order && L.TX <= kRowThreads * kRowCols)
+      launch_pdl(k_tile_rows, dim3(L.TY), dim3(kRowThreads), 0, s, a);
+    else
+      launch_pdl(k_tile_counts, dim3(1), dim3(1024), diff_bytes, s, a);
   }
   if (n > 0 && capacity > 0) {
     // Gaussians per thread: the smallest of 1, 2, 4, 8 that fits the grid in

@@ -201,9 +201,10 @@ class MapStep:
 
     # -- the four stages of one view ---------------------------------------------
     def stage_front(self, r, k, v):
-        """S1 + S2: projection and binning."""
+        """S1 + S2: projection and binning (no launch order from the binning
+        when the forward will reuse the lane's work order for this view)."""
         r.project(self.params, self.views[v])
-        r.bin_sort()
+        r.bin_sort(order=self.fwd_order(r, v) is None)
 
     def stage_fwd(self, r, k, v, tgt_ready=None):
         """S3 + S4 once the view's targets are on the device (tgt_ready):

@@ -423,9 +423,12 @@ class Rasterizer:
     def project(self, params: Params, view):
         gs_project(params, view, self.cam, self.proj, self.counters)
 
-    def bin_sort(self):
+    def bin_sort(self, order=True):
+        """S2; order=False: no heaviest-first launch order (a caller that
+        launches the forward in a reused work order; the binning then takes
+        its multi-CTA counts step)."""
         gs_bin_sort(self.proj, self.n, self.cam, self.sort_ws, self.capacity, self.sorted_idx, self.tile_range,
-                    self.n_pairs, self.counters, tile_order=self.tile_order)
+                    self.n_pairs, self.counters, tile_order=self.tile_order if order else None)
 
     def render(self, stats=False):
         gs_render_fwd(self.proj, self.sorted_idx, self.tile_range, self.cam, self.frame, stats,

@@ -98,6 +98,30 @@ def test_sort_parity(case):
     log("sort", case=case["name"], pairs=int(len(idx)))
 
 
+def test_sort_without_order_matches(case):
+    """gs_bin_sort without a launch order (tile_order = NULL, what the
+    pipelines request) takes the one-CTA-per-tile-row counts step: the same
+    tile ranges, sorted ids and pair count as with the order, and the same
+    overflow outcome at a capacity one pair short."""
+    r = case["r"]
+    from paper_2312_10070_b200.raster import gs_bin_sort
+    P = int(r.n_pairs.item())
+    ref_idx, ref_rng = gpu_sort(r)
+    for cap, over in ((r.capacity, False), (P - 1, True)):
+        idx = torch.full_like(r.sorted_idx, -7)
+        rng = torch.empty_like(r.tile_range)
+        n_pairs = torch.zeros_like(r.n_pairs)
+        cnt = torch.zeros_like(r.counters)
+        gs_bin_sort(r.proj, r.n, r.cam, r.sort_ws, cap, idx, rng, n_pairs, cnt, tile_order=None)
+        torch.cuda.synchronize()
+        assert int(n_pairs.item()) == P
+        if over:  # every range empty, the overflow counted (gs_counters.n_overflow)
+            assert not to_np(rng).any() and int(to_np(cnt)[2]) == 1  # gs_counters: (nonfinite, culled, overflow, reserved)
+        else:
+            assert np.array_equal(to_np(rng), ref_rng)
+            assert np.array_equal(to_np(idx)[:P], ref_idx)
+
+
 def test_sort_ties_by_index():
     """R10: exact fp32 depth ties are ordered by Gaussian id (duplicates)."""
     s = inputs.random_scene(31, 400, 64, 48, spread=1.0)
