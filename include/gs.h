@@ -212,7 +212,9 @@ int gs_project(gs_params p, const gs_view *view, gs_camera cam, gs_proj out,
  *   tile_order    (device, nullable) [T] int32 tile ids by descending list
  *                 length (64 buckets; order within a bucket unspecified): a
  *                 scheduling hint for gs_render_fwd / gs_render_bwd, which
- *                 then start the heaviest tiles first (no effect on results)
+ *                 then start the heaviest tiles first (no effect on results);
+ *                 NULL (a caller that reuses an earlier work order) also
+ *                 takes the cheaper multi-CTA counts step
  *   n_pairs       (device) [1] int64 total pair count P
  *   cnt           (device) counters, nullable
  * If P > capacity, n_overflow is incremented, every tile range is set empty
