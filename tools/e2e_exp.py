@@ -46,7 +46,7 @@ orig = ms.params
 print("host, no params  n/a (parameters are copied as whole arrays)")
 host.params = saved
 up = host.upload_targets
-host.upload_targets = lambda v, cam, c, d: None
+host.upload_targets = lambda *args, **kw: False
 print("host, no frames  %.3f ms" % timeit(lambda: ms.step(host=host)))
 host.upload_targets = up
 import time  # noqa: E402
