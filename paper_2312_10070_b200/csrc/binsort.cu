@@ -9,12 +9,14 @@
 //      one global array per block);
 //   2. k_tile_counts (one CTA): 2-D prefix -> counts -> tile ranges (scan),
 //      the capacity check, per-tile write cursors and the heaviest-first
-//      launch order;
+//      launch order; without a requested order, k_tile_rows instead (one CTA
+//      per tile row, closed-form row offsets, no inter-CTA communication);
 //   3. k_emit: every visible Gaussian appends its id to the segment of each
 //      tile of its rect (block-aggregated: shared-memory counts, one global
 //      cursor reservation per (block, tile), warp-balanced pair expansion);
 //      the order inside a segment is arbitrary at this point;
-//   4. k_tile_sort: one CTA per tile sorts its segment in shared memory in
+//   4. k_tile_sort (k_tile_sort_p: persistent CTAs taking tiles from a
+//      counter, loads pipelined across tiles) sorts a segment in shared memory in
 //      one pass: a counting sort on the top 10 (lists <= 2048) or 11 bits
 //      of (depth bits - tile minimum), then every entry ranked inside its
 //      bucket on the exact key (depth bits, id).  Segments longer than 4096
