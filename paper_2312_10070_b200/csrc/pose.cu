@@ -99,26 +99,45 @@ struct PoseArgs {
   float *dL_dview, *dL_dtwist, *dL_dqt;
 };
 
-constexpr int kPoseThreads = 384;  // 32 record lanes x 12 components
+#ifndef POSE_POW
+#define POSE_POW 1
+#endif
+#ifndef POSE_RED
+#define POSE_RED 1
+#endif
+#if POSE_RED
+// 64 record lanes x 12 components; the loads of 8 records are issued before
+// their (in-order) adds, then a fixed pairwise tree over the lanes
+constexpr int kPoseLanes = 64, kPoseThreads = kPoseLanes * 12, kPoseUnroll = 8;
+#else
+constexpr int kPoseLanes = 32, kPoseThreads = kPoseLanes * 12, kPoseUnroll = 1;
+#endif
 
 __global__ void __launch_bounds__(kPoseThreads) k_pose_grad(PoseArgs a) {
   pdl_begin();
   // fixed-order fp64 reduction of the [n][12] partials: thread t owns
-  // component c = t % 12 of the records k = t / 12 (mod 32) -> consecutive
-  // threads read consecutive floats (coalesced); then the 32 lane sums of
-  // each component are added in lane order
-  __shared__ double sh[32][13];
+  // component c = t % 12 of the records k = t / 12 (mod kPoseLanes) ->
+  // consecutive threads read consecutive floats (coalesced); then the lane
+  // sums of each component are added in a fixed order
+  __shared__ double sh[kPoseLanes][13];
   const int c = threadIdx.x % 12, l = threadIdx.x / 12;
   double acc = 0.0;
-  for (int k = l; k < a.n_partials; k += 32) acc += double(a.partials[size_t(k) * 12 + c]);
+  int k = l;
+  for (; k + (kPoseUnroll - 1) * kPoseLanes < a.n_partials; k += kPoseUnroll * kPoseLanes) {
+    float v[kPoseUnroll];
+#pragma unroll
+    for (int u = 0; u < kPoseUnroll; ++u) v[u] = a.partials[size_t(k + u * kPoseLanes) * 12 + c];
+#pragma unroll
+    for (int u = 0; u < kPoseUnroll; ++u) acc += double(v[u]);
+  }
+  for (; k < a.n_partials; k += kPoseLanes) acc += double(a.partials[size_t(k) * 12 + c]);
   sh[l][c] = acc;
   __syncthreads();
-  if (threadIdx.x < 12) {
-    double v = 0.0;
-    for (int k = 0; k < 32; ++k) v += sh[k][threadIdx.x];
-    sh[0][threadIdx.x] = v;  // row 0 is only read by thread 0 after the barrier
+#pragma unroll
+  for (int st = kPoseLanes / 2; st > 0; st >>= 1) {
+    if (l < st) sh[l][c] += sh[l + st][c];
+    __syncthreads();
   }
-  __syncthreads();
   if (threadIdx.x != 0) return;
   double gR[9], gt[3], R[9], t[3];
   for (int c = 0; c < 9; ++c) gR[c] = sh[0][c];
@@ -173,7 +192,22 @@ __global__ void __launch_bounds__(kPoseThreads) k_pose_grad(PoseArgs a) {
     const double stp = a.adam[12] + 1.0;
     a.adam[12] = stp;
     double d[6];
+#if POSE_POW
+    // beta^t by binary exponentiation of the integer step (a few ulp from
+    // pow; the fp64 pow is a long dependent chain on this single thread)
+    double p1 = 1.0, p2 = 1.0, q1 = b1, q2 = b2;
+    for (long long e = (long long)stp; e > 0; e >>= 1) {
+      if (e & 1) {
+        p1 *= q1;
+        p2 *= q2;
+      }
+      q1 *= q1;
+      q2 *= q2;
+    }
+    const double c1 = 1.0 - p1, c2 = 1.0 - p2;  // bias corrections, once
+#else
     const double c1 = 1.0 - pow(b1, stp), c2 = 1.0 - pow(b2, stp);  // bias corrections, once
+#endif
     for (int i = 0; i < 6; ++i) {
       const double m = b1 * a.adam[i] + (1.0 - b1) * tw[i];
       const double v = b2 * a.adam[6 + i] + (1.0 - b2) * tw[i] * tw[i];
