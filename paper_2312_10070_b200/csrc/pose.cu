@@ -4,8 +4,8 @@
 // round trip and can be captured in a CUDA graph.
 //
 // One CTA: the pose partials of gs_render_bwd are summed in fp64 in a fixed
-// order (thread k takes rows k, k+256, ... in order; then a fixed tree), so the
-// result is bit-deterministic.
+// order (lane l takes records l, l+64, ... in order; then a fixed pairwise tree
+// over the lanes), so the result is bit-deterministic.
 #include "gs_internal.cuh"
 
 namespace gs {
