@@ -51,6 +51,9 @@ struct FwdArgs {
 // resident CTAs per SM the register budget must allow: 8 (64 registers, no
 // spills; 72 without the cap = 7 CTAs): 94.2 -> 91.0 µs alone, 2816 it/s;
 // 9 no change, 10 (48 registers) 106 µs
+#ifndef FWD_PDL
+#define FWD_PDL 1
+#endif
 #ifndef FWD_MINB
 #define FWD_MINB 8
 #endif
@@ -345,6 +348,6 @@ extern "C" int gs_render_fwd_l1(gs_proj pr, const int32_t *sorted_idx, const int
             tile_order, cam.width, cam.height, tiles_x(cam), color, depth, alpha, T_final, n_contrib, nullptr,
             tile_work, tgt_color, tgt_depth, scales, dL_dcolor, dL_ddepth, loss_part, tile_done};
   const int T = tiles_x(cam) * tiles_y(cam);
-  launch_pdl(k_render_fwd<false, true>, dim3(T), dim3(FG::kThreads), 0, as_stream(stream), a);
+  launch_pdl_if(FWD_PDL, k_render_fwd<false, true>, dim3(T), dim3(FG::kThreads), 0, as_stream(stream), a);
   return check_launch("gs_render_fwd_l1");
 }
