@@ -122,6 +122,28 @@ def test_sort_without_order_matches(case):
             assert np.array_equal(to_np(idx)[:P], ref_idx)
 
 
+def test_sort_without_order_wide_image():
+    """The no-order counts step on an image wider than 128 tiles (its
+    column chunks and carries): same ranges and ids as the ordered path and
+    as the oracle's binning of the GPU projection."""
+    s = inputs.random_scene(37, 3000, 2600, 40, spread=1.0)
+    r, _, _ = gpu_forward(s)
+    assert (s.cam.width + 15) // 16 > 128
+    from paper_2312_10070_b200.raster import gs_bin_sort
+    P = int(r.n_pairs.item())
+    ref_idx, ref_rng = gpu_sort(r)
+    idx = torch.full_like(r.sorted_idx, -7)
+    rng = torch.empty_like(r.tile_range)
+    n_pairs = torch.zeros_like(r.n_pairs)
+    gs_bin_sort(r.proj, r.n, r.cam, r.sort_ws, r.capacity, idx, rng, n_pairs, None, tile_order=None)
+    torch.cuda.synchronize()
+    assert int(n_pairs.item()) == P
+    assert np.array_equal(to_np(rng), ref_rng) and np.array_equal(to_np(idx)[:P], ref_idx)
+    g = gpu_proj(r)
+    oi, orng = oracle.bin_sort(g["rect"], (g["tiles_touched"] == 0).astype(np.int32), g["depth"], s.cam)
+    assert np.array_equal(to_np(rng), orng) and np.array_equal(to_np(idx)[:P], oi)
+
+
 def test_sort_ties_by_index():
     """R10: exact fp32 depth ties are ordered by Gaussian id (duplicates)."""
     s = inputs.random_scene(31, 400, 64, 48, spread=1.0)
