@@ -120,6 +120,11 @@ __global__ void __launch_bounds__(kPoseThreads) k_pose_grad(PoseArgs a) {
   // consecutive threads read consecutive floats (coalesced); then the lane
   // sums of each component are added in a fixed order
   __shared__ double sh[kPoseLanes][13];
+  // the view and the Adam state are fetched now, in the shadow of the reduction
+  __shared__ float s_view[12];
+  __shared__ double s_adam[13], s_tw[6], s_d[6];
+  if (threadIdx.x < 12) s_view[threadIdx.x] = threadIdx.x < 9 ? a.view->R[threadIdx.x] : a.view->t[threadIdx.x - 9];
+  if (a.has_step && threadIdx.x >= 32 && threadIdx.x < 45) s_adam[threadIdx.x - 32] = a.adam[threadIdx.x - 32];
   const int c = threadIdx.x % 12, l = threadIdx.x / 12;
   double acc = 0.0;
   int k = l;
@@ -138,12 +143,13 @@ __global__ void __launch_bounds__(kPoseThreads) k_pose_grad(PoseArgs a) {
     if (l < st) sh[l][c] += sh[l + st][c];
     __syncthreads();
   }
-  if (threadIdx.x != 0) return;
+  if (threadIdx.x >= 32) return;
+  const int lane = threadIdx.x;
   double gR[9], gt[3], R[9], t[3];
   for (int c = 0; c < 9; ++c) gR[c] = sh[0][c];
   for (int c = 0; c < 3; ++c) gt[c] = sh[0][9 + c];
-  for (int c = 0; c < 9; ++c) R[c] = a.view->R[c];
-  for (int c = 0; c < 3; ++c) t[c] = a.view->t[c];
+  for (int c = 0; c < 9; ++c) R[c] = s_view[c];
+  for (int c = 0; c < 3; ++c) t[c] = s_view[9 + c];
   // twist of the left perturbation T <- exp(xi^) T:
   // dL/dv = dL/dt, dL/dw_k = <dL/dR, [e_k]x R> + dL/dt . (e_k x t)
   double tw[6];
@@ -163,11 +169,10 @@ __global__ void __launch_bounds__(kPoseThreads) k_pose_grad(PoseArgs a) {
     tw[4] = w1;
     tw[5] = w2;
   }
-  if (a.dL_dview)
-    for (int c = 0; c < 12; ++c) a.dL_dview[c] = float(c < 9 ? gR[c] : gt[c - 9]);
-  if (a.dL_dtwist)
-    for (int c = 0; c < 6; ++c) a.dL_dtwist[c] = float(tw[c]);
-  if (a.dL_dqt) {
+  if (lane < 6) s_tw[lane] = tw[lane];
+  if (a.dL_dview && lane < 12) a.dL_dview[lane] = float(lane < 9 ? gR[lane] : gt[lane - 9]);
+  if (a.dL_dtwist && lane < 6) a.dL_dtwist[lane] = float(tw[lane]);
+  if (a.dL_dqt && lane == 0) {
     // (q, t) of T_wc: dL/dq = (I - q q^T) sum_ij dL/dR_ij dR_ij/dq
     double q[4];
     rot_to_quat_d(R, q);
@@ -187,10 +192,11 @@ __global__ void __launch_bounds__(kPoseThreads) k_pose_grad(PoseArgs a) {
     for (int c = 0; c < 3; ++c) a.dL_dqt[4 + c] = float(gt[c]);
   }
   if (a.has_step) {
-    // Adam on the twist, applied as T <- exp(d^) T
+    // Adam on the twist, applied as T <- exp(d^) T; the six
+    // components on six lanes, the retraction on lane 0
+    __syncwarp();
     const double b1 = a.step.beta1, b2 = a.step.beta2, eps = a.step.eps;
-    const double stp = a.adam[12] + 1.0;
-    a.adam[12] = stp;
+    const double stp = s_adam[12] + 1.0;
     double d[6];
 #if POSE_POW
     // beta^t by binary exponentiation of the integer step (a few ulp from
@@ -208,14 +214,20 @@ __global__ void __launch_bounds__(kPoseThreads) k_pose_grad(PoseArgs a) {
 #else
     const double c1 = 1.0 - pow(b1, stp), c2 = 1.0 - pow(b2, stp);  // bias corrections, once
 #endif
-    for (int i = 0; i < 6; ++i) {
-      const double m = b1 * a.adam[i] + (1.0 - b1) * tw[i];
-      const double v = b2 * a.adam[6 + i] + (1.0 - b2) * tw[i] * tw[i];
+    if (lane < 6) {
+      const int i = lane;
+      const double tw_i = s_tw[i];
+      const double m = b1 * s_adam[i] + (1.0 - b1) * tw_i;
+      const double v = b2 * s_adam[6 + i] + (1.0 - b2) * tw_i * tw_i;
       a.adam[i] = m;
       a.adam[6 + i] = v;
       const double mh = m / c1, vh = v / c2;
-      d[i] = -(i < 3 ? double(a.step.lr_trans) : double(a.step.lr_rot)) * mh / (sqrt(vh) + eps);
+      s_d[i] = -(i < 3 ? double(a.step.lr_trans) : double(a.step.lr_rot)) * mh / (sqrt(vh) + eps);
     }
+    __syncwarp();
+    if (lane != 0) return;
+    a.adam[12] = stp;
+    for (int i = 0; i < 6; ++i) d[i] = s_d[i];
     double dR[9], dt[3], R2[9], t2[3];
     se3_exp_d(d, dR, dt);
     for (int r = 0; r < 3; ++r) {
