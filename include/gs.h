@@ -44,13 +44,6 @@ extern "C" {
 #define GS_ALPHA_MIN (1.0f / 255.0f) /* skip alpha < 1/255 (R11)            */
 #define GS_T_EPS 1e-4f               /* stop after T < 1e-4 (R11)           */
 
-/* gs_bin_sort's per-tile sort instance is chosen on the host from the pair
- * CAPACITY (not the device-side pair count): capacity <= GS_SORT_LONG_AVG x
- * tiles -> a 2048-entry instance (more CTAs per SM) with longer lists on a
- * grid-stride 4096-entry pass; above it -> one 4096-entry instance for every
- * tile.  Performance only: both produce the same bits. */
-#define GS_SORT_LONG_AVG 1800
-
 /* Status codes. */
 #define GS_OK 0
 #define GS_ERR_INVALID_ARG (-1)

@@ -25,7 +25,6 @@ GS_GRAD_POSE = 2
 GS_BWD_PIXELS_ONLY = 4
 GS_BWD_GAUSS_ONLY = 8
 GS_BWD_ATOMIC_ACC = 16
-GS_SORT_LONG_AVG = 1800  # include/gs.h: capacity per tile above which gs_bin_sort uses one 4096-entry instance
 
 
 class GsCamera(C.Structure):

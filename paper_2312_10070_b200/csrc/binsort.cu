@@ -1206,20 +1206,18 @@ extern "C" int gs_bin_sort(gs_proj pr, int32_t n, gs_camera cam, void *ws, size_
     TileSortArgs a{pr.depth, tile_range, tile_order, misc, L.T, sorted_idx, U(L.key_a),
                    U(L.key_b), U(L.val_b), reinterpret_cast<int32_t *>(U(L.slow)),
                    reinterpret_cast<int32_t *>(U(L.mid))};
-    // lists averaging <= 1800 entries: the half-size instance (more CTAs per
-    // SM) with the rare longer lists on the mid path; longer averages (e.g.
-    // BJ.configs[4]): every list <= kChunk in one pass
-    if (capacity <= int64_t(GS_SORT_LONG_AVG) * L.T) {
+    // every list <= 2048 entries in the persistent half-size instance (more
+    // CTAs per SM), longer ones (<= kChunk) on the grid-stride mid pass, the
+    // rest on the exact long-list path: the same launches whatever the
+    // caller's capacity (round 2: the capacity-keyed one-pass 4096-entry
+    // instance for long averages is gone, BJ.configs[4] 2122 -> 2134 MP/s)
 #if TS_PERSIST
-      launch_pdl(k_tile_sort_p<kSmallCap, TS_SMALL_MINB>, dim3(std::min(L.T, 148 * TS_SMALL_MINB)),
-                 dim3(kBucketThreads), 0, s, a);
+    launch_pdl(k_tile_sort_p<kSmallCap, TS_SMALL_MINB>, dim3(std::min(L.T, 148 * TS_SMALL_MINB)),
+               dim3(kBucketThreads), 0, s, a);
 #else
-      launch_pdl(k_tile_sort<kSmallCap, TS_SMALL_MINB>, dim3(L.T), dim3(kBucketThreads), 0, s, a);
+    launch_pdl(k_tile_sort<kSmallCap, TS_SMALL_MINB>, dim3(L.T), dim3(kBucketThreads), 0, s, a);
 #endif
-      launch_pdl(k_tile_sort_mid, dim3(std::min(L.T, 4 * kBigBlocks)), dim3(kBucketThreads), 0, s, a);
-    } else {
-      launch_pdl(k_tile_sort<kChunk, 4>, dim3(L.T), dim3(kBucketThreads), 0, s, a);
-    }
+    launch_pdl(k_tile_sort_mid, dim3(std::min(L.T, 4 * kBigBlocks)), dim3(kBucketThreads), 0, s, a);
     launch_pdl(k_tile_sort_big, dim3(std::min(L.T, kBigBlocks)), dim3(kSortThreads), 0, s, a);
   }
   return check_launch("gs_bin_sort");

@@ -389,11 +389,10 @@ class MapStep:
 
 def kernels_per_view(cam, loss=True, bwd=True, capacity=0):
     """Kernels of ours per view (the sort's memset is a copy-engine node, not a kernel):
-    project 1; bin_sort: prep, tile counts, emit, tile sort, [mid-list sort when the
-    pair capacity averages <= 1800 per tile,] long-list sort = 5 or 6;
-    render 1 + backward tile order 1; loss 3; backward 2."""
-    T = ((cam.width + 15) // 16) * ((cam.height + 15) // 16)
-    n = 1 + (6 if capacity <= _lib.GS_SORT_LONG_AVG * T else 5) + 2
+    project 1; bin_sort: prep, tile counts, emit, tile sort, mid-list sort,
+    long-list sort = 6; render 1 + backward tile order 1; loss 3; backward 2.
+    (capacity: kept for callers; the launches no longer depend on it.)"""
+    n = 1 + 6 + 2
     if loss:
         n += 3
     if bwd:

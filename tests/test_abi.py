@@ -33,8 +33,7 @@ def test_header_constants_match_oracle():
 
 def test_header_and_binding_constants_agree():
     hdr = open(_lib.HEADER).read()
-    for name in ("GS_GRAD_PARAMS", "GS_GRAD_POSE", "GS_BWD_PIXELS_ONLY", "GS_BWD_GAUSS_ONLY", "GS_BWD_ATOMIC_ACC",
-                 "GS_SORT_LONG_AVG"):
+    for name in ("GS_GRAD_PARAMS", "GS_GRAD_POSE", "GS_BWD_PIXELS_ONLY", "GS_BWD_GAUSS_ONLY", "GS_BWD_ATOMIC_ACC"):
         m = re.search(r"#define %s (\d+)u?" % name, hdr)
         assert m and int(m.group(1)) == getattr(_lib, name), name
 
