@@ -1,6 +1,8 @@
 """Experiment (not a bench number): effective cost of each stage inside the
 pipelined mapping step, measured by dropping it from the step (stale buffers
-stand in for its outputs).  BJ.configs[3], 8 views, 4 lanes."""
+stand in for its outputs; the parameters do not change between steps, so
+those are the same values).  BJ.configs[3], 8 views, 8 lanes, the bench's
+configuration (fused L1 loss, forward -> backward tile overlap)."""
 import os
 import sys
 
@@ -14,8 +16,8 @@ import bench  # noqa: E402
 dev = torch.device("cuda")
 s, P, views, tc, td = bench.make_workload(3, dev, 0, 1)
 lanes = int(sys.argv[1]) if len(sys.argv) > 1 else 8
-sched = sys.argv[2] if len(sys.argv) > 2 else "lanes"
-ms = MapStep(P, views, s.cam, tc, td, device=dev, lanes=lanes, schedule=sched)
+ms = MapStep(P, views, s.cam, tc, td, device=dev, lanes=lanes)
+ms.overlap = True
 ms.size()
 
 
@@ -27,14 +29,9 @@ def make(skip):
     elif "sort" in skip:
         hooks["front"] = lambda r, k, v: r.project(ms.params, ms.views[v])
     elif "project" in skip:
-        hooks["front"] = lambda r, k, v: r.bin_sort()
-
-    def fwd(r, k, v, tgt=None):
-        if "fwd" not in skip:
-            r.render()
-        if "loss" not in skip:
-            r.compute_loss(ms.tgt_color[v], ms.tgt_depth[v], None, ms.lc, ms.ld)
-    hooks["fwd"] = fwd
+        hooks["front"] = lambda r, k, v: r.bin_sort(order=ms.fwd_order(r, v) is None)
+    if "fwd" in skip:
+        hooks["fwd"] = noop
     if "bwd" in skip:
         hooks["bwd"] = noop
     if "gauss" in skip:
@@ -56,8 +53,8 @@ def timeit(hooks, n=20):
 
 
 base = timeit(make(set()))
-print(f"{sched} lanes {lanes}: full step {base:.3f} ms ({base / 8 * 1e3:.0f} us/view)")
-for sk in (["sort"], ["project", "sort"], ["loss"], ["gauss"], ["fwd"], ["bwd"], ["fwd", "bwd"],
-           ["project", "sort", "loss", "gauss"]):
+print(f"lanes {lanes}: full step {base:.3f} ms ({base / 8 * 1e3:.0f} us/view)")
+for sk in (["sort"], ["project"], ["project", "sort"], ["gauss"], ["fwd"], ["bwd"], ["fwd", "bwd"],
+           ["project", "sort", "gauss"]):
     t = timeit(make(set(sk)))
     print(f"  without {'+'.join(sk):28s} {t:.3f} ms  (stage costs {(base - t) / 8 * 1e3:6.1f} us/view)")
