@@ -703,6 +703,9 @@ struct TileSortArgs {
 #define TS_SMALL_MINB 5
 #endif
 constexpr int kSmallCap = TS_SMALL;
+#ifndef TS_GRID_PER_SM
+#define TS_GRID_PER_SM TS_SMALL_MINB  // persistent tile-sort CTAs per SM
+#endif
 #ifndef TS_PERSIST
 #define TS_PERSIST 1
 #endif
@@ -1212,7 +1215,7 @@ extern "C" int gs_bin_sort(gs_proj pr, int32_t n, gs_camera cam, void *ws, size_
     // caller's capacity (round 2: the capacity-keyed one-pass 4096-entry
     // instance for long averages is gone, BJ.configs[4] 2122 -> 2134 MP/s)
 #if TS_PERSIST
-    launch_pdl(k_tile_sort_p<kSmallCap, TS_SMALL_MINB>, dim3(std::min(L.T, 148 * TS_SMALL_MINB)),
+    launch_pdl(k_tile_sort_p<kSmallCap, TS_SMALL_MINB>, dim3(std::min(L.T, 148 * TS_GRID_PER_SM)),
                dim3(kBucketThreads), 0, s, a);
 #else
     launch_pdl(k_tile_sort<kSmallCap, TS_SMALL_MINB>, dim3(L.T), dim3(kBucketThreads), 0, s, a);
