@@ -48,6 +48,7 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-tracking", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-graph", action="store_true", help="time the mapping step launched eagerly, not replayed")
     ap.add_argument("--profile", action="store_true", help="short run for ncu (no clocks/cpu/e2e/tracking)")
     ap.add_argument("--lanes", type=int, default=8, help="per-view buffer sets (and lane streams)")
     ap.add_argument("--no-overlap", action="store_true",
@@ -290,10 +291,19 @@ def bench_ours(a):
     hooks = {"fwd": timed_fwd, "bwd": timed_bwd}
     ms.overlap = not a.no_overlap
 
-    # the timed steps run the product path as is (MapStep.step(), no hooks)
+    # the timed steps run the product path as is: MapStep.step() captured once
+    # as a CUDA graph and replayed (MapStep.capture / replay; one process),
+    # or launched eagerly (--no-graph, and every multi-process run)
     for _ in range(max(a.warmup, 3)):
         ms.step()
     torch.cuda.synchronize()
+    use_graph = world == 1 and not a.no_graph
+    if use_graph:
+        ms.capture()
+        for _ in range(2):
+            ms.replay()
+        torch.cuda.synchronize()
+    run_step = ms.replay if use_graph else ms.step
     if world > 1:
         dist.barrier()
     step_ms = []
@@ -305,7 +315,7 @@ def bench_ours(a):
             flush.zero_()  # L2 flush between timed steps (outside the step events)
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             e0.record(stream)
-            ms.step()
+            run_step()
             e1.record(stream)
             step_ms.append((e0, e1))
         torch.cuda.synchronize()
@@ -395,6 +405,8 @@ def bench_ours(a):
                    "parallelism": (f"view-sharded dp{world}, {a.backend.upper()} all-reduce of gradients"
                                    if world > 1 else "1 GPU"),
                    "l2": "256 MiB buffer written between timed steps (outside the step events)",
+                   "launch": ("MapStep.capture(): the step as one CUDA graph, replayed" if use_graph else
+                              "MapStep.step() launched eagerly"),
                    "pairs_per_view": int(np.mean([x["pairs"] for x in stats_views])),
                    "scanned_per_px": sum(x["scanned"] for x in stats_views) / (len(stats_views) * W * H),
                    "contrib_per_px": sum(x["contrib"] for x in stats_views) / (len(stats_views) * W * H)},

@@ -154,6 +154,7 @@ class MapStep:
         # BJ.configs[3] (2235 vs 2250 MP/s at 8 views; 0.446 vs 0.448 ms for one view)
         self.overlap = False
         self._pending = {}
+        self.graph = None
 
     def fwd_order(self, r, v):
         """Tile launch order for view v's forward on lane r (None: gs_bin_sort's)."""
@@ -198,6 +199,35 @@ class MapStep:
             self.size(slack)
             g = self.step(hooks, host)
         return g
+
+    def capture(self):
+        """The device-resident step (no host inputs, no hooks) captured once as
+        one CUDA graph over the lane streams; replay() then runs it with a few
+        µs of host work instead of ~1.5 ms of Python launches per step
+        (tools/graph_exp.py).  Single process only (the graph holds no
+        collective).  The captured step uses the lanes' state at capture time
+        (work orders, overlap path): capture after a few warm-up steps, and
+        again after re-sizing."""
+        if self.allreduce is not None:
+            raise ValueError("MapStep.capture: world > 1 (the all-reduce is not captured)")
+        main = torch.cuda.current_stream()
+        side = torch.cuda.Stream(device=self.params.mean_opa.device)
+        side.wait_stream(main)
+        with torch.cuda.stream(side):
+            self.step()  # warm-up on a side stream (lazy buffers)
+        main.wait_stream(side)
+        torch.cuda.synchronize()
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g):
+            self.step()
+        torch.cuda.synchronize()
+        self.graph = g
+        return g
+
+    def replay(self):
+        """One step by graph replay (capture() first); returns the gradients."""
+        self.graph.replay()
+        return self.grads
 
     # -- the four stages of one view ---------------------------------------------
     def stage_front(self, r, k, v):

@@ -189,3 +189,32 @@ def test_mapstep_matches_oracle():
         assert all(r.flag_timeouts() == 0 for r in ms.lanes)
     amb_frac = float(np.mean([ref["amb"][v].mean() for v in range(V)]))
     assert amb_frac < 0.02
+
+
+def test_mapstep_graph_replay_equals_eager():
+    """MapStep.capture / replay (the bench's timed path): the same summed
+    gradient and per-view losses as the eager step (atomic accumulation:
+    up to float rounding of the sum order)."""
+    from gpu_helpers import oracle_mapping_reference, small_submap
+    s = small_submap(seed=5)
+    d = torch.device("cuda")
+    P = Params.from_numpy(*s.params(), device=d)
+    views = torch.as_tensor(s.views, device=d)
+    ref = oracle_mapping_reference(s)
+    V = s.views.shape[0]
+    tc = {v: torch.as_tensor(ref["tc"][v], device=d) for v in range(V)}
+    td = {v: torch.as_tensor(ref["td"][v], device=d) for v in range(V)}
+    ms = MapStep(P, views, s.cam, tc, td, device=d)
+    ms.overlap = True
+    ms.size()
+    for _ in range(3):
+        ms.step()
+    eager = ms.step().buf.clone()
+    eager_loss = ms.losses.clone()
+    ms.capture()
+    for _ in range(2):
+        got = ms.replay().buf
+    torch.cuda.synchronize()
+    scale = eager.abs().max().item()
+    assert torch.allclose(got, eager, rtol=1e-5, atol=1e-6 * scale)
+    assert torch.allclose(ms.losses, eager_loss, rtol=1e-6, atol=0)

@@ -15,6 +15,7 @@ dev = torch.device("cuda")
 s, P, views, tc, td = bench.make_workload(3, dev, 0, 1)
 lanes = int(sys.argv[1]) if len(sys.argv) > 1 else 8
 ms = MapStep(P, views, s.cam, tc, td, device=dev, lanes=lanes)
+ms.overlap = True  # as the bench
 ms.size()
 for _ in range(5):
     ms.step()
