@@ -561,11 +561,16 @@ def scaling_budget(a, s, P, views, tc, td, device, ms_1gpu):
         for _ in range(3):
             ms.step()
         torch.cuda.synchronize()
+        run_step = ms.step
+        if not a.no_graph:  # launched as T(1) is: captured once (the all-reduce is modelled, not run)
+            ms.allreduce = None
+            ms.capture()
+            run_step = ms.replay
         t = []
         for _ in range(max(10, a.steps // 2)):
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             e0.record()
-            ms.step()
+            run_step()
             e1.record()
             t.append((e0, e1))
         torch.cuda.synchronize()
@@ -590,17 +595,22 @@ def bench_single_view(device, a):
     tc = {0: torch.as_tensor(s.extra["tgt_color"][0], device=device)}
     td = {0: torch.as_tensor(s.extra["tgt_depth"][0], device=device)}
     ms = MapStep(P, views, s.cam, tc, td, device=device, lanes=1)
+    ms.overlap = not a.no_overlap
     ms.size()
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=device)
     for _ in range(5):
         ms.step()
     torch.cuda.synchronize()
+    run_step = ms.step
+    if not a.no_graph:  # as the main line: the step captured once, replayed
+        ms.capture()
+        run_step = ms.replay
     t = []
     for _ in range(max(a.steps, 20)):
         flush.zero_()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record()
-        ms.step()
+        run_step()
         e1.record()
         t.append((e0, e1))
     torch.cuda.synchronize()
@@ -610,7 +620,8 @@ def bench_single_view(device, a):
     return {"metric": "fwd+bwd megapixels/s, one 640x480 view of 100k Gaussians (BJ.configs[1])",
             "value": mp / (med * 1e-3), "unit": UNIT, "ms_per_step_median": med,
             "ms_per_step_p10_p90": [float(x) for x in np.percentile(ms_step, [10, 90])],
-            "gpu_launches_per_step": ms.launches_per_step(), "l2": "256 MiB buffer written between steps"}
+            "gpu_launches_per_step": ms.launches_per_step(), "l2": "256 MiB buffer written between steps",
+            "launch": "CUDA graph replay" if not a.no_graph else "eager", "overlap": ms.overlap}
 
 
 def bench_tracking(device, masked=None):
