@@ -10,7 +10,7 @@ P = Params.from_numpy(*s.params(), device=d)
 gt = torch.as_tensor(s.extra["gt_view"], device=d)
 r = Rasterizer(s.n, s.cam, device=d); r.size_for(P, gt); r.forward(P, gt)
 tc, td = r.frame.color.clone(), r.frame.depth.clone(); del r
-for oe in (1, 4, 8, 16, 32):
+for oe in ([int(x) for x in sys.argv[1:]] or (1, 4, 8, 16, 32)):
     loop = TrackingLoop(P, s.cam, tc, td, torch.as_tensor(s.extra["start_view"], device=d), iters=100)
     loop.order_every = oe
     loop.size(); loop.capture()
