@@ -150,9 +150,11 @@ class MapStep:
         # per-pixel backward starts tile by tile as its forward finishes
         # (per-tile flags + programmatic dependent launch, as in tracking), both
         # in the previous step's work order; the order refresh and the loss
-        # reduction follow.  Off by default: measured no faster for
-        # BJ.configs[3] (2235 vs 2250 MP/s at 8 views; 0.446 vs 0.448 ms for one view)
-        self.overlap = False
+        # reduction follow.  On by default since the end of round 2 (graph-
+        # replayed step): 2534 -> 2537 MP/s at 8 views, the one-view share
+        # 0.393 -> 0.388 ms, the 2-view share 0.708 -> 0.683 ms, single view
+        # 1513 -> 1519 MP/s (first measured no faster, round 2 start)
+        self.overlap = True
         self._pending = {}
         self.graph = None
 
