@@ -55,7 +55,7 @@ constexpr int kBPX = 4;   // pixels per thread in the backward (two fp32x2 pairs
 #ifndef BWD_MINB
 #define BWD_MINB 1
 #endif
-constexpr int kBwdMinBlocks = BWD_MINB;
+constexpr int kBwdMinBlocks = BWD_MINB;  // resident CTAs per SM the register budget must allow
 // at most this many contributing lanes: per-lane vector reds instead of the
 // shared-memory slab.  Re-tuned at the end of round 2 (the faster binning
 // changed what overlaps the backward): mapping 20 — k_bwd_pixels alone 170 /
@@ -68,7 +68,7 @@ constexpr int kBwdMinBlocks = BWD_MINB;
 #endif
 #ifndef BWD_DIRECT_POSE
 #define BWD_DIRECT_POSE 24
-#endif  // resident CTAs per SM the register budget must allow
+#endif
 using BG = Geo<kBPX, 16>;  // 2 warps, 16x8 pixel strips
 
 __device__ __forceinline__ float rcp_approx(float x) {
