@@ -552,7 +552,9 @@ def scaling_budget(a, s, P, views, tc, td, device, ms_1gpu):
     nbytes = 4 * s.n * 16
     out = {"model": "projected_speedup = T(1) / (measured rank-0 share + modelled all-reduce); busbw 725 GB/s "
                     "(measured 8-rank all-reduce on this pool); not a multi-GPU measurement",
+           "l2": "256 MiB buffer written between timed shares (as for T(1))",
            "allreduce_bytes": nbytes}
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=device)
     for k in (2, 4, 8):
         ms = MapStep(P, views, s.cam, tc, td, rank=0, world=k, allreduce=lambda buf: None, device=device,
                      lanes=a.lanes)
@@ -568,6 +570,7 @@ def scaling_budget(a, s, P, views, tc, td, device, ms_1gpu):
             run_step = ms.replay
         t = []
         for _ in range(max(10, a.steps // 2)):
+            flush.zero_()  # L2 flushed between timed shares, as for T(1) (outside the events)
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             e0.record()
             run_step()
