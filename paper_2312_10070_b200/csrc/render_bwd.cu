@@ -63,6 +63,9 @@ constexpr int kBwdMinBlocks = BWD_MINB;  // resident CTAs per SM the register bu
 // 20 / 24, all 32 lanes direct 340 µs (every lane's reds on one record
 // contend in L2); pose-only 24 — 2765 / 2776 / 2788 / 2467 it/s for 16 / 20 /
 // 24 / 32)
+#ifndef BWD_OMA2
+#define BWD_OMA2 1
+#endif
 #ifndef BWD_DIRECT
 #define BWD_DIRECT 20
 #endif
@@ -134,7 +137,12 @@ __device__ __forceinline__ AlphaPrep alpha_prep(const float2 e[2], const bool pa
     const float a0 = fminf(ex2_approx(pass[2 * h] ? e[h].x : -INFINITY), kAlphaMax);
     const float a1 = fminf(ex2_approx(pass[2 * h + 1] ? e[h].y : -INFINITY), kAlphaMax);
     p.al[h] = make_float2(a0, a1);
+#if BWD_OMA2
+    const float2 oma = __fadd2_rn(make_float2(1.f, 1.f), make_float2(-a0, -a1));  // 1 - alpha as one FADD2
+    p.ir[h] = make_float2(rcp_approx(oma.x), rcp_approx(oma.y));
+#else
     p.ir[h] = make_float2(rcp_approx(1.f - a0), rcp_approx(1.f - a1));
+#endif
     p.ag[h] = make_float2(e[h].x < kExpClamp ? a0 : 0.f, e[h].y < kExpClamp ? a1 : 0.f);
   }
   return p;
